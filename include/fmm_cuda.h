@@ -1,0 +1,147 @@
+/*
+ * fmm-b200 — C ABI of the B200 near-field library (libfmmcuda.so, sm_100a).
+ *
+ * Plain pointers and sizes only.  This is the boundary the reference's
+ * near-field plug-in interface binds to:
+ *
+ *   reference (proj/include/fmm/backend.hpp)      this ABI
+ *   -------------------------------------------   ------------------------------
+ *   NearFieldBackend::launch(job, out)  :53-55    fmmcu_p2p_launch
+ *   NearFieldBackend::finish()          :56       fmmcu_p2p_finish
+ *   NearFieldJob                        :27-37    fmmcu_p2p_job (CSR-flattened)
+ *   NearFieldStats                      :39-42    pair_evals / seconds outputs
+ *   m2l_add (expansion.hpp:60, called at
+ *            engine.cpp:108-113)                  fmmcu_m2l_launch / _finish
+ *   errors thrown as BackendError /
+ *   SingularConfiguration (types.hpp:70-78)       int status + fmmcu_last_error
+ *
+ * The C++ class fmm::CudaBackend (backend kind "cuda") is a thin wrapper
+ * that flattens the job, calls these entry points and rethrows failures.
+ * Every function returns FMMCU_OK (0) or an FMMCU_E* code; the message is in
+ * fmmcu_last_error(ctx).  There is no CPU fallback: a missing device is an
+ * error (FMMCU_ECUDA).
+ */
+#ifndef FMM_CUDA_H_
+#define FMM_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMMCU_OK 0
+#define FMMCU_EINVAL 1    /* bad argument (InvalidParameter / InvalidInput) */
+#define FMMCU_ECUDA 2     /* CUDA runtime failure or no device */
+#define FMMCU_ESINGULAR 4 /* M2L with coincident centres (SingularConfiguration) */
+#define FMMCU_ENOMEM 5    /* device or pinned allocation failed */
+#define FMMCU_ESTATE 6    /* call out of order (finish without launch, ...) */
+
+#define FMMCU_KERNEL_HARMONIC 0 /* -m / (y - x)     (expansion.cpp:90-92) */
+#define FMMCU_KERNEL_LOG 1      /*  m * log(y - x) */
+
+#define FMMCU_SMOOTH_NONE 0     /* expansion.cpp:78-88 */
+#define FMMCU_SMOOTH_GAUSSIAN 1 /* 1 - exp(-r^2/delta^2) */
+#define FMMCU_SMOOTH_PLUMMER 2  /* r / sqrt(delta^2 + r^2) */
+
+#define FMMCU_MODE_FAST 0  /* FP64, rcp+Newton, FMA; <= 1e-12 normwise of the reference */
+#define FMMCU_MODE_EXACT 1 /* bit-compatible: restated __divdc3, reference order */
+
+typedef struct fmmcu_ctx fmmcu_ctx;
+
+/* One near-field evaluation (reference NearFieldJob, backend.hpp:27-37),
+ * flattened.  Leaf i of the finest level owns permuted sources
+ * [pt_off[i], pt_off[i+1]) and permuted evals [ev_off[i], ev_off[i+1])
+ * (MBox::point_begin/end, eval_begin/end, geometry.hpp:22-23 — contiguous at
+ * the finest level); its strong list (LevelConn::strong, geometry.hpp:44-47,
+ * self included, ascending) is strong_idx[strong_off[i] .. strong_off[i+1]).
+ * Complex arrays are interleaved (re, im) doubles, i.e. the bytes of
+ * std::vector<std::complex<double>>. */
+typedef struct {
+  uint32_t n_leaves;
+  uint32_t n_src;
+  uint32_t n_eval;
+  const uint32_t *pt_off;     /* [n_leaves + 1] */
+  const uint32_t *ev_off;     /* [n_leaves + 1] */
+  const uint32_t *strong_off; /* [n_leaves + 1] */
+  const uint32_t *strong_idx; /* [strong_off[n_leaves]] */
+  const uint32_t *perm;       /* [n_src]  Pyramid::perm (self-skip compares perm[j] to eval_sid) */
+  const double *src_z;        /* [2 n_src]  permuted source positions */
+  const double *src_m;        /* [2 n_src]  permuted strengths */
+  const double *eval_y;       /* [2 n_eval] permuted eval positions */
+  const int64_t *eval_sid;    /* [n_eval] permuted source ids, -1 = none; NULL = no ids */
+  int kernel;                 /* FMMCU_KERNEL_* */
+  int smoother;               /* FMMCU_SMOOTH_* */
+  double delta;
+  int mode;                   /* FMMCU_MODE_* */
+  uint32_t leaf_begin;        /* target-leaf shard [leaf_begin, leaf_end); 0,n_leaves = all */
+  uint32_t leaf_end;
+  double *out;                /* [2 n_eval] host; slots of the shard's evals are written */
+} fmmcu_p2p_job;
+
+/* M2L sums for every (target box, weak partner) pair of every level
+ * (downward pass, engine.cpp:96-114): out[t] = sum over weak_idx of
+ * m2l_add(outgoing[src], local about centers[target_box[t]]), partners in
+ * ascending order.  Box ids are global (all levels concatenated). */
+typedef struct {
+  int p;                      /* expansion order, <= 96 */
+  int kernel;                 /* FMMCU_KERNEL_* */
+  uint32_t n_boxes;           /* global box count */
+  const double *centers;      /* [2 n_boxes] */
+  const double *coeffs;       /* [2 (p+1) n_boxes] outgoing coefficients */
+  uint32_t n_targets;
+  const uint32_t *target_box; /* [n_targets] */
+  const uint32_t *weak_off;   /* [n_targets + 1] */
+  const uint32_t *weak_idx;   /* [weak_off[n_targets]] */
+  double *out;                /* [2 (p+1) n_targets] host */
+} fmmcu_m2l_job;
+
+/* ---- context ---------------------------------------------------------- */
+int fmmcu_create(fmmcu_ctx **ctx, int device);
+void fmmcu_destroy(fmmcu_ctx *ctx);
+const char *fmmcu_last_error(const fmmcu_ctx *ctx);
+int fmmcu_device_count(int *count);
+
+/* ---- reference-facing near field (host buffers) ------------------------- */
+/* Asynchronous: packs the job into pinned staging, enqueues H2D, the P2P
+ * kernels and the D2H of the shard's potentials, and returns.  All job
+ * pointers must stay valid until fmmcu_p2p_finish returns. */
+int fmmcu_p2p_launch(fmmcu_ctx *ctx, const fmmcu_p2p_job *job);
+/* Blocks (without spinning) until the launched job completed, scatters the
+ * potentials into job->out and reports NearFieldStats: pair_evals (exact,
+ * reference counting) and seconds (launch start -> results on host). */
+int fmmcu_p2p_finish(fmmcu_ctx *ctx, uint64_t *pair_evals, double *seconds);
+
+/* ---- device-resident near field (benchmarks, multi-GPU sharding) -------- */
+/* Uploads and packs the job's inputs once (synchronous); they stay resident. */
+int fmmcu_p2p_stage(fmmcu_ctx *ctx, const fmmcu_p2p_job *job);
+/* Enqueues only the P2P kernels over [leaf_begin, leaf_end) of the staged
+ * job on the context stream; potentials stay on the device (permuted eval
+ * order, double2).  *launches receives the number of kernels enqueued. */
+int fmmcu_p2p_run_staged(fmmcu_ctx *ctx, uint32_t leaf_begin, uint32_t leaf_end, int mode,
+                         int *launches);
+/* Device pointer to the staged potentials ([2 n_eval] doubles). */
+int fmmcu_p2p_device_out(fmmcu_ctx *ctx, double **dptr);
+/* Pair count of the last run (exact; waits for it). */
+int fmmcu_p2p_pairs(fmmcu_ctx *ctx, uint64_t *pair_evals);
+/* Pair work of leaves [0, n) of the staged job, prefix-summed on the host
+ * ([n_leaves + 1] uint64, before self-skips) -- for work-balanced shards. */
+int fmmcu_p2p_work_prefix(fmmcu_ctx *ctx, uint64_t *prefix);
+/* Use an external stream (cudaStream_t) for subsequent work; NULL = own. */
+int fmmcu_set_stream(fmmcu_ctx *ctx, void *stream);
+int fmmcu_synchronize(fmmcu_ctx *ctx);
+
+/* ---- M2L on the device --------------------------------------------------- */
+int fmmcu_m2l_launch(fmmcu_ctx *ctx, const fmmcu_m2l_job *job);
+int fmmcu_m2l_finish(fmmcu_ctx *ctx, uint64_t *m2l_ops, double *seconds);
+
+/* ---- diagnostics --------------------------------------------------------- */
+/* Kernels launched by this context since creation (evidence counter). */
+uint64_t fmmcu_kernel_launches(const fmmcu_ctx *ctx);
+/* Measured FP64 FMA throughput of this device (TFLOP/s, DFMA = 2 flops). */
+int fmmcu_fp64_peak(fmmcu_ctx *ctx, double *tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMM_CUDA_H_ */

@@ -1,0 +1,307 @@
+"""ctypes bindings of the in-tree native libraries.
+
+* ``libfmmcuda.so`` — the B200 near field behind the C ABI of
+  ``include/fmm_cuda.h`` (``fmmcu_*``).
+* ``libfmm.so``     — the C++ host library (``include/fmm/*.hpp``) and its
+  flat C ABI for Python (``include/fmm_host.h``, ``fmmh_*``).
+
+Both are built in-tree by ``__graft_entry__.build()`` (``make -C
+paper_1311_1006_b200``).  Loading fails loudly if they are missing: there is
+no CPU or PyTorch fallback for the device path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+CUDA_LIB = os.path.join(PKG, "libfmmcuda.so")
+HOST_LIB = os.path.join(PKG, "libfmm.so")
+
+FMMCU_OK = 0
+FMMCU_EINVAL = 1
+FMMCU_ECUDA = 2
+FMMCU_ESINGULAR = 4
+FMMCU_ENOMEM = 5
+FMMCU_ESTATE = 6
+
+KERNELS = {"harmonic": 0, "logarithmic": 1, "log": 1}
+SMOOTHERS = {"none": 0, "gaussian": 1, "plummer": 2}
+MODES = {"fast": 0, "exact": 1}
+
+_cuda = None
+_host = None
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+class FmmcuError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"fmmcu error {code}: {msg}")
+        self.code = code
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class P2PJob(C.Structure):
+    """Mirror of ``fmmcu_p2p_job`` (include/fmm_cuda.h)."""
+
+    _fields_ = [
+        ("n_leaves", C.c_uint32),
+        ("n_src", C.c_uint32),
+        ("n_eval", C.c_uint32),
+        ("pt_off", C.c_void_p),
+        ("ev_off", C.c_void_p),
+        ("strong_off", C.c_void_p),
+        ("strong_idx", C.c_void_p),
+        ("perm", C.c_void_p),
+        ("src_z", C.c_void_p),
+        ("src_m", C.c_void_p),
+        ("eval_y", C.c_void_p),
+        ("eval_sid", C.c_void_p),
+        ("kernel", C.c_int),
+        ("smoother", C.c_int),
+        ("delta", C.c_double),
+        ("mode", C.c_int),
+        ("leaf_begin", C.c_uint32),
+        ("leaf_end", C.c_uint32),
+        ("out", C.c_void_p),
+    ]
+
+
+class M2LJob(C.Structure):
+    """Mirror of ``fmmcu_m2l_job`` (include/fmm_cuda.h)."""
+
+    _fields_ = [
+        ("p", C.c_int),
+        ("kernel", C.c_int),
+        ("n_boxes", C.c_uint32),
+        ("centers", C.c_void_p),
+        ("coeffs", C.c_void_p),
+        ("n_targets", C.c_uint32),
+        ("target_box", C.c_void_p),
+        ("weak_off", C.c_void_p),
+        ("weak_idx", C.c_void_p),
+        ("out", C.c_void_p),
+    ]
+
+
+CUDA_SYMBOLS = [
+    "fmmcu_create", "fmmcu_destroy", "fmmcu_last_error", "fmmcu_device_count",
+    "fmmcu_p2p_launch", "fmmcu_p2p_finish", "fmmcu_p2p_stage", "fmmcu_p2p_run_staged",
+    "fmmcu_p2p_device_out", "fmmcu_p2p_pairs", "fmmcu_p2p_work_prefix", "fmmcu_set_stream",
+    "fmmcu_synchronize", "fmmcu_m2l_launch", "fmmcu_m2l_finish", "fmmcu_kernel_launches",
+    "fmmcu_fp64_peak",
+]
+
+
+def cuda_lib():
+    global _cuda
+    if _cuda is None:
+        if not os.path.exists(CUDA_LIB):
+            raise NativeLibraryMissing(f"{CUDA_LIB} not built (run __graft_entry__.build())")
+        lib = C.CDLL(CUDA_LIB)
+        vp = C.c_void_p
+        lib.fmmcu_create.argtypes = [C.POINTER(vp), C.c_int]
+        lib.fmmcu_destroy.argtypes = [vp]
+        lib.fmmcu_destroy.restype = None
+        lib.fmmcu_last_error.argtypes = [vp]
+        lib.fmmcu_last_error.restype = C.c_char_p
+        lib.fmmcu_device_count.argtypes = [C.POINTER(C.c_int)]
+        lib.fmmcu_p2p_launch.argtypes = [vp, C.POINTER(P2PJob)]
+        lib.fmmcu_p2p_finish.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        lib.fmmcu_p2p_stage.argtypes = [vp, C.POINTER(P2PJob)]
+        lib.fmmcu_p2p_run_staged.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_int,
+                                             C.POINTER(C.c_int)]
+        lib.fmmcu_p2p_device_out.argtypes = [vp, C.POINTER(C.c_void_p)]
+        lib.fmmcu_p2p_pairs.argtypes = [vp, C.POINTER(C.c_uint64)]
+        lib.fmmcu_p2p_work_prefix.argtypes = [vp, vp]
+        lib.fmmcu_set_stream.argtypes = [vp, vp]
+        lib.fmmcu_synchronize.argtypes = [vp]
+        lib.fmmcu_m2l_launch.argtypes = [vp, C.POINTER(M2LJob)]
+        lib.fmmcu_m2l_finish.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        lib.fmmcu_kernel_launches.argtypes = [vp]
+        lib.fmmcu_kernel_launches.restype = C.c_uint64
+        lib.fmmcu_fp64_peak.argtypes = [vp, C.POINTER(C.c_double)]
+        _cuda = lib
+    return _cuda
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    cuda_lib().fmmcu_device_count(C.byref(n))
+    return n.value
+
+
+class CudaContext:
+    """One ``fmmcu_ctx`` (one device).  Mirrors the reference's concurrent
+    near-field backend protocol: ``launch`` returns at once, ``finish`` joins
+    and reports ``(pair_evals, seconds)`` (backend.hpp:39-57)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = cuda_lib()
+        h = C.c_void_p()
+        rc = self.lib.fmmcu_create(C.byref(h), device)
+        self.h = h
+        if rc != FMMCU_OK:
+            msg = self.lib.fmmcu_last_error(h).decode() if h else "create failed"
+            if h:
+                self.lib.fmmcu_destroy(h)
+            self.h = None
+            raise FmmcuError(rc, msg)
+        self._keep = None
+
+    def close(self):
+        if self.h:
+            self.lib.fmmcu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != FMMCU_OK:
+            raise FmmcuError(rc, self.lib.fmmcu_last_error(self.h).decode())
+
+    # -- job construction --------------------------------------------------
+    @staticmethod
+    def make_job(pt_off, ev_off, s_off, s_idx, perm, zp, mp, yp, sidp, out, *, kernel=0,
+                 smoother=0, delta=0.0, mode=0, leaf_begin=0, leaf_end=None):
+        arrs = dict(
+            pt_off=np.ascontiguousarray(pt_off, dtype=np.uint32),
+            ev_off=np.ascontiguousarray(ev_off, dtype=np.uint32),
+            s_off=np.ascontiguousarray(s_off, dtype=np.uint32),
+            s_idx=np.ascontiguousarray(s_idx, dtype=np.uint32),
+            perm=np.ascontiguousarray(perm, dtype=np.uint32),
+            zp=np.ascontiguousarray(zp, dtype=np.float64),
+            mp=np.ascontiguousarray(mp, dtype=np.float64),
+            yp=np.ascontiguousarray(yp, dtype=np.float64),
+            sidp=None if sidp is None else np.ascontiguousarray(sidp, dtype=np.int64),
+        )
+        nl = len(arrs["pt_off"]) - 1
+        j = P2PJob()
+        j.n_leaves = nl
+        j.n_src = arrs["zp"].size // 2
+        j.n_eval = arrs["yp"].size // 2
+        j.pt_off = _ptr(arrs["pt_off"])
+        j.ev_off = _ptr(arrs["ev_off"])
+        j.strong_off = _ptr(arrs["s_off"])
+        j.strong_idx = _ptr(arrs["s_idx"]) if arrs["s_idx"].size else None
+        j.perm = _ptr(arrs["perm"])
+        j.src_z = _ptr(arrs["zp"])
+        j.src_m = _ptr(arrs["mp"])
+        j.eval_y = _ptr(arrs["yp"]) if arrs["yp"].size else None
+        j.eval_sid = _ptr(arrs["sidp"])
+        j.kernel = kernel
+        j.smoother = smoother
+        j.delta = delta
+        j.mode = mode
+        j.leaf_begin = leaf_begin
+        j.leaf_end = nl if leaf_end is None else leaf_end
+        j.out = _ptr(out) if out is not None and out.size else None
+        return j, arrs
+
+    # -- reference-facing protocol -----------------------------------------
+    def launch(self, job, keep):
+        self._keep = keep
+        self._check(self.lib.fmmcu_p2p_launch(self.h, C.byref(job)))
+
+    def finish(self):
+        pairs = C.c_uint64()
+        secs = C.c_double()
+        rc = self.lib.fmmcu_p2p_finish(self.h, C.byref(pairs), C.byref(secs))
+        self._keep = None
+        self._check(rc)
+        return int(pairs.value), float(secs.value)
+
+    # -- device-resident protocol ------------------------------------------
+    def stage(self, job, keep):
+        self._check(self.lib.fmmcu_p2p_stage(self.h, C.byref(job)))
+        del keep
+
+    def run_staged(self, leaf_begin, leaf_end, mode=0) -> int:
+        n = C.c_int()
+        self._check(self.lib.fmmcu_p2p_run_staged(self.h, leaf_begin, leaf_end, mode,
+                                                  C.byref(n)))
+        return n.value
+
+    def device_out_ptr(self) -> int:
+        p = C.c_void_p()
+        self._check(self.lib.fmmcu_p2p_device_out(self.h, C.byref(p)))
+        return p.value
+
+    def pairs(self) -> int:
+        v = C.c_uint64()
+        self._check(self.lib.fmmcu_p2p_pairs(self.h, C.byref(v)))
+        return int(v.value)
+
+    def work_prefix(self, n_leaves) -> np.ndarray:
+        out = np.empty(n_leaves + 1, dtype=np.uint64)
+        self._check(self.lib.fmmcu_p2p_work_prefix(self.h, _ptr(out)))
+        return out
+
+    def set_stream(self, stream_handle: int | None):
+        self._check(self.lib.fmmcu_set_stream(self.h, C.c_void_p(stream_handle or 0)))
+
+    def synchronize(self):
+        self._check(self.lib.fmmcu_synchronize(self.h))
+
+    def launches(self) -> int:
+        return int(self.lib.fmmcu_kernel_launches(self.h))
+
+    def fp64_peak(self) -> float:
+        v = C.c_double()
+        self._check(self.lib.fmmcu_fp64_peak(self.h, C.byref(v)))
+        return float(v.value)
+
+    # -- M2L ------------------------------------------------------------------
+    def m2l(self, p, kernel, centers, coeffs, target_box, weak_off, weak_idx):
+        centers = np.ascontiguousarray(centers, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        target_box = np.ascontiguousarray(target_box, dtype=np.uint32)
+        weak_off = np.ascontiguousarray(weak_off, dtype=np.uint32)
+        weak_idx = np.ascontiguousarray(weak_idx, dtype=np.uint32)
+        nt = len(target_box)
+        out = np.zeros((nt, p + 1, 2))
+        j = M2LJob()
+        j.p = p
+        j.kernel = kernel
+        j.n_boxes = centers.size // 2
+        j.centers = _ptr(centers)
+        j.coeffs = _ptr(coeffs)
+        j.n_targets = nt
+        j.target_box = _ptr(target_box) if nt else None
+        j.weak_off = _ptr(weak_off)
+        j.weak_idx = _ptr(weak_idx) if weak_idx.size else None
+        j.out = _ptr(out) if nt else None
+        self._check(self.lib.fmmcu_m2l_launch(self.h, C.byref(j)))
+        ops = C.c_uint64()
+        secs = C.c_double()
+        self._check(self.lib.fmmcu_m2l_finish(self.h, C.byref(ops), C.byref(secs)))
+        return out, int(ops.value), float(secs.value)
+
+
+def p2p(ctx: CudaContext, pt_off, ev_off, s_off, s_idx, perm, zp, mp, yp, sidp, *, kernel=0,
+        smoother=0, delta=0.0, mode=0, leaf_begin=0, leaf_end=None, out=None):
+    """One synchronous near-field evaluation through the reference-facing
+    protocol (launch + finish).  Returns (out[n_eval, 2] permuted, pairs, seconds)."""
+    n_eval = np.asarray(yp).size // 2
+    if out is None:
+        out = np.zeros((n_eval, 2))
+    job, keep = CudaContext.make_job(pt_off, ev_off, s_off, s_idx, perm, zp, mp, yp, sidp, out,
+                                     kernel=kernel, smoother=smoother, delta=delta, mode=mode,
+                                     leaf_begin=leaf_begin, leaf_end=leaf_end)
+    ctx.launch(job, keep)
+    pairs, secs = ctx.finish()
+    return out, pairs, secs

@@ -1,0 +1,766 @@
+// fmm-b200 — libfmmcuda.so: the C ABI of include/fmm_cuda.h.
+//
+// Host side of the device near field: validates the flattened NearFieldJob
+// (reference backend.hpp:27-37), packs sources into 32-byte device records
+// in pinned staging memory, builds the P2P work list (one item per target
+// leaf; heavy leaves split into strong-list chunks reduced in a fixed
+// order), enqueues H2D -> kernels -> D2H on the context stream and reports
+// NearFieldStats (exact pair count, busy seconds) at finish.  Also hosts the
+// batched M2L launch and an FP64 peak micro-benchmark.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "fmm_cuda.h"
+#include "m2l_kernels.cuh"
+#include "p2p_kernels.cuh"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+using namespace fmmcu;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kE = 2;
+constexpr int kTile = 1024;
+constexpr size_t kTileSmem = 128 + size_t(kTile) * 32;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocPortable);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+using Clock = std::chrono::steady_clock;
+
+}  // namespace
+
+struct fmmcu_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // current (own or external)
+  cudaStream_t m2l_stream = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_m2l0 = nullptr, ev_m2l1 = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+
+  // staged job (device)
+  DevBuf d_src, d_evy, d_eself, d_pt, d_ev, d_soff, d_sidx, d_items, d_fin, d_out, d_partial,
+      d_hits;
+  // pinned staging
+  HostBuf h_src, h_evy, h_eself, h_out, h_hits, h_csr;
+  std::vector<uint32_t> invperm;
+  // host mirror of the staged job
+  uint32_t n_leaves = 0, n_src = 0, n_eval = 0;
+  int kernel = 0, smoother = 0, mode = 0;
+  double delta = 0.0;
+  std::vector<uint32_t> ev_off;        // host copy
+  std::vector<uint64_t> leaf_work;     // prefix of nt * S
+  std::vector<P2PItem> items;
+  std::vector<uint32_t> item_first;    // [n_leaves + 1]
+  std::vector<P2PFinal> fins;
+  std::vector<uint32_t> fin_first;     // [n_leaves + 1]
+  bool staged = false;
+
+  // in-flight reference-facing launch
+  bool inflight = false;
+  fmmcu_p2p_job job{};
+  uint32_t run_lb = 0, run_le = 0;
+  double prep_seconds = 0.0;
+  uint64_t run_total_pairs = 0;
+
+  // m2l
+  DevBuf m_centers, m_coeffs, m_tbox, m_woff, m_widx, m_table, m_out, m_flag;
+  HostBuf mh_out, mh_flag;
+  int table_p = -1, table_kernel = -1;
+  bool m2l_inflight = false;
+  fmmcu_m2l_job m2l_job{};
+  uint64_t m2l_ops = 0;
+  double m2l_prep = 0.0;
+};
+
+#define CU_TRY(ctx, expr)                                                          \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(_e);            \
+      return _e == cudaErrorMemoryAllocation ? FMMCU_ENOMEM : FMMCU_ECUDA;        \
+    }                                                                             \
+  } while (0)
+
+namespace {
+
+int set_err(fmmcu_ctx* c, int code, const std::string& msg) {
+  c->err = msg;
+  return code;
+}
+
+P2PArgs make_args(fmmcu_ctx* c) {
+  P2PArgs a{};
+  a.src = c->d_src.as<double4>();
+  a.evy = c->d_evy.as<double2>();
+  a.eself = c->d_eself.as<uint32_t>();
+  a.pt_off = c->d_pt.as<uint32_t>();
+  a.ev_off = c->d_ev.as<uint32_t>();
+  a.s_off = c->d_soff.as<uint32_t>();
+  a.s_idx = c->d_sidx.as<uint32_t>();
+  a.items = c->d_items.as<P2PItem>();
+  a.out = c->d_out.as<double2>();
+  a.partial = c->d_partial.as<double2>();
+  a.hits = c->d_hits.as<unsigned long long>();
+  a.delta = c->delta;
+  a.delta2 = c->delta * c->delta;
+  a.inv_delta2 = c->delta != 0.0 ? 1.0 / (c->delta * c->delta) : 0.0;
+  return a;
+}
+
+template <int KN, int SM>
+void launch_tile(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
+  auto kfn = p2p_tile_kernel<KN, SM, kE, kThreads, kTile>;
+  p2p_tile_kernel<KN, SM, kE, kThreads, kTile><<<n_items, kThreads, kTileSmem, s>>>(a);
+  (void)kfn;
+}
+
+template <int KN, int SM>
+void launch_exact(const P2PArgs& a, uint32_t lb, uint32_t le, uint32_t eb, uint32_t ee,
+                  cudaStream_t s) {
+  const uint32_t n = ee - eb;
+  p2p_exact_kernel<KN, SM><<<(n + 127) / 128, 128, 0, s>>>(a, lb, le, eb, ee);
+}
+
+void dispatch_tile(int kn, int sm, const P2PArgs& a, uint32_t n, cudaStream_t s) {
+  if (kn == 0) {
+    if (sm == 0) launch_tile<0, 0>(a, n, s);
+    else if (sm == 1) launch_tile<0, 1>(a, n, s);
+    else launch_tile<0, 2>(a, n, s);
+  } else {
+    if (sm == 0) launch_tile<1, 0>(a, n, s);
+    else if (sm == 1) launch_tile<1, 1>(a, n, s);
+    else launch_tile<1, 2>(a, n, s);
+  }
+}
+
+void dispatch_exact(int kn, int sm, const P2PArgs& a, uint32_t lb, uint32_t le, uint32_t eb,
+                    uint32_t ee, cudaStream_t s) {
+  if (kn == 0) {
+    if (sm == 0) launch_exact<0, 0>(a, lb, le, eb, ee, s);
+    else if (sm == 1) launch_exact<0, 1>(a, lb, le, eb, ee, s);
+    else launch_exact<0, 2>(a, lb, le, eb, ee, s);
+  } else {
+    if (sm == 0) launch_exact<1, 0>(a, lb, le, eb, ee, s);
+    else if (sm == 1) launch_exact<1, 1>(a, lb, le, eb, ee, s);
+    else launch_exact<1, 2>(a, lb, le, eb, ee, s);
+  }
+}
+
+int validate(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  if (!j) return set_err(c, FMMCU_EINVAL, "null job");
+  if (j->kernel < 0 || j->kernel > 1) return set_err(c, FMMCU_EINVAL, "unknown kernel");
+  if (j->smoother < 0 || j->smoother > 2) return set_err(c, FMMCU_EINVAL, "unknown smoother");
+  if (j->mode < 0 || j->mode > 1) return set_err(c, FMMCU_EINVAL, "unknown mode");
+  if (j->smoother != 0 && !(j->delta > 0.0))
+    return set_err(c, FMMCU_EINVAL, "smoother delta must be > 0");
+  if (!j->pt_off || !j->ev_off || !j->strong_off)
+    return set_err(c, FMMCU_EINVAL, "null leaf offsets");
+  if (j->n_src > 0 && (!j->src_z || !j->src_m || !j->perm))
+    return set_err(c, FMMCU_EINVAL, "null source arrays");
+  if (j->n_eval > 0 && !j->eval_y) return set_err(c, FMMCU_EINVAL, "null eval array");
+  const uint32_t nl = j->n_leaves;
+  if (j->pt_off[0] != 0 || j->pt_off[nl] != j->n_src)
+    return set_err(c, FMMCU_EINVAL, "pt_off does not span the sources");
+  if (j->ev_off[0] != 0 || j->ev_off[nl] != j->n_eval)
+    return set_err(c, FMMCU_EINVAL, "ev_off does not span the evals");
+  for (uint32_t i = 0; i < nl; ++i)
+    if (j->pt_off[i] > j->pt_off[i + 1] || j->ev_off[i] > j->ev_off[i + 1] ||
+        j->strong_off[i] > j->strong_off[i + 1])
+      return set_err(c, FMMCU_EINVAL, "leaf offsets not monotone");
+  const uint32_t nnz = j->strong_off[nl];
+  if (nnz > 0 && !j->strong_idx) return set_err(c, FMMCU_EINVAL, "null strong list");
+  for (uint32_t s = 0; s < nnz; ++s)
+    if (j->strong_idx[s] >= nl) return set_err(c, FMMCU_EINVAL, "strong index out of range");
+  if (j->leaf_begin > j->leaf_end || j->leaf_end > nl)
+    return set_err(c, FMMCU_EINVAL, "bad leaf shard");
+  return FMMCU_OK;
+}
+
+// Host packing + work list + H2D.  `sync` = wait for the uploads.
+int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  if (int rc = validate(c, j)) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  const uint32_t nl = j->n_leaves, ns = j->n_src, ne = j->n_eval;
+  const uint32_t nnz = j->strong_off[nl];
+  c->n_leaves = nl;
+  c->n_src = ns;
+  c->n_eval = ne;
+  c->kernel = j->kernel;
+  c->smoother = j->smoother;
+  c->mode = j->mode;
+  c->delta = j->delta;
+
+  // ---- pinned packing -------------------------------------------------------
+  CU_TRY(c, c->h_src.ensure(size_t(ns) * 32));
+  CU_TRY(c, c->h_evy.ensure(size_t(ne) * 16));
+  CU_TRY(c, c->h_eself.ensure(size_t(ne) * 4));
+  double* hs = c->h_src.as<double>();
+  const double* z = j->src_z;
+  const double* m = j->src_m;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < int64_t(ns); ++i) {
+    hs[4 * i + 0] = z[2 * i];
+    hs[4 * i + 1] = z[2 * i + 1];
+    hs[4 * i + 2] = m[2 * i];
+    hs[4 * i + 3] = m[2 * i + 1];
+  }
+  if (ne) std::memcpy(c->h_evy.p, j->eval_y, size_t(ne) * 16);
+  uint32_t* eself = c->h_eself.as<uint32_t>();
+  if (j->eval_sid && ns > 0) {
+    c->invperm.resize(ns);
+    uint32_t* inv = c->invperm.data();
+    const uint32_t* perm = j->perm;
+    bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+    for (int64_t i = 0; i < int64_t(ns); ++i) {
+      if (perm[i] >= ns) ok = false;
+      else inv[perm[i]] = uint32_t(i);
+    }
+    if (!ok) return set_err(c, FMMCU_EINVAL, "perm is not a permutation of the sources");
+    const int64_t* sid = j->eval_sid;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < int64_t(ne); ++e) {
+      const int64_t s = sid[e];
+      eself[e] = (s >= 0 && s < int64_t(ns)) ? inv[s] : kNoSelf;
+    }
+  } else {
+    for (uint32_t e = 0; e < ne; ++e) eself[e] = kNoSelf;
+  }
+
+  // ---- work list ------------------------------------------------------------
+  c->ev_off.assign(j->ev_off, j->ev_off + nl + 1);
+  c->leaf_work.assign(nl + 1, 0);
+  std::vector<uint64_t> S(nl, 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < int64_t(nl); ++t) {
+    uint64_t s = 0;
+    for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q) {
+      const uint32_t sb = j->strong_idx[q];
+      s += j->pt_off[sb + 1] - j->pt_off[sb];
+    }
+    S[t] = s;
+  }
+  uint64_t total = 0;
+  for (uint32_t t = 0; t < nl; ++t) {
+    total += uint64_t(j->ev_off[t + 1] - j->ev_off[t]) * S[t];
+    c->leaf_work[t + 1] = total;
+  }
+  const uint64_t budget = std::max<uint64_t>(1ull << 16, total / (148ull * 16ull));
+  c->items.clear();
+  c->fins.clear();
+  c->item_first.assign(nl + 1, 0);
+  c->fin_first.assign(nl + 1, 0);
+  uint64_t partial_evals = 0;
+  for (uint32_t t = 0; t < nl; ++t) {
+    c->item_first[t] = uint32_t(c->items.size());
+    c->fin_first[t] = uint32_t(c->fins.size());
+    const uint32_t nt = j->ev_off[t + 1] - j->ev_off[t];
+    if (nt == 0) continue;
+    const uint32_t sb0 = j->strong_off[t], sb1 = j->strong_off[t + 1];
+    const uint64_t pairs = uint64_t(nt) * S[t];
+    if (pairs <= budget || sb1 - sb0 <= 1 || S[t] > 0xFFFFFFFFull) {
+      c->items.push_back(P2PItem{t, sb0, sb1, uint32_t(S[t]), kNoSelf, 0});
+      continue;
+    }
+    const uint64_t src_per_chunk = std::max<uint64_t>(1, budget / nt);
+    const uint32_t base = uint32_t(partial_evals);
+    uint32_t n_chunks = 0;
+    uint32_t q = sb0;
+    while (q < sb1) {
+      uint32_t q1 = q;
+      uint64_t acc = 0;
+      while (q1 < sb1 && (acc == 0 || acc + (j->pt_off[j->strong_idx[q1] + 1] -
+                                             j->pt_off[j->strong_idx[q1]]) <= src_per_chunk)) {
+        acc += j->pt_off[j->strong_idx[q1] + 1] - j->pt_off[j->strong_idx[q1]];
+        ++q1;
+      }
+      c->items.push_back(P2PItem{t, q, q1, uint32_t(acc), uint32_t(partial_evals), 0});
+      partial_evals += nt;
+      ++n_chunks;
+      q = q1;
+    }
+    c->fins.push_back(P2PFinal{t, base, n_chunks, 0});
+  }
+  c->item_first[nl] = uint32_t(c->items.size());
+  c->fin_first[nl] = uint32_t(c->fins.size());
+  if (partial_evals > 0xFFFFFFF0ull) return set_err(c, FMMCU_EINVAL, "partial buffer too large");
+
+  // ---- device buffers -------------------------------------------------------
+  CU_TRY(c, c->d_src.ensure(size_t(ns) * 32));
+  CU_TRY(c, c->d_evy.ensure(size_t(ne) * 16));
+  CU_TRY(c, c->d_eself.ensure(size_t(ne) * 4));
+  CU_TRY(c, c->d_pt.ensure(size_t(nl + 1) * 4));
+  CU_TRY(c, c->d_ev.ensure(size_t(nl + 1) * 4));
+  CU_TRY(c, c->d_soff.ensure(size_t(nl + 1) * 4));
+  CU_TRY(c, c->d_sidx.ensure(size_t(nnz) * 4));
+  CU_TRY(c, c->d_items.ensure(c->items.size() * sizeof(P2PItem)));
+  CU_TRY(c, c->d_fin.ensure(c->fins.size() * sizeof(P2PFinal)));
+  CU_TRY(c, c->d_out.ensure(size_t(ne) * 16));
+  CU_TRY(c, c->d_partial.ensure(size_t(partial_evals) * 16));
+  CU_TRY(c, c->d_hits.ensure(8));
+  CU_TRY(c, c->h_hits.ensure(8));
+  // CSR + work list through one pinned block
+  const size_t csr_bytes = size_t(nl + 1) * 12 + size_t(nnz) * 4 +
+                           c->items.size() * sizeof(P2PItem) + c->fins.size() * sizeof(P2PFinal);
+  CU_TRY(c, c->h_csr.ensure(csr_bytes));
+  unsigned char* hc = c->h_csr.as<unsigned char>();
+  size_t o = 0;
+  auto put = [&](const void* src, size_t bytes) {
+    if (bytes) std::memcpy(hc + o, src, bytes);
+    const size_t at = o;
+    o += bytes;
+    return at;
+  };
+  const size_t o_pt = put(j->pt_off, size_t(nl + 1) * 4);
+  const size_t o_ev = put(j->ev_off, size_t(nl + 1) * 4);
+  const size_t o_so = put(j->strong_off, size_t(nl + 1) * 4);
+  const size_t o_si = put(j->strong_idx, size_t(nnz) * 4);
+  const size_t o_it = put(c->items.data(), c->items.size() * sizeof(P2PItem));
+  const size_t o_fi = put(c->fins.data(), c->fins.size() * sizeof(P2PFinal));
+
+  cudaStream_t s = c->stream;
+  CU_TRY(c, cudaEventRecord(c->ev_start, s));
+  CU_TRY(c, cudaMemcpyAsync(c->d_src.p, c->h_src.p, size_t(ns) * 32, cudaMemcpyHostToDevice, s));
+  if (ne) {
+    CU_TRY(c, cudaMemcpyAsync(c->d_evy.p, c->h_evy.p, size_t(ne) * 16, cudaMemcpyHostToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(c->d_eself.p, c->h_eself.p, size_t(ne) * 4, cudaMemcpyHostToDevice, s));
+  }
+  CU_TRY(c, cudaMemcpyAsync(c->d_pt.p, hc + o_pt, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaMemcpyAsync(c->d_ev.p, hc + o_ev, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaMemcpyAsync(c->d_soff.p, hc + o_so, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
+  if (nnz) CU_TRY(c, cudaMemcpyAsync(c->d_sidx.p, hc + o_si, size_t(nnz) * 4, cudaMemcpyHostToDevice, s));
+  if (!c->items.empty())
+    CU_TRY(c, cudaMemcpyAsync(c->d_items.p, hc + o_it, c->items.size() * sizeof(P2PItem),
+                              cudaMemcpyHostToDevice, s));
+  if (!c->fins.empty())
+    CU_TRY(c, cudaMemcpyAsync(c->d_fin.p, hc + o_fi, c->fins.size() * sizeof(P2PFinal),
+                              cudaMemcpyHostToDevice, s));
+  c->staged = true;
+  return FMMCU_OK;
+}
+
+// Kernels over [lb, le) of the staged job.
+int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch) {
+  cudaStream_t s = c->stream;
+  int n = 0;
+  CU_TRY(c, cudaMemsetAsync(c->d_hits.p, 0, 8, s));
+  const P2PArgs a = make_args(c);
+  if (le > lb) {
+    if (mode == FMMCU_MODE_EXACT) {
+      const uint32_t eb = c->ev_off[lb], ee = c->ev_off[le];
+      if (ee > eb) {
+        dispatch_exact(c->kernel, c->smoother, a, lb, le, eb, ee, s);
+        ++n;
+      }
+    } else {
+      const uint32_t i0 = c->item_first[lb], i1 = c->item_first[le];
+      if (i1 > i0) {
+        P2PArgs aa = a;
+        aa.items = c->d_items.as<P2PItem>() + i0;
+        aa.n_items = i1 - i0;
+        dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s);
+        ++n;
+      }
+      const uint32_t f0 = c->fin_first[lb], f1 = c->fin_first[le];
+      if (f1 > f0) {
+        p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(c->d_fin.as<P2PFinal>() + f0, f1 - f0,
+                                                     c->d_ev.as<uint32_t>(),
+                                                     c->d_partial.as<double2>(),
+                                                     c->d_out.as<double2>());
+        ++n;
+      }
+    }
+  }
+  CU_TRY(c, cudaGetLastError());
+  c->launches += uint64_t(n);
+  if (nlaunch) *nlaunch = n;
+  return FMMCU_OK;
+}
+
+// FP64 peak: independent DFMA chains, 8 per thread.
+__global__ void dfma_peak_kernel(double* sink, int iters, double seed) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4,
+         a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, b = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, m, b); a1 = fma(a1, m, b); a2 = fma(a2, m, b); a3 = fma(a3, m, b);
+      a4 = fma(a4, m, b); a5 = fma(a5, m, b); a6 = fma(a6, m, b); a7 = fma(a7, m, b);
+    }
+  }
+  const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (r == 12345.678) sink[0] = r;
+}
+
+}  // namespace
+
+// =============================================================== C ABI ====
+extern "C" {
+
+int fmmcu_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (count) *count = (e == cudaSuccess) ? n : 0;
+  return e == cudaSuccess ? FMMCU_OK : FMMCU_ECUDA;
+}
+
+int fmmcu_create(fmmcu_ctx** out, int device) {
+  if (!out) return FMMCU_EINVAL;
+  *out = nullptr;
+  auto* c = new (std::nothrow) fmmcu_ctx();
+  if (!c) return FMMCU_ENOMEM;
+  c->device = device;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || device < 0 || device >= n) {
+    // keep the context so the caller can read the message, then fail
+    static thread_local std::string last;
+    last = std::string("no CUDA device ") + std::to_string(device) + " (" +
+           (e == cudaSuccess ? std::to_string(n) + " visible" : cudaGetErrorString(e)) + ")";
+    c->err = last;
+    *out = c;
+    return FMMCU_ECUDA;
+  }
+  auto fail = [&](cudaError_t er) {
+    c->err = cudaGetErrorString(er);
+    *out = c;
+    return FMMCU_ECUDA;
+  };
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(e);
+  if ((e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e);
+  if ((e = cudaStreamCreateWithFlags(&c->m2l_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e);
+  c->stream = c->own_stream;
+  const unsigned flags = cudaEventBlockingSync;
+  if ((e = cudaEventCreateWithFlags(&c->ev_start, flags)) != cudaSuccess) return fail(e);
+  if ((e = cudaEventCreateWithFlags(&c->ev_end, flags)) != cudaSuccess) return fail(e);
+  if ((e = cudaEventCreateWithFlags(&c->ev_m2l0, flags)) != cudaSuccess) return fail(e);
+  if ((e = cudaEventCreateWithFlags(&c->ev_m2l1, flags)) != cudaSuccess) return fail(e);
+  *out = c;
+  return FMMCU_OK;
+}
+
+void fmmcu_destroy(fmmcu_ctx* c) {
+  if (!c) return;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) == cudaSuccess && c->device < n && c->own_stream) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->own_stream);
+    if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->m2l_stream);
+    for (DevBuf* b : {&c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
+                      &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits,
+                      &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
+                      &c->m_table, &c->m_out, &c->m_flag})
+      b->release();
+    for (HostBuf* b : {&c->h_src, &c->h_evy, &c->h_eself, &c->h_out, &c->h_hits, &c->h_csr,
+                       &c->mh_out, &c->mh_flag})
+      b->release();
+    for (cudaEvent_t ev : {c->ev_start, c->ev_end, c->ev_m2l0, c->ev_m2l1})
+      if (ev) cudaEventDestroy(ev);
+    cudaStreamDestroy(c->own_stream);
+    cudaStreamDestroy(c->m2l_stream);
+  }
+  delete c;
+}
+
+const char* fmmcu_last_error(const fmmcu_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+uint64_t fmmcu_kernel_launches(const fmmcu_ctx* c) { return c ? c->launches : 0; }
+
+int fmmcu_set_stream(fmmcu_ctx* c, void* stream) {
+  if (!c) return FMMCU_EINVAL;
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  return FMMCU_OK;
+}
+
+int fmmcu_synchronize(fmmcu_ctx* c) {
+  if (!c) return FMMCU_EINVAL;
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_launch(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  if (!c) return FMMCU_EINVAL;
+  if (c->inflight) return set_err(c, FMMCU_ESTATE, "launch while a job is in flight");
+  const auto t0 = Clock::now();
+  if (int rc = stage_job(c, j)) return rc;
+  if (j->n_eval > 0 && !j->out) return set_err(c, FMMCU_EINVAL, "null output");
+  int nl = 0;
+  if (int rc = run_kernels(c, j->leaf_begin, j->leaf_end, j->mode, &nl)) return rc;
+  const uint32_t eb = c->ev_off[j->leaf_begin], ee = c->ev_off[j->leaf_end];
+  CU_TRY(c, c->h_out.ensure(size_t(c->n_eval) * 16 + 16));
+  if (ee > eb)
+    CU_TRY(c, cudaMemcpyAsync(c->h_out.as<double2>() + eb, c->d_out.as<double2>() + eb,
+                              size_t(ee - eb) * 16, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaEventRecord(c->ev_end, c->stream));
+  c->job = *j;
+  c->run_lb = j->leaf_begin;
+  c->run_le = j->leaf_end;
+  c->run_total_pairs = c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
+  c->prep_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  c->inflight = true;
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
+  if (!c) return FMMCU_EINVAL;
+  if (!c->inflight) return set_err(c, FMMCU_ESTATE, "finish without launch");
+  c->inflight = false;
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaEventSynchronize(c->ev_end));
+  CU_TRY(c, cudaGetLastError());
+  float ms = 0.f;
+  CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_start, c->ev_end));
+  const uint32_t eb = c->ev_off[c->run_lb], ee = c->ev_off[c->run_le];
+  if (ee > eb) std::memcpy(c->job.out + 2 * size_t(eb), c->h_out.as<double2>() + eb, size_t(ee - eb) * 16);
+  const uint64_t hits = *c->h_hits.as<unsigned long long>();
+  if (pair_evals) *pair_evals = c->run_total_pairs - hits;
+  if (seconds) *seconds = c->prep_seconds + 1e-3 * double(ms);
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_stage(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  if (!c) return FMMCU_EINVAL;
+  if (c->inflight) return set_err(c, FMMCU_ESTATE, "stage while a job is in flight");
+  if (int rc = stage_job(c, j)) return rc;
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_run_staged(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* launches) {
+  if (!c) return FMMCU_EINVAL;
+  if (!c->staged) return set_err(c, FMMCU_ESTATE, "no staged job");
+  if (lb > le || le > c->n_leaves) return set_err(c, FMMCU_EINVAL, "bad leaf shard");
+  if (mode < 0 || mode > 1) return set_err(c, FMMCU_EINVAL, "unknown mode");
+  CU_TRY(c, cudaSetDevice(c->device));
+  c->run_lb = lb;
+  c->run_le = le;
+  c->run_total_pairs = c->leaf_work[le] - c->leaf_work[lb];
+  return run_kernels(c, lb, le, mode, launches);
+}
+
+int fmmcu_p2p_device_out(fmmcu_ctx* c, double** dptr) {
+  if (!c || !dptr) return FMMCU_EINVAL;
+  if (!c->staged) return set_err(c, FMMCU_ESTATE, "no staged job");
+  *dptr = c->d_out.as<double>();
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_pairs(fmmcu_ctx* c, uint64_t* pairs) {
+  if (!c || !pairs) return FMMCU_EINVAL;
+  if (!c->staged) return set_err(c, FMMCU_ESTATE, "no staged job");
+  CU_TRY(c, cudaSetDevice(c->device));
+  unsigned long long h = 0;
+  CU_TRY(c, cudaMemcpyAsync(&h, c->d_hits.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  *pairs = c->run_total_pairs - h;
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_work_prefix(fmmcu_ctx* c, uint64_t* prefix) {
+  if (!c || !prefix) return FMMCU_EINVAL;
+  if (!c->staged) return set_err(c, FMMCU_ESTATE, "no staged job");
+  std::memcpy(prefix, c->leaf_work.data(), sizeof(uint64_t) * c->leaf_work.size());
+  return FMMCU_OK;
+}
+
+int fmmcu_fp64_peak(fmmcu_ctx* c, double* tflops) {
+  if (!c || !tflops) return FMMCU_EINVAL;
+  CU_TRY(c, cudaSetDevice(c->device));
+  int sms = 0;
+  CU_TRY(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  DevBuf sink;
+  CU_TRY(c, sink.ensure(64));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  CU_TRY(c, cudaEventCreate(&e0));
+  CU_TRY(c, cudaEventCreate(&e1));
+  dfma_peak_kernel<<<blocks, threads, 0, c->stream>>>(sink.as<double>(), 64, 1.0);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    CU_TRY(c, cudaEventRecord(e0, c->stream));
+    dfma_peak_kernel<<<blocks, threads, 0, c->stream>>>(sink.as<double>(), iters, 1.0);
+    CU_TRY(c, cudaEventRecord(e1, c->stream));
+    CU_TRY(c, cudaEventSynchronize(e1));
+    float ms = 0;
+    CU_TRY(c, cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+  }
+  CU_TRY(c, cudaGetLastError());
+  c->launches += 4;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  sink.release();
+  const double flops = double(blocks) * threads * iters * 16.0 * 8.0 * 2.0;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return FMMCU_OK;
+}
+
+// ------------------------------------------------------------------- M2L --
+int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
+  if (!c) return FMMCU_EINVAL;
+  if (c->m2l_inflight) return set_err(c, FMMCU_ESTATE, "m2l launch while in flight");
+  if (!j) return set_err(c, FMMCU_EINVAL, "null m2l job");
+  if (j->p < 1 || j->p > kM2LMaxP) return set_err(c, FMMCU_EINVAL, "m2l order out of range");
+  if (j->kernel < 0 || j->kernel > 1) return set_err(c, FMMCU_EINVAL, "unknown kernel");
+  const auto t0 = Clock::now();
+  CU_TRY(c, cudaSetDevice(c->device));
+  const int P1 = j->p + 1;
+  const uint32_t nb = j->n_boxes, nt = j->n_targets;
+  const uint32_t nnz = nt ? j->weak_off[nt] : 0;
+  for (uint32_t t = 0; t < nt; ++t)
+    if (j->target_box[t] >= nb || j->weak_off[t] > j->weak_off[t + 1])
+      return set_err(c, FMMCU_EINVAL, "bad m2l target list");
+  for (uint32_t q = 0; q < nnz; ++q)
+    if (j->weak_idx[q] >= nb) return set_err(c, FMMCU_EINVAL, "bad m2l weak index");
+  // binomial table T[k][l] (Pascal recurrence in doubles, as the reference's table)
+  if (c->table_p != j->p || c->table_kernel != j->kernel) {
+    const int rows = 2 * P1 + 2;
+    std::vector<double> pas(size_t(rows) * rows, 0.0);
+    for (int i = 0; i < rows; ++i) {
+      pas[size_t(i) * rows] = 1.0;
+      for (int k = 1; k <= i; ++k)
+        pas[size_t(i) * rows + k] = pas[size_t(i - 1) * rows + k - 1] + pas[size_t(i - 1) * rows + k];
+    }
+    std::vector<double> T(size_t(P1) * P1, 0.0);
+    for (int k = 0; k < P1; ++k)
+      for (int l = 0; l < P1; ++l) {
+        if (j->kernel == 0) T[size_t(k) * P1 + l] = pas[size_t(l + k) * rows + k];
+        else if (k >= 1) T[size_t(k) * P1 + l] = pas[size_t(l + k - 1) * rows + (k - 1)];
+      }
+    CU_TRY(c, c->m_table.ensure(T.size() * 8));
+    CU_TRY(c, cudaMemcpy(c->m_table.p, T.data(), T.size() * 8, cudaMemcpyHostToDevice));
+    c->table_p = j->p;
+    c->table_kernel = j->kernel;
+  }
+  CU_TRY(c, c->m_centers.ensure(size_t(nb) * 16));
+  CU_TRY(c, c->m_coeffs.ensure(size_t(nb) * P1 * 16));
+  CU_TRY(c, c->m_tbox.ensure(size_t(nt) * 4));
+  CU_TRY(c, c->m_woff.ensure(size_t(nt + 1) * 4));
+  CU_TRY(c, c->m_widx.ensure(size_t(nnz) * 4));
+  CU_TRY(c, c->m_out.ensure(size_t(nt) * P1 * 16));
+  CU_TRY(c, c->m_flag.ensure(8));
+  CU_TRY(c, c->mh_out.ensure(size_t(nt) * P1 * 16));
+  CU_TRY(c, c->mh_flag.ensure(8));
+  cudaStream_t s = c->m2l_stream;
+  CU_TRY(c, cudaEventRecord(c->ev_m2l0, s));
+  CU_TRY(c, cudaMemcpyAsync(c->m_centers.p, j->centers, size_t(nb) * 16, cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaMemcpyAsync(c->m_coeffs.p, j->coeffs, size_t(nb) * P1 * 16, cudaMemcpyHostToDevice, s));
+  if (nt) {
+    CU_TRY(c, cudaMemcpyAsync(c->m_tbox.p, j->target_box, size_t(nt) * 4, cudaMemcpyHostToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(c->m_woff.p, j->weak_off, size_t(nt + 1) * 4, cudaMemcpyHostToDevice, s));
+  }
+  if (nnz) CU_TRY(c, cudaMemcpyAsync(c->m_widx.p, j->weak_idx, size_t(nnz) * 4, cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaMemsetAsync(c->m_flag.p, 0, 8, s));
+  if (nt) {
+    M2LArgs a{};
+    a.p = j->p;
+    a.kernel = j->kernel;
+    a.centers = c->m_centers.as<double2>();
+    a.coeffs = c->m_coeffs.as<double2>();
+    a.target_box = c->m_tbox.as<uint32_t>();
+    a.weak_off = c->m_woff.as<uint32_t>();
+    a.weak_idx = c->m_widx.as<uint32_t>();
+    a.table = c->m_table.as<double>();
+    a.n_targets = nt;
+    // (p+2) log10|w| >= 250  <=>  |w|^2 >= 10^(500/(p+2))
+    a.big_w2 = std::pow(10.0, 500.0 / double(j->p + 2));
+    a.out = c->m_out.as<double2>();
+    a.singular = c->m_flag.as<int>();
+    m2l_batched_kernel<<<(nt + kM2LWarps - 1) / kM2LWarps, kM2LWarps * 32, 0, s>>>(a);
+    CU_TRY(c, cudaGetLastError());
+    c->launches += 1;
+    CU_TRY(c, cudaMemcpyAsync(c->mh_out.p, c->m_out.p, size_t(nt) * P1 * 16, cudaMemcpyDeviceToHost, s));
+  }
+  CU_TRY(c, cudaMemcpyAsync(c->mh_flag.p, c->m_flag.p, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaEventRecord(c->ev_m2l1, s));
+  c->m2l_job = *j;
+  c->m2l_ops = nnz;
+  c->m2l_prep = std::chrono::duration<double>(Clock::now() - t0).count();
+  c->m2l_inflight = true;
+  return FMMCU_OK;
+}
+
+int fmmcu_m2l_finish(fmmcu_ctx* c, uint64_t* ops, double* seconds) {
+  if (!c) return FMMCU_EINVAL;
+  if (!c->m2l_inflight) return set_err(c, FMMCU_ESTATE, "m2l finish without launch");
+  c->m2l_inflight = false;
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaEventSynchronize(c->ev_m2l1));
+  CU_TRY(c, cudaGetLastError());
+  float ms = 0.f;
+  CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_m2l0, c->ev_m2l1));
+  const int P1 = c->m2l_job.p + 1;
+  if (c->m2l_job.n_targets)
+    std::memcpy(c->m2l_job.out, c->mh_out.p, size_t(c->m2l_job.n_targets) * P1 * 16);
+  if (ops) *ops = c->m2l_ops;
+  if (seconds) *seconds = c->m2l_prep + 1e-3 * double(ms);
+  if (*c->mh_flag.as<int>())
+    return set_err(c, FMMCU_ESINGULAR, "m2l: target center coincides with source center");
+  return FMMCU_OK;
+}
+
+}  // extern "C"

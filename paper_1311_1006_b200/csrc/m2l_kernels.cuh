@@ -1,0 +1,179 @@
+// fmm-b200 — batched M2L (multipole-to-local) translations for sm_100a.
+//
+// Device restatement of m2l_add() (proj/src/expansion.cpp:188-269) as called
+// by the downward pass for every weak partner of every box with evaluation
+// points (proj/src/engine.cpp:96-114).  Because every outgoing expansion is
+// known after the upward pass, the M2L sums of *all* levels are independent
+// and run in one launch:
+//     out[t][l] = sum_{w in weak(t), ascending} M2L(outgoing[w] -> centre[t])[l]
+// The host then forms local = L2L(parent) + out[t] level by level.
+//
+// Mapping: one warp per target box, lanes over the local index l (chunks of
+// 32 for p >= 32).  Per partner: w = 1/z0; powers w^j by a warp shuffle scan;
+// v_k = b_k (-1)^{k+1} w^{k+1} (harmonic) or u_k = b_k (-1)^k w^k (log)
+// staged in shared memory; acc_l = sum_k T[k][l] v_k with the binomial table
+// T read coalesced through L1; c_l += w^l acc_l.
+// Reference semantics kept: z0 == 0 raises SingularConfiguration (flag);
+// when (p+2) log10|w| >= 250 (the reference's long double branch,
+// expansion.cpp:196-199) the power chains are formed progressively,
+// b_k w^(k+1) = (((b_k w) w) ...), so no intermediate exceeds the final value.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fmmcu {
+
+struct M2LArgs {
+  int p;
+  int kernel;
+  const double2* __restrict__ centers;
+  const double2* __restrict__ coeffs;  // [n_boxes][p+1]
+  const uint32_t* __restrict__ target_box;
+  const uint32_t* __restrict__ weak_off;
+  const uint32_t* __restrict__ weak_idx;
+  const double* __restrict__ table;  // [(p+1)][(p+1)]: T[k][l]
+  uint32_t n_targets;
+  double big_w2;                     // |w|^2 threshold of the overflow-safe branch
+  double2* __restrict__ out;         // [n_targets][p+1]
+  int* __restrict__ singular;
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+__device__ __forceinline__ double2 shfl_up2(double2 v, int d) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+constexpr int kM2LWarps = 4;
+constexpr int kM2LMaxP = 96;
+
+__global__ void __launch_bounds__(kM2LWarps * 32) m2l_batched_kernel(const M2LArgs a) {
+  __shared__ double2 s_v[kM2LWarps][kM2LMaxP + 1];
+  __shared__ double2 s_pw[kM2LWarps][kM2LMaxP + 2];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const uint32_t t = blockIdx.x * kM2LWarps + wid;
+  if (t >= a.n_targets) return;
+  const int P1 = a.p + 1;
+  const int nchunk = (P1 + 31) >> 5;
+  double2* v = s_v[wid];
+  double2* pw = s_pw[wid];
+  const double2 ct = a.centers[a.target_box[t]];
+
+  double2 c[4];  // local coefficients l = lane + 32*q
+#pragma unroll
+  for (int q = 0; q < 4; ++q) c[q] = make_double2(0.0, 0.0);
+
+  for (uint32_t wi = a.weak_off[t]; wi < a.weak_off[t + 1]; ++wi) {
+    const uint32_t sb = a.weak_idx[wi];
+    const double2 cs = a.centers[sb];
+    const double2 z0 = make_double2(cs.x - ct.x, cs.y - ct.y);
+    if (z0.x == 0.0 && z0.y == 0.0) {
+      if (lane == 0) atomicOr(a.singular, 1);
+      continue;
+    }
+    const double zz = fma(z0.x, z0.x, z0.y * z0.y);
+    const double2 w = make_double2(z0.x / zz, -z0.y / zz);
+    const double w2 = fma(w.x, w.x, w.y * w.y);
+    const double2* b = a.coeffs + (size_t)sb * P1;
+
+    if (w2 < a.big_w2) {
+      // powers w^j, j = 1..p+1, by a shuffle scan (lane L -> w^(L+1))
+      double2 x = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double2 y = shfl_up2(x, o);
+        if (lane >= o) x = cmul(x, y);
+      }
+      const double2 w32 = shfl2(x, 31);
+      if (lane == 0) pw[0] = make_double2(1.0, 0.0);
+      double2 xc = x;
+      for (int q = 0; q < nchunk; ++q) {
+        const int j = lane + 32 * q + 1;
+        if (j <= P1) pw[j] = xc;
+        xc = cmul(xc, w32);
+      }
+      __syncwarp();
+      // source vector
+      for (int k = lane; k < P1; k += 32) {
+        const double2 bk = b[k];
+        double2 val;
+        if (a.kernel == 0) {
+          const double sgn = (k & 1) ? 1.0 : -1.0;  // (-1)^(k+1)
+          val = cmul(make_double2(sgn * bk.x, sgn * bk.y), pw[k + 1]);
+        } else {
+          const double sgn = (k & 1) ? -1.0 : 1.0;  // (-1)^k
+          val = cmul(make_double2(sgn * bk.x, sgn * bk.y), pw[k]);
+        }
+        v[k] = val;
+      }
+    } else {
+      // overflow-safe progressive chains (rare: nearly coincident centres)
+      if (lane == 0) pw[0] = make_double2(1.0, 0.0);
+      for (int k = lane; k < P1; k += 32) {
+        const double2 bk = b[k];
+        const int n = (a.kernel == 0) ? k + 1 : k;
+        const double sgn = (a.kernel == 0) ? ((k & 1) ? 1.0 : -1.0) : ((k & 1) ? -1.0 : 1.0);
+        double2 val = make_double2(sgn * bk.x, sgn * bk.y);
+        for (int r = 0; r < n; ++r) val = cmul(val, w);
+        v[k] = val;
+      }
+    }
+    __syncwarp();
+
+    // acc_l = sum_k T[k][l] v_k
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q >= nchunk) break;
+      const int l = lane + 32 * q;
+      if (l >= P1) break;
+      double2 acc = make_double2(0.0, 0.0);
+      const int kbeg = (a.kernel == 0) ? 0 : 1;
+      for (int k = kbeg; k < P1; ++k) {
+        const double tk = __ldg(a.table + (size_t)k * P1 + l);
+        const double2 vk = v[k];
+        acc.x = fma(tk, vk.x, acc.x);
+        acc.y = fma(tk, vk.y, acc.y);
+      }
+      if (a.kernel != 0) {
+        const double2 a0 = b[0];
+        if (l == 0) {
+          // a0 * log(-z0)
+          const double lr = 0.5 * log(zz);
+          const double th = atan2(-z0.y, -z0.x);
+          acc.x += a0.x * lr - a0.y * th;
+          acc.y += a0.x * th + a0.y * lr;
+        } else {
+          acc.x -= a0.x / (double)l;
+          acc.y -= a0.y / (double)l;
+        }
+      }
+      double2 add;
+      if (w2 < a.big_w2) {
+        add = cmul(pw[l], acc);
+      } else {
+        add = acc;
+        for (int r = 0; r < l; ++r) add = cmul(add, w);
+      }
+      if (a.kernel != 0 && l == 0) add = acc;
+      c[q].x += add.x;
+      c[q].y += add.y;
+    }
+    __syncwarp();
+  }
+  double2* o = a.out + (size_t)t * P1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int l = lane + 32 * q;
+    if (l < P1) o[l] = c[q];
+  }
+}
+
+}  // namespace fmmcu
