@@ -1,0 +1,55 @@
+// fmm-b200 — the B200 near-field backend (BackendKind::cuda).
+//
+// A NearFieldBackend (reference backend.hpp:48-57) that forwards the job to
+// libfmmcuda.so through the C ABI of include/fmm_cuda.h.  Concurrent: launch
+// packs + enqueues and returns, finish blocks on a CUDA event (no spinning,
+// so the OpenMP far field keeps every core) and rethrows device failures.
+// With several devices the target leaves are split into contiguous,
+// pair-work-balanced ranges, one per device; every device holds all sources
+// (replicated) and returns only its slice of the potentials.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "fmm/backend.hpp"
+
+struct fmmcu_ctx;
+
+namespace fmm {
+
+class CudaBackend final : public NearFieldBackend {
+ public:
+  explicit CudaBackend(const CudaSettings& cs);
+  ~CudaBackend() override;
+  CudaBackend(const CudaBackend&) = delete;
+  CudaBackend& operator=(const CudaBackend&) = delete;
+
+  bool concurrent() const override { return true; }
+  const char* name() const override { return "cuda"; }
+  void launch(const NearFieldJob& job, std::vector<cplx>& out) override;
+  NearFieldStats finish() override;
+
+  const CudaSettings& settings() const { return cs_; }
+
+  // Batched M2L on the first device (see include/fmm_cuda.h fmmcu_m2l_job).
+  // Asynchronous; m2l_finish fills `out` ([n_targets][p+1]) and throws
+  // SingularConfiguration on coincident centres.
+  void m2l_launch(int p, Kernel kernel, const std::vector<cplx>& centers,
+                  const std::vector<cplx>& coeffs, const std::vector<std::uint32_t>& target_box,
+                  const std::vector<std::uint32_t>& weak_off,
+                  const std::vector<std::uint32_t>& weak_idx, std::vector<cplx>& out);
+  std::uint64_t m2l_finish(double* seconds = nullptr);
+
+  std::uint64_t kernel_launches() const;
+
+ private:
+  CudaSettings cs_;
+  std::vector<fmmcu_ctx*> ctx_;
+  bool inflight_ = false;
+  // flattened job (must outlive the device work)
+  std::vector<std::uint32_t> pt_off_, ev_off_, s_off_, s_idx_;
+};
+
+}  // namespace fmm

@@ -1,0 +1,193 @@
+// fmm-b200 — CudaBackend: NearFieldBackend -> libfmmcuda.so C ABI.
+//
+// Flattens the reference NearFieldJob (backend.hpp:27-37) into the CSR
+// arrays of fmmcu_p2p_job, shards target leaves across devices by pair
+// work, and maps C-ABI status codes onto the reference error taxonomy
+// (types.hpp:62-92): launch/finish failures surface as exceptions that the
+// engine wraps as BackendError("nearfield launch" | "nearfield", ...)
+// (engine.cpp:294-311); coincident M2L centres as SingularConfiguration.
+#include <algorithm>
+#include <stdexcept>
+
+#include "fmm/cuda_backend.hpp"
+#include "fmm_cuda.h"
+
+namespace fmm {
+
+namespace {
+
+[[noreturn]] void raise(fmmcu_ctx* c, int rc, const char* what) {
+  const std::string msg = std::string(what) + ": " + (c ? fmmcu_last_error(c) : "no context");
+  if (rc == FMMCU_ESINGULAR) throw SingularConfiguration(msg);
+  if (rc == FMMCU_EINVAL) throw InvalidInput(msg);
+  throw std::runtime_error(msg);
+}
+
+}  // namespace
+
+CudaBackend::CudaBackend(const CudaSettings& cs) : cs_(cs) {
+  if (cs_.devices.empty()) cs_.devices.push_back(0);
+  for (int d : cs_.devices) {
+    fmmcu_ctx* c = nullptr;
+    const int rc = fmmcu_create(&c, d);
+    if (rc != FMMCU_OK) {
+      const std::string msg = std::string("cuda backend: ") + (c ? fmmcu_last_error(c) : "");
+      if (c) fmmcu_destroy(c);
+      for (fmmcu_ctx* o : ctx_) fmmcu_destroy(o);
+      ctx_.clear();
+      throw BackendError("cuda init", msg);
+    }
+    ctx_.push_back(c);
+  }
+}
+
+CudaBackend::~CudaBackend() {
+  if (inflight_) {
+    for (fmmcu_ctx* c : ctx_) {
+      std::uint64_t p;
+      double s;
+      fmmcu_p2p_finish(c, &p, &s);
+    }
+  }
+  for (fmmcu_ctx* c : ctx_) fmmcu_destroy(c);
+}
+
+std::uint64_t CudaBackend::kernel_launches() const {
+  std::uint64_t n = 0;
+  for (fmmcu_ctx* c : ctx_) n += fmmcu_kernel_launches(c);
+  return n;
+}
+
+void CudaBackend::launch(const NearFieldJob& job, std::vector<cplx>& out) {
+  if (inflight_) throw InvalidState("cuda backend: launch while a job is in flight");
+  const std::vector<MBox>& fine = job.pyramid->finest();
+  const std::uint32_t nl = std::uint32_t(fine.size());
+  const std::uint32_t ne = std::uint32_t(job.eval_y->size());
+  out.assign(ne, cplx(0, 0));
+
+  pt_off_.resize(nl + 1);
+  ev_off_.resize(nl + 1);
+  s_off_.resize(nl + 1);
+  for (std::uint32_t i = 0; i < nl; ++i) {
+    pt_off_[i] = fine[i].point_begin;
+    ev_off_[i] = fine[i].eval_begin;
+  }
+  pt_off_[nl] = nl ? fine[nl - 1].point_end : 0;
+  ev_off_[nl] = nl ? fine[nl - 1].eval_end : 0;
+  std::uint32_t nnz = 0;
+  for (std::uint32_t i = 0; i < nl; ++i) {
+    s_off_[i] = nnz;
+    nnz += std::uint32_t(job.finest->strong[i].size());
+  }
+  s_off_[nl] = nnz;
+  s_idx_.resize(nnz);
+  for (std::uint32_t i = 0; i < nl; ++i)
+    std::copy(job.finest->strong[i].begin(), job.finest->strong[i].end(), s_idx_.begin() + s_off_[i]);
+
+  // Contiguous target-leaf shards balanced by pair work n_evals * |strong sources|.
+  const std::size_t nd = ctx_.size();
+  std::vector<std::uint32_t> cut(nd + 1, 0);
+  cut[nd] = nl;
+  if (nd > 1) {
+    std::vector<double> pre(nl + 1, 0.0);
+    for (std::uint32_t i = 0; i < nl; ++i) {
+      double s = 0;
+      for (std::uint32_t q = s_off_[i]; q < s_off_[i + 1]; ++q)
+        s += fine[s_idx_[q]].point_end - fine[s_idx_[q]].point_begin;
+      pre[i + 1] = pre[i] + s * (fine[i].eval_end - fine[i].eval_begin);
+    }
+    for (std::size_t d = 1; d < nd; ++d) {
+      const double want = pre[nl] * double(d) / double(nd);
+      cut[d] = std::uint32_t(std::lower_bound(pre.begin(), pre.end(), want) - pre.begin());
+      cut[d] = std::max(cut[d], cut[d - 1]);
+    }
+  }
+
+  fmmcu_p2p_job j{};
+  j.n_leaves = nl;
+  j.n_src = std::uint32_t(job.src_z->size());
+  j.n_eval = ne;
+  j.pt_off = pt_off_.data();
+  j.ev_off = ev_off_.data();
+  j.strong_off = s_off_.data();
+  j.strong_idx = s_idx_.data();
+  j.perm = job.pyramid->perm.data();
+  j.src_z = reinterpret_cast<const double*>(job.src_z->data());
+  j.src_m = reinterpret_cast<const double*>(job.src_m->data());
+  j.eval_y = reinterpret_cast<const double*>(job.eval_y->data());
+  j.eval_sid = (job.eval_sid && !job.eval_sid->empty()) ? job.eval_sid->data() : nullptr;
+  j.kernel = job.kernel == Kernel::harmonic ? FMMCU_KERNEL_HARMONIC : FMMCU_KERNEL_LOG;
+  j.smoother = job.smoother.kind == Smoother::Kind::none      ? FMMCU_SMOOTH_NONE
+               : job.smoother.kind == Smoother::Kind::gaussian ? FMMCU_SMOOTH_GAUSSIAN
+                                                               : FMMCU_SMOOTH_PLUMMER;
+  j.delta = job.smoother.delta;
+  j.mode = cs_.exact ? FMMCU_MODE_EXACT : FMMCU_MODE_FAST;
+  j.out = reinterpret_cast<double*>(out.data());
+  for (std::size_t d = 0; d < nd; ++d) {
+    j.leaf_begin = cut[d];
+    j.leaf_end = cut[d + 1];
+    const int rc = fmmcu_p2p_launch(ctx_[d], &j);
+    if (rc != FMMCU_OK) {
+      for (std::size_t q = 0; q < d; ++q) {
+        std::uint64_t p;
+        double s;
+        fmmcu_p2p_finish(ctx_[q], &p, &s);
+      }
+      raise(ctx_[d], rc, "cuda near field launch");
+    }
+  }
+  inflight_ = true;
+}
+
+NearFieldStats CudaBackend::finish() {
+  if (!inflight_) return NearFieldStats{};
+  inflight_ = false;
+  NearFieldStats st;
+  int bad = FMMCU_OK;
+  fmmcu_ctx* bad_ctx = nullptr;
+  for (fmmcu_ctx* c : ctx_) {
+    std::uint64_t pairs = 0;
+    double secs = 0;
+    const int rc = fmmcu_p2p_finish(c, &pairs, &secs);
+    if (rc != FMMCU_OK && bad == FMMCU_OK) {
+      bad = rc;
+      bad_ctx = c;
+    }
+    st.pair_evals += pairs;
+    st.seconds = std::max(st.seconds, secs);
+  }
+  if (bad != FMMCU_OK) raise(bad_ctx, bad, "cuda near field");
+  return st;
+}
+
+void CudaBackend::m2l_launch(int p, Kernel kernel, const std::vector<cplx>& centers,
+                             const std::vector<cplx>& coeffs,
+                             const std::vector<std::uint32_t>& target_box,
+                             const std::vector<std::uint32_t>& weak_off,
+                             const std::vector<std::uint32_t>& weak_idx, std::vector<cplx>& out) {
+  out.assign(target_box.size() * std::size_t(p + 1), cplx(0, 0));
+  fmmcu_m2l_job j{};
+  j.p = p;
+  j.kernel = kernel == Kernel::harmonic ? FMMCU_KERNEL_HARMONIC : FMMCU_KERNEL_LOG;
+  j.n_boxes = std::uint32_t(centers.size());
+  j.centers = reinterpret_cast<const double*>(centers.data());
+  j.coeffs = reinterpret_cast<const double*>(coeffs.data());
+  j.n_targets = std::uint32_t(target_box.size());
+  j.target_box = target_box.data();
+  j.weak_off = weak_off.data();
+  j.weak_idx = weak_idx.data();
+  j.out = reinterpret_cast<double*>(out.data());
+  const int rc = fmmcu_m2l_launch(ctx_[0], &j);
+  if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l launch");
+}
+
+std::uint64_t CudaBackend::m2l_finish(double* seconds) {
+  std::uint64_t ops = 0;
+  double s = 0;
+  const int rc = fmmcu_m2l_finish(ctx_[0], &ops, &s);
+  if (seconds) *seconds = s;
+  if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l");
+  return ops;
+}
+
+}  // namespace fmm

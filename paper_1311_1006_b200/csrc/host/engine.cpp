@@ -1,0 +1,413 @@
+// fmm-b200 — FMM evaluation pipeline (host orchestration).
+//
+// Semantics of the reference proj/src/engine.cpp:19-347: partition
+// (pyramid + connectivity + permutation) -> P2M -> serial M2M -> launch the
+// near field -> downward pass (L2L + M2L, fixed per-box accumulation order)
+// -> join -> assembly (near + L2P), with the same PhaseTimings / WorkCounters
+// and the observer hook the autotuner hangs on.
+//
+// B200 additions:
+//  * BackendKind::cuda runs the near field on the GPU(s) concurrently with
+//    the CPU downward pass (cpu_wait = time blocked in finish()).
+//  * FmmConfig::m2l_on_device offloads every M2L of every level in one
+//    batched launch that overlaps the device P2P; the host keeps the cheap
+//    L2L chain and adds the device M2L sums per box (local = L2L(parent) +
+//    sum_w M2L(w)).  m2l_ops is identical to the CPU path.
+#include <chrono>
+#include <cmath>
+
+#include "fmm/cuda_backend.hpp"
+#include "fmm/engine.hpp"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace fmm {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+Expansion fresh(cplx center, Expansion::Kind kind, Kernel kernel, int p) {
+  Expansion e;
+  e.center = center;
+  e.kind = kind;
+  e.kernel = kernel;
+  e.coeffs.assign(std::size_t(p) + 1, cplx(0, 0));
+  return e;
+}
+
+// P2M on every non-empty finest box (engine.cpp:37-59 / :244-265).
+void p2m_finest(const Pyramid& pyr, const std::vector<cplx>& zp, const std::vector<cplx>& mp,
+                Kernel kernel, int p, int threads, std::vector<Expansion>& fexp) {
+  const std::vector<MBox>& fine = pyr.finest();
+#pragma omp parallel for schedule(dynamic) num_threads(threads)
+  for (std::int64_t i = 0; i < std::int64_t(fine.size()); ++i) {
+    const MBox& b = fine[i];
+    if (b.n_points() == 0) continue;
+    fexp[i] = p2m(b.center, std::span<const cplx>(zp.data() + b.point_begin, b.n_points()),
+                  std::span<const cplx>(mp.data() + b.point_begin, b.n_points()), kernel, p);
+  }
+}
+
+// Serial M2M chain: parent = sum of its shifted children (engine.cpp:61-80).
+void m2m_chain(const Pyramid& pyr, Kernel kernel, int p, ExpansionPyramid& out) {
+  for (int l = pyr.finest_level() - 1; l >= 0; --l) {
+    for (std::size_t i = 0; i < pyr.levels[l].size(); ++i) {
+      const MBox& b = pyr.levels[l][i];
+      if (b.n_points() == 0) continue;
+      Expansion& acc = out.levels[l][i];
+      acc = fresh(b.center, Expansion::Kind::outgoing, kernel, p);
+      for (std::size_t c = 4 * i; c < 4 * i + 4; ++c) {
+        const Expansion& kid = out.levels[l + 1][c];
+        if (kid.coeffs.empty()) continue;
+        const Expansion moved = m2m(kid, b.center);
+        for (int k = 0; k <= p; ++k) acc.coeffs[k] += moved.coeffs[k];
+      }
+    }
+  }
+}
+
+struct Downward {
+  const Pyramid& pyr;
+  const Connectivity& conn;
+  const ExpansionPyramid& out;
+  ExpansionPyramid& loc;
+  Kernel kernel;
+  int p;
+};
+
+// Local of one box: L2L from the parent (l >= 2), then M2L from each weak
+// partner with content, ascending (engine.cpp:96-114).
+void local_of(Downward& d, int l, std::uint32_t i, std::uint64_t& ops) {
+  const MBox& b = d.pyr.levels[l][i];
+  if (b.n_evals() == 0) return;
+  Expansion& me = d.loc.levels[l][i];
+  me = fresh(b.center, Expansion::Kind::ingoing, d.kernel, d.p);
+  if (l >= 2) {
+    const Expansion& up = d.loc.levels[l - 1][i / 4];
+    if (!up.coeffs.empty()) l2l_add(up, me);
+  }
+  for (std::uint32_t w : d.conn.levels[l].weak[i]) {
+    const Expansion& src = d.out.levels[l][w];
+    if (src.coeffs.empty()) continue;
+    m2l_add(src, me);
+    ++ops;
+  }
+}
+
+void subtree(Downward& d, int l, std::uint32_t i, std::uint64_t& ops) {
+  if (l + 1 >= d.pyr.n_levels || d.pyr.levels[l][i].n_evals() == 0) return;
+  for (std::uint32_t c = 4 * i; c < 4 * i + 4; ++c) {
+    local_of(d, l + 1, c, ops);
+    subtree(d, l + 1, c, ops);
+  }
+}
+
+ExpansionPyramid empty_like(const Pyramid& pyr) {
+  ExpansionPyramid e;
+  e.levels.resize(pyr.n_levels);
+  for (int l = 0; l < pyr.n_levels; ++l) e.levels[l].resize(pyr.levels[l].size());
+  return e;
+}
+
+// Device M2L: flatten all levels, launch on the cuda backend.
+struct DeviceM2L {
+  std::vector<cplx> centers, coeffs, sums;
+  std::vector<std::uint32_t> tbox, woff, widx;
+  std::vector<std::uint32_t> level_base;  // global id of box 0 of level l
+  std::vector<std::int64_t> slot;         // global box id -> target row (-1 if none)
+};
+
+void device_m2l_launch(CudaBackend& be, const Pyramid& pyr, const Connectivity& conn,
+                       const ExpansionPyramid& out, Kernel kernel, int p, DeviceM2L& dm) {
+  const int L = pyr.n_levels;
+  dm.level_base.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l)
+    dm.level_base[l + 1] = dm.level_base[l] + std::uint32_t(pyr.levels[l].size());
+  const std::uint32_t nb = dm.level_base[L];
+  const std::size_t P1 = std::size_t(p) + 1;
+  dm.centers.resize(nb);
+  dm.coeffs.assign(std::size_t(nb) * P1, cplx(0, 0));
+  dm.slot.assign(nb, -1);
+  dm.tbox.clear();
+  dm.woff.assign(1, 0);
+  dm.widx.clear();
+  for (int l = 0; l < L; ++l) {
+    for (std::size_t i = 0; i < pyr.levels[l].size(); ++i) {
+      const std::uint32_t g = dm.level_base[l] + std::uint32_t(i);
+      dm.centers[g] = pyr.levels[l][i].center;
+      const Expansion& e = out.levels[l][i];
+      if (!e.coeffs.empty()) std::copy(e.coeffs.begin(), e.coeffs.end(), dm.coeffs.begin() + g * P1);
+    }
+  }
+  for (int l = 1; l < L; ++l) {
+    for (std::size_t i = 0; i < pyr.levels[l].size(); ++i) {
+      if (pyr.levels[l][i].n_evals() == 0) continue;
+      const std::uint32_t g = dm.level_base[l] + std::uint32_t(i);
+      dm.slot[g] = std::int64_t(dm.tbox.size());
+      dm.tbox.push_back(g);
+      for (std::uint32_t w : conn.levels[l].weak[i])
+        if (!out.levels[l][w].coeffs.empty()) dm.widx.push_back(dm.level_base[l] + w);
+      dm.woff.push_back(std::uint32_t(dm.widx.size()));
+    }
+  }
+  be.m2l_launch(p, kernel, dm.centers, dm.coeffs, dm.tbox, dm.woff, dm.widx, dm.sums);
+}
+
+// Host half of the device downward pass: L2L chain + device M2L sums.
+ExpansionPyramid device_m2l_assemble(const Pyramid& pyr, const DeviceM2L& dm, Kernel kernel,
+                                     int p, int threads) {
+  ExpansionPyramid loc = empty_like(pyr);
+  const std::size_t P1 = std::size_t(p) + 1;
+  for (int l = 1; l < pyr.n_levels; ++l) {
+    const std::int64_t n = std::int64_t(pyr.levels[l].size());
+#pragma omp parallel for schedule(dynamic, 64) num_threads(threads)
+    for (std::int64_t i = 0; i < n; ++i) {
+      const MBox& b = pyr.levels[l][i];
+      if (b.n_evals() == 0) continue;
+      Expansion& me = loc.levels[l][i];
+      me = fresh(b.center, Expansion::Kind::ingoing, kernel, p);
+      if (l >= 2) {
+        const Expansion& up = loc.levels[l - 1][i / 4];
+        if (!up.coeffs.empty()) l2l_add(up, me);
+      }
+      const std::int64_t row = dm.slot[dm.level_base[l] + std::uint32_t(i)];
+      const cplx* s = dm.sums.data() + std::size_t(row) * P1;
+      for (std::size_t k = 0; k < P1; ++k) me.coeffs[k] += s[k];
+    }
+  }
+  return loc;
+}
+
+}  // namespace
+
+int FmmConfig::expansion_order() const {
+  if (p_override > 0) return std::min(p_override, kMaxOrder);
+  return choose_p(p_rule, tol, theta, p_calibration);
+}
+
+// engine.cpp:24-35 (closed forms for a uniform unit square)
+CostEstimate estimate_cost(double n, int n_levels, double theta, int p) {
+  if (!(n > 0) || n_levels < 1 || !(theta > 0.0 && theta < 1.0) || p < 1)
+    throw InvalidParameter("estimate_cost: invalid parameters");
+  const double leaves = std::pow(4.0, n_levels - 1);
+  const double ring = M_PI * std::pow((1.0 + theta) / theta, 2.0);
+  const double pp = double(p) * p;
+  CostEstimate c;
+  c.c_p2p = n * n / (2.0 * leaves) * ring;
+  c.c_m2l = 1.5 * leaves * pp * ring;
+  c.c_m2m = (4.0 / 3.0) * leaves * pp;
+  c.c_p2m = n * p;
+  return c;
+}
+
+ExpansionPyramid upward_pass(const Pyramid& pyr, const std::vector<cplx>& src_z_perm,
+                             const std::vector<cplx>& src_m_perm, Kernel kernel, int p,
+                             int threads, WorkCounters* counters) {
+  ExpansionPyramid out = empty_like(pyr);
+  p2m_finest(pyr, src_z_perm, src_m_perm, kernel, p, threads, out.levels[pyr.finest_level()]);
+  if (counters) counters->p2m_points += src_z_perm.size();
+  m2m_chain(pyr, kernel, p, out);
+  return out;
+}
+
+// engine.cpp:127-169: serial breadth-first walk to the split level, then one
+// OpenMP task per split-level subtree (no shared mutable state).
+ExpansionPyramid downward_pass(const Pyramid& pyr, const Connectivity& conn,
+                               const ExpansionPyramid& outgoing, int p, int task_split_level,
+                               int threads, WorkCounters* counters) {
+  ExpansionPyramid loc = empty_like(pyr);
+  Kernel kernel = outgoing.levels[0][0].kernel;
+  if (outgoing.levels[0][0].coeffs.empty()) kernel = Kernel::harmonic;
+  Downward d{pyr, conn, outgoing, loc, kernel, p};
+  const int split = std::max(0, std::min(task_split_level, pyr.n_levels - 1));
+  std::uint64_t ops = 0;
+  for (int l = 1; l <= split; ++l)
+    for (std::uint32_t i = 0; i < pyr.levels[l].size(); ++i) local_of(d, l, i, ops);
+  const std::uint32_t roots = std::uint32_t(pyr.levels[split].size());
+  if (threads > 1 && split < pyr.n_levels - 1) {
+#pragma omp parallel num_threads(threads)
+#pragma omp single
+    for (std::uint32_t i = 0; i < roots; ++i) {
+#pragma omp task firstprivate(i)
+      {
+        std::uint64_t mine = 0;
+        subtree(d, split, i, mine);
+#pragma omp atomic
+        ops += mine;
+      }
+    }
+  } else {
+    for (std::uint32_t i = 0; i < roots; ++i) subtree(d, split, i, ops);
+  }
+  if (counters) counters->m2l_ops += ops;
+  return loc;
+}
+
+namespace {
+
+void permute_inputs(const Pyramid& pyr, const SourceSet& s, const EvalSet& e, int threads,
+                    std::vector<cplx>& zp, std::vector<cplx>& mp, std::vector<cplx>& yp,
+                    std::vector<std::int64_t>& sidp) {
+  zp.resize(s.size());
+  mp.resize(s.size());
+#pragma omp parallel for schedule(static) num_threads(threads)
+  for (std::int64_t i = 0; i < std::int64_t(s.size()); ++i) {
+    zp[i] = s.z[pyr.perm[i]];
+    mp[i] = s.m[pyr.perm[i]];
+  }
+  yp.resize(e.size());
+  sidp.clear();
+  if (!e.source_id.empty()) sidp.resize(e.size());
+#pragma omp parallel for schedule(static) num_threads(threads)
+  for (std::int64_t i = 0; i < std::int64_t(e.size()); ++i) {
+    yp[i] = e.y[pyr.eval_perm[i]];
+    if (!sidp.empty()) sidp[i] = e.source_id[pyr.eval_perm[i]];
+  }
+}
+
+}  // namespace
+
+// engine.cpp:171-194
+std::vector<cplx> nearfield_eval(NearFieldBackend& backend, const Pyramid& pyr,
+                                 const Connectivity& conn, const SourceSet& sources,
+                                 const EvalSet& evals, Kernel kernel, const Smoother& smoother) {
+  std::vector<cplx> zp, mp, yp;
+  std::vector<std::int64_t> sidp;
+  permute_inputs(pyr, sources, evals, 1, zp, mp, yp, sidp);
+  NearFieldJob job{&pyr, &conn.finest(), &zp, &mp, &yp, &sidp, kernel, smoother, 1};
+  std::vector<cplx> near;
+  backend.launch(job, near);
+  backend.finish();
+  std::vector<cplx> out(evals.size());
+  for (std::size_t i = 0; i < evals.size(); ++i) out[pyr.eval_perm[i]] = near[i];
+  return out;
+}
+
+FmmEngine::FmmEngine(FmmConfig cfg) : cfg_(std::move(cfg)), backend_kind_(cfg_.backend) {
+  backend_ = make_backend(cfg_.backend, cfg_.throttle, cfg_.cuda);
+}
+
+FmmEngine::~FmmEngine() = default;
+
+void FmmEngine::set_config(const FmmConfig& cfg) {
+  const bool devices_changed = cfg.backend == BackendKind::cuda &&
+                               (cfg.cuda.devices != cfg_.cuda.devices || cfg.cuda.exact != cfg_.cuda.exact);
+  if (cfg.backend != backend_kind_ || devices_changed) {
+    backend_ = make_backend(cfg.backend, cfg.throttle, cfg.cuda);
+    backend_kind_ = cfg.backend;
+  }
+  cfg_ = cfg;
+}
+
+EvalResult FmmEngine::evaluate(const SourceSet& sources, const EvalSet& evals) {
+  if (!(cfg_.theta > 0.0 && cfg_.theta < 1.0)) throw InvalidParameter("evaluate: theta outside (0,1)");
+  if (cfg_.n_levels < 1) throw InvalidParameter("evaluate: n_levels < 1");
+  if (cfg_.worker_threads < 1) throw InvalidParameter("evaluate: worker_threads < 1");
+  if (cfg_.p_override <= 0 && !(cfg_.tol > 0.0 && cfg_.tol < 1.0))
+    throw InvalidParameter("evaluate: tol outside (0,1)");
+  if (sources.size() == 0) throw InvalidInput("evaluate: empty source set");
+  if (cfg_.m2l_on_device && cfg_.backend != BackendKind::cuda)
+    throw InvalidParameter("evaluate: m2l_on_device requires the cuda backend");
+
+  EvalResult res;
+  res.p = cfg_.expansion_order();
+  const int p = res.p;
+  const int threads = cfg_.worker_threads;
+  PhaseTimings& T = res.timings;
+  const auto t_start = Clock::now();
+
+  // ---- partition ------------------------------------------------------------
+  const Pyramid pyr = build_pyramid(sources, evals, cfg_.n_levels, threads);
+  const Connectivity conn = build_connectivity(pyr, cfg_.theta);
+  std::vector<cplx> zp, mp, yp;
+  std::vector<std::int64_t> sidp;
+  permute_inputs(pyr, sources, evals, threads, zp, mp, yp, sidp);
+  T.t_partition = since(t_start);
+
+  // ---- upward -------------------------------------------------------------
+  const auto t_p2m = Clock::now();
+  ExpansionPyramid outgoing = empty_like(pyr);
+  p2m_finest(pyr, zp, mp, cfg_.kernel, p, threads, outgoing.levels[pyr.finest_level()]);
+  res.counters.p2m_points += sources.size();
+  T.t_p2m = since(t_p2m);
+  const auto t_up = Clock::now();
+  m2m_chain(pyr, cfg_.kernel, p, outgoing);
+  T.t_upward = since(t_up);
+
+  // ---- near field || downward ----------------------------------------------
+  NearFieldJob job{&pyr, &conn.finest(), &zp, &mp, &yp, &sidp, cfg_.kernel, cfg_.smoother, threads};
+  std::vector<cplx> near;
+  try {
+    backend_->launch(job, near);
+  } catch (const std::exception& e) {
+    throw BackendError("nearfield launch", e.what());
+  }
+
+  const auto t_m2l = Clock::now();
+  ExpansionPyramid locals;
+  if (cfg_.m2l_on_device) {
+    auto* cb = dynamic_cast<CudaBackend*>(backend_.get());
+    DeviceM2L dm;
+    try {
+      device_m2l_launch(*cb, pyr, conn, outgoing, cfg_.kernel, p, dm);
+      res.counters.m2l_ops += cb->m2l_finish();
+    } catch (const SingularConfiguration&) {
+      try {
+        backend_->finish();
+      } catch (...) {
+      }
+      throw;
+    } catch (const std::exception& e) {
+      try {
+        backend_->finish();
+      } catch (...) {
+      }
+      throw BackendError("m2l", e.what());
+    }
+    locals = device_m2l_assemble(pyr, dm, cfg_.kernel, p, threads);
+  } else {
+    locals = downward_pass(pyr, conn, outgoing, p, cfg_.task_split_level, threads, &res.counters);
+  }
+  T.t_m2l = since(t_m2l);
+
+  const auto t_join = Clock::now();
+  NearFieldStats nf;
+  try {
+    nf = backend_->finish();
+  } catch (const std::exception& e) {
+    throw BackendError("nearfield", e.what());
+  }
+  T.cpu_wait = backend_->concurrent() ? since(t_join) : 0.0;
+  T.t_p2p = nf.seconds;
+  res.counters.p2p_pairs += nf.pair_evals;
+
+  // ---- assembly (engine.cpp:316-339) -----------------------------------------
+  const auto t_asm = Clock::now();
+  const std::vector<MBox>& fine = pyr.finest();
+  const std::vector<Expansion>& floc = locals.levels[pyr.finest_level()];
+  res.potentials.resize(evals.size());
+  std::uint64_t l2p = 0;
+#pragma omp parallel for schedule(dynamic) reduction(+ : l2p) num_threads(threads)
+  for (std::int64_t i = 0; i < std::int64_t(fine.size()); ++i) {
+    const MBox& b = fine[i];
+    const Expansion& loc = floc[i];
+    const bool far = !loc.coeffs.empty();
+    for (std::uint32_t e = b.eval_begin; e < b.eval_end; ++e) {
+      const cplx v = far ? near[e] + eval_local(loc, yp[e]) : near[e];
+      res.potentials[pyr.eval_perm[e]] = v;
+    }
+    if (far) l2p += b.n_evals();
+  }
+  res.counters.l2p_points += l2p;
+  const double t_assembly = since(t_asm);
+  T.t_q = T.t_partition + T.t_p2m + T.t_upward + t_assembly;
+  T.t_total = since(t_start);
+  if (observer_) observer_(*this, res);
+  return res;
+}
+
+}  // namespace fmm

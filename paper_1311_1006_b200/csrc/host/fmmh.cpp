@@ -1,0 +1,409 @@
+// fmm-b200 — flat C ABI over the C++ host library (include/fmm_host.h).
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+
+#include "fmm/autotune.hpp"
+#include "fmm/cuda_backend.hpp"
+#include "fmm/engine.hpp"
+#include "fmm/sims.hpp"
+#include "fmm_host.h"
+
+using namespace fmm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int code_of(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const InvalidParameter*>(&e)) return 1;
+  if (dynamic_cast<const InvalidInput*>(&e)) return 2;
+  if (dynamic_cast<const SingularConfiguration*>(&e)) return 3;
+  if (dynamic_cast<const BackendError*>(&e)) return 4;
+  if (dynamic_cast<const InvalidState*>(&e) || dynamic_cast<const NoMeasurement*>(&e)) return 5;
+  return 9;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  } catch (...) {
+    g_err = "unknown exception";
+    return 9;
+  }
+}
+
+std::vector<cplx> to_cplx(const double* v, int64_t n) {
+  std::vector<cplx> out(std::size_t(n > 0 ? n : 0));
+  for (int64_t i = 0; i < n; ++i) out[i] = cplx(v[2 * i], v[2 * i + 1]);
+  return out;
+}
+
+SourceSet sources_of(const double* z, const double* m, int64_t n) {
+  SourceSet s;
+  s.z = to_cplx(z, n);
+  s.m = to_cplx(m, n);
+  return s;
+}
+
+EvalSet evals_of(const double* y, const int64_t* sid, int64_t n) {
+  EvalSet e;
+  if (n > 0) e.y = to_cplx(y, n);
+  if (sid && n > 0) e.source_id.assign(sid, sid + n);
+  return e;
+}
+
+Smoother smoother_of(int kind, double delta) {
+  if (kind == 1) return Smoother::gaussian(delta);
+  if (kind == 2) return Smoother::plummer(delta);
+  return Smoother::none();
+}
+
+BackendKind backend_of(int b) {
+  switch (b) {
+    case 0: return BackendKind::serial;
+    case 1: return BackendKind::pool;
+    case 2: return BackendKind::throttled;
+    case 3: return BackendKind::cuda;
+  }
+  throw InvalidParameter("unknown backend id " + std::to_string(b));
+}
+
+FmmConfig config_of(const double* f, const int* i, const int* devices, int n_devices) {
+  FmmConfig c;
+  c.theta = f[0];
+  c.tol = f[1];
+  c.p_calibration = f[2];
+  c.smoother = smoother_of(i[7], f[3]);
+  c.throttle.latency_s = f[4];
+  c.throttle.throughput = f[5];
+  c.n_levels = i[0];
+  c.kernel = i[1] ? Kernel::logarithmic : Kernel::harmonic;
+  c.p_rule = i[2] ? PRule::table : PRule::formula;
+  c.p_override = i[3];
+  c.backend = backend_of(i[4]);
+  c.worker_threads = i[5];
+  c.task_split_level = i[6];
+  c.cuda.exact = i[8] != 0;
+  c.m2l_on_device = i[9] != 0;
+  for (int d = 0; d < n_devices; ++d) c.cuda.devices.push_back(devices[d]);
+  return c;
+}
+
+struct Tree {
+  SourceSet src;
+  EvalSet ev;
+  Pyramid pyr;
+  Connectivity conn;
+};
+
+void write_timings(const EvalResult& r, double* timings, uint64_t* counters) {
+  if (timings) {
+    const PhaseTimings& t = r.timings;
+    const double v[8] = {t.t_partition, t.t_p2m, t.t_upward, t.t_m2l,
+                         t.t_p2p,       t.t_q,   t.t_total,  t.cpu_wait};
+    std::memcpy(timings, v, sizeof v);
+  }
+  if (counters) {
+    counters[0] = r.counters.p2p_pairs;
+    counters[1] = r.counters.m2l_ops;
+    counters[2] = r.counters.p2m_points;
+    counters[3] = r.counters.l2p_points;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fmmh_last_error(void) { return g_err.c_str(); }
+
+void fmmh_make_distribution(int kind, int64_t n, uint64_t seed, double* z, double* m) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u01(0.0, 1.0);
+  if (kind == 3 || kind == 4) {  // tests/test_util.hpp:10-23 (box = 1)
+    const bool positive = kind == 4;
+    std::uniform_real_distribution<double> um(positive ? 0.1 : -1.0, 1.0);
+    for (int64_t i = 0; i < n; ++i) {
+      z[2 * i] = u01(rng);
+      z[2 * i + 1] = u01(rng);
+      m[2 * i] = um(rng);
+      m[2 * i + 1] = positive ? 0.0 : um(rng);
+    }
+    return;
+  }
+  std::normal_distribution<double> g(0.0, 1.0);
+  for (int64_t i = 0; i < n; ++i) {  // tools/atfmm.cpp:70-86 (+ clusters)
+    if (kind == 2) {
+      const int c = int(i % 8);
+      const double g1 = g(rng), g2 = g(rng);
+      z[2 * i] = 0.15 + 0.1 * c + 0.02 * g1;
+      z[2 * i + 1] = 0.5 + 0.3 * std::sin(double(c)) + 0.02 * g2;
+    } else {
+      z[2 * i] = u01(rng);
+      z[2 * i + 1] = kind == 1 ? 0.005 * u01(rng) : u01(rng);
+    }
+    m[2 * i] = u01(rng);
+    m[2 * i + 1] = 0.0;
+  }
+}
+
+void* fmmh_tree_build(const double* z, const double* m, int64_t n_src, const double* y,
+                      const int64_t* sid, int64_t n_eval, int n_levels, double theta,
+                      int threads) {
+  std::unique_ptr<Tree> t;
+  const int rc = guarded([&] {
+    t = std::make_unique<Tree>();
+    t->src = sources_of(z, m, n_src);
+    t->ev = evals_of(y, sid, n_eval);
+    t->pyr = build_pyramid(t->src, t->ev, n_levels, threads);
+    t->conn = build_connectivity(t->pyr, theta);
+  });
+  return rc == 0 ? t.release() : nullptr;
+}
+
+void fmmh_tree_free(void* h) { delete static_cast<Tree*>(h); }
+
+int64_t fmmh_tree_nboxes(void* h, int level) {
+  return int64_t(static_cast<Tree*>(h)->pyr.levels[level].size());
+}
+
+void fmmh_tree_boxes(void* h, int level, double* f64, uint32_t* u32) {
+  const auto& boxes = static_cast<Tree*>(h)->pyr.levels[level];
+  for (std::size_t i = 0; i < boxes.size(); ++i) {
+    const MBox& b = boxes[i];
+    f64[5 * i + 0] = b.center.real();
+    f64[5 * i + 1] = b.center.imag();
+    f64[5 * i + 2] = b.half_width;
+    f64[5 * i + 3] = b.half_height;
+    f64[5 * i + 4] = b.radius;
+    u32[4 * i + 0] = b.point_begin;
+    u32[4 * i + 1] = b.point_end;
+    u32[4 * i + 2] = b.eval_begin;
+    u32[4 * i + 3] = b.eval_end;
+  }
+}
+
+void fmmh_tree_perm(void* h, uint32_t* perm, uint32_t* eperm) {
+  const Pyramid& p = static_cast<Tree*>(h)->pyr;
+  std::memcpy(perm, p.perm.data(), p.perm.size() * 4);
+  if (!p.eval_perm.empty()) std::memcpy(eperm, p.eval_perm.data(), p.eval_perm.size() * 4);
+}
+
+int64_t fmmh_tree_nnz(void* h, int level, int weak) {
+  const LevelConn& lc = static_cast<Tree*>(h)->conn.levels[level];
+  int64_t n = 0;
+  for (const auto& v : weak ? lc.weak : lc.strong) n += int64_t(v.size());
+  return n;
+}
+
+void fmmh_tree_lists(void* h, int level, int weak, uint32_t* off, uint32_t* idx) {
+  const LevelConn& lc = static_cast<Tree*>(h)->conn.levels[level];
+  const auto& lists = weak ? lc.weak : lc.strong;
+  uint32_t k = 0;
+  for (std::size_t i = 0; i < lists.size(); ++i) {
+    off[i] = k;
+    for (uint32_t v : lists[i]) idx[k++] = v;
+  }
+  off[lists.size()] = k;
+}
+
+int fmmh_tree_nearfield(void* h, int backend, const int* devices, int n_devices, int exact,
+                        int kernel, int smoother, double delta, int threads, double* out,
+                        uint64_t* pairs, double* seconds) {
+  return guarded([&] {
+    Tree* t = static_cast<Tree*>(h);
+    const Pyramid& pyr = t->pyr;
+    std::vector<cplx> zp(t->src.size()), mp(t->src.size()), yp(t->ev.size());
+    std::vector<int64_t> sidp;
+    for (std::size_t i = 0; i < zp.size(); ++i) {
+      zp[i] = t->src.z[pyr.perm[i]];
+      mp[i] = t->src.m[pyr.perm[i]];
+    }
+    if (!t->ev.source_id.empty()) sidp.resize(yp.size());
+    for (std::size_t i = 0; i < yp.size(); ++i) {
+      yp[i] = t->ev.y[pyr.eval_perm[i]];
+      if (!sidp.empty()) sidp[i] = t->ev.source_id[pyr.eval_perm[i]];
+    }
+    CudaSettings cs;
+    cs.exact = exact != 0;
+    for (int d = 0; d < n_devices; ++d) cs.devices.push_back(devices[d]);
+    auto be = make_backend(backend_of(backend), ThrottleSettings{0.0, 1.0}, cs);
+    NearFieldJob job{&pyr, &t->conn.finest(), &zp, &mp, &yp, &sidp,
+                     kernel ? Kernel::logarithmic : Kernel::harmonic, smoother_of(smoother, delta),
+                     threads};
+    std::vector<cplx> near;
+    be->launch(job, near);
+    const NearFieldStats st = be->finish();
+    if (out && !near.empty()) std::memcpy(out, near.data(), near.size() * 16);
+    if (pairs) *pairs = st.pair_evals;
+    if (seconds) *seconds = st.seconds;
+  });
+}
+
+void* fmmh_engine_create(const double* cfg_f, const int* cfg_i, const int* devices,
+                         int n_devices) {
+  std::unique_ptr<FmmEngine> e;
+  const int rc =
+      guarded([&] { e = std::make_unique<FmmEngine>(config_of(cfg_f, cfg_i, devices, n_devices)); });
+  return rc == 0 ? e.release() : nullptr;
+}
+
+int fmmh_engine_set_config(void* h, const double* cfg_f, const int* cfg_i, const int* devices,
+                           int n_devices) {
+  return guarded([&] {
+    static_cast<FmmEngine*>(h)->set_config(config_of(cfg_f, cfg_i, devices, n_devices));
+  });
+}
+
+int fmmh_engine_evaluate(void* h, const double* z, const double* m, int64_t n_src,
+                         const double* y, const int64_t* sid, int64_t n_eval, double* out,
+                         double* timings, uint64_t* counters, int* p) {
+  return guarded([&] {
+    const SourceSet s = sources_of(z, m, n_src);
+    const EvalSet e = evals_of(y, sid, n_eval);
+    const EvalResult r = static_cast<FmmEngine*>(h)->evaluate(s, e);
+    if (out && !r.potentials.empty()) std::memcpy(out, r.potentials.data(), r.potentials.size() * 16);
+    write_timings(r, timings, counters);
+    if (p) *p = r.p;
+  });
+}
+
+uint64_t fmmh_engine_kernel_launches(void* h) {
+  (void)h;
+  return 0;  // reported per backend via fmmcu_kernel_launches; kept for ABI symmetry
+}
+
+void fmmh_engine_free(void* h) { delete static_cast<FmmEngine*>(h); }
+
+int fmmh_controller_run(int kind, const double* ccfg_f, const int* ccfg_i, double theta0,
+                        int nl0, uint64_t seed, int64_t n, const double* meas, double* out,
+                        int* events) {
+  return guarded([&] {
+    ControllerConfig cc;
+    cc.theta_min = ccfg_f[0];
+    cc.theta_max = ccfg_f[1];
+    cc.base_thetastep = ccfg_f[2];
+    cc.cap = ccfg_f[3];
+    cc.nl_min = ccfg_i[0];
+    cc.nl_max = ccfg_i[1];
+    cc.theta_every = ccfg_i[2];
+    cc.nl_every = ccfg_i[3];
+    cc.filter_window = ccfg_i[4];
+    cc.init_fiblength = ccfg_i[5];
+    cc.max_fiblength = ccfg_i[6];
+    Controller ctl(static_cast<TunerKind>(kind), cc, Params{theta0, nl0}, seed);
+    for (int64_t i = 0; i < n; ++i) {
+      const Measurement m{int(i + 1), meas[3 * i], meas[3 * i + 1], meas[3 * i + 2] != 0.0};
+      const Params p = ctl.step(m);
+      out[2 * i] = p.theta;
+      out[2 * i + 1] = p.n_levels;
+      const StepEvent& ev = ctl.last_event();
+      events[3 * i] = int(ev.proposed);
+      events[3 * i + 1] = ev.move_dir;
+      events[3 * i + 2] = ev.accepted;
+    }
+  });
+}
+
+int fmmh_vortex_run(int n, double aspect, int steps, int tuner, double cap, uint64_t seed,
+                    const double* cfg_f, const int* cfg_i, const int* devices, int n_devices,
+                    double* trace, double* final_pos) {
+  return guarded([&] {
+    sims::VortexSystem sys = sims::init_shear_layer(n, aspect, 2.0 * aspect / n);
+    FmmEngine engine(config_of(cfg_f, cfg_i, devices, n_devices));
+    ControllerConfig cc;
+    cc.cap = cap;
+    cc.nl_max = std::max(engine.config().n_levels + 3, 8);
+    Controller ctl(static_cast<TunerKind>(tuner), cc,
+                   Params{engine.config().theta, engine.config().n_levels}, seed);
+    int it = 0;
+    // observer -> controller wiring as the reference CLI (atfmm.cpp:149-174)
+    engine.set_observer([&](FmmEngine& e, const EvalResult& r) {
+      ++it;
+      double* row = trace + 8 * std::size_t(it - 1);
+      row[0] = r.timings.t_total;
+      row[1] = r.timings.t_m2l;
+      row[2] = r.timings.t_p2p;
+      row[3] = r.timings.t_q;
+      row[4] = r.timings.cpu_wait;
+      row[5] = e.config().theta;
+      row[6] = e.config().n_levels;
+      row[7] = double(r.counters.p2p_pairs);
+      if (static_cast<TunerKind>(tuner) == TunerKind::none) return;
+      const Measurement m{it, r.timings.t_total, r.timings.cpu_wait, e.backend_concurrent()};
+      const Params next = ctl.step(m);
+      FmmConfig nc = e.config();
+      if (next.theta != nc.theta || next.n_levels != nc.n_levels) {
+        nc.theta = next.theta;
+        nc.n_levels = next.n_levels;
+        e.set_config(nc);
+      }
+    });
+    for (int s = 0; s < steps; ++s) sims::euler_step(sys, sims::vortex_velocities(sys, engine));
+    if (final_pos) std::memcpy(final_pos, sys.pos.data(), sys.pos.size() * 16);
+  });
+}
+
+int fmmh_m2l_add(int p, int kernel, const double* src_center, const double* coeffs,
+                 const double* tgt_center, double* local) {
+  return guarded([&] {
+    Expansion out;
+    out.center = cplx(src_center[0], src_center[1]);
+    out.kernel = kernel ? Kernel::logarithmic : Kernel::harmonic;
+    out.coeffs = to_cplx(coeffs, p + 1);
+    Expansion loc;
+    loc.center = cplx(tgt_center[0], tgt_center[1]);
+    loc.kind = Expansion::Kind::ingoing;
+    loc.kernel = out.kernel;
+    loc.coeffs = to_cplx(local, p + 1);
+    m2l_add(out, loc);
+    std::memcpy(local, loc.coeffs.data(), std::size_t(p + 1) * 16);
+  });
+}
+
+int fmmh_p2m(int p, int kernel, const double* center, const double* z, const double* m,
+             int64_t n, double* coeffs) {
+  return guarded([&] {
+    const std::vector<cplx> zz = to_cplx(z, n), mm = to_cplx(m, n);
+    const Expansion e = p2m(cplx(center[0], center[1]), zz, mm,
+                            kernel ? Kernel::logarithmic : Kernel::harmonic, p);
+    std::memcpy(coeffs, e.coeffs.data(), std::size_t(p + 1) * 16);
+  });
+}
+
+int fmmh_choose_p(int rule, double tol, double theta, double calibration) {
+  int p = -1;
+  const int rc = guarded([&] { p = choose_p(rule ? PRule::table : PRule::formula, tol, theta, calibration); });
+  return rc == 0 ? p : -rc;
+}
+
+int fmmh_estimate_cost(double n, int n_levels, double theta, int p, double* out4) {
+  return guarded([&] {
+    const CostEstimate c = estimate_cost(n, n_levels, theta, p);
+    out4[0] = c.c_p2p;
+    out4[1] = c.c_m2l;
+    out4[2] = c.c_m2m;
+    out4[3] = c.c_p2m;
+  });
+}
+
+int fmmh_p2p_direct(const double* z, const double* m, int64_t n_src, const double* y,
+                    const int64_t* sid, int64_t n_eval, int kernel, int smoother, double delta,
+                    double* out) {
+  return guarded([&] {
+    const std::vector<cplx> r = p2p_direct(evals_of(y, sid, n_eval), sources_of(z, m, n_src),
+                                           kernel ? Kernel::logarithmic : Kernel::harmonic,
+                                           smoother_of(smoother, delta));
+    if (!r.empty()) std::memcpy(out, r.data(), r.size() * 16);
+  });
+}
+
+}  // extern "C"
