@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""bench.py — B200 near-field (P2P) throughput of the balanced adaptive 2D FMM.
+
+Metric (BASELINE.json): P2P pair-interactions/sec (+ FMM evals/sec) at
+N = 10M, 1/2/4/8 B200 vs CPU.  Workload = config 4: N = 10,000,000 uniform
+points (x, y, m_re ~ U(0,1), std::mt19937_64(seed 4), tools/atfmm.cpp:70-86),
+self-evaluation, theta = 0.5, n_levels = 10 (38-39 points per leaf), harmonic
+kernel, FP64.  A step = one near-field pass over every target leaf.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one process per GPU: each rank evaluates a
+pair-work-balanced contiguous range of target leaves with sources replicated,
+and the potential slices are all-gathered over NVLink (NCCL) inside the timed
+step.  Rank 0 prints one JSON line.
+
+`--impl reference` times the reference's own CPU near-field loop
+(nearfield_run, proj/src/backend.cpp:73-89, compiled unmodified into
+oracle/_ref/libfmmref.so) on all host cores over a bounded sample of the same
+workload (a contiguous block of target leaves).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_PAIR = 23  # 2 DADD + r^2 (3) + 1/r^2 (8) + 2 DMUL + 4 DFMA (8)
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2 at clocks.max.sm
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--levels", type=int, default=10)
+    ap.add_argument("--theta", type=float, default=0.5)
+    ap.add_argument("--seed", type=int, default=4)
+    ap.add_argument("--dist", default="uniform")
+    ap.add_argument("--sample-frac", type=float, default=0.125,
+                    help="fraction of target leaves in one CPU-baseline step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fmm", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_desc():
+    model = "?"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        loaded = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- workload --
+def build_workload(args, threads):
+    from paper_1311_1006_b200 import fmm as F
+
+    t0 = time.perf_counter()
+    s = F.make_distribution(args.dist, args.n, args.seed)
+    e = F.EvalSet.self_of(s)
+    t1 = time.perf_counter()
+    tree = F.Tree(s, e, args.levels, args.theta, threads=threads)
+    t2 = time.perf_counter()
+    zp, mp, yp, sid = tree.permuted()
+    pt, ev, so, si = tree.leaf_csr()
+    wl = dict(pt=pt, ev=ev, so=so, si=si, perm=tree.perm, zp=zp, mp=mp, yp=yp, sid=sid,
+              n_leaves=len(pt) - 1, gen_s=t1 - t0, tree_s=t2 - t1)
+    del tree
+    return wl
+
+
+def config_block(args, world, extra=None):
+    c = {"workload": f"config4: N={args.n} {args.dist} self-eval, n_levels={args.levels} "
+                     f"(~{args.n / 4 ** (args.levels - 1):.1f} pts/leaf), theta={args.theta}, "
+                     f"harmonic, no smoother, P2P over every target leaf",
+         "n_points": args.n, "n_levels": args.levels, "theta": args.theta, "seed": args.seed,
+         "kernel": "harmonic", "precision": "fp64",
+         "parallelism": f"target-leaf shards x{world}, sources replicated, NCCL all-gather",
+         "l2": "inputs (320 MB packed sources + 160 MB evals) larger than the 126 MB L2"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------ CPU baseline --
+def cpu_baseline(wl, args, steps=1, warmup=0, threads=None):
+    """Reference nearfield_run on a contiguous sample of target leaves."""
+    from oracle import oracle as O
+
+    threads = threads or os.cpu_count()
+    nl = wl["n_leaves"]
+    lb = 0
+    le = max(1, int(nl * args.sample_frac))
+    csr = O.LeafCSR(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"])
+    if O.ref_available():
+        r = O.RefNearField(csr, wl["zp"], wl["mp"], wl["yp"], wl["sid"])
+        kind, cores = "reference", threads
+        times, pairs = [], 0
+        for i in range(warmup + steps):
+            _, pairs, secs = r.run(lb, le, parallel=True, threads=threads)
+            if i >= warmup:
+                times.append(secs)
+        r.close()
+    else:  # restated loop, single thread, smaller sample
+        kind, cores = "port", 1
+        le = max(1, le // 16)
+        times = []
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            _, pairs = O.nearfield(csr, wl["zp"], wl["mp"], wl["yp"], wl["sid"], leaf_begin=lb,
+                                   leaf_end=le)
+            if i >= warmup:
+                times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": pairs / best, "unit": "pairs/s", "cores": cores, "kind": kind,
+            "sample": f"target leaves [{lb},{le}) of {nl} ({pairs} pairs/step), "
+                      f"best of {len(times)}; {cpu_desc()['model']}",
+            "pairs_per_step": pairs, "seconds_per_step": statistics.median(times),
+            "step_seconds": times}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if world > 1 and rank != 0:
+        return 0  # rank 0 alone runs the CPU reference
+    wl = build_workload(args, os.cpu_count())
+    cb = cpu_baseline(wl, args, steps=args.steps, warmup=args.warmup)
+    ms = 1e3 * statistics.median(cb["step_seconds"])
+    line = {"impl": "reference", "metric": "p2p_pairs_per_sec", "value": cb["value"],
+            "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args, 1, {"sample": cb["sample"]}),
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "host": cpu_desc()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- ours --
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    from paper_1311_1006_b200 import _native as N
+    from paper_1311_1006_b200 import fmm as F
+    from paper_1311_1006_b200.sharding import PotentialGather, eval_slices, shard_cuts
+
+    threads = max(1, (os.cpu_count() or 1) // world)
+    wl = build_workload(args, threads)
+    n_eval = len(wl["yp"])
+    ctx = N.CudaContext(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    job, keep = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
+                                       wl["zp"], wl["mp"], wl["yp"], wl["sid"], None)
+    ctx.stage(job, keep)
+    prefix = ctx.work_prefix(wl["n_leaves"])
+    cuts = shard_cuts(prefix, world)
+    lb, le = int(cuts[rank]), int(cuts[rank + 1])
+    slices = eval_slices(wl["ev"], cuts)
+    full = torch.zeros(2 * n_eval, dtype=torch.float64, device=f"cuda:{local}")
+    torch.cuda.synchronize()
+    ctx.bind_device_out(full.data_ptr())
+    gather = PotentialGather(slices, rank, full) if world > 1 else None
+    fp64_peak = ctx.fp64_peak()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=full.device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return t.item()
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=full.device)
+        torch.distributed.all_reduce(t)
+        return t.item()
+
+    for _ in range(args.warmup):
+        ctx.run_staged(lb, le)
+        if gather:
+            gather()
+    torch.cuda.synchronize()
+    barrier()
+
+    K = args.steps
+    k0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    k1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches()
+    sampler = ClockSampler(local)
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    barrier()
+    t0.record()
+    for i in range(K):
+        k0[i].record()
+        ctx.run_staged(lb, le)
+        k1[i].record()
+        if gather:
+            gather()
+    t1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = ctx.launches() - launches0
+    ms_local = t0.elapsed_time(t1) / K
+    ms = allmax(ms_local)
+    kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(k0, k1))
+    my_pairs = ctx.pairs()
+    total_pairs = allsum(float(my_pairs))
+    value = total_pairs / (ms * 1e-3)
+    achieved = FLOPS_PER_PAIR * my_pairs / (kernel_ms * 1e-3) / 1e12
+
+    # parity of the gathered result on a few leaves (cheap; the tests do it fully)
+    # ---- e2e: reference-facing C ABI with host buffers (pack+H2D+kernel+D2H) ----
+    e2e = None
+    if not args.no_e2e:
+        ctx.bind_device_out(None)
+        host_out = np.zeros((n_eval, 2))
+        N.p2p(ctx, wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"], wl["zp"], wl["mp"], wl["yp"],
+              wl["sid"], leaf_begin=lb, leaf_end=le, out=host_out)  # warm (pinned buffers)
+        e2e_steps = max(1, min(K, 5))
+        barrier()
+        tt = []
+        for _ in range(e2e_steps):
+            barrier()
+            a = time.perf_counter()
+            _, pr, _ = N.p2p(ctx, wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"], wl["zp"],
+                             wl["mp"], wl["yp"], wl["sid"], leaf_begin=lb, leaf_end=le,
+                             out=host_out)
+            tt.append(time.perf_counter() - a)
+        h2d, d2h = ctx.transfer_bytes()
+        e2e_s = allmax(statistics.median(tt))
+        e2e = {"value": total_pairs / e2e_s, "unit": "pairs/s",
+               "h2d_bytes_per_step": int(allsum(float(h2d))),
+               "d2h_bytes_per_step": int(allsum(float(d2h))),
+               "ms_per_step": 1e3 * e2e_s,
+               "path": "fmmcu_p2p_launch + fmmcu_p2p_finish (include/fmm_cuda.h), host buffers"}
+
+    # ---- FMM evals/s through FmmEngine(cuda) (rank 0, single device) -------------
+    fmm = None
+    if not args.no_fmm and rank == 0:
+        s = F.make_distribution(args.dist, args.n, args.seed)
+        e = F.EvalSet.self_of(s)
+        eng = F.FmmEngine(F.FmmConfig(theta=args.theta, n_levels=args.levels, backend="cuda",
+                                      devices=(local,), m2l_on_device=True,
+                                      worker_threads=os.cpu_count()))
+        eng.evaluate(s, e)
+        r = eng.evaluate(s, e)
+        fmm = {"value": 1.0 / r.timings["t_total"], "unit": "evals/s",
+               "timings_s": {k: round(v, 4) for k, v in r.timings.items()},
+               "counters": r.counters, "p": r.p, "devices": 1,
+               "path": "FmmEngine::evaluate, backend=cuda, m2l_on_device (host tree+L2L+L2P)"}
+        del eng
+
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        cb = cpu_baseline(wl, args, steps=1)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "p2p_kernel_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("n_points") == args.n and tj.get("n_levels") == args.levels:
+                traffic = tj.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": "p2p_pairs_per_sec", "value": value, "unit": "pairs/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args, world, {"pairs_per_step": int(total_pairs)}),
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
+                         "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
+                         "peak_source": "measured DFMA micro-benchmark on this GPU in this run "
+                                        "(fmmcu_fp64_peak); nominal 148x64x2x1.965GHz = "
+                                        f"{NOMINAL_FP64_TFLOPS:.1f}",
+                         "frac_of_nominal": achieved / NOMINAL_FP64_TFLOPS,
+                         "kernel": "p2p_tile_kernel<harmonic,none>", "kernel_ms": kernel_ms,
+                         "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": int(my_pairs)},
+            "e2e": e2e,
+            "fmm_evals_per_sec": fmm,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": int(launches),
+            "host": cpu_desc(),
+            "setup_s": {"generate": round(wl["gen_s"], 3), "tree": round(wl["tree_s"], 3)},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

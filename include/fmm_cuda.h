@@ -122,6 +122,12 @@ int fmmcu_p2p_run_staged(fmmcu_ctx *ctx, uint32_t leaf_begin, uint32_t leaf_end,
                          int *launches);
 /* Device pointer to the staged potentials ([2 n_eval] doubles). */
 int fmmcu_p2p_device_out(fmmcu_ctx *ctx, double **dptr);
+/* Make subsequent runs write potentials into caller-owned device memory
+ * ([2 n_eval] doubles on this context's device, e.g. a torch tensor that is
+ * then all-gathered with NCCL); NULL restores the internal buffer. */
+int fmmcu_p2p_bind_device_out(fmmcu_ctx *ctx, double *dptr);
+/* Synchronous D2H of potentials [eval_begin, eval_end) of the last run. */
+int fmmcu_p2p_copy_out(fmmcu_ctx *ctx, double *host, uint32_t eval_begin, uint32_t eval_end);
 /* Pair count of the last run (exact; waits for it). */
 int fmmcu_p2p_pairs(fmmcu_ctx *ctx, uint64_t *pair_evals);
 /* Pair work of leaves [0, n) of the staged job, prefix-summed on the host
@@ -138,6 +144,9 @@ int fmmcu_m2l_finish(fmmcu_ctx *ctx, uint64_t *m2l_ops, double *seconds);
 /* ---- diagnostics --------------------------------------------------------- */
 /* Kernels launched by this context since creation (evidence counter). */
 uint64_t fmmcu_kernel_launches(const fmmcu_ctx *ctx);
+/* Host<->device bytes moved by the last fmmcu_p2p_launch (H2D: packed
+ * sources, evals, self map, CSR and work list; D2H: potentials + counter). */
+int fmmcu_last_transfer_bytes(const fmmcu_ctx *ctx, uint64_t *h2d, uint64_t *d2h);
 /* Measured FP64 FMA throughput of this device (TFLOP/s, DFMA = 2 flops). */
 int fmmcu_fp64_peak(fmmcu_ctx *ctx, double *tflops);
 

@@ -33,6 +33,8 @@ extern "C" {
 #endif
 
 const char *fmmh_last_error(void);
+/* Status of the last failing call on this thread (for handle-returning calls). */
+int fmmh_last_status(void);
 
 /* Synthetic inputs: 0 uniform (x,y,m_re ~ U(0,1)), 1 line band, 2 eight
  * Gaussian clusters, 3 random complex strengths U(-1,1)^2, 4 positive real

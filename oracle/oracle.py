@@ -97,6 +97,13 @@ def ref_lib():
         lib.fmmref_tree_nearfield.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int,
                                               C.c_int, C.c_int64, C.c_int64, _dp_n,
                                               C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        lib.fmmref_nf_create.argtypes = [C.c_uint32, _u32p, _u32p, _u32p, _u32p, _u32p,
+                                         C.c_uint32, C.c_uint32, _dp, _dp, _dp_n, _i64p_n]
+        lib.fmmref_nf_create.restype = C.c_void_p
+        lib.fmmref_nf_free.argtypes = [C.c_void_p]
+        lib.fmmref_nf_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                      C.c_int64, C.c_int64, _dp_n, C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_double)]
         lib.fmmref_evaluate.argtypes = [_dp, _dp, C.c_int64, _dp_n, _i64p_n, C.c_int64, _dp, _ip,
                                         _dp_n, _dp, _u64p, C.POINTER(C.c_int)]
         lib.fmmref_m2l_add.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _dp]
@@ -244,6 +251,39 @@ def ref_nearfield(tree: RefTree, kernel=0, smoother=0, delta=0.0, parallel=False
     if rc:
         raise RuntimeError(ref_lib().fmmref_last_error().decode())
     return (None if out is None else out[: 2 * ne].reshape(-1, 2)), int(pairs.value), secs.value
+
+
+class RefNearField:
+    """The reference's own nearfield_run over CSR leaves (ref_shim.cpp
+    fmmref_nf_*): the CPU baseline timed beside the device path."""
+
+    def __init__(self, csr: LeafCSR, zp, mp, yp, sidp):
+        self._keep = [np.ascontiguousarray(a) for a in (csr.pt_off, csr.ev_off, csr.s_off,
+                                                        csr.s_idx, csr.perm)]
+        zp = np.ascontiguousarray(zp, dtype=np.float64).reshape(-1)
+        mp = np.ascontiguousarray(mp, dtype=np.float64).reshape(-1)
+        yp = np.ascontiguousarray(yp, dtype=np.float64).reshape(-1)
+        sid = None if sidp is None else np.ascontiguousarray(sidp, dtype=np.int64)
+        self.n_eval = yp.size // 2
+        self.h = ref_lib().fmmref_nf_create(len(csr.pt_off) - 1, *self._keep, zp.size // 2,
+                                            self.n_eval, zp, mp, yp if yp.size else None, sid)
+
+    def run(self, leaf_begin, leaf_end, *, kernel=0, smoother=0, delta=0.0, parallel=True,
+            threads=1, want_out=False):
+        out = np.empty(max(self.n_eval, 1) * 2) if want_out else None
+        pairs = C.c_uint64()
+        secs = C.c_double()
+        rc = ref_lib().fmmref_nf_run(self.h, kernel, smoother, delta, int(parallel), threads,
+                                     leaf_begin, leaf_end, out, C.byref(pairs), C.byref(secs))
+        if rc:
+            raise RuntimeError(ref_lib().fmmref_last_error().decode())
+        return (None if out is None else out[: 2 * self.n_eval].reshape(-1, 2),
+                int(pairs.value), secs.value)
+
+    def close(self):
+        if self.h:
+            ref_lib().fmmref_nf_free(self.h)
+            self.h = None
 
 
 def ref_evaluate(z, m, y, sid, *, theta=0.5, tol=1e-6, n_levels=4, kernel=0, p_rule=1,

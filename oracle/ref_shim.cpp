@@ -242,6 +242,79 @@ int fmmref_tree_nearfield(void* h, int kernel, int smoother, double delta, int p
   }
 }
 
+// ------------------------------------------------- near field from CSR ----
+// The reference nearfield_run (backend.cpp:73-89) over a finest level given
+// as CSR arrays (the same arrays the product's C ABI takes), so bench.py can
+// time the reference's own loop on exactly the device workload without
+// rebuilding the reference tree.  The pyramid is a one-level shell holding
+// the leaf ranges; near_box() reads nothing else (backend.cpp:41-69).
+struct RefNF {
+  fmm::Pyramid pyr;
+  fmm::LevelConn conn;
+  std::vector<cplx> zp, mp, yp;
+  std::vector<int64_t> sidp;
+  std::vector<uint32_t> ev_begin;  // unmasked eval ranges
+  std::vector<uint32_t> ev_end;
+};
+
+void* fmmref_nf_create(uint32_t n_leaves, const uint32_t* pt_off, const uint32_t* ev_off,
+                       const uint32_t* s_off, const uint32_t* s_idx, const uint32_t* perm,
+                       uint32_t n_src, uint32_t n_eval, const double* zp, const double* mp,
+                       const double* yp, const int64_t* sidp) {
+  auto h = std::make_unique<RefNF>();
+  h->pyr.n_levels = 1;
+  h->pyr.levels.resize(1);
+  auto& fine = h->pyr.levels[0];
+  fine.resize(n_leaves);
+  h->ev_begin.resize(n_leaves);
+  h->ev_end.resize(n_leaves);
+  for (uint32_t i = 0; i < n_leaves; ++i) {
+    fine[i].point_begin = pt_off[i];
+    fine[i].point_end = pt_off[i + 1];
+    fine[i].eval_begin = h->ev_begin[i] = ev_off[i];
+    fine[i].eval_end = h->ev_end[i] = ev_off[i + 1];
+  }
+  h->pyr.perm.assign(perm, perm + n_src);
+  h->conn.strong.resize(n_leaves);
+  for (uint32_t i = 0; i < n_leaves; ++i) h->conn.strong[i].assign(s_idx + s_off[i], s_idx + s_off[i + 1]);
+  h->zp.resize(n_src);
+  h->mp.resize(n_src);
+  h->yp.resize(n_eval);
+  std::memcpy(h->zp.data(), zp, sizeof(double) * 2 * n_src);
+  std::memcpy(h->mp.data(), mp, sizeof(double) * 2 * n_src);
+  if (n_eval) std::memcpy(h->yp.data(), yp, sizeof(double) * 2 * n_eval);
+  if (sidp) h->sidp.assign(sidp, sidp + n_eval);
+  return h.release();
+}
+
+void fmmref_nf_free(void* h) { delete static_cast<RefNF*>(h); }
+
+int fmmref_nf_run(void* hv, int kernel, int smoother, double delta, int parallel, int threads,
+                  int64_t leaf_begin, int64_t leaf_end, double* out, uint64_t* pairs,
+                  double* seconds) {
+  try {
+    RefNF* h = static_cast<RefNF*>(hv);
+    auto& fine = h->pyr.levels[0];
+    const int64_t n = static_cast<int64_t>(fine.size());
+    for (int64_t i = 0; i < n; ++i) {
+      const bool in = i >= leaf_begin && i < leaf_end;
+      fine[i].eval_begin = h->ev_begin[i];
+      fine[i].eval_end = in ? h->ev_end[i] : h->ev_begin[i];
+    }
+    fmm::NearFieldJob job{&h->pyr, &h->conn, &h->zp, &h->mp, &h->yp, &h->sidp,
+                          kernel ? fmm::Kernel::logarithmic : fmm::Kernel::harmonic,
+                          make_smoother(smoother, delta), threads};
+    std::vector<cplx> near;
+    const fmm::NearFieldStats st = fmm::nearfield_run(job, near, parallel != 0);
+    if (out && !near.empty()) std::memcpy(out, near.data(), sizeof(double) * 2 * near.size());
+    *pairs = st.pair_evals;
+    *seconds = st.seconds;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // ------------------------------------------------------------- evaluate --
 // cfg_f: theta, tol, p_calibration, delta
 // cfg_i: n_levels, kernel, p_rule(0 formula,1 table), p_override, backend(0 serial,1 pool),

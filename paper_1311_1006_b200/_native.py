@@ -97,9 +97,9 @@ class M2LJob(C.Structure):
 CUDA_SYMBOLS = [
     "fmmcu_create", "fmmcu_destroy", "fmmcu_last_error", "fmmcu_device_count",
     "fmmcu_p2p_launch", "fmmcu_p2p_finish", "fmmcu_p2p_stage", "fmmcu_p2p_run_staged",
-    "fmmcu_p2p_device_out", "fmmcu_p2p_pairs", "fmmcu_p2p_work_prefix", "fmmcu_set_stream",
+    "fmmcu_p2p_device_out", "fmmcu_p2p_bind_device_out", "fmmcu_p2p_copy_out", "fmmcu_p2p_pairs", "fmmcu_p2p_work_prefix", "fmmcu_set_stream",
     "fmmcu_synchronize", "fmmcu_m2l_launch", "fmmcu_m2l_finish", "fmmcu_kernel_launches",
-    "fmmcu_fp64_peak",
+    "fmmcu_fp64_peak", "fmmcu_last_transfer_bytes",
 ]
 
 
@@ -122,6 +122,8 @@ def cuda_lib():
         lib.fmmcu_p2p_run_staged.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_int,
                                              C.POINTER(C.c_int)]
         lib.fmmcu_p2p_device_out.argtypes = [vp, C.POINTER(C.c_void_p)]
+        lib.fmmcu_p2p_bind_device_out.argtypes = [vp, vp]
+        lib.fmmcu_p2p_copy_out.argtypes = [vp, vp, C.c_uint32, C.c_uint32]
         lib.fmmcu_p2p_pairs.argtypes = [vp, C.POINTER(C.c_uint64)]
         lib.fmmcu_p2p_work_prefix.argtypes = [vp, vp]
         lib.fmmcu_set_stream.argtypes = [vp, vp]
@@ -131,6 +133,7 @@ def cuda_lib():
         lib.fmmcu_kernel_launches.argtypes = [vp]
         lib.fmmcu_kernel_launches.restype = C.c_uint64
         lib.fmmcu_fp64_peak.argtypes = [vp, C.POINTER(C.c_double)]
+        lib.fmmcu_last_transfer_bytes.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         _cuda = lib
     return _cuda
 
@@ -241,6 +244,16 @@ class CudaContext:
         self._check(self.lib.fmmcu_p2p_device_out(self.h, C.byref(p)))
         return p.value
 
+    def bind_device_out(self, dptr: int | None):
+        """Write potentials into caller-owned device memory (e.g. a torch tensor)."""
+        self._check(self.lib.fmmcu_p2p_bind_device_out(self.h, C.c_void_p(dptr or 0)))
+
+    def copy_out(self, n_eval: int, eval_begin: int = 0, eval_end: int | None = None):
+        out = np.zeros((n_eval, 2))
+        e1 = n_eval if eval_end is None else eval_end
+        self._check(self.lib.fmmcu_p2p_copy_out(self.h, _ptr(out), eval_begin, e1))
+        return out
+
     def pairs(self) -> int:
         v = C.c_uint64()
         self._check(self.lib.fmmcu_p2p_pairs(self.h, C.byref(v)))
@@ -259,6 +272,11 @@ class CudaContext:
 
     def launches(self) -> int:
         return int(self.lib.fmmcu_kernel_launches(self.h))
+
+    def transfer_bytes(self):
+        h2d, d2h = C.c_uint64(), C.c_uint64()
+        self._check(self.lib.fmmcu_last_transfer_bytes(self.h, C.byref(h2d), C.byref(d2h)))
+        return int(h2d.value), int(d2h.value)
 
     def fp64_peak(self) -> float:
         v = C.c_double()

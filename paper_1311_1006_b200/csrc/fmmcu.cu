@@ -112,6 +112,8 @@ struct fmmcu_ctx {
   std::vector<P2PFinal> fins;
   std::vector<uint32_t> fin_first;     // [n_leaves + 1]
   bool staged = false;
+  double2* ext_out = nullptr;  // caller-bound output (torch tensor), or null
+  double2* out_ptr() const { return ext_out ? ext_out : d_out.as<double2>(); }
 
   // in-flight reference-facing launch
   bool inflight = false;
@@ -119,6 +121,7 @@ struct fmmcu_ctx {
   uint32_t run_lb = 0, run_le = 0;
   double prep_seconds = 0.0;
   uint64_t run_total_pairs = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
 
   // m2l
   DevBuf m_centers, m_coeffs, m_tbox, m_woff, m_widx, m_table, m_out, m_flag;
@@ -156,7 +159,7 @@ P2PArgs make_args(fmmcu_ctx* c) {
   a.s_off = c->d_soff.as<uint32_t>();
   a.s_idx = c->d_sidx.as<uint32_t>();
   a.items = c->d_items.as<P2PItem>();
-  a.out = c->d_out.as<double2>();
+  a.out = c->out_ptr();
   a.partial = c->d_partial.as<double2>();
   a.hits = c->d_hits.as<unsigned long long>();
   a.delta = c->delta;
@@ -375,6 +378,7 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const size_t o_si = put(j->strong_idx, size_t(nnz) * 4);
   const size_t o_it = put(c->items.data(), c->items.size() * sizeof(P2PItem));
   const size_t o_fi = put(c->fins.data(), c->fins.size() * sizeof(P2PFinal));
+  c->h2d_bytes = uint64_t(ns) * 32 + uint64_t(ne) * 20 + o;
 
   cudaStream_t s = c->stream;
   CU_TRY(c, cudaEventRecord(c->ev_start, s));
@@ -424,7 +428,7 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch) 
         p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(c->d_fin.as<P2PFinal>() + f0, f1 - f0,
                                                      c->d_ev.as<uint32_t>(),
                                                      c->d_partial.as<double2>(),
-                                                     c->d_out.as<double2>());
+                                                     c->out_ptr());
         ++n;
       }
     }
@@ -528,6 +532,13 @@ const char* fmmcu_last_error(const fmmcu_ctx* c) { return c ? c->err.c_str() : "
 
 uint64_t fmmcu_kernel_launches(const fmmcu_ctx* c) { return c ? c->launches : 0; }
 
+int fmmcu_last_transfer_bytes(const fmmcu_ctx* c, uint64_t* h2d, uint64_t* d2h) {
+  if (!c) return FMMCU_EINVAL;
+  if (h2d) *h2d = c->h2d_bytes;
+  if (d2h) *d2h = c->d2h_bytes;
+  return FMMCU_OK;
+}
+
 int fmmcu_set_stream(fmmcu_ctx* c, void* stream) {
   if (!c) return FMMCU_EINVAL;
   c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
@@ -552,11 +563,12 @@ int fmmcu_p2p_launch(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const uint32_t eb = c->ev_off[j->leaf_begin], ee = c->ev_off[j->leaf_end];
   CU_TRY(c, c->h_out.ensure(size_t(c->n_eval) * 16 + 16));
   if (ee > eb)
-    CU_TRY(c, cudaMemcpyAsync(c->h_out.as<double2>() + eb, c->d_out.as<double2>() + eb,
+    CU_TRY(c, cudaMemcpyAsync(c->h_out.as<double2>() + eb, c->out_ptr() + eb,
                               size_t(ee - eb) * 16, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaEventRecord(c->ev_end, c->stream));
   c->job = *j;
+  c->d2h_bytes = uint64_t(ee - eb) * 16 + 8;
   c->run_lb = j->leaf_begin;
   c->run_le = j->leaf_end;
   c->run_total_pairs = c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
@@ -605,7 +617,25 @@ int fmmcu_p2p_run_staged(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* 
 int fmmcu_p2p_device_out(fmmcu_ctx* c, double** dptr) {
   if (!c || !dptr) return FMMCU_EINVAL;
   if (!c->staged) return set_err(c, FMMCU_ESTATE, "no staged job");
-  *dptr = c->d_out.as<double>();
+  *dptr = reinterpret_cast<double*>(c->out_ptr());
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_bind_device_out(fmmcu_ctx* c, double* dptr) {
+  if (!c) return FMMCU_EINVAL;
+  c->ext_out = reinterpret_cast<double2*>(dptr);
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_copy_out(fmmcu_ctx* c, double* host, uint32_t eb, uint32_t ee) {
+  if (!c || (!host && ee > eb)) return FMMCU_EINVAL;
+  if (!c->staged) return set_err(c, FMMCU_ESTATE, "no staged job");
+  if (eb > ee || ee > c->n_eval) return set_err(c, FMMCU_EINVAL, "bad eval range");
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (ee > eb)
+    CU_TRY(c, cudaMemcpyAsync(host + 2 * size_t(eb), c->out_ptr() + eb, size_t(ee - eb) * 16,
+                              cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
   return FMMCU_OK;
 }
 

@@ -16,8 +16,9 @@ using namespace fmm;
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_code = 0;
 
-int code_of(const std::exception& e) {
+int code_of_impl(const std::exception& e) {
   g_err = e.what();
   if (dynamic_cast<const InvalidParameter*>(&e)) return 1;
   if (dynamic_cast<const InvalidInput*>(&e)) return 2;
@@ -26,6 +27,8 @@ int code_of(const std::exception& e) {
   if (dynamic_cast<const InvalidState*>(&e) || dynamic_cast<const NoMeasurement*>(&e)) return 5;
   return 9;
 }
+
+int code_of(const std::exception& e) { return g_code = code_of_impl(e); }
 
 template <class F>
 int guarded(F&& f) {
@@ -36,7 +39,7 @@ int guarded(F&& f) {
     return code_of(e);
   } catch (...) {
     g_err = "unknown exception";
-    return 9;
+    return g_code = 9;
   }
 }
 
@@ -124,6 +127,7 @@ void write_timings(const EvalResult& r, double* timings, uint64_t* counters) {
 extern "C" {
 
 const char* fmmh_last_error(void) { return g_err.c_str(); }
+int fmmh_last_status(void) { return g_code; }
 
 void fmmh_make_distribution(int kind, int64_t n, uint64_t seed, double* z, double* m) {
   std::mt19937_64 rng(seed);

@@ -76,6 +76,7 @@ def host_lib():
         lib = C.CDLL(_native.HOST_LIB)
         vp = C.c_void_p
         lib.fmmh_last_error.restype = C.c_char_p
+        lib.fmmh_last_status.restype = C.c_int
         lib.fmmh_make_distribution.argtypes = [C.c_int, C.c_int64, C.c_uint64, vp, vp]
         lib.fmmh_make_distribution.restype = None
         lib.fmmh_tree_build.argtypes = [vp, vp, C.c_int64, vp, vp, C.c_int64, C.c_int, C.c_double,
@@ -188,10 +189,7 @@ class Tree:
         h = lib.fmmh_tree_build(_p(sources.z), _p(sources.m), sources.size(), _p(y),
                                 _p(evals.source_id) if ne else None, ne, n_levels, theta, threads)
         if not h:
-            msg = lib.fmmh_last_error().decode()
-            if "n_levels" in msg or "theta" in msg:
-                raise InvalidParameter(msg)
-            raise InvalidInput(msg)
+            _raise(lib.fmmh_last_status())
         self.h = h
         self.n_levels = n_levels
         self.perm = np.empty(sources.size(), dtype=np.uint32)
@@ -303,10 +301,7 @@ class FmmEngine:
         f, i, d = cfg.pack()
         h = host_lib().fmmh_engine_create(_p(f), _p(i), _p(d), len(d))
         if not h:
-            msg = host_lib().fmmh_last_error().decode()
-            if msg.startswith("backend error"):
-                raise BackendError(msg)
-            raise InvalidParameter(msg)
+            _raise(host_lib().fmmh_last_status())
         self.h = h
 
     def __del__(self):

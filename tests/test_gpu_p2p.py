@@ -1,0 +1,215 @@
+"""Device P2P parity (needs a B200).  Everything goes through the C ABI
+(include/fmm_cuda.h) via paper_1311_1006_b200._native.
+
+Bars:
+  * pair_evals exactly equal to the reference counter;
+  * exact mode (restated __divdc3, reference order): bitwise equal for the
+    harmonic kernel without smoother;
+  * fast FP64 mode: max|phi_gpu - phi_ref| <= 1e-12 * max|phi_ref|
+    (normwise, test_util.hpp:47-57 convention) for every kernel/smoother.
+"""
+import numpy as np
+import pytest
+
+from conftest import bitwise, golden_leaf_csr, golden_permuted, normwise
+from oracle import oracle as O
+from paper_1311_1006_b200 import _native as N
+from paper_1311_1006_b200 import fmm as F
+
+pytestmark = pytest.mark.gpu
+TOL_FP64 = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = N.CudaContext(0)
+    yield c
+    c.close()
+
+
+def _run(ctx, pt, ev, so, si, perm, zp, mp, yp, sid, **kw):
+    return N.p2p(ctx, pt, ev, so, si, perm, zp, mp, yp, sid, **kw)
+
+
+@pytest.mark.parametrize("variant", [(0, 0), (1, 0), (0, 1), (0, 2)])
+def test_golden_trees_fast_and_exact(ctx, golden_trees, variant):
+    k, s = variant
+    for name, d in golden_trees.items():
+        pt, ev, so, si = golden_leaf_csr(d)
+        zp, mp, yp, sid = golden_permuted(d)
+        want = d[f"near_k{k}_s{s}"]
+        delta = float(d[f"delta_k{k}_s{s}"])
+        for mode in (0, 1):
+            out, pairs, _ = _run(ctx, pt, ev, so, si, d["perm"], zp, mp, yp, sid, kernel=k,
+                                 smoother=s, delta=delta, mode=mode)
+            assert pairs == int(d[f"pairs_k{k}_s{s}"]), (name, mode)
+            assert normwise(out, want) <= TOL_FP64, (name, mode, normwise(out, want))
+            if mode == 1 and k == 0 and s == 0:
+                assert bitwise(out, want), name
+
+
+def _tree_case(kind, n, L, seed, self_eval=True, n_eval=None, theta=0.5):
+    s = F.make_distribution(kind, n, seed)
+    if self_eval:
+        e = F.EvalSet.self_of(s)
+    else:
+        e = F.EvalSet(F.make_distribution("random", n_eval, seed + 1).z * 1.1 - 0.05)
+    t = F.Tree(s, e, L, theta, threads=8)
+    zp, mp, yp, sid = t.permuted()
+    pt, ev, so, si = t.leaf_csr()
+    return t, (pt, ev, so, si, t.perm, zp, mp, yp, sid)
+
+
+@pytest.mark.parametrize("case", [(0, 100_000, 6, 1), (0, 100_000, 7, 1), (2, 200_000, 7, 3),
+                                  (1, 50_000, 6, 4), (3, 30_000, 5, 5)])
+def test_random_trees_vs_oracle(ctx, case):
+    kind, n, L, seed = case
+    t, args = _tree_case(kind, n, L, seed)
+    csr = O.LeafCSR(args[0], args[1], args[2], args[3], args[4])
+    want, wpairs = O.nearfield(csr, *args[5:9])
+    for mode in (0, 1):
+        out, pairs, _ = _run(ctx, *args, mode=mode)
+        assert pairs == wpairs
+        if mode == 1:
+            assert bitwise(out, want)
+        else:
+            assert normwise(out, want) <= TOL_FP64
+
+
+def test_separate_eval_points_no_ids(ctx):
+    t, args = _tree_case(0, 40_000, 6, 9, self_eval=False, n_eval=25_000)
+    csr = O.LeafCSR(*args[:5])
+    want, wpairs = O.nearfield(csr, *args[5:9])
+    out, pairs, _ = _run(ctx, *args)
+    assert pairs == wpairs
+    assert normwise(out, want) <= TOL_FP64
+    out, pairs, _ = _run(ctx, *args, mode=1)
+    assert bitwise(out, want)
+
+
+def test_lattice_layout_perm_differs_from_eval_perm(ctx):
+    g = np.arange(120) * (1.0 / 120)
+    z = (g[:, None] + 1j * g[None, :] * 0.25).ravel()
+    s = F.SourceSet(z, np.full(len(z), 0.5j))
+    e = F.EvalSet.self_of(s)
+    t = F.Tree(s, e, 6, 0.5)
+    assert not np.array_equal(t.perm, t.eval_perm)
+    zp, mp, yp, sid = t.permuted()
+    pt, ev, so, si = t.leaf_csr()
+    want, wpairs = O.nearfield(O.LeafCSR(pt, ev, so, si, t.perm), zp, mp, yp, sid, smoother=1,
+                               delta=0.01)
+    out, pairs, _ = _run(ctx, pt, ev, so, si, t.perm, zp, mp, yp, sid, smoother=1, delta=0.01)
+    assert pairs == wpairs
+    assert normwise(out, want) <= TOL_FP64
+
+
+def test_single_box_equals_direct_sum(ctx):
+    t, args = _tree_case(3, 3000, 1, 10)
+    want, wpairs = O.nearfield(O.LeafCSR(*args[:5]), *args[5:9])
+    out, pairs, _ = _run(ctx, *args)
+    assert pairs == 3000 * 2999 == wpairs
+    assert normwise(out, want) <= TOL_FP64
+
+
+def test_empty_eval_set_and_empty_leaves(ctx):
+    s = F.make_distribution("random", 500, 3)
+    t = F.Tree(s, F.EvalSet(np.zeros(0, complex)), 3, 0.5)
+    zp, mp, yp, sid = t.permuted()
+    pt, ev, so, si = t.leaf_csr()
+    out, pairs, _ = _run(ctx, pt, ev, so, si, t.perm, zp, mp, yp, None)
+    assert pairs == 0 and out.size == 0
+    # evals concentrated in a corner: most leaves have no evals
+    e = F.EvalSet(0.01 * F.make_distribution("random", 50, 4).z)
+    t = F.Tree(s, e, 4, 0.5)
+    zp, mp, yp, sid = t.permuted()
+    pt, ev, so, si = t.leaf_csr()
+    assert (np.diff(ev.astype(np.int64)) == 0).sum() > 0
+    want, wp = O.nearfield(O.LeafCSR(pt, ev, so, si, t.perm), zp, mp, yp, None)
+    out, pairs, _ = _run(ctx, pt, ev, so, si, t.perm, zp, mp, yp, None)
+    assert pairs == wp and normwise(out, want) <= TOL_FP64
+
+
+def test_heavy_leaves_are_split_and_reduced(ctx):
+    """Clustered input with a deep tree: strong lists of thousands of leaves
+     exercise the chunked work list and its fixed-order reduction."""
+    t, args = _tree_case(2, 300_000, 8, 3)
+    so = args[2]
+    assert np.diff(so.astype(np.int64)).max() > 1000
+    want, wpairs = O.nearfield(O.LeafCSR(*args[:5]), *args[5:9])
+    out, pairs, _ = _run(ctx, *args)
+    assert pairs == wpairs
+    assert normwise(out, want) <= TOL_FP64
+    out2, _, _ = _run(ctx, *args)
+    assert bitwise(out, out2)  # deterministic
+
+
+def test_leaf_shards_compose_to_the_full_result(ctx):
+    t, args = _tree_case(0, 120_000, 7, 12)
+    full, pairs_full, _ = _run(ctx, *args)
+    nl = len(args[0]) - 1
+    cuts = [0, nl // 3, nl // 2, nl]
+    acc = np.zeros_like(full)
+    tot = 0
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        out, pairs, _ = _run(ctx, *args, leaf_begin=a, leaf_end=b)
+        e0, e1 = int(args[1][a]), int(args[1][b])
+        acc[e0:e1] = out[e0:e1]
+        tot += pairs
+    assert tot == pairs_full
+    assert bitwise(acc, full)
+
+
+def test_staged_device_path_matches_launch(ctx):
+    t, args = _tree_case(0, 200_000, 7, 2)
+    full, pairs_full, _ = _run(ctx, *args)
+    job, keep = N.CudaContext.make_job(*args, None)
+    ctx.stage(job, keep)
+    nl = len(args[0]) - 1
+    n = ctx.run_staged(0, nl)
+    assert n >= 1
+    assert ctx.pairs() == pairs_full
+    assert bitwise(ctx.copy_out(len(full)), full)
+    # potentials written straight into a torch-owned device tensor
+    import torch
+    buf = torch.zeros(full.size, dtype=torch.float64, device="cuda:0")
+    torch.cuda.synchronize()
+    ctx.bind_device_out(buf.data_ptr())
+    ctx.run_staged(0, nl)
+    ctx.synchronize()
+    ctx.bind_device_out(None)
+    assert bitwise(buf.cpu().numpy().reshape(full.shape), full)
+
+
+def test_linearity_at_scale(ctx):
+    """Size-independent property at 2M: doubling every strength doubles every
+    potential exactly (2x is exact in binary FP), fast mode."""
+    t, args = _tree_case(0, 2_000_000, 9, 4)
+    out1, p1, _ = _run(ctx, *args)
+    args2 = list(args)
+    args2[6] = args[6] * 2.0
+    out2, p2, _ = _run(ctx, *args2)
+    assert p1 == p2
+    assert bitwise(out2, 2.0 * out1)
+    # spot-check 200 target leaves against the oracle
+    nl = len(args[0]) - 1
+    rng = np.random.default_rng(0)
+    csr = O.LeafCSR(*args[:5])
+    for lb in rng.choice(nl, 20, replace=False):
+        w, _ = O.nearfield(csr, *args[5:9], leaf_begin=int(lb), leaf_end=int(lb) + 1)
+        e0, e1 = int(args[1][lb]), int(args[1][lb + 1])
+        assert normwise(out1[e0:e1], w[e0:e1]) <= TOL_FP64
+
+
+def test_invalid_jobs_fail_loudly(ctx):
+    t, args = _tree_case(0, 1000, 3, 1)
+    with pytest.raises(N.FmmcuError):
+        _run(ctx, *args, kernel=7)
+    with pytest.raises(N.FmmcuError):
+        _run(ctx, *args, smoother=1, delta=0.0)
+    bad = list(args)
+    bad[3] = args[3].copy()
+    bad[3][0] = 10**6
+    with pytest.raises(N.FmmcuError):
+        _run(ctx, *bad)
+    with pytest.raises(N.FmmcuError):
+        ctx.finish()

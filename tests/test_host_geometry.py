@@ -1,0 +1,181 @@
+"""Host pyramid + connectivity: bit-exact against the reference, plus the
+reference's own geometry properties (proj/tests/test_geometry.cpp)."""
+import numpy as np
+import pytest
+
+from conftest import bitwise
+from oracle import oracle as O
+from paper_1311_1006_b200 import fmm as F
+
+
+def _tree_from_golden(d):
+    s = F.SourceSet(d["z"][:, 0] + 1j * d["z"][:, 1], d["m"][:, 0] + 1j * d["m"][:, 1])
+    y = d["y"][:, 0] + 1j * d["y"][:, 1]
+    e = F.EvalSet(y, d["sid"] if "sid" in d else None)
+    return F.Tree(s, e, int(d["n_levels"]), float(d["theta"]), threads=4)
+
+
+def test_tree_bitwise_vs_golden(golden_trees):
+    for name, d in golden_trees.items():
+        t = _tree_from_golden(d)
+        assert np.array_equal(t.perm, d["perm"]), name
+        assert np.array_equal(t.eval_perm, d["eval_perm"]), name
+        for lvl in range(t.n_levels):
+            assert bitwise(t.boxes_f[lvl], d[f"boxes_f_{lvl}"]), (name, lvl)
+            assert np.array_equal(t.boxes_u[lvl], d[f"boxes_u_{lvl}"]), (name, lvl)
+            assert np.array_equal(t.strong[lvl][0], d[f"strong_off_{lvl}"]), (name, lvl)
+            assert np.array_equal(t.strong[lvl][1], d[f"strong_idx_{lvl}"]), (name, lvl)
+            assert np.array_equal(t.weak[lvl][0], d[f"weak_off_{lvl}"]), (name, lvl)
+            assert np.array_equal(t.weak[lvl][1], d[f"weak_idx_{lvl}"]), (name, lvl)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
+@pytest.mark.parametrize("case", [(0, 50_000, 7, 1, None), (2, 30_000, 7, 3, None),
+                                  (1, 20_000, 6, 2, None), (0, 8000, 5, 9, 5000),
+                                  (3, 777, 4, 1, None)])
+def test_tree_bitwise_vs_live_reference(case):
+    kind, n, L, seed, ne = case
+    s = F.make_distribution(kind, n, seed)
+    if ne is None:
+        e = F.EvalSet.self_of(s)
+    else:
+        e = F.EvalSet(F.make_distribution(3, ne, seed + 7).z * 1.2 - 0.1)
+    t = F.Tree(s, e, L, 0.5, threads=8)
+    r = O.ref_tree(F._c2(s.z), F._c2(s.m), F._c2(e.y), e.source_id, L, 0.5, threads=8)
+    assert np.array_equal(t.perm, r.perm) and np.array_equal(t.eval_perm, r.eval_perm)
+    for lvl in range(L):
+        assert bitwise(t.boxes_f[lvl], r.boxes_f[lvl])
+        assert np.array_equal(t.boxes_u[lvl], r.boxes_u[lvl])
+        for a, b in ((t.strong[lvl], r.strong[lvl]), (t.weak[lvl], r.weak[lvl])):
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
+def test_tree_lattice_with_duplicates_vs_live_reference():
+    """Lattices put many points on split lines (perm != eval_perm)."""
+    g = np.arange(30) * 0.05
+    zz = (g[:, None] + 1j * g[None, :]).ravel()
+    z = np.concatenate([zz, zz[:77]])
+    s = F.SourceSet(z, np.ones(len(z)))
+    e = F.EvalSet.self_of(s)
+    t = F.Tree(s, e, 5, 0.5)
+    r = O.ref_tree(F._c2(s.z), F._c2(s.m), F._c2(e.y), e.source_id, 5, 0.5)
+    assert np.array_equal(t.perm, r.perm) and np.array_equal(t.eval_perm, r.eval_perm)
+    assert not np.array_equal(t.perm, t.eval_perm)
+    for lvl in range(5):
+        assert bitwise(t.boxes_f[lvl], r.boxes_f[lvl])
+
+
+def test_four_symmetric_sources_one_per_quadrant():
+    z = np.array([-1 - 1j, -1 + 1j, 1 - 1j, 1 + 1j])
+    t = F.Tree(F.SourceSet(z, np.ones(4)), F.EvalSet(np.zeros(0, complex)), 2, 0.5)
+    u = t.boxes_u[1]
+    assert np.all(u[:, 1] - u[:, 0] == 1)
+
+
+def test_collinear_sources_adapt_to_the_line():
+    z = np.arange(16) * 0.25 + 0j
+    t = F.Tree(F.SourceSet(z, np.ones(16)), F.EvalSet(np.zeros(0, complex)), 2, 0.5)
+    u = t.boxes_u[1]
+    assert np.all(u[:, 1] - u[:, 0] == 4)
+
+
+def test_balance_on_skewed_distributions():
+    for n, seed in ((777, 1), (1024, 2), (333, 3)):
+        s = F.make_distribution("random", n, seed)
+        z = s.z.copy()
+        z[: n // 2] = (0.001 + 0.001j) + 1e-4 * z[: n // 2]
+        t = F.Tree(F.SourceSet(z, s.m), F.EvalSet(np.zeros(0, complex)), 4, 0.5)
+        cnt = np.diff(t.leaf_csr()[0].astype(np.int64))
+        assert cnt.max() - cnt.min() <= 4
+
+
+def test_permutation_bijection_and_nesting():
+    s = F.make_distribution("random", 500, 7)
+    e = F.EvalSet(F.make_distribution("random", 300, 8).z)
+    t = F.Tree(s, e, 4, 0.5)
+    assert np.array_equal(np.sort(t.perm), np.arange(500))
+    assert np.array_equal(np.sort(t.eval_perm), np.arange(300))
+    for lvl in range(3):
+        pu, cu = t.boxes_u[lvl], t.boxes_u[lvl + 1]
+        for i in range(len(pu)):
+            kids = cu[4 * i: 4 * i + 4]
+            assert kids[0, 0] == pu[i, 0] and kids[-1, 1] == pu[i, 1]
+            assert kids[0, 2] == pu[i, 2] and kids[-1, 3] == pu[i, 3]
+            assert np.all(kids[1:, 0] == kids[:-1, 1]) and np.all(kids[1:, 2] == kids[:-1, 3])
+
+
+def test_boxes_contain_points_and_radius_identity():
+    s = F.make_distribution("random", 400, 11)
+    e = F.EvalSet(F.make_distribution("random", 100, 12).z * 2.0)
+    t = F.Tree(s, e, 3, 0.5)
+    for lvl in range(3):
+        f, u = t.boxes_f[lvl], t.boxes_u[lvl]
+        assert np.allclose(f[:, 4], np.hypot(f[:, 2], f[:, 3]), rtol=1e-12, atol=0)
+        for i in range(len(f)):
+            zz = s.z[t.perm[u[i, 0]:u[i, 1]]]
+            assert np.all(np.abs(zz.real - f[i, 0]) <= f[i, 2] + 1e-12)
+            assert np.all(np.abs(zz.imag - f[i, 1]) <= f[i, 3] + 1e-12)
+
+
+def test_connectivity_symmetric_self_strong_disjoint():
+    s = F.make_distribution("random", 600, 21)
+    for theta in (0.35, 0.5, 0.65):
+        t = F.Tree(s, F.EvalSet(np.zeros(0, complex)), 4, theta)
+        for lvl in range(4):
+            so, si = t.strong[lvl]
+            wo, wi = t.weak[lvl]
+            n = len(so) - 1
+            S = [set(si[so[i]:so[i + 1]].tolist()) for i in range(n)]
+            W = [set(wi[wo[i]:wo[i + 1]].tolist()) for i in range(n)]
+            for i in range(n):
+                assert i in S[i]
+                assert not (S[i] & W[i])
+                for j in S[i]:
+                    assert i in S[j]
+                for j in W[i]:
+                    assert i in W[j]
+
+
+def test_pair_coverage_every_pair_exactly_once():
+    for n in (17, 64, 160):
+        s = F.make_distribution("random", n, 100 + n)
+        for L in (2, 3, 4):
+            t = F.Tree(s, F.EvalSet.self_of(s), L, 0.5)
+            box = np.empty((L, n), dtype=np.int64)
+            for lvl in range(L):
+                u = t.boxes_u[lvl]
+                for b in range(len(u)):
+                    box[lvl, t.perm[u[b, 0]:u[b, 1]]] = b
+            for lvl_lists in [t.strong[-1]]:
+                pass
+            strong = [set(t.strong[-1][1][t.strong[-1][0][b]:t.strong[-1][0][b + 1]].tolist())
+                      for b in range(len(t.boxes_u[-1]))]
+            weak = [[set(t.weak[lvl][1][t.weak[lvl][0][b]:t.weak[lvl][0][b + 1]].tolist())
+                     for b in range(len(t.boxes_u[lvl]))] for lvl in range(L)]
+            for i in range(n):
+                for j in range(n):
+                    if i == j:
+                        continue
+                    h = int(box[L - 1, j] in strong[box[L - 1, i]])
+                    h += sum(int(box[lvl, j] in weak[lvl][box[lvl, i]]) for lvl in range(L))
+                    assert h == 1
+
+
+def test_empty_boxes_keep_zero_ranges():
+    z = np.array([0.0, 0.1 + 0.1j])
+    t = F.Tree(F.SourceSet(z, np.ones(2)), F.EvalSet(np.zeros(0, complex)), 3, 0.5)
+    u, f = t.boxes_u[2], t.boxes_f[2]
+    empty = (u[:, 1] - u[:, 0]) == 0
+    assert empty.sum() == 14 and np.all(f[empty, 4] == 0.0)
+
+
+def test_errors():
+    s = F.SourceSet(np.array([0j]), np.ones(1))
+    with pytest.raises(F.InvalidParameter):
+        F.Tree(s, F.EvalSet(np.zeros(0, complex)), 0, 0.5)
+    with pytest.raises(F.InvalidInput):
+        F.Tree(F.SourceSet(np.zeros(0, complex), np.zeros(0)), F.EvalSet(np.zeros(0, complex)), 2, 0.5)
+    with pytest.raises(F.InvalidInput):
+        F.Tree(F.SourceSet(np.array([np.nan + 0j]), np.ones(1)), F.EvalSet(np.zeros(0, complex)), 2,
+               0.5)
