@@ -233,7 +233,11 @@ def run_ours(args):
     wl = build_workload(args, threads)
     n_eval = len(wl["yp"])
     ctx = N.CudaContext(local)
-    stream = torch.cuda.current_stream()
+    # One explicit stream shared by our kernels, the torch events that time
+    # them and the NCCL gather (the legacy default stream has handle 0, which
+    # the C ABI reads as "use the context's own stream").
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     job, keep = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
                                        wl["zp"], wl["mp"], wl["yp"], wl["sid"], None)

@@ -69,9 +69,12 @@ def tree_fixture(name, kind, n, seed, L, theta, n_eval):
 def m2l_fixture():
     rng = np.random.default_rng(1311)
     rows = []
+    # the small scale sends m2l_add down its long double branch
+    # ((p+2) log10|w| >= 250) while the local coefficients stay finite
+    small = {8: 1e-30, 17: 1e-15, 19: 1e-15, 30: 3e-9}
     for p in (8, 17, 19, 30):
         for kernel in (0, 1):
-            for scale in (1.0, 1e-15):  # 1e-15 exercises the long double branch
+            for scale in (1.0, small[p]):
                 sc = rng.uniform(-1, 1, 2) * scale
                 tc = rng.uniform(-1, 1, 2) * scale + np.array([3.0, 0.5]) * scale
                 coeffs = rng.uniform(-1, 1, (p + 1, 2)) * (0.4 * scale) ** np.arange(p + 1)[:, None]
