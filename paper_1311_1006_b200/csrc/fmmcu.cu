@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -29,10 +30,23 @@ using namespace fmmcu;
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kE = 2;
-constexpr int kTile = 1024;
-constexpr size_t kTileSmem = 128 + size_t(kTile) * 32;
+// Fast-kernel shape variants (threads per CTA x evals per thread); the
+// default is chosen from measurements (profiles/), FMMCU_P2P_VARIANT
+// overrides it for experiments: 0 = 256x2, 1 = 128x2, 2 = 128x4, 3 = 256x4.
+constexpr int kTile = 512;  // source records per shared tile (x2, double-buffered)
+constexpr int kMaxEvalsPerItem = 256;
+int variant_index() {
+  static int v = [] {
+    const char* s = std::getenv("FMMCU_P2P_VARIANT");
+    int i = s ? std::atoi(s) : 0;
+    return (i >= 0 && i < 4) ? i : 0;
+  }();
+  return v;
+}
+
+constexpr size_t tile_smem(int threads, int e) {
+  return 128 + size_t(2 * kTile) * 32 + size_t(threads) * e * 16;
+}
 
 struct DevBuf {
   void* p = nullptr;
@@ -97,7 +111,7 @@ struct fmmcu_ctx {
 
   // staged job (device)
   DevBuf d_src, d_evy, d_eself, d_pt, d_ev, d_soff, d_sidx, d_items, d_fin, d_out, d_partial,
-      d_hits;
+      d_hits, d_seg, d_counter;
   // pinned staging
   HostBuf h_src, h_evy, h_eself, h_out, h_hits, h_csr;
   std::vector<uint32_t> invperm;
@@ -159,6 +173,8 @@ P2PArgs make_args(fmmcu_ctx* c) {
   a.s_off = c->d_soff.as<uint32_t>();
   a.s_idx = c->d_sidx.as<uint32_t>();
   a.items = c->d_items.as<P2PItem>();
+  a.seg = c->d_seg.as<uint2>();
+  a.next_item = c->d_counter.as<unsigned int>();
   a.out = c->out_ptr();
   a.partial = c->d_partial.as<double2>();
   a.hits = c->d_hits.as<unsigned long long>();
@@ -168,11 +184,31 @@ P2PArgs make_args(fmmcu_ctx* c) {
   return a;
 }
 
+template <int KN, int SM, int T, int E>
+void launch_tile_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
+  auto kfn = p2p_tile_kernel<KN, SM, E, T, kTile>;
+  constexpr size_t smem = tile_smem(T, E);
+  static int grid_cap = [&] {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, T, smem);
+    return std::max(1, sms * std::max(1, per_sm));
+  }();
+  const uint32_t grid = std::min<uint32_t>(n_items, uint32_t(grid_cap));
+  kfn<<<grid, T, smem, s>>>(a);
+}
+
 template <int KN, int SM>
 void launch_tile(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
-  auto kfn = p2p_tile_kernel<KN, SM, kE, kThreads, kTile>;
-  p2p_tile_kernel<KN, SM, kE, kThreads, kTile><<<n_items, kThreads, kTileSmem, s>>>(a);
-  (void)kfn;
+  switch (variant_index()) {
+    case 1: launch_tile_v<KN, SM, 128, 2>(a, n_items, s); break;
+    case 2: launch_tile_v<KN, SM, 128, 4>(a, n_items, s); break;
+    case 3: launch_tile_v<KN, SM, 256, 4>(a, n_items, s); break;
+    default: launch_tile_v<KN, SM, 256, 2>(a, n_items, s); break;
+  }
 }
 
 template <int KN, int SM>
@@ -312,35 +348,41 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->item_first.assign(nl + 1, 0);
   c->fin_first.assign(nl + 1, 0);
   uint64_t partial_evals = 0;
+  // Items: eval blocks of <= kMaxEvalsPerItem evals; a block whose pair work
+  // exceeds the budget is split into strong-list chunks whose partials are
+  // summed in chunk order by p2p_finalize_kernel.
   for (uint32_t t = 0; t < nl; ++t) {
     c->item_first[t] = uint32_t(c->items.size());
     c->fin_first[t] = uint32_t(c->fins.size());
-    const uint32_t nt = j->ev_off[t + 1] - j->ev_off[t];
-    if (nt == 0) continue;
+    const uint32_t ntl = j->ev_off[t + 1] - j->ev_off[t];
     const uint32_t sb0 = j->strong_off[t], sb1 = j->strong_off[t + 1];
-    const uint64_t pairs = uint64_t(nt) * S[t];
-    if (pairs <= budget || sb1 - sb0 <= 1 || S[t] > 0xFFFFFFFFull) {
-      c->items.push_back(P2PItem{t, sb0, sb1, uint32_t(S[t]), kNoSelf, 0});
-      continue;
-    }
-    const uint64_t src_per_chunk = std::max<uint64_t>(1, budget / nt);
-    const uint32_t base = uint32_t(partial_evals);
-    uint32_t n_chunks = 0;
-    uint32_t q = sb0;
-    while (q < sb1) {
-      uint32_t q1 = q;
-      uint64_t acc = 0;
-      while (q1 < sb1 && (acc == 0 || acc + (j->pt_off[j->strong_idx[q1] + 1] -
-                                             j->pt_off[j->strong_idx[q1]]) <= src_per_chunk)) {
-        acc += j->pt_off[j->strong_idx[q1] + 1] - j->pt_off[j->strong_idx[q1]];
-        ++q1;
+    for (uint32_t e0 = 0; e0 < ntl; e0 += kMaxEvalsPerItem) {
+      const uint32_t nt = std::min<uint32_t>(kMaxEvalsPerItem, ntl - e0);
+      const uint32_t evb = j->ev_off[t] + e0;
+      const uint64_t pairs = uint64_t(nt) * S[t];
+      if (pairs <= budget || sb1 - sb0 <= 1 || S[t] > 0xFFFFFFFFull) {
+        c->items.push_back(P2PItem{t, evb, nt, sb0, sb1, uint32_t(S[t]), kNoSelf, 0});
+        continue;
       }
-      c->items.push_back(P2PItem{t, q, q1, uint32_t(acc), uint32_t(partial_evals), 0});
-      partial_evals += nt;
-      ++n_chunks;
-      q = q1;
+      const uint64_t src_per_chunk = std::max<uint64_t>(1, budget / nt);
+      const uint32_t base = uint32_t(partial_evals);
+      uint32_t n_chunks = 0;
+      uint32_t q = sb0;
+      while (q < sb1) {
+        uint32_t q1 = q;
+        uint64_t acc = 0;
+        while (q1 < sb1 && (acc == 0 || acc + (j->pt_off[j->strong_idx[q1] + 1] -
+                                               j->pt_off[j->strong_idx[q1]]) <= src_per_chunk)) {
+          acc += j->pt_off[j->strong_idx[q1] + 1] - j->pt_off[j->strong_idx[q1]];
+          ++q1;
+        }
+        c->items.push_back(P2PItem{t, evb, nt, q, q1, uint32_t(acc), uint32_t(partial_evals), 0});
+        partial_evals += nt;
+        ++n_chunks;
+        q = q1;
+      }
+      c->fins.push_back(P2PFinal{evb, nt, base, n_chunks});
     }
-    c->fins.push_back(P2PFinal{t, base, n_chunks, 0});
   }
   c->item_first[nl] = uint32_t(c->items.size());
   c->fin_first[nl] = uint32_t(c->fins.size());
@@ -359,6 +401,8 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   CU_TRY(c, c->d_out.ensure(size_t(ne) * 16));
   CU_TRY(c, c->d_partial.ensure(size_t(partial_evals) * 16));
   CU_TRY(c, c->d_hits.ensure(8));
+  CU_TRY(c, c->d_counter.ensure(8));
+  CU_TRY(c, c->d_seg.ensure(size_t(nnz) * 8));
   CU_TRY(c, c->h_hits.ensure(8));
   // CSR + work list through one pinned block
   const size_t csr_bytes = size_t(nl + 1) * 12 + size_t(nnz) * 4 +
@@ -397,6 +441,13 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   if (!c->fins.empty())
     CU_TRY(c, cudaMemcpyAsync(c->d_fin.p, hc + o_fi, c->fins.size() * sizeof(P2PFinal),
                               cudaMemcpyHostToDevice, s));
+  if (nnz) {
+    p2p_segments_kernel<<<(nnz + 255) / 256, 256, 0, s>>>(c->d_sidx.as<uint32_t>(),
+                                                          c->d_pt.as<uint32_t>(), nnz,
+                                                          c->d_seg.as<uint2>());
+    CU_TRY(c, cudaGetLastError());
+    c->launches += 1;
+  }
   c->staged = true;
   return FMMCU_OK;
 }
@@ -406,6 +457,7 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch) 
   cudaStream_t s = c->stream;
   int n = 0;
   CU_TRY(c, cudaMemsetAsync(c->d_hits.p, 0, 8, s));
+  CU_TRY(c, cudaMemsetAsync(c->d_counter.p, 0, 8, s));
   const P2PArgs a = make_args(c);
   if (le > lb) {
     if (mode == FMMCU_MODE_EXACT) {
@@ -426,7 +478,6 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch) 
       const uint32_t f0 = c->fin_first[lb], f1 = c->fin_first[le];
       if (f1 > f0) {
         p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(c->d_fin.as<P2PFinal>() + f0, f1 - f0,
-                                                     c->d_ev.as<uint32_t>(),
                                                      c->d_partial.as<double2>(),
                                                      c->out_ptr());
         ++n;
@@ -513,7 +564,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->m2l_stream);
     for (DevBuf* b : {&c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
-                      &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits,
+                      &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter,
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
                       &c->m_table, &c->m_out, &c->m_flag})
       b->release();

@@ -4,18 +4,22 @@
 // (proj/src/backend.cpp:41-69) with the per-pair arithmetic of
 // kernel_term()/smoother_factor() (proj/src/expansion.cpp:78-92).
 //
-// Fast path (p2p_tile_kernel):
-//   * one work item (= one target leaf, or one chunk of a heavy leaf's
-//     strong list) per CTA;
-//   * the item's source leaves are contiguous runs of packed 32-byte records
-//     {x, y, m_re, m_im}; an elected thread issues one TMA bulk copy
-//     (cp.async.bulk + mbarrier complete_tx) per run into a shared tile;
+// Fast path (p2p_tile_kernel), FP64 CUDA-core pipe, no tensor cores:
+//   * persistent CTAs pull work items (a target leaf, or an eval block /
+//     strong-list chunk of a heavy leaf) from a global counter;
+//   * an item's source leaves are contiguous runs of packed 32-byte records
+//     {x, y, m_re, m_im}; warp 0 builds the run list of the next tile with
+//     one coalesced load + shuffle scan over the precomputed (begin, length)
+//     of each strong entry and issues one TMA bulk copy
+//     (cp.async.bulk + mbarrier complete_tx) per run into the other of two
+//     shared tiles -- the next tile streams in while this one is computed;
 //   * thread (g, k) owns E evals of eval-slot g and walks sources
-//     k, k+K, k+2K, ... of the tile (broadcast LDS.128); partials are reduced
-//     over k in a fixed order through shared memory (deterministic);
+//     k, k+K, k+2K, ... of the tile (broadcast LDS.128); the K partials of
+//     an eval are reduced in fixed k order through shared memory, so results
+//     are deterministic;
 //   * per pair: 2 DADD, r^2 (DMUL+DFMA), 1/r^2 = MUFU.RCP64H seed + one
 //     cubic Newton step (3 DFMA), m*conj(d) (2 DMUL + 2 DFMA), 2 DFMA
-//     accumulate -- 13 FP64 instructions, 23 algorithmic flops.
+//     accumulate -- 13 FP64 instructions for 23 algorithmic flops.
 // Exact path (p2p_exact_kernel): one thread per eval, reference order,
 // libgcc __divdc3 restated with non-contracted __d*_rn intrinsics -- bitwise
 // equal to the reference for the harmonic kernel without smoother.
@@ -28,9 +32,12 @@ namespace fmmcu {
 
 constexpr uint32_t kNoSelf = 0xFFFFFFFFu;
 
-// Work item: target leaf `leaf`, strong entries [s_begin, s_end) of its list.
+// Work item: evals [ev_begin, ev_begin + nt) of target leaf `leaf` against
+// strong entries [s_begin, s_end) of its list.
 struct P2PItem {
   uint32_t leaf;
+  uint32_t ev_begin;
+  uint32_t nt;
   uint32_t s_begin;
   uint32_t s_end;
   uint32_t n_src;        // sources covered by this item
@@ -39,15 +46,17 @@ struct P2PItem {
 };
 
 struct P2PArgs {
-  const double4* __restrict__ src;   // packed sources, permuted order
-  const double2* __restrict__ evy;   // eval positions, permuted order
+  const double4* __restrict__ src;     // packed sources, permuted order
+  const double2* __restrict__ evy;     // eval positions, permuted order
   const uint32_t* __restrict__ eself;  // permuted slot of the eval's own source, or kNoSelf
   const uint32_t* __restrict__ pt_off;
   const uint32_t* __restrict__ ev_off;
   const uint32_t* __restrict__ s_off;
   const uint32_t* __restrict__ s_idx;
+  const uint2* __restrict__ seg;       // per strong entry: (pt_off[s], n_points(s))
   const P2PItem* __restrict__ items;
   uint32_t n_items;
+  unsigned int* __restrict__ next_item;  // dynamic scheduler counter (zeroed per launch)
   double2* __restrict__ out;
   double2* __restrict__ partial;
   unsigned long long* __restrict__ hits;  // self pairs skipped (pair count correction)
@@ -106,6 +115,10 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
 // Per-pair contribution accumulated with the sign folded out:
 //   harmonic: acc += m * conj(d) / |d|^2     (term = -acc)
 //   log     : acc += m * log(d)              (term = +acc)
@@ -145,220 +158,268 @@ __device__ __forceinline__ void pair_accum(double yx, double yy, const double4 s
   }
 }
 
+// seg[q] = (first permuted source slot, source count) of strong entry q.
+__global__ void p2p_segments_kernel(const uint32_t* __restrict__ s_idx,
+                                    const uint32_t* __restrict__ pt_off, uint32_t nnz,
+                                    uint2* __restrict__ seg) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nnz) {
+    const uint32_t b = s_idx[q];
+    const uint32_t p0 = pt_off[b];
+    seg[q] = make_uint2(p0, pt_off[b + 1] - p0);
+  }
+}
+
+constexpr int kMaxSeg = 128;  // source runs per tile
+
 // ------------------------------------------------------------ fast kernel --
-// Dynamic smem layout: [mbarrier 16 B][tile: TILE double4][reduction scratch]
+// Dynamic smem: [2 mbarriers | pad to 128][tile 0][tile 1][reduction E*THREADS double2]
 template <int KERNEL, int SMOOTH, int E, int THREADS, int TILE>
-__global__ void __launch_bounds__(THREADS)
-    p2p_tile_kernel(const P2PArgs a) {
+__global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
+  static_assert(TILE % 32 == 0, "tile");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-  double4* tile = reinterpret_cast<double4*>(smem_raw + 128);
-  __shared__ uint32_t seg_gbeg[64];  // segments (source leaf runs) of the current tile
-  __shared__ uint32_t seg_tpos[65];
-  __shared__ uint32_t s_nseg;
-  __shared__ uint32_t s_cursor_entry, s_cursor_off;
+  double4* tiles = reinterpret_cast<double4*>(smem_raw + 128);
+  double2* red = reinterpret_cast<double2*>(smem_raw + 128 + 2 * TILE * 32);
+  __shared__ uint32_t seg_gbeg[2][kMaxSeg];
+  __shared__ uint32_t seg_tpos[2][kMaxSeg + 1];
+  __shared__ uint32_t meta_item[2], meta_nseg[2], meta_flags[2];
   __shared__ unsigned int s_hits;
 
-  const P2PItem it = a.items[blockIdx.x];
-  const uint32_t ev0 = a.ev_off[it.leaf];
-  const uint32_t nt = a.ev_off[it.leaf + 1] - ev0;
   const int tid = threadIdx.x;
-  if (nt == 0 || it.n_src == 0) {  // host never emits these; keep the kernel total
-    if (it.partial_off != kNoSelf)
-      for (uint32_t e = tid; e < nt; e += THREADS) a.partial[it.partial_off + e] = make_double2(0.0, 0.0);
-    else
-      for (uint32_t e = tid; e < nt; e += THREADS) a.out[ev0 + e] = make_double2(0.0, 0.0);
-    return;
-  }
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  constexpr unsigned FULL = 0xffffffffu;
 
-  // eval-slot g owns evals [g*E, g*E+E); K source lanes share the slot.
-  const uint32_t G = (nt + E - 1) / E;
-  const uint32_t Gc = G < THREADS ? G : THREADS;  // slots per pass
-  const uint32_t K = THREADS / Gc;
+  // ---- producer state (warp 0, warp-uniform registers) ----------------------
+  uint32_t st_item = kNoSelf, st_ent = 0, st_off = 0, st_end = 0, st_left = 0;
+
+  // Builds the run list of the next tile into buffer `b` and issues its TMA
+  // copies.  Called by all 32 lanes of warp 0.
+  auto stage = [&](int b) {
+    uint32_t flags = 0;
+    if (st_left == 0) {  // current item exhausted: fetch the next one
+      uint32_t nxt = 0;
+      if (lane == 0) nxt = atomicAdd(a.next_item, 1u);
+      nxt = __shfl_sync(FULL, nxt, 0);
+      if (nxt >= a.n_items) {
+        if (lane == 0) meta_item[b] = kNoSelf;
+        return;
+      }
+      const P2PItem it = a.items[nxt];
+      st_item = nxt;
+      st_ent = it.s_begin;
+      st_end = it.s_end;
+      st_off = 0;
+      st_left = it.n_src;
+      flags |= 1u;
+    }
+    uint32_t filled = 0, nseg = 0;
+    while (filled < TILE && st_ent < st_end && nseg + 32 <= kMaxSeg) {
+      const uint32_t q = st_ent + lane;
+      const bool valid = q < st_end;
+      const uint2 sg = valid ? a.seg[q] : make_uint2(0u, 0u);
+      uint32_t b0 = sg.x, n = sg.y;
+      if (lane == 0) {
+        b0 += st_off;
+        n -= st_off;
+      }
+      uint32_t incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t excl = incl - n;
+      const uint32_t room = TILE - filled;
+      const uint32_t take = excl >= room ? 0u : min(n, room - excl);
+      const unsigned has = __ballot_sync(FULL, take > 0);
+      if (take > 0) {
+        const uint32_t pos = nseg + __popc(has & ((1u << lane) - 1u));
+        seg_gbeg[b][pos] = b0;
+        seg_tpos[b][pos] = filled + excl;
+      }
+      const unsigned part = __ballot_sync(FULL, valid && take < n);
+      const uint32_t total = __shfl_sync(FULL, incl, 31);
+      const uint32_t got = min(total, room);
+      if (part == 0) {
+        st_ent += min(32u, st_end - st_ent);
+        st_off = 0;
+      } else {
+        const int L = __ffs(part) - 1;
+        const uint32_t tL = __shfl_sync(FULL, take, L);
+        st_off = (L == 0 ? st_off : 0u) + tL;
+        st_ent += uint32_t(L);
+      }
+      filled += got;
+      nseg += uint32_t(__popc(has));
+      st_left -= got;
+    }
+    if (st_left == 0) flags |= 2u;
+    if (lane == 0) {
+      seg_tpos[b][nseg] = filled;
+      meta_item[b] = st_item;
+      meta_nseg[b] = nseg;
+      meta_flags[b] = flags;
+      fence_proxy_async();
+      mbar_expect_tx(&bar[b], filled * 32u);
+    }
+    __syncwarp();
+    for (uint32_t s = lane; s < nseg; s += 32) {
+      const uint32_t t0 = seg_tpos[b][s];
+      const uint32_t t1 = seg_tpos[b][s + 1];
+      bulk_g2s(tiles + b * TILE + t0, a.src + seg_gbeg[b][s], (t1 - t0) * 32u, &bar[b]);
+    }
+  };
 
   if (tid == 0) {
-    mbar_init(bar, 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     s_hits = 0;
-    s_cursor_entry = it.s_begin;
-    s_cursor_off = 0;
+    fence_mbar_init();
   }
   __syncthreads();
-  uint32_t phase = 0;
+  if (warp == 0) stage(0);
+  __syncthreads();
 
-  for (uint32_t g0 = 0; g0 < G; g0 += Gc) {  // eval passes (only > 1 for huge leaves)
-    const uint32_t g = g0 + (uint32_t)tid % Gc;
-    const uint32_t k = (uint32_t)tid / Gc;
-    const bool active = (k < K) && (g < G);
-    double yx[E], yy[E], ar[E], ai[E];
-    uint32_t sg[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const uint32_t le = g * E + e;
-      const bool ok = active && le < nt;
-      const double2 y = ok ? a.evy[ev0 + le] : make_double2(1e300, 1e300);
-      yx[e] = y.x;
-      yy[e] = y.y;
-      sg[e] = ok ? a.eself[ev0 + le] : kNoSelf;
-      ar[e] = 0.0;
-      ai[e] = 0.0;
-    }
+  // ---- consumer state (all threads) ------------------------------------------
+  uint32_t parity[2] = {0u, 0u};
+  uint32_t nt = 0, G = 1, K = 1, g = 0, k = 0, ev0 = 0, poff = kNoSelf;
+  bool active = false;
+  double yx[E], yy[E], ar[E], ai[E];
+  uint32_t sg[E];
+  unsigned int hits = 0;
 
-    if (tid == 0) {
-      s_cursor_entry = it.s_begin;
-      s_cursor_off = 0;
-    }
-    __syncthreads();
-
-    uint32_t remaining = it.n_src;
-    while (remaining > 0) {
-      // ---- stage one tile: elected thread issues bulk copies -------------
-      if (tid == 0) {
-        uint32_t filled = 0, nseg = 0;
-        uint32_t ent = s_cursor_entry, off = s_cursor_off;
-        // count bytes first (expect_tx must precede completion accounting)
-        uint32_t ent2 = ent, off2 = off, bytes = 0, f2 = 0;
-        while (f2 < TILE && ent2 < it.s_end && nseg < 64) {
-          const uint32_t sb = a.s_idx[ent2];
-          const uint32_t b = a.pt_off[sb], n = a.pt_off[sb + 1] - b;
-          const uint32_t take = min(n - off2, (uint32_t)TILE - f2);
-          if (take > 0) {
-            seg_gbeg[nseg] = b + off2;
-            seg_tpos[nseg] = f2;
-            ++nseg;
-          }
-          f2 += take;
-          bytes += take * 32u;
-          off2 += take;
-          if (off2 == n) {
-            ++ent2;
-            off2 = 0;
-          }
-        }
-        seg_tpos[nseg] = f2;
-        s_nseg = nseg;
-        fence_proxy_async();
-        mbar_expect_tx(bar, bytes);
-        for (uint32_t sIdx = 0; sIdx < nseg; ++sIdx) {
-          const uint32_t n = seg_tpos[sIdx + 1] - seg_tpos[sIdx];
-          bulk_g2s(tile + seg_tpos[sIdx], a.src + seg_gbeg[sIdx], n * 32u, bar);
-        }
-        filled = f2;
-        (void)filled;
-        s_cursor_entry = ent2;
-        s_cursor_off = off2;
-      }
-      __syncthreads();
-      const uint32_t nseg = s_nseg;
-      const uint32_t ntile = seg_tpos[nseg];
-      // tile position of each eval's own source (segments ascend in gbeg)
-      uint32_t ps[E];
+  for (uint32_t n = 0;; ++n) {
+    const int b = int(n & 1u);
+    const uint32_t item = meta_item[b];
+    if (item == kNoSelf) break;
+    const uint32_t flags = meta_flags[b];
+    const uint32_t nseg = meta_nseg[b];
+    if (flags & 1u) {  // first tile of an item: roles and eval registers
+      const P2PItem it = a.items[item];
+      nt = it.nt;
+      ev0 = it.ev_begin;
+      poff = it.partial_off;
+      G = (nt + E - 1) / E;  // host guarantees nt <= E * THREADS
+      K = THREADS / G;
+      g = uint32_t(tid) % G;
+      k = uint32_t(tid) / G;
+      active = k < K;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        ps[e] = kNoSelf;
-        const uint32_t s = sg[e];
-        if (s != kNoSelf && nseg > 0 && s >= seg_gbeg[0]) {
-          uint32_t lo = 0, hi = nseg;  // seg_gbeg[lo] <= s < seg_gbeg[hi]
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (seg_gbeg[mid] <= s) lo = mid; else hi = mid;
-          }
-          const uint32_t n = seg_tpos[lo + 1] - seg_tpos[lo];
-          if (s - seg_gbeg[lo] < n) ps[e] = seg_tpos[lo] + (s - seg_gbeg[lo]);
-        }
+        const uint32_t le = g * E + e;
+        const bool ok = active && le < nt;
+        const double2 y = ok ? a.evy[ev0 + le] : make_double2(0.0, 0.0);
+        yx[e] = y.x;
+        yy[e] = y.y;
+        sg[e] = ok ? a.eself[ev0 + le] : kNoSelf;
+        ar[e] = 0.0;
+        ai[e] = 0.0;
       }
-      if (ntile == 0) break;  // defensive: never spin on an empty tile
-      mbar_wait(bar, phase);
-      phase ^= 1u;
+    }
+    if (warp == 0) stage(b ^ 1);  // next tile streams in while this one is computed
 
-      bool my_self = false;
+    // tile position of each eval's own source (runs ascend in source slot)
+    const uint32_t ntile = seg_tpos[b][nseg];
+    uint32_t ps[E];
+    bool my_self = false;
 #pragma unroll
-      for (int e = 0; e < E; ++e) my_self |= (ps[e] != kNoSelf);
-      const bool warp_self = __any_sync(0xffffffffu, my_self);  // warp-uniform path choice
-      if (active) {
-        if (!warp_self) {
+    for (int e = 0; e < E; ++e) {
+      ps[e] = kNoSelf;
+      const uint32_t s = sg[e];
+      if (s != kNoSelf && nseg > 0 && s >= seg_gbeg[b][0]) {
+        uint32_t lo = 0, hi = nseg;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (seg_gbeg[b][mid] <= s) lo = mid; else hi = mid;
+        }
+        const uint32_t len = seg_tpos[b][lo + 1] - seg_tpos[b][lo];
+        if (s - seg_gbeg[b][lo] < len) ps[e] = seg_tpos[b][lo] + (s - seg_gbeg[b][lo]);
+      }
+      my_self |= ps[e] != kNoSelf;
+    }
+    const bool warp_self = __any_sync(FULL, my_self);
+
+    mbar_wait(&bar[b], parity[b]);
+    parity[b] ^= 1u;
+
+    const double4* tile = tiles + b * TILE;
+    if (active) {
+      if (!warp_self) {
 #pragma unroll 2
-          for (uint32_t j = k; j < ntile; j += K) {
-            const double4 s = tile[j];
-#pragma unroll
-            for (int e = 0; e < E; ++e)
-              pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, true, ar[e],
-                                         ai[e]);
-          }
-        } else {
-#pragma unroll 2
-          for (uint32_t j = k; j < ntile; j += K) {
-            const double4 s = tile[j];
-#pragma unroll
-            for (int e = 0; e < E; ++e)
-              pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, j != ps[e],
-                                         ar[e], ai[e]);
-          }
-          // a self pair is skipped by exactly one source lane
-          unsigned int h = 0;
+        for (uint32_t j = k; j < ntile; j += K) {
+          const double4 s = tile[j];
 #pragma unroll
           for (int e = 0; e < E; ++e)
-            h += (ps[e] != kNoSelf && (ps[e] % K) == k && g * E + e < nt) ? 1u : 0u;
-          if (h) atomicAdd(&s_hits, h);
+            pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, true, ar[e], ai[e]);
         }
+      } else {
+#pragma unroll 2
+        for (uint32_t j = k; j < ntile; j += K) {
+          const double4 s = tile[j];
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, j != ps[e], ar[e],
+                                       ai[e]);
+        }
+        // each skipped self pair is seen by exactly one source lane
+#pragma unroll
+        for (int e = 0; e < E; ++e) hits += (ps[e] != kNoSelf && ps[e] % K == k) ? 1u : 0u;
       }
-      remaining -= ntile;
-      __syncthreads();  // tile consumed before it is overwritten
     }
 
-    // ---- reduce the K partials of each eval in fixed k order -------------
-    double2* red = reinterpret_cast<double2*>(tile);  // reuse the tile
-    if (active) {
+    if (flags & 2u) {  // last tile of the item: reduce the K partials in k order
+      if (active) {
 #pragma unroll
-      for (int e = 0; e < E; ++e) red[k * (Gc * E) + (g - g0) * E + e] = make_double2(ar[e], ai[e]);
-    }
-    __syncthreads();
-    const uint32_t nslot = min(Gc * E, nt - g0 * E);
-    for (uint32_t le = tid; le < nslot; le += THREADS) {
-      double sr = 0.0, si = 0.0;
-      for (uint32_t kk = 0; kk < K; ++kk) {
-        const double2 v = red[kk * (Gc * E) + le];
-        sr += v.x;
-        si += v.y;
+        for (int e = 0; e < E; ++e) red[(e * K + k) * G + g] = make_double2(ar[e], ai[e]);
       }
-      const double2 res = (KERNEL == 0) ? make_double2(-sr, -si) : make_double2(sr, si);
-      const uint32_t gl = g0 * E + le;
-      if (it.partial_off == kNoSelf)
-        a.out[ev0 + gl] = res;
-      else
-        a.partial[it.partial_off + gl] = res;
+      __syncthreads();
+      for (uint32_t le = tid; le < nt; le += THREADS) {
+        const uint32_t gg = le / E, ee = le % E;
+        double sr = 0.0, si = 0.0;
+        for (uint32_t kk = 0; kk < K; ++kk) {
+          const double2 v = red[(ee * K + kk) * G + gg];
+          sr += v.x;
+          si += v.y;
+        }
+        const double2 res = (KERNEL == 0) ? make_double2(-sr, -si) : make_double2(sr, si);
+        if (poff == kNoSelf)
+          a.out[ev0 + le] = res;
+        else
+          a.partial[poff + le] = res;
+      }
     }
-    __syncthreads();
+    __syncthreads();  // tile b and the reduction buffer are free; meta[b^1] is visible
   }
+  for (int o = 16; o > 0; o >>= 1) hits += __shfl_down_sync(FULL, hits, o);
+  if (lane == 0 && hits) atomicAdd(&s_hits, hits);
+  __syncthreads();
   if (tid == 0 && s_hits) atomicAdd(a.hits, (unsigned long long)s_hits);
 }
 
-// Sum the partials of split leaves in chunk order.  One thread per eval.
-// fin: per split leaf {leaf, first partial base, n_chunks}; chunks of one
-// leaf are consecutive, each nt evals long.
+// Sum the chunk partials of split eval blocks in chunk order (deterministic).
 struct P2PFinal {
-  uint32_t leaf;
+  uint32_t ev_begin;
+  uint32_t nt;
   uint32_t base;
   uint32_t n_chunks;
-  uint32_t pad;
 };
 
 __global__ void p2p_finalize_kernel(const P2PFinal* __restrict__ fin, uint32_t n_fin,
-                                    const uint32_t* __restrict__ ev_off,
                                     const double2* __restrict__ partial,
                                     double2* __restrict__ out) {
   const uint32_t f = blockIdx.x;
   if (f >= n_fin) return;
   const P2PFinal F = fin[f];
-  const uint32_t ev0 = ev_off[F.leaf];
-  const uint32_t nt = ev_off[F.leaf + 1] - ev0;
-  for (uint32_t e = threadIdx.x; e < nt; e += blockDim.x) {
+  for (uint32_t e = threadIdx.x; e < F.nt; e += blockDim.x) {
     double sr = 0.0, si = 0.0;
     for (uint32_t c = 0; c < F.n_chunks; ++c) {
-      const double2 v = partial[F.base + c * nt + e];
+      const double2 v = partial[F.base + c * F.nt + e];
       sr += v.x;
       si += v.y;
     }
-    out[ev0 + e] = make_double2(sr, si);
+    out[F.ev_begin + e] = make_double2(sr, si);
   }
 }
 
