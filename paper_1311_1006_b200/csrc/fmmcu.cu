@@ -30,22 +30,25 @@ using namespace fmmcu;
 
 namespace {
 
-// Fast-kernel shape variants (threads per CTA x evals per thread); the
-// default is chosen from measurements (profiles/), FMMCU_P2P_VARIANT
-// overrides it for experiments: 0 = 256x2, 1 = 128x2, 2 = 128x4, 3 = 256x4.
-constexpr int kTile = 512;  // source records per shared tile (x2, double-buffered)
-constexpr int kMaxEvalsPerItem = 256;
+// Fast-kernel shape variants (threads x evals/thread, source records per
+// shared tile, source-loop unroll); the default is chosen from measurements
+// (profiles/), FMMCU_P2P_VARIANT overrides it for experiments:
+//   0 = 256x2 t384 u4                 1 = 256x2 t384 u4, producer warp
+//   2 = 288x2 t384 u4, producer warp  3 = 160x4 t384 u2, producer warp
+//   4 = 128x4 t384 u2                 5 = 256x2 t512 u4, producer warp
+constexpr int kMaxEvalsPerItem = 128;  // eval records per item (staged with the first tile)
 int variant_index() {
   static int v = [] {
     const char* s = std::getenv("FMMCU_P2P_VARIANT");
     int i = s ? std::atoi(s) : 0;
-    return (i >= 0 && i < 4) ? i : 0;
+    return (i >= 0 && i < 6) ? i : 0;
   }();
   return v;
 }
 
-constexpr size_t tile_smem(int threads, int e) {
-  return 128 + size_t(2 * kTile) * 32 + size_t(threads) * e * 16;
+constexpr size_t tile_smem(int threads, int e, int tile) {
+  return 128 + size_t(2 * tile) * 32 + size_t(2 * kMaxEvalsPerItem) * 32 +
+         size_t(2 * threads) * e * 16;
 }
 
 struct DevBuf {
@@ -111,7 +114,7 @@ struct fmmcu_ctx {
 
   // staged job (device)
   DevBuf d_src, d_evy, d_eself, d_pt, d_ev, d_soff, d_sidx, d_items, d_fin, d_out, d_partial,
-      d_hits, d_seg, d_counter;
+      d_hits, d_seg, d_counter, d_evr;
   // pinned staging
   HostBuf h_src, h_evy, h_eself, h_out, h_hits, h_csr;
   std::vector<uint32_t> invperm;
@@ -174,6 +177,7 @@ P2PArgs make_args(fmmcu_ctx* c) {
   a.s_idx = c->d_sidx.as<uint32_t>();
   a.items = c->d_items.as<P2PItem>();
   a.seg = c->d_seg.as<uint2>();
+  a.evr = c->d_evr.as<double4>();
   a.next_item = c->d_counter.as<unsigned int>();
   a.out = c->out_ptr();
   a.partial = c->d_partial.as<double2>();
@@ -184,10 +188,10 @@ P2PArgs make_args(fmmcu_ctx* c) {
   return a;
 }
 
-template <int KN, int SM, int T, int E>
+template <int KN, int SM, int T, int E, int TILE, int U, bool PROD>
 void launch_tile_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
-  auto kfn = p2p_tile_kernel<KN, SM, E, T, kTile>;
-  constexpr size_t smem = tile_smem(T, E);
+  auto kfn = p2p_tile_kernel<KN, SM, E, T, TILE, kMaxEvalsPerItem, U, PROD>;
+  constexpr size_t smem = tile_smem(T, E, TILE);
   static int grid_cap = [&] {
     cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -204,10 +208,12 @@ void launch_tile_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
 template <int KN, int SM>
 void launch_tile(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
   switch (variant_index()) {
-    case 1: launch_tile_v<KN, SM, 128, 2>(a, n_items, s); break;
-    case 2: launch_tile_v<KN, SM, 128, 4>(a, n_items, s); break;
-    case 3: launch_tile_v<KN, SM, 256, 4>(a, n_items, s); break;
-    default: launch_tile_v<KN, SM, 256, 2>(a, n_items, s); break;
+    case 1: launch_tile_v<KN, SM, 256, 2, 384, 4, true>(a, n_items, s); break;
+    case 2: launch_tile_v<KN, SM, 288, 2, 384, 4, true>(a, n_items, s); break;
+    case 3: launch_tile_v<KN, SM, 160, 4, 384, 2, true>(a, n_items, s); break;
+    case 4: launch_tile_v<KN, SM, 128, 4, 384, 2, false>(a, n_items, s); break;
+    case 5: launch_tile_v<KN, SM, 256, 2, 512, 4, true>(a, n_items, s); break;
+    default: launch_tile_v<KN, SM, 256, 2, 384, 4, false>(a, n_items, s); break;
   }
 }
 
@@ -403,6 +409,7 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   CU_TRY(c, c->d_hits.ensure(8));
   CU_TRY(c, c->d_counter.ensure(8));
   CU_TRY(c, c->d_seg.ensure(size_t(nnz) * 8));
+  CU_TRY(c, c->d_evr.ensure(size_t(ne) * 32));
   CU_TRY(c, c->h_hits.ensure(8));
   // CSR + work list through one pinned block
   const size_t csr_bytes = size_t(nl + 1) * 12 + size_t(nnz) * 4 +
@@ -442,6 +449,12 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     CU_TRY(c, cudaMemcpyAsync(c->d_fin.p, hc + o_fi, c->fins.size() * sizeof(P2PFinal),
                               cudaMemcpyHostToDevice, s));
   if (nnz) {
+    if (ne) {
+      p2p_evrec_kernel<<<(ne + 255) / 256, 256, 0, s>>>(c->d_evy.as<double2>(),
+                                                        c->d_eself.as<uint32_t>(), ne,
+                                                        c->d_evr.as<double4>());
+      c->launches += 1;
+    }
     p2p_segments_kernel<<<(nnz + 255) / 256, 256, 0, s>>>(c->d_sidx.as<uint32_t>(),
                                                           c->d_pt.as<uint32_t>(), nnz,
                                                           c->d_seg.as<uint2>());
@@ -564,7 +577,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->m2l_stream);
     for (DevBuf* b : {&c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
-                      &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter,
+                      &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter, &c->d_evr,
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
                       &c->m_table, &c->m_out, &c->m_flag})
       b->release();

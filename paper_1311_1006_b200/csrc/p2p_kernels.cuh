@@ -48,6 +48,7 @@ struct P2PItem {
 struct P2PArgs {
   const double4* __restrict__ src;     // packed sources, permuted order
   const double2* __restrict__ evy;     // eval positions, permuted order
+  const double4* __restrict__ evr;     // eval records {x, y, self bits, 0} (fast path)
   const uint32_t* __restrict__ eself;  // permuted slot of the eval's own source, or kNoSelf
   const uint32_t* __restrict__ pt_off;
   const uint32_t* __restrict__ ev_off;
@@ -173,17 +174,34 @@ __global__ void p2p_segments_kernel(const uint32_t* __restrict__ s_idx,
 constexpr int kMaxSeg = 128;  // source runs per tile
 
 // ------------------------------------------------------------ fast kernel --
-// Dynamic smem: [2 mbarriers | pad to 128][tile 0][tile 1][reduction E*THREADS double2]
-template <int KERNEL, int SMOOTH, int E, int THREADS, int TILE>
+// Eval record as staged on the device: {x, y, self slot (bits), 0}.
+__global__ void p2p_evrec_kernel(const double2* __restrict__ evy,
+                                 const uint32_t* __restrict__ eself, uint32_t n,
+                                 double4* __restrict__ evr) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double2 y = evy[i];
+    evr[i] = make_double4(y.x, y.y, __longlong_as_double((long long)eself[i]), 0.0);
+  }
+}
+
+// Dynamic smem: [2 mbarriers | pad to 128][src tile 0][src tile 1]
+//               [eval tile 0][eval tile 1][reduction 0][reduction 1]
+template <int KERNEL, int SMOOTH, int E, int THREADS, int TILE, int MAXEV, int U, bool PRODUCER>
 __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
-  static_assert(TILE % 32 == 0, "tile");
+  // PRODUCER: warp 0 only stages tiles (its global-latency chain never delays
+  // the consumers' tile barrier); otherwise warp 0 stages and computes.
+  constexpr int TC = PRODUCER ? THREADS - 32 : THREADS;  // consumer threads
+  static_assert(TILE % 32 == 0 && MAXEV <= TC * E, "shape");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   double4* tiles = reinterpret_cast<double4*>(smem_raw + 128);
-  double2* red = reinterpret_cast<double2*>(smem_raw + 128 + 2 * TILE * 32);
+  double4* evt = tiles + 2 * TILE;
+  double2* red = reinterpret_cast<double2*>(evt + 2 * MAXEV);
   __shared__ uint32_t seg_gbeg[2][kMaxSeg];
   __shared__ uint32_t seg_tpos[2][kMaxSeg + 1];
-  __shared__ uint32_t meta_item[2], meta_nseg[2], meta_flags[2];
+  __shared__ uint32_t meta_item[2], meta_nseg[2], meta_flags[2], meta_ev[2], meta_nt[2],
+      meta_poff[2];
   __shared__ unsigned int s_hits;
 
   const int tid = threadIdx.x;
@@ -193,9 +211,10 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
 
   // ---- producer state (warp 0, warp-uniform registers) ----------------------
   uint32_t st_item = kNoSelf, st_ent = 0, st_off = 0, st_end = 0, st_left = 0;
+  uint32_t st_ev = 0, st_nt = 0, st_poff = kNoSelf;
 
-  // Builds the run list of the next tile into buffer `b` and issues its TMA
-  // copies.  Called by all 32 lanes of warp 0.
+  // Builds the next tile into buffer `b` (run list + TMA copies; on an
+  // item's first tile also its eval records).  All 32 lanes of warp 0.
   auto stage = [&](int b) {
     uint32_t flags = 0;
     if (st_left == 0) {  // current item exhausted: fetch the next one
@@ -212,6 +231,9 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
       st_end = it.s_end;
       st_off = 0;
       st_left = it.n_src;
+      st_ev = it.ev_begin;
+      st_nt = it.nt;
+      st_poff = it.partial_off;
       flags |= 1u;
     }
     uint32_t filled = 0, nseg = 0;
@@ -256,13 +278,18 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
       st_left -= got;
     }
     if (st_left == 0) flags |= 2u;
+    const uint32_t ev_bytes = (flags & 1u) ? st_nt * 32u : 0u;
     if (lane == 0) {
       seg_tpos[b][nseg] = filled;
       meta_item[b] = st_item;
       meta_nseg[b] = nseg;
       meta_flags[b] = flags;
+      meta_ev[b] = st_ev;
+      meta_nt[b] = st_nt;
+      meta_poff[b] = st_poff;
       fence_proxy_async();
-      mbar_expect_tx(&bar[b], filled * 32u);
+      mbar_expect_tx(&bar[b], filled * 32u + ev_bytes);
+      if (ev_bytes) bulk_g2s(evt + b * MAXEV, a.evr + st_ev, ev_bytes, &bar[b]);
     }
     __syncwarp();
     for (uint32_t s = lane; s < nseg; s += 32) {
@@ -282,13 +309,36 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
   if (warp == 0) stage(0);
   __syncthreads();
 
-  // ---- consumer state (all threads) ------------------------------------------
+  // ---- consumer state ---------------------------------------------------------
   uint32_t parity[2] = {0u, 0u};
   uint32_t nt = 0, G = 1, K = 1, g = 0, k = 0, ev0 = 0, poff = kNoSelf;
   bool active = false;
   double yx[E], yy[E], ar[E], ai[E];
   uint32_t sg[E];
   unsigned int hits = 0;
+  // pending reduction of the previous item (deferred by one tile: no extra barrier)
+  uint32_t r_nt = 0, r_G = 1, r_K = 1, r_ev0 = 0, r_poff = kNoSelf, r_buf = 0, items_done = 0;
+  bool r_pending = false;
+
+  const int ctid = PRODUCER ? tid - 32 : tid;  // consumer index (< 0: producer warp)
+  auto reduce_pending = [&]() {
+    const double2* rb = red + r_buf * (TC * E);
+    for (uint32_t le = uint32_t(ctid); ctid >= 0 && le < r_nt; le += TC) {
+      const uint32_t gg = le / E, ee = le % E;
+      double sr = 0.0, si = 0.0;
+      for (uint32_t kk = 0; kk < r_K; ++kk) {
+        const double2 v = rb[(ee * r_K + kk) * r_G + gg];
+        sr += v.x;
+        si += v.y;
+      }
+      const double2 res = (KERNEL == 0) ? make_double2(-sr, -si) : make_double2(sr, si);
+      if (r_poff == kNoSelf)
+        a.out[r_ev0 + le] = res;
+      else
+        a.partial[r_poff + le] = res;
+    }
+    r_pending = false;
+  };
 
   for (uint32_t n = 0;; ++n) {
     const int b = int(n & 1u);
@@ -296,34 +346,40 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
     if (item == kNoSelf) break;
     const uint32_t flags = meta_flags[b];
     const uint32_t nseg = meta_nseg[b];
-    if (flags & 1u) {  // first tile of an item: roles and eval registers
-      const P2PItem it = a.items[item];
-      nt = it.nt;
-      ev0 = it.ev_begin;
-      poff = it.partial_off;
-      G = (nt + E - 1) / E;  // host guarantees nt <= E * THREADS
-      K = THREADS / G;
-      g = uint32_t(tid) % G;
-      k = uint32_t(tid) / G;
-      active = k < K;
+    if (flags & 1u) {  // first tile of an item: thread roles
+      nt = meta_nt[b];
+      ev0 = meta_ev[b];
+      poff = meta_poff[b];
+      G = (nt + E - 1) / E;  // host guarantees nt <= MAXEV <= E * TC
+      K = TC / G;
+      g = uint32_t(ctid) % G;
+      k = uint32_t(ctid) / G;
+      active = ctid >= 0 && k < K;
+    }
+    if (warp == 0) stage(b ^ 1);  // next tile streams in while this one is computed
+    if (r_pending) reduce_pending();
+
+    mbar_wait(&bar[b], parity[b]);
+    parity[b] ^= 1u;
+    if (flags & 1u) {  // eval registers from the staged eval records
+      const double4* ev = evt + b * MAXEV;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const uint32_t le = g * E + e;
         const bool ok = active && le < nt;
-        const double2 y = ok ? a.evy[ev0 + le] : make_double2(0.0, 0.0);
-        yx[e] = y.x;
-        yy[e] = y.y;
-        sg[e] = ok ? a.eself[ev0 + le] : kNoSelf;
+        const double4 r = ok ? ev[le] : make_double4(0.0, 0.0, 0.0, 0.0);
+        yx[e] = r.x;
+        yy[e] = r.y;
+        sg[e] = ok ? uint32_t(__double_as_longlong(r.z)) : kNoSelf;
         ar[e] = 0.0;
         ai[e] = 0.0;
       }
     }
-    if (warp == 0) stage(b ^ 1);  // next tile streams in while this one is computed
 
     // tile position of each eval's own source (runs ascend in source slot)
     const uint32_t ntile = seg_tpos[b][nseg];
     uint32_t ps[E];
-    bool my_self = false;
+    uint32_t plo = kNoSelf, phi = 0u;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       ps[e] = kNoSelf;
@@ -335,32 +391,45 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
           if (seg_gbeg[b][mid] <= s) lo = mid; else hi = mid;
         }
         const uint32_t len = seg_tpos[b][lo + 1] - seg_tpos[b][lo];
-        if (s - seg_gbeg[b][lo] < len) ps[e] = seg_tpos[b][lo] + (s - seg_gbeg[b][lo]);
+        if (s - seg_gbeg[b][lo] < len) {
+          ps[e] = seg_tpos[b][lo] + (s - seg_gbeg[b][lo]);
+          plo = min(plo, ps[e]);
+          phi = max(phi, ps[e]);
+        }
       }
-      my_self |= ps[e] != kNoSelf;
     }
-    const bool warp_self = __any_sync(FULL, my_self);
-
-    mbar_wait(&bar[b], parity[b]);
-    parity[b] ^= 1u;
+    // Self pairs of this warp can only sit at tile positions [plo, phi]
+    // (the target leaf's own run for self-evaluation): only that stretch of
+    // the source loop pays for the per-pair exclusion test.
+    plo = __reduce_min_sync(FULL, plo);
+    phi = __reduce_max_sync(FULL, phi);
 
     const double4* tile = tiles + b * TILE;
     if (active) {
-      if (!warp_self) {
-#pragma unroll 2
-        for (uint32_t j = k; j < ntile; j += K) {
-          const double4 s = tile[j];
+      uint32_t j = k;
+      const uint32_t end1 = min(plo, ntile);
+#pragma unroll U
+      for (; j < end1; j += K) {
+        const double4 s = tile[j];
 #pragma unroll
-          for (int e = 0; e < E; ++e)
-            pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, true, ar[e], ai[e]);
-        }
-      } else {
-#pragma unroll 2
-        for (uint32_t j = k; j < ntile; j += K) {
+        for (int e = 0; e < E; ++e)
+          pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, true, ar[e], ai[e]);
+      }
+      if (plo != kNoSelf) {
+        const uint32_t end2 = min(phi + 1u, ntile);
+        for (; j < end2; j += K) {
           const double4 s = tile[j];
 #pragma unroll
           for (int e = 0; e < E; ++e)
             pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, j != ps[e], ar[e],
+                                       ai[e]);
+        }
+#pragma unroll U
+        for (; j < ntile; j += K) {
+          const double4 s = tile[j];
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, true, ar[e],
                                        ai[e]);
         }
         // each skipped self pair is seen by exactly one source lane
@@ -369,29 +438,25 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
       }
     }
 
-    if (flags & 2u) {  // last tile of the item: reduce the K partials in k order
+    if (flags & 2u) {  // last tile of the item: park the K partials, reduce next tile
+      const uint32_t rb = items_done & 1u;
       if (active) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) red[(e * K + k) * G + g] = make_double2(ar[e], ai[e]);
+        for (int e = 0; e < E; ++e)
+          red[rb * (TC * E) + (e * K + k) * G + g] = make_double2(ar[e], ai[e]);
       }
-      __syncthreads();
-      for (uint32_t le = tid; le < nt; le += THREADS) {
-        const uint32_t gg = le / E, ee = le % E;
-        double sr = 0.0, si = 0.0;
-        for (uint32_t kk = 0; kk < K; ++kk) {
-          const double2 v = red[(ee * K + kk) * G + gg];
-          sr += v.x;
-          si += v.y;
-        }
-        const double2 res = (KERNEL == 0) ? make_double2(-sr, -si) : make_double2(sr, si);
-        if (poff == kNoSelf)
-          a.out[ev0 + le] = res;
-        else
-          a.partial[poff + le] = res;
-      }
+      r_pending = true;
+      r_nt = nt;
+      r_G = G;
+      r_K = K;
+      r_ev0 = ev0;
+      r_poff = poff;
+      r_buf = rb;
+      ++items_done;
     }
-    __syncthreads();  // tile b and the reduction buffer are free; meta[b^1] is visible
+    __syncthreads();  // tile b free, partials visible, meta[b^1] visible
   }
+  if (r_pending) reduce_pending();
   for (int o = 16; o > 0; o >>= 1) hits += __shfl_down_sync(FULL, hits, o);
   if (lane == 0 && hits) atomicAdd(&s_hits, hits);
   __syncthreads();
