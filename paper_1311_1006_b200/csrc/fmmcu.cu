@@ -21,6 +21,7 @@
 #include "fmm_cuda.h"
 #include "m2l_kernels.cuh"
 #include "p2p_kernels.cuh"
+#include "p2p_warp.cuh"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -33,10 +34,10 @@ namespace {
 // Fast-kernel shape variants (threads x evals/thread, source records per
 // shared tile, source-loop unroll); the default is chosen from measurements
 // (profiles/), FMMCU_P2P_VARIANT overrides it for experiments:
-//   0 = 256x2 t384 u4                 1 = 256x2 t384 u4, producer warp
-//   2 = 288x2 t384 u4, producer warp  3 = 160x4 t384 u2, producer warp
-//   4 = 128x4 t384 u2                 5 = 256x2 t512 u4, producer warp
-constexpr int kMaxEvalsPerItem = 128;  // eval records per item (staged with the first tile)
+//   (threads x evals, tile, unroll, min CTAs/SM -> register cap)
+//   0 = 256x2 t512 u4 m4   1 = 256x2 t512 u4 m3   2 = 256x2 t512 u2 m4
+//   3 = 256x2 t512 u3 m4   4 = 128x4 t512 u2 m4   5 = 256x2 t512 u4 m2
+constexpr int kMaxEvalsPerItem = 64;  // eval records per item (staged with the first tile)
 int variant_index() {
   static int v = [] {
     const char* s = std::getenv("FMMCU_P2P_VARIANT");
@@ -44,6 +45,19 @@ int variant_index() {
     return (i >= 0 && i < 6) ? i : 0;
   }();
   return v;
+}
+
+// FMMCU_P2P_KERNEL=tile selects the CTA-tile kernel; default: warp pipelines.
+bool use_warp_kernel() {
+  static bool w = [] {
+    const char* s = std::getenv("FMMCU_P2P_KERNEL");
+    return !(s && std::string(s) == "tile");
+  }();
+  return w;
+}
+
+constexpr size_t warp_smem(int warps, int chunk) {
+  return size_t(warps) * (128 + size_t(2 * chunk) * 32);
 }
 
 constexpr size_t tile_smem(int threads, int e, int tile) {
@@ -101,6 +115,21 @@ struct HostBuf {
 
 using Clock = std::chrono::steady_clock;
 
+// Host memcpy split across the OpenMP threads (pinned staging copies).
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  if (bytes < (size_t(1) << 22)) {
+    if (bytes) std::memcpy(dst, src, bytes);
+    return;
+  }
+  const int64_t blocks = int64_t((bytes + (size_t(1) << 20) - 1) >> 20);
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < blocks; ++b) {
+    const size_t o = size_t(b) << 20;
+    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                std::min<size_t>(size_t(1) << 20, bytes - o));
+  }
+}
+
 }  // namespace
 
 struct fmmcu_ctx {
@@ -129,6 +158,9 @@ struct fmmcu_ctx {
   std::vector<P2PFinal> fins;
   std::vector<uint32_t> fin_first;     // [n_leaves + 1]
   bool staged = false;
+  bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
+  bool warp_items = false;     // work list built for p2p_warp_kernel
+  bool trace = std::getenv("FMMCU_TRACE") != nullptr;
   double2* ext_out = nullptr;  // caller-bound output (torch tensor), or null
   double2* out_ptr() const { return ext_out ? ext_out : d_out.as<double2>(); }
 
@@ -137,6 +169,7 @@ struct fmmcu_ctx {
   fmmcu_p2p_job job{};
   uint32_t run_lb = 0, run_le = 0;
   double prep_seconds = 0.0;
+  Clock::time_point t_evstart{};
   uint64_t run_total_pairs = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
 
@@ -166,6 +199,20 @@ int set_err(fmmcu_ctx* c, int code, const std::string& msg) {
   return code;
 }
 
+// FMMCU_TRACE=1: host phase times of a launch on stderr.
+struct Trace {
+  fmmcu_ctx* c;
+  Clock::time_point t = Clock::now();
+  explicit Trace(fmmcu_ctx* cc) : c(cc) {}
+  void mark(const char* what) {
+    if (!c->trace) return;
+    const auto now = Clock::now();
+    std::fprintf(stderr, "[fmmcu] %-22s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 P2PArgs make_args(fmmcu_ctx* c) {
   P2PArgs a{};
   a.src = c->d_src.as<double4>();
@@ -188,9 +235,9 @@ P2PArgs make_args(fmmcu_ctx* c) {
   return a;
 }
 
-template <int KN, int SM, int T, int E, int TILE, int U, bool PROD>
+template <int KN, int SM, int T, int E, int TILE, int U, bool PROD, int MINB>
 void launch_tile_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
-  auto kfn = p2p_tile_kernel<KN, SM, E, T, TILE, kMaxEvalsPerItem, U, PROD>;
+  auto kfn = p2p_tile_kernel<KN, SM, E, T, TILE, kMaxEvalsPerItem, U, PROD, MINB>;
   constexpr size_t smem = tile_smem(T, E, TILE);
   static int grid_cap = [&] {
     cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -208,12 +255,12 @@ void launch_tile_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
 template <int KN, int SM>
 void launch_tile(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
   switch (variant_index()) {
-    case 1: launch_tile_v<KN, SM, 256, 2, 384, 4, true>(a, n_items, s); break;
-    case 2: launch_tile_v<KN, SM, 288, 2, 384, 4, true>(a, n_items, s); break;
-    case 3: launch_tile_v<KN, SM, 160, 4, 384, 2, true>(a, n_items, s); break;
-    case 4: launch_tile_v<KN, SM, 128, 4, 384, 2, false>(a, n_items, s); break;
-    case 5: launch_tile_v<KN, SM, 256, 2, 512, 4, true>(a, n_items, s); break;
-    default: launch_tile_v<KN, SM, 256, 2, 384, 4, false>(a, n_items, s); break;
+    case 1: launch_tile_v<KN, SM, 256, 2, 512, 4, false, 3>(a, n_items, s); break;
+    case 2: launch_tile_v<KN, SM, 256, 2, 512, 2, false, 4>(a, n_items, s); break;
+    case 3: launch_tile_v<KN, SM, 256, 2, 512, 3, false, 4>(a, n_items, s); break;
+    case 4: launch_tile_v<KN, SM, 128, 4, 512, 2, false, 4>(a, n_items, s); break;
+    case 5: launch_tile_v<KN, SM, 256, 2, 512, 4, false, 2>(a, n_items, s); break;
+    default: launch_tile_v<KN, SM, 256, 2, 512, 4, false, 4>(a, n_items, s); break;
   }
 }
 
@@ -224,7 +271,52 @@ void launch_exact(const P2PArgs& a, uint32_t lb, uint32_t le, uint32_t eb, uint3
   p2p_exact_kernel<KN, SM><<<(n + 127) / 128, 128, 0, s>>>(a, lb, le, eb, ee);
 }
 
+template <int KN, int SM, int W, int E, int C, int U, int MINB>
+void launch_warp_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
+  auto kfn = p2p_warp_kernel<KN, SM, E, W, C, U, MINB>;
+  constexpr size_t smem = warp_smem(W, C);
+  static int grid_cap = [&] {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, W * 32, smem);
+    return std::max(1, sms * std::max(1, per_sm));
+  }();
+  const uint32_t need = (n_items + W - 1) / W;
+  const uint32_t grid = std::max(1u, std::min<uint32_t>(need, uint32_t(grid_cap)));
+  kfn<<<grid, W * 32, smem, s>>>(a);
+}
+
+// warp-kernel variants (warps/CTA, evals/lane, chunk, unroll, min CTAs/SM):
+//   0 = 4w E4 c128 u2 m4   1 = 4w E4 c128 u2 m5   2 = 8w E4 c128 u2 m2
+//   3 = 4w E4 c128 u1 m5   4 = 4w E4 c256 u2 m4   5 = 4w E4 c128 u2 m3
+template <int KN, int SM>
+void launch_warp(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
+  switch (variant_index()) {
+    case 1: launch_warp_v<KN, SM, 4, 4, 128, 2, 5>(a, n_items, s); break;
+    case 2: launch_warp_v<KN, SM, 8, 4, 128, 2, 2>(a, n_items, s); break;
+    case 3: launch_warp_v<KN, SM, 4, 4, 128, 1, 5>(a, n_items, s); break;
+    case 4: launch_warp_v<KN, SM, 4, 4, 256, 2, 4>(a, n_items, s); break;
+    case 5: launch_warp_v<KN, SM, 4, 4, 128, 2, 3>(a, n_items, s); break;
+    default: launch_warp_v<KN, SM, 4, 4, 128, 2, 4>(a, n_items, s); break;
+  }
+}
+
 void dispatch_tile(int kn, int sm, const P2PArgs& a, uint32_t n, cudaStream_t s) {
+  if (use_warp_kernel()) {
+    if (kn == 0) {
+      if (sm == 0) launch_warp<0, 0>(a, n, s);
+      else if (sm == 1) launch_warp<0, 1>(a, n, s);
+      else launch_warp<0, 2>(a, n, s);
+    } else {
+      if (sm == 0) launch_warp<1, 0>(a, n, s);
+      else if (sm == 1) launch_warp<1, 1>(a, n, s);
+      else launch_warp<1, 2>(a, n, s);
+    }
+    return;
+  }
   if (kn == 0) {
     if (sm == 0) launch_tile<0, 0>(a, n, s);
     else if (sm == 1) launch_tile<0, 1>(a, n, s);
@@ -293,23 +385,52 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->mode = j->mode;
   c->delta = j->delta;
 
-  // ---- pinned packing -------------------------------------------------------
+  Trace tr(c);
+  cudaStream_t s = c->stream;
+  CU_TRY(c, c->d_src.ensure(size_t(ns) * 32));
+  CU_TRY(c, c->d_evy.ensure(size_t(ne) * 16));
+  CU_TRY(c, c->d_eself.ensure(size_t(ne) * 4));
+  CU_TRY(c, cudaEventRecord(c->ev_start, s));
+  c->t_evstart = Clock::now();
+
+  // ---- sources: pack 32-byte records into pinned chunks, each chunk's H2D
+  // issued as soon as it is packed (host packing overlaps the PCIe copy) ----
   CU_TRY(c, c->h_src.ensure(size_t(ns) * 32));
   CU_TRY(c, c->h_evy.ensure(size_t(ne) * 16));
   CU_TRY(c, c->h_eself.ensure(size_t(ne) * 4));
   double* hs = c->h_src.as<double>();
   const double* z = j->src_z;
   const double* m = j->src_m;
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < int64_t(ns); ++i) {
-    hs[4 * i + 0] = z[2 * i];
-    hs[4 * i + 1] = z[2 * i + 1];
-    hs[4 * i + 2] = m[2 * i];
-    hs[4 * i + 3] = m[2 * i + 1];
+  // Self layout (EvalSet::self_of with perm == eval_perm): eval e is source
+  // slot e.  Detected while packing; the eval arrays are then derived on the
+  // device instead of uploaded (saves 20 B/eval of PCIe traffic).
+  const bool maybe_self = j->eval_sid && ne == ns && ns > 0;
+  bool self_layout = maybe_self;
+  constexpr int64_t kChunk = 1 << 20;  // sources per pipelined chunk (32 MB)
+  for (int64_t c0 = 0; c0 < int64_t(ns); c0 += kChunk) {
+    const int64_t c1 = std::min<int64_t>(ns, c0 + kChunk);
+    bool same = true;
+#pragma omp parallel for schedule(static) reduction(&& : same)
+    for (int64_t i = c0; i < c1; ++i) {
+      hs[4 * i + 0] = z[2 * i];
+      hs[4 * i + 1] = z[2 * i + 1];
+      hs[4 * i + 2] = m[2 * i];
+      hs[4 * i + 3] = m[2 * i + 1];
+      if (maybe_self)
+        same = same && j->eval_sid[i] == int64_t(j->perm[i]) &&
+               j->eval_y[2 * i] == z[2 * i] && j->eval_y[2 * i + 1] == z[2 * i + 1];
+    }
+    self_layout = self_layout && same;
+    CU_TRY(c, cudaMemcpyAsync(c->d_src.as<double>() + 4 * c0, hs + 4 * c0, size_t(c1 - c0) * 32,
+                              cudaMemcpyHostToDevice, s));
   }
-  if (ne) std::memcpy(c->h_evy.p, j->eval_y, size_t(ne) * 16);
+  tr.mark("pack+h2d sources");
+  c->self_layout = self_layout;
   uint32_t* eself = c->h_eself.as<uint32_t>();
-  if (j->eval_sid && ns > 0) {
+  if (self_layout) {
+    // built on the device after the uploads (p2p_self_evals_kernel)
+  } else if (j->eval_sid && ns > 0) {
+    par_memcpy(c->h_evy.p, j->eval_y, size_t(ne) * 16);
     c->invperm.resize(ns);
     uint32_t* inv = c->invperm.data();
     const uint32_t* perm = j->perm;
@@ -323,12 +444,19 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     const int64_t* sid = j->eval_sid;
 #pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < int64_t(ne); ++e) {
-      const int64_t s = sid[e];
-      eself[e] = (s >= 0 && s < int64_t(ns)) ? inv[s] : kNoSelf;
+      const int64_t sv = sid[e];
+      eself[e] = (sv >= 0 && sv < int64_t(ns)) ? inv[sv] : kNoSelf;
     }
   } else {
-    for (uint32_t e = 0; e < ne; ++e) eself[e] = kNoSelf;
+    par_memcpy(c->h_evy.p, j->eval_y, size_t(ne) * 16);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < int64_t(ne); ++e) eself[e] = kNoSelf;
   }
+  if (!self_layout && ne) {
+    CU_TRY(c, cudaMemcpyAsync(c->d_evy.p, c->h_evy.p, size_t(ne) * 16, cudaMemcpyHostToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(c->d_eself.p, c->h_eself.p, size_t(ne) * 4, cudaMemcpyHostToDevice, s));
+  }
+  tr.mark("evals");
 
   // ---- work list ------------------------------------------------------------
   c->ev_off.assign(j->ev_off, j->ev_off + nl + 1);
@@ -354,7 +482,11 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->item_first.assign(nl + 1, 0);
   c->fin_first.assign(nl + 1, 0);
   uint64_t partial_evals = 0;
-  // Items: eval blocks of <= kMaxEvalsPerItem evals; a block whose pair work
+  const bool warp_kernel = use_warp_kernel();
+  const uint32_t max_ev = warp_kernel ? uint32_t(kWarpMaxEv) : uint32_t(kMaxEvalsPerItem);
+  const uint32_t max_ent = warp_kernel ? uint32_t(kWarpMaxEntries) : 0xFFFFFFFFu;
+  c->warp_items = warp_kernel;
+  // Items: eval blocks of <= max_ev evals; a block whose pair work
   // exceeds the budget is split into strong-list chunks whose partials are
   // summed in chunk order by p2p_finalize_kernel.
   for (uint32_t t = 0; t < nl; ++t) {
@@ -362,11 +494,11 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     c->fin_first[t] = uint32_t(c->fins.size());
     const uint32_t ntl = j->ev_off[t + 1] - j->ev_off[t];
     const uint32_t sb0 = j->strong_off[t], sb1 = j->strong_off[t + 1];
-    for (uint32_t e0 = 0; e0 < ntl; e0 += kMaxEvalsPerItem) {
-      const uint32_t nt = std::min<uint32_t>(kMaxEvalsPerItem, ntl - e0);
+    for (uint32_t e0 = 0; e0 < ntl; e0 += max_ev) {
+      const uint32_t nt = std::min<uint32_t>(max_ev, ntl - e0);
       const uint32_t evb = j->ev_off[t] + e0;
       const uint64_t pairs = uint64_t(nt) * S[t];
-      if (pairs <= budget || sb1 - sb0 <= 1 || S[t] > 0xFFFFFFFFull) {
+      if ((pairs <= budget || sb1 - sb0 <= 1) && sb1 - sb0 <= max_ent && S[t] <= 0xFFFFFFFFull) {
         c->items.push_back(P2PItem{t, evb, nt, sb0, sb1, uint32_t(S[t]), kNoSelf, 0});
         continue;
       }
@@ -377,8 +509,9 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       while (q < sb1) {
         uint32_t q1 = q;
         uint64_t acc = 0;
-        while (q1 < sb1 && (acc == 0 || acc + (j->pt_off[j->strong_idx[q1] + 1] -
-                                               j->pt_off[j->strong_idx[q1]]) <= src_per_chunk)) {
+        while (q1 < sb1 && q1 - q < max_ent &&
+               (acc == 0 || acc + (j->pt_off[j->strong_idx[q1] + 1] -
+                                   j->pt_off[j->strong_idx[q1]]) <= src_per_chunk)) {
           acc += j->pt_off[j->strong_idx[q1] + 1] - j->pt_off[j->strong_idx[q1]];
           ++q1;
         }
@@ -394,10 +527,8 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->fin_first[nl] = uint32_t(c->fins.size());
   if (partial_evals > 0xFFFFFFF0ull) return set_err(c, FMMCU_EINVAL, "partial buffer too large");
 
+  tr.mark("worklist");
   // ---- device buffers -------------------------------------------------------
-  CU_TRY(c, c->d_src.ensure(size_t(ns) * 32));
-  CU_TRY(c, c->d_evy.ensure(size_t(ne) * 16));
-  CU_TRY(c, c->d_eself.ensure(size_t(ne) * 4));
   CU_TRY(c, c->d_pt.ensure(size_t(nl + 1) * 4));
   CU_TRY(c, c->d_ev.ensure(size_t(nl + 1) * 4));
   CU_TRY(c, c->d_soff.ensure(size_t(nl + 1) * 4));
@@ -418,7 +549,7 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   unsigned char* hc = c->h_csr.as<unsigned char>();
   size_t o = 0;
   auto put = [&](const void* src, size_t bytes) {
-    if (bytes) std::memcpy(hc + o, src, bytes);
+    if (bytes) par_memcpy(hc + o, src, bytes);
     const size_t at = o;
     o += bytes;
     return at;
@@ -429,15 +560,8 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const size_t o_si = put(j->strong_idx, size_t(nnz) * 4);
   const size_t o_it = put(c->items.data(), c->items.size() * sizeof(P2PItem));
   const size_t o_fi = put(c->fins.data(), c->fins.size() * sizeof(P2PFinal));
-  c->h2d_bytes = uint64_t(ns) * 32 + uint64_t(ne) * 20 + o;
+  c->h2d_bytes = uint64_t(ns) * 32 + (self_layout ? 0 : uint64_t(ne) * 20) + o;
 
-  cudaStream_t s = c->stream;
-  CU_TRY(c, cudaEventRecord(c->ev_start, s));
-  CU_TRY(c, cudaMemcpyAsync(c->d_src.p, c->h_src.p, size_t(ns) * 32, cudaMemcpyHostToDevice, s));
-  if (ne) {
-    CU_TRY(c, cudaMemcpyAsync(c->d_evy.p, c->h_evy.p, size_t(ne) * 16, cudaMemcpyHostToDevice, s));
-    CU_TRY(c, cudaMemcpyAsync(c->d_eself.p, c->h_eself.p, size_t(ne) * 4, cudaMemcpyHostToDevice, s));
-  }
   CU_TRY(c, cudaMemcpyAsync(c->d_pt.p, hc + o_pt, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
   CU_TRY(c, cudaMemcpyAsync(c->d_ev.p, hc + o_ev, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
   CU_TRY(c, cudaMemcpyAsync(c->d_soff.p, hc + o_so, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
@@ -449,18 +573,24 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     CU_TRY(c, cudaMemcpyAsync(c->d_fin.p, hc + o_fi, c->fins.size() * sizeof(P2PFinal),
                               cudaMemcpyHostToDevice, s));
   if (nnz) {
-    if (ne) {
-      p2p_evrec_kernel<<<(ne + 255) / 256, 256, 0, s>>>(c->d_evy.as<double2>(),
-                                                        c->d_eself.as<uint32_t>(), ne,
-                                                        c->d_evr.as<double4>());
-      c->launches += 1;
-    }
     p2p_segments_kernel<<<(nnz + 255) / 256, 256, 0, s>>>(c->d_sidx.as<uint32_t>(),
                                                           c->d_pt.as<uint32_t>(), nnz,
                                                           c->d_seg.as<uint2>());
-    CU_TRY(c, cudaGetLastError());
     c->launches += 1;
   }
+  if (ne) {
+    if (self_layout) {
+      p2p_self_evals_kernel<<<(ne + 255) / 256, 256, 0, s>>>(c->d_src.as<double4>(), ne,
+                                                             c->d_evy.as<double2>(),
+                                                             c->d_eself.as<uint32_t>());
+      c->launches += 1;
+    }
+    // eval records {x, y, self slot, strong entry of the self slot}; needs seg
+    p2p_evrec_kernel<<<(nl + 7) / 8, 256, 0, s>>>(make_args(c), nl, c->d_evr.as<double4>());
+    c->launches += 1;
+  }
+  CU_TRY(c, cudaGetLastError());
+  tr.mark("csr+worklist h2d");
   c->staged = true;
   return FMMCU_OK;
 }
@@ -636,7 +766,9 @@ int fmmcu_p2p_launch(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->run_lb = j->leaf_begin;
   c->run_le = j->leaf_end;
   c->run_total_pairs = c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
-  c->prep_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  // busy time = host work before the first device operation + device span
+  // (ev_start .. ev_end covers packing-overlapped uploads, kernels, D2H)
+  c->prep_seconds = std::chrono::duration<double>(c->t_evstart - t0).count();
   c->inflight = true;
   return FMMCU_OK;
 }
@@ -651,7 +783,7 @@ int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
   float ms = 0.f;
   CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_start, c->ev_end));
   const uint32_t eb = c->ev_off[c->run_lb], ee = c->ev_off[c->run_le];
-  if (ee > eb) std::memcpy(c->job.out + 2 * size_t(eb), c->h_out.as<double2>() + eb, size_t(ee - eb) * 16);
+  if (ee > eb) par_memcpy(c->job.out + 2 * size_t(eb), c->h_out.as<double2>() + eb, size_t(ee - eb) * 16);
   const uint64_t hits = *c->h_hits.as<unsigned long long>();
   if (pair_evals) *pair_evals = c->run_total_pairs - hits;
   if (seconds) *seconds = c->prep_seconds + 1e-3 * double(ms);

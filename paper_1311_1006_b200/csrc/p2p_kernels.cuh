@@ -159,6 +159,36 @@ __device__ __forceinline__ void pair_accum(double yx, double yy, const double4 s
   }
 }
 
+// Sources p, p+K, p+2K, ... < end without the self test: blocks of U
+// independent sources with no branch inside a block (so the compiler
+// interleaves the U*E pair chains), then a tail.  Per eval the accumulation
+// order is still ascending in the source position.
+template <int KERNEL, int SMOOTH, int E, int U>
+__device__ __forceinline__ const double4* run_unchecked(const double4* p, const double4* end,
+                                                        uint32_t K, const double* yx,
+                                                        const double* yy, double inv_d2, double d2,
+                                                        double* ar, double* ai) {
+  const ptrdiff_t step = ptrdiff_t(K);
+  while (p + (U - 1) * step < end) {
+    double4 s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[u] = p[u * step];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s[u], inv_d2, d2, true, ar[e], ai[e]);
+    p += U * step;
+  }
+  for (; p < end; p += step) {
+    const double4 s = *p;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, inv_d2, d2, true, ar[e], ai[e]);
+  }
+  return p;
+}
+
 // seg[q] = (first permuted source slot, source count) of strong entry q.
 __global__ void p2p_segments_kernel(const uint32_t* __restrict__ s_idx,
                                     const uint32_t* __restrict__ pt_off, uint32_t nnz,
@@ -174,23 +204,51 @@ __global__ void p2p_segments_kernel(const uint32_t* __restrict__ s_idx,
 constexpr int kMaxSeg = 128;  // source runs per tile
 
 // ------------------------------------------------------------ fast kernel --
-// Eval record as staged on the device: {x, y, self slot (bits), 0}.
-__global__ void p2p_evrec_kernel(const double2* __restrict__ evy,
-                                 const uint32_t* __restrict__ eself, uint32_t n,
-                                 double4* __restrict__ evr) {
+// Eval record as staged on the device: {x, y, self slot (bits), q_self (bits)}
+// where q_self is the global strong-entry index (position in strong_idx) of
+// the eval's own leaf's entry whose source run holds the self slot, or
+// kNoSelf -- this makes the per-tile self lookup O(1).
+__device__ __forceinline__ uint32_t find_self_entry(const P2PArgs& a, uint32_t leaf,
+                                                    uint32_t self) {
+  if (self == kNoSelf) return kNoSelf;
+  for (uint32_t q = a.s_off[leaf]; q < a.s_off[leaf + 1]; ++q) {
+    const uint2 sg = a.seg[q];
+    if (self - sg.x < sg.y) return q;
+  }
+  return kNoSelf;
+}
+
+// One warp per leaf, lanes over its evals.
+__global__ void p2p_evrec_kernel(const P2PArgs a, uint32_t n_leaves, double4* __restrict__ evr) {
+  const uint32_t leaf = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (leaf >= n_leaves) return;
+  for (uint32_t e = a.ev_off[leaf] + (threadIdx.x & 31); e < a.ev_off[leaf + 1]; e += 32) {
+    const double2 y = a.evy[e];
+    const uint32_t self = a.eself[e];
+    const uint32_t q = find_self_entry(a, leaf, self);
+    evr[e] = make_double4(y.x, y.y, __longlong_as_double((long long)self),
+                          __longlong_as_double((long long)q));
+  }
+}
+
+// Self layout (eval e == source slot e): derive the eval arrays from the
+// already uploaded sources instead of uploading them.
+__global__ void p2p_self_evals_kernel(const double4* __restrict__ src, uint32_t n,
+                                      double2* __restrict__ evy, uint32_t* __restrict__ eself) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
-    const double2 y = evy[i];
-    evr[i] = make_double4(y.x, y.y, __longlong_as_double((long long)eself[i]), 0.0);
+    const double4 s = src[i];
+    evy[i] = make_double2(s.x, s.y);
+    eself[i] = i;
   }
 }
 
 // Dynamic smem: [2 mbarriers | pad to 128][src tile 0][src tile 1]
 //               [eval tile 0][eval tile 1][reduction 0][reduction 1]
-template <int KERNEL, int SMOOTH, int E, int THREADS, int TILE, int MAXEV, int U, bool PRODUCER>
-__global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
-  // PRODUCER: warp 0 only stages tiles (its global-latency chain never delays
-  // the consumers' tile barrier); otherwise warp 0 stages and computes.
+template <int KERNEL, int SMOOTH, int E, int THREADS, int TILE, int MAXEV, int U, bool PRODUCER,
+          int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) p2p_tile_kernel(const P2PArgs a) {
+  // PRODUCER: warp 0 only stages tiles; otherwise warp 0 stages and computes.
   constexpr int TC = PRODUCER ? THREADS - 32 : THREADS;  // consumer threads
   static_assert(TILE % 32 == 0 && MAXEV <= TC * E, "shape");
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -198,10 +256,12 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
   double4* tiles = reinterpret_cast<double4*>(smem_raw + 128);
   double4* evt = tiles + 2 * TILE;
   double2* red = reinterpret_cast<double2*>(evt + 2 * MAXEV);
+  // run r of a tile = strong entry q0 + r (runs are 1:1 with entries,
+  // empty leaves give empty runs)
   __shared__ uint32_t seg_gbeg[2][kMaxSeg];
   __shared__ uint32_t seg_tpos[2][kMaxSeg + 1];
   __shared__ uint32_t meta_item[2], meta_nseg[2], meta_flags[2], meta_ev[2], meta_nt[2],
-      meta_poff[2];
+      meta_poff[2], meta_q0[2];
   __shared__ unsigned int s_hits;
 
   const int tid = threadIdx.x;
@@ -212,19 +272,20 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
   // ---- producer state (warp 0, warp-uniform registers) ----------------------
   uint32_t st_item = kNoSelf, st_ent = 0, st_off = 0, st_end = 0, st_left = 0;
   uint32_t st_ev = 0, st_nt = 0, st_poff = kNoSelf;
+  // lane 0 of warp 0 claims the next item id one item ahead, so the atomic's
+  // latency is hidden behind a whole item of compute
+  uint32_t claim = 0;
+  if (tid == 0) claim = atomicAdd(a.next_item, 1u);
 
-  // Builds the next tile into buffer `b` (run list + TMA copies; on an
-  // item's first tile also its eval records).  All 32 lanes of warp 0.
   auto stage = [&](int b) {
     uint32_t flags = 0;
-    if (st_left == 0) {  // current item exhausted: fetch the next one
-      uint32_t nxt = 0;
-      if (lane == 0) nxt = atomicAdd(a.next_item, 1u);
-      nxt = __shfl_sync(FULL, nxt, 0);
+    if (st_left == 0) {  // current item exhausted: take the claimed one, claim another
+      const uint32_t nxt = __shfl_sync(FULL, claim, 0);
       if (nxt >= a.n_items) {
         if (lane == 0) meta_item[b] = kNoSelf;
         return;
       }
+      if (lane == 0) claim = atomicAdd(a.next_item, 1u);
       const P2PItem it = a.items[nxt];
       st_item = nxt;
       st_ent = it.s_begin;
@@ -236,6 +297,7 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
       st_poff = it.partial_off;
       flags |= 1u;
     }
+    const uint32_t q0 = st_ent;
     uint32_t filled = 0, nseg = 0;
     while (filled < TILE && st_ent < st_end && nseg + 32 <= kMaxSeg) {
       const uint32_t q = st_ent + lane;
@@ -254,14 +316,14 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
       }
       const uint32_t excl = incl - n;
       const uint32_t room = TILE - filled;
-      const uint32_t take = excl >= room ? 0u : min(n, room - excl);
-      const unsigned has = __ballot_sync(FULL, take > 0);
-      if (take > 0) {
-        const uint32_t pos = nseg + __popc(has & ((1u << lane) - 1u));
-        seg_gbeg[b][pos] = b0;
-        seg_tpos[b][pos] = filled + excl;
+      const bool in = valid && excl < room;  // a prefix of the lanes
+      const uint32_t take = in ? min(n, room - excl) : 0u;
+      if (in) {
+        seg_gbeg[b][nseg + lane] = b0;
+        seg_tpos[b][nseg + lane] = filled + excl;
       }
       const unsigned part = __ballot_sync(FULL, valid && take < n);
+      const uint32_t n_in = __popc(__ballot_sync(FULL, in));
       const uint32_t total = __shfl_sync(FULL, incl, 31);
       const uint32_t got = min(total, room);
       if (part == 0) {
@@ -274,7 +336,7 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
         st_ent += uint32_t(L);
       }
       filled += got;
-      nseg += uint32_t(__popc(has));
+      nseg += n_in;
       st_left -= got;
     }
     if (st_left == 0) flags |= 2u;
@@ -287,6 +349,7 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
       meta_ev[b] = st_ev;
       meta_nt[b] = st_nt;
       meta_poff[b] = st_poff;
+      meta_q0[b] = q0;
       fence_proxy_async();
       mbar_expect_tx(&bar[b], filled * 32u + ev_bytes);
       if (ev_bytes) bulk_g2s(evt + b * MAXEV, a.evr + st_ev, ev_bytes, &bar[b]);
@@ -295,7 +358,8 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
     for (uint32_t s = lane; s < nseg; s += 32) {
       const uint32_t t0 = seg_tpos[b][s];
       const uint32_t t1 = seg_tpos[b][s + 1];
-      bulk_g2s(tiles + b * TILE + t0, a.src + seg_gbeg[b][s], (t1 - t0) * 32u, &bar[b]);
+      if (t1 > t0)
+        bulk_g2s(tiles + b * TILE + t0, a.src + seg_gbeg[b][s], (t1 - t0) * 32u, &bar[b]);
     }
   };
 
@@ -314,20 +378,23 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
   uint32_t nt = 0, G = 1, K = 1, g = 0, k = 0, ev0 = 0, poff = kNoSelf;
   bool active = false;
   double yx[E], yy[E], ar[E], ai[E];
-  uint32_t sg[E];
+  uint32_t sg[E], sq[E];
   unsigned int hits = 0;
-  // pending reduction of the previous item (deferred by one tile: no extra barrier)
+  // pending reduction of the previous item (deferred by one tile: no extra
+  // barrier), done by the highest warps (warp 0 also stages)
   uint32_t r_nt = 0, r_G = 1, r_K = 1, r_ev0 = 0, r_poff = kNoSelf, r_buf = 0, items_done = 0;
   bool r_pending = false;
 
   const int ctid = PRODUCER ? tid - 32 : tid;  // consumer index (< 0: producer warp)
   auto reduce_pending = [&]() {
     const double2* rb = red + r_buf * (TC * E);
-    for (uint32_t le = uint32_t(ctid); ctid >= 0 && le < r_nt; le += TC) {
+    const int rt = THREADS - 1 - tid;  // highest threads first
+    for (uint32_t le = uint32_t(rt); le < r_nt; le += THREADS) {
       const uint32_t gg = le / E, ee = le % E;
+      const double2* p = rb + ee * r_K * r_G + gg;
       double sr = 0.0, si = 0.0;
-      for (uint32_t kk = 0; kk < r_K; ++kk) {
-        const double2 v = rb[(ee * r_K + kk) * r_G + gg];
+      for (uint32_t kk = 0; kk < r_K; ++kk, p += r_G) {
+        const double2 v = *p;
         sr += v.x;
         si += v.y;
       }
@@ -346,14 +413,16 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
     if (item == kNoSelf) break;
     const uint32_t flags = meta_flags[b];
     const uint32_t nseg = meta_nseg[b];
-    if (flags & 1u) {  // first tile of an item: thread roles
+    const uint32_t q0 = meta_q0[b];
+    if (flags & 1u) {  // first tile of an item: thread roles (no integer division)
       nt = meta_nt[b];
       ev0 = meta_ev[b];
       poff = meta_poff[b];
-      G = (nt + E - 1) / E;  // host guarantees nt <= MAXEV <= E * TC
-      K = TC / G;
-      g = uint32_t(ctid) % G;
-      k = uint32_t(ctid) / G;
+      G = (nt + E - 1) / E;  // E is a power of two; host guarantees nt <= MAXEV <= E * TC
+      const float rG = 1.0f / float(G);
+      K = uint32_t(float(TC) * rG + 1e-4f);
+      k = uint32_t((float(ctid) + 0.5f) * rG);
+      g = uint32_t(ctid) - k * G;
       active = ctid >= 0 && k < K;
     }
     if (warp == 0) stage(b ^ 1);  // next tile streams in while this one is computed
@@ -371,67 +440,53 @@ __global__ void __launch_bounds__(THREADS) p2p_tile_kernel(const P2PArgs a) {
         yx[e] = r.x;
         yy[e] = r.y;
         sg[e] = ok ? uint32_t(__double_as_longlong(r.z)) : kNoSelf;
+        sq[e] = ok ? uint32_t(__double_as_longlong(r.w)) : kNoSelf;
         ar[e] = 0.0;
         ai[e] = 0.0;
       }
     }
 
-    // tile position of each eval's own source (runs ascend in source slot)
+    // O(1) tile position of each eval's own source: its entry's run r = q - q0
     const uint32_t ntile = seg_tpos[b][nseg];
     uint32_t ps[E];
     uint32_t plo = kNoSelf, phi = 0u;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       ps[e] = kNoSelf;
-      const uint32_t s = sg[e];
-      if (s != kNoSelf && nseg > 0 && s >= seg_gbeg[b][0]) {
-        uint32_t lo = 0, hi = nseg;
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (seg_gbeg[b][mid] <= s) lo = mid; else hi = mid;
-        }
-        const uint32_t len = seg_tpos[b][lo + 1] - seg_tpos[b][lo];
-        if (s - seg_gbeg[b][lo] < len) {
-          ps[e] = seg_tpos[b][lo] + (s - seg_gbeg[b][lo]);
+      const uint32_t r = sq[e] - q0;
+      if (sq[e] != kNoSelf && r < nseg) {
+        const uint32_t d = sg[e] - seg_gbeg[b][r];
+        const uint32_t t0 = seg_tpos[b][r];
+        if (d < seg_tpos[b][r + 1] - t0) {
+          ps[e] = t0 + d;
           plo = min(plo, ps[e]);
           phi = max(phi, ps[e]);
         }
       }
     }
-    // Self pairs of this warp can only sit at tile positions [plo, phi]
-    // (the target leaf's own run for self-evaluation): only that stretch of
-    // the source loop pays for the per-pair exclusion test.
+    // Self pairs of this warp sit at tile positions [plo, phi] (the target
+    // leaf's own run for self-evaluation): only that stretch pays for the
+    // per-pair exclusion test.
     plo = __reduce_min_sync(FULL, plo);
     phi = __reduce_max_sync(FULL, phi);
 
-    const double4* tile = tiles + b * TILE;
     if (active) {
-      uint32_t j = k;
-      const uint32_t end1 = min(plo, ntile);
-#pragma unroll U
-      for (; j < end1; j += K) {
-        const double4 s = tile[j];
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-          pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, true, ar[e], ai[e]);
-      }
+      const double4* tile = tiles + b * TILE;
+      const double4* p = tile + k;
+      const double4* const end1 = tile + min(plo, ntile);
+      const double4* const end = tile + ntile;
+      p = run_unchecked<KERNEL, SMOOTH, E, U>(p, end1, K, yx, yy, a.inv_delta2, a.delta2, ar, ai);
       if (plo != kNoSelf) {
-        const uint32_t end2 = min(phi + 1u, ntile);
-        for (; j < end2; j += K) {
-          const double4 s = tile[j];
+        const double4* const end2 = tile + min(phi + 1u, ntile);
+        for (; p < end2; p += K) {
+          const double4 s = *p;
+          const uint32_t j = uint32_t(p - tile);
 #pragma unroll
           for (int e = 0; e < E; ++e)
             pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, j != ps[e], ar[e],
                                        ai[e]);
         }
-#pragma unroll U
-        for (; j < ntile; j += K) {
-          const double4 s = tile[j];
-#pragma unroll
-          for (int e = 0; e < E; ++e)
-            pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, true, ar[e],
-                                       ai[e]);
-        }
+        run_unchecked<KERNEL, SMOOTH, E, U>(p, end, K, yx, yy, a.inv_delta2, a.delta2, ar, ai);
         // each skipped self pair is seen by exactly one source lane
 #pragma unroll
         for (int e = 0; e < E; ++e) hits += (ps[e] != kNoSelf && ps[e] % K == k) ? 1u : 0u;
