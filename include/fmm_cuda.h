@@ -112,6 +112,12 @@ int fmmcu_p2p_launch(fmmcu_ctx *ctx, const fmmcu_p2p_job *job);
  * reference counting) and seconds (launch start -> results on host). */
 int fmmcu_p2p_finish(fmmcu_ctx *ctx, uint64_t *pair_evals, double *seconds);
 
+/* Page-lock caller memory (cudaHostRegister).  When job->out of
+ * fmmcu_p2p_launch is page-locked, the potentials are copied straight into it
+ * slice by slice instead of through pinned staging + a host copy in finish. */
+int fmmcu_host_register(fmmcu_ctx *ctx, void *ptr, uint64_t bytes);
+int fmmcu_host_unregister(fmmcu_ctx *ctx, void *ptr);
+
 /* ---- device-resident near field (benchmarks, multi-GPU sharding) -------- */
 /* Uploads and packs the job's inputs once (synchronous); they stay resident. */
 int fmmcu_p2p_stage(fmmcu_ctx *ctx, const fmmcu_p2p_job *job);

@@ -99,7 +99,7 @@ CUDA_SYMBOLS = [
     "fmmcu_p2p_launch", "fmmcu_p2p_finish", "fmmcu_p2p_stage", "fmmcu_p2p_run_staged",
     "fmmcu_p2p_device_out", "fmmcu_p2p_bind_device_out", "fmmcu_p2p_copy_out", "fmmcu_p2p_pairs", "fmmcu_p2p_work_prefix", "fmmcu_set_stream",
     "fmmcu_synchronize", "fmmcu_m2l_launch", "fmmcu_m2l_finish", "fmmcu_kernel_launches",
-    "fmmcu_fp64_peak", "fmmcu_last_transfer_bytes",
+    "fmmcu_fp64_peak", "fmmcu_last_transfer_bytes", "fmmcu_host_register", "fmmcu_host_unregister",
 ]
 
 
@@ -127,6 +127,8 @@ def cuda_lib():
         lib.fmmcu_p2p_pairs.argtypes = [vp, C.POINTER(C.c_uint64)]
         lib.fmmcu_p2p_work_prefix.argtypes = [vp, vp]
         lib.fmmcu_set_stream.argtypes = [vp, vp]
+        lib.fmmcu_host_register.argtypes = [vp, vp, C.c_uint64]
+        lib.fmmcu_host_unregister.argtypes = [vp, vp]
         lib.fmmcu_synchronize.argtypes = [vp]
         lib.fmmcu_m2l_launch.argtypes = [vp, C.POINTER(M2LJob)]
         lib.fmmcu_m2l_finish.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
@@ -266,6 +268,13 @@ class CudaContext:
 
     def set_stream(self, stream_handle: int | None):
         self._check(self.lib.fmmcu_set_stream(self.h, C.c_void_p(stream_handle or 0)))
+
+    def host_register(self, arr: np.ndarray):
+        """Page-lock a host array (cudaHostRegister) so D2H lands in it directly."""
+        self._check(self.lib.fmmcu_host_register(self.h, arr.ctypes.data, arr.nbytes))
+
+    def host_unregister(self, arr: np.ndarray):
+        self._check(self.lib.fmmcu_host_unregister(self.h, arr.ctypes.data))
 
     def synchronize(self):
         self._check(self.lib.fmmcu_synchronize(self.h))

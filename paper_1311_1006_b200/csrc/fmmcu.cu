@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <new>
 #include <string>
 #include <vector>
@@ -137,6 +138,12 @@ struct fmmcu_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // current (own or external)
   cudaStream_t m2l_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr;  // potentials D2H, overlapping the next slice's kernels
+  static constexpr int kMaxSlices = 8;
+  cudaEvent_t ev_kslice[kMaxSlices] = {}, ev_cslice[kMaxSlices] = {};
+  int n_slices = 0;
+  uint32_t slice_eb[kMaxSlices + 1] = {};
+  bool direct_out = false;  // job->out is page-locked: D2H lands in it directly
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_m2l0 = nullptr, ev_m2l1 = nullptr;
   std::string err;
   uint64_t launches = 0;
@@ -160,6 +167,8 @@ struct fmmcu_ctx {
   bool staged = false;
   bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
   bool warp_items = false;     // work list built for p2p_warp_kernel
+  int warp_e = 4;              // evals per lane of the warp kernel (choose_warp_e)
+  uint64_t partial_evals = 0;  // partial-sum slots of split items
   bool trace = std::getenv("FMMCU_TRACE") != nullptr;
   double2* ext_out = nullptr;  // caller-bound output (torch tensor), or null
   double2* out_ptr() const { return ext_out ? ext_out : d_out.as<double2>(); }
@@ -289,31 +298,43 @@ void launch_warp_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
   kfn<<<grid, W * 32, smem, s>>>(a);
 }
 
-// warp-kernel variants (warps/CTA, evals/lane, chunk, unroll, min CTAs/SM):
-//   0 = 4w E4 c128 u2 m4   1 = 4w E4 c128 u2 m5   2 = 8w E4 c128 u2 m2
-//   3 = 4w E4 c128 u1 m5   4 = 4w E4 c256 u2 m4   5 = 4w E4 c128 u2 m3
-template <int KN, int SM>
-void launch_warp(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
-  switch (variant_index()) {
-    case 1: launch_warp_v<KN, SM, 4, 4, 128, 2, 5>(a, n_items, s); break;
-    case 2: launch_warp_v<KN, SM, 8, 4, 128, 2, 2>(a, n_items, s); break;
-    case 3: launch_warp_v<KN, SM, 4, 4, 128, 1, 5>(a, n_items, s); break;
-    case 4: launch_warp_v<KN, SM, 4, 4, 256, 2, 4>(a, n_items, s); break;
-    case 5: launch_warp_v<KN, SM, 4, 4, 128, 2, 3>(a, n_items, s); break;
-    default: launch_warp_v<KN, SM, 4, 4, 128, 2, 4>(a, n_items, s); break;
+// warp-kernel variants (warps/CTA, chunk, unroll, min CTAs/SM) for the hot
+// instantiation (harmonic, no smoother); E (evals per lane) is chosen per
+// staged job by choose_warp_e():
+//   0 = 4w c128 u2(E4)/u1(E5) m4   1 = 4w c128 u2 m3   2 = 4w c128 u1 m5
+//   3 = 8w c128 u1 m2              4 = 4w c256 u1 m4   5 = 4w c128 u2 m4
+template <int KN, int SM, int E>
+void launch_warp_e(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
+  constexpr int U0 = E >= 5 ? 1 : 2;
+  if (KN == 0 && SM == 0) {
+    switch (variant_index()) {
+      case 1: launch_warp_v<KN, SM, 4, E, 128, 2, 3>(a, n_items, s); return;
+      case 2: launch_warp_v<KN, SM, 4, E, 128, 1, 5>(a, n_items, s); return;
+      case 3: launch_warp_v<KN, SM, 8, E, 128, 1, 2>(a, n_items, s); return;
+      case 4: launch_warp_v<KN, SM, 4, E, 256, 1, 4>(a, n_items, s); return;
+      case 5: launch_warp_v<KN, SM, 4, E, 128, 2, 4>(a, n_items, s); return;
+      default: break;
+    }
   }
+  launch_warp_v<KN, SM, 4, E, 128, U0, 4>(a, n_items, s);
 }
 
-void dispatch_tile(int kn, int sm, const P2PArgs& a, uint32_t n, cudaStream_t s) {
+template <int KN, int SM>
+void launch_warp(const P2PArgs& a, uint32_t n_items, cudaStream_t s, int E) {
+  if (E == 5) launch_warp_e<KN, SM, 5>(a, n_items, s);
+  else launch_warp_e<KN, SM, 4>(a, n_items, s);
+}
+
+void dispatch_tile(int kn, int sm, const P2PArgs& a, uint32_t n, cudaStream_t s, int E) {
   if (use_warp_kernel()) {
     if (kn == 0) {
-      if (sm == 0) launch_warp<0, 0>(a, n, s);
-      else if (sm == 1) launch_warp<0, 1>(a, n, s);
-      else launch_warp<0, 2>(a, n, s);
+      if (sm == 0) launch_warp<0, 0>(a, n, s, E);
+      else if (sm == 1) launch_warp<0, 1>(a, n, s, E);
+      else launch_warp<0, 2>(a, n, s, E);
     } else {
-      if (sm == 0) launch_warp<1, 0>(a, n, s);
-      else if (sm == 1) launch_warp<1, 1>(a, n, s);
-      else launch_warp<1, 2>(a, n, s);
+      if (sm == 0) launch_warp<1, 0>(a, n, s, E);
+      else if (sm == 1) launch_warp<1, 1>(a, n, s, E);
+      else launch_warp<1, 2>(a, n, s, E);
     }
     return;
   }
@@ -358,16 +379,159 @@ int validate(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     return set_err(c, FMMCU_EINVAL, "pt_off does not span the sources");
   if (j->ev_off[0] != 0 || j->ev_off[nl] != j->n_eval)
     return set_err(c, FMMCU_EINVAL, "ev_off does not span the evals");
-  for (uint32_t i = 0; i < nl; ++i)
-    if (j->pt_off[i] > j->pt_off[i + 1] || j->ev_off[i] > j->ev_off[i + 1] ||
-        j->strong_off[i] > j->strong_off[i + 1])
-      return set_err(c, FMMCU_EINVAL, "leaf offsets not monotone");
+  bool mono = true;
+#pragma omp parallel for schedule(static) reduction(&& : mono)
+  for (int64_t i = 0; i < int64_t(nl); ++i)
+    mono = mono && j->pt_off[i] <= j->pt_off[i + 1] && j->ev_off[i] <= j->ev_off[i + 1] &&
+           j->strong_off[i] <= j->strong_off[i + 1];
+  if (!mono) return set_err(c, FMMCU_EINVAL, "leaf offsets not monotone");
   const uint32_t nnz = j->strong_off[nl];
   if (nnz > 0 && !j->strong_idx) return set_err(c, FMMCU_EINVAL, "null strong list");
-  for (uint32_t s = 0; s < nnz; ++s)
-    if (j->strong_idx[s] >= nl) return set_err(c, FMMCU_EINVAL, "strong index out of range");
+  bool in_range = true;
+#pragma omp parallel for schedule(static) reduction(&& : in_range)
+  for (int64_t q = 0; q < int64_t(nnz); ++q) in_range = in_range && j->strong_idx[q] < nl;
+  if (!in_range) return set_err(c, FMMCU_EINVAL, "strong index out of range");
   if (j->leaf_begin > j->leaf_end || j->leaf_end > nl)
     return set_err(c, FMMCU_EINVAL, "bad leaf shard");
+  return FMMCU_OK;
+}
+
+// Evals per lane of the warp kernel.  An eval block of nt <= 8E evals runs
+// as G = ceil(nt/E) eval slots x K = floor(32/G) source lanes; a lane sweeps
+// S/K sources for E evals, so the block costs ~ E * S / K lane-pair slots
+// for nt * S / 32 useful ones.  Pick the E with the least modelled cost over
+// the job's leaves (38-39 evals/leaf -> E = 5: 8 x 4 lanes, 95% useful,
+// against 89% for E = 4).  FMMCU_P2P_E overrides.
+int choose_warp_e(const uint32_t* ev_off, const std::vector<uint64_t>& S, uint32_t nl) {
+  if (const char* env = std::getenv("FMMCU_P2P_E")) {
+    const int e = std::atoi(env);
+    if (e == 4 || e == 5) return e;
+  }
+  double best_cost = 0.0;
+  int best = 4;
+  for (int E : {4, 5}) {
+    const uint32_t max_ev = uint32_t(kWarpSlots * E);
+    double cost = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : cost)
+    for (int64_t t = 0; t < int64_t(nl); ++t) {
+      const uint32_t ntl = ev_off[t + 1] - ev_off[t];
+      if (!ntl || !S[t]) continue;
+      const uint32_t nblk = (ntl + max_ev - 1) / max_ev;
+      const uint32_t nt = (ntl + nblk - 1) / nblk;
+      const uint32_t G = (nt + E - 1) / E;
+      const uint32_t K = 32 / G;
+      cost += double(nblk) * double(E) * double((S[t] + K - 1) / K);
+    }
+    if (E == 4 || cost < best_cost) {
+      best_cost = cost;
+      best = E;
+    }
+  }
+  return best;
+}
+
+// Work list of a job (host, OpenMP): per-leaf pair work and its prefix,
+// evals-per-lane choice, and the item / finalize lists.  Touches only the
+// job's CSR and host-side context fields, so it runs on a helper thread
+// while the main thread packs and uploads the sources.
+int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  const uint32_t nl = j->n_leaves;
+  c->ev_off.assign(j->ev_off, j->ev_off + nl + 1);
+  c->leaf_work.assign(nl + 1, 0);
+  std::vector<uint64_t> S(nl, 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < int64_t(nl); ++t) {
+    uint64_t s = 0;
+    for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q) {
+      const uint32_t sb = j->strong_idx[q];
+      s += j->pt_off[sb + 1] - j->pt_off[sb];
+    }
+    S[t] = s;
+  }
+  uint64_t total = 0;
+  for (uint32_t t = 0; t < nl; ++t) {
+    total += uint64_t(j->ev_off[t + 1] - j->ev_off[t]) * S[t];
+    c->leaf_work[t + 1] = total;
+  }
+  const uint64_t budget = std::max<uint64_t>(1ull << 16, total / (148ull * 16ull));
+  const bool warp_kernel = use_warp_kernel();
+  c->warp_e = warp_kernel ? choose_warp_e(j->ev_off, S, nl) : 4;
+  const uint32_t max_ev = warp_kernel ? uint32_t(kWarpSlots * c->warp_e) : uint32_t(kMaxEvalsPerItem);
+  const uint32_t max_ent = warp_kernel ? uint32_t(kWarpMaxEntries) : 0xFFFFFFFFu;
+  c->warp_items = warp_kernel;
+  // Items: eval blocks of <= max_ev evals (balanced: ceil(ntl / max_ev)
+  // blocks of near-equal size); a block whose pair work exceeds the budget is
+  // split into strong-list chunks whose partials are summed in chunk order by
+  // p2p_finalize_kernel.  Two parallel passes over the leaves (count, then
+  // fill at prefix offsets) give the same list as a serial build.
+  struct LeafCount {
+    uint32_t items, fins, pevals;
+  };
+  auto leaf_items = [&](uint32_t t, P2PItem* it, P2PFinal* fin, uint32_t pbase) {
+    LeafCount n{0, 0, 0};
+    const uint32_t ntl = j->ev_off[t + 1] - j->ev_off[t];
+    const uint32_t sb0 = j->strong_off[t], sb1 = j->strong_off[t + 1];
+    const uint32_t nblk = (ntl + max_ev - 1) / max_ev;
+    for (uint32_t b = 0, e0 = 0; b < nblk; ++b) {
+      const uint32_t nt = (ntl - e0) / (nblk - b) + ((ntl - e0) % (nblk - b) ? 1u : 0u);
+      const uint32_t evb = j->ev_off[t] + e0;
+      e0 += nt;
+      const uint64_t pairs = uint64_t(nt) * S[t];
+      if ((pairs <= budget || sb1 - sb0 <= 1) && sb1 - sb0 <= max_ent && S[t] <= 0xFFFFFFFFull) {
+        if (it) it[n.items] = P2PItem{t, evb, nt, sb0, sb1, uint32_t(S[t]), kNoSelf, 0};
+        ++n.items;
+        continue;
+      }
+      const uint64_t src_per_chunk = std::max<uint64_t>(1, budget / nt);
+      const uint32_t base = pbase + n.pevals;
+      uint32_t n_chunks = 0;
+      uint32_t q = sb0;
+      while (q < sb1) {
+        uint32_t q1 = q;
+        uint64_t acc = 0;
+        while (q1 < sb1 && q1 - q < max_ent &&
+               (acc == 0 || acc + (j->pt_off[j->strong_idx[q1] + 1] -
+                                   j->pt_off[j->strong_idx[q1]]) <= src_per_chunk)) {
+          acc += j->pt_off[j->strong_idx[q1] + 1] - j->pt_off[j->strong_idx[q1]];
+          ++q1;
+        }
+        if (it) it[n.items] = P2PItem{t, evb, nt, q, q1, uint32_t(acc), pbase + n.pevals, 0};
+        ++n.items;
+        n.pevals += nt;
+        ++n_chunks;
+        q = q1;
+      }
+      if (fin) fin[n.fins] = P2PFinal{evb, nt, base, n_chunks};
+      ++n.fins;
+    }
+    return n;
+  };
+  std::vector<uint32_t> pev_first(nl + 1, 0);
+  c->item_first.assign(nl + 1, 0);
+  c->fin_first.assign(nl + 1, 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < int64_t(nl); ++t) {
+    const LeafCount n = leaf_items(uint32_t(t), nullptr, nullptr, 0);
+    c->item_first[t + 1] = n.items;
+    c->fin_first[t + 1] = n.fins;
+    pev_first[t + 1] = n.pevals;
+  }
+  uint64_t partial_evals = 0;
+  for (uint32_t t = 0; t < nl; ++t) {
+    c->item_first[t + 1] += c->item_first[t];
+    c->fin_first[t + 1] += c->fin_first[t];
+    partial_evals += pev_first[t + 1];
+    pev_first[t + 1] = uint32_t(std::min<uint64_t>(partial_evals, 0xFFFFFFFFull));
+  }
+  if (partial_evals > 0xFFFFFFF0ull) return set_err(c, FMMCU_EINVAL, "partial buffer too large");
+  c->partial_evals = partial_evals;
+  c->items.resize(c->item_first[nl]);
+  c->fins.resize(c->fin_first[nl]);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < int64_t(nl); ++t)
+    leaf_items(uint32_t(t), c->items.data() + c->item_first[t], c->fins.data() + c->fin_first[t],
+               pev_first[t]);
+
   return FMMCU_OK;
 }
 
@@ -386,6 +550,8 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->delta = j->delta;
 
   Trace tr(c);
+  std::future<int> worklist =
+      std::async(std::launch::async, [c, j] { return build_worklist(c, j); });
   cudaStream_t s = c->stream;
   CU_TRY(c, c->d_src.ensure(size_t(ns) * 32));
   CU_TRY(c, c->d_evy.ensure(size_t(ne) * 16));
@@ -458,75 +624,8 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   }
   tr.mark("evals");
 
-  // ---- work list ------------------------------------------------------------
-  c->ev_off.assign(j->ev_off, j->ev_off + nl + 1);
-  c->leaf_work.assign(nl + 1, 0);
-  std::vector<uint64_t> S(nl, 0);
-#pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < int64_t(nl); ++t) {
-    uint64_t s = 0;
-    for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q) {
-      const uint32_t sb = j->strong_idx[q];
-      s += j->pt_off[sb + 1] - j->pt_off[sb];
-    }
-    S[t] = s;
-  }
-  uint64_t total = 0;
-  for (uint32_t t = 0; t < nl; ++t) {
-    total += uint64_t(j->ev_off[t + 1] - j->ev_off[t]) * S[t];
-    c->leaf_work[t + 1] = total;
-  }
-  const uint64_t budget = std::max<uint64_t>(1ull << 16, total / (148ull * 16ull));
-  c->items.clear();
-  c->fins.clear();
-  c->item_first.assign(nl + 1, 0);
-  c->fin_first.assign(nl + 1, 0);
-  uint64_t partial_evals = 0;
-  const bool warp_kernel = use_warp_kernel();
-  const uint32_t max_ev = warp_kernel ? uint32_t(kWarpMaxEv) : uint32_t(kMaxEvalsPerItem);
-  const uint32_t max_ent = warp_kernel ? uint32_t(kWarpMaxEntries) : 0xFFFFFFFFu;
-  c->warp_items = warp_kernel;
-  // Items: eval blocks of <= max_ev evals; a block whose pair work
-  // exceeds the budget is split into strong-list chunks whose partials are
-  // summed in chunk order by p2p_finalize_kernel.
-  for (uint32_t t = 0; t < nl; ++t) {
-    c->item_first[t] = uint32_t(c->items.size());
-    c->fin_first[t] = uint32_t(c->fins.size());
-    const uint32_t ntl = j->ev_off[t + 1] - j->ev_off[t];
-    const uint32_t sb0 = j->strong_off[t], sb1 = j->strong_off[t + 1];
-    for (uint32_t e0 = 0; e0 < ntl; e0 += max_ev) {
-      const uint32_t nt = std::min<uint32_t>(max_ev, ntl - e0);
-      const uint32_t evb = j->ev_off[t] + e0;
-      const uint64_t pairs = uint64_t(nt) * S[t];
-      if ((pairs <= budget || sb1 - sb0 <= 1) && sb1 - sb0 <= max_ent && S[t] <= 0xFFFFFFFFull) {
-        c->items.push_back(P2PItem{t, evb, nt, sb0, sb1, uint32_t(S[t]), kNoSelf, 0});
-        continue;
-      }
-      const uint64_t src_per_chunk = std::max<uint64_t>(1, budget / nt);
-      const uint32_t base = uint32_t(partial_evals);
-      uint32_t n_chunks = 0;
-      uint32_t q = sb0;
-      while (q < sb1) {
-        uint32_t q1 = q;
-        uint64_t acc = 0;
-        while (q1 < sb1 && q1 - q < max_ent &&
-               (acc == 0 || acc + (j->pt_off[j->strong_idx[q1] + 1] -
-                                   j->pt_off[j->strong_idx[q1]]) <= src_per_chunk)) {
-          acc += j->pt_off[j->strong_idx[q1] + 1] - j->pt_off[j->strong_idx[q1]];
-          ++q1;
-        }
-        c->items.push_back(P2PItem{t, evb, nt, q, q1, uint32_t(acc), uint32_t(partial_evals), 0});
-        partial_evals += nt;
-        ++n_chunks;
-        q = q1;
-      }
-      c->fins.push_back(P2PFinal{evb, nt, base, n_chunks});
-    }
-  }
-  c->item_first[nl] = uint32_t(c->items.size());
-  c->fin_first[nl] = uint32_t(c->fins.size());
-  if (partial_evals > 0xFFFFFFF0ull) return set_err(c, FMMCU_EINVAL, "partial buffer too large");
-
+  // ---- work list (built concurrently with the source packing above) -------
+  if (int rc = worklist.get()) return rc;
   tr.mark("worklist");
   // ---- device buffers -------------------------------------------------------
   CU_TRY(c, c->d_pt.ensure(size_t(nl + 1) * 4));
@@ -536,7 +635,7 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   CU_TRY(c, c->d_items.ensure(c->items.size() * sizeof(P2PItem)));
   CU_TRY(c, c->d_fin.ensure(c->fins.size() * sizeof(P2PFinal)));
   CU_TRY(c, c->d_out.ensure(size_t(ne) * 16));
-  CU_TRY(c, c->d_partial.ensure(size_t(partial_evals) * 16));
+  CU_TRY(c, c->d_partial.ensure(size_t(c->partial_evals) * 16));
   CU_TRY(c, c->d_hits.ensure(8));
   CU_TRY(c, c->d_counter.ensure(8));
   CU_TRY(c, c->d_seg.ensure(size_t(nnz) * 8));
@@ -596,10 +695,11 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
 }
 
 // Kernels over [lb, le) of the staged job.
-int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch) {
+int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
+                bool reset_hits = true) {
   cudaStream_t s = c->stream;
   int n = 0;
-  CU_TRY(c, cudaMemsetAsync(c->d_hits.p, 0, 8, s));
+  if (reset_hits) CU_TRY(c, cudaMemsetAsync(c->d_hits.p, 0, 8, s));
   CU_TRY(c, cudaMemsetAsync(c->d_counter.p, 0, 8, s));
   const P2PArgs a = make_args(c);
   if (le > lb) {
@@ -615,7 +715,7 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch) 
         P2PArgs aa = a;
         aa.items = c->d_items.as<P2PItem>() + i0;
         aa.n_items = i1 - i0;
-        dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s);
+        dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s, c->warp_e);
         ++n;
       }
       const uint32_t f0 = c->fin_first[lb], f1 = c->fin_first[le];
@@ -688,8 +788,17 @@ int fmmcu_create(fmmcu_ctx** out, int device) {
     return fail(e);
   if ((e = cudaStreamCreateWithFlags(&c->m2l_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(e);
+  if ((e = cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e);
   c->stream = c->own_stream;
   const unsigned flags = cudaEventBlockingSync;
+  for (int i = 0; i < fmmcu_ctx::kMaxSlices; ++i) {
+    if ((e = cudaEventCreateWithFlags(&c->ev_kslice[i], cudaEventDefault)) != cudaSuccess)
+      return fail(e);
+    if ((e = cudaEventCreateWithFlags(&c->ev_cslice[i], cudaEventDisableTiming | flags)) !=
+        cudaSuccess)
+      return fail(e);
+  }
   if ((e = cudaEventCreateWithFlags(&c->ev_start, flags)) != cudaSuccess) return fail(e);
   if ((e = cudaEventCreateWithFlags(&c->ev_end, flags)) != cudaSuccess) return fail(e);
   if ((e = cudaEventCreateWithFlags(&c->ev_m2l0, flags)) != cudaSuccess) return fail(e);
@@ -706,6 +815,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamSynchronize(c->own_stream);
     if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->m2l_stream);
+    cudaStreamSynchronize(c->d2h_stream);
     for (DevBuf* b : {&c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
                       &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter, &c->d_evr,
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
@@ -716,8 +826,13 @@ void fmmcu_destroy(fmmcu_ctx* c) {
       b->release();
     for (cudaEvent_t ev : {c->ev_start, c->ev_end, c->ev_m2l0, c->ev_m2l1})
       if (ev) cudaEventDestroy(ev);
+    for (int i = 0; i < fmmcu_ctx::kMaxSlices; ++i) {
+      if (c->ev_kslice[i]) cudaEventDestroy(c->ev_kslice[i]);
+      if (c->ev_cslice[i]) cudaEventDestroy(c->ev_cslice[i]);
+    }
     cudaStreamDestroy(c->own_stream);
     cudaStreamDestroy(c->m2l_stream);
+    cudaStreamDestroy(c->d2h_stream);
   }
   delete c;
 }
@@ -752,20 +867,60 @@ int fmmcu_p2p_launch(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const auto t0 = Clock::now();
   if (int rc = stage_job(c, j)) return rc;
   if (j->n_eval > 0 && !j->out) return set_err(c, FMMCU_EINVAL, "null output");
-  int nl = 0;
-  if (int rc = run_kernels(c, j->leaf_begin, j->leaf_end, j->mode, &nl)) return rc;
-  const uint32_t eb = c->ev_off[j->leaf_begin], ee = c->ev_off[j->leaf_end];
-  CU_TRY(c, c->h_out.ensure(size_t(c->n_eval) * 16 + 16));
-  if (ee > eb)
-    CU_TRY(c, cudaMemcpyAsync(c->h_out.as<double2>() + eb, c->out_ptr() + eb,
-                              size_t(ee - eb) * 16, cudaMemcpyDeviceToHost, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, c->stream));
-  CU_TRY(c, cudaEventRecord(c->ev_end, c->stream));
+  const uint32_t lb = j->leaf_begin, le = j->leaf_end;
+  const uint32_t eb = c->ev_off[lb], ee = c->ev_off[le];
+  // A page-locked output (cudaHostRegister / fmmcu_host_register) receives
+  // the D2H directly; otherwise it goes through pinned staging.
+  cudaPointerAttributes pa{};
+  c->direct_out = j->out && cudaPointerGetAttributes(&pa, j->out) == cudaSuccess &&
+                  pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // clear a "not a device pointer" status on old drivers
+  double2* dst = reinterpret_cast<double2*>(j->out);
+  if (!c->direct_out) {
+    CU_TRY(c, c->h_out.ensure(size_t(c->n_eval) * 16 + 16));
+    dst = c->h_out.as<double2>();
+  }
+  // Kernels in pair-work-balanced leaf slices; slice i's potentials go D2H
+  // on the copy stream while slice i+1 computes.
+  const uint64_t w0 = c->leaf_work[lb], w1 = c->leaf_work[le];
+  int ns = (ee - eb > (1u << 20) && j->mode == FMMCU_MODE_FAST) ? fmmcu_ctx::kMaxSlices : 1;
+  uint32_t cut[fmmcu_ctx::kMaxSlices + 1];
+  cut[0] = lb;
+  for (int i = 1; i < ns; ++i) {
+    const uint64_t target = w0 + (w1 - w0) * uint64_t(i) / uint64_t(ns);
+    const uint64_t* b = c->leaf_work.data();
+    uint32_t t = uint32_t(std::lower_bound(b + cut[i - 1], b + le, target) - b);
+    cut[i] = std::max(cut[i - 1], std::min(t, le));
+  }
+  cut[ns] = le;
+  c->n_slices = ns;
+  for (int i = 0; i < ns; ++i) {
+    int nl = 0;
+    if (int rc = run_kernels(c, cut[i], cut[i + 1], j->mode, &nl, i == 0)) return rc;
+    const uint32_t sb = c->ev_off[cut[i]], se = c->ev_off[cut[i + 1]];
+    c->slice_eb[i] = sb;
+    c->slice_eb[i + 1] = se;
+    CU_TRY(c, cudaEventRecord(c->ev_kslice[i], c->stream));
+    CU_TRY(c, cudaStreamWaitEvent(c->d2h_stream, c->ev_kslice[i], 0));
+    if (se > sb)
+      CU_TRY(c, cudaMemcpyAsync(dst + sb, c->out_ptr() + sb, size_t(se - sb) * 16,
+                                cudaMemcpyDeviceToHost, c->d2h_stream));
+    if (i == ns - 1)
+      CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost,
+                                c->d2h_stream));
+    CU_TRY(c, cudaEventRecord(c->ev_cslice[i], c->d2h_stream));
+  }
+  CU_TRY(c, cudaEventRecord(c->ev_end, c->d2h_stream));
+  if (c->trace)
+    std::fprintf(stderr, "[fmmcu] launch total (host)     %8.3f ms  (%d slices)\n",
+                 std::chrono::duration<double, std::milli>(Clock::now() - t0).count(), ns);
+  // the compute stream must not run ahead of the copies that read d_out
+  CU_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_end, 0));
   c->job = *j;
   c->d2h_bytes = uint64_t(ee - eb) * 16 + 8;
-  c->run_lb = j->leaf_begin;
-  c->run_le = j->leaf_end;
-  c->run_total_pairs = c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
+  c->run_lb = lb;
+  c->run_le = le;
+  c->run_total_pairs = w1 - w0;
   // busy time = host work before the first device operation + device span
   // (ev_start .. ev_end covers packing-overlapped uploads, kernels, D2H)
   c->prep_seconds = std::chrono::duration<double>(c->t_evstart - t0).count();
@@ -778,15 +933,41 @@ int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
   if (!c->inflight) return set_err(c, FMMCU_ESTATE, "finish without launch");
   c->inflight = false;
   CU_TRY(c, cudaSetDevice(c->device));
+  // staged output: copy each slice out as soon as its D2H has landed
+  for (int i = 0; i < c->n_slices; ++i) {
+    CU_TRY(c, cudaEventSynchronize(c->ev_cslice[i]));
+    const uint32_t sb = c->slice_eb[i], se = c->slice_eb[i + 1];
+    if (!c->direct_out && se > sb)
+      par_memcpy(c->job.out + 2 * size_t(sb), c->h_out.as<double2>() + sb, size_t(se - sb) * 16);
+  }
   CU_TRY(c, cudaEventSynchronize(c->ev_end));
   CU_TRY(c, cudaGetLastError());
   float ms = 0.f;
   CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_start, c->ev_end));
-  const uint32_t eb = c->ev_off[c->run_lb], ee = c->ev_off[c->run_le];
-  if (ee > eb) par_memcpy(c->job.out + 2 * size_t(eb), c->h_out.as<double2>() + eb, size_t(ee - eb) * 16);
+  if (c->trace) {
+    float kms = 0.f;
+    cudaEventElapsedTime(&kms, c->ev_start, c->ev_kslice[c->n_slices - 1]);
+    std::fprintf(stderr, "[fmmcu] device span %8.3f ms (start->last kernel %8.3f ms), prep %8.3f ms\n",
+                 ms, kms, 1e3 * c->prep_seconds);
+  }
   const uint64_t hits = *c->h_hits.as<unsigned long long>();
   if (pair_evals) *pair_evals = c->run_total_pairs - hits;
   if (seconds) *seconds = c->prep_seconds + 1e-3 * double(ms);
+  return FMMCU_OK;
+}
+
+/* Page-lock caller memory so fmmcu_p2p_launch can DMA straight into it. */
+int fmmcu_host_register(fmmcu_ctx* c, void* ptr, uint64_t bytes) {
+  if (!c || !ptr || !bytes) return FMMCU_EINVAL;
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterPortable));
+  return FMMCU_OK;
+}
+
+int fmmcu_host_unregister(fmmcu_ctx* c, void* ptr) {
+  if (!c || !ptr) return FMMCU_EINVAL;
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaHostUnregister(ptr));
   return FMMCU_OK;
 }
 

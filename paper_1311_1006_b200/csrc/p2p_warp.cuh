@@ -3,7 +3,7 @@
 // Same arithmetic and semantics as p2p_tile_kernel (near_box(),
 // proj/src/backend.cpp:41-69), different decomposition: every warp is an
 // independent pipeline with no CTA-level synchronisation at all.
-//   * a warp claims work items (<= 40 evals of one target leaf x <= 32
+//   * a warp claims work items (<= 8E evals of one target leaf x <= 32
 //     strong-list entries) from a global counter;
 //   * lane q holds the source run (first slot, length) of strong entry q and
 //     its offset in the item's virtual source stream (warp prefix scan);
@@ -20,12 +20,12 @@
 
 namespace fmmcu {
 
-constexpr int kWarpMaxEv = 40;     // evals per warp item (E = 4 -> G <= 10, K >= 3)
+constexpr int kWarpSlots = 8;        // eval slots per warp item: <= 8E evals, K >= 4 source lanes
 constexpr int kWarpMaxEntries = 32;  // strong entries per warp item (one per lane)
 
 template <int KERNEL, int SMOOTH, int E, int WARPS, int C, int U, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_warp_kernel(const P2PArgs a) {
-  static_assert(E * 32 >= kWarpMaxEv && C % 32 == 0, "shape");
+  static_assert(E >= 1 && kWarpSlots <= 32 && C % 32 == 0, "shape");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;

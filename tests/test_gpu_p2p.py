@@ -200,6 +200,37 @@ def test_linearity_at_scale(ctx):
         assert normwise(out1[e0:e1], w[e0:e1]) <= TOL_FP64
 
 
+def test_sliced_launch_direct_into_registered_output(ctx):
+    """n_eval > 2^20: the launch runs 8 pair-balanced leaf slices whose D2H
+    overlaps the next slice.  Staged and page-locked (direct DMA) outputs,
+    a shard spanning slices and the device-resident path all agree bitwise."""
+    t, args = _tree_case(0, 1_500_000, 8, 6)
+    staged, p_staged, _ = _run(ctx, *args)
+    host = np.full_like(staged, np.nan)
+    ctx.host_register(host)
+    try:
+        out, p_direct, _ = _run(ctx, *args, out=host)
+    finally:
+        ctx.host_unregister(host)
+    assert out is host and p_direct == p_staged
+    assert bitwise(host, staged)
+    nl = len(args[0]) - 1
+    a, b = nl // 5, nl - nl // 7
+    part, _, _ = _run(ctx, *args, leaf_begin=a, leaf_end=b)
+    e0, e1 = int(args[1][a]), int(args[1][b])
+    assert bitwise(part[e0:e1], staged[e0:e1])
+    job, keep = N.CudaContext.make_job(*args, None)
+    ctx.stage(job, keep)
+    ctx.run_staged(0, nl)
+    assert ctx.pairs() == p_staged
+    assert bitwise(ctx.copy_out(len(staged)), staged)
+    csr = O.LeafCSR(*args[:5])
+    for lb in (0, nl // 2, nl - 1):
+        w, _ = O.nearfield(csr, *args[5:9], leaf_begin=lb, leaf_end=lb + 1)
+        e0, e1 = int(args[1][lb]), int(args[1][lb + 1])
+        assert normwise(staged[e0:e1], w[e0:e1]) <= TOL_FP64
+
+
 def test_invalid_jobs_fail_loudly(ctx):
     t, args = _tree_case(0, 1000, 3, 1)
     with pytest.raises(N.FmmcuError):
