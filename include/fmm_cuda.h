@@ -147,7 +147,56 @@ int fmmcu_synchronize(fmmcu_ctx *ctx);
 int fmmcu_m2l_launch(fmmcu_ctx *ctx, const fmmcu_m2l_job *job);
 int fmmcu_m2l_finish(fmmcu_ctx *ctx, uint64_t *m2l_ops, double *seconds);
 
+/* ---- the whole FMM evaluation on one device ------------------------------
+ * FmmEngine::evaluate (reference engine.cpp:208-347) with every phase on the
+ * GPU: median-split pyramid and theta connectivity (bit-exact with
+ * build_pyramid / build_connectivity, geometry.cpp:106-216), P2M, M2M, the
+ * batched M2L, L2L, the P2P near field and near + L2P assembly.  Inputs and
+ * the output are in the caller's original order (like evaluate()). */
+typedef struct {
+  uint32_t n_src;
+  uint32_t n_eval;
+  const double *src_z;       /* [2 n_src]  source positions */
+  const double *src_m;       /* [2 n_src]  strengths */
+  const double *eval_y;      /* [2 n_eval] eval positions */
+  const int64_t *eval_sid;   /* [n_eval] source id of each eval (-1 none), or NULL */
+  int n_levels;
+  double theta;
+  int p;                     /* expansion order (FmmConfig::expansion_order) */
+  int kernel;                /* FMMCU_KERNEL_* */
+  int smoother;              /* FMMCU_SMOOTH_* (near field only, as the reference) */
+  double delta;
+  double *out;               /* [2 n_eval] potentials, original eval order */
+} fmmcu_fmm_job;
+
+typedef struct {
+  uint64_t p2p_pairs, m2l_ops, p2m_points, l2p_points; /* WorkCounters */
+  double t_upload;      /* H2D of the inputs (device span, s) */
+  double t_tree;        /* pyramid build */
+  double t_connect;     /* connectivity + permutation/packing */
+  double t_p2m_upward;  /* P2M + M2M chain (far stream) */
+  double t_m2l;         /* M2L + L2L (far stream) */
+  double t_p2p;         /* near-field kernels */
+  double t_device;      /* first H2D .. potentials on the host */
+  double t_total;       /* host wall time of the call */
+  uint64_t h2d_bytes, d2h_bytes;
+} fmmcu_fmm_stats;
+
+int fmmcu_fmm_evaluate(fmmcu_ctx *ctx, const fmmcu_fmm_job *job, fmmcu_fmm_stats *stats);
+/* The device-built pyramid / connectivity of the last fmmcu_fmm_evaluate
+ * (parity checks).  Box layout as fmmh_tree_boxes: f64[5 n] = centre x, y,
+ * half width, half height, radius; u32[4 n] = point and eval ranges. */
+int fmmcu_fmm_tree_level(fmmcu_ctx *ctx, int level, uint32_t *n_boxes, double *f64,
+                         uint32_t *u32);
+int fmmcu_fmm_tree_perm(fmmcu_ctx *ctx, uint32_t *perm, uint32_t *eval_perm);
+/* nnz of the level's strong (weak = 0) or weak (weak = 1) lists; off [n+1]
+ * and idx [nnz] filled when non-NULL. */
+int fmmcu_fmm_tree_lists(fmmcu_ctx *ctx, int level, int weak, uint64_t *nnz, uint32_t *off,
+                         uint32_t *idx);
+
 /* ---- diagnostics --------------------------------------------------------- */
+/* Device restatement of glibc hypot (box radii / theta distances), batched. */
+int fmmcu_hypot_batch(fmmcu_ctx *ctx, const double *xy, uint32_t n, double *out);
 /* Kernels launched by this context since creation (evidence counter). */
 uint64_t fmmcu_kernel_launches(const fmmcu_ctx *ctx);
 /* Host<->device bytes moved by the last fmmcu_p2p_launch (H2D: packed

@@ -20,6 +20,15 @@
  *                      over CSR-flattened leaf ranges / strong lists
  *   orc_m2l_add        expansion.cpp:188-269 (double path and long double path)
  *   orc_binomial       expansion.cpp:12-32 (Pascal table, doubles)
+ *   orc_hypot          glibc 2.39 __hypot (sysdeps/ieee754/dbl-64/e_hypot.c,
+ *                      x86-64 build without FMA): the reference reaches it
+ *                      through std::hypot (box radius, geometry.cpp:100) and
+ *                      std::abs(complex) -> cabs (theta criterion,
+ *                      geometry.cpp:13-19).  glibc is a third-party dependency
+ *                      outside /root/reference; the algorithm (Borges 2019
+ *                      correction, 2^+-600 scaling outside [2^-459, 2^511]) is
+ *                      restated from its object code and pinned against libm
+ *                      hypot() and cabs() (tests/test_oracle.py).
  */
 #include <complex.h>
 #include <math.h>
@@ -301,4 +310,55 @@ void orc_cdiv_batch(int64_t n, const double *in, double *out, int native) {
     else
       orc_divdc3(q[0], q[1], q[2], q[3], out + 2 * i, out + 2 * i + 1);
   }
+}
+
+/* ------------------------------------------------------------- __hypot -- */
+static double orc_hypot_kernel(double ax, double ay) {
+  const double h = sqrt(ax * ax + ay * ay);
+  double t1, t2;
+  if (h <= ay + ay) {
+    const double delta = h - ay;
+    t1 = ((delta + delta) - ax) * ax;
+    t2 = (delta - ((ax - ay) + (ax - ay))) * delta;
+  } else {
+    const double delta = h - ax;
+    t1 = (delta + delta) * (ax - (ay + ay));
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  return h - (t1 + t2) / (h + h);
+}
+
+double orc_hypot(double x, double y) {
+  if (!isfinite(x) || !isfinite(y)) {
+    if (isinf(x) || isinf(y)) return INFINITY;
+    return x + y;
+  }
+  x = fabs(x);
+  y = fabs(y);
+  double ax = y > x ? y : x;
+  double ay = y > x ? x : y;
+  if (ax > 0x1p511) {
+    if (ax * 0x1p-54 >= ay) return ax + ay;
+    return orc_hypot_kernel(ax * 0x1p-600, ay * 0x1p-600) * 0x1p600;
+  }
+  if (0x1p-459 > ay) {
+    if (ax >= ay * 0x1p54) return ax + ay;
+    return orc_hypot_kernel(ax * 0x1p600, ay * 0x1p600) * 0x1p-600;
+  }
+  if (ax * 0x1p-54 >= ay) return ax + ay;
+  return orc_hypot_kernel(ax, ay);
+}
+
+/* mismatches of orc_hypot against libm hypot() and cabs() over n pairs */
+int64_t orc_hypot_check(int64_t n, const double *xy, double *out) {
+  int64_t bad = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double x = xy[2 * i], y = xy[2 * i + 1];
+    const double r = orc_hypot(x, y);
+    const double a = hypot(x, y);
+    const double b = cabs(x + I * y);
+    if (out) out[i] = r;
+    if (memcmp(&r, &a, 8) != 0 || memcmp(&r, &b, 8) != 0) ++bad;
+  }
+  return bad;
 }

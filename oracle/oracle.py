@@ -66,6 +66,10 @@ def oracle_lib():
         lib.orc_m2l_add.restype = C.c_int
         lib.orc_binomial.argtypes = [C.c_int, C.c_int]
         lib.orc_binomial.restype = C.c_double
+        lib.orc_hypot.argtypes = [C.c_double, C.c_double]
+        lib.orc_hypot.restype = C.c_double
+        lib.orc_hypot_check.argtypes = [C.c_int64, _dp, _dp_n]
+        lib.orc_hypot_check.restype = C.c_int64
         _ORC = lib
     return _ORC
 
@@ -120,6 +124,14 @@ def ref_lib():
 
 
 # --------------------------------------------------------------- restatement
+def hypot_check(xy: np.ndarray):
+    """(mismatches vs libm hypot/cabs, restated glibc hypot values) for pairs xy[n, 2]."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    out = np.empty(len(xy))
+    bad = oracle_lib().orc_hypot_check(len(xy), xy, out)
+    return int(bad), out
+
+
 def cdiv(q: np.ndarray, native: bool = False) -> np.ndarray:
     """q: (n, 4) [a, b, c, d] -> (n, 2) of (a+ib)/(c+id) via restated __divdc3."""
     q = np.ascontiguousarray(q, dtype=np.float64)

@@ -35,6 +35,38 @@ _cuda = None
 _host = None
 
 
+class FmmJob(C.Structure):
+    """Mirror of ``fmmcu_fmm_job`` (include/fmm_cuda.h)."""
+
+    _fields_ = [
+        ("n_src", C.c_uint32),
+        ("n_eval", C.c_uint32),
+        ("src_z", C.c_void_p),
+        ("src_m", C.c_void_p),
+        ("eval_y", C.c_void_p),
+        ("eval_sid", C.c_void_p),
+        ("n_levels", C.c_int),
+        ("theta", C.c_double),
+        ("p", C.c_int),
+        ("kernel", C.c_int),
+        ("smoother", C.c_int),
+        ("delta", C.c_double),
+        ("out", C.c_void_p),
+    ]
+
+
+class FmmStats(C.Structure):
+    """Mirror of ``fmmcu_fmm_stats`` (include/fmm_cuda.h)."""
+
+    _fields_ = [(n, C.c_uint64) for n in ("p2p_pairs", "m2l_ops", "p2m_points", "l2p_points")] + \
+               [(n, C.c_double) for n in ("t_upload", "t_tree", "t_connect", "t_p2m_upward",
+                                          "t_m2l", "t_p2p", "t_device", "t_total")] + \
+               [("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
 class NativeLibraryMissing(RuntimeError):
     pass
 
@@ -43,6 +75,13 @@ class FmmcuError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"fmmcu error {code}: {msg}")
         self.code = code
+
+
+def _as_pairs(a):
+    a = np.asarray(a)
+    if np.iscomplexobj(a):
+        return np.ascontiguousarray(a, dtype=np.complex128).view(np.float64).reshape(-1, 2)
+    return np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 2)
 
 
 def _ptr(a):
@@ -100,6 +139,8 @@ CUDA_SYMBOLS = [
     "fmmcu_p2p_device_out", "fmmcu_p2p_bind_device_out", "fmmcu_p2p_copy_out", "fmmcu_p2p_pairs", "fmmcu_p2p_work_prefix", "fmmcu_set_stream",
     "fmmcu_synchronize", "fmmcu_m2l_launch", "fmmcu_m2l_finish", "fmmcu_kernel_launches",
     "fmmcu_fp64_peak", "fmmcu_last_transfer_bytes", "fmmcu_host_register", "fmmcu_host_unregister",
+    "fmmcu_fmm_evaluate", "fmmcu_fmm_tree_level", "fmmcu_fmm_tree_perm", "fmmcu_fmm_tree_lists",
+    "fmmcu_hypot_batch",
 ]
 
 
@@ -129,6 +170,11 @@ def cuda_lib():
         lib.fmmcu_set_stream.argtypes = [vp, vp]
         lib.fmmcu_host_register.argtypes = [vp, vp, C.c_uint64]
         lib.fmmcu_host_unregister.argtypes = [vp, vp]
+        lib.fmmcu_fmm_evaluate.argtypes = [vp, C.POINTER(FmmJob), C.POINTER(FmmStats)]
+        lib.fmmcu_fmm_tree_level.argtypes = [vp, C.c_int, C.POINTER(C.c_uint32), vp, vp]
+        lib.fmmcu_fmm_tree_perm.argtypes = [vp, vp, vp]
+        lib.fmmcu_fmm_tree_lists.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_uint64), vp, vp]
+        lib.fmmcu_hypot_batch.argtypes = [vp, vp, C.c_uint32, vp]
         lib.fmmcu_synchronize.argtypes = [vp]
         lib.fmmcu_m2l_launch.argtypes = [vp, C.POINTER(M2LJob)]
         lib.fmmcu_m2l_finish.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
@@ -275,6 +321,69 @@ class CudaContext:
 
     def host_unregister(self, arr: np.ndarray):
         self._check(self.lib.fmmcu_host_unregister(self.h, arr.ctypes.data))
+
+    # -- whole FMM evaluation on the device (fmmcu_fmm_*) -------------------
+    def fmm_evaluate(self, z, m, y, sid, *, n_levels, theta, p, kernel=0, smoother=0, delta=0.0,
+                     out=None):
+        """One device FmmEngine::evaluate.  z, m: [n] complex (or [n,2] float);
+        y: [ne] eval positions, sid: [ne] int64 source ids or None.
+        Returns (potentials [ne] complex in original order, stats dict)."""
+        zz = _as_pairs(z)
+        mm = _as_pairs(m)
+        yy = _as_pairs(y)
+        ne = len(yy)
+        if out is None:
+            out = np.zeros(max(ne, 1), dtype=np.complex128)
+        sidp = None if sid is None else np.ascontiguousarray(sid, dtype=np.int64)
+        j = FmmJob()
+        j.n_src = len(zz)
+        j.n_eval = ne
+        j.src_z = _ptr(zz)
+        j.src_m = _ptr(mm)
+        j.eval_y = _ptr(yy) if ne else None
+        j.eval_sid = _ptr(sidp)
+        j.n_levels = n_levels
+        j.theta = theta
+        j.p = p
+        j.kernel = kernel
+        j.smoother = smoother
+        j.delta = delta
+        j.out = _ptr(out) if ne else None
+        st = FmmStats()
+        self._check(self.lib.fmmcu_fmm_evaluate(self.h, C.byref(j), C.byref(st)))
+        return out[:ne], st.as_dict()
+
+    def fmm_tree(self, n_levels: int, n_src: int, n_eval: int):
+        """Device pyramid + connectivity of the last fmm_evaluate, in the
+        layout of fmm.Tree: (boxes_f, boxes_u, perm, eval_perm, strong, weak)."""
+        bf, bu, strong, weak = [], [], [], []
+        for lvl in range(n_levels):
+            nb = C.c_uint32()
+            self._check(self.lib.fmmcu_fmm_tree_level(self.h, lvl, C.byref(nb), None, None))
+            f = np.zeros((nb.value, 5))
+            u = np.zeros((nb.value, 4), dtype=np.uint32)
+            self._check(self.lib.fmmcu_fmm_tree_level(self.h, lvl, C.byref(nb), _ptr(f), _ptr(u)))
+            bf.append(f)
+            bu.append(u)
+            for weak_flag, dst in ((0, strong), (1, weak)):
+                nnz = C.c_uint64()
+                self._check(self.lib.fmmcu_fmm_tree_lists(self.h, lvl, weak_flag, C.byref(nnz),
+                                                          None, None))
+                off = np.zeros(nb.value + 1, dtype=np.uint32)
+                idx = np.zeros(max(nnz.value, 1), dtype=np.uint32)
+                self._check(self.lib.fmmcu_fmm_tree_lists(self.h, lvl, weak_flag, C.byref(nnz),
+                                                          _ptr(off), _ptr(idx)))
+                dst.append((off, idx[: nnz.value]))
+        perm = np.zeros(n_src, dtype=np.uint32)
+        eperm = np.zeros(max(n_eval, 1), dtype=np.uint32)
+        self._check(self.lib.fmmcu_fmm_tree_perm(self.h, _ptr(perm), _ptr(eperm)))
+        return bf, bu, perm, eperm[:n_eval], strong, weak
+
+    def hypot(self, xy: np.ndarray) -> np.ndarray:
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        out = np.zeros(len(xy))
+        self._check(self.lib.fmmcu_hypot_batch(self.h, _ptr(xy), len(xy), _ptr(out)))
+        return out
 
     def synchronize(self):
         self._check(self.lib.fmmcu_synchronize(self.h))

@@ -1,0 +1,861 @@
+// fmm-b200 — the device FMM pipeline: one whole FmmEngine::evaluate
+// (proj/src/engine.cpp:208-347) on one B200.
+//
+//   H2D  z, m (and eval y / ids unless evals are the sources)   pinned chunks
+//   pyramid build (tree_kernels.cuh)            bit-exact with build_pyramid
+//   theta connectivity, every level             bit-exact with build_connectivity
+//   pack permuted sources, permuted evals, self slots
+//   far stream:  P2M -> M2M chain -> batched M2L (all levels) -> L2L + sums
+//   main stream: P2P (the warp kernel of fmmcu.cu over the finest strong lists)
+//   assembly: near + L2P, scattered to the original eval order -> D2H
+//
+// The host only builds the P2P work list from the finest CSR (which it reads
+// back once) while the far field already runs.  Counters equal the
+// reference's (p2p_pairs, m2l_ops, p2m_points, l2p_points); phase times are
+// device event spans.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdio>
+
+#include "far_kernels.cuh"
+#include "fmmcu_internal.cuh"
+#include "m2l_kernels.cuh"
+#include "tree_kernels.cuh"
+
+using namespace fmmcu;
+using namespace fmmcu::detail;
+
+namespace fmmcu {
+
+struct LevelConnDev {
+  DevBuf s_off, s_idx, w_off, w_idx;
+  uint32_t s_nnz = 0, w_nnz = 0;
+};
+
+struct DevicePipeline {
+  // inputs (original order)
+  DevBuf z, m, y, sid;
+  HostBuf hz, hm, hy, hsid, hres;
+  // pyramid
+  DevBuf keys0, keys1, ids, sx, sy, ex, ey, sxn, syn, exn, eyn, flag_s, flag_e, ind, scan,
+      cub_tmp, xmid_s, xmid_e, ymid_s, ymid_e, half_s, half_e, leaf_of, perm, eperm, inv;
+  DevBuf soff, eoff;                       // all levels: level l at off_base[l]
+  DevBuf center, hw, hh, radius;           // all levels: level l at box_base[l]
+  std::vector<uint64_t> off_base, box_base;
+  // connectivity
+  std::vector<LevelConnDev> conn;
+  DevBuf cnt_s, cnt_w;
+  // far field
+  DevBuf binom, out, loc, tcnt, wcnt, trow, wstart, m2l_row, tbox, woff, widx, m2l_sum, flag, res;
+  HostBuf h_flag, h_count;
+  int L = 0, p = 0, kernel = 0;
+  uint32_t N = 0, M = 0, n_targets = 0, m2l_nnz = 0;
+  bool self_eval = false;
+  bool tree_valid = false;
+  cudaStream_t far = nullptr;
+  cudaEvent_t ev[12] = {};
+};
+
+void destroy_pipeline(DevicePipeline* p) {
+  if (!p) return;
+  if (p->far) cudaStreamDestroy(p->far);
+  for (cudaEvent_t e : p->ev)
+    if (e) cudaEventDestroy(e);
+  DevBuf* bufs[] = {&p->z, &p->m, &p->y, &p->sid, &p->keys0, &p->keys1, &p->ids, &p->sx, &p->sy,
+                    &p->ex, &p->ey, &p->sxn, &p->syn, &p->exn, &p->eyn, &p->flag_s, &p->flag_e,
+                    &p->ind, &p->scan, &p->cub_tmp, &p->xmid_s, &p->xmid_e, &p->ymid_s,
+                    &p->ymid_e, &p->half_s, &p->half_e, &p->leaf_of, &p->perm, &p->eperm,
+                    &p->inv, &p->soff, &p->eoff, &p->center, &p->hw, &p->hh, &p->radius,
+                    &p->cnt_s, &p->cnt_w, &p->binom, &p->out, &p->loc, &p->tcnt, &p->wcnt,
+                    &p->trow, &p->wstart, &p->m2l_row, &p->tbox, &p->woff, &p->widx,
+                    &p->m2l_sum, &p->flag, &p->res};
+  for (DevBuf* b : bufs) b->release();
+  for (auto& c : p->conn) {
+    c.s_off.release();
+    c.s_idx.release();
+    c.w_off.release();
+    c.w_idx.release();
+  }
+  for (HostBuf* b : {&p->hz, &p->hm, &p->hy, &p->hsid, &p->hres, &p->h_flag, &p->h_count})
+    b->release();
+  delete p;
+}
+
+}  // namespace fmmcu
+
+namespace {
+
+constexpr int TB = 256;
+inline uint32_t blocks(uint64_t n) { return uint32_t((n + TB - 1) / TB); }
+inline uint64_t pow4(int l) { return uint64_t(1) << (2 * l); }
+
+__global__ void iota_kernel(uint32_t* __restrict__ v, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+// M2L lists of one level: targets = boxes with evals (l >= 1), partners =
+// weak entries whose box has sources (engine.cpp:98, :108-113).
+__global__ void m2l_count_kernel(const uint32_t* __restrict__ w_off,
+                                 const uint32_t* __restrict__ w_idx,
+                                 const uint32_t* __restrict__ soff, const uint32_t* __restrict__ eoff,
+                                 uint32_t nbox, uint32_t base, uint32_t* __restrict__ tcnt,
+                                 uint32_t* __restrict__ wcnt) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  uint32_t t = 0, w = 0;
+  if (eoff[i + 1] > eoff[i]) {
+    t = 1;
+    for (uint32_t q = w_off[i]; q < w_off[i + 1]; ++q) {
+      const uint32_t b = w_idx[q];
+      w += soff[b + 1] > soff[b] ? 1u : 0u;
+    }
+  }
+  tcnt[base + i] = t;
+  wcnt[base + i] = w;
+}
+
+__global__ void m2l_fill_kernel(const uint32_t* __restrict__ w_off, const uint32_t* __restrict__ w_idx,
+                                const uint32_t* __restrict__ soff, const uint32_t* __restrict__ eoff,
+                                uint32_t nbox, uint32_t base, const uint32_t* __restrict__ trow,
+                                const uint32_t* __restrict__ wstart, uint32_t* __restrict__ tbox,
+                                uint32_t* __restrict__ woff_out, uint32_t* __restrict__ widx,
+                                int32_t* __restrict__ m2l_row) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  const uint32_t g = base + i;
+  if (eoff[i + 1] == eoff[i]) {
+    m2l_row[g] = -1;
+    return;
+  }
+  const uint32_t row = trow[g];
+  m2l_row[g] = int32_t(row);
+  tbox[row] = g;
+  uint32_t o = wstart[g];
+  woff_out[row] = o;
+  for (uint32_t q = w_off[i]; q < w_off[i + 1]; ++q) {
+    const uint32_t b = w_idx[q];
+    if (soff[b + 1] > soff[b]) widx[o++] = base + b;
+  }
+}
+
+template <class T>
+int scan_excl(fmmcu_ctx* c, DevicePipeline* P, const T* in, T* out, uint64_t n, cudaStream_t s) {
+  size_t bytes = 0;
+  CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, int64_t(n), s));
+  CU_TRY(c, P->cub_tmp.ensure(bytes));
+  CU_TRY(c, cub::DeviceScan::ExclusiveSum(P->cub_tmp.p, bytes, in, out, int64_t(n), s));
+  return FMMCU_OK;
+}
+
+template <class K>
+int sort_pairs(fmmcu_ctx* c, DevicePipeline* P, const K* kin, K* kout, const uint32_t* vin,
+               uint32_t* vout, uint64_t n, int end_bit, cudaStream_t s) {
+  size_t bytes = 0;
+  CU_TRY(c, cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, int64_t(n), 0,
+                                            end_bit, s));
+  CU_TRY(c, P->cub_tmp.ensure(bytes));
+  CU_TRY(c, cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, bytes, kin, kout, vin, vout, int64_t(n),
+                                            0, end_bit, s));
+  return FMMCU_OK;
+}
+
+// list sorted along axis of points p[0..n) (ties by index)
+int sorted_list(fmmcu_ctx* c, DevicePipeline* P, const double2* pts, uint32_t n, int axis,
+                uint32_t* list, cudaStream_t s) {
+  if (!n) return FMMCU_OK;
+  auto* k0 = P->keys0.as<unsigned long long>();
+  auto* k1 = P->keys1.as<unsigned long long>();
+  coord_keys_kernel<<<blocks(n), TB, 0, s>>>(pts, n, axis, k0, P->ids.as<uint32_t>());
+  return sort_pairs(c, P, k0, k1, P->ids.as<uint32_t>(), list, n, 64, s);
+}
+
+// Stable partition of every segment of `list` (offsets off[0..nseg], first
+// high slot mid[seg]) by the per-id flags; result in `out`.
+int partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint32_t n,
+              const uint8_t* flag, const uint32_t* off, const uint32_t* mid, uint32_t nseg,
+              uint32_t* out, cudaStream_t s) {
+  if (!n) return FMMCU_OK;
+  uint32_t* ind = P->ind.as<uint32_t>();
+  uint32_t* scan = P->scan.as<uint32_t>();
+  gather_flags_kernel<<<blocks(n), TB, 0, s>>>(list, n, flag, ind);
+  if (int rc = scan_excl(c, P, ind, scan, n, s)) return rc;
+  partition_kernel<<<blocks(n), TB, 0, s>>>(list, n, off, mid, nseg, ind, scan, out);
+  return FMMCU_OK;
+}
+
+// ------------------------------------------------------------ the pyramid --
+int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_t s) {
+  (void)theta;
+  const uint32_t N = P->N, M = P->M;
+  const int L = P->L;
+  const double2* zp = P->z.as<double2>();
+  const double2* yp = P->self_eval ? zp : P->y.as<double2>();
+  P->off_base.assign(L + 1, 0);
+  P->box_base.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) {
+    P->off_base[l + 1] = P->off_base[l] + pow4(l) + 1;
+    P->box_base[l + 1] = P->box_base[l] + pow4(l);
+  }
+  const uint64_t nb = P->box_base[L], no = P->off_base[L];
+  const uint64_t nmax = std::max<uint64_t>(std::max(N, M), 1);
+  const uint64_t top = pow4(L - 1);  // boxes of the finest level
+  CU_TRY(c, P->keys0.ensure(nmax * 8));
+  CU_TRY(c, P->keys1.ensure(nmax * 8));
+  CU_TRY(c, P->ids.ensure(nmax * 4));
+  for (DevBuf* b : {&P->sx, &P->sy, &P->sxn, &P->syn, &P->perm, &P->inv})
+    CU_TRY(c, b->ensure(uint64_t(std::max(N, 1u)) * 4));
+  for (DevBuf* b : {&P->ex, &P->ey, &P->exn, &P->eyn, &P->eperm})
+    CU_TRY(c, b->ensure(uint64_t(std::max(M, 1u)) * 4));
+  CU_TRY(c, P->leaf_of.ensure(nmax * 4));
+  CU_TRY(c, P->flag_s.ensure(std::max(N, 1u)));
+  CU_TRY(c, P->flag_e.ensure(std::max(M, 1u)));
+  CU_TRY(c, P->ind.ensure((nmax + 1) * 4));
+  CU_TRY(c, P->scan.ensure((nmax + 1) * 4));
+  CU_TRY(c, P->soff.ensure(no * 4));
+  CU_TRY(c, P->eoff.ensure(no * 4));
+  CU_TRY(c, P->center.ensure(nb * 16));
+  CU_TRY(c, P->hw.ensure(nb * 8));
+  CU_TRY(c, P->hh.ensure(nb * 8));
+  CU_TRY(c, P->radius.ensure(nb * 8));
+  const uint64_t np_max = std::max<uint64_t>(pow4(std::max(L - 2, 0)), 1);
+  for (DevBuf* b : {&P->xmid_s, &P->xmid_e}) CU_TRY(c, b->ensure(np_max * 4));
+  for (DevBuf* b : {&P->ymid_s, &P->ymid_e}) CU_TRY(c, b->ensure(2 * np_max * 4));
+  for (DevBuf* b : {&P->half_s, &P->half_e}) CU_TRY(c, b->ensure((2 * np_max + 1) * 4));
+  (void)top;
+
+  uint32_t* SX = P->sx.as<uint32_t>();
+  uint32_t* SY = P->sy.as<uint32_t>();
+  uint32_t* EX = P->ex.as<uint32_t>();
+  uint32_t* EY = P->ey.as<uint32_t>();
+  uint32_t* SXn = P->sxn.as<uint32_t>();
+  uint32_t* SYn = P->syn.as<uint32_t>();
+  uint32_t* EXn = P->exn.as<uint32_t>();
+  uint32_t* EYn = P->eyn.as<uint32_t>();
+  if (int rc = sorted_list(c, P, zp, N, 0, SX, s)) return rc;
+  if (int rc = sorted_list(c, P, zp, N, 1, SY, s)) return rc;
+  if (int rc = sorted_list(c, P, yp, M, 0, EX, s)) return rc;
+  if (int rc = sorted_list(c, P, yp, M, 1, EY, s)) return rc;
+
+  uint32_t* soff = P->soff.as<uint32_t>();
+  uint32_t* eoff = P->eoff.as<uint32_t>();
+  double2* center = P->center.as<double2>();
+  const uint32_t root_off[4] = {0, N, 0, M};
+  CU_TRY(c, cudaMemcpyAsync(soff, root_off, 8, cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaMemcpyAsync(eoff, root_off + 2, 8, cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaStreamSynchronize(s));  // root_off lives on this stack frame
+
+  auto geometry = [&](int l) {
+    BoxArgs g{};
+    g.src = zp;
+    g.ev = yp;
+    g.sx = SX;
+    g.sy = SY;
+    g.ex = EX;
+    g.ey = EY;
+    g.soff = soff + P->off_base[l];
+    g.eoff = eoff + P->off_base[l];
+    g.parent_center = l ? center + P->box_base[l - 1] : nullptr;
+    g.nbox = uint32_t(pow4(l));
+    g.center = center + P->box_base[l];
+    g.hw = P->hw.as<double>() + P->box_base[l];
+    g.hh = P->hh.as<double>() + P->box_base[l];
+    g.radius = P->radius.as<double>() + P->box_base[l];
+    box_geometry_kernel<<<blocks(g.nbox), TB, 0, s>>>(g);
+  };
+  geometry(0);
+
+  uint32_t* xmid_s = P->xmid_s.as<uint32_t>();
+  uint32_t* xmid_e = P->xmid_e.as<uint32_t>();
+  uint32_t* ymid_s = P->ymid_s.as<uint32_t>();
+  uint32_t* ymid_e = P->ymid_e.as<uint32_t>();
+  uint32_t* half_s = P->half_s.as<uint32_t>();
+  uint32_t* half_e = P->half_e.as<uint32_t>();
+  uint8_t* fs = P->flag_s.as<uint8_t>();
+  uint8_t* fe = P->flag_e.as<uint8_t>();
+  for (int l = 1; l < L; ++l) {
+    const uint32_t np = uint32_t(pow4(l - 1));
+    const uint32_t* ps = soff + P->off_base[l - 1];
+    const uint32_t* pe = eoff + P->off_base[l - 1];
+    const double2* pc = center + P->box_base[l - 1];
+    // x split of every parent (geometry.cpp:141-142)
+    SplitArgs a{};
+    a.src = zp;
+    a.ev = yp;
+    a.slist = SX;
+    a.elist = EX;
+    a.soff = ps;
+    a.eoff = pe;
+    a.fallback = pc;
+    a.fb_div = 1;
+    a.nseg = np;
+    a.axis = 0;
+    a.smid = xmid_s;
+    a.emid = xmid_e;
+    split_kernel<<<blocks(np), TB, 0, s>>>(a);
+    if (N) low_flags_kernel<<<blocks(N), TB, 0, s>>>(SX, N, ps, xmid_s, np, fs);
+    if (M) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EX, M, pe, xmid_e, np, fe);
+    if (int rc = partition(c, P, SY, N, fs, ps, xmid_s, np, SYn, s)) return rc;
+    if (int rc = partition(c, P, EY, M, fe, pe, xmid_e, np, EYn, s)) return rc;
+    std::swap(SY, SYn);
+    std::swap(EY, EYn);
+    child_offsets_kernel<<<blocks(np), TB, 0, s>>>(ps, xmid_s, nullptr, np, half_s, nullptr);
+    child_offsets_kernel<<<blocks(np), TB, 0, s>>>(pe, xmid_e, nullptr, np, half_e, nullptr);
+    // y split of both halves (geometry.cpp:143-146)
+    a.slist = SY;
+    a.elist = EY;
+    a.soff = half_s;
+    a.eoff = half_e;
+    a.fb_div = 2;
+    a.nseg = 2 * np;
+    a.axis = 1;
+    a.smid = ymid_s;
+    a.emid = ymid_e;
+    split_kernel<<<blocks(2 * np), TB, 0, s>>>(a);
+    if (N) low_flags_kernel<<<blocks(N), TB, 0, s>>>(SY, N, half_s, ymid_s, 2 * np, fs);
+    if (M) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EY, M, half_e, ymid_e, 2 * np, fe);
+    if (int rc = partition(c, P, SX, N, fs, half_s, ymid_s, 2 * np, SXn, s)) return rc;
+    if (int rc = partition(c, P, EX, M, fe, half_e, ymid_e, 2 * np, EXn, s)) return rc;
+    std::swap(SX, SXn);
+    std::swap(EX, EXn);
+    child_offsets_kernel<<<blocks(np), TB, 0, s>>>(ps, xmid_s, ymid_s, np, nullptr,
+                                                   soff + P->off_base[l]);
+    child_offsets_kernel<<<blocks(np), TB, 0, s>>>(pe, xmid_e, ymid_e, np, nullptr,
+                                                   eoff + P->off_base[l]);
+    geometry(l);
+  }
+  // leaf-internal order = original index order (geometry.cpp:156-161)
+  const uint32_t nleaf = uint32_t(pow4(L - 1));
+  int bits = 1;
+  while ((uint64_t(1) << bits) < nleaf) ++bits;
+  uint32_t* leaf_of = P->leaf_of.as<uint32_t>();
+  uint32_t* iota = P->ids.as<uint32_t>();
+  if (N) {
+    leaf_of_kernel<<<blocks(N), TB, 0, s>>>(SX, N, soff + P->off_base[L - 1], nleaf, leaf_of);
+    iota_kernel<<<blocks(N), TB, 0, s>>>(iota, N);
+    if (int rc = sort_pairs(c, P, leaf_of, P->keys1.as<uint32_t>(), iota, P->perm.as<uint32_t>(),
+                            N, bits, s))
+      return rc;
+  }
+  if (M) {
+    leaf_of_kernel<<<blocks(M), TB, 0, s>>>(EX, M, eoff + P->off_base[L - 1], nleaf, leaf_of);
+    iota_kernel<<<blocks(M), TB, 0, s>>>(iota, M);
+    if (int rc = sort_pairs(c, P, leaf_of, P->keys1.as<uint32_t>(), iota, P->eperm.as<uint32_t>(),
+                            M, bits, s))
+      return rc;
+  }
+  CU_TRY(c, cudaGetLastError());
+  c->launches += uint64_t(8 + 14 * (L - 1));
+  return FMMCU_OK;
+}
+
+// ----------------------------------------------------------- connectivity --
+int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_t s) {
+  const int L = P->L;
+  P->conn.resize(L);
+  const uint32_t zero_one[3] = {0, 1, 0};
+  {
+    LevelConnDev& c0 = P->conn[0];
+    CU_TRY(c, c0.s_off.ensure(8));
+    CU_TRY(c, c0.s_idx.ensure(4));
+    CU_TRY(c, c0.w_off.ensure(8));
+    CU_TRY(c, c0.w_idx.ensure(4));
+    CU_TRY(c, cudaMemcpyAsync(c0.s_off.p, zero_one, 8, cudaMemcpyHostToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(c0.s_idx.p, zero_one, 4, cudaMemcpyHostToDevice, s));
+    CU_TRY(c, cudaMemsetAsync(c0.w_off.p, 0, 8, s));
+    c0.s_nnz = 1;
+    c0.w_nnz = 0;
+  }
+  const uint64_t nmax = pow4(L - 1);
+  CU_TRY(c, P->cnt_s.ensure((nmax + 1) * 4));
+  CU_TRY(c, P->cnt_w.ensure((nmax + 1) * 4));
+  CU_TRY(c, P->h_count.ensure(16));
+  uint32_t* cs = P->cnt_s.as<uint32_t>();
+  uint32_t* cw = P->cnt_w.as<uint32_t>();
+  for (int l = 1; l < L; ++l) {
+    const uint32_t nbox = uint32_t(pow4(l));
+    LevelConnDev& pc = P->conn[l - 1];
+    LevelConnDev& lc = P->conn[l];
+    const double2* cen = P->center.as<double2>() + P->box_base[l];
+    const double* rad = P->radius.as<double>() + P->box_base[l];
+    CU_TRY(c, lc.s_off.ensure((nbox + 1) * 4));
+    CU_TRY(c, lc.w_off.ensure((nbox + 1) * 4));
+    CU_TRY(c, cudaMemsetAsync(cs + nbox, 0, 4, s));
+    CU_TRY(c, cudaMemsetAsync(cw + nbox, 0, 4, s));
+    classify_kernel<false><<<blocks(nbox), TB, 0, s>>>(
+        pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, cs, cw, nullptr,
+        nullptr, nullptr, nullptr);
+    if (int rc = scan_excl(c, P, cs, lc.s_off.as<uint32_t>(), nbox + 1, s)) return rc;
+    if (int rc = scan_excl(c, P, cw, lc.w_off.as<uint32_t>(), nbox + 1, s)) return rc;
+    uint32_t* hc = P->h_count.as<uint32_t>();
+    CU_TRY(c, cudaMemcpyAsync(hc, lc.s_off.as<uint32_t>() + nbox, 4, cudaMemcpyDeviceToHost, s));
+    CU_TRY(c, cudaMemcpyAsync(hc + 1, lc.w_off.as<uint32_t>() + nbox, 4, cudaMemcpyDeviceToHost, s));
+    CU_TRY(c, cudaStreamSynchronize(s));
+    lc.s_nnz = hc[0];
+    lc.w_nnz = hc[1];
+    CU_TRY(c, lc.s_idx.ensure(uint64_t(std::max(lc.s_nnz, 1u)) * 4));
+    CU_TRY(c, lc.w_idx.ensure(uint64_t(std::max(lc.w_nnz, 1u)) * 4));
+    classify_kernel<true><<<blocks(nbox), TB, 0, s>>>(
+        pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, nullptr, nullptr,
+        lc.s_off.as<uint32_t>(), lc.w_off.as<uint32_t>(), lc.s_idx.as<uint32_t>(),
+        lc.w_idx.as<uint32_t>());
+    c->launches += 2;
+  }
+  CU_TRY(c, cudaGetLastError());
+  return FMMCU_OK;
+}
+
+// ------------------------------------------------------------- far field --
+int far_setup(fmmcu_ctx* c, DevicePipeline* P) {
+  const int P1 = P->p + 1;
+  // Pascal rows as the reference's table (expansion.cpp:12-26)
+  const int brow = 2 * P1 + 4;
+  std::vector<double> t(size_t(brow) * brow, 0.0);
+  for (int i = 0; i < brow; ++i) {
+    t[size_t(i) * brow] = 1.0;
+    for (int j = 1; j <= i; ++j) t[size_t(i) * brow + j] = t[size_t(i - 1) * brow + j - 1] + t[size_t(i - 1) * brow + j];
+  }
+  CU_TRY(c, P->binom.ensure(t.size() * 8));
+  CU_TRY(c, cudaMemcpy(P->binom.p, t.data(), t.size() * 8, cudaMemcpyHostToDevice));
+  return FMMCU_OK;
+}
+
+FarArgs far_args(DevicePipeline* P, int l) {
+  FarArgs a{};
+  a.p = P->p;
+  a.kernel = P->kernel;
+  a.binom = P->binom.as<double>();
+  a.brow = 2 * (P->p + 1) + 4;
+  a.center = P->center.as<double2>();
+  a.soff_l = P->soff.as<uint32_t>() + P->off_base[l];
+  a.eoff_l = P->eoff.as<uint32_t>() + P->off_base[l];
+  a.soff_c = (l + 1 < P->L) ? P->soff.as<uint32_t>() + P->off_base[l + 1] : nullptr;
+  a.base = uint32_t(P->box_base[l]);
+  a.nbox = uint32_t(pow4(l));
+  a.out = P->out.as<double2>();
+  a.loc = P->loc.as<double2>();
+  a.m2l = P->m2l_sum.as<double2>();
+  a.m2l_row = P->m2l_row.as<int32_t>();
+  return a;
+}
+
+// M2L target/partner lists of all levels (device) -> n_targets, m2l_nnz
+int m2l_lists(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s) {
+  const int L = P->L;
+  const uint64_t nb = P->box_base[L];
+  CU_TRY(c, P->tcnt.ensure((nb + 1) * 4));
+  CU_TRY(c, P->wcnt.ensure((nb + 1) * 4));
+  CU_TRY(c, P->trow.ensure((nb + 1) * 4));
+  CU_TRY(c, P->wstart.ensure((nb + 1) * 4));
+  CU_TRY(c, P->m2l_row.ensure(nb * 4));
+  uint32_t* tc = P->tcnt.as<uint32_t>();
+  uint32_t* wc = P->wcnt.as<uint32_t>();
+  CU_TRY(c, cudaMemsetAsync(tc, 0, (nb + 1) * 4, s));
+  CU_TRY(c, cudaMemsetAsync(wc, 0, (nb + 1) * 4, s));
+  CU_TRY(c, cudaMemsetAsync(P->m2l_row.p, 0xFF, nb * 4, s));
+  for (int l = 1; l < L; ++l) {
+    const uint32_t nbox = uint32_t(pow4(l));
+    m2l_count_kernel<<<blocks(nbox), TB, 0, s>>>(
+        P->conn[l].w_off.as<uint32_t>(), P->conn[l].w_idx.as<uint32_t>(),
+        P->soff.as<uint32_t>() + P->off_base[l], P->eoff.as<uint32_t>() + P->off_base[l], nbox,
+        uint32_t(P->box_base[l]), tc, wc);
+  }
+  if (int rc = scan_excl(c, P, tc, P->trow.as<uint32_t>(), nb + 1, s)) return rc;
+  if (int rc = scan_excl(c, P, wc, P->wstart.as<uint32_t>(), nb + 1, s)) return rc;
+  uint32_t* hc = P->h_count.as<uint32_t>();
+  CU_TRY(c, cudaMemcpyAsync(hc, P->trow.as<uint32_t>() + nb, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaMemcpyAsync(hc + 1, P->wstart.as<uint32_t>() + nb, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaStreamSynchronize(s));
+  P->n_targets = hc[0];
+  P->m2l_nnz = hc[1];
+  CU_TRY(c, P->tbox.ensure(uint64_t(std::max(P->n_targets, 1u)) * 4));
+  CU_TRY(c, P->woff.ensure(uint64_t(P->n_targets + 1) * 4));
+  CU_TRY(c, P->widx.ensure(uint64_t(std::max(P->m2l_nnz, 1u)) * 4));
+  for (int l = 1; l < L; ++l) {
+    const uint32_t nbox = uint32_t(pow4(l));
+    m2l_fill_kernel<<<blocks(nbox), TB, 0, s>>>(
+        P->conn[l].w_off.as<uint32_t>(), P->conn[l].w_idx.as<uint32_t>(),
+        P->soff.as<uint32_t>() + P->off_base[l], P->eoff.as<uint32_t>() + P->off_base[l], nbox,
+        uint32_t(P->box_base[l]), P->trow.as<uint32_t>(), P->wstart.as<uint32_t>(),
+        P->tbox.as<uint32_t>(), P->woff.as<uint32_t>(), P->widx.as<uint32_t>(),
+        P->m2l_row.as<int32_t>());
+  }
+  CU_TRY(c, cudaMemcpyAsync(P->woff.as<uint32_t>() + P->n_targets, &P->m2l_nnz, 4,
+                            cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaStreamSynchronize(s));
+  c->launches += uint64_t(2 * (L - 1));
+  return FMMCU_OK;
+}
+
+// P2M -> M2M -> M2L -> locals on stream s
+int far_field(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, cudaEvent_t e_up,
+              cudaEvent_t e_m2l) {
+  const int L = P->L;
+  const int P1 = P->p + 1;
+  const uint64_t nb = P->box_base[L];
+  CU_TRY(c, P->out.ensure(nb * P1 * 16));
+  CU_TRY(c, P->loc.ensure(nb * P1 * 16));
+  {
+    const FarArgs a = far_args(P, L - 1);
+    p2m_kernel<<<(a.nbox + kFarWarps - 1) / kFarWarps, kFarWarps * 32, 0, s>>>(
+        a, c->d_src.as<double4>());
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    FarArgs a = far_args(P, l);
+    a.cbase = uint32_t(P->box_base[l + 1]);
+    m2m_kernel<<<(a.nbox + kFarWarps - 1) / kFarWarps, kFarWarps * 32, 0, s>>>(a);
+  }
+  CU_TRY(c, cudaEventRecord(e_up, s));
+  CU_TRY(c, P->m2l_sum.ensure(uint64_t(std::max(P->n_targets, 1u)) * P1 * 16));
+  CU_TRY(c, P->flag.ensure(8));
+  CU_TRY(c, cudaMemsetAsync(P->flag.p, 0, 8, s));
+  if (P->n_targets) {
+    if (int rc = m2l_table(c, P->p, P->kernel, s)) return rc;
+    M2LArgs m{};
+    m.p = P->p;
+    m.kernel = P->kernel;
+    m.centers = P->center.as<double2>();
+    m.coeffs = P->out.as<double2>();
+    m.target_box = P->tbox.as<uint32_t>();
+    m.weak_off = P->woff.as<uint32_t>();
+    m.weak_idx = P->widx.as<uint32_t>();
+    m.table = c->m_table.as<double>();
+    m.n_targets = P->n_targets;
+    m.big_w2 = std::pow(10.0, 500.0 / double(P->p + 2));
+    m.out = P->m2l_sum.as<double2>();
+    m.singular = P->flag.as<int>();
+    m2l_batched_kernel<<<(P->n_targets + kM2LWarps - 1) / kM2LWarps, kM2LWarps * 32, 0, s>>>(m);
+  }
+  for (int l = 1; l < L; ++l) {
+    FarArgs a = far_args(P, l);
+    a.cbase = uint32_t(P->box_base[l - 1]);
+    local_kernel<<<(a.nbox + kFarWarps - 1) / kFarWarps, kFarWarps * 32, 0, s>>>(a, l);
+  }
+  CU_TRY(c, cudaEventRecord(e_m2l, s));
+  CU_TRY(c, cudaGetLastError());
+  c->launches += uint64_t(2 * L + 1);
+  return FMMCU_OK;
+}
+
+float span_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) ms = 0.f;
+  return ms;
+}
+
+}  // namespace
+
+// ================================================================ C ABI ====
+extern "C" {
+
+int fmmcu_fmm_evaluate(fmmcu_ctx* c, const fmmcu_fmm_job* j, fmmcu_fmm_stats* st) {
+  if (!c) return FMMCU_EINVAL;
+  if (!j) return set_err(c, FMMCU_EINVAL, "null fmm job");
+  if (c->inflight || c->m2l_inflight) return set_err(c, FMMCU_ESTATE, "context busy");
+  if (j->n_src == 0 || !j->src_z || !j->src_m) return set_err(c, FMMCU_EINVAL, "empty source set");
+  if (j->n_levels < 1 || j->n_levels > 14) return set_err(c, FMMCU_EINVAL, "n_levels out of range");
+  if (!(j->theta > 0.0 && j->theta < 1.0)) return set_err(c, FMMCU_EINVAL, "theta outside (0,1)");
+  if (j->p < 1 || j->p > kM2LMaxP || j->p + 1 > kFarMaxP1)
+    return set_err(c, FMMCU_EINVAL, "expansion order out of range");
+  if (j->kernel < 0 || j->kernel > 1) return set_err(c, FMMCU_EINVAL, "unknown kernel");
+  if (j->smoother < 0 || j->smoother > 2) return set_err(c, FMMCU_EINVAL, "unknown smoother");
+  if (j->smoother != 0 && !(j->delta > 0.0))
+    return set_err(c, FMMCU_EINVAL, "smoother delta must be > 0");
+  if (j->n_eval > 0 && (!j->eval_y || !j->out)) return set_err(c, FMMCU_EINVAL, "null eval arrays");
+  const auto t_host0 = Clock::now();
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (!c->pipe) {
+    c->pipe = new DevicePipeline();
+    CU_TRY(c, cudaStreamCreateWithFlags(&c->pipe->far, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : c->pipe->ev) CU_TRY(c, cudaEventCreate(&e));
+  }
+  DevicePipeline* P = c->pipe;
+  const uint32_t N = j->n_src, M = j->n_eval;
+  P->N = N;
+  P->M = M;
+  P->L = j->n_levels;
+  P->p = j->p;
+  P->kernel = j->kernel;
+  P->tree_valid = false;
+  cudaStream_t s = c->stream;
+  cudaEvent_t* ev = P->ev;
+  CU_TRY(c, cudaEventRecord(ev[0], s));
+
+  // ---- H2D through pinned chunks; finiteness + self-evaluation detection --
+  CU_TRY(c, P->z.ensure(uint64_t(N) * 16));
+  CU_TRY(c, P->m.ensure(uint64_t(N) * 16));
+  CU_TRY(c, P->hz.ensure(uint64_t(N) * 16));
+  CU_TRY(c, P->hm.ensure(uint64_t(N) * 16));
+  const bool maybe_self = j->eval_sid && M == N;
+  bool self = maybe_self, finite = true;
+  constexpr int64_t kChunk = 1 << 20;
+  double* hz = P->hz.as<double>();
+  double* hm = P->hm.as<double>();
+  for (int64_t c0 = 0; c0 < int64_t(N); c0 += kChunk) {
+    const int64_t c1 = std::min<int64_t>(N, c0 + kChunk);
+    bool same = true, fin = true;
+#pragma omp parallel for schedule(static) reduction(&& : same, fin)
+    for (int64_t i = c0; i < c1; ++i) {
+      const double x = j->src_z[2 * i], y = j->src_z[2 * i + 1];
+      hz[2 * i] = x;
+      hz[2 * i + 1] = y;
+      hm[2 * i] = j->src_m[2 * i];
+      hm[2 * i + 1] = j->src_m[2 * i + 1];
+      fin = fin && std::isfinite(x) && std::isfinite(y);
+      if (maybe_self)
+        same = same && j->eval_sid[i] == i &&
+               std::memcmp(&j->eval_y[2 * i], &j->src_z[2 * i], 16) == 0;
+    }
+    self = self && same;
+    finite = finite && fin;
+    CU_TRY(c, cudaMemcpyAsync(P->z.as<double>() + 2 * c0, hz + 2 * c0, size_t(c1 - c0) * 16,
+                              cudaMemcpyHostToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(P->m.as<double>() + 2 * c0, hm + 2 * c0, size_t(c1 - c0) * 16,
+                              cudaMemcpyHostToDevice, s));
+  }
+  if (!finite) {
+    cudaStreamSynchronize(s);
+    return set_err(c, FMMCU_EINVAL, "build_pyramid: non-finite source position");
+  }
+  P->self_eval = self;
+  uint64_t h2d = uint64_t(N) * 32;
+  if (!self && M) {
+    CU_TRY(c, P->y.ensure(uint64_t(M) * 16));
+    CU_TRY(c, P->hy.ensure(uint64_t(M) * 16));
+    bool fin = true;
+    double* hy = P->hy.as<double>();
+#pragma omp parallel for schedule(static) reduction(&& : fin)
+    for (int64_t i = 0; i < int64_t(M); ++i) {
+      hy[2 * i] = j->eval_y[2 * i];
+      hy[2 * i + 1] = j->eval_y[2 * i + 1];
+      fin = fin && std::isfinite(hy[2 * i]) && std::isfinite(hy[2 * i + 1]);
+    }
+    if (!fin) {
+      cudaStreamSynchronize(s);
+      return set_err(c, FMMCU_EINVAL, "build_pyramid: non-finite eval position");
+    }
+    CU_TRY(c, cudaMemcpyAsync(P->y.p, hy, uint64_t(M) * 16, cudaMemcpyHostToDevice, s));
+    h2d += uint64_t(M) * 16;
+    if (j->eval_sid) {
+      CU_TRY(c, P->sid.ensure(uint64_t(M) * 8));
+      CU_TRY(c, P->hsid.ensure(uint64_t(M) * 8));
+      par_memcpy(P->hsid.p, j->eval_sid, uint64_t(M) * 8);
+      CU_TRY(c, cudaMemcpyAsync(P->sid.p, P->hsid.p, uint64_t(M) * 8, cudaMemcpyHostToDevice, s));
+      h2d += uint64_t(M) * 8;
+    }
+  }
+  CU_TRY(c, cudaEventRecord(ev[1], s));
+
+  // ---- pyramid + connectivity ------------------------------------------------
+  if (int rc = build_pyramid_dev(c, P, j->theta, s)) return rc;
+  CU_TRY(c, cudaEventRecord(ev[2], s));
+  if (int rc = build_connectivity_dev(c, P, j->theta, s)) return rc;
+  P->tree_valid = true;
+  const int L = P->L;
+  const uint32_t nleaf = uint32_t(pow4(L - 1));
+
+  // ---- permuted inputs into the P2P staging of the context ----------------
+  CU_TRY(c, c->d_src.ensure(uint64_t(N) * 32));
+  CU_TRY(c, c->d_evy.ensure(uint64_t(std::max(M, 1u)) * 16));
+  CU_TRY(c, c->d_eself.ensure(uint64_t(std::max(M, 1u)) * 4));
+  pack_sources_kernel<<<blocks(N), TB, 0, s>>>(P->z.as<double2>(), P->m.as<double2>(),
+                                               P->perm.as<uint32_t>(), N, c->d_src.as<double4>());
+  if (M) {
+    inverse_perm_kernel<<<blocks(N), TB, 0, s>>>(P->perm.as<uint32_t>(), N, P->inv.as<uint32_t>());
+    permute_evals_kernel<<<blocks(M), TB, 0, s>>>(
+        self ? P->z.as<double2>() : P->y.as<double2>(),
+        (!self && j->eval_sid) ? P->sid.as<int64_t>() : nullptr, self ? 1 : 0,
+        P->eperm.as<uint32_t>(), P->inv.as<uint32_t>(), M, N, c->d_evy.as<double2>(),
+        c->d_eself.as<uint32_t>());
+  }
+  c->launches += 3;
+  CU_TRY(c, cudaEventRecord(ev[3], s));  // partition done
+
+  // ---- far field on its own stream (overlaps the host work list + P2P) ----
+  if (int rc = far_setup(c, P)) return rc;
+  if (int rc = m2l_lists(c, P, s)) return rc;
+  CU_TRY(c, cudaEventRecord(ev[4], s));
+  CU_TRY(c, cudaStreamWaitEvent(P->far, ev[4], 0));
+  CU_TRY(c, cudaEventRecord(ev[5], P->far));
+  if (int rc = far_field(c, P, P->far, ev[6], ev[7])) return rc;
+
+  // ---- near field: host work list from the finest CSR, then the P2P kernels
+  std::vector<uint32_t> pt(nleaf + 1), evo(nleaf + 1), so(nleaf + 1);
+  const LevelConnDev& fc = P->conn[L - 1];
+  std::vector<uint32_t> si(std::max(fc.s_nnz, 1u));
+  CU_TRY(c, cudaMemcpyAsync(pt.data(), P->soff.as<uint32_t>() + P->off_base[L - 1],
+                            (nleaf + 1) * 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaMemcpyAsync(evo.data(), P->eoff.as<uint32_t>() + P->off_base[L - 1],
+                            (nleaf + 1) * 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaMemcpyAsync(so.data(), fc.s_off.p, (nleaf + 1) * 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaMemcpyAsync(si.data(), fc.s_idx.p, uint64_t(fc.s_nnz) * 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaStreamSynchronize(s));
+  fmmcu_p2p_job pj{};
+  pj.n_leaves = nleaf;
+  pj.n_src = N;
+  pj.n_eval = M;
+  pj.pt_off = pt.data();
+  pj.ev_off = evo.data();
+  pj.strong_off = so.data();
+  pj.strong_idx = si.data();
+  pj.kernel = j->kernel;
+  pj.smoother = j->smoother;
+  pj.delta = j->delta;
+  pj.mode = FMMCU_MODE_FAST;
+  pj.leaf_begin = 0;
+  pj.leaf_end = nleaf;
+  c->n_leaves = nleaf;
+  c->n_src = N;
+  c->n_eval = M;
+  c->kernel = j->kernel;
+  c->smoother = j->smoother;
+  c->mode = FMMCU_MODE_FAST;
+  c->delta = j->delta;
+  c->self_layout = false;
+  c->ext_out = nullptr;
+  if (int rc = build_worklist(c, &pj)) return rc;
+  if (int rc = stage_csr(c, &pj)) return rc;
+  CU_TRY(c, cudaEventRecord(ev[8], s));
+  int nk = 0;
+  if (int rc = run_kernels(c, 0, nleaf, FMMCU_MODE_FAST, &nk)) return rc;
+  CU_TRY(c, cudaEventRecord(ev[9], s));
+
+  // ---- assembly + D2H ---------------------------------------------------------
+  CU_TRY(c, cudaStreamWaitEvent(s, ev[7], 0));
+  CU_TRY(c, P->res.ensure(uint64_t(std::max(M, 1u)) * 16));
+  if (M) {
+    FarArgs a = far_args(P, L - 1);
+    assemble_kernel<<<blocks(M), TB, 0, s>>>(a, c->out_ptr(), c->d_evy.as<double2>(),
+                                             P->eperm.as<uint32_t>(), M, L >= 2 ? 1 : 0,
+                                             P->res.as<double2>());
+    c->launches += 1;
+  }
+  CU_TRY(c, P->h_flag.ensure(16));
+  CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.p, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, s));
+  cudaPointerAttributes pa{};
+  const bool direct = M && cudaPointerGetAttributes(&pa, j->out) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (M) {
+    if (direct) {
+      CU_TRY(c, cudaMemcpyAsync(j->out, P->res.p, uint64_t(M) * 16, cudaMemcpyDeviceToHost, s));
+    } else {
+      CU_TRY(c, P->hres.ensure(uint64_t(M) * 16));
+      CU_TRY(c, cudaMemcpyAsync(P->hres.p, P->res.p, uint64_t(M) * 16, cudaMemcpyDeviceToHost, s));
+    }
+  }
+  CU_TRY(c, cudaEventRecord(ev[10], s));
+  CU_TRY(c, cudaEventSynchronize(ev[10]));
+  CU_TRY(c, cudaGetLastError());
+  if (M && !direct) par_memcpy(j->out, P->hres.p, uint64_t(M) * 16);
+  if (*P->h_flag.as<int>())
+    return set_err(c, FMMCU_ESINGULAR, "m2l: target center coincides with source center");
+  if (st) {
+    const uint64_t hits = *c->h_hits.as<unsigned long long>();
+    st->p2p_pairs = c->leaf_work[nleaf] - hits;
+    st->m2l_ops = P->m2l_nnz;
+    st->p2m_points = N;
+    st->l2p_points = L >= 2 ? M : 0;
+    st->t_upload = 1e-3 * span_ms(ev[0], ev[1]);
+    st->t_tree = 1e-3 * span_ms(ev[1], ev[2]);
+    st->t_connect = 1e-3 * span_ms(ev[2], ev[3]);
+    st->t_p2m_upward = 1e-3 * span_ms(ev[5], ev[6]);
+    st->t_m2l = 1e-3 * span_ms(ev[6], ev[7]);
+    st->t_p2p = 1e-3 * span_ms(ev[8], ev[9]);
+    st->t_device = 1e-3 * span_ms(ev[0], ev[10]);
+    st->t_total = std::chrono::duration<double>(Clock::now() - t_host0).count();
+    st->h2d_bytes = h2d;
+    st->d2h_bytes = uint64_t(M) * 16;
+  }
+  return FMMCU_OK;
+}
+
+int fmmcu_fmm_tree_level(fmmcu_ctx* c, int level, uint32_t* n_boxes, double* f64, uint32_t* u32) {
+  if (!c || !n_boxes) return FMMCU_EINVAL;
+  DevicePipeline* P = c->pipe;
+  if (!P || !P->tree_valid) return set_err(c, FMMCU_ESTATE, "no device tree");
+  if (level < 0 || level >= P->L) return set_err(c, FMMCU_EINVAL, "level out of range");
+  const uint32_t nb = uint32_t(pow4(level));
+  *n_boxes = nb;
+  if (!f64 && !u32) return FMMCU_OK;
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  std::vector<double2> cen(nb);
+  std::vector<double> hw(nb), hh(nb), r(nb);
+  std::vector<uint32_t> so(nb + 1), eo(nb + 1);
+  const uint64_t bb = P->box_base[level], ob = P->off_base[level];
+  CU_TRY(c, cudaMemcpy(cen.data(), P->center.as<double2>() + bb, nb * 16, cudaMemcpyDeviceToHost));
+  CU_TRY(c, cudaMemcpy(hw.data(), P->hw.as<double>() + bb, nb * 8, cudaMemcpyDeviceToHost));
+  CU_TRY(c, cudaMemcpy(hh.data(), P->hh.as<double>() + bb, nb * 8, cudaMemcpyDeviceToHost));
+  CU_TRY(c, cudaMemcpy(r.data(), P->radius.as<double>() + bb, nb * 8, cudaMemcpyDeviceToHost));
+  CU_TRY(c, cudaMemcpy(so.data(), P->soff.as<uint32_t>() + ob, (nb + 1) * 4, cudaMemcpyDeviceToHost));
+  CU_TRY(c, cudaMemcpy(eo.data(), P->eoff.as<uint32_t>() + ob, (nb + 1) * 4, cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < nb; ++i) {
+    if (f64) {
+      f64[5 * i + 0] = cen[i].x;
+      f64[5 * i + 1] = cen[i].y;
+      f64[5 * i + 2] = hw[i];
+      f64[5 * i + 3] = hh[i];
+      f64[5 * i + 4] = r[i];
+    }
+    if (u32) {
+      u32[4 * i + 0] = so[i];
+      u32[4 * i + 1] = so[i + 1];
+      u32[4 * i + 2] = eo[i];
+      u32[4 * i + 3] = eo[i + 1];
+    }
+  }
+  return FMMCU_OK;
+}
+
+int fmmcu_fmm_tree_perm(fmmcu_ctx* c, uint32_t* perm, uint32_t* eval_perm) {
+  if (!c) return FMMCU_EINVAL;
+  DevicePipeline* P = c->pipe;
+  if (!P || !P->tree_valid) return set_err(c, FMMCU_ESTATE, "no device tree");
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (perm) CU_TRY(c, cudaMemcpy(perm, P->perm.p, uint64_t(P->N) * 4, cudaMemcpyDeviceToHost));
+  if (eval_perm && P->M)
+    CU_TRY(c, cudaMemcpy(eval_perm, P->eperm.p, uint64_t(P->M) * 4, cudaMemcpyDeviceToHost));
+  return FMMCU_OK;
+}
+
+int fmmcu_fmm_tree_lists(fmmcu_ctx* c, int level, int weak, uint64_t* nnz, uint32_t* off,
+                         uint32_t* idx) {
+  if (!c || !nnz) return FMMCU_EINVAL;
+  DevicePipeline* P = c->pipe;
+  if (!P || !P->tree_valid) return set_err(c, FMMCU_ESTATE, "no device tree");
+  if (level < 0 || level >= P->L) return set_err(c, FMMCU_EINVAL, "level out of range");
+  const LevelConnDev& lc = P->conn[level];
+  *nnz = weak ? lc.w_nnz : lc.s_nnz;
+  CU_TRY(c, cudaSetDevice(c->device));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  const uint64_t nb = pow4(level);
+  if (off)
+    CU_TRY(c, cudaMemcpy(off, (weak ? lc.w_off : lc.s_off).p, (nb + 1) * 4, cudaMemcpyDeviceToHost));
+  if (idx && *nnz)
+    CU_TRY(c, cudaMemcpy(idx, (weak ? lc.w_idx : lc.s_idx).p, *nnz * 4, cudaMemcpyDeviceToHost));
+  return FMMCU_OK;
+}
+
+int fmmcu_hypot_batch(fmmcu_ctx* c, const double* xy, uint32_t n, double* out) {
+  if (!c || (n && (!xy || !out))) return FMMCU_EINVAL;
+  if (!n) return FMMCU_OK;
+  CU_TRY(c, cudaSetDevice(c->device));
+  double2* d_in = nullptr;
+  double* d_out = nullptr;
+  CU_TRY(c, cudaMalloc(&d_in, uint64_t(n) * 16));
+  CU_TRY(c, cudaMalloc(&d_out, uint64_t(n) * 8));
+  cudaMemcpy(d_in, xy, uint64_t(n) * 16, cudaMemcpyHostToDevice);
+  hypot_batch_kernel<<<blocks(n), TB>>>(d_in, n, d_out);
+  cudaError_t e = cudaMemcpy(out, d_out, uint64_t(n) * 8, cudaMemcpyDeviceToHost);
+  cudaFree(d_in);
+  cudaFree(d_out);
+  CU_TRY(c, e);
+  c->launches += 1;
+  return FMMCU_OK;
+}
+
+}  // extern "C"

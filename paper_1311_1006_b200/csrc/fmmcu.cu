@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "fmm_cuda.h"
+#include "fmmcu_internal.cuh"
 #include "m2l_kernels.cuh"
 #include "p2p_kernels.cuh"
 #include "p2p_warp.cuh"
@@ -66,142 +67,9 @@ constexpr size_t tile_smem(int threads, int e, int tile) {
          size_t(2 * threads) * e * 16;
 }
 
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  cudaError_t ensure(size_t bytes) {
-    if (bytes <= cap) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-    size_t want = std::max<size_t>(bytes, 256);
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) cap = want;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
-
-struct HostBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  cudaError_t ensure(size_t bytes) {
-    if (bytes <= cap) return cudaSuccess;
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    cap = 0;
-    size_t want = std::max<size_t>(bytes, 256);
-    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocPortable);
-    if (e == cudaSuccess) cap = want;
-    return e;
-  }
-  void release() {
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    cap = 0;
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
-
-using Clock = std::chrono::steady_clock;
-
-// Host memcpy split across the OpenMP threads (pinned staging copies).
-void par_memcpy(void* dst, const void* src, size_t bytes) {
-  if (bytes < (size_t(1) << 22)) {
-    if (bytes) std::memcpy(dst, src, bytes);
-    return;
-  }
-  const int64_t blocks = int64_t((bytes + (size_t(1) << 20) - 1) >> 20);
-#pragma omp parallel for schedule(static)
-  for (int64_t b = 0; b < blocks; ++b) {
-    const size_t o = size_t(b) << 20;
-    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
-                std::min<size_t>(size_t(1) << 20, bytes - o));
-  }
-}
-
 }  // namespace
 
-struct fmmcu_ctx {
-  int device = 0;
-  cudaStream_t own_stream = nullptr;
-  cudaStream_t stream = nullptr;  // current (own or external)
-  cudaStream_t m2l_stream = nullptr;
-  cudaStream_t d2h_stream = nullptr;  // potentials D2H, overlapping the next slice's kernels
-  static constexpr int kMaxSlices = 8;
-  cudaEvent_t ev_kslice[kMaxSlices] = {}, ev_cslice[kMaxSlices] = {};
-  int n_slices = 0;
-  uint32_t slice_eb[kMaxSlices + 1] = {};
-  bool direct_out = false;  // job->out is page-locked: D2H lands in it directly
-  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_m2l0 = nullptr, ev_m2l1 = nullptr;
-  std::string err;
-  uint64_t launches = 0;
-
-  // staged job (device)
-  DevBuf d_src, d_evy, d_eself, d_pt, d_ev, d_soff, d_sidx, d_items, d_fin, d_out, d_partial,
-      d_hits, d_seg, d_counter, d_evr;
-  // pinned staging
-  HostBuf h_src, h_evy, h_eself, h_out, h_hits, h_csr;
-  std::vector<uint32_t> invperm;
-  // host mirror of the staged job
-  uint32_t n_leaves = 0, n_src = 0, n_eval = 0;
-  int kernel = 0, smoother = 0, mode = 0;
-  double delta = 0.0;
-  std::vector<uint32_t> ev_off;        // host copy
-  std::vector<uint64_t> leaf_work;     // prefix of nt * S
-  std::vector<P2PItem> items;
-  std::vector<uint32_t> item_first;    // [n_leaves + 1]
-  std::vector<P2PFinal> fins;
-  std::vector<uint32_t> fin_first;     // [n_leaves + 1]
-  bool staged = false;
-  bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
-  bool warp_items = false;     // work list built for p2p_warp_kernel
-  int warp_e = 4;              // evals per lane of the warp kernel (choose_warp_e)
-  uint64_t partial_evals = 0;  // partial-sum slots of split items
-  bool trace = std::getenv("FMMCU_TRACE") != nullptr;
-  double2* ext_out = nullptr;  // caller-bound output (torch tensor), or null
-  double2* out_ptr() const { return ext_out ? ext_out : d_out.as<double2>(); }
-
-  // in-flight reference-facing launch
-  bool inflight = false;
-  fmmcu_p2p_job job{};
-  uint32_t run_lb = 0, run_le = 0;
-  double prep_seconds = 0.0;
-  Clock::time_point t_evstart{};
-  uint64_t run_total_pairs = 0;
-  uint64_t h2d_bytes = 0, d2h_bytes = 0;
-
-  // m2l
-  DevBuf m_centers, m_coeffs, m_tbox, m_woff, m_widx, m_table, m_out, m_flag;
-  HostBuf mh_out, mh_flag;
-  int table_p = -1, table_kernel = -1;
-  bool m2l_inflight = false;
-  fmmcu_m2l_job m2l_job{};
-  uint64_t m2l_ops = 0;
-  double m2l_prep = 0.0;
-};
-
-#define CU_TRY(ctx, expr)                                                          \
-  do {                                                                            \
-    cudaError_t _e = (expr);                                                      \
-    if (_e != cudaSuccess) {                                                      \
-      (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(_e);            \
-      return _e == cudaErrorMemoryAllocation ? FMMCU_ENOMEM : FMMCU_ECUDA;        \
-    }                                                                             \
-  } while (0)
-
-namespace {
+namespace fmmcu::detail {
 
 int set_err(fmmcu_ctx* c, int code, const std::string& msg) {
   c->err = msg;
@@ -540,7 +408,6 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   if (int rc = validate(c, j)) return rc;
   CU_TRY(c, cudaSetDevice(c->device));
   const uint32_t nl = j->n_leaves, ns = j->n_src, ne = j->n_eval;
-  const uint32_t nnz = j->strong_off[nl];
   c->n_leaves = nl;
   c->n_src = ns;
   c->n_eval = ne;
@@ -627,6 +494,16 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // ---- work list (built concurrently with the source packing above) -------
   if (int rc = worklist.get()) return rc;
   tr.mark("worklist");
+  if (int rc = stage_csr(c, j)) return rc;
+  tr.mark("csr+worklist h2d");
+  return FMMCU_OK;
+}
+
+int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  const uint32_t nl = j->n_leaves, ne = j->n_eval;
+  const uint32_t nnz = j->strong_off[nl];
+  const bool self_layout = c->self_layout;
+  cudaStream_t s = c->stream;
   // ---- device buffers -------------------------------------------------------
   CU_TRY(c, c->d_pt.ensure(size_t(nl + 1) * 4));
   CU_TRY(c, c->d_ev.ensure(size_t(nl + 1) * 4));
@@ -659,7 +536,7 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const size_t o_si = put(j->strong_idx, size_t(nnz) * 4);
   const size_t o_it = put(c->items.data(), c->items.size() * sizeof(P2PItem));
   const size_t o_fi = put(c->fins.data(), c->fins.size() * sizeof(P2PFinal));
-  c->h2d_bytes = uint64_t(ns) * 32 + (self_layout ? 0 : uint64_t(ne) * 20) + o;
+  c->h2d_bytes = uint64_t(c->n_src) * 32 + (self_layout ? 0 : uint64_t(ne) * 20) + o;
 
   CU_TRY(c, cudaMemcpyAsync(c->d_pt.p, hc + o_pt, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
   CU_TRY(c, cudaMemcpyAsync(c->d_ev.p, hc + o_ev, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
@@ -689,14 +566,13 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     c->launches += 1;
   }
   CU_TRY(c, cudaGetLastError());
-  tr.mark("csr+worklist h2d");
   c->staged = true;
   return FMMCU_OK;
 }
 
 // Kernels over [lb, le) of the staged job.
 int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
-                bool reset_hits = true) {
+                bool reset_hits) {
   cudaStream_t s = c->stream;
   int n = 0;
   if (reset_hits) CU_TRY(c, cudaMemsetAsync(c->d_hits.p, 0, 8, s));
@@ -749,7 +625,35 @@ __global__ void dfma_peak_kernel(double* sink, int iters, double seed) {
   if (r == 12345.678) sink[0] = r;
 }
 
-}  // namespace
+// binomial table T[k][l] of the M2L kernel (Pascal recurrence in doubles,
+// as the reference's table, expansion.cpp:12-26)
+int m2l_table(fmmcu_ctx* c, int p, int kernel, cudaStream_t stream) {
+  (void)stream;
+  if (c->table_p == p && c->table_kernel == kernel) return FMMCU_OK;
+  const int P1 = p + 1;
+  const int rows = 2 * P1 + 2;
+  std::vector<double> pas(size_t(rows) * rows, 0.0);
+  for (int i = 0; i < rows; ++i) {
+    pas[size_t(i) * rows] = 1.0;
+    for (int k = 1; k <= i; ++k)
+      pas[size_t(i) * rows + k] = pas[size_t(i - 1) * rows + k - 1] + pas[size_t(i - 1) * rows + k];
+  }
+  std::vector<double> T(size_t(P1) * P1, 0.0);
+  for (int k = 0; k < P1; ++k)
+    for (int l = 0; l < P1; ++l) {
+      if (kernel == 0) T[size_t(k) * P1 + l] = pas[size_t(l + k) * rows + k];
+      else if (k >= 1) T[size_t(k) * P1 + l] = pas[size_t(l + k - 1) * rows + (k - 1)];
+    }
+  CU_TRY(c, c->m_table.ensure(T.size() * 8));
+  CU_TRY(c, cudaMemcpy(c->m_table.p, T.data(), T.size() * 8, cudaMemcpyHostToDevice));
+  c->table_p = p;
+  c->table_kernel = kernel;
+  return FMMCU_OK;
+}
+
+}  // namespace fmmcu::detail
+
+using namespace fmmcu::detail;
 
 // =============================================================== C ABI ====
 extern "C" {
@@ -816,6 +720,8 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->m2l_stream);
     cudaStreamSynchronize(c->d2h_stream);
+    fmmcu::destroy_pipeline(c->pipe);
+    c->pipe = nullptr;
     for (DevBuf* b : {&c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
                       &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter, &c->d_evr,
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
@@ -1083,26 +989,7 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
       return set_err(c, FMMCU_EINVAL, "bad m2l target list");
   for (uint32_t q = 0; q < nnz; ++q)
     if (j->weak_idx[q] >= nb) return set_err(c, FMMCU_EINVAL, "bad m2l weak index");
-  // binomial table T[k][l] (Pascal recurrence in doubles, as the reference's table)
-  if (c->table_p != j->p || c->table_kernel != j->kernel) {
-    const int rows = 2 * P1 + 2;
-    std::vector<double> pas(size_t(rows) * rows, 0.0);
-    for (int i = 0; i < rows; ++i) {
-      pas[size_t(i) * rows] = 1.0;
-      for (int k = 1; k <= i; ++k)
-        pas[size_t(i) * rows + k] = pas[size_t(i - 1) * rows + k - 1] + pas[size_t(i - 1) * rows + k];
-    }
-    std::vector<double> T(size_t(P1) * P1, 0.0);
-    for (int k = 0; k < P1; ++k)
-      for (int l = 0; l < P1; ++l) {
-        if (j->kernel == 0) T[size_t(k) * P1 + l] = pas[size_t(l + k) * rows + k];
-        else if (k >= 1) T[size_t(k) * P1 + l] = pas[size_t(l + k - 1) * rows + (k - 1)];
-      }
-    CU_TRY(c, c->m_table.ensure(T.size() * 8));
-    CU_TRY(c, cudaMemcpy(c->m_table.p, T.data(), T.size() * 8, cudaMemcpyHostToDevice));
-    c->table_p = j->p;
-    c->table_kernel = j->kernel;
-  }
+  if (int rc = m2l_table(c, j->p, j->kernel, c->m2l_stream)) return rc;
   CU_TRY(c, c->m_centers.ensure(size_t(nb) * 16));
   CU_TRY(c, c->m_coeffs.ensure(size_t(nb) * P1 * 16));
   CU_TRY(c, c->m_tbox.ensure(size_t(nt) * 4));

@@ -1,0 +1,189 @@
+// fmm-b200 — internals shared by the translation units of libfmmcuda.so
+// (fmmcu.cu: near field + M2L; fmm_device.cu: the device FMM pipeline).
+// Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fmm_cuda.h"
+#include "p2p_kernels.cuh"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace fmmcu {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocPortable);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+using Clock = std::chrono::steady_clock;
+
+// Host memcpy split across the OpenMP threads (pinned staging copies).
+inline void par_memcpy(void* dst, const void* src, size_t bytes) {
+  if (bytes < (size_t(1) << 22)) {
+    if (bytes) std::memcpy(dst, src, bytes);
+    return;
+  }
+  const int64_t blocks = int64_t((bytes + (size_t(1) << 20) - 1) >> 20);
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < blocks; ++b) {
+    const size_t o = size_t(b) << 20;
+    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                std::min<size_t>(size_t(1) << 20, bytes - o));
+  }
+}
+
+
+struct DevicePipeline;  // fmm_device.cu
+void destroy_pipeline(DevicePipeline* p);
+
+}  // namespace fmmcu
+
+using fmmcu::Clock;
+using fmmcu::DevBuf;
+using fmmcu::HostBuf;
+using fmmcu::par_memcpy;
+using fmmcu::P2PFinal;
+using fmmcu::P2PItem;
+
+struct fmmcu_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // current (own or external)
+  cudaStream_t m2l_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr;  // potentials D2H, overlapping the next slice's kernels
+  static constexpr int kMaxSlices = 8;
+  cudaEvent_t ev_kslice[kMaxSlices] = {}, ev_cslice[kMaxSlices] = {};
+  int n_slices = 0;
+  uint32_t slice_eb[kMaxSlices + 1] = {};
+  bool direct_out = false;  // job->out is page-locked: D2H lands in it directly
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_m2l0 = nullptr, ev_m2l1 = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+
+  // staged job (device)
+  DevBuf d_src, d_evy, d_eself, d_pt, d_ev, d_soff, d_sidx, d_items, d_fin, d_out, d_partial,
+      d_hits, d_seg, d_counter, d_evr;
+  // pinned staging
+  HostBuf h_src, h_evy, h_eself, h_out, h_hits, h_csr;
+  std::vector<uint32_t> invperm;
+  // host mirror of the staged job
+  uint32_t n_leaves = 0, n_src = 0, n_eval = 0;
+  int kernel = 0, smoother = 0, mode = 0;
+  double delta = 0.0;
+  std::vector<uint32_t> ev_off;        // host copy
+  std::vector<uint64_t> leaf_work;     // prefix of nt * S
+  std::vector<P2PItem> items;
+  std::vector<uint32_t> item_first;    // [n_leaves + 1]
+  std::vector<P2PFinal> fins;
+  std::vector<uint32_t> fin_first;     // [n_leaves + 1]
+  bool staged = false;
+  bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
+  bool warp_items = false;     // work list built for p2p_warp_kernel
+  int warp_e = 4;              // evals per lane of the warp kernel (choose_warp_e)
+  uint64_t partial_evals = 0;  // partial-sum slots of split items
+  bool trace = std::getenv("FMMCU_TRACE") != nullptr;
+  double2* ext_out = nullptr;  // caller-bound output (torch tensor), or null
+  double2* out_ptr() const { return ext_out ? ext_out : d_out.as<double2>(); }
+
+  // in-flight reference-facing launch
+  bool inflight = false;
+  fmmcu_p2p_job job{};
+  uint32_t run_lb = 0, run_le = 0;
+  double prep_seconds = 0.0;
+  Clock::time_point t_evstart{};
+  uint64_t run_total_pairs = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
+
+  // m2l
+  DevBuf m_centers, m_coeffs, m_tbox, m_woff, m_widx, m_table, m_out, m_flag;
+  HostBuf mh_out, mh_flag;
+  int table_p = -1, table_kernel = -1;
+  bool m2l_inflight = false;
+  fmmcu_m2l_job m2l_job{};
+  uint64_t m2l_ops = 0;
+  double m2l_prep = 0.0;
+
+  // device FMM pipeline state (fmm_device.cu), created on first use
+  fmmcu::DevicePipeline* pipe = nullptr;
+};
+
+#define CU_TRY(ctx, expr)                                                          \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(_e);            \
+      return _e == cudaErrorMemoryAllocation ? FMMCU_ENOMEM : FMMCU_ECUDA;        \
+    }                                                                             \
+  } while (0)
+
+namespace fmmcu::detail {
+
+int set_err(fmmcu_ctx* c, int code, const std::string& msg);
+P2PArgs make_args(fmmcu_ctx* c);
+// Work list of a job from its host CSR (pt_off, ev_off, strong_off, strong_idx).
+int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j);
+// Device buffers for the CSR + work list, their H2D, the run table and the
+// eval records (needs d_src, d_evy, d_eself filled unless c->self_layout).
+int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j);
+// P2P kernels over leaves [lb, le) of the staged job on c->stream.
+int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
+                bool reset_hits = true);
+// Batched M2L on `stream` from device-resident arrays (see m2l_kernels.cuh).
+int m2l_table(fmmcu_ctx* c, int p, int kernel, cudaStream_t stream);
+
+}  // namespace fmmcu::detail

@@ -54,7 +54,7 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src) {
 constexpr int kM2LWarps = 4;
 constexpr int kM2LMaxP = 96;
 
-__global__ void __launch_bounds__(kM2LWarps * 32) m2l_batched_kernel(const M2LArgs a) {
+static __global__ void __launch_bounds__(kM2LWarps * 32) m2l_batched_kernel(const M2LArgs a) {
   __shared__ double2 s_v[kM2LWarps][kM2LMaxP + 1];
   __shared__ double2 s_pw[kM2LWarps][kM2LMaxP + 2];
   const int lane = threadIdx.x & 31;

@@ -190,7 +190,7 @@ __device__ __forceinline__ const double4* run_unchecked(const double4* p, const 
 }
 
 // seg[q] = (first permuted source slot, source count) of strong entry q.
-__global__ void p2p_segments_kernel(const uint32_t* __restrict__ s_idx,
+static __global__ void p2p_segments_kernel(const uint32_t* __restrict__ s_idx,
                                     const uint32_t* __restrict__ pt_off, uint32_t nnz,
                                     uint2* __restrict__ seg) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -219,7 +219,7 @@ __device__ __forceinline__ uint32_t find_self_entry(const P2PArgs& a, uint32_t l
 }
 
 // One warp per leaf, lanes over its evals.
-__global__ void p2p_evrec_kernel(const P2PArgs a, uint32_t n_leaves, double4* __restrict__ evr) {
+static __global__ void p2p_evrec_kernel(const P2PArgs a, uint32_t n_leaves, double4* __restrict__ evr) {
   const uint32_t leaf = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (leaf >= n_leaves) return;
   for (uint32_t e = a.ev_off[leaf] + (threadIdx.x & 31); e < a.ev_off[leaf + 1]; e += 32) {
@@ -233,7 +233,7 @@ __global__ void p2p_evrec_kernel(const P2PArgs a, uint32_t n_leaves, double4* __
 
 // Self layout (eval e == source slot e): derive the eval arrays from the
 // already uploaded sources instead of uploading them.
-__global__ void p2p_self_evals_kernel(const double4* __restrict__ src, uint32_t n,
+static __global__ void p2p_self_evals_kernel(const double4* __restrict__ src, uint32_t n,
                                       double2* __restrict__ evy, uint32_t* __restrict__ eself) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
@@ -526,7 +526,7 @@ struct P2PFinal {
   uint32_t n_chunks;
 };
 
-__global__ void p2p_finalize_kernel(const P2PFinal* __restrict__ fin, uint32_t n_fin,
+static __global__ void p2p_finalize_kernel(const P2PFinal* __restrict__ fin, uint32_t n_fin,
                                     const double2* __restrict__ partial,
                                     double2* __restrict__ out) {
   const uint32_t f = blockIdx.x;

@@ -1,0 +1,118 @@
+"""Device FMM pipeline parity (needs a B200): fmmcu_fmm_evaluate runs the whole
+FmmEngine::evaluate on the GPU (include/fmm_cuda.h).
+
+Bars:
+  * glibc hypot restated on the device: bitwise equal to libm hypot;
+  * device pyramid (boxes, ranges, perm, eval_perm) and connectivity (strong
+    and weak lists, every level): bitwise equal to the host library, which
+    is itself bit-exact with the compiled reference (tests/test_host_geometry.py);
+  * potentials: <= 1e-12 * max|phi| (normwise) against the CPU evaluate()
+    of the host library (reference semantics), counters identical.
+"""
+import numpy as np
+import pytest
+
+from paper_1311_1006_b200 import _native as N
+from paper_1311_1006_b200 import fmm as F
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = N.CudaContext(0)
+    yield c
+    c.close()
+
+
+def _lattice(n_side, aspect=0.25):
+    g = np.arange(n_side) * (1.0 / n_side)
+    z = (g[:, None] + 1j * g[None, :] * aspect).ravel()
+    return F.SourceSet(z, np.full(len(z), 0.5j))
+
+
+def _cases():
+    yield "uniform20k_L5", F.make_distribution("uniform", 20_000, 1), None, 5, 0.5
+    yield "gauss30k_L6", F.make_distribution("gauss8", 30_000, 3), None, 6, 0.5
+    yield "line8k_L5_t065", F.make_distribution("line", 8_000, 4), None, 5, 0.65
+    yield "lattice_ties_L6", _lattice(120), None, 6, 0.5
+    s = F.make_distribution("random", 5_000, 5)
+    yield "separate_evals_L4", s, F.EvalSet(F.make_distribution("random", 3_000, 6).z * 1.2 - 0.1), 4, 0.5
+    yield "single_level", F.make_distribution("random", 700, 7), None, 1, 0.5
+    yield "two_levels", F.make_distribution("random", 900, 8), None, 2, 0.4
+
+
+def _evals(s, e):
+    return F.EvalSet.self_of(s) if e is None else e
+
+
+def test_device_hypot_matches_libm(ctx):
+    rng = np.random.default_rng(3)
+    n = 1_000_000
+    xy = rng.random((n, 2))
+    xy[: n // 4] *= rng.random((n // 4, 1)) ** 8
+    ex = rng.integers(-1074, 1023, (n // 4, 2)).astype(float)
+    xy[n // 4: n // 2] = rng.random((n // 4, 2)) * 2.0 ** ex
+    xy[n // 2: 3 * n // 4] = (rng.random((n // 4, 2)) - 0.5) * 1e-3
+    got = ctx.hypot(xy)
+    want = np.hypot(xy[:, 0], xy[:, 1])
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("case", list(_cases()), ids=lambda c: c[0])
+def test_device_tree_bitwise_equal_to_host(ctx, case):
+    name, s, e, L, theta = case
+    e = _evals(s, e)
+    host = F.Tree(s, e, L, theta, threads=4)
+    ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=L, theta=theta, p=17)
+    bf, bu, perm, eperm, strong, weak = ctx.fmm_tree(L, s.size(), e.size())
+    for lvl in range(L):
+        assert np.array_equal(bu[lvl], host.boxes_u[lvl]), (name, lvl, "ranges")
+        assert np.array_equal(bf[lvl].view(np.uint64), host.boxes_f[lvl].view(np.uint64)), \
+            (name, lvl, "geometry")
+        for got, want in ((strong[lvl], host.strong[lvl]), (weak[lvl], host.weak[lvl])):
+            assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), (name, lvl)
+    assert np.array_equal(perm, host.perm)
+    assert np.array_equal(eperm, host.eval_perm)
+
+
+@pytest.mark.parametrize("kernel,smoother,delta", [("harmonic", "none", 0.0),
+                                                   ("logarithmic", "none", 0.0),
+                                                   ("harmonic", "gaussian", 0.01)])
+@pytest.mark.parametrize("case", list(_cases())[:5], ids=lambda c: c[0])
+def test_device_potentials_match_cpu_evaluate(ctx, case, kernel, smoother, delta):
+    name, s, e, L, theta = case
+    e = _evals(s, e)
+    cfg = F.FmmConfig(n_levels=L, theta=theta, kernel=kernel, smoother=smoother, delta=delta,
+                      backend="pool", worker_threads=4)
+    ref = F.FmmEngine(cfg).evaluate(s, e)
+    got, st = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=L, theta=theta, p=ref.p,
+                               kernel=N.KERNELS[kernel], smoother=N.SMOOTHERS[smoother],
+                               delta=delta)
+    scale = np.abs(ref.potentials).max()
+    assert np.abs(got - ref.potentials).max() <= TOL * scale, name
+    for k in ("p2p_pairs", "m2l_ops", "p2m_points", "l2p_points"):
+        assert st[k] == ref.counters[k], (name, k)
+
+
+def test_device_pipeline_is_deterministic_and_reusable(ctx):
+    s = F.make_distribution("uniform", 50_000, 11)
+    e = F.EvalSet.self_of(s)
+    a, _ = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=6, theta=0.5, p=17)
+    s2 = F.make_distribution("gauss8", 20_000, 12)
+    ctx.fmm_evaluate(s2.z, s2.m, s2.z, None, n_levels=5, theta=0.5, p=17)
+    b, _ = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=6, theta=0.5, p=17)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_device_pipeline_rejects_bad_input(ctx):
+    s = F.make_distribution("random", 100, 1)
+    z = s.z.copy()
+    z[5] = np.nan
+    with pytest.raises(N.FmmcuError):
+        ctx.fmm_evaluate(z, s.m, s.z, None, n_levels=3, theta=0.5, p=17)
+    with pytest.raises(N.FmmcuError):
+        ctx.fmm_evaluate(s.z, s.m, s.z, None, n_levels=3, theta=1.5, p=17)
+    with pytest.raises(N.FmmcuError):
+        ctx.fmm_evaluate(s.z[:0], s.m[:0], s.z, None, n_levels=3, theta=0.5, p=17)

@@ -92,3 +92,23 @@ def test_oracle_vs_live_reference_random_trees():
         t.free()
         assert opairs == pairs
         assert bitwise(out, ref)
+
+
+def test_hypot_restatement_matches_libm_and_cabs():
+    """glibc 2.39 __hypot restated (oracle/fmm_oracle.c orc_hypot): bitwise
+    equal to libm hypot() and cabs() -- the two entry points the reference
+    uses for box radii and centre distances (geometry.cpp:13-19,100) -- over
+    unit-square magnitudes, tiny ratios, subnormal/huge exponents and signs."""
+    rng = np.random.default_rng(7)
+    n = 400_000
+    xy = rng.random((n, 2))
+    xy[: n // 5] *= rng.random((n // 5, 1)) ** 8
+    xy[n // 5: 2 * n // 5, 1] *= 1e-9
+    ex = rng.integers(-1074, 1023, (n // 5, 2)).astype(float)
+    xy[2 * n // 5: 3 * n // 5] = rng.random((n // 5, 2)) * 2.0 ** ex
+    xy[3 * n // 5: 4 * n // 5] = (rng.random((n // 5, 2)) - 0.5) * 1e-3
+    xy[4 * n // 5:] = rng.integers(-4, 5, (n - 4 * n // 5, 2)) * 0.125
+    special = np.array([[0.0, 0.0], [-0.0, 0.0], [3.0, 4.0], [1e308, 1e308], [5e-324, 5e-324],
+                        [2.0 ** 511, 1.0], [2.0 ** -460, 2.0 ** -460], [1.0, 2.0 ** -54]])
+    bad, _ = O.hypot_check(np.vstack([xy, special]))
+    assert bad == 0
