@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "fmm/backend.hpp"
+#include "fmm/engine.hpp"
 
 struct fmmcu_ctx;
 
@@ -41,6 +42,17 @@ class CudaBackend final : public NearFieldBackend {
                   const std::vector<std::uint32_t>& weak_off,
                   const std::vector<std::uint32_t>& weak_idx, std::vector<cplx>& out);
   std::uint64_t m2l_finish(double* seconds = nullptr);
+
+  // The whole FmmEngine::evaluate on the first device (fmmcu_fmm_evaluate):
+  // potentials in the original eval order, counters, device phase times.
+  struct DeviceEval {
+    WorkCounters counters;
+    double t_upload = 0, t_tree = 0, t_connect = 0, t_p2m_upward = 0, t_m2l = 0, t_p2p = 0,
+           t_device = 0;
+  };
+  DeviceEval fmm_evaluate(const SourceSet& sources, const EvalSet& evals, int n_levels,
+                          double theta, int p, Kernel kernel, const Smoother& smoother,
+                          std::vector<cplx>& out);
 
   std::uint64_t kernel_launches() const;
 

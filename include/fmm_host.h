@@ -16,11 +16,11 @@
  * Config vectors:
  *   cfg_f[6] = theta, tol, p_calibration, smoother delta, throttle latency_s,
  *              throttle throughput
- *   cfg_i[10] = n_levels, kernel (0 harmonic, 1 log), p_rule (0 formula,
+ *   cfg_i[11] = n_levels, kernel (0 harmonic, 1 log), p_rule (0 formula,
  *              1 table), p_override, backend (0 serial, 1 pool, 2 throttled,
  *              3 cuda), worker_threads, task_split_level, smoother kind
  *              (0 none, 1 gaussian, 2 plummer), cuda exact (0/1),
- *              m2l_on_device (0/1)
+ *              m2l_on_device (0/1), device_pipeline (0/1)
  *   timings[8] = PhaseTimings in declaration order; counters[4] = WorkCounters.
  */
 #ifndef FMM_HOST_H_

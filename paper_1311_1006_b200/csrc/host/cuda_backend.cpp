@@ -52,6 +52,48 @@ CudaBackend::~CudaBackend() {
   for (fmmcu_ctx* c : ctx_) fmmcu_destroy(c);
 }
 
+CudaBackend::DeviceEval CudaBackend::fmm_evaluate(const SourceSet& sources, const EvalSet& evals,
+                                                  int n_levels, double theta, int p,
+                                                  Kernel kernel, const Smoother& smoother,
+                                                  std::vector<cplx>& out) {
+  if (inflight_) throw InvalidState("cuda backend: evaluate while a near field is in flight");
+  if (sources.size() > 0xFFFFFFFFull || evals.size() > 0xFFFFFFFFull)
+    throw InvalidInput("device pipeline: more than 2^32 points");
+  out.assign(evals.size(), cplx(0, 0));
+  fmmcu_fmm_job j{};
+  j.n_src = std::uint32_t(sources.size());
+  j.n_eval = std::uint32_t(evals.size());
+  j.src_z = reinterpret_cast<const double*>(sources.z.data());
+  j.src_m = reinterpret_cast<const double*>(sources.m.data());
+  j.eval_y = evals.size() ? reinterpret_cast<const double*>(evals.y.data()) : nullptr;
+  j.eval_sid = evals.source_id.empty() ? nullptr : evals.source_id.data();
+  j.n_levels = n_levels;
+  j.theta = theta;
+  j.p = p;
+  j.kernel = kernel == Kernel::harmonic ? FMMCU_KERNEL_HARMONIC : FMMCU_KERNEL_LOG;
+  j.smoother = smoother.kind == Smoother::Kind::none       ? FMMCU_SMOOTH_NONE
+               : smoother.kind == Smoother::Kind::gaussian ? FMMCU_SMOOTH_GAUSSIAN
+                                                           : FMMCU_SMOOTH_PLUMMER;
+  j.delta = smoother.delta;
+  j.out = evals.size() ? reinterpret_cast<double*>(out.data()) : nullptr;
+  fmmcu_fmm_stats st{};
+  const int rc = fmmcu_fmm_evaluate(ctx_[0], &j, &st);
+  if (rc != FMMCU_OK) raise(ctx_[0], rc, "device pipeline");
+  DeviceEval d;
+  d.counters.p2p_pairs = st.p2p_pairs;
+  d.counters.m2l_ops = st.m2l_ops;
+  d.counters.p2m_points = st.p2m_points;
+  d.counters.l2p_points = st.l2p_points;
+  d.t_upload = st.t_upload;
+  d.t_tree = st.t_tree;
+  d.t_connect = st.t_connect;
+  d.t_p2m_upward = st.t_p2m_upward;
+  d.t_m2l = st.t_m2l;
+  d.t_p2p = st.t_p2p;
+  d.t_device = st.t_device;
+  return d;
+}
+
 std::uint64_t CudaBackend::kernel_launches() const {
   std::uint64_t n = 0;
   for (fmmcu_ctx* c : ctx_) n += fmmcu_kernel_launches(c);

@@ -13,6 +13,7 @@
 //    batched launch that overlaps the device P2P; the host keeps the cheap
 //    L2L chain and adds the device M2L sums per box (local = L2L(parent) +
 //    sum_w M2L(w)).  m2l_ops is identical to the CPU path.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 
@@ -313,12 +314,44 @@ EvalResult FmmEngine::evaluate(const SourceSet& sources, const EvalSet& evals) {
   if (cfg_.m2l_on_device && cfg_.backend != BackendKind::cuda)
     throw InvalidParameter("evaluate: m2l_on_device requires the cuda backend");
 
+  if (cfg_.device_pipeline && cfg_.backend != BackendKind::cuda)
+    throw InvalidParameter("evaluate: device_pipeline requires the cuda backend");
+
   EvalResult res;
   res.p = cfg_.expansion_order();
   const int p = res.p;
   const int threads = cfg_.worker_threads;
   PhaseTimings& T = res.timings;
   const auto t_start = Clock::now();
+
+  if (cfg_.device_pipeline) {
+    // everything on the first device (fmmcu_fmm_evaluate); the reference's
+    // phase split is reported from device event spans
+    auto* cb = dynamic_cast<CudaBackend*>(backend_.get());
+    CudaBackend::DeviceEval d;
+    try {
+      d = cb->fmm_evaluate(sources, evals, cfg_.n_levels, cfg_.theta, p, cfg_.kernel,
+                           cfg_.smoother, res.potentials);
+    } catch (const SingularConfiguration&) {
+      throw;
+    } catch (const InvalidInput&) {
+      throw;
+    } catch (const std::exception& e) {
+      throw BackendError("device pipeline", e.what());
+    }
+    res.counters = d.counters;
+    T.t_partition = d.t_upload + d.t_tree + d.t_connect;
+    T.t_p2m = d.t_p2m_upward;
+    T.t_upward = 0.0;
+    T.t_m2l = d.t_m2l;
+    T.t_p2p = d.t_p2p;
+    T.t_total = since(t_start);
+    T.t_q = T.t_partition + T.t_p2m + T.t_upward +
+            std::max(0.0, d.t_device - T.t_partition - std::max(T.t_p2p, T.t_p2m + T.t_m2l));
+    T.cpu_wait = 0.0;
+    if (observer_) observer_(*this, res);
+    return res;
+  }
 
   // ---- partition ------------------------------------------------------------
   const Pyramid pyr = build_pyramid(sources, evals, cfg_.n_levels, threads);

@@ -269,13 +269,15 @@ class FmmConfig:
     devices: tuple = (0,)
     exact: bool = False
     m2l_on_device: bool = False
+    device_pipeline: bool = False
 
     def pack(self):
         f = np.array([self.theta, self.tol, self.p_calibration, self.delta,
                       self.throttle_latency_s, self.throttle_throughput])
         i = np.array([self.n_levels, KERNEL[self.kernel], PRULE[self.p_rule], self.p_override,
                       BACKEND[self.backend], self.worker_threads, self.task_split_level,
-                      SMOOTHER[self.smoother], int(self.exact), int(self.m2l_on_device)],
+                      SMOOTHER[self.smoother], int(self.exact), int(self.m2l_on_device),
+                      int(self.device_pipeline)],
                      dtype=np.int32)
         d = np.asarray(self.devices, dtype=np.int32)
         return f, i, d

@@ -104,3 +104,34 @@ def test_vortex_sheet_steps_cuda_vs_pool():
                                want_positions=True)
     assert np.array_equal(tr_c[:, 7], tr_p[:, 7])  # identical pair counts per step
     assert np.abs(pos_c - pos_p).max() <= 1e-12 * np.abs(pos_p).max()
+
+
+def test_engine_device_pipeline_vs_reference_golden(golden_trees):
+    """FmmConfig.device_pipeline: the whole evaluate() on the GPU against the
+    reference's own evaluate() outputs (golden fixtures): counters identical,
+    potentials <= 1e-12 normwise."""
+    for name, d in golden_trees.items():
+        s, e = _sets(d)
+        eng = F.FmmEngine(F.FmmConfig(theta=float(d["theta"]), n_levels=int(d["n_levels"]),
+                                      backend="cuda", device_pipeline=True))
+        r = eng.evaluate(s, e)
+        assert [r.counters[k] for k in F.COUNTER_KEYS] == d["eval_counters"].tolist(), name
+        assert normwise(F._c2(r.potentials), d["eval_pot"]) <= 1e-12, name
+        assert r.timings["t_total"] > 0 and r.timings["t_p2p"] > 0
+
+
+@pytest.mark.parametrize("dist,n,L", [("uniform", 200_000, 7), ("gauss8", 200_000, 8)])
+def test_engine_device_pipeline_vs_pool(dist, n, L):
+    s = F.make_distribution(dist, n, 5)
+    e = F.EvalSet.self_of(s)
+    ref = F.FmmEngine(F.FmmConfig(n_levels=L, backend="pool", worker_threads=8)).evaluate(s, e)
+    r = F.FmmEngine(F.FmmConfig(n_levels=L, backend="cuda", device_pipeline=True)).evaluate(s, e)
+    assert r.counters == ref.counters
+    assert np.abs(r.potentials - ref.potentials).max() <= 1e-12 * np.abs(ref.potentials).max()
+
+
+def test_engine_device_pipeline_requires_cuda_backend():
+    s = F.make_distribution("uniform", 1000, 1)
+    with pytest.raises(F.InvalidParameter):
+        F.FmmEngine(F.FmmConfig(n_levels=3, backend="pool", device_pipeline=True)).evaluate(
+            s, F.EvalSet.self_of(s))
