@@ -11,6 +11,7 @@
 
 #include <cstdint>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fmm/backend.hpp"
@@ -60,6 +61,7 @@ class CudaBackend final : public NearFieldBackend {
   CudaSettings cs_;
   std::vector<fmmcu_ctx*> ctx_;
   bool inflight_ = false;
+  std::thread fill_;  // zero fill of the caller's near-field vector (launch -> finish)
   // flattened job (must outlive the device work)
   std::vector<std::uint32_t> pt_off_, ev_off_, s_off_, s_idx_;
 };

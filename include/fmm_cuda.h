@@ -183,6 +183,11 @@ typedef struct {
 } fmmcu_fmm_stats;
 
 int fmmcu_fmm_evaluate(fmmcu_ctx *ctx, const fmmcu_fmm_job *job, fmmcu_fmm_stats *stats);
+/* The same call split in two: launch returns once the potentials' D2H is
+ * enqueued (job->out is not touched); finish waits and writes them to `out`
+ * ([2 n_eval] doubles) chunk by chunk as they land. */
+int fmmcu_fmm_launch(fmmcu_ctx *ctx, const fmmcu_fmm_job *job);
+int fmmcu_fmm_finish(fmmcu_ctx *ctx, double *out, fmmcu_fmm_stats *stats);
 /* The device-built pyramid / connectivity of the last fmmcu_fmm_evaluate
  * (parity checks).  Box layout as fmmh_tree_boxes: f64[5 n] = centre x, y,
  * half width, half height, radius; u32[4 n] = point and eval ranges. */

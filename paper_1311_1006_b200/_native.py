@@ -139,7 +139,7 @@ CUDA_SYMBOLS = [
     "fmmcu_p2p_device_out", "fmmcu_p2p_bind_device_out", "fmmcu_p2p_copy_out", "fmmcu_p2p_pairs", "fmmcu_p2p_work_prefix", "fmmcu_set_stream",
     "fmmcu_synchronize", "fmmcu_m2l_launch", "fmmcu_m2l_finish", "fmmcu_kernel_launches",
     "fmmcu_fp64_peak", "fmmcu_last_transfer_bytes", "fmmcu_host_register", "fmmcu_host_unregister",
-    "fmmcu_fmm_evaluate", "fmmcu_fmm_tree_level", "fmmcu_fmm_tree_perm", "fmmcu_fmm_tree_lists",
+    "fmmcu_fmm_evaluate", "fmmcu_fmm_launch", "fmmcu_fmm_finish", "fmmcu_fmm_tree_level", "fmmcu_fmm_tree_perm", "fmmcu_fmm_tree_lists",
     "fmmcu_hypot_batch",
 ]
 
@@ -171,6 +171,8 @@ def cuda_lib():
         lib.fmmcu_host_register.argtypes = [vp, vp, C.c_uint64]
         lib.fmmcu_host_unregister.argtypes = [vp, vp]
         lib.fmmcu_fmm_evaluate.argtypes = [vp, C.POINTER(FmmJob), C.POINTER(FmmStats)]
+        lib.fmmcu_fmm_launch.argtypes = [vp, C.POINTER(FmmJob)]
+        lib.fmmcu_fmm_finish.argtypes = [vp, vp, C.POINTER(FmmStats)]
         lib.fmmcu_fmm_tree_level.argtypes = [vp, C.c_int, C.POINTER(C.c_uint32), vp, vp]
         lib.fmmcu_fmm_tree_perm.argtypes = [vp, vp, vp]
         lib.fmmcu_fmm_tree_lists.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_uint64), vp, vp]

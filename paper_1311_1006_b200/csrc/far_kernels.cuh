@@ -55,40 +55,69 @@ struct FarArgs {
   const int32_t* __restrict__ m2l_row; // global box id -> row (or -1)
 };
 
-// P2M of every finest box with sources (expansion.cpp:124-149): lane k keeps
-// coefficient k, sources in ascending permuted order, t^k by the reference's
-// incremental chain.
+// P2M of every finest box with sources (expansion.cpp:124-149).  Sources go
+// in batches of 32: lane j forms the power chain of source j into shared
+// memory (tp *= t, exactly the reference's sequence), then lane k sums
+// coefficient k over the batch in ascending source order.
 __global__ void __launch_bounds__(kFarWarps * 32) p2m_kernel(const FarArgs a,
                                                              const double4* __restrict__ src) {
+  extern __shared__ double2 s_p2m[];  // [warps][32 sources][P1 powers] + [warps][32] strengths
   const int lane = threadIdx.x & 31;
-  const uint32_t box = blockIdx.x * kFarWarps + (threadIdx.x >> 5);
+  const int w = threadIdx.x >> 5;
+  const uint32_t box = blockIdx.x * (blockDim.x >> 5) + w;
   if (box >= a.nbox) return;
   const uint32_t b = a.soff_l[box], e = a.soff_l[box + 1];
   if (b == e) return;
   const int P1 = a.p + 1;
+  double2* pw = s_p2m + size_t(w) * 32 * P1;
+  double2* ms = s_p2m + size_t(blockDim.x >> 5) * 32 * P1 + w * 32;
   const double2 c = a.center[a.base + box];
-  for (int k0 = 0; k0 < P1; k0 += 32) {
-    const int k = k0 + lane;
-    double2 acc = make_double2(0.0, 0.0);
-    for (uint32_t j = b; j < e; ++j) {
-      const double4 s = src[j];
-      const double2 t = cx_sub(make_double2(s.x, s.y), c);
-      const double2 m = make_double2(s.z, s.w);
+  double2 acc[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) acc[r] = make_double2(0.0, 0.0);
+  for (uint32_t j0 = b; j0 < e; j0 += 32) {
+    const uint32_t nb = min(32u, e - j0);
+    __syncwarp();
+    if (uint32_t(lane) < nb) {
+      const double4 s4 = src[j0 + lane];
+      const double2 t = cx_sub(make_double2(s4.x, s4.y), c);
+      ms[lane] = make_double2(s4.z, s4.w);
+      double2* my = pw + size_t(lane) * P1;
       if (a.kernel == 0) {
         double2 tp = make_double2(1.0, 0.0);
-        for (int q = 0; q < k && q < P1; ++q) tp = cx_mul(tp, t);
-        if (k < P1) acc = cx_sub(acc, cx_mul(m, tp));
+        for (int k = 0; k < P1; ++k) {
+          my[k] = tp;
+          tp = cx_mul(tp, t);
+        }
       } else {
-        if (k == 0) {
-          acc = cx_add(acc, m);
-        } else if (k < P1) {
-          double2 tp = t;
-          for (int q = 1; q < k; ++q) tp = cx_mul(tp, t);
-          acc = cx_sub(acc, cx_div_real(cx_mul(m, tp), double(k)));
+        double2 tp = t;
+        for (int k = 1; k < P1; ++k) {
+          my[k] = tp;
+          tp = cx_mul(tp, t);
         }
       }
     }
-    if (k < P1) a.out[size_t(a.base + box) * P1 + k] = acc;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int k = r * 32 + lane;
+      if (k >= P1) break;
+      for (uint32_t j = 0; j < nb; ++j) {
+        const double2 m = ms[j];
+        if (a.kernel == 0) {
+          acc[r] = cx_sub(acc[r], cx_mul(m, pw[size_t(j) * P1 + k]));
+        } else if (k == 0) {
+          acc[r] = cx_add(acc[r], m);
+        } else {
+          acc[r] = cx_sub(acc[r], cx_div_real(cx_mul(m, pw[size_t(j) * P1 + k]), double(k)));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int k = r * 32 + lane;
+    if (k < P1) a.out[size_t(a.base + box) * P1 + k] = acc[r];
   }
 }
 

@@ -55,12 +55,21 @@ struct DevicePipeline {
   bool tree_valid = false;
   cudaStream_t far = nullptr;
   cudaEvent_t ev[12] = {};
+  static constexpr int kChunksMax = 64;
+  cudaEvent_t ev_res[kChunksMax] = {};
+  uint32_t chunk_off[kChunksMax + 1] = {};
+  int n_chunks = 0;
+  bool pending = false;
+  Clock::time_point t_host0{};
+  uint64_t h2d = 0;
 };
 
 void destroy_pipeline(DevicePipeline* p) {
   if (!p) return;
   if (p->far) cudaStreamDestroy(p->far);
   for (cudaEvent_t e : p->ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_res)
     if (e) cudaEventDestroy(e);
   DevBuf* bufs[] = {&p->z, &p->m, &p->y, &p->sid, &p->keys0, &p->keys1, &p->ids, &p->sx, &p->sy,
                     &p->ex, &p->ey, &p->sxn, &p->syn, &p->exn, &p->eyn, &p->flag_s, &p->flag_e,
@@ -87,6 +96,7 @@ void destroy_pipeline(DevicePipeline* p) {
 namespace {
 
 constexpr int TB = 256;
+constexpr uint32_t kResChunks = 16;
 inline uint32_t blocks(uint64_t n) { return uint32_t((n + TB - 1) / TB); }
 inline uint64_t pow4(int l) { return uint64_t(1) << (2 * l); }
 
@@ -235,8 +245,13 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
   uint32_t* EYn = P->eyn.as<uint32_t>();
   if (int rc = sorted_list(c, P, zp, N, 0, SX, s)) return rc;
   if (int rc = sorted_list(c, P, zp, N, 1, SY, s)) return rc;
-  if (int rc = sorted_list(c, P, yp, M, 0, EX, s)) return rc;
-  if (int rc = sorted_list(c, P, yp, M, 1, EY, s)) return rc;
+  if (P->self_eval) {  // evals are the sources: same sorted lists
+    CU_TRY(c, cudaMemcpyAsync(EX, SX, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(EY, SY, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
+  } else {
+    if (int rc = sorted_list(c, P, yp, M, 0, EX, s)) return rc;
+    if (int rc = sorted_list(c, P, yp, M, 1, EY, s)) return rc;
+  }
 
   uint32_t* soff = P->soff.as<uint32_t>();
   uint32_t* eoff = P->eoff.as<uint32_t>();
@@ -498,8 +513,12 @@ int far_field(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, cudaEvent_t e_up,
   CU_TRY(c, P->loc.ensure(nb * P1 * 16));
   {
     const FarArgs a = far_args(P, L - 1);
-    p2m_kernel<<<(a.nbox + kFarWarps - 1) / kFarWarps, kFarWarps * 32, 0, s>>>(
-        a, c->d_src.as<double4>());
+    const int warps = P1 <= 40 ? kFarWarps : 1;
+    const size_t smem = size_t(warps) * 32 * (P1 + 1) * 16;
+    if (smem > 48 * 1024)
+      CU_TRY(c, cudaFuncSetAttribute(p2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
+    p2m_kernel<<<(a.nbox + warps - 1) / warps, warps * 32, smem, s>>>(a, c->d_src.as<double4>());
   }
   for (int l = L - 2; l >= 0; --l) {
     FarArgs a = far_args(P, l);
@@ -525,7 +544,8 @@ int far_field(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, cudaEvent_t e_up,
     m.big_w2 = std::pow(10.0, 500.0 / double(P->p + 2));
     m.out = P->m2l_sum.as<double2>();
     m.singular = P->flag.as<int>();
-    m2l_batched_kernel<<<(P->n_targets + kM2LWarps - 1) / kM2LWarps, kM2LWarps * 32, 0, s>>>(m);
+    CU_TRY(c, m2l_set_const_table(c->m_table.as<double>(), P->p + 1, s));
+    launch_m2l(m, s);
   }
   for (int l = 1; l < L; ++l) {
     FarArgs a = far_args(P, l);
@@ -549,9 +569,10 @@ float span_ms(cudaEvent_t a, cudaEvent_t b) {
 // ================================================================ C ABI ====
 extern "C" {
 
-int fmmcu_fmm_evaluate(fmmcu_ctx* c, const fmmcu_fmm_job* j, fmmcu_fmm_stats* st) {
+int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   if (!c) return FMMCU_EINVAL;
   if (!j) return set_err(c, FMMCU_EINVAL, "null fmm job");
+  if (c->pipe && c->pipe->pending) return set_err(c, FMMCU_ESTATE, "fmm launch while in flight");
   if (c->inflight || c->m2l_inflight) return set_err(c, FMMCU_ESTATE, "context busy");
   if (j->n_src == 0 || !j->src_z || !j->src_m) return set_err(c, FMMCU_EINVAL, "empty source set");
   if (j->n_levels < 1 || j->n_levels > 14) return set_err(c, FMMCU_EINVAL, "n_levels out of range");
@@ -562,13 +583,15 @@ int fmmcu_fmm_evaluate(fmmcu_ctx* c, const fmmcu_fmm_job* j, fmmcu_fmm_stats* st
   if (j->smoother < 0 || j->smoother > 2) return set_err(c, FMMCU_EINVAL, "unknown smoother");
   if (j->smoother != 0 && !(j->delta > 0.0))
     return set_err(c, FMMCU_EINVAL, "smoother delta must be > 0");
-  if (j->n_eval > 0 && (!j->eval_y || !j->out)) return set_err(c, FMMCU_EINVAL, "null eval arrays");
+  if (j->n_eval > 0 && !j->eval_y) return set_err(c, FMMCU_EINVAL, "null eval arrays");
   const auto t_host0 = Clock::now();
   CU_TRY(c, cudaSetDevice(c->device));
   if (!c->pipe) {
     c->pipe = new DevicePipeline();
     CU_TRY(c, cudaStreamCreateWithFlags(&c->pipe->far, cudaStreamNonBlocking));
     for (cudaEvent_t& e : c->pipe->ev) CU_TRY(c, cudaEventCreate(&e));
+    for (cudaEvent_t& e : c->pipe->ev_res)
+      CU_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
   }
   DevicePipeline* P = c->pipe;
   const uint32_t N = j->n_src, M = j->n_eval;
@@ -734,30 +757,53 @@ int fmmcu_fmm_evaluate(fmmcu_ctx* c, const fmmcu_fmm_job* j, fmmcu_fmm_stats* st
   CU_TRY(c, P->h_flag.ensure(16));
   CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.p, 4, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, s));
-  cudaPointerAttributes pa{};
-  const bool direct = M && cudaPointerGetAttributes(&pa, j->out) == cudaSuccess &&
-                      pa.type == cudaMemoryTypeHost;
-  cudaGetLastError();
+  // D2H in chunks so that fmmcu_fmm_finish copies chunk i out of the pinned
+  // staging while chunk i+1 is still in flight
+  CU_TRY(c, P->hres.ensure(uint64_t(std::max(M, 1u)) * 16));
+  P->n_chunks = 0;
   if (M) {
-    if (direct) {
-      CU_TRY(c, cudaMemcpyAsync(j->out, P->res.p, uint64_t(M) * 16, cudaMemcpyDeviceToHost, s));
-    } else {
-      CU_TRY(c, P->hres.ensure(uint64_t(M) * 16));
-      CU_TRY(c, cudaMemcpyAsync(P->hres.p, P->res.p, uint64_t(M) * 16, cudaMemcpyDeviceToHost, s));
+    const uint32_t per = std::max<uint32_t>(1u << 18, (M + kResChunks - 1) / kResChunks);
+    for (uint32_t e0 = 0; e0 < M; e0 += per) {
+      const uint32_t e1 = std::min(M, e0 + per);
+      CU_TRY(c, cudaMemcpyAsync(P->hres.as<double2>() + e0, P->res.as<double2>() + e0,
+                                uint64_t(e1 - e0) * 16, cudaMemcpyDeviceToHost, s));
+      CU_TRY(c, cudaEventRecord(P->ev_res[P->n_chunks], s));
+      P->chunk_off[P->n_chunks] = e0;
+      P->chunk_off[++P->n_chunks] = e1;
     }
   }
   CU_TRY(c, cudaEventRecord(ev[10], s));
+  P->pending = true;
+  P->t_host0 = t_host0;
+  P->h2d = h2d;
+  return FMMCU_OK;
+}
+
+int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {
+  if (!c) return FMMCU_EINVAL;
+  DevicePipeline* P = c->pipe;
+  if (!P || !P->pending) return set_err(c, FMMCU_ESTATE, "fmm finish without launch");
+  P->pending = false;
+  CU_TRY(c, cudaSetDevice(c->device));
+  const uint32_t M = P->M;
+  if (M && !out) return set_err(c, FMMCU_EINVAL, "null output");
+  for (int i = 0; i < P->n_chunks; ++i) {
+    CU_TRY(c, cudaEventSynchronize(P->ev_res[i]));
+    const uint32_t e0 = P->chunk_off[i], e1 = P->chunk_off[i + 1];
+    par_memcpy(out + 2 * uint64_t(e0), P->hres.as<double2>() + e0, uint64_t(e1 - e0) * 16);
+  }
+  cudaEvent_t* ev = P->ev;
   CU_TRY(c, cudaEventSynchronize(ev[10]));
   CU_TRY(c, cudaGetLastError());
-  if (M && !direct) par_memcpy(j->out, P->hres.p, uint64_t(M) * 16);
   if (*P->h_flag.as<int>())
     return set_err(c, FMMCU_ESINGULAR, "m2l: target center coincides with source center");
   if (st) {
+    const uint32_t nleaf = uint32_t(pow4(P->L - 1));
     const uint64_t hits = *c->h_hits.as<unsigned long long>();
     st->p2p_pairs = c->leaf_work[nleaf] - hits;
     st->m2l_ops = P->m2l_nnz;
-    st->p2m_points = N;
-    st->l2p_points = L >= 2 ? M : 0;
+    st->p2m_points = P->N;
+    st->l2p_points = P->L >= 2 ? M : 0;
     st->t_upload = 1e-3 * span_ms(ev[0], ev[1]);
     st->t_tree = 1e-3 * span_ms(ev[1], ev[2]);
     st->t_connect = 1e-3 * span_ms(ev[2], ev[3]);
@@ -765,11 +811,16 @@ int fmmcu_fmm_evaluate(fmmcu_ctx* c, const fmmcu_fmm_job* j, fmmcu_fmm_stats* st
     st->t_m2l = 1e-3 * span_ms(ev[6], ev[7]);
     st->t_p2p = 1e-3 * span_ms(ev[8], ev[9]);
     st->t_device = 1e-3 * span_ms(ev[0], ev[10]);
-    st->t_total = std::chrono::duration<double>(Clock::now() - t_host0).count();
-    st->h2d_bytes = h2d;
+    st->t_total = std::chrono::duration<double>(Clock::now() - P->t_host0).count();
+    st->h2d_bytes = P->h2d;
     st->d2h_bytes = uint64_t(M) * 16;
   }
   return FMMCU_OK;
+}
+
+int fmmcu_fmm_evaluate(fmmcu_ctx* c, const fmmcu_fmm_job* j, fmmcu_fmm_stats* st) {
+  if (int rc = fmmcu_fmm_launch(c, j)) return rc;
+  return fmmcu_fmm_finish(c, j->out, st);
 }
 
 int fmmcu_fmm_tree_level(fmmcu_ctx* c, int level, uint32_t* n_boxes, double* f64, uint32_t* u32) {

@@ -1024,7 +1024,8 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
     a.big_w2 = std::pow(10.0, 500.0 / double(j->p + 2));
     a.out = c->m_out.as<double2>();
     a.singular = c->m_flag.as<int>();
-    m2l_batched_kernel<<<(nt + kM2LWarps - 1) / kM2LWarps, kM2LWarps * 32, 0, s>>>(a);
+    CU_TRY(c, m2l_set_const_table(c->m_table.as<double>(), P1, s));
+    launch_m2l(a, s);
     CU_TRY(c, cudaGetLastError());
     c->launches += 1;
     CU_TRY(c, cudaMemcpyAsync(c->mh_out.p, c->m_out.p, size_t(nt) * P1 * 16, cudaMemcpyDeviceToHost, s));

