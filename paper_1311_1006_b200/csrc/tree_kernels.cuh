@@ -95,9 +95,21 @@ __global__ void coord_keys_kernel(const double2* __restrict__ p, uint32_t n, int
   id[i] = i;
 }
 
-// segment of position i in offsets off[0..nseg] (off[0] = 0, off[nseg] = n)
+// segment of position i in offsets off[0..nseg] (off[0] = 0, off[nseg] = n).
+// Median splits keep source segments balanced (sizes within one of n/nseg),
+// so the proportional guess is almost always right: probe it and its
+// neighbours first, then fall back to bisection (unbalanced eval segments).
 __device__ __forceinline__ uint32_t seg_of(const uint32_t* __restrict__ off, uint32_t nseg,
                                            uint32_t i) {
+  const uint32_t n = off[nseg];
+  uint32_t g = uint32_t((uint64_t(i) * nseg) / n);
+  if (g >= nseg) g = nseg - 1;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (off[g] > i) --g;
+    else if (off[g + 1] <= i) ++g;
+  }
+  if (off[g] <= i && i < off[g + 1]) return g;  // the unique non-empty segment holding i
   uint32_t lo = 0, hi = nseg;  // off[lo] <= i < off[hi]
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
