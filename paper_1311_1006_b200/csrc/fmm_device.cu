@@ -737,8 +737,9 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   c->delta = j->delta;
   c->self_layout = false;
   c->ext_out = nullptr;
+  c->group_k = 0;
   if (int rc = build_worklist(c, &pj)) return rc;
-  if (int rc = stage_csr(c, &pj)) return rc;
+  if (int rc = stage_csr(c, &pj, true)) return rc;
   CU_TRY(c, cudaEventRecord(ev[8], s));
   int nk = 0;
   if (int rc = run_kernels(c, 0, nleaf, FMMCU_MODE_FAST, &nk)) return rc;

@@ -58,8 +58,8 @@ bool use_warp_kernel() {
   return w;
 }
 
-constexpr size_t warp_smem(int warps, int chunk) {
-  return size_t(warps) * (128 + size_t(2 * chunk) * 32);
+constexpr size_t warp_smem(int warps, int chunk, int e) {
+  return size_t(warps) * warp_region_bytes(chunk, e);
 }
 
 constexpr size_t tile_smem(int threads, int e, int tile) {
@@ -70,6 +70,17 @@ constexpr size_t tile_smem(int threads, int e, int tile) {
 }  // namespace
 
 namespace fmmcu::detail {
+
+// packed source records of slots [i0, i1) from interleaved z and m (DMA'd
+// straight from page-locked caller arrays)
+__global__ void pack_zm_kernel(const double2* __restrict__ z, const double2* __restrict__ m,
+                               uint32_t i0, uint32_t i1, double4* __restrict__ src) {
+  const uint32_t i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < i1) {
+    const double2 a = z[i], b = m[i];
+    src[i] = make_double4(a.x, a.y, b.x, b.y);
+  }
+}
 
 int set_err(fmmcu_ctx* c, int code, const std::string& msg) {
   c->err = msg;
@@ -151,7 +162,7 @@ void launch_exact(const P2PArgs& a, uint32_t lb, uint32_t le, uint32_t eb, uint3
 template <int KN, int SM, int W, int E, int C, int U, int MINB>
 void launch_warp_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
   auto kfn = p2p_warp_kernel<KN, SM, E, W, C, U, MINB>;
-  constexpr size_t smem = warp_smem(W, C);
+  constexpr size_t smem = warp_smem(W, C, E);
   static int grid_cap = [&] {
     cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -302,11 +313,50 @@ int choose_warp_e(const uint32_t* ev_off, const std::vector<uint64_t>& S, uint32
 // evals-per-lane choice, and the item / finalize lists.  Touches only the
 // job's CSR and host-side context fields, so it runs on a helper thread
 // while the main thread packs and uploads the sources.
+// In-place inclusive prefix sum of v[1..n] (v[0] = 0 stays), blocked over the
+// OpenMP threads: per-block sums, a serial scan of the block sums, then each
+// block adds its offset.
+template <class T>
+void par_prefix(T* v, int64_t n) {
+  if (n <= 0) return;
+  if (n < (int64_t(1) << 15)) {
+    for (int64_t i = 1; i <= n; ++i) v[i] += v[i - 1];
+    return;
+  }
+  int nb = 1;
+#ifdef _OPENMP
+  nb = omp_get_max_threads();
+#endif
+  std::vector<T> part(nb + 1, T(0));
+  const int64_t per = (n + nb - 1) / nb;
+#pragma omp parallel for schedule(static, 1) num_threads(nb)
+  for (int b = 0; b < nb; ++b) {
+    const int64_t i0 = 1 + b * per, i1 = std::min<int64_t>(n, i0 + per - 1);
+    T acc = 0;
+    for (int64_t i = i0; i <= i1; ++i) acc += v[i];
+    part[b + 1] = acc;
+  }
+  for (int b = 0; b < nb; ++b) part[b + 1] += part[b];
+#pragma omp parallel for schedule(static, 1) num_threads(nb)
+  for (int b = 0; b < nb; ++b) {
+    const int64_t i0 = 1 + b * per, i1 = std::min<int64_t>(n, i0 + per - 1);
+    T acc = part[b];
+    for (int64_t i = i0; i <= i1; ++i) {
+      acc += v[i];
+      v[i] = acc;
+    }
+  }
+}
+
 int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const uint32_t nl = j->n_leaves;
-  c->ev_off.assign(j->ev_off, j->ev_off + nl + 1);
-  c->leaf_work.assign(nl + 1, 0);
-  std::vector<uint64_t> S(nl, 0);
+  c->ev_off.resize(nl + 1);
+  c->leaf_work.resize(nl + 1);
+  c->wl_S.resize(nl);
+  std::vector<uint64_t>& S = c->wl_S;
+  uint32_t* evo = c->ev_off.data();
+  uint64_t* work = c->leaf_work.data();
+  work[0] = 0;
 #pragma omp parallel for schedule(static)
   for (int64_t t = 0; t < int64_t(nl); ++t) {
     uint64_t s = 0;
@@ -315,12 +365,12 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       s += j->pt_off[sb + 1] - j->pt_off[sb];
     }
     S[t] = s;
+    evo[t] = j->ev_off[t];
+    work[t + 1] = uint64_t(j->ev_off[t + 1] - j->ev_off[t]) * s;
   }
-  uint64_t total = 0;
-  for (uint32_t t = 0; t < nl; ++t) {
-    total += uint64_t(j->ev_off[t + 1] - j->ev_off[t]) * S[t];
-    c->leaf_work[t + 1] = total;
-  }
+  evo[nl] = j->ev_off[nl];
+  par_prefix(work, int64_t(nl));
+  const uint64_t total = work[nl];
   const uint64_t budget = std::max<uint64_t>(1ull << 16, total / (148ull * 16ull));
   const bool warp_kernel = use_warp_kernel();
   c->warp_e = warp_kernel ? choose_warp_e(j->ev_off, S, nl) : 4;
@@ -374,31 +424,65 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     }
     return n;
   };
-  std::vector<uint32_t> pev_first(nl + 1, 0);
-  c->item_first.assign(nl + 1, 0);
-  c->fin_first.assign(nl + 1, 0);
+  // Leaf processing order.  Default: every leaf, ascending (item_first is
+  // indexed by leaf).  Grouped (overlapped launch, c->group_k > 0): the
+  // shard's leaves ordered by the upload chunk holding the last source slot
+  // their strong list reads, so group g can run as soon as chunks 0..g are on
+  // the device; item_first / fin_first are then indexed by position and
+  // grp_item / grp_fin delimit the groups.
+  std::vector<uint32_t>& order = c->wl_order;
+  const bool grouped = c->group_k > 0;
+  const uint32_t np = grouped ? j->leaf_end - j->leaf_begin : nl;
+  if (grouped) {
+    const int K = c->group_k;
+    std::vector<uint32_t>& kc = c->wl_kc;
+    kc.resize(np);
 #pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < int64_t(nl); ++t) {
-    const LeafCount n = leaf_items(uint32_t(t), nullptr, nullptr, 0);
+    for (int64_t i = 0; i < int64_t(np); ++i) {
+      const uint32_t t = j->leaf_begin + uint32_t(i);
+      uint32_t need = j->pt_off[t + 1];
+      for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q)
+        need = std::max(need, j->pt_off[j->strong_idx[q] + 1]);
+      // chunk k holds leaves [chunk_leaf[k], chunk_leaf[k+1]), i.e. slots up to pt_off[chunk_leaf[k+1]]
+      int k = 0;
+      while (k < K - 1 && j->pt_off[c->chunk_leaf[k + 1]] < need) ++k;
+      kc[i] = uint32_t(k);
+    }
+    std::vector<uint32_t> cnt(K + 1, 0);
+    for (uint32_t i = 0; i < np; ++i) ++cnt[kc[i] + 1];
+    for (int k = 0; k < K; ++k) cnt[k + 1] += cnt[k];
+    c->grp_pos.assign(cnt.begin(), cnt.end());
+    order.resize(np);
+    for (uint32_t i = 0; i < np; ++i) order[cnt[kc[i]]++] = j->leaf_begin + i;
+  }
+  auto leaf_at = [&](int64_t pos) { return grouped ? order[pos] : uint32_t(pos); };
+  std::vector<uint64_t>& pev_first = c->wl_pev;
+  pev_first.resize(np + 1);
+  c->item_first.resize(np + 1);
+  c->fin_first.resize(np + 1);
+  pev_first[0] = 0;
+  c->item_first[0] = 0;
+  c->fin_first[0] = 0;
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < int64_t(np); ++t) {
+    const LeafCount n = leaf_items(leaf_at(t), nullptr, nullptr, 0);
     c->item_first[t + 1] = n.items;
     c->fin_first[t + 1] = n.fins;
     pev_first[t + 1] = n.pevals;
   }
-  uint64_t partial_evals = 0;
-  for (uint32_t t = 0; t < nl; ++t) {
-    c->item_first[t + 1] += c->item_first[t];
-    c->fin_first[t + 1] += c->fin_first[t];
-    partial_evals += pev_first[t + 1];
-    pev_first[t + 1] = uint32_t(std::min<uint64_t>(partial_evals, 0xFFFFFFFFull));
-  }
+  par_prefix(c->item_first.data(), int64_t(np));
+  par_prefix(c->fin_first.data(), int64_t(np));
+  par_prefix(pev_first.data(), int64_t(np));
+  const uint64_t partial_evals = pev_first[np];
   if (partial_evals > 0xFFFFFFF0ull) return set_err(c, FMMCU_EINVAL, "partial buffer too large");
   c->partial_evals = partial_evals;
-  c->items.resize(c->item_first[nl]);
-  c->fins.resize(c->fin_first[nl]);
+  c->items.resize(c->item_first[np]);
+  c->fins.resize(c->fin_first[np]);
 #pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < int64_t(nl); ++t)
-    leaf_items(uint32_t(t), c->items.data() + c->item_first[t], c->fins.data() + c->fin_first[t],
-               pev_first[t]);
+  for (int64_t t = 0; t < int64_t(np); ++t)
+    leaf_items(leaf_at(t), c->items.data() + c->item_first[t], c->fins.data() + c->fin_first[t],
+               uint32_t(pev_first[t]));
+  c->grouped = grouped;
 
   return FMMCU_OK;
 }
@@ -407,6 +491,7 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
 int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   if (int rc = validate(c, j)) return rc;
   CU_TRY(c, cudaSetDevice(c->device));
+  c->group_k = 0;
   const uint32_t nl = j->n_leaves, ns = j->n_src, ne = j->n_eval;
   c->n_leaves = nl;
   c->n_src = ns;
@@ -494,12 +579,12 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // ---- work list (built concurrently with the source packing above) -------
   if (int rc = worklist.get()) return rc;
   tr.mark("worklist");
-  if (int rc = stage_csr(c, j)) return rc;
+  if (int rc = stage_csr(c, j, true)) return rc;
   tr.mark("csr+worklist h2d");
   return FMMCU_OK;
 }
 
-int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals) {
   const uint32_t nl = j->n_leaves, ne = j->n_eval;
   const uint32_t nnz = j->strong_off[nl];
   const bool self_layout = c->self_layout;
@@ -554,19 +639,265 @@ int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
                                                           c->d_seg.as<uint2>());
     c->launches += 1;
   }
-  if (ne) {
+  if (ne && evals) {
     if (self_layout) {
-      p2p_self_evals_kernel<<<(ne + 255) / 256, 256, 0, s>>>(c->d_src.as<double4>(), ne,
+      p2p_self_evals_kernel<<<(ne + 255) / 256, 256, 0, s>>>(c->d_src.as<double4>(), 0, ne,
                                                              c->d_evy.as<double2>(),
                                                              c->d_eself.as<uint32_t>());
       c->launches += 1;
     }
     // eval records {x, y, self slot, strong entry of the self slot}; needs seg
-    p2p_evrec_kernel<<<(nl + 7) / 8, 256, 0, s>>>(make_args(c), nl, c->d_evr.as<double4>());
+    p2p_evrec_kernel<<<(nl + 7) / 8, 256, 0, s>>>(make_args(c), 0, nl, c->d_evr.as<double4>());
     c->launches += 1;
   }
   CU_TRY(c, cudaGetLastError());
   c->staged = true;
+  return FMMCU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Reference-facing launch, fast mode: the upload overlaps the kernels.
+//  * sources go H2D in K leaf-aligned chunks on the copy stream;
+//  * the work list (helper thread) orders the shard's leaves by the chunk
+//    holding the last source slot their strong list reads, so group g runs
+//    as soon as chunks 0..g have landed;
+//  * eval records of a chunk's leaves are derived on the device from its
+//    sources when every eval there is its own source (self layout), else the
+//    chunk's eval arrays ride the copy stream with it;
+//  * potentials are written by the kernels' TMA bulk stores straight into
+//    the page-locked output (the caller's, or pinned staging): no D2H pass.
+int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  if (int rc = validate(c, j)) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  const uint32_t nl = j->n_leaves, ns = j->n_src, ne = j->n_eval;
+  const uint32_t lb = j->leaf_begin, le = j->leaf_end;
+  c->n_leaves = nl;
+  c->n_src = ns;
+  c->n_eval = ne;
+  c->kernel = j->kernel;
+  c->smoother = j->smoother;
+  c->mode = j->mode;
+  c->delta = j->delta;
+  Trace tr(c);
+  // leaf-aligned upload chunks of ~1M sources
+  constexpr uint32_t kChunkSrc = 1u << 20;
+  const int K = int(std::min<uint32_t>(fmmcu_ctx::kMaxChunks,
+                                       std::max<uint32_t>(1u, (ns + kChunkSrc - 1) / kChunkSrc)));
+  c->chunk_leaf.assign(K + 1, nl);
+  c->chunk_leaf[0] = 0;
+  for (int k = 1; k < K; ++k) {
+    const uint64_t target = uint64_t(ns) * uint64_t(k) / uint64_t(K);
+    const uint32_t t = uint32_t(std::lower_bound(j->pt_off, j->pt_off + nl + 1, uint32_t(target)) -
+                                j->pt_off);
+    c->chunk_leaf[k] = std::max(c->chunk_leaf[k - 1], std::min(t, nl));
+  }
+  c->group_k = K;
+  // The work list (~1 ms on all cores at 10M) is built first, on this thread:
+  // built concurrently it starves behind the OpenMP packing team and the DMA
+  // traffic, and every group needs it before its kernels can be enqueued.
+  if (int rc = build_worklist(c, j)) return rc;
+  tr.mark("worklist");
+
+  cudaStream_t s = c->stream, h = c->h2d_stream;
+  CU_TRY(c, c->d_src.ensure(size_t(ns) * 32));
+  CU_TRY(c, c->d_evy.ensure(size_t(ne) * 16));
+  CU_TRY(c, c->d_eself.ensure(size_t(ne) * 4));
+  CU_TRY(c, c->h_src.ensure(size_t(ns) * 32));
+  CU_TRY(c, c->h_evy.ensure(size_t(ne) * 16));
+  CU_TRY(c, c->h_eself.ensure(size_t(ne) * 4));
+  CU_TRY(c, c->d_evr.ensure(size_t(ne) * 32));
+  CU_TRY(c, c->d_hits.ensure(8));
+  CU_TRY(c, c->d_counter.ensure(8));
+  CU_TRY(c, c->h_hits.ensure(8));
+  // output: the caller's page-locked buffer, else pinned (mapped) staging
+  const uint32_t eb = j->ev_off[lb], ee = j->ev_off[le];
+  cudaPointerAttributes pa{};
+  void* dev_out = nullptr;
+  c->direct_out = ne && cudaPointerGetAttributes(&pa, j->out) == cudaSuccess &&
+                  pa.type == cudaMemoryTypeHost &&
+                  cudaHostGetDevicePointer(&dev_out, j->out, 0) == cudaSuccess;
+  cudaGetLastError();
+  if (!c->direct_out) {
+    CU_TRY(c, c->h_out.ensure(size_t(ne) * 16 + 16));
+    CU_TRY(c, cudaHostGetDevicePointer(&dev_out, c->h_out.p, 0));
+  }
+  c->out_dev = static_cast<double2*>(dev_out);
+  CU_TRY(c, cudaEventRecord(c->ev_start, s));
+  c->t_evstart = Clock::now();
+  CU_TRY(c, cudaStreamWaitEvent(h, c->ev_start, 0));
+  CU_TRY(c, cudaMemsetAsync(c->d_hits.p, 0, 8, s));
+
+  const double* z = j->src_z;
+  const double* m = j->src_m;
+  double* hs = c->h_src.as<double>();
+  uint64_t h2d = uint64_t(ns) * 32;
+  // page-locked caller inputs: DMA z and m as they are and pack on the device
+  // (no host staging copy); the host only runs the self-layout check
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes at{};
+    const bool ok = p && cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+                    at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  const bool direct_in = ns > 0 && pinned(z) && pinned(m);
+  if (direct_in) {
+    CU_TRY(c, c->d_zin.ensure(size_t(ns) * 16));
+    CU_TRY(c, c->d_min.ensure(size_t(ns) * 16));
+  }
+  if (int rc = stage_csr(c, j, false)) return rc;
+  h2d += c->h2d_bytes - uint64_t(ns) * 32 - (c->self_layout ? 0 : uint64_t(ne) * 20);
+  tr.mark("csr");
+  double2* hy = c->h_evy.as<double2>();
+  uint32_t* hself = c->h_eself.as<uint32_t>();
+  // self layout per chunk requires eval slot e == source slot e
+  const bool maybe_self = j->eval_sid && ne == ns && ns > 0 &&
+                          std::memcmp(j->ev_off, j->pt_off, size_t(nl + 1) * 4) == 0;
+  bool all_self = maybe_self;
+  // eval arrays of slots [e0, e1) on the host (non-self chunks / layouts)
+  bool inv_ready = false;
+  auto host_evals = [&](int64_t e0, int64_t e1) -> int {
+    if (j->eval_sid && !inv_ready) {
+      c->invperm.resize(ns);
+      uint32_t* inv = c->invperm.data();
+      bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+      for (int64_t i = 0; i < int64_t(ns); ++i) {
+        if (j->perm[i] >= ns) ok = false;
+        else inv[j->perm[i]] = uint32_t(i);
+      }
+      if (!ok) return set_err(c, FMMCU_EINVAL, "perm is not a permutation of the sources");
+      inv_ready = true;
+    }
+    const uint32_t* inv = c->invperm.data();
+#pragma omp parallel for schedule(static)
+    for (int64_t e = e0; e < e1; ++e) {
+      hy[e] = make_double2(j->eval_y[2 * e], j->eval_y[2 * e + 1]);
+      const int64_t sv = j->eval_sid ? j->eval_sid[e] : -1;
+      hself[e] = (sv >= 0 && sv < int64_t(ns)) ? inv[sv] : kNoSelf;
+    }
+    return FMMCU_OK;
+  };
+  bool evals_event = false;
+  if (!maybe_self && ne) {
+    if (int rc = host_evals(0, ne)) return rc;
+    CU_TRY(c, cudaMemcpyAsync(c->d_evy.p, hy, size_t(ne) * 16, cudaMemcpyHostToDevice, h));
+    CU_TRY(c, cudaMemcpyAsync(c->d_eself.p, hself, size_t(ne) * 4, cudaMemcpyHostToDevice, h));
+    CU_TRY(c, cudaEventRecord(c->ev_evals, h));
+    evals_event = true;
+    h2d += uint64_t(ne) * 20;
+  }
+
+  std::vector<char> chunk_self(K, 0);
+  int launched = 0;
+  int nk = 0;
+  auto run_group = [&](int k) -> int {
+    CU_TRY(c, cudaStreamWaitEvent(s, c->ev_chunk[k], 0));
+    if (evals_event) CU_TRY(c, cudaStreamWaitEvent(s, c->ev_evals, 0));
+    const uint32_t l0 = c->chunk_leaf[k], l1 = c->chunk_leaf[k + 1];
+    const uint32_t a0 = j->ev_off[l0], a1 = j->ev_off[l1];
+    if (maybe_self && !chunk_self[k] && a1 > a0) {  // this chunk's evals are not its sources
+      CU_TRY(c, cudaMemcpyAsync(c->d_evy.as<double2>() + a0, hy + a0, size_t(a1 - a0) * 16,
+                                cudaMemcpyHostToDevice, s));
+      CU_TRY(c, cudaMemcpyAsync(c->d_eself.as<uint32_t>() + a0, hself + a0,
+                                size_t(a1 - a0) * 4, cudaMemcpyHostToDevice, s));
+    }
+    if (direct_in) {
+      const uint32_t s0 = j->pt_off[l0], s1 = j->pt_off[l1];
+      if (s1 > s0) {
+        pack_zm_kernel<<<(s1 - s0 + 255) / 256, 256, 0, s>>>(c->d_zin.as<double2>(),
+                                                            c->d_min.as<double2>(), s0, s1,
+                                                            c->d_src.as<double4>());
+        ++nk;
+      }
+    }
+    P2PArgs a = make_args(c);
+    a.out = c->out_dev;
+    if (a1 > a0) {
+      if (chunk_self[k]) {
+        p2p_self_evals_kernel<<<(a1 - a0 + 255) / 256, 256, 0, s>>>(
+            c->d_src.as<double4>(), a0, a1, c->d_evy.as<double2>(), c->d_eself.as<uint32_t>());
+        ++nk;
+      }
+      p2p_evrec_kernel<<<(l1 - l0 + 7) / 8, 256, 0, s>>>(a, l0, l1, c->d_evr.as<double4>());
+      ++nk;
+    }
+    const uint32_t p0 = c->grp_pos[k], p1 = c->grp_pos[k + 1];
+    const uint32_t i0 = c->item_first[p0], i1 = c->item_first[p1];
+    if (i1 > i0) {
+      CU_TRY(c, cudaMemsetAsync(c->d_counter.p, 0, 8, s));
+      P2PArgs aa = a;
+      aa.items = c->d_items.as<P2PItem>() + i0;
+      aa.n_items = i1 - i0;
+      dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s, c->warp_e);
+      ++nk;
+    }
+    const uint32_t f0 = c->fin_first[p0], f1 = c->fin_first[p1];
+    if (f1 > f0) {
+      p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(c->d_fin.as<P2PFinal>() + f0, f1 - f0,
+                                                   c->d_partial.as<double2>(), c->out_dev);
+      ++nk;
+    }
+    CU_TRY(c, cudaEventRecord(c->ev_group[k], s));
+    CU_TRY(c, cudaGetLastError());
+    return FMMCU_OK;
+  };
+
+  for (int k = 0; k < K; ++k) {
+    const uint32_t l0 = c->chunk_leaf[k], l1 = c->chunk_leaf[k + 1];
+    const int64_t c0 = j->pt_off[l0], c1 = j->pt_off[l1];
+    bool same = maybe_self;
+    if (direct_in) {
+      if (c1 > c0) {
+        CU_TRY(c, cudaMemcpyAsync(c->d_zin.as<double>() + 2 * c0, z + 2 * c0,
+                                  size_t(c1 - c0) * 16, cudaMemcpyHostToDevice, h));
+        CU_TRY(c, cudaMemcpyAsync(c->d_min.as<double>() + 2 * c0, m + 2 * c0,
+                                  size_t(c1 - c0) * 16, cudaMemcpyHostToDevice, h));
+      }
+      CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+      if (maybe_self) {
+#pragma omp parallel for schedule(static) reduction(&& : same)
+        for (int64_t i = c0; i < c1; ++i)
+          same = same && j->eval_sid[i] == int64_t(j->perm[i]) &&
+                 j->eval_y[2 * i] == z[2 * i] && j->eval_y[2 * i + 1] == z[2 * i + 1];
+      }
+    } else {
+#pragma omp parallel for schedule(static) reduction(&& : same)
+      for (int64_t i = c0; i < c1; ++i) {
+        hs[4 * i + 0] = z[2 * i];
+        hs[4 * i + 1] = z[2 * i + 1];
+        hs[4 * i + 2] = m[2 * i];
+        hs[4 * i + 3] = m[2 * i + 1];
+        if (maybe_self)
+          same = same && j->eval_sid[i] == int64_t(j->perm[i]) &&
+                 j->eval_y[2 * i] == z[2 * i] && j->eval_y[2 * i + 1] == z[2 * i + 1];
+      }
+      if (c1 > c0)
+        CU_TRY(c, cudaMemcpyAsync(c->d_src.as<double>() + 4 * c0, hs + 4 * c0,
+                                  size_t(c1 - c0) * 32, cudaMemcpyHostToDevice, h));
+      CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+    }
+    if (maybe_self && !same && c1 > c0) {
+      if (int rc = host_evals(c0, c1)) return rc;
+      h2d += uint64_t(c1 - c0) * 20;
+    }
+    chunk_self[k] = maybe_self && same;
+    all_self = all_self && same;
+    if (c->trace)
+      std::fprintf(stderr, "[fmmcu] chunk %2d enqueued at %8.3f ms\n", k,
+                   std::chrono::duration<double, std::milli>(Clock::now() - c->t_evstart).count());
+    if (int rc = run_group(launched++)) return rc;
+  }
+  tr.mark("pack+h2d (overlapped)");
+  c->self_layout = all_self;
+  CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaEventRecord(c->ev_end, s));
+  tr.mark("enqueue done");
+  c->launches += uint64_t(nk);
+  c->h2d_bytes = h2d;
+  c->d2h_bytes = uint64_t(ee - eb) * 16 + 8;
+  c->n_slices = 0;
+  c->n_groups = K;
   return FMMCU_OK;
 }
 
@@ -694,6 +1025,14 @@ int fmmcu_create(fmmcu_ctx** out, int device) {
     return fail(e);
   if ((e = cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(e);
+  if ((e = cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e);
+  if ((e = cudaEventCreateWithFlags(&c->ev_evals, cudaEventDisableTiming)) != cudaSuccess)
+    return fail(e);
+  for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
+    if ((e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDefault)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_group[i], cudaEventDefault)) != cudaSuccess)
+      return fail(e);
   c->stream = c->own_stream;
   const unsigned flags = cudaEventBlockingSync;
   for (int i = 0; i < fmmcu_ctx::kMaxSlices; ++i) {
@@ -720,9 +1059,10 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->m2l_stream);
     cudaStreamSynchronize(c->d2h_stream);
+    cudaStreamSynchronize(c->h2d_stream);
     fmmcu::destroy_pipeline(c->pipe);
     c->pipe = nullptr;
-    for (DevBuf* b : {&c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
+    for (DevBuf* b : {&c->d_zin, &c->d_min, &c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
                       &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter, &c->d_evr,
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
                       &c->m_table, &c->m_out, &c->m_flag})
@@ -739,6 +1079,12 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamDestroy(c->own_stream);
     cudaStreamDestroy(c->m2l_stream);
     cudaStreamDestroy(c->d2h_stream);
+    cudaStreamDestroy(c->h2d_stream);
+    if (c->ev_evals) cudaEventDestroy(c->ev_evals);
+    for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
+      if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
+    for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
+      if (c->ev_group[i]) cudaEventDestroy(c->ev_group[i]);
   }
   delete c;
 }
@@ -771,8 +1117,20 @@ int fmmcu_p2p_launch(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   if (!c) return FMMCU_EINVAL;
   if (c->inflight) return set_err(c, FMMCU_ESTATE, "launch while a job is in flight");
   const auto t0 = Clock::now();
+  if (j && j->n_eval > 0 && !j->out) return set_err(c, FMMCU_EINVAL, "null output");
+  if (j && j->mode == FMMCU_MODE_FAST && !std::getenv("FMMCU_NO_OVERLAP")) {
+    if (int rc = launch_overlapped(c, j)) return rc;
+    c->overlapped = true;
+    c->job = *j;
+    c->run_lb = j->leaf_begin;
+    c->run_le = j->leaf_end;
+    c->run_total_pairs = c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
+    c->prep_seconds = std::chrono::duration<double>(c->t_evstart - t0).count();
+    c->inflight = true;
+    return FMMCU_OK;
+  }
+  c->overlapped = false;
   if (int rc = stage_job(c, j)) return rc;
-  if (j->n_eval > 0 && !j->out) return set_err(c, FMMCU_EINVAL, "null output");
   const uint32_t lb = j->leaf_begin, le = j->leaf_end;
   const uint32_t eb = c->ev_off[lb], ee = c->ev_off[le];
   // A page-locked output (cudaHostRegister / fmmcu_host_register) receives
@@ -848,9 +1206,24 @@ int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
   }
   CU_TRY(c, cudaEventSynchronize(c->ev_end));
   CU_TRY(c, cudaGetLastError());
+  if (c->overlapped && c->trace) {
+    for (int k = 0; k < c->n_groups; ++k) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, c->ev_start, c->ev_chunk[k]);
+      cudaEventElapsedTime(&b, c->ev_start, c->ev_group[k]);
+      std::fprintf(stderr,
+                   "[fmmcu] group %2d: chunk landed %8.3f ms, kernels done %8.3f ms, items %u\n",
+                   k, a, b, c->item_first[c->grp_pos[k + 1]] - c->item_first[c->grp_pos[k]]);
+    }
+  }
+  if (c->overlapped && !c->direct_out) {
+    const uint32_t eb = c->ev_off[c->run_lb], ee = c->ev_off[c->run_le];
+    if (ee > eb)
+      par_memcpy(c->job.out + 2 * size_t(eb), c->h_out.as<double2>() + eb, size_t(ee - eb) * 16);
+  }
   float ms = 0.f;
   CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_start, c->ev_end));
-  if (c->trace) {
+  if (c->trace && !c->overlapped) {
     float kms = 0.f;
     cudaEventElapsedTime(&kms, c->ev_start, c->ev_kslice[c->n_slices - 1]);
     std::fprintf(stderr, "[fmmcu] device span %8.3f ms (start->last kernel %8.3f ms), prep %8.3f ms\n",
@@ -866,7 +1239,7 @@ int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
 int fmmcu_host_register(fmmcu_ctx* c, void* ptr, uint64_t bytes) {
   if (!c || !ptr || !bytes) return FMMCU_EINVAL;
   CU_TRY(c, cudaSetDevice(c->device));
-  CU_TRY(c, cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterPortable));
+  CU_TRY(c, cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterPortable | cudaHostRegisterMapped));
   return FMMCU_OK;
 }
 
@@ -887,7 +1260,7 @@ int fmmcu_p2p_stage(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
 
 int fmmcu_p2p_run_staged(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* launches) {
   if (!c) return FMMCU_EINVAL;
-  if (!c->staged) return set_err(c, FMMCU_ESTATE, "no staged job");
+  if (!c->staged || c->grouped) return set_err(c, FMMCU_ESTATE, "no staged job (fmmcu_p2p_stage)");
   if (lb > le || le > c->n_leaves) return set_err(c, FMMCU_EINVAL, "bad leaf shard");
   if (mode < 0 || mode > 1) return set_err(c, FMMCU_EINVAL, "unknown mode");
   CU_TRY(c, cudaSetDevice(c->device));

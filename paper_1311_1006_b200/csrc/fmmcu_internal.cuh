@@ -55,7 +55,7 @@ struct HostBuf {
     p = nullptr;
     cap = 0;
     size_t want = std::max<size_t>(bytes, 256);
-    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocPortable);
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocPortable | cudaHostAllocMapped);
     if (e == cudaSuccess) cap = want;
     return e;
   }
@@ -110,12 +110,25 @@ struct fmmcu_ctx {
   cudaEvent_t ev_kslice[kMaxSlices] = {}, ev_cslice[kMaxSlices] = {};
   int n_slices = 0;
   uint32_t slice_eb[kMaxSlices + 1] = {};
-  bool direct_out = false;  // job->out is page-locked: D2H lands in it directly
+  bool direct_out = false;  // job->out is page-locked: written in place
+  // overlapped launch: upload chunks (leaf-aligned) and need-ordered groups
+  cudaStream_t h2d_stream = nullptr;
+  static constexpr int kMaxChunks = 32;
+  cudaEvent_t ev_chunk[kMaxChunks] = {}, ev_group[kMaxChunks] = {};
+  int n_groups = 0;
+  cudaEvent_t ev_evals = nullptr;  // evals uploaded (overlapped launch, non-self layouts)
+  int group_k = 0;                      // > 0: build_worklist groups leaves by need chunk
+  std::vector<uint32_t> chunk_leaf;     // [group_k + 1] leaf boundaries of the upload chunks
+  std::vector<uint32_t> grp_pos;        // [group_k + 1] first position of each group
+  bool grouped = false;                 // items / fins are in grouped order
+  double2* out_dev = nullptr;           // device view of the launch's output (host memory)
+  bool overlapped = false;              // the in-flight launch took launch_overlapped
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_m2l0 = nullptr, ev_m2l1 = nullptr;
   std::string err;
   uint64_t launches = 0;
 
   // staged job (device)
+  DevBuf d_zin, d_min;  // caller z / m DMA'd as-is (page-locked inputs)
   DevBuf d_src, d_evy, d_eself, d_pt, d_ev, d_soff, d_sidx, d_items, d_fin, d_out, d_partial,
       d_hits, d_seg, d_counter, d_evr;
   // pinned staging
@@ -131,6 +144,9 @@ struct fmmcu_ctx {
   std::vector<uint32_t> item_first;    // [n_leaves + 1]
   std::vector<P2PFinal> fins;
   std::vector<uint32_t> fin_first;     // [n_leaves + 1]
+  // work-list scratch kept across launches (no reallocation / page faults)
+  std::vector<uint64_t> wl_S, wl_pev;
+  std::vector<uint32_t> wl_kc, wl_order;
   bool staged = false;
   bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
   bool warp_items = false;     // work list built for p2p_warp_kernel
@@ -179,7 +195,7 @@ P2PArgs make_args(fmmcu_ctx* c);
 int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j);
 // Device buffers for the CSR + work list, their H2D, the run table and the
 // eval records (needs d_src, d_evy, d_eself filled unless c->self_layout).
-int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j);
+int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals);
 // P2P kernels over leaves [lb, le) of the staged job on c->stream.
 int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
                 bool reset_hits = true);

@@ -112,6 +112,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// TMA 1-D bulk copy shared -> global (bulk async-group completion).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile(
+      "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+      "cp.async.bulk.commit_group;\n" ::"l"(dst),
+      "r"(smem_u32(src)), "r"(bytes)
+      : "memory");
+}
+
+// wait until every committed bulk store has finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// wait until every committed bulk store has completed
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -218,10 +237,11 @@ __device__ __forceinline__ uint32_t find_self_entry(const P2PArgs& a, uint32_t l
   return kNoSelf;
 }
 
-// One warp per leaf, lanes over its evals.
-static __global__ void p2p_evrec_kernel(const P2PArgs a, uint32_t n_leaves, double4* __restrict__ evr) {
-  const uint32_t leaf = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (leaf >= n_leaves) return;
+// One warp per leaf of [leaf_begin, leaf_end), lanes over its evals.
+static __global__ void p2p_evrec_kernel(const P2PArgs a, uint32_t leaf_begin, uint32_t leaf_end,
+                                        double4* __restrict__ evr) {
+  const uint32_t leaf = leaf_begin + blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (leaf >= leaf_end) return;
   for (uint32_t e = a.ev_off[leaf] + (threadIdx.x & 31); e < a.ev_off[leaf + 1]; e += 32) {
     const double2 y = a.evy[e];
     const uint32_t self = a.eself[e];
@@ -233,10 +253,11 @@ static __global__ void p2p_evrec_kernel(const P2PArgs a, uint32_t n_leaves, doub
 
 // Self layout (eval e == source slot e): derive the eval arrays from the
 // already uploaded sources instead of uploading them.
-static __global__ void p2p_self_evals_kernel(const double4* __restrict__ src, uint32_t n,
-                                      double2* __restrict__ evy, uint32_t* __restrict__ eself) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
+static __global__ void p2p_self_evals_kernel(const double4* __restrict__ src, uint32_t i0,
+                                             uint32_t i1, double2* __restrict__ evy,
+                                             uint32_t* __restrict__ eself) {
+  const uint32_t i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < i1) {
     const double4 s = src[i];
     evy[i] = make_double2(s.x, s.y);
     eself[i] = i;

@@ -13,7 +13,10 @@
 //     overlapping chunk c+1;
 //   * lane (g, k) owns E evals of eval-slot g and strides the chunk by K
 //     (broadcast LDS.128); the K partials of each eval are summed over the
-//     lanes g, g+G, g+2G, ... with shuffles in fixed order (deterministic).
+//     lanes g, g+G, g+2G, ... with shuffles in fixed order (deterministic);
+//   * the item's results are staged in shared memory and written with one
+//     TMA bulk store (cp.async.bulk.global.shared::cta), so the output may
+//     live in page-locked host memory (zero-copy over PCIe) as well as HBM.
 #pragma once
 
 #include "p2p_kernels.cuh"
@@ -23,6 +26,10 @@ namespace fmmcu {
 constexpr int kWarpSlots = 8;        // eval slots per warp item: <= 8E evals, K >= 4 source lanes
 constexpr int kWarpMaxEntries = 32;  // strong entries per warp item (one per lane)
 
+constexpr size_t warp_region_bytes(int C, int E) {
+  return 128 + size_t(2 * C) * 32 + size_t(kWarpSlots * E) * 16;
+}
+
 template <int KERNEL, int SMOOTH, int E, int WARPS, int C, int U, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_warp_kernel(const P2PArgs a) {
   static_assert(E >= 1 && kWarpSlots <= 32 && C % 32 == 0, "shape");
@@ -30,11 +37,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_warp_kernel(const P2PArg
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr unsigned FULL = 0xffffffffu;
-  // per-warp region: [2 mbarriers | pad 128][chunk 0][chunk 1]
-  constexpr size_t kWarpBytes = 128 + size_t(2 * C) * 32;
+  // per-warp region: [2 mbarriers | pad 128][chunk 0][chunk 1][item results]
+  constexpr size_t kWarpBytes = warp_region_bytes(C, E);
   unsigned char* base = smem_raw + size_t(warp) * kWarpBytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(base);
   double4* buf = reinterpret_cast<double4*>(base + 128);
+  double2* stage = reinterpret_cast<double2*>(base + 128 + size_t(2 * C) * 32);
 
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -164,6 +172,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_warp_kernel(const P2PArg
       __syncwarp();  // chunk b fully read before it is refilled
     }
 
+    // the previous item's result store must have read the staging area
+    if (lane == 0) bulk_wait_read();
+    __syncwarp();
     // sum the K partials of every eval over lanes g, g+G, ... (fixed order)
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -176,15 +187,19 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_warp_kernel(const P2PArg
         si += vi;
       }
       const uint32_t le = g * E + e;
-      if (k == 0 && active && le < nt) {
-        const double2 res = (KERNEL == 0) ? make_double2(-sr, -si) : make_double2(sr, si);
-        if (it.partial_off == kNoSelf)
-          a.out[ev0 + le] = res;
-        else
-          a.partial[it.partial_off + le] = res;
-      }
+      if (k == 0 && active && le < nt)
+        stage[le] = (KERNEL == 0) ? make_double2(-sr, -si) : make_double2(sr, si);
+    }
+    // one TMA bulk store of the item's nt contiguous results (device memory,
+    // or page-locked host memory written straight over PCIe)
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0 && nt) {
+      double2* dst = (it.partial_off == kNoSelf) ? a.out + ev0 : a.partial + it.partial_off;
+      bulk_s2g(dst, stage, nt * 16u);
     }
   }
+  if (lane == 0) bulk_wait_all();
   for (int o = 16; o > 0; o >>= 1) hits += __shfl_down_sync(FULL, hits, o);
   if (lane == 0 && hits) atomicAdd(a.hits, (unsigned long long)hits);
 }

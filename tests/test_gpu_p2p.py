@@ -231,6 +231,29 @@ def test_sliced_launch_direct_into_registered_output(ctx):
         assert normwise(staged[e0:e1], w[e0:e1]) <= TOL_FP64
 
 
+def test_page_locked_inputs_take_the_dma_path(ctx):
+    """Page-locked z / m: the launch DMAs them as-is and packs the records on
+    the device; results bitwise equal to the staged-copy path, and for a
+    layout that is not self-evaluation (separate evals) too."""
+    for self_eval in (True, False):
+        t, args = _tree_case(0, 1_200_000, 8, 21, self_eval=self_eval, n_eval=700_000)
+        want, pw, _ = _run(ctx, *args)
+        zp = np.ascontiguousarray(args[5]).copy()
+        mp = np.ascontiguousarray(args[6]).copy()
+        out = np.zeros_like(want)
+        for a in (zp, mp, out):
+            ctx.host_register(a)
+        try:
+            a2 = list(args)
+            a2[5], a2[6] = zp, mp
+            got, pg, _ = _run(ctx, *a2, out=out)
+        finally:
+            for a in (zp, mp, out):
+                ctx.host_unregister(a)
+        assert pg == pw
+        assert bitwise(got, want)
+
+
 def test_invalid_jobs_fail_loudly(ctx):
     t, args = _tree_case(0, 1000, 3, 1)
     with pytest.raises(N.FmmcuError):
