@@ -281,32 +281,22 @@ int validate(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
 // for nt * S / 32 useful ones.  Pick the E with the least modelled cost over
 // the job's leaves (38-39 evals/leaf -> E = 5: 8 x 4 lanes, 95% useful,
 // against 89% for E = 4).  FMMCU_P2P_E overrides.
-int choose_warp_e(const uint32_t* ev_off, const std::vector<uint64_t>& S, uint32_t nl) {
+double lane_cost(uint32_t ntl, uint64_t S, int E) {
+  if (!ntl || !S) return 0.0;
+  const uint32_t max_ev = uint32_t(kWarpSlots * E);
+  const uint32_t nblk = (ntl + max_ev - 1) / max_ev;
+  const uint32_t nt = (ntl + nblk - 1) / nblk;
+  const uint32_t G = (nt + E - 1) / E;
+  const uint32_t K = 32 / G;
+  return double(nblk) * double(E) * double((S + K - 1) / K);
+}
+
+int choose_warp_e(double cost4, double cost5) {
   if (const char* env = std::getenv("FMMCU_P2P_E")) {
     const int e = std::atoi(env);
     if (e == 4 || e == 5) return e;
   }
-  double best_cost = 0.0;
-  int best = 4;
-  for (int E : {4, 5}) {
-    const uint32_t max_ev = uint32_t(kWarpSlots * E);
-    double cost = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : cost)
-    for (int64_t t = 0; t < int64_t(nl); ++t) {
-      const uint32_t ntl = ev_off[t + 1] - ev_off[t];
-      if (!ntl || !S[t]) continue;
-      const uint32_t nblk = (ntl + max_ev - 1) / max_ev;
-      const uint32_t nt = (ntl + nblk - 1) / nblk;
-      const uint32_t G = (nt + E - 1) / E;
-      const uint32_t K = 32 / G;
-      cost += double(nblk) * double(E) * double((S[t] + K - 1) / K);
-    }
-    if (E == 4 || cost < best_cost) {
-      best_cost = cost;
-      best = E;
-    }
-  }
-  return best;
+  return cost5 < cost4 ? 5 : 4;
 }
 
 // Work list of a job (host, OpenMP): per-leaf pair work and its prefix,
@@ -349,6 +339,7 @@ void par_prefix(T* v, int64_t n) {
 }
 
 int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  Trace tr(c);
   const uint32_t nl = j->n_leaves;
   c->ev_off.resize(nl + 1);
   c->leaf_work.resize(nl + 1);
@@ -357,26 +348,40 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   uint32_t* evo = c->ev_off.data();
   uint64_t* work = c->leaf_work.data();
   work[0] = 0;
-#pragma omp parallel for schedule(static)
+  c->wl_need.resize(nl);
+  uint32_t* needv = c->wl_need.data();
+  // one pass: sources of the strong list S, last source slot it reads (need),
+  // pair work, and the modelled lane cost of E = 4 and E = 5 (choose_warp_e)
+  double cost4 = 0.0, cost5 = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : cost4, cost5)
   for (int64_t t = 0; t < int64_t(nl); ++t) {
     uint64_t s = 0;
+    uint32_t need = j->pt_off[t + 1];
     for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q) {
       const uint32_t sb = j->strong_idx[q];
-      s += j->pt_off[sb + 1] - j->pt_off[sb];
+      const uint32_t e1 = j->pt_off[sb + 1];
+      s += e1 - j->pt_off[sb];
+      need = std::max(need, e1);
     }
     S[t] = s;
+    needv[t] = need;
     evo[t] = j->ev_off[t];
-    work[t + 1] = uint64_t(j->ev_off[t + 1] - j->ev_off[t]) * s;
+    const uint32_t ntl = j->ev_off[t + 1] - j->ev_off[t];
+    work[t + 1] = uint64_t(ntl) * s;
+    cost4 += lane_cost(ntl, s, 4);
+    cost5 += lane_cost(ntl, s, 5);
   }
   evo[nl] = j->ev_off[nl];
   par_prefix(work, int64_t(nl));
   const uint64_t total = work[nl];
+  tr.mark("wl: S + work prefix");
   const uint64_t budget = std::max<uint64_t>(1ull << 16, total / (148ull * 16ull));
   const bool warp_kernel = use_warp_kernel();
-  c->warp_e = warp_kernel ? choose_warp_e(j->ev_off, S, nl) : 4;
+  c->warp_e = warp_kernel ? choose_warp_e(cost4, cost5) : 4;
   const uint32_t max_ev = warp_kernel ? uint32_t(kWarpSlots * c->warp_e) : uint32_t(kMaxEvalsPerItem);
   const uint32_t max_ent = warp_kernel ? uint32_t(kWarpMaxEntries) : 0xFFFFFFFFu;
   c->warp_items = warp_kernel;
+  tr.mark("wl: choose E");
   // Items: eval blocks of <= max_ev evals (balanced: ceil(ntl / max_ev)
   // blocks of near-equal size); a block whose pair work exceeds the budget is
   // split into strong-list chunks whose partials are summed in chunk order by
@@ -437,24 +442,51 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     const int K = c->group_k;
     std::vector<uint32_t>& kc = c->wl_kc;
     kc.resize(np);
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < int64_t(np); ++i) {
-      const uint32_t t = j->leaf_begin + uint32_t(i);
-      uint32_t need = j->pt_off[t + 1];
-      for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q)
-        need = std::max(need, j->pt_off[j->strong_idx[q] + 1]);
-      // chunk k holds leaves [chunk_leaf[k], chunk_leaf[k+1]), i.e. slots up to pt_off[chunk_leaf[k+1]]
-      int k = 0;
-      while (k < K - 1 && j->pt_off[c->chunk_leaf[k + 1]] < need) ++k;
-      kc[i] = uint32_t(k);
+    // chunk k holds leaves [chunk_leaf[k], chunk_leaf[k+1]), i.e. slots below slot_end[k]
+    uint32_t slot_end[fmmcu_ctx::kMaxChunks];
+    for (int k = 0; k < K; ++k) slot_end[k] = j->pt_off[c->chunk_leaf[k + 1]];
+    // stable parallel counting sort of the shard's leaves by chunk
+    int nb = 1;
+#ifdef _OPENMP
+    nb = omp_get_max_threads();
+#endif
+    const int64_t per = (int64_t(np) + nb - 1) / nb;
+    std::vector<uint32_t> hist(size_t(nb) * (K + 1), 0);
+#pragma omp parallel for schedule(static, 1) num_threads(nb)
+    for (int b = 0; b < nb; ++b) {
+      uint32_t* hb = hist.data() + size_t(b) * (K + 1);
+      const int64_t i1 = std::min<int64_t>(np, (b + 1) * per);
+      for (int64_t i = b * per; i < i1; ++i) {
+        const uint32_t need = needv[j->leaf_begin + i];
+        int k = 0;
+        while (k < K - 1 && slot_end[k] < need) ++k;
+        kc[i] = uint32_t(k);
+        ++hb[k];
+      }
     }
+    // offsets: group k first, then block b within it
     std::vector<uint32_t> cnt(K + 1, 0);
-    for (uint32_t i = 0; i < np; ++i) ++cnt[kc[i] + 1];
-    for (int k = 0; k < K; ++k) cnt[k + 1] += cnt[k];
+    uint32_t run = 0;
+    for (int k = 0; k < K; ++k) {
+      cnt[k] = run;
+      for (int b = 0; b < nb; ++b) {
+        uint32_t& hb = hist[size_t(b) * (K + 1) + k];
+        const uint32_t n = hb;
+        hb = run;
+        run += n;
+      }
+    }
+    cnt[K] = run;
     c->grp_pos.assign(cnt.begin(), cnt.end());
     order.resize(np);
-    for (uint32_t i = 0; i < np; ++i) order[cnt[kc[i]]++] = j->leaf_begin + i;
+#pragma omp parallel for schedule(static, 1) num_threads(nb)
+    for (int b = 0; b < nb; ++b) {
+      uint32_t* hb = hist.data() + size_t(b) * (K + 1);
+      const int64_t i1 = std::min<int64_t>(np, (b + 1) * per);
+      for (int64_t i = b * per; i < i1; ++i) order[hb[kc[i]]++] = j->leaf_begin + uint32_t(i);
+    }
   }
+  tr.mark("wl: grouping");
   auto leaf_at = [&](int64_t pos) { return grouped ? order[pos] : uint32_t(pos); };
   std::vector<uint64_t>& pev_first = c->wl_pev;
   pev_first.resize(np + 1);
@@ -474,6 +506,7 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   par_prefix(c->fin_first.data(), int64_t(np));
   par_prefix(pev_first.data(), int64_t(np));
   const uint64_t partial_evals = pev_first[np];
+  tr.mark("wl: count + prefix");
   if (partial_evals > 0xFFFFFFF0ull) return set_err(c, FMMCU_EINVAL, "partial buffer too large");
   c->partial_evals = partial_evals;
   c->items.resize(c->item_first[np]);
@@ -483,6 +516,7 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     leaf_items(leaf_at(t), c->items.data() + c->item_first[t], c->fins.data() + c->fin_first[t],
                uint32_t(pev_first[t]));
   c->grouped = grouped;
+  tr.mark("wl: fill");
 
   return FMMCU_OK;
 }

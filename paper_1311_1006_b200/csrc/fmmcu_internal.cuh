@@ -146,7 +146,7 @@ struct fmmcu_ctx {
   std::vector<uint32_t> fin_first;     // [n_leaves + 1]
   // work-list scratch kept across launches (no reallocation / page faults)
   std::vector<uint64_t> wl_S, wl_pev;
-  std::vector<uint32_t> wl_kc, wl_order;
+  std::vector<uint32_t> wl_kc, wl_order, wl_need;
   bool staged = false;
   bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
   bool warp_items = false;     // work list built for p2p_warp_kernel
