@@ -289,6 +289,35 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
   uint32_t* half_e = P->half_e.as<uint32_t>();
   uint8_t* fs = P->flag_s.as<uint8_t>();
   uint8_t* fe = P->flag_e.as<uint8_t>();
+  // Self-evaluation: the evals are the sources (same points, same ids), so
+  // while no split value is tied (the count of coords <= split equals the
+  // median rank in every segment) the eval lists and offsets ARE the source
+  // ones and all eval work is skipped.  The first tied split materialises
+  // the eval lists and the build continues with both.
+  bool same = P->self_eval;
+  int* differ = nullptr;
+  int* h_differ = nullptr;
+  if (same) {
+    CU_TRY(c, P->flag.ensure(8));
+    CU_TRY(c, P->h_flag.ensure(16));
+    differ = P->flag.as<int>();
+    h_differ = P->h_flag.as<int>();
+  }
+  // after a split computed with the aliased lists: still no tie anywhere?
+  auto check_same = [&](uint32_t* sxl, uint32_t* syl, const uint32_t* soffl, uint32_t* eoffl,
+                        size_t noff, const uint32_t* half_src) -> int {
+    CU_TRY(c, cudaMemcpyAsync(h_differ, differ, 4, cudaMemcpyDeviceToHost, s));
+    CU_TRY(c, cudaStreamSynchronize(s));
+    if (*h_differ == 0) return FMMCU_OK;
+    same = false;  // materialise the eval lists as they stand
+    CU_TRY(c, cudaMemcpyAsync(EX, sxl, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(EY, syl, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(eoffl, soffl, noff * 4, cudaMemcpyDeviceToDevice, s));
+    if (half_src)  // 2 (noff - 1) + 1 half offsets
+      CU_TRY(c, cudaMemcpyAsync(half_e, half_src, (2 * noff - 1) * 4, cudaMemcpyDeviceToDevice, s));
+    return FMMCU_OK;
+  };
+  if (same) CU_TRY(c, cudaMemsetAsync(differ, 0, 4, s));
   for (int l = 1; l < L; ++l) {
     const uint32_t np = uint32_t(pow4(l - 1));
     const uint32_t* ps = soff + P->off_base[l - 1];
@@ -299,46 +328,83 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
     a.src = zp;
     a.ev = yp;
     a.slist = SX;
-    a.elist = EX;
+    a.elist = same ? SX : EX;
     a.soff = ps;
-    a.eoff = pe;
+    a.eoff = same ? ps : pe;
     a.fallback = pc;
     a.fb_div = 1;
     a.nseg = np;
     a.axis = 0;
     a.smid = xmid_s;
     a.emid = xmid_e;
+    a.differ = same ? differ : nullptr;
     split_kernel<<<blocks(np), TB, 0, s>>>(a);
+    if (same) {
+      // on a tie: eval lists = the source lists before this split
+      if (int rc = check_same(SX, SY, ps, eoff + P->off_base[l - 1], np + 1, nullptr)) return rc;
+    }
     if (N) low_flags_kernel<<<blocks(N), TB, 0, s>>>(SX, N, ps, xmid_s, np, fs);
-    if (M) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EX, M, pe, xmid_e, np, fe);
+    if (M && !same) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EX, M, pe, xmid_e, np, fe);
     if (int rc = partition(c, P, SY, N, fs, ps, xmid_s, np, SYn, s)) return rc;
-    if (int rc = partition(c, P, EY, M, fe, pe, xmid_e, np, EYn, s)) return rc;
+    if (!same)
+      if (int rc = partition(c, P, EY, M, fe, pe, xmid_e, np, EYn, s)) return rc;
     std::swap(SY, SYn);
-    std::swap(EY, EYn);
+    if (!same) std::swap(EY, EYn);
     child_offsets_kernel<<<blocks(np), TB, 0, s>>>(ps, xmid_s, nullptr, np, half_s, nullptr);
-    child_offsets_kernel<<<blocks(np), TB, 0, s>>>(pe, xmid_e, nullptr, np, half_e, nullptr);
+    if (!same)
+      child_offsets_kernel<<<blocks(np), TB, 0, s>>>(pe, xmid_e, nullptr, np, half_e, nullptr);
     // y split of both halves (geometry.cpp:143-146)
     a.slist = SY;
-    a.elist = EY;
+    a.elist = same ? SY : EY;
     a.soff = half_s;
-    a.eoff = half_e;
+    a.eoff = same ? half_s : half_e;
     a.fb_div = 2;
     a.nseg = 2 * np;
     a.axis = 1;
     a.smid = ymid_s;
     a.emid = ymid_e;
+    a.differ = same ? differ : nullptr;
     split_kernel<<<blocks(2 * np), TB, 0, s>>>(a);
+    if (same) {
+      // on a tie: eval lists = source lists after the x split, halves alike
+      if (int rc = check_same(SX, SY, ps, eoff + P->off_base[l - 1], np + 1, half_s)) return rc;
+      if (!same) {
+        // the x split itself had no tie: its eval counts equal the source ones
+        CU_TRY(c, cudaMemcpyAsync(xmid_e, xmid_s, uint64_t(np) * 4, cudaMemcpyDeviceToDevice, s));
+      }
+    }
     if (N) low_flags_kernel<<<blocks(N), TB, 0, s>>>(SY, N, half_s, ymid_s, 2 * np, fs);
-    if (M) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EY, M, half_e, ymid_e, 2 * np, fe);
+    if (M && !same) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EY, M, half_e, ymid_e, 2 * np, fe);
     if (int rc = partition(c, P, SX, N, fs, half_s, ymid_s, 2 * np, SXn, s)) return rc;
-    if (int rc = partition(c, P, EX, M, fe, half_e, ymid_e, 2 * np, EXn, s)) return rc;
+    if (!same)
+      if (int rc = partition(c, P, EX, M, fe, half_e, ymid_e, 2 * np, EXn, s)) return rc;
     std::swap(SX, SXn);
-    std::swap(EX, EXn);
+    if (!same) std::swap(EX, EXn);
     child_offsets_kernel<<<blocks(np), TB, 0, s>>>(ps, xmid_s, ymid_s, np, nullptr,
                                                    soff + P->off_base[l]);
-    child_offsets_kernel<<<blocks(np), TB, 0, s>>>(pe, xmid_e, ymid_e, np, nullptr,
-                                                   eoff + P->off_base[l]);
-    geometry(l);
+    if (!same) {
+      child_offsets_kernel<<<blocks(np), TB, 0, s>>>(pe, xmid_e, ymid_e, np, nullptr,
+                                                     eoff + P->off_base[l]);
+    } else {
+      CU_TRY(c, cudaMemcpyAsync(eoff + P->off_base[l], soff + P->off_base[l],
+                                (pow4(l) + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    if (same) {
+      // geometry reads the eval lists: they are the source lists
+      uint32_t* ex_save = EX;
+      uint32_t* ey_save = EY;
+      EX = SX;
+      EY = SY;
+      geometry(l);
+      EX = ex_save;
+      EY = ey_save;
+    } else {
+      geometry(l);
+    }
+  }
+  if (same) {  // no tie anywhere: eval order = source order
+    EX = SX;
+    EY = SY;
   }
   // leaf-internal order = original index order (geometry.cpp:156-161)
   const uint32_t nleaf = uint32_t(pow4(L - 1));
@@ -353,7 +419,9 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
                             N, bits, s))
       return rc;
   }
-  if (M) {
+  if (M && same) {
+    CU_TRY(c, cudaMemcpyAsync(P->eperm.p, P->perm.p, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
+  } else if (M) {
     leaf_of_kernel<<<blocks(M), TB, 0, s>>>(EX, M, eoff + P->off_base[L - 1], nleaf, leaf_of);
     iota_kernel<<<blocks(M), TB, 0, s>>>(iota, M);
     if (int rc = sort_pairs(c, P, leaf_of, P->keys1.as<uint32_t>(), iota, P->eperm.as<uint32_t>(),

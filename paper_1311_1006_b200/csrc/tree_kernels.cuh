@@ -143,6 +143,7 @@ struct SplitArgs {
   int axis;
   uint32_t* __restrict__ smid;  // [nseg] first high position
   uint32_t* __restrict__ emid;  // [nseg]
+  int* __restrict__ differ;     // non-null: set when emid != smid (eval lists alias sources)
 };
 
 __global__ void split_kernel(const SplitArgs a) {
@@ -165,6 +166,7 @@ __global__ void split_kernel(const SplitArgs a) {
     else hi = m;
   }
   a.emid[s] = lo;
+  if (a.differ && lo != mid) atomicOr(a.differ, 1);
 }
 
 // flag[id] = 1 for the entries of list that fall before mid of their segment
