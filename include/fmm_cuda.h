@@ -167,6 +167,12 @@ typedef struct {
   int smoother;              /* FMMCU_SMOOTH_* (near field only, as the reference) */
   double delta;
   double *out;               /* [2 n_eval] potentials, original eval order */
+  /* optional: called on the launching thread once the inputs have been read
+   * (staged for upload); the host is then idle until the potentials land, so
+   * the caller can prepare its result buffer without competing for memory
+   * bandwidth with the staging copies */
+  void (*inputs_consumed)(void *arg);
+  void *inputs_consumed_arg;
 } fmmcu_fmm_job;
 
 typedef struct {

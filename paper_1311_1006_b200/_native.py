@@ -52,6 +52,8 @@ class FmmJob(C.Structure):
         ("smoother", C.c_int),
         ("delta", C.c_double),
         ("out", C.c_void_p),
+        ("inputs_consumed", C.c_void_p),
+        ("inputs_consumed_arg", C.c_void_p),
     ]
 
 

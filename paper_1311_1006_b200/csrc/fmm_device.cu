@@ -737,6 +737,7 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
     }
   }
   CU_TRY(c, cudaEventRecord(ev[1], s));
+  if (j->inputs_consumed) j->inputs_consumed(j->inputs_consumed_arg);
 
   // ---- pyramid + connectivity ------------------------------------------------
   if (int rc = build_pyramid_dev(c, P, j->theta, s)) return rc;

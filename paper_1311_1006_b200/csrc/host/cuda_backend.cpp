@@ -88,7 +88,14 @@ CudaBackend::DeviceEval CudaBackend::fmm_evaluate(const SourceSet& sources, cons
   // it has finished.  reserve() fixes the storage, so data() stays valid.
   out.clear();
   out.reserve(evals.size());
-  std::thread zero_fill([&out, n = evals.size()] { resize_huge(out, n); });
+  // started once the pipeline has read the inputs (the host then only waits
+  // on the device), so the fill does not compete with the upload staging
+  std::thread zero_fill;
+  struct Hook {
+    std::thread* t;
+    std::vector<cplx>* out;
+    std::size_t n;
+  } hook{&zero_fill, &out, evals.size()};
   fmmcu_fmm_job j{};
   j.n_src = std::uint32_t(sources.size());
   j.n_eval = std::uint32_t(evals.size());
@@ -105,9 +112,15 @@ CudaBackend::DeviceEval CudaBackend::fmm_evaluate(const SourceSet& sources, cons
                                                            : FMMCU_SMOOTH_PLUMMER;
   j.delta = smoother.delta;
   j.out = nullptr;
+  j.inputs_consumed = [](void* arg) {
+    auto* h = static_cast<Hook*>(arg);
+    *h->t = std::thread([out = h->out, n = h->n] { resize_huge(*out, n); });
+  };
+  j.inputs_consumed_arg = &hook;
   fmmcu_fmm_stats st{};
   int rc = fmmcu_fmm_launch(ctx_[0], &j);
-  zero_fill.join();
+  if (zero_fill.joinable()) zero_fill.join();
+  else resize_huge(out, evals.size());
   if (rc == FMMCU_OK)
     rc = fmmcu_fmm_finish(ctx_[0], evals.size() ? reinterpret_cast<double*>(out.data()) : nullptr,
                           &st);
