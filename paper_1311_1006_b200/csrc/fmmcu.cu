@@ -180,11 +180,11 @@ void launch_warp_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
 // warp-kernel variants (warps/CTA, chunk, unroll, min CTAs/SM) for the hot
 // instantiation (harmonic, no smoother); E (evals per lane) is chosen per
 // staged job by choose_warp_e():
-//   0 = 4w c128 u2(E4)/u1(E5) m4   1 = 4w c128 u2 m3   2 = 4w c128 u1 m5
+//   0 = 4w c128 u2 m4   1 = 4w c128 u2 m3   2 = 4w c128 u1 m5
 //   3 = 8w c128 u1 m2              4 = 4w c256 u1 m4   5 = 4w c128 u2 m4
 template <int KN, int SM, int E>
 void launch_warp_e(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
-  constexpr int U0 = E >= 5 ? 1 : 2;
+  constexpr int U0 = 2;  // E5 U2 measured best (profiles/r01: 1.027 vs 1.018 Tpairs/s for U1)
   if (KN == 0 && SM == 0) {
     switch (variant_index()) {
       case 1: launch_warp_v<KN, SM, 4, E, 128, 2, 3>(a, n_items, s); return;
