@@ -188,18 +188,18 @@ static __global__ void __launch_bounds__(kM2LWarps * 32) m2l_batched_kernel(cons
 constexpr int kM2LConstP1 = 40;
 static __constant__ double c_m2l_table[kM2LConstP1 * kM2LConstP1];
 
-template <int P1>
-static __global__ void __launch_bounds__(128) m2l_thread_kernel(const M2LArgs a) {
+template <int P1, int TBK = (P1 > 20 ? 64 : 128)>
+static __global__ void __launch_bounds__(TBK, 384 / TBK) m2l_thread_kernel(const M2LArgs a) {
+  // local coefficients in shared memory, [l][thread] (conflict-free), so the
+  // registers hold only the partner's v_k: 12 warps/SM instead of 8
+  __shared__ double2 s_c[P1][TBK];
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int l = 0; l < P1; ++l) s_c[l][tid] = make_double2(0.0, 0.0);
   if (t >= a.n_targets) return;
   const double2 ct = a.centers[a.target_box[t]];
   const bool harm = a.kernel == 0;
-  double cr[P1], ci[P1];
-#pragma unroll
-  for (int l = 0; l < P1; ++l) {
-    cr[l] = 0.0;
-    ci[l] = 0.0;
-  }
   const uint32_t w0 = a.weak_off[t], w1 = a.weak_off[t + 1];
   for (uint32_t wi = w0; wi < w1; ++wi) {
     const uint32_t sb = a.weak_idx[wi];
@@ -263,14 +263,16 @@ static __global__ void __launch_bounds__(128) m2l_thread_kernel(const M2LArgs a)
         add = acc;
         for (int r = 0; r < l; ++r) add = cmul(add, w);
       }
-      cr[l] += add.x;
-      ci[l] += add.y;
+      double2 cur = s_c[l][tid];
+      cur.x += add.x;
+      cur.y += add.y;
+      s_c[l][tid] = cur;
       wl = cmul(wl, w);
     }
   }
   double2* o = a.out + (size_t)t * P1;
 #pragma unroll
-  for (int l = 0; l < P1; ++l) o[l] = make_double2(cr[l], ci[l]);
+  for (int l = 0; l < P1; ++l) o[l] = s_c[l][tid];
 }
 
 // Upload the binomial table of the thread kernel (this translation unit's
@@ -285,17 +287,19 @@ static inline cudaError_t m2l_set_const_table(const double* T, int P1, cudaStrea
 // otherwise.  The constant table must have been set for a.p (thread path).
 static inline void launch_m2l(const M2LArgs& a, cudaStream_t s) {
   if (a.n_targets == 0) return;
-  const uint32_t tb = 128, g = (a.n_targets + tb - 1) / tb;
+  auto go = [&](auto kern, uint32_t tb) {
+    kern<<<(a.n_targets + tb - 1) / tb, tb, 0, s>>>(a);
+  };
   switch (a.p + 1) {
-    case 12: m2l_thread_kernel<12><<<g, tb, 0, s>>>(a); return;
-    case 14: m2l_thread_kernel<14><<<g, tb, 0, s>>>(a); return;
-    case 15: m2l_thread_kernel<15><<<g, tb, 0, s>>>(a); return;
-    case 17: m2l_thread_kernel<17><<<g, tb, 0, s>>>(a); return;
-    case 18: m2l_thread_kernel<18><<<g, tb, 0, s>>>(a); return;
-    case 19: m2l_thread_kernel<19><<<g, tb, 0, s>>>(a); return;
-    case 20: m2l_thread_kernel<20><<<g, tb, 0, s>>>(a); return;
-    case 22: m2l_thread_kernel<22><<<g, tb, 0, s>>>(a); return;
-    case 25: m2l_thread_kernel<25><<<g, tb, 0, s>>>(a); return;
+    case 12: go(m2l_thread_kernel<12>, 128); return;
+    case 14: go(m2l_thread_kernel<14>, 128); return;
+    case 15: go(m2l_thread_kernel<15>, 128); return;
+    case 17: go(m2l_thread_kernel<17>, 128); return;
+    case 18: go(m2l_thread_kernel<18>, 128); return;
+    case 19: go(m2l_thread_kernel<19>, 128); return;
+    case 20: go(m2l_thread_kernel<20>, 128); return;
+    case 22: go(m2l_thread_kernel<22>, 64); return;
+    case 25: go(m2l_thread_kernel<25>, 64); return;
     default:
       m2l_batched_kernel<<<(a.n_targets + kM2LWarps - 1) / kM2LWarps, kM2LWarps * 32, 0, s>>>(a);
   }
