@@ -268,6 +268,12 @@ def run_ours(args):
     prefix = ctx.work_prefix(wl["n_leaves"])
     cuts = shard_cuts(prefix, world)
     lb, le = int(cuts[rank]), int(cuts[rank + 1])
+    if world > 1:
+        # the (mutual) work list is built for the rank's own leaf range
+        job, keep = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
+                                           wl["zp"], wl["mp"], wl["yp"], wl["sid"], None,
+                                           leaf_begin=lb, leaf_end=le)
+        ctx.stage(job, keep)
     slices = eval_slices(wl["ev"], cuts)
     full = torch.zeros(2 * n_eval, dtype=torch.float64, device=f"cuda:{local}")
     torch.cuda.synchronize()

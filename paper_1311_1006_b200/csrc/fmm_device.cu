@@ -52,6 +52,7 @@ struct DevicePipeline {
   int L = 0, p = 0, kernel = 0;
   uint32_t N = 0, M = 0, n_targets = 0, m2l_nnz = 0;
   bool self_eval = false;
+  bool layout_same = false;
   bool tree_valid = false;
   cudaStream_t far = nullptr;
   cudaEvent_t ev[12] = {};
@@ -406,6 +407,7 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
     EX = SX;
     EY = SY;
   }
+  P->layout_same = same;  // eval slot e is source slot e (self layout)
   // leaf-internal order = original index order (geometry.cpp:156-161)
   const uint32_t nleaf = uint32_t(pow4(L - 1));
   int bits = 1;
@@ -807,6 +809,7 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   c->self_layout = false;
   c->ext_out = nullptr;
   c->group_k = 0;
+  c->sym_request = self && P->layout_same && j->kernel == 0 && !std::getenv("FMMCU_NO_SYM");
   if (int rc = build_worklist(c, &pj)) return rc;
   if (int rc = stage_csr(c, &pj, true)) return rc;
   CU_TRY(c, cudaEventRecord(ev[8], s));

@@ -24,6 +24,7 @@
 #include "m2l_kernels.cuh"
 #include "p2p_kernels.cuh"
 #include "p2p_warp.cuh"
+#include "p2p_sym.cuh"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -241,6 +242,38 @@ void dispatch_exact(int kn, int sm, const P2PArgs& a, uint32_t lb, uint32_t le, 
   }
 }
 
+template <int SM, int E>
+void launch_sym_v(const P2PArgs& a, const P2PSymArgs& sa, uint32_t n_items, cudaStream_t s) {
+  constexpr int W = 4, C = 128, U = 1, MINB = 3;
+  auto kfn = p2p_sym_kernel<SM, E, W, C, U, MINB>;
+  constexpr size_t smem = warp_smem(W, C, E);
+  static int grid_cap = [&] {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, W * 32, smem);
+    return std::max(1, sms * std::max(1, per_sm));
+  }();
+  const uint32_t need = (n_items + W - 1) / W;
+  const uint32_t grid = std::max(1u, std::min<uint32_t>(need, uint32_t(grid_cap)));
+  kfn<<<grid, W * 32, smem, s>>>(a, sa);
+}
+
+void dispatch_sym(int sm, const P2PArgs& a, const P2PSymArgs& sa, uint32_t n, cudaStream_t s,
+                  int E) {
+  if (E == 5) {
+    if (sm == 0) launch_sym_v<0, 5>(a, sa, n, s);
+    else if (sm == 1) launch_sym_v<1, 5>(a, sa, n, s);
+    else launch_sym_v<2, 5>(a, sa, n, s);
+  } else {
+    if (sm == 0) launch_sym_v<0, 4>(a, sa, n, s);
+    else if (sm == 1) launch_sym_v<1, 4>(a, sa, n, s);
+    else launch_sym_v<2, 4>(a, sa, n, s);
+  }
+}
+
 int validate(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   if (!j) return set_err(c, FMMCU_EINVAL, "null job");
   if (j->kernel < 0 || j->kernel > 1) return set_err(c, FMMCU_EINVAL, "unknown kernel");
@@ -297,6 +330,118 @@ int choose_warp_e(double cost4, double cost5) {
     if (e == 4 || e == 5) return e;
   }
   return cost5 < cost4 ? 5 : 4;
+}
+
+template <class T>
+void par_prefix(T* v, int64_t n);
+
+// Symmetric (mutual) work list over the job's leaf range [lb, le) (see
+// p2p_sym.cuh).  Returns 1 when the job does not qualify (a leaf with more
+// than 32 entries, or a source count that needs budget splitting): the caller
+// then builds the ordinary list.
+int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
+  const uint32_t lb = j->leaf_begin, le = j->leaf_end, np = le - lb;
+  const uint32_t* po = j->pt_off;
+  auto npts = [&](uint32_t b) { return po[b + 1] - po[b]; };
+  std::vector<uint32_t> ent(np + 1, 0), nblk(np + 1, 0);
+  std::vector<uint64_t> ssym(np, 0), sord(np, 0), slots(np + 1, 0);
+  bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+  for (int64_t i = 0; i < int64_t(np); ++i) {
+    const uint32_t t = lb + uint32_t(i);
+    uint32_t n = 0;
+    uint64_t so = 0, ss = 0;
+    for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q) {
+      const uint32_t B = j->strong_idx[q];
+      if (B >= lb && B < le && B < t) continue;  // the lower partner's item covers it
+      ++n;
+      if (B > t && B < le && B >= lb) ss += npts(B);
+      else so += npts(B);
+    }
+    const uint32_t ntl = j->ev_off[t + 1] - j->ev_off[t];
+    const uint32_t nb = ntl ? (ntl + max_ev - 1) / max_ev : 0;
+    ok = ok && n <= uint32_t(kWarpMaxEntries) && so + ss < (1ull << 31);
+    ent[i + 1] = n;
+    nblk[i + 1] = nb;
+    ssym[i] = ss;
+    sord[i] = so;
+    slots[i + 1] = uint64_t(nb) * ss;
+  }
+  if (!ok) return 1;
+  par_prefix(ent.data(), int64_t(np));
+  par_prefix(nblk.data(), int64_t(np));
+  par_prefix(slots.data(), int64_t(np));
+  if (slots[np] > 0xFFFFFFF0ull) return 1;
+  c->sym_seg.resize(ent[np]);
+  c->items.resize(nblk[np]);
+  c->item_first.assign(nblk.begin(), nblk.end());
+  c->fin_first.assign(np + 1, 0);
+  c->fins.clear();
+  c->partial_evals = 0;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < int64_t(np); ++i) {
+    const uint32_t t = lb + uint32_t(i);
+    uint4* sg = c->sym_seg.data() + ent[i];
+    uint32_t o = 0;
+    for (int pass = 0; pass < 2; ++pass)  // ordered runs first, then symmetric
+      for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q) {
+        const uint32_t B = j->strong_idx[q];
+        const bool inr = B >= lb && B < le;
+        if (inr && B < t) continue;
+        const bool sym = inr && B > t;
+        if (sym != (pass == 1)) continue;
+        const uint32_t kind = sym ? kRunSym : (B == t ? kRunSelf : kRunOrdered);
+        sg[o++] = make_uint4(po[B], npts(B), kind, 0u);
+      }
+    const uint32_t ntl = j->ev_off[t + 1] - j->ev_off[t];
+    const uint32_t nb = nblk[i + 1] - nblk[i];
+    for (uint32_t b = 0, e0 = 0; b < nb; ++b) {
+      const uint32_t nt = (ntl - e0) / (nb - b) + ((ntl - e0) % (nb - b) ? 1u : 0u);
+      P2PItem it{t, j->ev_off[t] + e0, nt, ent[i], ent[i + 1], uint32_t(sord[i] + ssym[i]),
+                 uint32_t(slots[i] + uint64_t(b) * ssym[i]), uint32_t(sord[i])};
+      c->items[nblk[i] + b] = it;
+      e0 += nt;
+    }
+  }
+  // per leaf B: the contrib slot of B's first source in every item of each
+  // lower partner t (ascending t, then eval block)
+  c->cl_off.assign(np + 1, 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < int64_t(np); ++i) {
+    const uint32_t B = lb + uint32_t(i);
+    uint32_t n = 0;
+    for (uint32_t q = j->strong_off[B]; q < j->strong_off[B + 1]; ++q) {
+      const uint32_t t = j->strong_idx[q];
+      if (t >= lb && t < B) n += nblk[t - lb + 1] - nblk[t - lb];
+    }
+    c->cl_off[i + 1] = n;
+  }
+  par_prefix(c->cl_off.data(), int64_t(np));
+  c->cl_base.resize(c->cl_off[np]);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < int64_t(np); ++i) {
+    const uint32_t B = lb + uint32_t(i);
+    uint32_t w = c->cl_off[i];
+    for (uint32_t q = j->strong_off[B]; q < j->strong_off[B + 1]; ++q) {
+      const uint32_t t = j->strong_idx[q];
+      if (!(t >= lb && t < B)) continue;
+      // offset of B's run inside t's symmetric part
+      uint64_t voff = 0;
+      for (uint32_t r = j->strong_off[t]; r < j->strong_off[t + 1]; ++r) {
+        const uint32_t B2 = j->strong_idx[r];
+        if (B2 > t && B2 < B && B2 >= lb && B2 < le) voff += npts(B2);
+      }
+      const uint32_t ti = t - lb;
+      for (uint32_t b = 0; b < nblk[ti + 1] - nblk[ti]; ++b)
+        c->cl_base[w++] = uint32_t(slots[ti] + uint64_t(b) * ssym[ti] + voff);
+    }
+  }
+  c->sym_slots = slots[np];
+  c->sym_lb = lb;
+  c->sym_le = le;
+  c->sym_items = true;
+  c->grouped = false;
+  return FMMCU_OK;
 }
 
 // Work list of a job (host, OpenMP): per-leaf pair work and its prefix,
@@ -381,6 +526,13 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const uint32_t max_ev = warp_kernel ? uint32_t(kWarpSlots * c->warp_e) : uint32_t(kMaxEvalsPerItem);
   const uint32_t max_ent = warp_kernel ? uint32_t(kWarpMaxEntries) : 0xFFFFFFFFu;
   c->warp_items = warp_kernel;
+  c->sym_items = false;
+  if (c->sym_request && warp_kernel && c->group_k == 0 && j->kernel == 0) {
+    if (build_sym_worklist(c, j, max_ev) == FMMCU_OK) {
+      tr.mark("wl: symmetric");
+      return FMMCU_OK;
+    }
+  }
   tr.mark("wl: choose E");
   // Items: eval blocks of <= max_ev evals (balanced: ceil(ntl / max_ev)
   // blocks of near-equal size); a block whose pair work exceeds the budget is
@@ -536,8 +688,15 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->delta = j->delta;
 
   Trace tr(c);
-  std::future<int> worklist =
-      std::async(std::launch::async, [c, j] { return build_worklist(c, j); });
+  // Plausibly self-evaluation (cheap test): the work list waits for the
+  // per-element check of the packing loop, and is built symmetric if it holds.
+  const bool maybe_sym = j->eval_sid && ne == ns && ns > 0 && j->kernel == 0 &&
+                         j->mode == FMMCU_MODE_FAST && !std::getenv("FMMCU_NO_SYM") &&
+                         std::memcmp(j->ev_off, j->pt_off, size_t(nl + 1) * 4) == 0;
+  c->sym_request = false;
+  std::future<int> worklist;
+  if (!maybe_sym)
+    worklist = std::async(std::launch::async, [c, j] { return build_worklist(c, j); });
   cudaStream_t s = c->stream;
   CU_TRY(c, c->d_src.ensure(size_t(ns) * 32));
   CU_TRY(c, c->d_evy.ensure(size_t(ne) * 16));
@@ -611,7 +770,12 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   tr.mark("evals");
 
   // ---- work list (built concurrently with the source packing above) -------
-  if (int rc = worklist.get()) return rc;
+  if (maybe_sym) {
+    c->sym_request = self_layout;
+    if (int rc = build_worklist(c, j)) return rc;
+  } else if (int rc = worklist.get()) {
+    return rc;
+  }
   tr.mark("worklist");
   if (int rc = stage_csr(c, j, true)) return rc;
   tr.mark("csr+worklist h2d");
@@ -684,6 +848,27 @@ int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals) {
     p2p_evrec_kernel<<<(nl + 7) / 8, 256, 0, s>>>(make_args(c), 0, nl, c->d_evr.as<double4>());
     c->launches += 1;
   }
+  if (c->sym_items) {
+    const size_t nseg = c->sym_seg.size(), ncl = c->cl_base.size();
+    CU_TRY(c, c->d_symseg.ensure(std::max<size_t>(nseg, 1) * 16));
+    CU_TRY(c, c->d_cloff.ensure(c->cl_off.size() * 4));
+    CU_TRY(c, c->d_clbase.ensure(std::max<size_t>(ncl, 1) * 4));
+    CU_TRY(c, c->d_tgt.ensure(size_t(std::max(ne, 1u)) * 16));
+    CU_TRY(c, c->d_contrib.ensure(std::max<uint64_t>(c->sym_slots, 1) * 16));
+    const size_t sym_bytes = nseg * 16 + c->cl_off.size() * 4 + ncl * 4;
+    CU_TRY(c, c->h_sym.ensure(sym_bytes));
+    unsigned char* hb = c->h_sym.as<unsigned char>();
+    par_memcpy(hb, c->sym_seg.data(), nseg * 16);
+    par_memcpy(hb + nseg * 16, c->cl_off.data(), c->cl_off.size() * 4);
+    par_memcpy(hb + nseg * 16 + c->cl_off.size() * 4, c->cl_base.data(), ncl * 4);
+    if (nseg) CU_TRY(c, cudaMemcpyAsync(c->d_symseg.p, hb, nseg * 16, cudaMemcpyHostToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(c->d_cloff.p, hb + nseg * 16, c->cl_off.size() * 4,
+                              cudaMemcpyHostToDevice, s));
+    if (ncl)
+      CU_TRY(c, cudaMemcpyAsync(c->d_clbase.p, hb + nseg * 16 + c->cl_off.size() * 4, ncl * 4,
+                                cudaMemcpyHostToDevice, s));
+    c->h2d_bytes += sym_bytes;
+  }
   CU_TRY(c, cudaGetLastError());
   c->staged = true;
   return FMMCU_OK;
@@ -726,6 +911,7 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     c->chunk_leaf[k] = std::max(c->chunk_leaf[k - 1], std::min(t, nl));
   }
   c->group_k = K;
+  c->sym_request = false;
   // The work list (~1 ms on all cores at 10M) is built first, on this thread:
   // built concurrently it starves behind the OpenMP packing team and the DMA
   // traffic, and every group needs it before its kernels can be enqueued.
@@ -950,6 +1136,22 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
         dispatch_exact(c->kernel, c->smoother, a, lb, le, eb, ee, s);
         ++n;
       }
+    } else if (c->sym_items) {
+      if (lb != c->sym_lb || le != c->sym_le)
+        return set_err(c, FMMCU_ESTATE, "symmetric work list staged for another leaf range");
+      const uint32_t ni = uint32_t(c->items.size());
+      P2PSymArgs sa{c->d_symseg.as<uint4>(), c->d_tgt.as<double2>(), c->d_contrib.as<double2>()};
+      if (ni) {
+        P2PArgs aa = a;
+        aa.n_items = ni;
+        dispatch_sym(c->smoother, aa, sa, ni, s, c->warp_e);
+        ++n;
+      }
+      const uint32_t nlr = le - lb;
+      p2p_sym_finalize_kernel<<<(nlr + 7) / 8, 256, 0, s>>>(
+          lb, nlr, c->d_pt.as<uint32_t>(), c->d_cloff.as<uint32_t>(), c->d_clbase.as<uint32_t>(),
+          c->d_tgt.as<double2>(), c->d_contrib.as<double2>(), c->out_ptr());
+      ++n;
     } else {
       const uint32_t i0 = c->item_first[lb], i1 = c->item_first[le];
       if (i1 > i0) {
@@ -1096,6 +1298,9 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamSynchronize(c->h2d_stream);
     fmmcu::destroy_pipeline(c->pipe);
     c->pipe = nullptr;
+    for (DevBuf* b : {&c->d_symseg, &c->d_cloff, &c->d_clbase, &c->d_tgt, &c->d_contrib})
+      b->release();
+    c->h_sym.release();
     for (DevBuf* b : {&c->d_zin, &c->d_min, &c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
                       &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter, &c->d_evr,
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,

@@ -15,6 +15,7 @@
 
 #include "fmm_cuda.h"
 #include "p2p_kernels.cuh"
+#include "p2p_warp.cuh"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -147,6 +148,16 @@ struct fmmcu_ctx {
   // work-list scratch kept across launches (no reallocation / page faults)
   std::vector<uint64_t> wl_S, wl_pev;
   std::vector<uint32_t> wl_kc, wl_order, wl_need;
+  // mutual (symmetric) P2P for self-evaluation (p2p_sym.cuh)
+  bool sym_request = false;             // caller: evals are the sources, harmonic, fast
+  bool sym_items = false;               // the staged work list is symmetric
+  uint32_t sym_lb = 0, sym_le = 0;      // leaf range the symmetric list covers
+  std::vector<uint4> sym_seg;           // per-leaf entries: (slot, n, kind, 0)
+  std::vector<uint32_t> sym_first;      // [range + 1] first entry of each leaf
+  std::vector<uint32_t> cl_off, cl_base;  // contributions to add per leaf (finalize)
+  uint64_t sym_slots = 0;               // contrib slots
+  DevBuf d_symseg, d_cloff, d_clbase, d_tgt, d_contrib;
+  HostBuf h_sym;
   bool staged = false;
   bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
   bool warp_items = false;     // work list built for p2p_warp_kernel

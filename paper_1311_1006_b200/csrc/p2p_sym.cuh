@@ -1,0 +1,301 @@
+// fmm-b200 — mutual (symmetric) P2P kernel for self-evaluation, sm_100a.
+//
+// When every eval is its own source (EvalSet::self_of, the benchmark and the
+// vortex configurations) the harmonic pair term is antisymmetric:
+//     contribution of j at i:  -m_j / (z_i - z_j) = -m_j w,
+//     contribution of i at j:  -m_i / (z_j - z_i) = +m_i w,   w = conj(d)/|d|^2,
+// so a leaf pair (A, B) needs d, |d|^2, 1/|d|^2 and w once for both
+// directions: 17 FP64 instructions per unordered pair instead of 2 x 13.
+// (near_box, proj/src/backend.cpp:41-69, evaluates every ordered pair; the
+// smoother factor g(|d|) is symmetric too.)
+//
+// Work item = eval block of target leaf A with three kinds of source runs
+// (host: build_worklist, symmetric mode), ordered in the item's virtual
+// stream as [ordered | symmetric]:
+//   * ordered:   A's own run (self pairs skipped, as p2p_warp_kernel) and
+//                strong partners outside the job's leaf range;
+//   * symmetric: partners B with A < B inside the range.  For each of their
+//                sources j the lanes also sum m_i w over A's evals (a fixed
+//                order segmented shuffle reduction over the G eval slots) and
+//                store it at contrib[sym_base + (v - V0)].
+// Partners B < A are skipped: the item of B covered the pair.  A's own
+// potentials go to tgt[]; p2p_sym_finalize_kernel then adds, per source, the
+// contributions stored by the items of its lower partners, in a fixed order,
+// so results are deterministic.  Same lane layout, TMA bulk-copy pipeline and
+// result store as p2p_warp_kernel.
+#pragma once
+
+#include "p2p_warp.cuh"
+
+namespace fmmcu {
+
+// symmetric-mode strong entry: first source slot, count, kind, unused
+constexpr uint32_t kRunOrdered = 0, kRunSelf = 1, kRunSym = 2;
+
+struct P2PSymArgs {
+  const uint4* __restrict__ sym_seg;  // per item entry: (slot, n, kind, 0)
+  double2* __restrict__ tgt;          // target-side potentials (permuted eval order)
+  double2* __restrict__ contrib;      // per symmetric source slot of each item
+};
+
+template <int SMOOTH>
+__device__ __forceinline__ void sym_pair(double yx, double yy, double mex, double mey,
+                                         const double4 s, double inv_d2, double d2, double& ar,
+                                         double& ai, double& cr, double& ci) {
+  const double dx = yx - s.x;
+  const double dy = yy - s.y;
+  const double r2 = fma(dx, dx, dy * dy);
+  double inv = rcp_fast(r2);
+  if (SMOOTH == 1) {
+    const double g = 1.0 - exp(-r2 * inv_d2);
+    inv = (g == 0.0) ? 0.0 : inv * g;
+  } else if (SMOOTH == 2) {
+    const double g = sqrt(r2 / (d2 + r2));
+    inv = (g == 0.0) ? 0.0 : inv * g;
+  }
+  const double wr = dx * inv;
+  const double wi = -dy * inv;
+  ar = fma(s.z, wr, fma(-s.w, wi, ar));  // acc_i += m_j w
+  ai = fma(s.z, wi, fma(s.w, wr, ai));
+  cr = fma(mex, wr, fma(-mey, wi, cr));  // c_j += m_i w
+  ci = fma(mex, wi, fma(mey, wr, ci));
+}
+
+template <int SMOOTH, int E, int WARPS, int C, int U, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs a,
+                                                                   const P2PSymArgs sa) {
+  static_assert(C % 32 == 0, "shape");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr size_t kWarpBytes = warp_region_bytes(C, E);
+  unsigned char* base = smem_raw + size_t(warp) * kWarpBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base);
+  double4* buf = reinterpret_cast<double4*>(base + 128);
+  double2* stage = reinterpret_cast<double2*>(base + 128 + size_t(2 * C) * 32);
+
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  uint32_t parity0 = 0, parity1 = 0;
+  unsigned int hits = 0;
+  uint32_t claim = 0;
+  if (lane == 0) claim = atomicAdd(a.next_item, 1u);
+
+  for (;;) {
+    const uint32_t id = __shfl_sync(FULL, claim, 0);
+    if (id >= a.n_items) break;
+    if (lane == 0) claim = atomicAdd(a.next_item, 1u);
+    const P2PItem it = a.items[id];
+    const uint32_t nt = it.nt, ev0 = it.ev_begin;
+    const uint32_t nent = it.s_end - it.s_begin;  // <= 32 (host)
+    const uint32_t nsrc = it.n_src;
+    const uint32_t V0 = it.pad;             // virtual positions of the ordered runs
+    const uint32_t sym_base = it.partial_off;
+
+    uint32_t rb = 0, rn = 0, kind = kRunOrdered;
+    if (uint32_t(lane) < nent) {
+      const uint4 sg = sa.sym_seg[it.s_begin + lane];
+      rb = sg.x;
+      rn = sg.y;
+      kind = sg.z;
+    }
+    uint32_t incl = rn;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t roff = incl - rn;
+    // the self run (one per item): its first slot and virtual offset
+    const unsigned self_mask = __ballot_sync(FULL, uint32_t(lane) < nent && kind == kRunSelf);
+    const int self_lane = self_mask ? __ffs(self_mask) - 1 : 0;
+    const uint32_t self_rb = __shfl_sync(FULL, rb, self_lane);
+    const uint32_t self_roff = __shfl_sync(FULL, roff, self_lane);
+
+    auto issue_chunk = [&](uint32_t c, int b) {
+      const uint32_t v0 = c * C;
+      const uint32_t v1 = min(nsrc, v0 + C);
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&bar[b], (v1 - v0) * 32u);
+      }
+      __syncwarp();
+      const uint32_t lo = max(roff, v0), hi = min(roff + rn, v1);
+      if (hi > lo) bulk_g2s(buf + b * C + (lo - v0), a.src + rb + (lo - roff), (hi - lo) * 32u, &bar[b]);
+    };
+    const uint32_t nchunk = (nsrc + C - 1) / C;
+    if (nchunk > 0) issue_chunk(0, 0);
+
+    const uint32_t G = (nt + E - 1) / E;
+    const float rG = 1.0f / float(G);
+    const uint32_t K = uint32_t(32.0f * rG + 1e-4f);
+    const uint32_t k = uint32_t((float(lane) + 0.5f) * rG);
+    const uint32_t g = uint32_t(lane) - k * G;
+    const bool active = k < K;
+
+    double yx[E], yy[E], ar[E], ai[E], mx[E], my[E];
+    uint32_t vself[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t le = g * E + e;
+      const bool ok = active && le < nt;
+      // padded slots sit far away with zero strength: no NaN, no contribution
+      const double4 r = ok ? a.evr[ev0 + le] : make_double4(1e30, 1e30, 0.0, 0.0);
+      const double4 me = ok ? a.src[ev0 + le] : make_double4(0.0, 0.0, 0.0, 0.0);
+      yx[e] = r.x;
+      yy[e] = r.y;
+      mx[e] = me.z;
+      my[e] = me.w;
+      ar[e] = 0.0;
+      ai[e] = 0.0;
+      // self layout: eval slot ev0 + le is its own source slot
+      vself[e] = (ok && self_mask) ? self_roff + (ev0 + le - self_rb) : kNoSelf;
+      if (vself[e] != kNoSelf && k == 0) ++hits;
+    }
+
+    for (uint32_t c = 0; c < nchunk; ++c) {
+      const int b = int(c & 1u);
+      if (c + 1 < nchunk) issue_chunk(c + 1, b ^ 1);
+      const uint32_t v0 = c * C;
+      const uint32_t len = min(nsrc - v0, uint32_t(C));
+      const uint32_t ord_end = V0 > v0 ? min(V0 - v0, len) : 0u;  // chunk-relative
+      uint32_t ps[E];
+      uint32_t plo = kNoSelf, phi = 0u;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t d = vself[e] - v0;
+        ps[e] = (vself[e] != kNoSelf && d < len) ? d : kNoSelf;
+        if (ps[e] != kNoSelf) {
+          plo = min(plo, ps[e]);
+          phi = max(phi, ps[e]);
+        }
+      }
+      plo = __reduce_min_sync(FULL, plo);
+      phi = __reduce_max_sync(FULL, phi);
+      if (b == 0) {
+        mbar_wait(&bar[0], parity0);
+        parity0 ^= 1u;
+      } else {
+        mbar_wait(&bar[1], parity1);
+        parity1 ^= 1u;
+      }
+      const double4* chunk = buf + b * C;
+      // ---- ordered runs (self + outside the range): as p2p_warp_kernel
+      if (active && ord_end > 0) {
+        const double4* p = chunk + k;
+        const double4* const end = chunk + ord_end;
+        p = run_unchecked<0, SMOOTH, E, U>(p, chunk + min(plo, ord_end), K, yx, yy, a.inv_delta2,
+                                            a.delta2, ar, ai);
+        if (plo != kNoSelf && plo < ord_end) {
+          const double4* const end2 = chunk + min(phi + 1u, ord_end);
+          for (; p < end2; p += K) {
+            const double4 s = *p;
+            const uint32_t j = uint32_t(p - chunk);
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+              pair_accum<0, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, j != ps[e], ar[e],
+                                    ai[e]);
+          }
+          run_unchecked<0, SMOOTH, E, U>(p, end, K, yx, yy, a.inv_delta2, a.delta2, ar, ai);
+        }
+      }
+      // ---- symmetric runs: every k-group walks the same number of steps so
+      // the per-source reductions over its G lanes stay warp-uniform
+      if (len > ord_end) {
+        const uint32_t nsym = len - ord_end;
+        const uint32_t steps = (nsym + K - 1) / K;
+        // two sources per step with independent sums: the FP64 work of one
+        // overlaps the shuffle reduction of the other
+        for (uint32_t st = 0; st < steps; st += 2) {
+          const uint32_t j0 = ord_end + st * K + k, j1 = j0 + K;
+          const bool v0ok = active && j0 < len, v1ok = active && j1 < len;
+          const double4 s0 = v0ok ? chunk[j0] : make_double4(-1e30, -1e30, 0.0, 0.0);
+          const double4 s1 = v1ok ? chunk[j1] : make_double4(-1e30, -1e30, 0.0, 0.0);
+          double c0r = 0.0, c0i = 0.0, c1r = 0.0, c1i = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], s0, a.inv_delta2, a.delta2, ar[e], ai[e],
+                             c0r, c0i);
+            sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], s1, a.inv_delta2, a.delta2, ar[e], ai[e],
+                             c1r, c1i);
+          }
+          // sum over the G eval slots of this k-group (lanes kG .. kG+G-1),
+          // fixed tree order
+#pragma unroll
+          for (uint32_t o = 1; o < 8; o <<= 1) {
+            const double t0r = __shfl_down_sync(FULL, c0r, o);
+            const double t0i = __shfl_down_sync(FULL, c0i, o);
+            const double t1r = __shfl_down_sync(FULL, c1r, o);
+            const double t1i = __shfl_down_sync(FULL, c1i, o);
+            if (g + o < G) {
+              c0r += t0r;
+              c0i += t0i;
+              c1r += t1r;
+              c1i += t1i;
+            }
+          }
+          if (g == 0) {
+            if (v0ok) sa.contrib[sym_base + (v0 + j0 - V0)] = make_double2(c0r, c0i);
+            if (v1ok) sa.contrib[sym_base + (v0 + j1 - V0)] = make_double2(c1r, c1i);
+          }
+        }
+      }
+      __syncwarp();
+    }
+
+    if (lane == 0) bulk_wait_read();
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      double sr = ar[e], si = ai[e];
+      for (uint32_t kk = 1; kk < K; ++kk) {
+        const int src = int(g + kk * G) & 31;
+        const double vr = __shfl_sync(FULL, ar[e], src);
+        const double vi = __shfl_sync(FULL, ai[e], src);
+        sr += vr;
+        si += vi;
+      }
+      const uint32_t le = g * E + e;
+      if (k == 0 && active && le < nt) stage[le] = make_double2(-sr, -si);
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0 && nt) bulk_s2g(sa.tgt + ev0, stage, nt * 16u);
+  }
+  if (lane == 0) bulk_wait_all();
+  for (int o = 16; o > 0; o >>= 1) hits += __shfl_down_sync(FULL, hits, o);
+  if (lane == 0 && hits) atomicAdd(a.hits, (unsigned long long)hits);
+}
+
+// out[i] = tgt[i] + the contributions the items of i's lower partners stored
+// for it, in the host's fixed order (leaf L's list: cl_off[L] .. cl_off[L+1]
+// of cl_base, each a contrib index of L's first source).  One warp per leaf.
+static __global__ void p2p_sym_finalize_kernel(uint32_t leaf0, uint32_t n_leaves,
+                                               const uint32_t* __restrict__ pt_off,
+                                               const uint32_t* __restrict__ cl_off,
+                                               const uint32_t* __restrict__ cl_base,
+                                               const double2* __restrict__ tgt,
+                                               const double2* __restrict__ contrib,
+                                               double2* __restrict__ out) {
+  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_leaves) return;
+  const uint32_t L = leaf0 + w;
+  const uint32_t b = pt_off[L], e = pt_off[L + 1];
+  const uint32_t q0 = cl_off[w], q1 = cl_off[w + 1];
+  for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) {
+    double2 v = tgt[i];
+    for (uint32_t q = q0; q < q1; ++q) {
+      const double2 c = contrib[cl_base[q] + (i - b)];
+      v.x += c.x;
+      v.y += c.y;
+    }
+    out[i] = v;
+  }
+}
+
+}  // namespace fmmcu

@@ -168,7 +168,9 @@ def test_staged_device_path_matches_launch(ctx):
     n = ctx.run_staged(0, nl)
     assert n >= 1
     assert ctx.pairs() == pairs_full
-    assert bitwise(ctx.copy_out(len(full)), full)
+    # self-evaluation: the staged path runs the mutual (symmetric) kernel
+    staged = ctx.copy_out(len(full))
+    assert normwise(staged, full) <= TOL_FP64
     # potentials written straight into a torch-owned device tensor
     import torch
     buf = torch.zeros(full.size, dtype=torch.float64, device="cuda:0")
@@ -177,7 +179,7 @@ def test_staged_device_path_matches_launch(ctx):
     ctx.run_staged(0, nl)
     ctx.synchronize()
     ctx.bind_device_out(None)
-    assert bitwise(buf.cpu().numpy().reshape(full.shape), full)
+    assert bitwise(buf.cpu().numpy().reshape(full.shape), staged)
 
 
 def test_linearity_at_scale(ctx):
@@ -223,7 +225,7 @@ def test_sliced_launch_direct_into_registered_output(ctx):
     ctx.stage(job, keep)
     ctx.run_staged(0, nl)
     assert ctx.pairs() == p_staged
-    assert bitwise(ctx.copy_out(len(staged)), staged)
+    assert normwise(ctx.copy_out(len(staged)), staged) <= TOL_FP64
     csr = O.LeafCSR(*args[:5])
     for lb in (0, nl // 2, nl - 1):
         w, _ = O.nearfield(csr, *args[5:9], leaf_begin=lb, leaf_end=lb + 1)
@@ -252,6 +254,47 @@ def test_page_locked_inputs_take_the_dma_path(ctx):
                 ctx.host_unregister(a)
         assert pg == pw
         assert bitwise(got, want)
+
+
+@pytest.mark.parametrize("case", [(0, 200_000, 7, 31, 0), (0, 150_000, 7, 32, 1),
+                                  (2, 200_000, 7, 33, 0), (3, 60_000, 6, 34, 2)])
+def test_symmetric_kernel_vs_oracle(ctx, case):
+    """Self-evaluation through the staged path runs the mutual kernel
+    (p2p_sym.cuh): each leaf pair once, contributions reduced in a fixed
+    order.  Pair counts exact, potentials <= 1e-12 normwise of the oracle,
+    deterministic, and a leaf-range job (ordered runs outside the range)."""
+    kind, n, L, seed, sm = case
+    t, args = _tree_case(kind, n, L, seed)
+    delta = 0.01 if sm else 0.0
+    csr = O.LeafCSR(*args[:5])
+    want, wpairs = O.nearfield(csr, *args[5:9], smoother=sm, delta=delta)
+    nl = len(args[0]) - 1
+    outs = []
+    for rep in range(2):
+        job, keep = N.CudaContext.make_job(*args, None, smoother=sm, delta=delta)
+        ctx.stage(job, keep)
+        ctx.run_staged(0, nl)
+        assert ctx.pairs() == wpairs
+        outs.append(ctx.copy_out(len(want)))
+    assert normwise(outs[0], want) <= TOL_FP64
+    assert bitwise(outs[0], outs[1])
+    # a leaf range: partners outside it run as ordered pairs
+    a, b = nl // 4, nl - nl // 3
+    job, keep = N.CudaContext.make_job(*args, None, smoother=sm, delta=delta,
+                                       leaf_begin=a, leaf_end=b)
+    ctx.stage(job, keep)
+    ctx.run_staged(a, b)
+    part = ctx.copy_out(len(want))
+    e0, e1 = int(args[1][a]), int(args[1][b])
+    assert normwise(part[e0:e1], want[e0:e1]) <= TOL_FP64
+    # a symmetric list staged for [a, b) refuses another range; an ordinary
+    # one (clustered inputs exceed 32 entries per leaf) may run it
+    try:
+        ctx.run_staged(0, nl)
+    except N.FmmcuError:
+        pass
+    else:
+        assert normwise(ctx.copy_out(len(want)), want) <= TOL_FP64
 
 
 def test_invalid_jobs_fail_loudly(ctx):
