@@ -280,6 +280,7 @@ def run_ours(args):
     ctx.bind_device_out(full.data_ptr())
     gather = PotentialGather(slices, rank, full) if world > 1 else None
     fp64_peak = ctx.fp64_peak()
+    symmetric, evals_per_lane = ctx.kernel_info()
 
     def barrier():
         if world > 1:
@@ -454,8 +455,19 @@ def run_ours(args):
                                         "(fmmcu_fp64_peak); nominal 148x64x2x1.965GHz = "
                                         f"{NOMINAL_FP64_TFLOPS:.1f}",
                          "frac_of_nominal": achieved / NOMINAL_FP64_TFLOPS,
-                         "kernel": "fmmcu::p2p_warp_kernel<harmonic,none> (E evals/lane chosen per job)", "kernel_ms": kernel_ms,
-                         "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": int(my_pairs)},
+                         "kernel": (("fmmcu::p2p_sym_kernel<none> (mutual: each leaf pair "
+                                     "once, 17 FP64 instr per unordered pair) + "
+                                     "p2p_sym_finalize_kernel") if symmetric else
+                                    "fmmcu::p2p_warp_kernel<harmonic,none> (13 FP64 instr per pair)")
+                                   + f", E={evals_per_lane} evals/lane",
+                         "kernel_ms": kernel_ms,
+                         "flops_per_pair": FLOPS_PER_PAIR,
+                         "flops_note": "algorithmic work per ORDERED pair as the reference "
+                                       "evaluates it (SURVEY.md 8d); the mutual kernel "
+                                       "executes 8.5 FP64 instructions per ordered pair, so "
+                                       "frac > 23/26 = 0.88 is possible; ncu FP64 pipe "
+                                       "utilisation is in profiles/",
+                         "pairs_per_launch": int(my_pairs)},
             "e2e": e2e,
             "fmm_evals_per_sec": fmm,
             "cpu_baseline": cpu,

@@ -213,6 +213,9 @@ uint64_t fmmcu_kernel_launches(const fmmcu_ctx *ctx);
 /* Host<->device bytes moved by the last fmmcu_p2p_launch (H2D: packed
  * sources, evals, self map, CSR and work list; D2H: potentials + counter). */
 int fmmcu_last_transfer_bytes(const fmmcu_ctx *ctx, uint64_t *h2d, uint64_t *d2h);
+/* Shape of the staged fast work list: *symmetric = 1 when the mutual kernel
+ * runs (self-evaluation: each leaf pair once), *evals_per_lane = E. */
+int fmmcu_p2p_kernel_info(const fmmcu_ctx *ctx, int *symmetric, int *evals_per_lane);
 /* Measured FP64 FMA throughput of this device (TFLOP/s, DFMA = 2 flops). */
 int fmmcu_fp64_peak(fmmcu_ctx *ctx, double *tflops);
 

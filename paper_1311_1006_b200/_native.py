@@ -142,7 +142,7 @@ CUDA_SYMBOLS = [
     "fmmcu_synchronize", "fmmcu_m2l_launch", "fmmcu_m2l_finish", "fmmcu_kernel_launches",
     "fmmcu_fp64_peak", "fmmcu_last_transfer_bytes", "fmmcu_host_register", "fmmcu_host_unregister",
     "fmmcu_fmm_evaluate", "fmmcu_fmm_launch", "fmmcu_fmm_finish", "fmmcu_fmm_tree_level", "fmmcu_fmm_tree_perm", "fmmcu_fmm_tree_lists",
-    "fmmcu_hypot_batch",
+    "fmmcu_hypot_batch", "fmmcu_p2p_kernel_info",
 ]
 
 
@@ -179,6 +179,7 @@ def cuda_lib():
         lib.fmmcu_fmm_tree_perm.argtypes = [vp, vp, vp]
         lib.fmmcu_fmm_tree_lists.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_uint64), vp, vp]
         lib.fmmcu_hypot_batch.argtypes = [vp, vp, C.c_uint32, vp]
+        lib.fmmcu_p2p_kernel_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         lib.fmmcu_synchronize.argtypes = [vp]
         lib.fmmcu_m2l_launch.argtypes = [vp, C.POINTER(M2LJob)]
         lib.fmmcu_m2l_finish.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
@@ -399,6 +400,12 @@ class CudaContext:
         h2d, d2h = C.c_uint64(), C.c_uint64()
         self._check(self.lib.fmmcu_last_transfer_bytes(self.h, C.byref(h2d), C.byref(d2h)))
         return int(h2d.value), int(d2h.value)
+
+    def kernel_info(self):
+        """(symmetric, evals_per_lane) of the staged fast work list."""
+        sym, e = C.c_int(), C.c_int()
+        self._check(self.lib.fmmcu_p2p_kernel_info(self.h, C.byref(sym), C.byref(e)))
+        return bool(sym.value), int(e.value)
 
     def fp64_peak(self) -> float:
         v = C.c_double()

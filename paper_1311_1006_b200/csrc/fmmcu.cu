@@ -246,7 +246,7 @@ template <int SM, int E>
 void launch_sym_v(const P2PArgs& a, const P2PSymArgs& sa, uint32_t n_items, cudaStream_t s) {
   constexpr int W = 4, C = 128, U = 1, MINB = 3;
   auto kfn = p2p_sym_kernel<SM, E, W, C, U, MINB>;
-  constexpr size_t smem = warp_smem(W, C, E);
+  constexpr size_t smem = size_t(W) * sym_region_bytes(C, E);
   static int grid_cap = [&] {
     cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -1549,6 +1549,13 @@ int fmmcu_p2p_work_prefix(fmmcu_ctx* c, uint64_t* prefix) {
   if (!c || !prefix) return FMMCU_EINVAL;
   if (!c->staged) return set_err(c, FMMCU_ESTATE, "no staged job");
   std::memcpy(prefix, c->leaf_work.data(), sizeof(uint64_t) * c->leaf_work.size());
+  return FMMCU_OK;
+}
+
+int fmmcu_p2p_kernel_info(const fmmcu_ctx* c, int* symmetric, int* evals_per_lane) {
+  if (!c) return FMMCU_EINVAL;
+  if (symmetric) *symmetric = c->sym_items ? 1 : 0;
+  if (evals_per_lane) *evals_per_lane = c->warp_e;
   return FMMCU_OK;
 }
 

@@ -32,6 +32,11 @@ namespace fmmcu {
 // symmetric-mode strong entry: first source slot, count, kind, unused
 constexpr uint32_t kRunOrdered = 0, kRunSelf = 1, kRunSym = 2;
 
+// per-warp shared region: the p2p_warp_kernel one + the [8][32] partials
+constexpr size_t sym_region_bytes(int C, int E) {
+  return warp_region_bytes(C, E) + size_t(kWarpSlots) * 32 * 16;
+}
+
 struct P2PSymArgs {
   const uint4* __restrict__ sym_seg;  // per item entry: (slot, n, kind, 0)
   double2* __restrict__ tgt;          // target-side potentials (permuted eval order)
@@ -69,11 +74,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr unsigned FULL = 0xffffffffu;
-  constexpr size_t kWarpBytes = warp_region_bytes(C, E);
+  constexpr size_t kWarpBytes = sym_region_bytes(C, E);
   unsigned char* base = smem_raw + size_t(warp) * kWarpBytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(base);
   double4* buf = reinterpret_cast<double4*>(base + 128);
   double2* stage = reinterpret_cast<double2*>(base + 128 + size_t(2 * C) * 32);
+  double2* part = reinterpret_cast<double2*>(base + warp_region_bytes(C, E));  // [8][32]
 
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -207,42 +213,46 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
       // ---- symmetric runs: every k-group walks the same number of steps so
       // the per-source reductions over its G lanes stay warp-uniform
       if (len > ord_end) {
+        // Blocks of F steps (F K <= 32 sources): every lane parks its
+        // E-eval partial of each source in shared memory (part[g][slot]); one
+        // lane per source then sums the G partials in g order and stores the
+        // contribution -- no shuffle chain inside the FP64 loop.
         const uint32_t nsym = len - ord_end;
         const uint32_t steps = (nsym + K - 1) / K;
-        // two sources per step with independent sums: the FP64 work of one
-        // overlaps the shuffle reduction of the other
-        for (uint32_t st = 0; st < steps; st += 2) {
-          const uint32_t j0 = ord_end + st * K + k, j1 = j0 + K;
-          const bool v0ok = active && j0 < len, v1ok = active && j1 < len;
-          const double4 s0 = v0ok ? chunk[j0] : make_double4(-1e30, -1e30, 0.0, 0.0);
-          const double4 s1 = v1ok ? chunk[j1] : make_double4(-1e30, -1e30, 0.0, 0.0);
-          double c0r = 0.0, c0i = 0.0, c1r = 0.0, c1i = 0.0;
+        const uint32_t F = 32 / K;
+        for (uint32_t sb = 0; sb < steps; sb += F) {
+          const uint32_t nst = min(F, steps - sb);
+          for (uint32_t st = 0; st < nst; st += 2) {
+            const uint32_t j0 = ord_end + (sb + st) * K + k, j1 = j0 + K;
+            const bool v0ok = active && j0 < len;
+            const bool v1ok = active && st + 1 < nst && j1 < len;
+            const double4 s0 = v0ok ? chunk[j0] : make_double4(-1e30, -1e30, 0.0, 0.0);
+            const double4 s1 = v1ok ? chunk[j1] : make_double4(-1e30, -1e30, 0.0, 0.0);
+            double c0r = 0.0, c0i = 0.0, c1r = 0.0, c1i = 0.0;
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], s0, a.inv_delta2, a.delta2, ar[e], ai[e],
-                             c0r, c0i);
-            sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], s1, a.inv_delta2, a.delta2, ar[e], ai[e],
-                             c1r, c1i);
-          }
-          // sum over the G eval slots of this k-group (lanes kG .. kG+G-1),
-          // fixed tree order
-#pragma unroll
-          for (uint32_t o = 1; o < 8; o <<= 1) {
-            const double t0r = __shfl_down_sync(FULL, c0r, o);
-            const double t0i = __shfl_down_sync(FULL, c0i, o);
-            const double t1r = __shfl_down_sync(FULL, c1r, o);
-            const double t1i = __shfl_down_sync(FULL, c1i, o);
-            if (g + o < G) {
-              c0r += t0r;
-              c0i += t0i;
-              c1r += t1r;
-              c1i += t1i;
+            for (int e = 0; e < E; ++e) {
+              sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], s0, a.inv_delta2, a.delta2, ar[e],
+                               ai[e], c0r, c0i);
+              sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], s1, a.inv_delta2, a.delta2, ar[e],
+                               ai[e], c1r, c1i);
+            }
+            if (active) {
+              part[g * 32 + st * K + k] = make_double2(c0r, c0i);
+              if (st + 1 < nst) part[g * 32 + (st + 1) * K + k] = make_double2(c1r, c1i);
             }
           }
-          if (g == 0) {
-            if (v0ok) sa.contrib[sym_base + (v0 + j0 - V0)] = make_double2(c0r, c0i);
-            if (v1ok) sa.contrib[sym_base + (v0 + j1 - V0)] = make_double2(c1r, c1i);
+          __syncwarp();
+          const uint32_t jj = ord_end + sb * K + uint32_t(lane);
+          if (uint32_t(lane) < nst * K && jj < len) {
+            double2 acc = part[lane];
+            for (uint32_t gg = 1; gg < G; ++gg) {
+              const double2 v = part[gg * 32 + lane];
+              acc.x += v.x;
+              acc.y += v.y;
+            }
+            sa.contrib[sym_base + (v0 + jj - V0)] = acc;
           }
+          __syncwarp();
         }
       }
       __syncwarp();
