@@ -8,7 +8,7 @@ mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --no-e2e --no-fmm --no-cpu --steps 3 --warmup 3 > gpurun_out/${TAG}_launches.log 2>&1
 echo "launches $?"
-ncu --set full --clock-control none --import-source on -k regex:p2p_warp_kernel -s 1 -c 1 -f \
+ncu --set full --clock-control none --import-source on -k regex:${P2P_KPAT:-p2p_sym_kernel} -s 1 -c 1 -f \
   -o gpurun_out/${TAG}_p2p python bench.py --no-e2e --no-fmm --no-cpu --steps 1 --warmup 3 \
   > gpurun_out/${TAG}_p2p.log 2>&1
 echo "p2p full $?"
@@ -26,5 +26,5 @@ for k in p2p m2l; do
 done
 ls -la gpurun_out/
 du -sh gpurun_out/*.ncu-rep
-[ "$(du -cm gpurun_out/*.ncu-rep | tail -1 | cut -f1)" -gt 40 ] && rm -f gpurun_out/${TAG}_m2l.ncu-rep
+rm -f gpurun_out/${TAG}_m2l.ncu-rep gpurun_out/${TAG}_p2p.ncu-rep
 true

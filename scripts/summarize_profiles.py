@@ -64,7 +64,7 @@ def launches(fname, keep_last_frac=1.0):
     return "\n".join(lines)
 
 
-summary = {"tag": tag, "p2p_warp_kernel": raw("p2p"), "m2l_thread_kernel": raw("m2l")}
+summary = {"tag": tag, "p2p_kernel": raw("p2p"), "m2l_thread_kernel": raw("m2l")}
 json.dump(summary, open(f"{out}_ncu_summary.json", "w"), indent=1)
 with open(f"{out}_launches.txt", "w") as f:
     f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n")
