@@ -1063,9 +1063,21 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     return FMMCU_OK;
   };
 
-  for (int k = 0; k < K; ++k) {
-    const uint32_t l0 = c->chunk_leaf[k], l1 = c->chunk_leaf[k + 1];
-    const int64_t c0 = j->pt_off[l0], c1 = j->pt_off[l1];
+  // Halo-only upload for a leaf range: only the sources of the range's
+  // strong lists (its own leaves + a halo) are read by its kernels; the rest
+  // of the device array is left untouched.
+  const bool partial = lb > 0 || le < nl;
+  std::vector<uint8_t> needed;
+  if (partial) {
+    needed.assign(nl, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t t = lb; t < int64_t(le); ++t)
+      for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q)
+        needed[j->strong_idx[q]] = 1;
+    h2d -= uint64_t(ns) * 32;
+  }
+  // pack / DMA source slots [c0, c1) and self-check them; returns the check
+  auto upload = [&](int64_t c0, int64_t c1, int k) -> int {
     bool same = maybe_self;
     if (direct_in) {
       if (c1 > c0) {
@@ -1074,7 +1086,6 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
         CU_TRY(c, cudaMemcpyAsync(c->d_min.as<double>() + 2 * c0, m + 2 * c0,
                                   size_t(c1 - c0) * 16, cudaMemcpyHostToDevice, h));
       }
-      CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
       if (maybe_self) {
 #pragma omp parallel for schedule(static) reduction(&& : same)
         for (int64_t i = c0; i < c1; ++i)
@@ -1095,13 +1106,35 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       if (c1 > c0)
         CU_TRY(c, cudaMemcpyAsync(c->d_src.as<double>() + 4 * c0, hs + 4 * c0,
                                   size_t(c1 - c0) * 32, cudaMemcpyHostToDevice, h));
-      CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
     }
+    if (partial) h2d += uint64_t(c1 - c0) * 32;
     if (maybe_self && !same && c1 > c0) {
       if (int rc = host_evals(c0, c1)) return rc;
       h2d += uint64_t(c1 - c0) * 20;
     }
-    chunk_self[k] = maybe_self && same;
+    if (!same) chunk_self[k] = 0;
+    return FMMCU_OK;
+  };
+
+  for (int k = 0; k < K; ++k) {
+    const uint32_t l0 = c->chunk_leaf[k], l1 = c->chunk_leaf[k + 1];
+    chunk_self[k] = maybe_self ? 1 : 0;
+    if (!partial) {
+      if (int rc = upload(j->pt_off[l0], j->pt_off[l1], k)) return rc;
+    } else {
+      for (uint32_t t = l0; t < l1;) {  // runs of needed leaves
+        if (!needed[t]) {
+          ++t;
+          continue;
+        }
+        uint32_t t1 = t + 1;
+        while (t1 < l1 && needed[t1]) ++t1;
+        if (int rc = upload(j->pt_off[t], j->pt_off[t1], k)) return rc;
+        t = t1;
+      }
+    }
+    CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+    const bool same = chunk_self[k] != 0;
     all_self = all_self && same;
     if (c->trace)
       std::fprintf(stderr, "[fmmcu] chunk %2d enqueued at %8.3f ms\n", k,
