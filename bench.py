@@ -374,6 +374,9 @@ def run_ours(args):
                        "in leaf-aligned chunks overlapping the kernels, potentials written "
                        "to host memory by the kernels' TMA bulk stores"}
 
+    # the P2P context's pinned staging (~1 GB) is released before the engine runs
+    del full
+    ctx.close()
     # ---- FMM evals/s through FmmEngine(cuda) (rank 0, single device) -------------
     # (a) device_pipeline: the whole evaluate() on the GPU (tree + lists bit-exact,
     #     P2M/M2M/M2L/L2L/P2P/L2P kernels); host arrays in, potentials out.
@@ -410,6 +413,31 @@ def run_ours(args):
         if not args.no_cpu and world == 1:
             fmm["cpu_baseline"] = cpu_fmm_baseline(s, e, args)
         del s, e
+        # configs 2 and 3 (1M points): the level count autotuned
+        # by sweeping L as acceptance does; device pipeline, median of 3
+        others = {}
+        for name, dist, seed in (("config2_uniform_1M", "uniform", 2),
+                                 ("config3_gauss8_1M", "gauss8", 3)):
+            s2 = F.make_distribution(dist, 1_000_000, seed)
+            e2 = F.EvalSet.self_of(s2)
+            best = None
+            for L in (7, 8, 9):
+                eng = F.FmmEngine(F.FmmConfig(n_levels=L, backend="cuda", devices=(local,),
+                                              device_pipeline=True))
+                eng.evaluate(s2, e2)
+                rs = sorted((eng.evaluate(s2, e2) for _ in range(3)),
+                            key=lambda r: r.timings["t_total"])
+                r = rs[1]
+                if best is None or r.timings["t_total"] < best[1].timings["t_total"]:
+                    best = (L, r)
+                del eng
+            L, r = best
+            others[name] = {"value": 1.0 / r.timings["t_total"], "unit": "evals/s",
+                            "n_levels": L, "t_total_ms": round(1e3 * r.timings["t_total"], 3),
+                            "t_p2p_ms": round(1e3 * r.timings["t_p2p"], 3),
+                            "p2p_pairs": r.counters["p2p_pairs"],
+                            "m2l_ops": r.counters["m2l_ops"]}
+        fmm["other_configs"] = others
         # config 5: vortex-sheet time stepping, N = 2M, 100 Euler steps, AT3b
         # tuner (cap 0.1) rebalancing theta / n_levels online, device pipeline
         vcfg = F.FmmConfig(theta=0.5, n_levels=9, p_rule="formula", backend="cuda",
@@ -477,7 +505,6 @@ def run_ours(args):
             "setup_s": {"generate": round(wl["gen_s"], 3), "tree": round(wl["tree_s"], 3)},
         }
         print(json.dumps(line), flush=True)
-    ctx.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
