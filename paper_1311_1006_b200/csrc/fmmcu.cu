@@ -242,9 +242,8 @@ void dispatch_exact(int kn, int sm, const P2PArgs& a, uint32_t lb, uint32_t le, 
   }
 }
 
-template <int SM, int E>
+template <int SM, int E, int W = 4, int C = 128, int U = 1, int MINB = 3>
 void launch_sym_v(const P2PArgs& a, const P2PSymArgs& sa, uint32_t n_items, cudaStream_t s) {
-  constexpr int W = 4, C = 128, U = 1, MINB = 3;
   auto kfn = p2p_sym_kernel<SM, E, W, C, U, MINB>;
   constexpr size_t smem = size_t(W) * sym_region_bytes(C, E);
   static int grid_cap = [&] {
@@ -261,8 +260,27 @@ void launch_sym_v(const P2PArgs& a, const P2PSymArgs& sa, uint32_t n_items, cuda
   kfn<<<grid, W * 32, smem, s>>>(a, sa);
 }
 
+// mutual-kernel shapes (FMMCU_SYM_VARIANT, harmonic / no smoother, E = 5):
+//   0 = 4w c128 u1 m3   1 = 4w c256 u1 m3   2 = 2w c128 u1 m6   3 = 4w c128 u2 m3
+int sym_variant() {
+  static int v = [] {
+    const char* e = std::getenv("FMMCU_SYM_VARIANT");
+    const int i = e ? std::atoi(e) : 0;
+    return (i >= 0 && i < 4) ? i : 0;
+  }();
+  return v;
+}
+
 void dispatch_sym(int sm, const P2PArgs& a, const P2PSymArgs& sa, uint32_t n, cudaStream_t s,
                   int E) {
+  if (E == 5 && sm == 0) {
+    switch (sym_variant()) {
+      case 1: launch_sym_v<0, 5, 4, 256, 1, 3>(a, sa, n, s); return;
+      case 2: launch_sym_v<0, 5, 2, 128, 1, 6>(a, sa, n, s); return;
+      case 3: launch_sym_v<0, 5, 4, 128, 2, 3>(a, sa, n, s); return;
+      default: break;
+    }
+  }
   if (E == 5) {
     if (sm == 0) launch_sym_v<0, 5>(a, sa, n, s);
     else if (sm == 1) launch_sym_v<1, 5>(a, sa, n, s);
