@@ -14,6 +14,7 @@
 // reference's (p2p_pairs, m2l_ops, p2m_points, l2p_points); phase times are
 // device event spans.
 #include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <cmath>
 #include <cstdio>
@@ -184,15 +185,24 @@ int sorted_list(fmmcu_ctx* c, DevicePipeline* P, const double2* pts, uint32_t n,
 
 // Stable partition of every segment of `list` (offsets off[0..nseg], first
 // high slot mid[seg]) by the per-id flags; result in `out`.
+struct FlagOf {
+  const uint8_t* flag;
+  __host__ __device__ uint32_t operator()(uint32_t id) const { return flag[id]; }
+};
+
+// The scan reads the flags through the list on the fly (no gathered copy);
+// the scatter re-reads them (10 MB of flags stay in L2).
 int partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint32_t n,
               const uint8_t* flag, const uint32_t* off, const uint32_t* mid, uint32_t nseg,
               uint32_t* out, cudaStream_t s) {
   if (!n) return FMMCU_OK;
-  uint32_t* ind = P->ind.as<uint32_t>();
   uint32_t* scan = P->scan.as<uint32_t>();
-  gather_flags_kernel<<<blocks(n), TB, 0, s>>>(list, n, flag, ind);
-  if (int rc = scan_excl(c, P, ind, scan, n, s)) return rc;
-  partition_kernel<<<blocks(n), TB, 0, s>>>(list, n, off, mid, nseg, ind, scan, out);
+  auto it = thrust::make_transform_iterator(list, FlagOf{flag});
+  size_t bytes = 0;
+  CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, scan, int64_t(n), s));
+  CU_TRY(c, P->cub_tmp.ensure(bytes));
+  CU_TRY(c, cub::DeviceScan::ExclusiveSum(P->cub_tmp.p, bytes, it, scan, int64_t(n), s));
+  partition_flags_kernel<<<blocks(n), TB, 0, s>>>(list, n, off, mid, nseg, flag, scan, out);
   return FMMCU_OK;
 }
 

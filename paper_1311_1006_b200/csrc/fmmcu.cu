@@ -8,6 +8,7 @@
 // NearFieldStats (exact pair count, busy seconds) at finish.  Also hosts the
 // batched M2L launch and an FP64 peak micro-benchmark.
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -358,11 +359,24 @@ void par_prefix(T* v, int64_t n);
 // than 32 entries, or a source count that needs budget splitting): the caller
 // then builds the ordinary list.
 int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
+  Trace tr(c);
   const uint32_t lb = j->leaf_begin, le = j->leaf_end, np = le - lb;
   const uint32_t* po = j->pt_off;
   auto npts = [&](uint32_t b) { return po[b + 1] - po[b]; };
-  std::vector<uint32_t> ent(np + 1, 0), nblk(np + 1, 0);
-  std::vector<uint64_t> ssym(np, 0), sord(np, 0), slots(np + 1, 0);
+  // scratch kept in the context (no reallocation / first-touch faults per call)
+  std::vector<uint32_t>& ent = c->sw_ent;
+  std::vector<uint32_t>& nblk = c->sw_nblk;
+  std::vector<uint64_t>& ssym = c->sw_ssym;
+  std::vector<uint64_t>& sord = c->sw_sord;
+  std::vector<uint64_t>& slots = c->sw_slots;
+  ent.resize(np + 1);
+  nblk.resize(np + 1);
+  ssym.resize(np);
+  sord.resize(np);
+  slots.resize(np + 1);
+  ent[0] = 0;
+  nblk[0] = 0;
+  slots[0] = 0;
   bool ok = true;
 #pragma omp parallel for schedule(static) reduction(&& : ok)
   for (int64_t i = 0; i < int64_t(np); ++i) {
@@ -386,6 +400,7 @@ int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
     slots[i + 1] = uint64_t(nb) * ss;
   }
   if (!ok) return 1;
+  tr.mark("sym: count");
   par_prefix(ent.data(), int64_t(np));
   par_prefix(nblk.data(), int64_t(np));
   par_prefix(slots.data(), int64_t(np));
@@ -421,39 +436,16 @@ int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
       e0 += nt;
     }
   }
-  // per leaf B: the contrib slot of B's first source in every item of each
-  // lower partner t (ascending t, then eval block)
-  c->cl_off.assign(np + 1, 0);
+  tr.mark("sym: entries + items");
+  // per leaf of the range: (first entry, first item, first contrib slot,
+  // symmetric sources per item); the finalize kernel finds each lower
+  // partner's contributions from these and the strong lists
+  c->sym_info.resize(size_t(np) + 1);
 #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < int64_t(np); ++i) {
-    const uint32_t B = lb + uint32_t(i);
-    uint32_t n = 0;
-    for (uint32_t q = j->strong_off[B]; q < j->strong_off[B + 1]; ++q) {
-      const uint32_t t = j->strong_idx[q];
-      if (t >= lb && t < B) n += nblk[t - lb + 1] - nblk[t - lb];
-    }
-    c->cl_off[i + 1] = n;
-  }
-  par_prefix(c->cl_off.data(), int64_t(np));
-  c->cl_base.resize(c->cl_off[np]);
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < int64_t(np); ++i) {
-    const uint32_t B = lb + uint32_t(i);
-    uint32_t w = c->cl_off[i];
-    for (uint32_t q = j->strong_off[B]; q < j->strong_off[B + 1]; ++q) {
-      const uint32_t t = j->strong_idx[q];
-      if (!(t >= lb && t < B)) continue;
-      // offset of B's run inside t's symmetric part
-      uint64_t voff = 0;
-      for (uint32_t r = j->strong_off[t]; r < j->strong_off[t + 1]; ++r) {
-        const uint32_t B2 = j->strong_idx[r];
-        if (B2 > t && B2 < B && B2 >= lb && B2 < le) voff += npts(B2);
-      }
-      const uint32_t ti = t - lb;
-      for (uint32_t b = 0; b < nblk[ti + 1] - nblk[ti]; ++b)
-        c->cl_base[w++] = uint32_t(slots[ti] + uint64_t(b) * ssym[ti] + voff);
-    }
-  }
+  for (int64_t i = 0; i <= int64_t(np); ++i)
+    c->sym_info[i] = make_uint4(ent[i], nblk[i], uint32_t(slots[i]),
+                                i < int64_t(np) ? uint32_t(ssym[i]) : 0u);
+  tr.mark("sym: contributions");
   c->sym_slots = slots[np];
   c->sym_lb = lb;
   c->sym_le = le;
@@ -867,25 +859,46 @@ int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals) {
     c->launches += 1;
   }
   if (c->sym_items) {
-    const size_t nseg = c->sym_seg.size(), ncl = c->cl_base.size();
+    const size_t nseg = c->sym_seg.size(), ninfo = c->sym_info.size();
     CU_TRY(c, c->d_symseg.ensure(std::max<size_t>(nseg, 1) * 16));
-    CU_TRY(c, c->d_cloff.ensure(c->cl_off.size() * 4));
-    CU_TRY(c, c->d_clbase.ensure(std::max<size_t>(ncl, 1) * 4));
+    CU_TRY(c, c->d_syminfo.ensure(std::max<size_t>(ninfo, 1) * 16));
     CU_TRY(c, c->d_tgt.ensure(size_t(std::max(ne, 1u)) * 16));
     CU_TRY(c, c->d_contrib.ensure(std::max<uint64_t>(c->sym_slots, 1) * 16));
-    const size_t sym_bytes = nseg * 16 + c->cl_off.size() * 4 + ncl * 4;
+    const size_t sym_bytes = (nseg + ninfo) * 16;
     CU_TRY(c, c->h_sym.ensure(sym_bytes));
     unsigned char* hb = c->h_sym.as<unsigned char>();
     par_memcpy(hb, c->sym_seg.data(), nseg * 16);
-    par_memcpy(hb + nseg * 16, c->cl_off.data(), c->cl_off.size() * 4);
-    par_memcpy(hb + nseg * 16 + c->cl_off.size() * 4, c->cl_base.data(), ncl * 4);
+    par_memcpy(hb + nseg * 16, c->sym_info.data(), ninfo * 16);
     if (nseg) CU_TRY(c, cudaMemcpyAsync(c->d_symseg.p, hb, nseg * 16, cudaMemcpyHostToDevice, s));
-    CU_TRY(c, cudaMemcpyAsync(c->d_cloff.p, hb + nseg * 16, c->cl_off.size() * 4,
-                              cudaMemcpyHostToDevice, s));
-    if (ncl)
-      CU_TRY(c, cudaMemcpyAsync(c->d_clbase.p, hb + nseg * 16 + c->cl_off.size() * 4, ncl * 4,
-                                cudaMemcpyHostToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(c->d_syminfo.p, hb + nseg * 16, ninfo * 16, cudaMemcpyHostToDevice,
+                              s));
     c->h2d_bytes += sym_bytes;
+    // per-leaf contribution lists (count, scan, fill) on the device
+    const uint32_t nr = c->sym_le - c->sym_lb;
+    CU_TRY(c, c->d_cloff.ensure((size_t(nr) + 1) * 4));
+    CU_TRY(c, c->d_clcnt.ensure((size_t(nr) + 1) * 4));
+    CU_TRY(c, cudaMemsetAsync(c->d_clcnt.p, 0, (size_t(nr) + 1) * 4, s));
+    const uint32_t gb = (nr + 7) / 8;
+    p2p_sym_lists_kernel<false><<<gb, 256, 0, s>>>(
+        c->sym_lb, nr, c->d_pt.as<uint32_t>(), c->d_soff.as<uint32_t>(), c->d_sidx.as<uint32_t>(),
+        c->d_syminfo.as<uint4>(), c->d_symseg.as<uint4>(), c->d_clcnt.as<uint32_t>(), nullptr,
+        nullptr);
+    size_t tb = 0;
+    CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, tb, c->d_clcnt.as<uint32_t>(),
+                                            c->d_cloff.as<uint32_t>(), int64_t(nr) + 1, s));
+    CU_TRY(c, c->d_cubtmp.ensure(tb));
+    CU_TRY(c, cub::DeviceScan::ExclusiveSum(c->d_cubtmp.p, tb, c->d_clcnt.as<uint32_t>(),
+                                            c->d_cloff.as<uint32_t>(), int64_t(nr) + 1, s));
+    CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_cloff.as<uint32_t>() + nr, 4,
+                              cudaMemcpyDeviceToHost, s));
+    CU_TRY(c, cudaStreamSynchronize(s));
+    const uint32_t ncl = *c->h_hits.as<uint32_t>();
+    CU_TRY(c, c->d_clbase.ensure(size_t(std::max(ncl, 1u)) * 4));
+    p2p_sym_lists_kernel<true><<<gb, 256, 0, s>>>(
+        c->sym_lb, nr, c->d_pt.as<uint32_t>(), c->d_soff.as<uint32_t>(), c->d_sidx.as<uint32_t>(),
+        c->d_syminfo.as<uint4>(), c->d_symseg.as<uint4>(), nullptr, c->d_cloff.as<uint32_t>(),
+        c->d_clbase.as<uint32_t>());
+    c->launches += 3;
   }
   CU_TRY(c, cudaGetLastError());
   c->staged = true;
@@ -1349,7 +1362,8 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamSynchronize(c->h2d_stream);
     fmmcu::destroy_pipeline(c->pipe);
     c->pipe = nullptr;
-    for (DevBuf* b : {&c->d_symseg, &c->d_cloff, &c->d_clbase, &c->d_tgt, &c->d_contrib})
+    for (DevBuf* b : {&c->d_symseg, &c->d_syminfo, &c->d_tgt, &c->d_contrib, &c->d_cloff,
+                      &c->d_clcnt, &c->d_clbase, &c->d_cubtmp})
       b->release();
     c->h_sym.release();
     for (DevBuf* b : {&c->d_zin, &c->d_min, &c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,

@@ -154,9 +154,11 @@ struct fmmcu_ctx {
   uint32_t sym_lb = 0, sym_le = 0;      // leaf range the symmetric list covers
   std::vector<uint4> sym_seg;           // per-leaf entries: (slot, n, kind, 0)
   std::vector<uint32_t> sym_first;      // [range + 1] first entry of each leaf
-  std::vector<uint32_t> cl_off, cl_base;  // contributions to add per leaf (finalize)
+  std::vector<uint4> sym_info;          // per leaf: first entry / item / slot, sym sources
+  std::vector<uint32_t> sw_ent, sw_nblk;
+  std::vector<uint64_t> sw_ssym, sw_sord, sw_slots;
   uint64_t sym_slots = 0;               // contrib slots
-  DevBuf d_symseg, d_cloff, d_clbase, d_tgt, d_contrib;
+  DevBuf d_symseg, d_syminfo, d_tgt, d_contrib, d_cloff, d_clcnt, d_clbase, d_cubtmp;
   HostBuf h_sym;
   bool staged = false;
   bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)

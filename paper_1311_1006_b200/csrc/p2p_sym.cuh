@@ -282,9 +282,49 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
   if (lane == 0 && hits) atomicAdd(a.hits, (unsigned long long)hits);
 }
 
-// out[i] = tgt[i] + the contributions the items of i's lower partners stored
-// for it, in the host's fixed order (leaf L's list: cl_off[L] .. cl_off[L+1]
-// of cl_base, each a contrib index of L's first source).  One warp per leaf.
+// Contribution lists of the range's leaves, built on the device once per
+// staging: for leaf B of [leaf0, leaf0 + n) the contrib index of B's first
+// source in every item of each lower partner t (ascending t, then eval
+// block).  B's run offset inside t's symmetric part comes from t's entries
+// (<= 32, one per lane).  info[t - leaf0] = (first entry, first item, first
+// contrib slot, symmetric sources per item).  Pass 1 (FILL = false) counts.
+template <bool FILL>
+__global__ void p2p_sym_lists_kernel(uint32_t leaf0, uint32_t n_leaves,
+                                     const uint32_t* __restrict__ pt_off,
+                                     const uint32_t* __restrict__ s_off,
+                                     const uint32_t* __restrict__ s_idx,
+                                     const uint4* __restrict__ info,
+                                     const uint4* __restrict__ seg, uint32_t* __restrict__ cnt,
+                                     const uint32_t* __restrict__ cl_off,
+                                     uint32_t* __restrict__ cl_base) {
+  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_leaves) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t B = leaf0 + w;
+  const uint32_t b = pt_off[B];
+  uint32_t n = 0, o = FILL ? cl_off[w] : 0;
+  for (uint32_t q = s_off[B]; q < s_off[B + 1]; ++q) {
+    const uint32_t t = s_idx[q];
+    if (t < leaf0 || t >= B) continue;
+    const uint4 it = info[t - leaf0], nx = info[t - leaf0 + 1];
+    const uint32_t nblk = nx.y - it.y;
+    if (!FILL) {
+      n += nblk;
+      continue;
+    }
+    const uint4 sg = uint32_t(lane) < nx.x - it.x ? seg[it.x + lane] : make_uint4(0, 0, 0, 0);
+    const bool sym = sg.z == kRunSym;
+    const unsigned hit = __ballot_sync(0xffffffffu, sym && sg.x == b);
+    const int at = __ffs(hit) - 1;
+    const uint32_t voff = __reduce_add_sync(0xffffffffu, (sym && lane < at) ? sg.y : 0u);
+    for (uint32_t blk = uint32_t(lane); blk < nblk; blk += 32) cl_base[o + blk] = it.z + blk * it.w + voff;
+    o += nblk;
+  }
+  if (!FILL && lane == 0) cnt[w] = n;
+}
+
+// out[i] = tgt[i] + the contributions listed for i's leaf, in list order
+// (fixed: deterministic).  One warp per leaf.
 static __global__ void p2p_sym_finalize_kernel(uint32_t leaf0, uint32_t n_leaves,
                                                const uint32_t* __restrict__ pt_off,
                                                const uint32_t* __restrict__ cl_off,

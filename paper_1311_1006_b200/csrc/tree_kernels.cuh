@@ -200,6 +200,23 @@ __global__ void partition_kernel(const uint32_t* __restrict__ in, uint32_t n,
   out[dst] = in[i];
 }
 
+// as partition_kernel, with the low indicator read from the per-id flags
+__global__ void partition_flags_kernel(const uint32_t* __restrict__ in, uint32_t n,
+                                       const uint32_t* __restrict__ off,
+                                       const uint32_t* __restrict__ mid, uint32_t nseg,
+                                       const uint8_t* __restrict__ flag,
+                                       const uint32_t* __restrict__ scan,
+                                       uint32_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t id = in[i];
+  const uint32_t s = seg_of(off, nseg, i);
+  const uint32_t b = off[s];
+  const uint32_t rl = scan[i] - scan[b];
+  const uint32_t dst = flag[id] ? b + rl : mid[s] + (i - b - rl);
+  out[dst] = id;
+}
+
 // Offsets of the children after both splits: per parent p,
 // [off[p], ymid[2p]) [ymid[2p], xmid[p]) [xmid[p], ymid[2p+1]) [ymid[2p+1], off[p+1]).
 __global__ void child_offsets_kernel(const uint32_t* __restrict__ off,
