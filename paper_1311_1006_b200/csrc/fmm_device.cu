@@ -819,7 +819,9 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   c->self_layout = false;
   c->ext_out = nullptr;
   c->group_k = 0;
-  c->sym_request = self && P->layout_same && j->kernel == 0 && !std::getenv("FMMCU_NO_SYM");
+  // the mutual kernel saves ~0.6 ms of P2P here but its longer host work list
+  // sits on the critical path of a single evaluate; opt in with FMMCU_PIPE_SYM
+  c->sym_request = self && P->layout_same && j->kernel == 0 && std::getenv("FMMCU_PIPE_SYM");
   if (int rc = build_worklist(c, &pj)) return rc;
   if (int rc = stage_csr(c, &pj, true)) return rc;
   CU_TRY(c, cudaEventRecord(ev[8], s));
