@@ -33,7 +33,18 @@ void resize_huge(std::vector<cplx>& v, std::size_t n) {
     const auto b = reinterpret_cast<std::uintptr_t>(v.data());
     const std::uintptr_t a0 = (b + kHuge - 1) & ~(kHuge - 1);
     const std::uintptr_t a1 = (b + bytes) & ~(kHuge - 1);
-    if (a1 > a0) madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
+    if (a1 > a0) {
+      madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
+#ifdef MADV_POPULATE_WRITE
+      // fault the pages in from all cores (the value-initialising memset
+      // below then runs over populated memory)
+      const std::int64_t pages = std::int64_t((a1 - a0) / kHuge);
+#pragma omp parallel for schedule(static)
+      for (std::int64_t p = 0; p < pages; ++p)
+        madvise(reinterpret_cast<void*>(a0 + std::uintptr_t(p) * kHuge), kHuge,
+                MADV_POPULATE_WRITE);
+#endif
+    }
   }
   v.resize(n);
 }
