@@ -35,13 +35,8 @@ using namespace fmmcu;
 
 namespace {
 
-// Fast-kernel shape variants (threads x evals/thread, source records per
-// shared tile, source-loop unroll); the default is chosen from measurements
-// (profiles/), FMMCU_P2P_VARIANT overrides it for experiments:
-//   (threads x evals, tile, unroll, min CTAs/SM -> register cap)
-//   0 = 256x2 t512 u4 m4   1 = 256x2 t512 u4 m3   2 = 256x2 t512 u2 m4
-//   3 = 256x2 t512 u3 m4   4 = 128x4 t512 u2 m4   5 = 256x2 t512 u4 m2
-constexpr int kMaxEvalsPerItem = 64;  // eval records per item (staged with the first tile)
+// Warp-kernel shape variant (see launch_warp_e); FMMCU_P2P_VARIANT overrides
+// the measured default for experiments.
 int variant_index() {
   static int v = [] {
     const char* s = std::getenv("FMMCU_P2P_VARIANT");
@@ -51,23 +46,10 @@ int variant_index() {
   return v;
 }
 
-// FMMCU_P2P_KERNEL=tile selects the CTA-tile kernel; default: warp pipelines.
-bool use_warp_kernel() {
-  static bool w = [] {
-    const char* s = std::getenv("FMMCU_P2P_KERNEL");
-    return !(s && std::string(s) == "tile");
-  }();
-  return w;
-}
-
 constexpr size_t warp_smem(int warps, int chunk, int e) {
   return size_t(warps) * warp_region_bytes(chunk, e);
 }
 
-constexpr size_t tile_smem(int threads, int e, int tile) {
-  return 128 + size_t(2 * tile) * 32 + size_t(2 * kMaxEvalsPerItem) * 32 +
-         size_t(2 * threads) * e * 16;
-}
 
 }  // namespace
 
@@ -125,35 +107,6 @@ P2PArgs make_args(fmmcu_ctx* c) {
   return a;
 }
 
-template <int KN, int SM, int T, int E, int TILE, int U, bool PROD, int MINB>
-void launch_tile_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
-  auto kfn = p2p_tile_kernel<KN, SM, E, T, TILE, kMaxEvalsPerItem, U, PROD, MINB>;
-  constexpr size_t smem = tile_smem(T, E, TILE);
-  static int grid_cap = [&] {
-    cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, T, smem);
-    return std::max(1, sms * std::max(1, per_sm));
-  }();
-  const uint32_t grid = std::min<uint32_t>(n_items, uint32_t(grid_cap));
-  kfn<<<grid, T, smem, s>>>(a);
-}
-
-template <int KN, int SM>
-void launch_tile(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
-  switch (variant_index()) {
-    case 1: launch_tile_v<KN, SM, 256, 2, 512, 4, false, 3>(a, n_items, s); break;
-    case 2: launch_tile_v<KN, SM, 256, 2, 512, 2, false, 4>(a, n_items, s); break;
-    case 3: launch_tile_v<KN, SM, 256, 2, 512, 3, false, 4>(a, n_items, s); break;
-    case 4: launch_tile_v<KN, SM, 128, 4, 512, 2, false, 4>(a, n_items, s); break;
-    case 5: launch_tile_v<KN, SM, 256, 2, 512, 4, false, 2>(a, n_items, s); break;
-    default: launch_tile_v<KN, SM, 256, 2, 512, 4, false, 4>(a, n_items, s); break;
-  }
-}
-
 template <int KN, int SM>
 void launch_exact(const P2PArgs& a, uint32_t lb, uint32_t le, uint32_t eb, uint32_t ee,
                   cudaStream_t s) {
@@ -207,26 +160,14 @@ void launch_warp(const P2PArgs& a, uint32_t n_items, cudaStream_t s, int E) {
 }
 
 void dispatch_tile(int kn, int sm, const P2PArgs& a, uint32_t n, cudaStream_t s, int E) {
-  if (use_warp_kernel()) {
-    if (kn == 0) {
-      if (sm == 0) launch_warp<0, 0>(a, n, s, E);
-      else if (sm == 1) launch_warp<0, 1>(a, n, s, E);
-      else launch_warp<0, 2>(a, n, s, E);
-    } else {
-      if (sm == 0) launch_warp<1, 0>(a, n, s, E);
-      else if (sm == 1) launch_warp<1, 1>(a, n, s, E);
-      else launch_warp<1, 2>(a, n, s, E);
-    }
-    return;
-  }
   if (kn == 0) {
-    if (sm == 0) launch_tile<0, 0>(a, n, s);
-    else if (sm == 1) launch_tile<0, 1>(a, n, s);
-    else launch_tile<0, 2>(a, n, s);
+    if (sm == 0) launch_warp<0, 0>(a, n, s, E);
+    else if (sm == 1) launch_warp<0, 1>(a, n, s, E);
+    else launch_warp<0, 2>(a, n, s, E);
   } else {
-    if (sm == 0) launch_tile<1, 0>(a, n, s);
-    else if (sm == 1) launch_tile<1, 1>(a, n, s);
-    else launch_tile<1, 2>(a, n, s);
+    if (sm == 0) launch_warp<1, 0>(a, n, s, E);
+    else if (sm == 1) launch_warp<1, 1>(a, n, s, E);
+    else launch_warp<1, 2>(a, n, s, E);
   }
 }
 
@@ -531,9 +472,9 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const uint64_t total = work[nl];
   tr.mark("wl: S + work prefix");
   const uint64_t budget = std::max<uint64_t>(1ull << 16, total / (148ull * 16ull));
-  const bool warp_kernel = use_warp_kernel();
+  const bool warp_kernel = true;
   c->warp_e = warp_kernel ? choose_warp_e(cost4, cost5) : 4;
-  const uint32_t max_ev = warp_kernel ? uint32_t(kWarpSlots * c->warp_e) : uint32_t(kMaxEvalsPerItem);
+  const uint32_t max_ev = uint32_t(kWarpSlots * c->warp_e);
   const uint32_t max_ent = warp_kernel ? uint32_t(kWarpMaxEntries) : 0xFFFFFFFFu;
   c->warp_items = warp_kernel;
   c->sym_items = false;

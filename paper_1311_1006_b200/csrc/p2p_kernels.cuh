@@ -4,22 +4,12 @@
 // (proj/src/backend.cpp:41-69) with the per-pair arithmetic of
 // kernel_term()/smoother_factor() (proj/src/expansion.cpp:78-92).
 //
-// Fast path (p2p_tile_kernel), FP64 CUDA-core pipe, no tensor cores:
-//   * persistent CTAs pull work items (a target leaf, or an eval block /
-//     strong-list chunk of a heavy leaf) from a global counter;
-//   * an item's source leaves are contiguous runs of packed 32-byte records
-//     {x, y, m_re, m_im}; warp 0 builds the run list of the next tile with
-//     one coalesced load + shuffle scan over the precomputed (begin, length)
-//     of each strong entry and issues one TMA bulk copy
-//     (cp.async.bulk + mbarrier complete_tx) per run into the other of two
-//     shared tiles -- the next tile streams in while this one is computed;
-//   * thread (g, k) owns E evals of eval-slot g and walks sources
-//     k, k+K, k+2K, ... of the tile (broadcast LDS.128); the K partials of
-//     an eval are reduced in fixed k order through shared memory, so results
-//     are deterministic;
-//   * per pair: 2 DADD, r^2 (DMUL+DFMA), 1/r^2 = MUFU.RCP64H seed + one
-//     cubic Newton step (3 DFMA), m*conj(d) (2 DMUL + 2 DFMA), 2 DFMA
-//     accumulate -- 13 FP64 instructions for 23 algorithmic flops.
+// Shared pieces of the fast paths (p2p_warp.cuh, p2p_sym.cuh): work items,
+// TMA bulk-copy / mbarrier helpers, the per-pair arithmetic (FP64 CUDA-core
+// pipe, no tensor cores: 2 DADD, r^2 (DMUL+DFMA), 1/r^2 = MUFU.RCP64H seed +
+// one cubic Newton step (3 DFMA), m*conj(d) (2 DMUL + 2 DFMA), 2 DFMA
+// accumulate -- 13 FP64 instructions for 23 algorithmic flops), eval records
+// and the fixed-order reduction of split heavy leaves.
 // Exact path (p2p_exact_kernel): one thread per eval, reference order,
 // libgcc __divdc3 restated with non-contracted __d*_rn intrinsics -- bitwise
 // equal to the reference for the harmonic kernel without smoother.
@@ -220,8 +210,6 @@ static __global__ void p2p_segments_kernel(const uint32_t* __restrict__ s_idx,
   }
 }
 
-constexpr int kMaxSeg = 128;  // source runs per tile
-
 // ------------------------------------------------------------ fast kernel --
 // Eval record as staged on the device: {x, y, self slot (bits), q_self (bits)}
 // where q_self is the global strong-entry index (position in strong_idx) of
@@ -262,281 +250,6 @@ static __global__ void p2p_self_evals_kernel(const double4* __restrict__ src, ui
     evy[i] = make_double2(s.x, s.y);
     eself[i] = i;
   }
-}
-
-// Dynamic smem: [2 mbarriers | pad to 128][src tile 0][src tile 1]
-//               [eval tile 0][eval tile 1][reduction 0][reduction 1]
-template <int KERNEL, int SMOOTH, int E, int THREADS, int TILE, int MAXEV, int U, bool PRODUCER,
-          int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) p2p_tile_kernel(const P2PArgs a) {
-  // PRODUCER: warp 0 only stages tiles; otherwise warp 0 stages and computes.
-  constexpr int TC = PRODUCER ? THREADS - 32 : THREADS;  // consumer threads
-  static_assert(TILE % 32 == 0 && MAXEV <= TC * E, "shape");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-  double4* tiles = reinterpret_cast<double4*>(smem_raw + 128);
-  double4* evt = tiles + 2 * TILE;
-  double2* red = reinterpret_cast<double2*>(evt + 2 * MAXEV);
-  // run r of a tile = strong entry q0 + r (runs are 1:1 with entries,
-  // empty leaves give empty runs)
-  __shared__ uint32_t seg_gbeg[2][kMaxSeg];
-  __shared__ uint32_t seg_tpos[2][kMaxSeg + 1];
-  __shared__ uint32_t meta_item[2], meta_nseg[2], meta_flags[2], meta_ev[2], meta_nt[2],
-      meta_poff[2], meta_q0[2];
-  __shared__ unsigned int s_hits;
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
-  constexpr unsigned FULL = 0xffffffffu;
-
-  // ---- producer state (warp 0, warp-uniform registers) ----------------------
-  uint32_t st_item = kNoSelf, st_ent = 0, st_off = 0, st_end = 0, st_left = 0;
-  uint32_t st_ev = 0, st_nt = 0, st_poff = kNoSelf;
-  // lane 0 of warp 0 claims the next item id one item ahead, so the atomic's
-  // latency is hidden behind a whole item of compute
-  uint32_t claim = 0;
-  if (tid == 0) claim = atomicAdd(a.next_item, 1u);
-
-  auto stage = [&](int b) {
-    uint32_t flags = 0;
-    if (st_left == 0) {  // current item exhausted: take the claimed one, claim another
-      const uint32_t nxt = __shfl_sync(FULL, claim, 0);
-      if (nxt >= a.n_items) {
-        if (lane == 0) meta_item[b] = kNoSelf;
-        return;
-      }
-      if (lane == 0) claim = atomicAdd(a.next_item, 1u);
-      const P2PItem it = a.items[nxt];
-      st_item = nxt;
-      st_ent = it.s_begin;
-      st_end = it.s_end;
-      st_off = 0;
-      st_left = it.n_src;
-      st_ev = it.ev_begin;
-      st_nt = it.nt;
-      st_poff = it.partial_off;
-      flags |= 1u;
-    }
-    const uint32_t q0 = st_ent;
-    uint32_t filled = 0, nseg = 0;
-    while (filled < TILE && st_ent < st_end && nseg + 32 <= kMaxSeg) {
-      const uint32_t q = st_ent + lane;
-      const bool valid = q < st_end;
-      const uint2 sg = valid ? a.seg[q] : make_uint2(0u, 0u);
-      uint32_t b0 = sg.x, n = sg.y;
-      if (lane == 0) {
-        b0 += st_off;
-        n -= st_off;
-      }
-      uint32_t incl = n;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const uint32_t excl = incl - n;
-      const uint32_t room = TILE - filled;
-      const bool in = valid && excl < room;  // a prefix of the lanes
-      const uint32_t take = in ? min(n, room - excl) : 0u;
-      if (in) {
-        seg_gbeg[b][nseg + lane] = b0;
-        seg_tpos[b][nseg + lane] = filled + excl;
-      }
-      const unsigned part = __ballot_sync(FULL, valid && take < n);
-      const uint32_t n_in = __popc(__ballot_sync(FULL, in));
-      const uint32_t total = __shfl_sync(FULL, incl, 31);
-      const uint32_t got = min(total, room);
-      if (part == 0) {
-        st_ent += min(32u, st_end - st_ent);
-        st_off = 0;
-      } else {
-        const int L = __ffs(part) - 1;
-        const uint32_t tL = __shfl_sync(FULL, take, L);
-        st_off = (L == 0 ? st_off : 0u) + tL;
-        st_ent += uint32_t(L);
-      }
-      filled += got;
-      nseg += n_in;
-      st_left -= got;
-    }
-    if (st_left == 0) flags |= 2u;
-    const uint32_t ev_bytes = (flags & 1u) ? st_nt * 32u : 0u;
-    if (lane == 0) {
-      seg_tpos[b][nseg] = filled;
-      meta_item[b] = st_item;
-      meta_nseg[b] = nseg;
-      meta_flags[b] = flags;
-      meta_ev[b] = st_ev;
-      meta_nt[b] = st_nt;
-      meta_poff[b] = st_poff;
-      meta_q0[b] = q0;
-      fence_proxy_async();
-      mbar_expect_tx(&bar[b], filled * 32u + ev_bytes);
-      if (ev_bytes) bulk_g2s(evt + b * MAXEV, a.evr + st_ev, ev_bytes, &bar[b]);
-    }
-    __syncwarp();
-    for (uint32_t s = lane; s < nseg; s += 32) {
-      const uint32_t t0 = seg_tpos[b][s];
-      const uint32_t t1 = seg_tpos[b][s + 1];
-      if (t1 > t0)
-        bulk_g2s(tiles + b * TILE + t0, a.src + seg_gbeg[b][s], (t1 - t0) * 32u, &bar[b]);
-    }
-  };
-
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    s_hits = 0;
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == 0) stage(0);
-  __syncthreads();
-
-  // ---- consumer state ---------------------------------------------------------
-  uint32_t parity[2] = {0u, 0u};
-  uint32_t nt = 0, G = 1, K = 1, g = 0, k = 0, ev0 = 0, poff = kNoSelf;
-  bool active = false;
-  double yx[E], yy[E], ar[E], ai[E];
-  uint32_t sg[E], sq[E];
-  unsigned int hits = 0;
-  // pending reduction of the previous item (deferred by one tile: no extra
-  // barrier), done by the highest warps (warp 0 also stages)
-  uint32_t r_nt = 0, r_G = 1, r_K = 1, r_ev0 = 0, r_poff = kNoSelf, r_buf = 0, items_done = 0;
-  bool r_pending = false;
-
-  const int ctid = PRODUCER ? tid - 32 : tid;  // consumer index (< 0: producer warp)
-  auto reduce_pending = [&]() {
-    const double2* rb = red + r_buf * (TC * E);
-    const int rt = THREADS - 1 - tid;  // highest threads first
-    for (uint32_t le = uint32_t(rt); le < r_nt; le += THREADS) {
-      const uint32_t gg = le / E, ee = le % E;
-      const double2* p = rb + ee * r_K * r_G + gg;
-      double sr = 0.0, si = 0.0;
-      for (uint32_t kk = 0; kk < r_K; ++kk, p += r_G) {
-        const double2 v = *p;
-        sr += v.x;
-        si += v.y;
-      }
-      const double2 res = (KERNEL == 0) ? make_double2(-sr, -si) : make_double2(sr, si);
-      if (r_poff == kNoSelf)
-        a.out[r_ev0 + le] = res;
-      else
-        a.partial[r_poff + le] = res;
-    }
-    r_pending = false;
-  };
-
-  for (uint32_t n = 0;; ++n) {
-    const int b = int(n & 1u);
-    const uint32_t item = meta_item[b];
-    if (item == kNoSelf) break;
-    const uint32_t flags = meta_flags[b];
-    const uint32_t nseg = meta_nseg[b];
-    const uint32_t q0 = meta_q0[b];
-    if (flags & 1u) {  // first tile of an item: thread roles (no integer division)
-      nt = meta_nt[b];
-      ev0 = meta_ev[b];
-      poff = meta_poff[b];
-      G = (nt + E - 1) / E;  // E is a power of two; host guarantees nt <= MAXEV <= E * TC
-      const float rG = 1.0f / float(G);
-      K = uint32_t(float(TC) * rG + 1e-4f);
-      k = uint32_t((float(ctid) + 0.5f) * rG);
-      g = uint32_t(ctid) - k * G;
-      active = ctid >= 0 && k < K;
-    }
-    if (warp == 0) stage(b ^ 1);  // next tile streams in while this one is computed
-    if (r_pending) reduce_pending();
-
-    mbar_wait(&bar[b], parity[b]);
-    parity[b] ^= 1u;
-    if (flags & 1u) {  // eval registers from the staged eval records
-      const double4* ev = evt + b * MAXEV;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const uint32_t le = g * E + e;
-        const bool ok = active && le < nt;
-        const double4 r = ok ? ev[le] : make_double4(0.0, 0.0, 0.0, 0.0);
-        yx[e] = r.x;
-        yy[e] = r.y;
-        sg[e] = ok ? uint32_t(__double_as_longlong(r.z)) : kNoSelf;
-        sq[e] = ok ? uint32_t(__double_as_longlong(r.w)) : kNoSelf;
-        ar[e] = 0.0;
-        ai[e] = 0.0;
-      }
-    }
-
-    // O(1) tile position of each eval's own source: its entry's run r = q - q0
-    const uint32_t ntile = seg_tpos[b][nseg];
-    uint32_t ps[E];
-    uint32_t plo = kNoSelf, phi = 0u;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      ps[e] = kNoSelf;
-      const uint32_t r = sq[e] - q0;
-      if (sq[e] != kNoSelf && r < nseg) {
-        const uint32_t d = sg[e] - seg_gbeg[b][r];
-        const uint32_t t0 = seg_tpos[b][r];
-        if (d < seg_tpos[b][r + 1] - t0) {
-          ps[e] = t0 + d;
-          plo = min(plo, ps[e]);
-          phi = max(phi, ps[e]);
-        }
-      }
-    }
-    // Self pairs of this warp sit at tile positions [plo, phi] (the target
-    // leaf's own run for self-evaluation): only that stretch pays for the
-    // per-pair exclusion test.
-    plo = __reduce_min_sync(FULL, plo);
-    phi = __reduce_max_sync(FULL, phi);
-
-    if (active) {
-      const double4* tile = tiles + b * TILE;
-      const double4* p = tile + k;
-      const double4* const end1 = tile + min(plo, ntile);
-      const double4* const end = tile + ntile;
-      p = run_unchecked<KERNEL, SMOOTH, E, U>(p, end1, K, yx, yy, a.inv_delta2, a.delta2, ar, ai);
-      if (plo != kNoSelf) {
-        const double4* const end2 = tile + min(phi + 1u, ntile);
-        for (; p < end2; p += K) {
-          const double4 s = *p;
-          const uint32_t j = uint32_t(p - tile);
-#pragma unroll
-          for (int e = 0; e < E; ++e)
-            pair_accum<KERNEL, SMOOTH>(yx[e], yy[e], s, a.inv_delta2, a.delta2, j != ps[e], ar[e],
-                                       ai[e]);
-        }
-        run_unchecked<KERNEL, SMOOTH, E, U>(p, end, K, yx, yy, a.inv_delta2, a.delta2, ar, ai);
-        // each skipped self pair is seen by exactly one source lane
-#pragma unroll
-        for (int e = 0; e < E; ++e) hits += (ps[e] != kNoSelf && ps[e] % K == k) ? 1u : 0u;
-      }
-    }
-
-    if (flags & 2u) {  // last tile of the item: park the K partials, reduce next tile
-      const uint32_t rb = items_done & 1u;
-      if (active) {
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-          red[rb * (TC * E) + (e * K + k) * G + g] = make_double2(ar[e], ai[e]);
-      }
-      r_pending = true;
-      r_nt = nt;
-      r_G = G;
-      r_K = K;
-      r_ev0 = ev0;
-      r_poff = poff;
-      r_buf = rb;
-      ++items_done;
-    }
-    __syncthreads();  // tile b free, partials visible, meta[b^1] visible
-  }
-  if (r_pending) reduce_pending();
-  for (int o = 16; o > 0; o >>= 1) hits += __shfl_down_sync(FULL, hits, o);
-  if (lane == 0 && hits) atomicAdd(&s_hits, hits);
-  __syncthreads();
-  if (tid == 0 && s_hits) atomicAdd(a.hits, (unsigned long long)s_hits);
 }
 
 // Sum the chunk partials of split eval blocks in chunk order (deterministic).

@@ -1,8 +1,8 @@
 // fmm-b200 — warp-pipelined P2P kernel (fast FP64 path) for sm_100a.
 //
-// Same arithmetic and semantics as p2p_tile_kernel (near_box(),
-// proj/src/backend.cpp:41-69), different decomposition: every warp is an
-// independent pipeline with no CTA-level synchronisation at all.
+// FP64 restatement of near_box() (proj/src/backend.cpp:41-69) with the
+// per-pair arithmetic of p2p_kernels.cuh.  Every warp is an independent
+// pipeline with no CTA-level synchronisation at all.
 //   * a warp claims work items (<= 8E evals of one target leaf x <= 32
 //     strong-list entries) from a global counter;
 //   * lane q holds the source run (first slot, length) of strong entry q and
