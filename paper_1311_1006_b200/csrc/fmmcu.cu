@@ -932,14 +932,46 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     CU_TRY(c, c->d_zin.ensure(size_t(ns) * 16));
     CU_TRY(c, c->d_min.ensure(size_t(ns) * 16));
   }
-  // The work list (~1 ms on all cores at 10M) is built on this thread, before
-  // any chunk moves: on a helper thread it starves behind the OpenMP packing
-  // team, and with the DMA already running it slows down and the CSR upload
-  // queues behind the chunks (measured: 13.2 vs 10.7 ms per 10M step).
+  // Halo-only upload for a leaf range: only the sources of the range's
+  // strong lists (its own leaves + a halo) are read by its kernels; the rest
+  // of the device array is left untouched.
+  const bool partial = lb > 0 || le < nl;
+  std::vector<uint8_t> needed;
+  if (partial) {
+    needed.assign(nl, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t t = lb; t < int64_t(le); ++t)
+      for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q)
+        needed[j->strong_idx[q]] = 1;
+    h2d -= uint64_t(ns) * 32;
+  }
+  // visit the source runs of chunk k that the range reads
+  auto for_runs = [&](int k, auto&& fn) -> int {
+    const uint32_t l0 = c->chunk_leaf[k], l1 = c->chunk_leaf[k + 1];
+    if (!partial) return fn(int64_t(j->pt_off[l0]), int64_t(j->pt_off[l1]));
+    for (uint32_t t = l0; t < l1;) {
+      if (!needed[t]) {
+        ++t;
+        continue;
+      }
+      uint32_t t1 = t + 1;
+      while (t1 < l1 && needed[t1]) ++t1;
+      if (int rc = fn(int64_t(j->pt_off[t]), int64_t(j->pt_off[t1]))) return rc;
+      t = t1;
+    }
+    return FMMCU_OK;
+  };
+  // The work list (~1 ms at 10M) is built first, on this thread, and goes up
+  // with the CSR before any chunk moves.  Measured alternatives, both slower
+  // at 10M: a helper thread (starves behind the OpenMP packing team), and the
+  // CSR + all chunk DMAs first with the work list built meanwhile and read by
+  // the kernels from mapped memory (10.3 vs 10.2 ms per step).
   if (int rc = build_worklist(c, j)) return rc;
   tr.mark("worklist");
   if (int rc = stage_csr(c, j, false)) return rc;
   h2d += c->h2d_bytes - uint64_t(ns) * 32 - (c->self_layout ? 0 : uint64_t(ne) * 20);
+  const P2PItem* items_dev = c->d_items.as<P2PItem>();
+  const P2PFinal* fins_dev = c->d_fin.as<P2PFinal>();
   tr.mark("csr");
   double2* hy = c->h_evy.as<double2>();
   uint32_t* hself = c->h_eself.as<uint32_t>();
@@ -1020,14 +1052,14 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     if (i1 > i0) {
       CU_TRY(c, cudaMemsetAsync(c->d_counter.p, 0, 8, s));
       P2PArgs aa = a;
-      aa.items = c->d_items.as<P2PItem>() + i0;
+      aa.items = items_dev + i0;
       aa.n_items = i1 - i0;
       dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s, c->warp_e);
       ++nk;
     }
     const uint32_t f0 = c->fin_first[p0], f1 = c->fin_first[p1];
     if (f1 > f0) {
-      p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(c->d_fin.as<P2PFinal>() + f0, f1 - f0,
+      p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(fins_dev + f0, f1 - f0,
                                                    c->d_partial.as<double2>(), c->out_dev);
       ++nk;
     }
@@ -1036,19 +1068,6 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     return FMMCU_OK;
   };
 
-  // Halo-only upload for a leaf range: only the sources of the range's
-  // strong lists (its own leaves + a halo) are read by its kernels; the rest
-  // of the device array is left untouched.
-  const bool partial = lb > 0 || le < nl;
-  std::vector<uint8_t> needed;
-  if (partial) {
-    needed.assign(nl, 0);
-#pragma omp parallel for schedule(static)
-    for (int64_t t = lb; t < int64_t(le); ++t)
-      for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q)
-        needed[j->strong_idx[q]] = 1;
-    h2d -= uint64_t(ns) * 32;
-  }
   // pack / DMA source slots [c0, c1) and self-check them; returns the check
   auto upload = [&](int64_t c0, int64_t c1, int k) -> int {
     bool same = maybe_self;
@@ -1090,22 +1109,8 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   };
 
   for (int k = 0; k < K; ++k) {
-    const uint32_t l0 = c->chunk_leaf[k], l1 = c->chunk_leaf[k + 1];
     chunk_self[k] = maybe_self ? 1 : 0;
-    if (!partial) {
-      if (int rc = upload(j->pt_off[l0], j->pt_off[l1], k)) return rc;
-    } else {
-      for (uint32_t t = l0; t < l1;) {  // runs of needed leaves
-        if (!needed[t]) {
-          ++t;
-          continue;
-        }
-        uint32_t t1 = t + 1;
-        while (t1 < l1 && needed[t1]) ++t1;
-        if (int rc = upload(j->pt_off[t], j->pt_off[t1], k)) return rc;
-        t = t1;
-      }
-    }
+    if (int rc = for_runs(k, [&](int64_t c0, int64_t c1) { return upload(c0, c1, k); })) return rc;
     CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
     const bool same = chunk_self[k] != 0;
     all_self = all_self && same;
