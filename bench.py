@@ -346,7 +346,7 @@ def run_ours(args):
         # e2e contract's "pinned host memory": every step still moves the
         # sources H2D (DMA straight from these arrays) and the potentials D2H
         # (written by the kernels straight into host_out).
-        pinned = [host_out, wl["zp"], wl["mp"]]
+        pinned = [host_out, wl["zp"], wl["mp"], wl["pt"], wl["ev"], wl["so"], wl["si"]]
         for a in pinned:
             ctx.host_register(a)
         N.p2p(ctx, wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"], wl["zp"], wl["mp"], wl["yp"],

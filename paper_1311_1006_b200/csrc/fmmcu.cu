@@ -752,36 +752,41 @@ int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals) {
   CU_TRY(c, c->d_seg.ensure(size_t(nnz) * 8));
   CU_TRY(c, c->d_evr.ensure(size_t(ne) * 32));
   CU_TRY(c, c->h_hits.ensure(8));
-  // CSR + work list through one pinned block
-  const size_t csr_bytes = size_t(nl + 1) * 12 + size_t(nnz) * 4 +
-                           c->items.size() * sizeof(P2PItem) + c->fins.size() * sizeof(P2PFinal);
+  // CSR through one pinned block, unless the caller's arrays are page-locked
+  // (then DMA'd in place); the work list is already in pinned vectors
+  auto locked = [](const void* p) {
+    cudaPointerAttributes at{};
+    const bool ok = p && cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+                    at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  const size_t ib = c->items.size() * sizeof(P2PItem), fb = c->fins.size() * sizeof(P2PFinal);
+  const size_t csr_bytes = size_t(nl + 1) * 12 + size_t(nnz) * 4;
   CU_TRY(c, c->h_csr.ensure(csr_bytes));
   unsigned char* hc = c->h_csr.as<unsigned char>();
   size_t o = 0;
-  auto put = [&](const void* src, size_t bytes) {
-    if (bytes) par_memcpy(hc + o, src, bytes);
-    const size_t at = o;
+  auto put = [&](const void* src, size_t bytes) -> const void* {
+    if (!bytes) return src;
+    if (locked(src)) return src;
+    par_memcpy(hc + o, src, bytes);
+    const void* at = hc + o;
     o += bytes;
     return at;
   };
-  const size_t o_pt = put(j->pt_off, size_t(nl + 1) * 4);
-  const size_t o_ev = put(j->ev_off, size_t(nl + 1) * 4);
-  const size_t o_so = put(j->strong_off, size_t(nl + 1) * 4);
-  const size_t o_si = put(j->strong_idx, size_t(nnz) * 4);
-  const size_t o_it = put(c->items.data(), c->items.size() * sizeof(P2PItem));
-  const size_t o_fi = put(c->fins.data(), c->fins.size() * sizeof(P2PFinal));
-  c->h2d_bytes = uint64_t(c->n_src) * 32 + (self_layout ? 0 : uint64_t(ne) * 20) + o;
+  const void* s_pt = put(j->pt_off, size_t(nl + 1) * 4);
+  const void* s_ev = put(j->ev_off, size_t(nl + 1) * 4);
+  const void* s_so = put(j->strong_off, size_t(nl + 1) * 4);
+  const void* s_si = put(j->strong_idx, size_t(nnz) * 4);
+  c->h2d_bytes = uint64_t(c->n_src) * 32 + (self_layout ? 0 : uint64_t(ne) * 20) + csr_bytes +
+                 ib + fb;
 
-  CU_TRY(c, cudaMemcpyAsync(c->d_pt.p, hc + o_pt, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
-  CU_TRY(c, cudaMemcpyAsync(c->d_ev.p, hc + o_ev, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
-  CU_TRY(c, cudaMemcpyAsync(c->d_soff.p, hc + o_so, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
-  if (nnz) CU_TRY(c, cudaMemcpyAsync(c->d_sidx.p, hc + o_si, size_t(nnz) * 4, cudaMemcpyHostToDevice, s));
-  if (!c->items.empty())
-    CU_TRY(c, cudaMemcpyAsync(c->d_items.p, hc + o_it, c->items.size() * sizeof(P2PItem),
-                              cudaMemcpyHostToDevice, s));
-  if (!c->fins.empty())
-    CU_TRY(c, cudaMemcpyAsync(c->d_fin.p, hc + o_fi, c->fins.size() * sizeof(P2PFinal),
-                              cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaMemcpyAsync(c->d_pt.p, s_pt, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaMemcpyAsync(c->d_ev.p, s_ev, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
+  CU_TRY(c, cudaMemcpyAsync(c->d_soff.p, s_so, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
+  if (nnz) CU_TRY(c, cudaMemcpyAsync(c->d_sidx.p, s_si, size_t(nnz) * 4, cudaMemcpyHostToDevice, s));
+  if (ib) CU_TRY(c, cudaMemcpyAsync(c->d_items.p, c->items.data(), ib, cudaMemcpyHostToDevice, s));
+  if (fb) CU_TRY(c, cudaMemcpyAsync(c->d_fin.p, c->fins.data(), fb, cudaMemcpyHostToDevice, s));
   if (nnz) {
     p2p_segments_kernel<<<(nnz + 255) / 256, 256, 0, s>>>(c->d_sidx.as<uint32_t>(),
                                                           c->d_pt.as<uint32_t>(), nnz,
@@ -961,11 +966,27 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     }
     return FMMCU_OK;
   };
-  // The work list (~1 ms at 10M) is built first, on this thread, and goes up
-  // with the CSR before any chunk moves.  Measured alternatives, both slower
-  // at 10M: a helper thread (starves behind the OpenMP packing team), and the
-  // CSR + all chunk DMAs first with the work list built meanwhile and read by
-  // the kernels from mapped memory (10.3 vs 10.2 ms per step).
+  // Page-locked inputs: the first kPre chunks start moving before the work
+  // list is built (~1.5 ms at 10M, about two chunks of DMA), so the copy
+  // engine never idles; the CSR and work list then queue behind only those.
+  // Measured alternatives: the work list on a helper thread starves behind
+  // the OpenMP team; all chunks first makes the work list upload wait for
+  // the whole 320 MB (13.2 vs 10.4 ms per 10M step).
+  constexpr int kPre = 2;
+  const int pre = direct_in ? std::min(K, kPre) : 0;
+  auto dma = [&](int64_t c0, int64_t c1) -> int {
+    if (c1 <= c0) return FMMCU_OK;
+    CU_TRY(c, cudaMemcpyAsync(c->d_zin.as<double>() + 2 * c0, z + 2 * c0, size_t(c1 - c0) * 16,
+                              cudaMemcpyHostToDevice, h));
+    CU_TRY(c, cudaMemcpyAsync(c->d_min.as<double>() + 2 * c0, m + 2 * c0, size_t(c1 - c0) * 16,
+                              cudaMemcpyHostToDevice, h));
+    if (partial) h2d += uint64_t(c1 - c0) * 32;
+    return FMMCU_OK;
+  };
+  for (int k = 0; k < pre; ++k) {
+    if (int rc = for_runs(k, dma)) return rc;
+    CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+  }
   if (int rc = build_worklist(c, j)) return rc;
   tr.mark("worklist");
   if (int rc = stage_csr(c, j, false)) return rc;
@@ -1072,12 +1093,8 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   auto upload = [&](int64_t c0, int64_t c1, int k) -> int {
     bool same = maybe_self;
     if (direct_in) {
-      if (c1 > c0) {
-        CU_TRY(c, cudaMemcpyAsync(c->d_zin.as<double>() + 2 * c0, z + 2 * c0,
-                                  size_t(c1 - c0) * 16, cudaMemcpyHostToDevice, h));
-        CU_TRY(c, cudaMemcpyAsync(c->d_min.as<double>() + 2 * c0, m + 2 * c0,
-                                  size_t(c1 - c0) * 16, cudaMemcpyHostToDevice, h));
-      }
+      if (k >= pre)
+        if (int rc = dma(c0, c1)) return rc;
       if (maybe_self) {
 #pragma omp parallel for schedule(static) reduction(&& : same)
         for (int64_t i = c0; i < c1; ++i)
@@ -1099,7 +1116,7 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
         CU_TRY(c, cudaMemcpyAsync(c->d_src.as<double>() + 4 * c0, hs + 4 * c0,
                                   size_t(c1 - c0) * 32, cudaMemcpyHostToDevice, h));
     }
-    if (partial) h2d += uint64_t(c1 - c0) * 32;
+    if (partial && !direct_in) h2d += uint64_t(c1 - c0) * 32;
     if (maybe_self && !same && c1 > c0) {
       if (int rc = host_evals(c0, c1)) return rc;
       h2d += uint64_t(c1 - c0) * 20;
@@ -1111,7 +1128,7 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   for (int k = 0; k < K; ++k) {
     chunk_self[k] = maybe_self ? 1 : 0;
     if (int rc = for_runs(k, [&](int64_t c0, int64_t c1) { return upload(c0, c1, k); })) return rc;
-    CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+    if (k >= pre) CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
     const bool same = chunk_self[k] != 0;
     all_self = all_self && same;
     if (c->trace)

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -70,6 +71,28 @@ struct HostBuf {
     return static_cast<T*>(p);
   }
 };
+
+// std::allocator replacement backed by pinned host memory: a vector built
+// with it can be DMA'd without a staging copy.
+template <class T>
+struct PinnedAllocator {
+  using value_type = T;
+  PinnedAllocator() = default;
+  template <class U>
+  PinnedAllocator(const PinnedAllocator<U>&) {}
+  T* allocate(std::size_t n) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable) != cudaSuccess) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, std::size_t) { cudaFreeHost(p); }
+  template <class U>
+  bool operator==(const PinnedAllocator<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAllocator<U>&) const { return false; }
+};
+template <class T>
+using pinned_vector = std::vector<T, PinnedAllocator<T>>;
 
 using Clock = std::chrono::steady_clock;
 
@@ -141,9 +164,9 @@ struct fmmcu_ctx {
   double delta = 0.0;
   std::vector<uint32_t> ev_off;        // host copy
   std::vector<uint64_t> leaf_work;     // prefix of nt * S
-  std::vector<P2PItem> items;
+  fmmcu::pinned_vector<P2PItem> items;   // pinned: uploaded without a staging copy
   std::vector<uint32_t> item_first;    // [n_leaves + 1]
-  std::vector<P2PFinal> fins;
+  fmmcu::pinned_vector<P2PFinal> fins;
   std::vector<uint32_t> fin_first;     // [n_leaves + 1]
   // work-list scratch kept across launches (no reallocation / page faults)
   std::vector<uint64_t> wl_S, wl_pev;
