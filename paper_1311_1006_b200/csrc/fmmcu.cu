@@ -967,12 +967,12 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     return FMMCU_OK;
   };
   // Page-locked inputs: the first kPre chunks start moving before the work
-  // list is built (~1.5 ms at 10M, about two chunks of DMA), so the copy
+  // list is built (~1.5 ms at 10M, two to three chunks of DMA), so the copy
   // engine never idles; the CSR and work list then queue behind only those.
   // Measured alternatives: the work list on a helper thread starves behind
   // the OpenMP team; all chunks first makes the work list upload wait for
   // the whole 320 MB (13.2 vs 10.4 ms per 10M step).
-  constexpr int kPre = 2;
+  constexpr int kPre = 3;
   const int pre = direct_in ? std::min(K, kPre) : 0;
   auto dma = [&](int64_t c0, int64_t c1) -> int {
     if (c1 <= c0) return FMMCU_OK;
