@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--n", "--points", dest="n", type=int, default=10_000_000)
     ap.add_argument("--levels", type=int, default=10)
     ap.add_argument("--theta", type=float, default=0.5)
     ap.add_argument("--seed", type=int, default=4)
@@ -242,10 +242,19 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
+    # FMM_BENCH_SHARED_GPU=1: test mode for the multi-rank path on a one-GPU
+    # box -- every rank on cuda:0, gloo collectives (staged through the host).
+    # Not a measurement mode.
+    shared = os.environ.get("FMM_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(local)
     from paper_1311_1006_b200 import _native as N
@@ -278,7 +287,7 @@ def run_ours(args):
     full = torch.zeros(2 * n_eval, dtype=torch.float64, device=f"cuda:{local}")
     torch.cuda.synchronize()
     ctx.bind_device_out(full.data_ptr())
-    gather = PotentialGather(slices, rank, full) if world > 1 else None
+    gather = PotentialGather(slices, rank, full, via_host=shared) if world > 1 else None
     fp64_peak = ctx.fp64_peak()
     symmetric, evals_per_lane = ctx.kernel_info()
 
@@ -286,17 +295,19 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
 
+    red_dev = "cpu" if shared else full.device
+
     def allmax(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=full.device)
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return t.item()
 
     def allsum(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=full.device)
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         torch.distributed.all_reduce(t)
         return t.item()
 
@@ -336,7 +347,25 @@ def run_ours(args):
     value = total_pairs / (ms * 1e-3)
     achieved = FLOPS_PER_PAIR * my_pairs / (kernel_ms * 1e-3) / 1e12
 
-    # parity of the gathered result on a few leaves (cheap; the tests do it fully)
+    gather_check = None
+    if world > 1:
+        # The gathered potentials must match one rank evaluating every leaf
+        # (the mutual kernel sums shard-boundary pairs in a different order,
+        # so compare to 1e-12 relative, not bitwise).
+        if rank == 0:
+            ref = torch.zeros_like(full)
+            jf, kf = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
+                                            wl["zp"], wl["mp"], wl["yp"], wl["sid"], None)
+            ctx.stage(jf, kf)
+            ctx.bind_device_out(ref.data_ptr())
+            ctx.run_staged(0, wl["n_leaves"])
+            torch.cuda.synchronize()
+            err = ((full - ref).abs().max() / ref.abs().max().clamp_min(1e-300)).item()
+            gather_check = {"max_rel_err": err, "ok": bool(err < 1e-12)}
+            if not gather_check["ok"]:
+                print(f"gathered potentials differ from the 1-rank result: {err:g}", file=sys.stderr)
+        barrier()
+
     # ---- e2e: reference-facing C ABI with host buffers (pack+H2D+kernel+D2H) ----
     e2e = None
     if not args.no_e2e:
@@ -476,7 +505,9 @@ def run_ours(args):
             "metric": "p2p_pairs_per_sec", "value": value, "unit": "pairs/s", "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args, world, {"pairs_per_step": int(total_pairs)}),
+            "config": config_block(args, world, {"pairs_per_step": int(total_pairs)}
+                                   | ({"parallelism": f"target-leaf shards x{world} sharing "
+                                       "cuda:0, gloo all-gather via host"} if shared else {})),
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
                          "peak_source": "measured DFMA micro-benchmark on this GPU in this run "
@@ -504,6 +535,11 @@ def run_ours(args):
             "host": cpu_desc(),
             "setup_s": {"generate": round(wl["gen_s"], 3), "tree": round(wl["tree_s"], 3)},
         }
+        if gather_check is not None:
+            line["gather_check"] = gather_check
+        if shared:
+            line["test_mode"] = ("FMM_BENCH_SHARED_GPU=1: all ranks on cuda:0 with gloo "
+                                 "collectives -- a logic check, not a measurement")
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -44,7 +44,7 @@ class PotentialGather:
     pad buffers are allocated once so the gather is allocation-free inside a
     timed loop."""
 
-    def __init__(self, slices, rank: int, full, group=None):
+    def __init__(self, slices, rank: int, full, group=None, via_host: bool = False):
         import torch
 
         self.slices = slices
@@ -53,8 +53,10 @@ class PotentialGather:
         self.full = full
         self.group = group
         self.maxlen = max(1, max(e1 - e0 for e0, e1 in slices)) * 2
-        self.send = torch.zeros(self.maxlen, dtype=full.dtype, device=full.device)
-        self.recv = torch.zeros(self.maxlen * self.world, dtype=full.dtype, device=full.device)
+        # via_host: gloo test mode (several ranks sharing one GPU)
+        dev = "cpu" if via_host else full.device
+        self.send = torch.zeros(self.maxlen, dtype=full.dtype, device=dev)
+        self.recv = torch.zeros(self.maxlen * self.world, dtype=full.dtype, device=dev)
 
     def bytes_moved(self) -> int:
         return int(self.recv.numel() * self.recv.element_size())
@@ -71,5 +73,6 @@ class PotentialGather:
             if r == self.rank or b == a:
                 continue
             m = (b - a) * 2
-            self.full[2 * a: 2 * b].copy_(self.recv[r * self.maxlen: r * self.maxlen + m])
+            self.full[2 * a: 2 * b].copy_(self.recv[r * self.maxlen: r * self.maxlen + m],
+                                          non_blocking=False)
         return self.full
