@@ -167,10 +167,13 @@ typedef struct {
   int smoother;              /* FMMCU_SMOOTH_* (near field only, as the reference) */
   double delta;
   double *out;               /* [2 n_eval] potentials, original eval order */
-  /* optional: called on the launching thread once the inputs have been read
-   * (staged for upload); the host is then idle until the potentials land, so
-   * the caller can prepare its result buffer without competing for memory
-   * bandwidth with the staging copies */
+  /* optional: called once every input has been read (staged for upload, or
+   * handed to the DMA engines when page-locked), before fmmcu_fmm_launch
+   * returns -- on the launching thread, or on the helper thread that stages
+   * the masses while the pyramid builds.  From then on the host only drives
+   * the device, so the caller can prepare its result buffer without
+   * competing for memory bandwidth with the staging copies.  The input arrays
+   * must stay unchanged until fmmcu_fmm_launch returns. */
   void (*inputs_consumed)(void *arg);
   void *inputs_consumed_arg;
 } fmmcu_fmm_job;

@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <thread>
 
 #include "far_kernels.cuh"
 #include "fmmcu_internal.cuh"
@@ -56,18 +57,24 @@ struct DevicePipeline {
   bool layout_same = false;
   bool tree_valid = false;
   cudaStream_t far = nullptr;
-  cudaEvent_t ev[12] = {};
+  cudaEvent_t ev[14] = {};
+  fmmcu::pinned_vector<uint32_t> h_pt, h_evo, h_so, h_si;  // finest CSR for the work list
   static constexpr int kChunksMax = 64;
   cudaEvent_t ev_res[kChunksMax] = {};
   uint32_t chunk_off[kChunksMax + 1] = {};
   int n_chunks = 0;
   bool pending = false;
+  bool direct_res = false;      // D2H straight into the caller's page-locked out
+  double2* res_host = nullptr;  // where the D2H lands (out, or the hres staging)
   Clock::time_point t_host0{};
   uint64_t h2d = 0;
+  std::thread m_stager;         // stages the masses while the pyramid builds
+  cudaError_t m_err = cudaSuccess;
 };
 
 void destroy_pipeline(DevicePipeline* p) {
   if (!p) return;
+  if (p->m_stager.joinable()) p->m_stager.join();
   if (p->far) cudaStreamDestroy(p->far);
   for (cudaEvent_t e : p->ev)
     if (e) cudaEventDestroy(e);
@@ -674,6 +681,7 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
       CU_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
   }
   DevicePipeline* P = c->pipe;
+  if (P->m_stager.joinable()) P->m_stager.join();  // left over by an error return
   const uint32_t N = j->n_src, M = j->n_eval;
   P->N = N;
   P->M = M;
@@ -685,37 +693,46 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   cudaEvent_t* ev = P->ev;
   CU_TRY(c, cudaEventRecord(ev[0], s));
 
-  // ---- H2D through pinned chunks; finiteness + self-evaluation detection --
+  // ---- H2D ------------------------------------------------------------------
+  // Positions first: the pyramid needs only z (and y, sid).  The masses follow
+  // on the h2d stream behind them while the pyramid builds -- DMA'd in place
+  // when the caller's arrays are page-locked, else staged through pinned
+  // chunks by a helper thread.  The host checks finiteness and detects
+  // self-evaluation while the position chunks are in flight.
   CU_TRY(c, P->z.ensure(uint64_t(N) * 16));
   CU_TRY(c, P->m.ensure(uint64_t(N) * 16));
-  CU_TRY(c, P->hz.ensure(uint64_t(N) * 16));
-  CU_TRY(c, P->hm.ensure(uint64_t(N) * 16));
+  const bool z_locked = host_locked(j->src_z, uint64_t(N) * 16);
+  const bool m_locked = host_locked(j->src_m, uint64_t(N) * 16);
+  if (!z_locked) CU_TRY(c, P->hz.ensure(uint64_t(N) * 16));
+  if (!m_locked) CU_TRY(c, P->hm.ensure(uint64_t(N) * 16));
   const bool maybe_self = j->eval_sid && M == N;
+  const bool y_is_z = maybe_self && j->eval_y == j->src_z;
   bool self = maybe_self, finite = true;
   constexpr int64_t kChunk = 1 << 20;
   double* hz = P->hz.as<double>();
-  double* hm = P->hm.as<double>();
   for (int64_t c0 = 0; c0 < int64_t(N); c0 += kChunk) {
     const int64_t c1 = std::min<int64_t>(N, c0 + kChunk);
+    if (z_locked)  // DMA first, read-only checks while it flies
+      CU_TRY(c, cudaMemcpyAsync(P->z.as<double>() + 2 * c0, j->src_z + 2 * c0,
+                                size_t(c1 - c0) * 16, cudaMemcpyHostToDevice, s));
     bool same = true, fin = true;
 #pragma omp parallel for schedule(static) reduction(&& : same, fin)
     for (int64_t i = c0; i < c1; ++i) {
       const double x = j->src_z[2 * i], y = j->src_z[2 * i + 1];
-      hz[2 * i] = x;
-      hz[2 * i + 1] = y;
-      hm[2 * i] = j->src_m[2 * i];
-      hm[2 * i + 1] = j->src_m[2 * i + 1];
+      if (!z_locked) {
+        hz[2 * i] = x;
+        hz[2 * i + 1] = y;
+      }
       fin = fin && std::isfinite(x) && std::isfinite(y);
       if (maybe_self)
         same = same && j->eval_sid[i] == i &&
-               std::memcmp(&j->eval_y[2 * i], &j->src_z[2 * i], 16) == 0;
+               (y_is_z || std::memcmp(&j->eval_y[2 * i], &j->src_z[2 * i], 16) == 0);
     }
     self = self && same;
     finite = finite && fin;
-    CU_TRY(c, cudaMemcpyAsync(P->z.as<double>() + 2 * c0, hz + 2 * c0, size_t(c1 - c0) * 16,
-                              cudaMemcpyHostToDevice, s));
-    CU_TRY(c, cudaMemcpyAsync(P->m.as<double>() + 2 * c0, hm + 2 * c0, size_t(c1 - c0) * 16,
-                              cudaMemcpyHostToDevice, s));
+    if (!z_locked)
+      CU_TRY(c, cudaMemcpyAsync(P->z.as<double>() + 2 * c0, hz + 2 * c0, size_t(c1 - c0) * 16,
+                                cudaMemcpyHostToDevice, s));
   }
   if (!finite) {
     cudaStreamSynchronize(s);
@@ -725,39 +742,124 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   uint64_t h2d = uint64_t(N) * 32;
   if (!self && M) {
     CU_TRY(c, P->y.ensure(uint64_t(M) * 16));
-    CU_TRY(c, P->hy.ensure(uint64_t(M) * 16));
     bool fin = true;
-    double* hy = P->hy.as<double>();
+    const bool y_locked = host_locked(j->eval_y, uint64_t(M) * 16);
+    if (y_locked) {
+      CU_TRY(c, cudaMemcpyAsync(P->y.p, j->eval_y, uint64_t(M) * 16, cudaMemcpyHostToDevice, s));
 #pragma omp parallel for schedule(static) reduction(&& : fin)
-    for (int64_t i = 0; i < int64_t(M); ++i) {
-      hy[2 * i] = j->eval_y[2 * i];
-      hy[2 * i + 1] = j->eval_y[2 * i + 1];
-      fin = fin && std::isfinite(hy[2 * i]) && std::isfinite(hy[2 * i + 1]);
+      for (int64_t i = 0; i < int64_t(M); ++i)
+        fin = fin && std::isfinite(j->eval_y[2 * i]) && std::isfinite(j->eval_y[2 * i + 1]);
+    } else {
+      CU_TRY(c, P->hy.ensure(uint64_t(M) * 16));
+      double* hy = P->hy.as<double>();
+#pragma omp parallel for schedule(static) reduction(&& : fin)
+      for (int64_t i = 0; i < int64_t(M); ++i) {
+        hy[2 * i] = j->eval_y[2 * i];
+        hy[2 * i + 1] = j->eval_y[2 * i + 1];
+        fin = fin && std::isfinite(hy[2 * i]) && std::isfinite(hy[2 * i + 1]);
+      }
+      CU_TRY(c, cudaMemcpyAsync(P->y.p, hy, uint64_t(M) * 16, cudaMemcpyHostToDevice, s));
     }
     if (!fin) {
       cudaStreamSynchronize(s);
       return set_err(c, FMMCU_EINVAL, "build_pyramid: non-finite eval position");
     }
-    CU_TRY(c, cudaMemcpyAsync(P->y.p, hy, uint64_t(M) * 16, cudaMemcpyHostToDevice, s));
     h2d += uint64_t(M) * 16;
     if (j->eval_sid) {
       CU_TRY(c, P->sid.ensure(uint64_t(M) * 8));
-      CU_TRY(c, P->hsid.ensure(uint64_t(M) * 8));
-      par_memcpy(P->hsid.p, j->eval_sid, uint64_t(M) * 8);
-      CU_TRY(c, cudaMemcpyAsync(P->sid.p, P->hsid.p, uint64_t(M) * 8, cudaMemcpyHostToDevice, s));
+      if (host_locked(j->eval_sid, uint64_t(M) * 8)) {
+        CU_TRY(c, cudaMemcpyAsync(P->sid.p, j->eval_sid, uint64_t(M) * 8, cudaMemcpyHostToDevice, s));
+      } else {
+        CU_TRY(c, P->hsid.ensure(uint64_t(M) * 8));
+        par_memcpy(P->hsid.p, j->eval_sid, uint64_t(M) * 8);
+        CU_TRY(c, cudaMemcpyAsync(P->sid.p, P->hsid.p, uint64_t(M) * 8, cudaMemcpyHostToDevice, s));
+      }
       h2d += uint64_t(M) * 8;
     }
   }
   CU_TRY(c, cudaEventRecord(ev[1], s));
-  if (j->inputs_consumed) j->inputs_consumed(j->inputs_consumed_arg);
+  // masses: behind the positions on the PCIe link, in parallel with the pyramid
+  cudaStream_t hs = c->h2d_stream;
+  CU_TRY(c, cudaStreamWaitEvent(hs, ev[1], 0));
+  if (m_locked) {
+    CU_TRY(c, cudaMemcpyAsync(P->m.p, j->src_m, uint64_t(N) * 16, cudaMemcpyHostToDevice, hs));
+    CU_TRY(c, cudaEventRecord(ev[11], hs));
+    if (j->inputs_consumed) j->inputs_consumed(j->inputs_consumed_arg);
+  } else {
+    P->m_err = cudaSuccess;
+    const int dev = c->device;
+    double* hm = P->hm.as<double>();
+    double* dm = P->m.as<double>();
+    const double* src_m = j->src_m;
+    cudaEvent_t done = ev[11];
+    void (*hook)(void*) = j->inputs_consumed;
+    void* hook_arg = j->inputs_consumed_arg;
+    P->m_stager = std::thread([=] {
+      cudaError_t e = cudaSetDevice(dev);
+      for (int64_t c0 = 0; e == cudaSuccess && c0 < int64_t(N); c0 += kChunk) {
+        const int64_t c1 = std::min<int64_t>(N, c0 + kChunk);
+        par_memcpy(hm + 2 * c0, src_m + 2 * c0, size_t(c1 - c0) * 16);
+        e = cudaMemcpyAsync(dm + 2 * c0, hm + 2 * c0, size_t(c1 - c0) * 16,
+                            cudaMemcpyHostToDevice, hs);
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(done, hs);
+      P->m_err = e;
+      // every input has been read: the caller's result-buffer work now
+      // overlaps the pyramid build without competing with the staging copies
+      if (hook) hook(hook_arg);
+    });
+  }
+  // every return from here on joins the mass stager first (it may call the
+  // caller's hook); join_masses() also reports its outcome
+  struct StagerJoin {
+    DevicePipeline* P;
+    ~StagerJoin() {
+      if (P->m_stager.joinable()) P->m_stager.join();
+    }
+  } stager_join{P};
+  auto join_masses = [&]() -> int {
+    if (!P->m_stager.joinable()) return FMMCU_OK;
+    P->m_stager.join();
+    if (P->m_err != cudaSuccess) return set_err(c, FMMCU_ECUDA, cudaGetErrorString(P->m_err));
+    return FMMCU_OK;
+  };
 
   // ---- pyramid + connectivity ------------------------------------------------
-  if (int rc = build_pyramid_dev(c, P, j->theta, s)) return rc;
+  if (int rc = build_pyramid_dev(c, P, j->theta, s)) {
+    join_masses();
+    return rc;
+  }
   CU_TRY(c, cudaEventRecord(ev[2], s));
-  if (int rc = build_connectivity_dev(c, P, j->theta, s)) return rc;
+  if (int rc = build_connectivity_dev(c, P, j->theta, s)) {
+    join_masses();
+    return rc;
+  }
   P->tree_valid = true;
   const int L = P->L;
   const uint32_t nleaf = uint32_t(pow4(L - 1));
+  // the finest CSR goes to the host right away (d2h stream, pinned vectors):
+  // the host builds the P2P work list while the device permutes the inputs
+  // and starts the far field
+  const LevelConnDev& fc = P->conn[L - 1];
+  {
+    cudaStream_t ds = c->d2h_stream;
+    CU_TRY(c, cudaEventRecord(ev[12], s));
+    CU_TRY(c, cudaStreamWaitEvent(ds, ev[12], 0));
+    P->h_pt.resize(nleaf + 1);
+    P->h_evo.resize(nleaf + 1);
+    P->h_so.resize(nleaf + 1);
+    P->h_si.resize(std::max(fc.s_nnz, 1u));
+    CU_TRY(c, cudaMemcpyAsync(P->h_pt.data(), P->soff.as<uint32_t>() + P->off_base[L - 1],
+                              (nleaf + 1) * 4, cudaMemcpyDeviceToHost, ds));
+    CU_TRY(c, cudaMemcpyAsync(P->h_evo.data(), P->eoff.as<uint32_t>() + P->off_base[L - 1],
+                              (nleaf + 1) * 4, cudaMemcpyDeviceToHost, ds));
+    CU_TRY(c, cudaMemcpyAsync(P->h_so.data(), fc.s_off.p, (nleaf + 1) * 4, cudaMemcpyDeviceToHost, ds));
+    CU_TRY(c, cudaMemcpyAsync(P->h_si.data(), fc.s_idx.p, uint64_t(fc.s_nnz) * 4,
+                              cudaMemcpyDeviceToHost, ds));
+    CU_TRY(c, cudaEventRecord(ev[13], ds));
+  }
+  if (int rc = join_masses()) return rc;
+  CU_TRY(c, cudaStreamWaitEvent(s, ev[11], 0));  // pack_sources reads the masses
 
   // ---- permuted inputs into the P2P staging of the context ----------------
   CU_TRY(c, c->d_src.ensure(uint64_t(N) * 32));
@@ -785,24 +887,15 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   if (int rc = far_field(c, P, P->far, ev[6], ev[7])) return rc;
 
   // ---- near field: host work list from the finest CSR, then the P2P kernels
-  std::vector<uint32_t> pt(nleaf + 1), evo(nleaf + 1), so(nleaf + 1);
-  const LevelConnDev& fc = P->conn[L - 1];
-  std::vector<uint32_t> si(std::max(fc.s_nnz, 1u));
-  CU_TRY(c, cudaMemcpyAsync(pt.data(), P->soff.as<uint32_t>() + P->off_base[L - 1],
-                            (nleaf + 1) * 4, cudaMemcpyDeviceToHost, s));
-  CU_TRY(c, cudaMemcpyAsync(evo.data(), P->eoff.as<uint32_t>() + P->off_base[L - 1],
-                            (nleaf + 1) * 4, cudaMemcpyDeviceToHost, s));
-  CU_TRY(c, cudaMemcpyAsync(so.data(), fc.s_off.p, (nleaf + 1) * 4, cudaMemcpyDeviceToHost, s));
-  CU_TRY(c, cudaMemcpyAsync(si.data(), fc.s_idx.p, uint64_t(fc.s_nnz) * 4, cudaMemcpyDeviceToHost, s));
-  CU_TRY(c, cudaStreamSynchronize(s));
+  CU_TRY(c, cudaEventSynchronize(ev[13]));
   fmmcu_p2p_job pj{};
   pj.n_leaves = nleaf;
   pj.n_src = N;
   pj.n_eval = M;
-  pj.pt_off = pt.data();
-  pj.ev_off = evo.data();
-  pj.strong_off = so.data();
-  pj.strong_idx = si.data();
+  pj.pt_off = P->h_pt.data();
+  pj.ev_off = P->h_evo.data();
+  pj.strong_off = P->h_so.data();
+  pj.strong_idx = P->h_si.data();
   pj.kernel = j->kernel;
   pj.smoother = j->smoother;
   pj.delta = j->delta;
@@ -842,15 +935,22 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   CU_TRY(c, P->h_flag.ensure(16));
   CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.p, 4, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, s));
-  // D2H in chunks so that fmmcu_fmm_finish copies chunk i out of the pinned
-  // staging while chunk i+1 is still in flight
-  CU_TRY(c, P->hres.ensure(uint64_t(std::max(M, 1u)) * 16));
+  // D2H straight into the caller's out when it is page-locked; else in chunks
+  // so that fmmcu_fmm_finish copies chunk i out of the pinned staging while
+  // chunk i+1 is still in flight
+  P->direct_res = M && host_locked(j->out, uint64_t(M) * 16);
+  P->res_host = P->direct_res ? reinterpret_cast<double2*>(j->out) : nullptr;
+  if (!P->direct_res) {
+    CU_TRY(c, P->hres.ensure(uint64_t(std::max(M, 1u)) * 16));
+    P->res_host = P->hres.as<double2>();
+  }
   P->n_chunks = 0;
   if (M) {
-    const uint32_t per = std::max<uint32_t>(1u << 18, (M + kResChunks - 1) / kResChunks);
+    const uint32_t per = P->direct_res ? M
+                                       : std::max<uint32_t>(1u << 18, (M + kResChunks - 1) / kResChunks);
     for (uint32_t e0 = 0; e0 < M; e0 += per) {
       const uint32_t e1 = std::min(M, e0 + per);
-      CU_TRY(c, cudaMemcpyAsync(P->hres.as<double2>() + e0, P->res.as<double2>() + e0,
+      CU_TRY(c, cudaMemcpyAsync(P->res_host + e0, P->res.as<double2>() + e0,
                                 uint64_t(e1 - e0) * 16, cudaMemcpyDeviceToHost, s));
       CU_TRY(c, cudaEventRecord(P->ev_res[P->n_chunks], s));
       P->chunk_off[P->n_chunks] = e0;
@@ -872,10 +972,26 @@ int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {
   CU_TRY(c, cudaSetDevice(c->device));
   const uint32_t M = P->M;
   if (M && !out) return set_err(c, FMMCU_EINVAL, "null output");
+  double t_wait = 0, t_copy = 0;
   for (int i = 0; i < P->n_chunks; ++i) {
+    const auto a = Clock::now();
     CU_TRY(c, cudaEventSynchronize(P->ev_res[i]));
+    const auto b = Clock::now();
     const uint32_t e0 = P->chunk_off[i], e1 = P->chunk_off[i + 1];
-    par_memcpy(out + 2 * uint64_t(e0), P->hres.as<double2>() + e0, uint64_t(e1 - e0) * 16);
+    if (reinterpret_cast<double2*>(out) != P->res_host)
+      par_memcpy(out + 2 * uint64_t(e0), P->res_host + e0, uint64_t(e1 - e0) * 16);
+    t_wait += std::chrono::duration<double, std::milli>(b - a).count();
+    t_copy += std::chrono::duration<double, std::milli>(Clock::now() - b).count();
+  }
+  if (c->trace) {
+    std::fprintf(stderr, "[fmmcu] finish: %d result chunks, wait %.3f ms, copy-out %.3f ms\n",
+                 P->n_chunks, t_wait, t_copy);
+    cudaEventSynchronize(P->ev[10]);
+    std::fprintf(stderr, "[fmmcu] device timeline (ms from start):");
+    static const char* names[] = {"start", "positions", "pyramid", "connect+perm", "m2l lists",
+                                  "far start", "upward", "m2l", "p2p start", "p2p end", "end"};
+    for (int e = 1; e <= 10; ++e) std::fprintf(stderr, " %s %.2f", names[e], span_ms(P->ev[0], P->ev[e]));
+    std::fprintf(stderr, "\n");
   }
   cudaEvent_t* ev = P->ev;
   CU_TRY(c, cudaEventSynchronize(ev[10]));

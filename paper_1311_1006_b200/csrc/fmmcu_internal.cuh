@@ -111,6 +111,18 @@ inline void par_memcpy(void* dst, const void* src, size_t bytes) {
   }
 }
 
+// True when [p, p + bytes) is page-locked host memory the DMA engines can read
+// or write in place (cudaHostRegister'ed or cudaHostAlloc'ed at both ends).
+inline bool host_locked(const void* p, size_t bytes) {
+  if (!p || !bytes) return false;
+  auto one = [](const void* q) {
+    cudaPointerAttributes at{};
+    const bool ok = cudaPointerGetAttributes(&at, q) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  return one(p) && one(static_cast<const char*>(p) + bytes - 1);
+}
 
 struct DevicePipeline;  // fmm_device.cu
 void destroy_pipeline(DevicePipeline* p);

@@ -6,6 +6,9 @@
 // (types.hpp:62-92): launch/finish failures surface as exceptions that the
 // engine wraps as BackendError("nearfield launch" | "nearfield", ...)
 // (engine.cpp:294-311); coincident M2L centres as SingularConfiguration.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <sys/mman.h>
 
 #include <algorithm>
@@ -97,8 +100,13 @@ CudaBackend::DeviceEval CudaBackend::fmm_evaluate(const SourceSet& sources, cons
   // its 16 B/eval zero fill + first-touch page faults run on a helper thread
   // while the device pipeline works, and the potentials are copied in once
   // it has finished.  reserve() fixes the storage, so data() stays valid.
-  out.clear();
-  out.reserve(evals.size());
+  // A result that already has the right size (evaluate_into) is overwritten
+  // in place: no allocation, no zero fill.
+  const bool reuse = !out.empty() && out.size() == evals.size();
+  if (!reuse) {
+    out.clear();
+    out.reserve(evals.size());
+  }
   // started once the pipeline has read the inputs (the host then only waits
   // on the device), so the fill does not compete with the upload staging
   std::thread zero_fill;
@@ -122,19 +130,31 @@ CudaBackend::DeviceEval CudaBackend::fmm_evaluate(const SourceSet& sources, cons
                : smoother.kind == Smoother::Kind::gaussian ? FMMCU_SMOOTH_GAUSSIAN
                                                            : FMMCU_SMOOTH_PLUMMER;
   j.delta = smoother.delta;
-  j.out = nullptr;
+  j.out = reuse ? reinterpret_cast<double*>(out.data()) : nullptr;  // direct D2H if page-locked
   j.inputs_consumed = [](void* arg) {
     auto* h = static_cast<Hook*>(arg);
     *h->t = std::thread([out = h->out, n = h->n] { resize_huge(*out, n); });
   };
   j.inputs_consumed_arg = &hook;
+  if (reuse) j.inputs_consumed = nullptr;
   fmmcu_fmm_stats st{};
+  using TClock = std::chrono::steady_clock;
+  const auto t0 = TClock::now();
   int rc = fmmcu_fmm_launch(ctx_[0], &j);
+  const auto t1 = TClock::now();
   if (zero_fill.joinable()) zero_fill.join();
-  else resize_huge(out, evals.size());
+  else if (!reuse) resize_huge(out, evals.size());
+  const auto t2 = TClock::now();
   if (rc == FMMCU_OK)
     rc = fmmcu_fmm_finish(ctx_[0], evals.size() ? reinterpret_cast<double*>(out.data()) : nullptr,
                           &st);
+  if (std::getenv("FMMCU_TRACE")) {
+    auto ms = [](TClock::time_point a, TClock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    std::fprintf(stderr, "[fmm] launch %.3f ms, result fill join %.3f ms, finish %.3f ms\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, TClock::now()));
+  }
   if (rc != FMMCU_OK) raise(ctx_[0], rc, "device pipeline");
   DeviceEval d;
   d.counters.p2p_pairs = st.p2p_pairs;

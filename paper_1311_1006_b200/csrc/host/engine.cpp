@@ -305,6 +305,12 @@ void FmmEngine::set_config(const FmmConfig& cfg) {
 }
 
 EvalResult FmmEngine::evaluate(const SourceSet& sources, const EvalSet& evals) {
+  EvalResult res;
+  evaluate_into(sources, evals, res);
+  return res;
+}
+
+void FmmEngine::evaluate_into(const SourceSet& sources, const EvalSet& evals, EvalResult& res) {
   if (!(cfg_.theta > 0.0 && cfg_.theta < 1.0)) throw InvalidParameter("evaluate: theta outside (0,1)");
   if (cfg_.n_levels < 1) throw InvalidParameter("evaluate: n_levels < 1");
   if (cfg_.worker_threads < 1) throw InvalidParameter("evaluate: worker_threads < 1");
@@ -317,7 +323,8 @@ EvalResult FmmEngine::evaluate(const SourceSet& sources, const EvalSet& evals) {
   if (cfg_.device_pipeline && cfg_.backend != BackendKind::cuda)
     throw InvalidParameter("evaluate: device_pipeline requires the cuda backend");
 
-  EvalResult res;
+  res.timings = PhaseTimings{};
+  res.counters = WorkCounters{};
   res.p = cfg_.expansion_order();
   const int p = res.p;
   const int threads = cfg_.worker_threads;
@@ -350,7 +357,7 @@ EvalResult FmmEngine::evaluate(const SourceSet& sources, const EvalSet& evals) {
             std::max(0.0, d.t_device - T.t_partition - std::max(T.t_p2p, T.t_p2m + T.t_m2l));
     T.cpu_wait = 0.0;
     if (observer_) observer_(*this, res);
-    return res;
+    return;
   }
 
   // ---- partition ------------------------------------------------------------
@@ -440,7 +447,7 @@ EvalResult FmmEngine::evaluate(const SourceSet& sources, const EvalSet& evals) {
   T.t_q = T.t_partition + T.t_p2m + T.t_upward + t_assembly;
   T.t_total = since(t_start);
   if (observer_) observer_(*this, res);
-  return res;
+  return;
 }
 
 }  // namespace fmm

@@ -116,3 +116,45 @@ def test_device_pipeline_rejects_bad_input(ctx):
         ctx.fmm_evaluate(s.z, s.m, s.z, None, n_levels=3, theta=1.5, p=17)
     with pytest.raises(N.FmmcuError):
         ctx.fmm_evaluate(s.z[:0], s.m[:0], s.z, None, n_levels=3, theta=0.5, p=17)
+
+
+def test_device_pipeline_page_locked_io_is_identical(ctx):
+    """Page-locked inputs are DMA'd in place (no staging) and a page-locked
+    out receives the D2H directly; the potentials must not change."""
+    s = F.make_distribution("uniform", 60_000, 13)
+    e = F.EvalSet.self_of(s)
+    a, _ = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=6, theta=0.5, p=17)
+    out = np.zeros(len(e.y), dtype=np.complex128)
+    arrs = (s.z, s.m, e.y, e.source_id, out)
+    for x in arrs:
+        ctx.host_register(x)
+    try:
+        b, _ = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=6, theta=0.5, p=17, out=out)
+        # separate evals, page-locked y
+        y = F.make_distribution("random", 7_000, 14).z
+        ctx.host_register(y)
+        try:
+            c1, _ = ctx.fmm_evaluate(s.z, s.m, y, None, n_levels=6, theta=0.5, p=17)
+        finally:
+            ctx.host_unregister(y)
+    finally:
+        for x in arrs:
+            ctx.host_unregister(x)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    c0, _ = ctx.fmm_evaluate(s.z, s.m, y.copy(), None, n_levels=6, theta=0.5, p=17)
+    assert np.array_equal(c0.view(np.uint64), c1.view(np.uint64))
+
+
+def test_engine_result_reuse_across_sizes():
+    """The Python engine handle reuses its SourceSet/EvalSet/EvalResult
+    storage (FmmEngine::evaluate_into); results must match fresh engines
+    whether the problem size stays or changes between calls."""
+    eng = F.FmmEngine(F.FmmConfig(n_levels=5, backend="cuda", device_pipeline=True))
+    sets = [F.make_distribution("uniform", 30_000, 21), F.make_distribution("uniform", 30_000, 22),
+            F.make_distribution("gauss8", 12_000, 23), F.make_distribution("uniform", 30_000, 21)]
+    got = [eng.evaluate(s, F.EvalSet.self_of(s)).potentials.copy() for s in sets]
+    for s, g in zip(sets, got):
+        fresh = F.FmmEngine(F.FmmConfig(n_levels=5, backend="cuda", device_pipeline=True))
+        want = fresh.evaluate(s, F.EvalSet.self_of(s)).potentials
+        assert np.array_equal(g.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(got[0].view(np.uint64), got[3].view(np.uint64))
