@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <future>
 #include <thread>
 
 #include "far_kernels.cuh"
@@ -68,8 +69,8 @@ struct DevicePipeline {
   double2* res_host = nullptr;  // where the D2H lands (out, or the hres staging)
   Clock::time_point t_host0{};
   uint64_t h2d = 0;
-  std::thread m_stager;         // stages the masses while the pyramid builds
-  cudaError_t m_err = cudaSuccess;
+  std::thread m_stager;         // stages the masses / checks self-evaluation
+  bool self_ok = true;          // the helper's self-evaluation verdict
 };
 
 void destroy_pipeline(DevicePipeline* p) {
@@ -656,7 +657,8 @@ float span_ms(cudaEvent_t a, cudaEvent_t b) {
 // ================================================================ C ABI ====
 extern "C" {
 
-int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
+namespace {
+int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   if (!c) return FMMCU_EINVAL;
   if (!j) return set_err(c, FMMCU_EINVAL, "null fmm job");
   if (c->pipe && c->pipe->pending) return set_err(c, FMMCU_ESTATE, "fmm launch while in flight");
@@ -682,6 +684,7 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   }
   DevicePipeline* P = c->pipe;
   if (P->m_stager.joinable()) P->m_stager.join();  // left over by an error return
+
   const uint32_t N = j->n_src, M = j->n_eval;
   P->N = N;
   P->M = M;
@@ -697,26 +700,28 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   // Positions first: the pyramid needs only z (and y, sid).  The masses follow
   // on the h2d stream behind them while the pyramid builds -- DMA'd in place
   // when the caller's arrays are page-locked, else staged through pinned
-  // chunks by a helper thread.  The host checks finiteness and detects
-  // self-evaluation while the position chunks are in flight.
+  // chunks by a helper thread.  Self-evaluation (evals = the sources, ids =
+  // their indices) is taken speculatively when the job has its shape (ids
+  // given, M == N): the helper thread verifies it while the pyramid builds,
+  // and a failed check uploads the evals and rebuilds (bit-identical to a
+  // non-speculative build; never happens for EvalSet::self_of inputs).
   CU_TRY(c, P->z.ensure(uint64_t(N) * 16));
   CU_TRY(c, P->m.ensure(uint64_t(N) * 16));
   const bool z_locked = host_locked(j->src_z, uint64_t(N) * 16);
   const bool m_locked = host_locked(j->src_m, uint64_t(N) * 16);
   if (!z_locked) CU_TRY(c, P->hz.ensure(uint64_t(N) * 16));
   if (!m_locked) CU_TRY(c, P->hm.ensure(uint64_t(N) * 16));
-  const bool maybe_self = j->eval_sid && M == N;
-  const bool y_is_z = maybe_self && j->eval_y == j->src_z;
-  bool self = maybe_self, finite = true;
+  const bool maybe_self = speculate && j->eval_sid && M == N && j->eval_y;
+  bool finite = true;
   constexpr int64_t kChunk = 1 << 20;
   double* hz = P->hz.as<double>();
   for (int64_t c0 = 0; c0 < int64_t(N); c0 += kChunk) {
     const int64_t c1 = std::min<int64_t>(N, c0 + kChunk);
-    if (z_locked)  // DMA first, read-only checks while it flies
+    if (z_locked)  // DMA first, read-only check while it flies
       CU_TRY(c, cudaMemcpyAsync(P->z.as<double>() + 2 * c0, j->src_z + 2 * c0,
                                 size_t(c1 - c0) * 16, cudaMemcpyHostToDevice, s));
-    bool same = true, fin = true;
-#pragma omp parallel for schedule(static) reduction(&& : same, fin)
+    bool fin = true;
+#pragma omp parallel for schedule(static) reduction(&& : fin)
     for (int64_t i = c0; i < c1; ++i) {
       const double x = j->src_z[2 * i], y = j->src_z[2 * i + 1];
       if (!z_locked) {
@@ -724,11 +729,7 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
         hz[2 * i + 1] = y;
       }
       fin = fin && std::isfinite(x) && std::isfinite(y);
-      if (maybe_self)
-        same = same && j->eval_sid[i] == i &&
-               (y_is_z || std::memcmp(&j->eval_y[2 * i], &j->src_z[2 * i], 16) == 0);
     }
-    self = self && same;
     finite = finite && fin;
     if (!z_locked)
       CU_TRY(c, cudaMemcpyAsync(P->z.as<double>() + 2 * c0, hz + 2 * c0, size_t(c1 - c0) * 16,
@@ -738,13 +739,12 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
     cudaStreamSynchronize(s);
     return set_err(c, FMMCU_EINVAL, "build_pyramid: non-finite source position");
   }
-  P->self_eval = self;
   uint64_t h2d = uint64_t(N) * 32;
-  if (!self && M) {
+  // eval positions (and ids) when they are not the sources
+  auto upload_evals = [&]() -> int {
     CU_TRY(c, P->y.ensure(uint64_t(M) * 16));
     bool fin = true;
-    const bool y_locked = host_locked(j->eval_y, uint64_t(M) * 16);
-    if (y_locked) {
+    if (host_locked(j->eval_y, uint64_t(M) * 16)) {
       CU_TRY(c, cudaMemcpyAsync(P->y.p, j->eval_y, uint64_t(M) * 16, cudaMemcpyHostToDevice, s));
 #pragma omp parallel for schedule(static) reduction(&& : fin)
       for (int64_t i = 0; i < int64_t(M); ++i)
@@ -776,7 +776,12 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
       }
       h2d += uint64_t(M) * 8;
     }
-  }
+    return FMMCU_OK;
+  };
+  if (!maybe_self && M)
+    if (int rc = upload_evals()) return rc;
+  P->self_eval = maybe_self;
+  P->self_ok = true;
   CU_TRY(c, cudaEventRecord(ev[1], s));
   // masses: behind the positions on the PCIe link, in parallel with the pyramid
   cudaStream_t hs = c->h2d_stream;
@@ -784,32 +789,55 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   if (m_locked) {
     CU_TRY(c, cudaMemcpyAsync(P->m.p, j->src_m, uint64_t(N) * 16, cudaMemcpyHostToDevice, hs));
     CU_TRY(c, cudaEventRecord(ev[11], hs));
-    if (j->inputs_consumed) j->inputs_consumed(j->inputs_consumed_arg);
-  } else {
-    P->m_err = cudaSuccess;
+  }
+  // One helper thread stages the masses (joined through masses_staged before
+  // pack_sources reads them), then verifies a speculative self-evaluation;
+  // the verdict is only joined at the end of the launch, and a failed check
+  // re-runs the launch without the speculation.  Host memory bandwidth is
+  // the scarce resource here, so the phases run back to back, not in parallel.
+  std::promise<cudaError_t> masses_promise;
+  std::future<cudaError_t> masses_staged = masses_promise.get_future();
+  if (!m_locked || maybe_self) {
     const int dev = c->device;
     double* hm = P->hm.as<double>();
     double* dm = P->m.as<double>();
-    const double* src_m = j->src_m;
+    const double* src_m = m_locked ? nullptr : j->src_m;
+    const double* src_z = j->src_z;
+    const double* ey = maybe_self ? j->eval_y : nullptr;
+    const int64_t* esid = j->eval_sid;
     cudaEvent_t done = ev[11];
     void (*hook)(void*) = j->inputs_consumed;
     void* hook_arg = j->inputs_consumed_arg;
-    P->m_stager = std::thread([=] {
-      cudaError_t e = cudaSetDevice(dev);
-      for (int64_t c0 = 0; e == cudaSuccess && c0 < int64_t(N); c0 += kChunk) {
-        const int64_t c1 = std::min<int64_t>(N, c0 + kChunk);
-        par_memcpy(hm + 2 * c0, src_m + 2 * c0, size_t(c1 - c0) * 16);
-        e = cudaMemcpyAsync(dm + 2 * c0, hm + 2 * c0, size_t(c1 - c0) * 16,
-                            cudaMemcpyHostToDevice, hs);
+    P->m_stager = std::thread([=, pr = std::move(masses_promise)]() mutable {
+      cudaError_t e = cudaSuccess;
+      if (src_m) {
+        e = cudaSetDevice(dev);
+        for (int64_t c0 = 0; e == cudaSuccess && c0 < int64_t(N); c0 += kChunk) {
+          const int64_t c1 = std::min<int64_t>(N, c0 + kChunk);
+          par_memcpy(hm + 2 * c0, src_m + 2 * c0, size_t(c1 - c0) * 16);
+          e = cudaMemcpyAsync(dm + 2 * c0, hm + 2 * c0, size_t(c1 - c0) * 16,
+                              cudaMemcpyHostToDevice, hs);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(done, hs);
       }
-      if (e == cudaSuccess) e = cudaEventRecord(done, hs);
-      P->m_err = e;
+      pr.set_value(e);
+      if (ey) {
+        const bool y_is_z = ey == src_z;
+        bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+        for (int64_t i = 0; i < int64_t(N); ++i)
+          ok = ok && esid[i] == i && (y_is_z || std::memcmp(ey + 2 * i, src_z + 2 * i, 16) == 0);
+        P->self_ok = ok;
+      }
       // every input has been read: the caller's result-buffer work now
-      // overlaps the pyramid build without competing with the staging copies
+      // overlaps the device work
       if (hook) hook(hook_arg);
     });
+  } else {
+    masses_promise.set_value(cudaSuccess);
+    if (j->inputs_consumed) j->inputs_consumed(j->inputs_consumed_arg);
   }
-  // every return from here on joins the mass stager first (it may call the
+  // every return from here on joins the helper first (it may call the
   // caller's hook); join_masses() also reports its outcome
   struct StagerJoin {
     DevicePipeline* P;
@@ -818,22 +846,17 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
     }
   } stager_join{P};
   auto join_masses = [&]() -> int {
-    if (!P->m_stager.joinable()) return FMMCU_OK;
-    P->m_stager.join();
-    if (P->m_err != cudaSuccess) return set_err(c, FMMCU_ECUDA, cudaGetErrorString(P->m_err));
+    const cudaError_t e = masses_staged.get();
+    if (e != cudaSuccess) return set_err(c, FMMCU_ECUDA, cudaGetErrorString(e));
     return FMMCU_OK;
   };
 
   // ---- pyramid + connectivity ------------------------------------------------
-  if (int rc = build_pyramid_dev(c, P, j->theta, s)) {
-    join_masses();
-    return rc;
-  }
+  if (int rc = build_pyramid_dev(c, P, j->theta, s)) return rc;
   CU_TRY(c, cudaEventRecord(ev[2], s));
-  if (int rc = build_connectivity_dev(c, P, j->theta, s)) {
-    join_masses();
-    return rc;
-  }
+  if (int rc = build_connectivity_dev(c, P, j->theta, s)) return rc;
+  if (int rc = join_masses()) return rc;
+  const bool self = P->self_eval;
   P->tree_valid = true;
   const int L = P->L;
   const uint32_t nleaf = uint32_t(pow4(L - 1));
@@ -858,7 +881,6 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
                               cudaMemcpyDeviceToHost, ds));
     CU_TRY(c, cudaEventRecord(ev[13], ds));
   }
-  if (int rc = join_masses()) return rc;
   CU_TRY(c, cudaStreamWaitEvent(s, ev[11], 0));  // pack_sources reads the masses
 
   // ---- permuted inputs into the P2P staging of the context ----------------
@@ -961,7 +983,25 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   P->pending = true;
   P->t_host0 = t_host0;
   P->h2d = h2d;
+  if (P->m_stager.joinable()) P->m_stager.join();  // the self-evaluation verdict
   return FMMCU_OK;
+}
+}  // namespace
+
+int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
+  const int rc = fmm_launch_impl(c, j, true);
+  DevicePipeline* P = c ? c->pipe : nullptr;
+  if (rc != FMMCU_OK || !P || !P->self_eval || P->self_ok) return rc;
+  // the evals only looked like the sources (ids given, M == N): drop the
+  // speculative self-evaluation and evaluate them as separate points
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  P->pending = false;
+  const auto t0 = P->t_host0;
+  fmmcu_fmm_job j2 = *j;
+  j2.inputs_consumed = nullptr;  // already called once
+  const int rc2 = fmm_launch_impl(c, &j2, false);
+  P->t_host0 = t0;
+  return rc2;
 }
 
 int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {

@@ -41,6 +41,12 @@ def _cases():
     yield "separate_evals_L4", s, F.EvalSet(F.make_distribution("random", 3_000, 6).z * 1.2 - 0.1), 4, 0.5
     yield "single_level", F.make_distribution("random", 700, 7), None, 1, 0.5
     yield "two_levels", F.make_distribution("random", 900, 8), None, 2, 0.4
+    # self-evaluation shape (ids given, M == N) but not self-evaluation: the
+    # pipeline's speculative self build must be discarded and redone
+    s = F.make_distribution("uniform", 6_000, 9)
+    perm = np.random.default_rng(9).permutation(6_000)
+    yield "self_shape_permuted", s, F.EvalSet(s.z[perm], perm.astype(np.int64)), 5, 0.5
+    yield "self_shape_moved", s, F.EvalSet(s.z + 1e-9, np.arange(6_000, dtype=np.int64)), 5, 0.5
 
 
 def _evals(s, e):
@@ -80,7 +86,7 @@ def test_device_tree_bitwise_equal_to_host(ctx, case):
 @pytest.mark.parametrize("kernel,smoother,delta", [("harmonic", "none", 0.0),
                                                    ("logarithmic", "none", 0.0),
                                                    ("harmonic", "gaussian", 0.01)])
-@pytest.mark.parametrize("case", list(_cases())[:5], ids=lambda c: c[0])
+@pytest.mark.parametrize("case", list(_cases())[:5] + list(_cases())[7:], ids=lambda c: c[0])
 def test_device_potentials_match_cpu_evaluate(ctx, case, kernel, smoother, delta):
     name, s, e, L, theta = case
     e = _evals(s, e)
