@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <omp.h>
 #include <future>
 #include <thread>
 
@@ -215,8 +216,10 @@ int partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint32_t n,
 }
 
 // ------------------------------------------------------------ the pyramid --
-int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_t s) {
-  (void)theta;
+// One build.  alias: self-evaluation with the eval lists aliased to the
+// source lists (all eval work skipped); any tied split is flagged in
+// P->flag and the caller then rebuilds with alias = false.
+int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool alias) {
   const uint32_t N = P->N, M = P->M;
   const int L = P->L;
   const double2* zp = P->z.as<double2>();
@@ -311,31 +314,15 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
   // Self-evaluation: the evals are the sources (same points, same ids), so
   // while no split value is tied (the count of coords <= split equals the
   // median rank in every segment) the eval lists and offsets ARE the source
-  // ones and all eval work is skipped.  The first tied split materialises
-  // the eval lists and the build continues with both.
-  bool same = P->self_eval;
+  // ones and all eval work is skipped.  A tie anywhere is only flagged here
+  // (no per-split host round trip); build_pyramid_dev then rebuilds with
+  // separate eval lists, which reproduces the aliased build up to the tie.
+  const bool same = alias;
   int* differ = nullptr;
-  int* h_differ = nullptr;
   if (same) {
     CU_TRY(c, P->flag.ensure(8));
-    CU_TRY(c, P->h_flag.ensure(16));
     differ = P->flag.as<int>();
-    h_differ = P->h_flag.as<int>();
   }
-  // after a split computed with the aliased lists: still no tie anywhere?
-  auto check_same = [&](uint32_t* sxl, uint32_t* syl, const uint32_t* soffl, uint32_t* eoffl,
-                        size_t noff, const uint32_t* half_src) -> int {
-    CU_TRY(c, cudaMemcpyAsync(h_differ, differ, 4, cudaMemcpyDeviceToHost, s));
-    CU_TRY(c, cudaStreamSynchronize(s));
-    if (*h_differ == 0) return FMMCU_OK;
-    same = false;  // materialise the eval lists as they stand
-    CU_TRY(c, cudaMemcpyAsync(EX, sxl, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
-    CU_TRY(c, cudaMemcpyAsync(EY, syl, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
-    CU_TRY(c, cudaMemcpyAsync(eoffl, soffl, noff * 4, cudaMemcpyDeviceToDevice, s));
-    if (half_src)  // 2 (noff - 1) + 1 half offsets
-      CU_TRY(c, cudaMemcpyAsync(half_e, half_src, (2 * noff - 1) * 4, cudaMemcpyDeviceToDevice, s));
-    return FMMCU_OK;
-  };
   if (same) CU_TRY(c, cudaMemsetAsync(differ, 0, 4, s));
   for (int l = 1; l < L; ++l) {
     const uint32_t np = uint32_t(pow4(l - 1));
@@ -358,10 +345,6 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
     a.emid = xmid_e;
     a.differ = same ? differ : nullptr;
     split_kernel<<<blocks(np), TB, 0, s>>>(a);
-    if (same) {
-      // on a tie: eval lists = the source lists before this split
-      if (int rc = check_same(SX, SY, ps, eoff + P->off_base[l - 1], np + 1, nullptr)) return rc;
-    }
     if (N) low_flags_kernel<<<blocks(N), TB, 0, s>>>(SX, N, ps, xmid_s, np, fs);
     if (M && !same) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EX, M, pe, xmid_e, np, fe);
     if (int rc = partition(c, P, SY, N, fs, ps, xmid_s, np, SYn, s)) return rc;
@@ -384,14 +367,6 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
     a.emid = ymid_e;
     a.differ = same ? differ : nullptr;
     split_kernel<<<blocks(2 * np), TB, 0, s>>>(a);
-    if (same) {
-      // on a tie: eval lists = source lists after the x split, halves alike
-      if (int rc = check_same(SX, SY, ps, eoff + P->off_base[l - 1], np + 1, half_s)) return rc;
-      if (!same) {
-        // the x split itself had no tie: its eval counts equal the source ones
-        CU_TRY(c, cudaMemcpyAsync(xmid_e, xmid_s, uint64_t(np) * 4, cudaMemcpyDeviceToDevice, s));
-      }
-    }
     if (N) low_flags_kernel<<<blocks(N), TB, 0, s>>>(SY, N, half_s, ymid_s, 2 * np, fs);
     if (M && !same) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EY, M, half_e, ymid_e, 2 * np, fe);
     if (int rc = partition(c, P, SX, N, fs, half_s, ymid_s, 2 * np, SXn, s)) return rc;
@@ -451,6 +426,17 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
   CU_TRY(c, cudaGetLastError());
   c->launches += uint64_t(8 + 14 * (L - 1));
   return FMMCU_OK;
+}
+
+int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_t s) {
+  (void)theta;
+  if (int rc = build_pyramid_pass(c, P, s, P->self_eval)) return rc;
+  if (!P->self_eval) return FMMCU_OK;
+  CU_TRY(c, P->h_flag.ensure(16));
+  CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.p, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaStreamSynchronize(s));
+  if (*P->h_flag.as<int>() == 0) return FMMCU_OK;
+  return build_pyramid_pass(c, P, s, false);  // a split was tied: separate eval lists
 }
 
 // ----------------------------------------------------------- connectivity --
@@ -790,45 +776,31 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
     CU_TRY(c, cudaMemcpyAsync(P->m.p, j->src_m, uint64_t(N) * 16, cudaMemcpyHostToDevice, hs));
     CU_TRY(c, cudaEventRecord(ev[11], hs));
   }
-  // One helper thread stages the masses (joined through masses_staged before
-  // pack_sources reads them), then verifies a speculative self-evaluation;
-  // the verdict is only joined at the end of the launch, and a failed check
-  // re-runs the launch without the speculation.  Host memory bandwidth is
-  // the scarce resource here, so the phases run back to back, not in parallel.
+  // A helper thread stages the masses (joined through masses_staged before
+  // pack_sources reads them).  A speculative self-evaluation is verified by
+  // the launching thread once the P2P kernels are queued (it is idle then; an
+  // OpenMP team on the helper would fight the work-list build for the
+  // cores), and a failed check re-runs the launch without the speculation.
   std::promise<cudaError_t> masses_promise;
   std::future<cudaError_t> masses_staged = masses_promise.get_future();
-  if (!m_locked || maybe_self) {
+  if (!m_locked) {
     const int dev = c->device;
     double* hm = P->hm.as<double>();
     double* dm = P->m.as<double>();
-    const double* src_m = m_locked ? nullptr : j->src_m;
-    const double* src_z = j->src_z;
-    const double* ey = maybe_self ? j->eval_y : nullptr;
-    const int64_t* esid = j->eval_sid;
+    const double* src_m = j->src_m;
     cudaEvent_t done = ev[11];
     void (*hook)(void*) = j->inputs_consumed;
     void* hook_arg = j->inputs_consumed_arg;
     P->m_stager = std::thread([=, pr = std::move(masses_promise)]() mutable {
-      cudaError_t e = cudaSuccess;
-      if (src_m) {
-        e = cudaSetDevice(dev);
-        for (int64_t c0 = 0; e == cudaSuccess && c0 < int64_t(N); c0 += kChunk) {
-          const int64_t c1 = std::min<int64_t>(N, c0 + kChunk);
-          par_memcpy(hm + 2 * c0, src_m + 2 * c0, size_t(c1 - c0) * 16);
-          e = cudaMemcpyAsync(dm + 2 * c0, hm + 2 * c0, size_t(c1 - c0) * 16,
-                              cudaMemcpyHostToDevice, hs);
-        }
-        if (e == cudaSuccess) e = cudaEventRecord(done, hs);
+      cudaError_t e = cudaSetDevice(dev);
+      for (int64_t c0 = 0; e == cudaSuccess && c0 < int64_t(N); c0 += kChunk) {
+        const int64_t c1 = std::min<int64_t>(N, c0 + kChunk);
+        par_memcpy(hm + 2 * c0, src_m + 2 * c0, size_t(c1 - c0) * 16);
+        e = cudaMemcpyAsync(dm + 2 * c0, hm + 2 * c0, size_t(c1 - c0) * 16,
+                            cudaMemcpyHostToDevice, hs);
       }
+      if (e == cudaSuccess) e = cudaEventRecord(done, hs);
       pr.set_value(e);
-      if (ey) {
-        const bool y_is_z = ey == src_z;
-        bool ok = true;
-#pragma omp parallel for schedule(static) reduction(&& : ok)
-        for (int64_t i = 0; i < int64_t(N); ++i)
-          ok = ok && esid[i] == i && (y_is_z || std::memcmp(ey + 2 * i, src_z + 2 * i, 16) == 0);
-        P->self_ok = ok;
-      }
       // every input has been read: the caller's result-buffer work now
       // overlaps the device work
       if (hook) hook(hook_arg);
@@ -983,7 +955,18 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   P->pending = true;
   P->t_host0 = t_host0;
   P->h2d = h2d;
-  if (P->m_stager.joinable()) P->m_stager.join();  // the self-evaluation verdict
+  if (P->m_stager.joinable()) P->m_stager.join();
+  if (maybe_self) {  // verify the speculation
+    const double* ey = j->eval_y;
+    const double* zz = j->src_z;
+    const int64_t* esid = j->eval_sid;
+    const bool y_is_z = ey == zz;
+    bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+    for (int64_t i = 0; i < int64_t(N); ++i)
+      ok = ok && esid[i] == i && (y_is_z || std::memcmp(ey + 2 * i, zz + 2 * i, 16) == 0);
+    P->self_ok = ok;
+  }
   return FMMCU_OK;
 }
 }  // namespace

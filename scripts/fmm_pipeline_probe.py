@@ -40,10 +40,16 @@ if a.register:
     for arr in (s.z, s.m, e.y, e.source_id, out):
         ctx.host_unregister(arr)
 ctx.close()
+totals = []
 eng = F.FmmEngine(F.FmmConfig(n_levels=a.levels, backend="cuda", device_pipeline=True))
 for r in range(a.reps):
     t0 = time.perf_counter()
     res = eng.evaluate(s, e)
     t1 = time.perf_counter()
+    totals.append(res.timings["t_total"])
     print(f"engine rep {r}: wall {1e3 * (t1 - t0):.2f} ms  t_total {1e3 * res.timings['t_total']:.2f} ms",
           flush=True)
+if len(totals) > 2:
+    t = sorted(totals[1:])
+    print(f"engine t_total over reps 1..: median {1e3 * t[len(t) // 2]:.2f} ms, "
+          f"min {1e3 * t[0]:.2f}, max {1e3 * t[-1]:.2f}", flush=True)
