@@ -68,20 +68,43 @@ std::vector<cplx> vortex_velocities(const VortexSystem& sys, FmmEngine& engine, 
     return {cplx(0, 0)};
   }
   use_vortex_kernel(engine, sys.delta);
-  SourceSet src;
-  src.z = sys.pos;
-  src.m.resize(sys.size());
-  for (std::size_t k = 0; k < sys.size(); ++k) src.m[k] = sys.gamma[k] * kOneOverTwoPiI;
-  EvalResult r = engine.evaluate(src, EvalSet::self_of(src));
-  std::vector<cplx> v(sys.size());
-  for (std::size_t k = 0; k < v.size(); ++k) v[k] = std::conj(r.potentials[k]);
-  if (info) *info = std::move(r);
+  // Time stepping evaluates one problem size over and over: the sources, the
+  // (self) evals and the result live in per-thread buffers that are refilled
+  // in parallel, and evaluate_into() reuses the result storage.  Same values
+  // as building them afresh (reference sims.cpp:66-84).
+  thread_local SourceSet tl_src;
+  thread_local EvalSet tl_ev;
+  thread_local EvalResult tl_r;
+  // plain references: inside the OpenMP regions a thread_local name would
+  // denote each worker's own (empty) copy
+  SourceSet& src = tl_src;
+  EvalSet& ev = tl_ev;
+  EvalResult& r = tl_r;
+  const std::int64_t n = std::int64_t(sys.size());
+  src.z.resize(n);
+  src.m.resize(n);
+  ev.y.resize(n);
+  ev.source_id.resize(n);
+#pragma omp parallel for schedule(static)
+  for (std::int64_t k = 0; k < n; ++k) {
+    src.z[k] = sys.pos[k];
+    src.m[k] = sys.gamma[k] * kOneOverTwoPiI;
+    ev.y[k] = sys.pos[k];
+    ev.source_id[k] = k;
+  }
+  engine.evaluate_into(src, ev, r);
+  std::vector<cplx> v(n);
+#pragma omp parallel for schedule(static)
+  for (std::int64_t k = 0; k < n; ++k) v[k] = std::conj(r.potentials[k]);
+  if (info) *info = r;
   return v;
 }
 
 void euler_step(VortexSystem& sys, const std::vector<cplx>& velocities) {
   if (velocities.size() != sys.size()) throw InvalidInput("euler_step: velocity count mismatch");
-  for (std::size_t k = 0; k < sys.size(); ++k) sys.pos[k] += sys.dt * velocities[k];
+  const std::int64_t n = std::int64_t(sys.size());
+#pragma omp parallel for schedule(static)
+  for (std::int64_t k = 0; k < n; ++k) sys.pos[k] += sys.dt * velocities[k];
 }
 
 }  // namespace fmm::sims
