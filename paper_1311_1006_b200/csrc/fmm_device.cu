@@ -14,6 +14,7 @@
 // reference's (p2p_pairs, m2l_ops, p2m_points, l2p_points); phase times are
 // device event spans.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
 #include <cmath>
@@ -42,6 +43,7 @@ struct DevicePipeline {
   DevBuf z, m, y, sid;
   HostBuf hz, hm, hy, hsid, hres;
   // pyramid
+  DevBuf px_s, py_s, px_e, py_e, lowbase, tstate;  // list positions (fused partition)
   DevBuf keys0, keys1, ids, sx, sy, ex, ey, sxn, syn, exn, eyn, flag_s, flag_e, ind, scan,
       cub_tmp, xmid_s, xmid_e, ymid_s, ymid_e, half_s, half_e, leaf_of, perm, eperm, inv;
   DevBuf soff, eoff;                       // all levels: level l at off_base[l]
@@ -60,6 +62,7 @@ struct DevicePipeline {
   bool tree_valid = false;
   cudaStream_t far = nullptr;
   cudaEvent_t ev[14] = {};
+  cudaEvent_t ev_lvl[18] = {};  // FMMCU_TRACE: pyramid phases
   fmmcu::pinned_vector<uint32_t> h_pt, h_evo, h_so, h_si;  // finest CSR for the work list
   static constexpr int kChunksMax = 64;
   cudaEvent_t ev_res[kChunksMax] = {};
@@ -80,10 +83,13 @@ void destroy_pipeline(DevicePipeline* p) {
   if (p->far) cudaStreamDestroy(p->far);
   for (cudaEvent_t e : p->ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_lvl)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_res)
     if (e) cudaEventDestroy(e);
   DevBuf* bufs[] = {&p->z, &p->m, &p->y, &p->sid, &p->keys0, &p->keys1, &p->ids, &p->sx, &p->sy,
                     &p->ex, &p->ey, &p->sxn, &p->syn, &p->exn, &p->eyn, &p->flag_s, &p->flag_e,
+                    &p->px_s, &p->py_s, &p->px_e, &p->py_e, &p->lowbase, &p->tstate,
                     &p->ind, &p->scan, &p->cub_tmp, &p->xmid_s, &p->xmid_e, &p->ymid_s,
                     &p->ymid_e, &p->half_s, &p->half_e, &p->leaf_of, &p->perm, &p->eperm,
                     &p->inv, &p->soff, &p->eoff, &p->center, &p->hw, &p->hh, &p->radius,
@@ -192,26 +198,110 @@ int sorted_list(fmmcu_ctx* c, DevicePipeline* P, const double2* pts, uint32_t n,
   return sort_pairs(c, P, k0, k1, P->ids.as<uint32_t>(), list, n, 64, s);
 }
 
-// Stable partition of every segment of `list` (offsets off[0..nseg], first
-// high slot mid[seg]) by the per-id flags; result in `out`.
-struct FlagOf {
-  const uint8_t* flag;
-  __host__ __device__ uint32_t operator()(uint32_t id) const { return flag[id]; }
+// One-pass stable segmented partition (decoupled look-back).  Each id's low
+// flag comes from its position in the OTHER sorted list: at an x split the
+// x-sorted list is already split (the lows are the first mid - off slots of
+// every segment), so an id of the y list is low iff posx[id] < mid[seg];
+// the y list is partitioned and the new positions go to posy (and the other
+// way round at a y split).  Replaces flag scatter + scan + scatter with one
+// read of the list.  lowbase[s] = lows in the segments before s.
+constexpr int kPartTB = 256, kPartIPT = 8;
+using PartTileState = cub::ScanTileState<uint32_t>;
+
+__global__ void part_tiles_init_kernel(PartTileState ts, int tiles) { ts.InitializeStatus(tiles); }
+
+struct LowCount {
+  const uint32_t* off;
+  const uint32_t* mid;
+  __host__ __device__ uint32_t operator()(uint32_t s) const { return mid[s] - off[s]; }
 };
 
-// The scan reads the flags through the list on the fly (no gathered copy);
-// the scatter re-reads them (10 MB of flags stay in L2).
-int partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint32_t n,
-              const uint8_t* flag, const uint32_t* off, const uint32_t* mid, uint32_t nseg,
-              uint32_t* out, cudaStream_t s) {
+__global__ void __launch_bounds__(kPartTB)
+    fused_partition_kernel(const uint32_t* __restrict__ in, uint32_t n,
+                           const uint32_t* __restrict__ off, const uint32_t* __restrict__ mid,
+                           uint32_t nseg, const uint32_t* __restrict__ lowbase,
+                           const uint32_t* __restrict__ pos_other, uint32_t* __restrict__ out,
+                           uint32_t* __restrict__ pos_self, PartTileState ts) {
+  using BlockScan = cub::BlockScan<uint32_t, kPartTB>;
+  using Prefix = cub::TilePrefixCallbackOp<uint32_t, cuda::std::plus<uint32_t>, PartTileState>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  __shared__ typename Prefix::TempStorage prefix_tmp;
+  const int tile = blockIdx.x;
+  const uint32_t i0 = uint32_t(tile) * (kPartTB * kPartIPT) + threadIdx.x * kPartIPT;
+  uint32_t id[kPartIPT], sg[kPartIPT];
+  uint32_t lowmask = 0, cnt = 0;
+  if (i0 + kPartIPT <= n) {
+    const uint4 a = *reinterpret_cast<const uint4*>(in + i0);
+    const uint4 b = *reinterpret_cast<const uint4*>(in + i0 + 4);
+    id[0] = a.x, id[1] = a.y, id[2] = a.z, id[3] = a.w;
+    id[4] = b.x, id[5] = b.y, id[6] = b.z, id[7] = b.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < kPartIPT; ++k) id[k] = i0 + k < n ? in[i0 + k] : 0u;
+  }
+  if (i0 < n) {
+    uint32_t g = seg_of(off, nseg, i0);
+#pragma unroll
+    for (int k = 0; k < kPartIPT; ++k) {
+      const uint32_t i = i0 + k;
+      if (i < n) {
+        while (off[g + 1] <= i) ++g;
+        sg[k] = g;
+        const uint32_t lo = pos_other[id[k]] < mid[g] ? 1u : 0u;
+        lowmask |= lo << k;
+        cnt += lo;
+      }
+    }
+  }
+  uint32_t excl;
+  if (tile == 0) {
+    uint32_t agg;
+    BlockScan(scan_tmp).ExclusiveSum(cnt, excl, agg);
+    if (threadIdx.x == 0) ts.SetInclusive(0, agg);
+  } else {
+    Prefix op(ts, prefix_tmp, cuda::std::plus<uint32_t>{}, tile);
+    BlockScan(scan_tmp).ExclusiveSum(cnt, excl, op);
+  }
+#pragma unroll
+  for (int k = 0; k < kPartIPT; ++k) {
+    const uint32_t i = i0 + k;
+    if (i >= n) break;
+    const uint32_t g = sg[k], b = off[g];
+    const uint32_t rl = excl - lowbase[g];  // lows of this segment before i
+    const bool lo = (lowmask >> k) & 1u;
+    const uint32_t dst = lo ? b + rl : mid[g] + (i - b - rl);
+    out[dst] = id[k];
+    pos_self[id[k]] = dst;
+    excl += lo ? 1u : 0u;
+  }
+}
+
+// list -> positions: pos[list[i]] = i
+__global__ void list_positions_kernel(const uint32_t* __restrict__ list, uint32_t n,
+                                      uint32_t* __restrict__ pos) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) pos[list[i]] = i;
+}
+
+int fused_partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint32_t n,
+                    const uint32_t* off, const uint32_t* mid, uint32_t nseg,
+                    const uint32_t* pos_other, uint32_t* out, uint32_t* pos_self, cudaStream_t s) {
   if (!n) return FMMCU_OK;
-  uint32_t* scan = P->scan.as<uint32_t>();
-  auto it = thrust::make_transform_iterator(list, FlagOf{flag});
+  uint32_t* lowbase = P->lowbase.as<uint32_t>();
+  auto cnt = thrust::make_transform_iterator(thrust::counting_iterator<uint32_t>(0), LowCount{off, mid});
   size_t bytes = 0;
-  CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, scan, int64_t(n), s));
+  CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, lowbase, int64_t(nseg), s));
   CU_TRY(c, P->cub_tmp.ensure(bytes));
-  CU_TRY(c, cub::DeviceScan::ExclusiveSum(P->cub_tmp.p, bytes, it, scan, int64_t(n), s));
-  partition_flags_kernel<<<blocks(n), TB, 0, s>>>(list, n, off, mid, nseg, flag, scan, out);
+  CU_TRY(c, cub::DeviceScan::ExclusiveSum(P->cub_tmp.p, bytes, cnt, lowbase, int64_t(nseg), s));
+  const int tiles = int((uint64_t(n) + kPartTB * kPartIPT - 1) / (kPartTB * kPartIPT));
+  size_t tbytes = 0;
+  CU_TRY(c, PartTileState::AllocationSize(tiles, tbytes));
+  CU_TRY(c, P->tstate.ensure(tbytes));
+  PartTileState ts;
+  CU_TRY(c, ts.Init(tiles, P->tstate.p, tbytes));
+  part_tiles_init_kernel<<<(tiles + 32 + 255) / 256, 256, 0, s>>>(ts, tiles);
+  fused_partition_kernel<<<tiles, kPartTB, 0, s>>>(list, n, off, mid, nseg, lowbase, pos_other,
+                                                   out, pos_self, ts);
   return FMMCU_OK;
 }
 
@@ -241,8 +331,8 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   for (DevBuf* b : {&P->ex, &P->ey, &P->exn, &P->eyn, &P->eperm})
     CU_TRY(c, b->ensure(uint64_t(std::max(M, 1u)) * 4));
   CU_TRY(c, P->leaf_of.ensure(nmax * 4));
-  CU_TRY(c, P->flag_s.ensure(std::max(N, 1u)));
-  CU_TRY(c, P->flag_e.ensure(std::max(M, 1u)));
+  for (DevBuf* b : {&P->px_s, &P->py_s}) CU_TRY(c, b->ensure(uint64_t(std::max(N, 1u)) * 4));
+  for (DevBuf* b : {&P->px_e, &P->py_e}) CU_TRY(c, b->ensure(uint64_t(std::max(M, 1u)) * 4));
   CU_TRY(c, P->ind.ensure((nmax + 1) * 4));
   CU_TRY(c, P->scan.ensure((nmax + 1) * 4));
   CU_TRY(c, P->soff.ensure(no * 4));
@@ -255,6 +345,7 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   for (DevBuf* b : {&P->xmid_s, &P->xmid_e}) CU_TRY(c, b->ensure(np_max * 4));
   for (DevBuf* b : {&P->ymid_s, &P->ymid_e}) CU_TRY(c, b->ensure(2 * np_max * 4));
   for (DevBuf* b : {&P->half_s, &P->half_e}) CU_TRY(c, b->ensure((2 * np_max + 1) * 4));
+  CU_TRY(c, P->lowbase.ensure((2 * np_max + 1) * 4));
   (void)top;
 
   uint32_t* SX = P->sx.as<uint32_t>();
@@ -266,6 +357,7 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   uint32_t* EXn = P->exn.as<uint32_t>();
   uint32_t* EYn = P->eyn.as<uint32_t>();
   if (int rc = sorted_list(c, P, zp, N, 0, SX, s)) return rc;
+  if (c->trace) cudaEventRecord(P->ev_lvl[0], s);
   if (int rc = sorted_list(c, P, zp, N, 1, SY, s)) return rc;
   if (P->self_eval) {  // evals are the sources: same sorted lists
     CU_TRY(c, cudaMemcpyAsync(EX, SX, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
@@ -309,8 +401,18 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   uint32_t* ymid_e = P->ymid_e.as<uint32_t>();
   uint32_t* half_s = P->half_s.as<uint32_t>();
   uint32_t* half_e = P->half_e.as<uint32_t>();
-  uint8_t* fs = P->flag_s.as<uint8_t>();
-  uint8_t* fe = P->flag_e.as<uint8_t>();
+  uint32_t* pxs = P->px_s.as<uint32_t>();
+  uint32_t* pys = P->py_s.as<uint32_t>();
+  uint32_t* pxe = P->px_e.as<uint32_t>();
+  uint32_t* pye = P->py_e.as<uint32_t>();
+  if (N) {
+    list_positions_kernel<<<blocks(N), TB, 0, s>>>(SX, N, pxs);
+    list_positions_kernel<<<blocks(N), TB, 0, s>>>(SY, N, pys);
+  }
+  if (M && !alias) {
+    list_positions_kernel<<<blocks(M), TB, 0, s>>>(EX, M, pxe);
+    list_positions_kernel<<<blocks(M), TB, 0, s>>>(EY, M, pye);
+  }
   // Self-evaluation: the evals are the sources (same points, same ids), so
   // while no split value is tied (the count of coords <= split equals the
   // median rank in every segment) the eval lists and offsets ARE the source
@@ -345,11 +447,9 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     a.emid = xmid_e;
     a.differ = same ? differ : nullptr;
     split_kernel<<<blocks(np), TB, 0, s>>>(a);
-    if (N) low_flags_kernel<<<blocks(N), TB, 0, s>>>(SX, N, ps, xmid_s, np, fs);
-    if (M && !same) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EX, M, pe, xmid_e, np, fe);
-    if (int rc = partition(c, P, SY, N, fs, ps, xmid_s, np, SYn, s)) return rc;
+    if (int rc = fused_partition(c, P, SY, N, ps, xmid_s, np, pxs, SYn, pys, s)) return rc;
     if (!same)
-      if (int rc = partition(c, P, EY, M, fe, pe, xmid_e, np, EYn, s)) return rc;
+      if (int rc = fused_partition(c, P, EY, M, pe, xmid_e, np, pxe, EYn, pye, s)) return rc;
     std::swap(SY, SYn);
     if (!same) std::swap(EY, EYn);
     child_offsets_kernel<<<blocks(np), TB, 0, s>>>(ps, xmid_s, nullptr, np, half_s, nullptr);
@@ -367,11 +467,10 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     a.emid = ymid_e;
     a.differ = same ? differ : nullptr;
     split_kernel<<<blocks(2 * np), TB, 0, s>>>(a);
-    if (N) low_flags_kernel<<<blocks(N), TB, 0, s>>>(SY, N, half_s, ymid_s, 2 * np, fs);
-    if (M && !same) low_flags_kernel<<<blocks(M), TB, 0, s>>>(EY, M, half_e, ymid_e, 2 * np, fe);
-    if (int rc = partition(c, P, SX, N, fs, half_s, ymid_s, 2 * np, SXn, s)) return rc;
+    if (int rc = fused_partition(c, P, SX, N, half_s, ymid_s, 2 * np, pys, SXn, pxs, s)) return rc;
     if (!same)
-      if (int rc = partition(c, P, EX, M, fe, half_e, ymid_e, 2 * np, EXn, s)) return rc;
+      if (int rc = fused_partition(c, P, EX, M, half_e, ymid_e, 2 * np, pye, EXn, pxe, s))
+        return rc;
     std::swap(SX, SXn);
     if (!same) std::swap(EX, EXn);
     child_offsets_kernel<<<blocks(np), TB, 0, s>>>(ps, xmid_s, ymid_s, np, nullptr,
@@ -395,6 +494,7 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     } else {
       geometry(l);
     }
+    if (c->trace && l < 16) cudaEventRecord(P->ev_lvl[l], s);
   }
   if (same) {  // no tie anywhere: eval order = source order
     EX = SX;
@@ -430,7 +530,23 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
 
 int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_t s) {
   (void)theta;
+  if (c->trace) cudaEventRecord(P->ev_lvl[17], s);
   if (int rc = build_pyramid_pass(c, P, s, P->self_eval)) return rc;
+  if (c->trace) {
+    cudaEventRecord(P->ev_lvl[16], s);
+    cudaEventSynchronize(P->ev_lvl[16]);
+    float a = 0;
+    cudaEventElapsedTime(&a, P->ev_lvl[17], P->ev_lvl[0]);
+    std::fprintf(stderr, "[fmmcu] pyramid: x sort %.3f ms, levels:", a);
+    cudaEvent_t prev = P->ev_lvl[0];
+    for (int l = 1; l < P->L && l < 16; ++l) {
+      cudaEventElapsedTime(&a, prev, P->ev_lvl[l]);
+      std::fprintf(stderr, " %.3f", a);
+      prev = P->ev_lvl[l];
+    }
+    cudaEventElapsedTime(&a, prev, P->ev_lvl[16]);
+    std::fprintf(stderr, ", leaf order %.3f ms\n", a);
+  }
   if (!P->self_eval) return FMMCU_OK;
   CU_TRY(c, P->h_flag.ensure(16));
   CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.p, 4, cudaMemcpyDeviceToHost, s));
@@ -665,6 +781,7 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
     c->pipe = new DevicePipeline();
     CU_TRY(c, cudaStreamCreateWithFlags(&c->pipe->far, cudaStreamNonBlocking));
     for (cudaEvent_t& e : c->pipe->ev) CU_TRY(c, cudaEventCreate(&e));
+    for (cudaEvent_t& e : c->pipe->ev_lvl) CU_TRY(c, cudaEventCreate(&e));
     for (cudaEvent_t& e : c->pipe->ev_res)
       CU_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
   }
