@@ -972,7 +972,7 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // Measured alternatives: the work list on a helper thread starves behind
   // the OpenMP team; all chunks first makes the work list upload wait for
   // the whole 320 MB (13.2 vs 10.4 ms per 10M step).
-  constexpr int kPre = 3;
+  constexpr int kPre = 2;
   const int pre = direct_in ? std::min(K, kPre) : 0;
   auto dma = [&](int64_t c0, int64_t c1) -> int {
     if (c1 <= c0) return FMMCU_OK;
@@ -990,6 +990,10 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   if (int rc = build_worklist(c, j)) return rc;
   tr.mark("worklist");
   if (int rc = stage_csr(c, j, false)) return rc;
+  // the remaining chunks queue behind the CSR and work list: on their own
+  // stream the copy engine would serve them first and starve the kernels
+  CU_TRY(c, cudaEventRecord(c->ev_staged, s));
+  CU_TRY(c, cudaStreamWaitEvent(h, c->ev_staged, 0));
   h2d += c->h2d_bytes - uint64_t(ns) * 32 - (c->self_layout ? 0 : uint64_t(ne) * 20);
   const P2PItem* items_dev = c->d_items.as<P2PItem>();
   const P2PFinal* fins_dev = c->d_fin.as<P2PFinal>();
@@ -999,6 +1003,10 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // self layout per chunk requires eval slot e == source slot e
   const bool maybe_self = j->eval_sid && ne == ns && ns > 0 &&
                           std::memcmp(j->ev_off, j->pt_off, size_t(nl + 1) * 4) == 0;
+  // the per-chunk self check reads 44 B per point, which paces the chunks at
+  // host memory speed; a caller passing one array for both positions saves
+  // the 32 B position comparison
+  const bool y_is_z = j->eval_y == j->src_z;
   bool all_self = maybe_self;
   // eval arrays of slots [e0, e1) on the host (non-self chunks / layouts)
   bool inv_ready = false;
@@ -1095,7 +1103,10 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     if (direct_in) {
       if (k >= pre)
         if (int rc = dma(c0, c1)) return rc;
-      if (maybe_self) {
+      if (maybe_self && y_is_z) {  // the positions are the same array: ids only
+#pragma omp parallel for schedule(static) reduction(&& : same)
+        for (int64_t i = c0; i < c1; ++i) same = same && j->eval_sid[i] == int64_t(j->perm[i]);
+      } else if (maybe_self) {
 #pragma omp parallel for schedule(static) reduction(&& : same)
         for (int64_t i = c0; i < c1; ++i)
           same = same && j->eval_sid[i] == int64_t(j->perm[i]) &&
@@ -1293,6 +1304,8 @@ int fmmcu_create(fmmcu_ctx** out, int device) {
     return fail(e);
   if ((e = cudaEventCreateWithFlags(&c->ev_evals, cudaEventDisableTiming)) != cudaSuccess)
     return fail(e);
+  if ((e = cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming)) != cudaSuccess)
+    return fail(e);
   for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
     if ((e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDefault)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_group[i], cudaEventDefault)) != cudaSuccess)
@@ -1349,6 +1362,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamDestroy(c->d2h_stream);
     cudaStreamDestroy(c->h2d_stream);
     if (c->ev_evals) cudaEventDestroy(c->ev_evals);
+    if (c->ev_staged) cudaEventDestroy(c->ev_staged);
     for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
       if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
     for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)

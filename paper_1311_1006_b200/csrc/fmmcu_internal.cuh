@@ -153,6 +153,7 @@ struct fmmcu_ctx {
   cudaEvent_t ev_chunk[kMaxChunks] = {}, ev_group[kMaxChunks] = {};
   int n_groups = 0;
   cudaEvent_t ev_evals = nullptr;  // evals uploaded (overlapped launch, non-self layouts)
+  cudaEvent_t ev_staged = nullptr;  // CSR + work list uploaded (overlapped launch)
   int group_k = 0;                      // > 0: build_worklist groups leaves by need chunk
   std::vector<uint32_t> chunk_leaf;     // [group_k + 1] leaf boundaries of the upload chunks
   std::vector<uint32_t> grp_pos;        // [group_k + 1] first position of each group

@@ -256,6 +256,36 @@ def test_page_locked_inputs_take_the_dma_path(ctx):
         assert bitwise(got, want)
 
 
+def test_one_array_for_both_positions(ctx):
+    """Self-evaluation with page-locked inputs and one array passed as both
+    src_z and eval_y: the per-chunk self check then reads only the ids.  The
+    result is bitwise the separate-array result; with ids that do not match
+    the sources (a shuffled sid) the chunks fall back to uploaded evals and
+    still match the separate-array launch."""
+    t, args = _tree_case(0, 1_200_000, 8, 23, self_eval=True)
+    zp = np.ascontiguousarray(args[5]).copy()
+    mp = np.ascontiguousarray(args[6]).copy()
+    for a in (zp, mp):
+        ctx.host_register(a)
+    try:
+        for shuffle in (False, True):
+            a2 = list(args)
+            a2[5], a2[6] = zp, mp
+            if shuffle:
+                sid = np.asarray(a2[8]).copy()
+                sid[:1000] = np.roll(sid[:1000], 1)
+                a2[8] = sid
+            a2[7] = zp.copy()
+            want, pw, _ = _run(ctx, *a2)
+            a2[7] = zp  # the same array for both positions
+            got, pg, _ = _run(ctx, *a2)
+            assert pg == pw
+            assert bitwise(got, want)
+    finally:
+        for a in (zp, mp):
+            ctx.host_unregister(a)
+
+
 @pytest.mark.parametrize("case", [(0, 200_000, 7, 31, 0), (0, 150_000, 7, 32, 1),
                                   (2, 200_000, 7, 33, 0), (3, 60_000, 6, 34, 2)])
 def test_symmetric_kernel_vs_oracle(ctx, case):
