@@ -35,6 +35,7 @@ struct DevBuf {
     size_t want = std::max<size_t>(bytes, 256);
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) cap = want;
+    if (e == cudaSuccess && std::getenv("FMMCU_DEBUG_POISON")) e = cudaMemset(p, 0xFF, want);
     return e;
   }
   void release() {
