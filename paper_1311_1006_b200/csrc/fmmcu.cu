@@ -1042,8 +1042,6 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     h2d += uint64_t(ne) * 20;
   }
 
-  CU_TRY(c, cudaEventRecord(c->ev_staged, s));
-  for (cudaStream_t gs : c->grp_stream) CU_TRY(c, cudaStreamWaitEvent(gs, c->ev_staged, 0));
   std::vector<char> chunk_self(K, 0);
   int launched = 0;
   int nk = 0;
@@ -1078,32 +1076,23 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       p2p_evrec_kernel<<<(l1 - l0 + 7) / 8, 256, 0, s>>>(a, l0, l1, c->d_evr.as<double4>());
       ++nk;
     }
-    // The group's P2P kernels alternate between two streams behind the
-    // chunk preparation on s: group k+1 starts filling SMs while group k's
-    // last items drain (each group has its own scheduler counter).  They read
-    // only sources of chunks <= k, all packed on s before ev_prep[k].
-    CU_TRY(c, cudaEventRecord(c->ev_prep[k], s));
-    cudaStream_t gs = c->grp_stream[k & 1];
-    CU_TRY(c, cudaStreamWaitEvent(gs, c->ev_prep[k], 0));
     const uint32_t p0 = c->grp_pos[k], p1 = c->grp_pos[k + 1];
     const uint32_t i0 = c->item_first[p0], i1 = c->item_first[p1];
     if (i1 > i0) {
-      unsigned int* counter = c->d_counter.as<unsigned int>() + (k & 1);
-      CU_TRY(c, cudaMemsetAsync(counter, 0, 4, gs));
+      CU_TRY(c, cudaMemsetAsync(c->d_counter.p, 0, 8, s));
       P2PArgs aa = a;
       aa.items = items_dev + i0;
       aa.n_items = i1 - i0;
-      aa.next_item = counter;
-      dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, gs, c->warp_e);
+      dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s, c->warp_e);
       ++nk;
     }
     const uint32_t f0 = c->fin_first[p0], f1 = c->fin_first[p1];
     if (f1 > f0) {
-      p2p_finalize_kernel<<<f1 - f0, 128, 0, gs>>>(fins_dev + f0, f1 - f0,
-                                                    c->d_partial.as<double2>(), c->out_dev);
+      p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(fins_dev + f0, f1 - f0,
+                                                   c->d_partial.as<double2>(), c->out_dev);
       ++nk;
     }
-    CU_TRY(c, cudaEventRecord(c->ev_group[k], gs));
+    CU_TRY(c, cudaEventRecord(c->ev_group[k], s));
     CU_TRY(c, cudaGetLastError());
     return FMMCU_OK;
   };
@@ -1160,8 +1149,6 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   }
   tr.mark("pack+h2d (overlapped)");
   c->self_layout = all_self;
-  for (int g = std::max(0, K - 2); g < K; ++g)  // the last group of each group stream
-    CU_TRY(c, cudaStreamWaitEvent(s, c->ev_group[g], 0));
   CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaEventRecord(c->ev_end, s));
   tr.mark("enqueue done");
@@ -1319,10 +1306,6 @@ int fmmcu_create(fmmcu_ctx** out, int device) {
     return fail(e);
   if ((e = cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming)) != cudaSuccess)
     return fail(e);
-  for (cudaStream_t& gs : c->grp_stream)
-    if ((e = cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
-  for (cudaEvent_t& ep : c->ev_prep)
-    if ((e = cudaEventCreateWithFlags(&ep, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
   for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
     if ((e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDefault)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_group[i], cudaEventDefault)) != cudaSuccess)
@@ -1380,10 +1363,6 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamDestroy(c->h2d_stream);
     if (c->ev_evals) cudaEventDestroy(c->ev_evals);
     if (c->ev_staged) cudaEventDestroy(c->ev_staged);
-    for (cudaStream_t gs : c->grp_stream)
-      if (gs) cudaStreamSynchronize(gs), cudaStreamDestroy(gs);
-    for (cudaEvent_t ep : c->ev_prep)
-      if (ep) cudaEventDestroy(ep);
     for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
       if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
     for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)

@@ -155,8 +155,6 @@ struct fmmcu_ctx {
   int n_groups = 0;
   cudaEvent_t ev_evals = nullptr;  // evals uploaded (overlapped launch, non-self layouts)
   cudaEvent_t ev_staged = nullptr;  // CSR + work list uploaded (overlapped launch)
-  cudaStream_t grp_stream[2] = {};  // overlapped launch: P2P kernels of even / odd groups
-  cudaEvent_t ev_prep[kMaxChunks] = {};  // chunk k packed + eval records written (on stream)
   int group_k = 0;                      // > 0: build_worklist groups leaves by need chunk
   std::vector<uint32_t> chunk_leaf;     // [group_k + 1] leaf boundaries of the upload chunks
   std::vector<uint32_t> grp_pos;        // [group_k + 1] first position of each group
