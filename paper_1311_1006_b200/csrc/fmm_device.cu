@@ -578,6 +578,64 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
   CU_TRY(c, P->h_count.ensure(16));
   uint32_t* cs = P->cnt_s.as<uint32_t>();
   uint32_t* cw = P->cnt_w.as<uint32_t>();
+  // Speculative pass: every level's lists are filled into buffers sized by
+  // a guess (12 strong / 36 weak entries per box, or what an earlier build
+  // needed), with no host read between levels; one read at the end gets all
+  // counts.  A level that does not fit is flagged, and the build is redone
+  // with a count read per level (the exact sizes).
+  if (!std::getenv("FMMCU_CONN_SYNC")) {
+    std::vector<uint32_t> scap(L, 0), wcap(L, 0);
+    // FMMCU_CONN_TIGHT (tests): guess one entry per box so the redo path runs
+    const bool tight = std::getenv("FMMCU_CONN_TIGHT") != nullptr;
+    for (int l = 1; l < L; ++l) {
+      const uint32_t nbox = uint32_t(pow4(l));
+      LevelConnDev& lc = P->conn[l];
+      CU_TRY(c, lc.s_off.ensure((nbox + 1) * 4));
+      CU_TRY(c, lc.w_off.ensure((nbox + 1) * 4));
+      CU_TRY(c, lc.s_idx.ensure(uint64_t(nbox) * 12 * 4));
+      CU_TRY(c, lc.w_idx.ensure(uint64_t(nbox) * 36 * 4));
+      scap[l] = tight ? nbox : uint32_t(std::min<uint64_t>(lc.s_idx.cap / 4, 0xFFFFFFFFull));
+      wcap[l] = tight ? nbox : uint32_t(std::min<uint64_t>(lc.w_idx.cap / 4, 0xFFFFFFFFull));
+    }
+    CU_TRY(c, P->flag.ensure(8));
+    CU_TRY(c, P->h_count.ensure(uint64_t(2 * L + 2) * 4));
+    int* ovf = P->flag.as<int>();
+    CU_TRY(c, cudaMemsetAsync(ovf, 0, 4, s));
+    uint32_t* hc = P->h_count.as<uint32_t>();
+    for (int l = 1; l < L; ++l) {
+      const uint32_t nbox = uint32_t(pow4(l));
+      LevelConnDev& pc = P->conn[l - 1];
+      LevelConnDev& lc = P->conn[l];
+      const double2* cen = P->center.as<double2>() + P->box_base[l];
+      const double* rad = P->radius.as<double>() + P->box_base[l];
+      CU_TRY(c, cudaMemsetAsync(cs + nbox, 0, 4, s));
+      CU_TRY(c, cudaMemsetAsync(cw + nbox, 0, 4, s));
+      classify_kernel<false><<<blocks(nbox), TB, 0, s>>>(
+          pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, cs, cw, nullptr,
+          nullptr, nullptr, nullptr, 0xFFFFFFFFu, 0xFFFFFFFFu, ovf);
+      if (int rc = scan_excl(c, P, cs, lc.s_off.as<uint32_t>(), nbox + 1, s)) return rc;
+      if (int rc = scan_excl(c, P, cw, lc.w_off.as<uint32_t>(), nbox + 1, s)) return rc;
+      classify_kernel<true><<<blocks(nbox), TB, 0, s>>>(
+          pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, nullptr, nullptr,
+          lc.s_off.as<uint32_t>(), lc.w_off.as<uint32_t>(), lc.s_idx.as<uint32_t>(),
+          lc.w_idx.as<uint32_t>(), scap[l], wcap[l], ovf);
+      CU_TRY(c, cudaMemcpyAsync(hc + 2 * l, lc.s_off.as<uint32_t>() + nbox, 4,
+                                cudaMemcpyDeviceToHost, s));
+      CU_TRY(c, cudaMemcpyAsync(hc + 2 * l + 1, lc.w_off.as<uint32_t>() + nbox, 4,
+                                cudaMemcpyDeviceToHost, s));
+      c->launches += 2;
+    }
+    CU_TRY(c, cudaMemcpyAsync(hc, ovf, 4, cudaMemcpyDeviceToHost, s));
+    CU_TRY(c, cudaStreamSynchronize(s));
+    if (hc[0] == 0) {
+      for (int l = 1; l < L; ++l) {
+        P->conn[l].s_nnz = hc[2 * l];
+        P->conn[l].w_nnz = hc[2 * l + 1];
+      }
+      CU_TRY(c, cudaGetLastError());
+      return FMMCU_OK;
+    }
+  }
   for (int l = 1; l < L; ++l) {
     const uint32_t nbox = uint32_t(pow4(l));
     LevelConnDev& pc = P->conn[l - 1];

@@ -322,12 +322,21 @@ __global__ void classify_kernel(const uint32_t* __restrict__ ps_off,
                                 const double* __restrict__ r, uint32_t nbox, double theta,
                                 uint32_t* __restrict__ s_cnt, uint32_t* __restrict__ w_cnt,
                                 const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ w_off,
-                                uint32_t* __restrict__ s_idx, uint32_t* __restrict__ w_idx) {
+                                uint32_t* __restrict__ s_idx, uint32_t* __restrict__ w_idx,
+                                uint32_t s_cap = 0xFFFFFFFFu, uint32_t w_cap = 0xFFFFFFFFu,
+                                int* __restrict__ overflow = nullptr) {
   const uint32_t a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= nbox) return;
+  if (overflow && *overflow) return;  // a coarser level did not fit: lists are invalid
   const uint32_t p = a >> 2;
   uint32_t ns = 0, nw = 0;
   uint32_t so = FILL ? s_off[a] : 0, wo = FILL ? w_off[a] : 0;
+  // capacity guard: the lists may be filled into buffers sized by a guess
+  // before the host has read the counts (a miss is flagged and redone)
+  if (FILL && overflow && (uint64_t(s_off[a + 1]) > s_cap || uint64_t(w_off[a + 1]) > w_cap)) {
+    *overflow = 1;
+    return;
+  }
   for (uint32_t q = ps_off[p]; q < ps_off[p + 1]; ++q) {
     const uint32_t pq = ps_idx[q];
     for (uint32_t b = 4 * pq; b < 4 * pq + 4; ++b) {

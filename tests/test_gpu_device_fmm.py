@@ -164,3 +164,22 @@ def test_engine_result_reuse_across_sizes():
         want = fresh.evaluate(s, F.EvalSet.self_of(s)).potentials
         assert np.array_equal(g.view(np.uint64), want.view(np.uint64))
     assert np.array_equal(got[0].view(np.uint64), got[3].view(np.uint64))
+
+
+@pytest.mark.parametrize("env", ["FMMCU_CONN_SYNC", "FMMCU_CONN_TIGHT"])
+def test_connectivity_paths_agree(ctx, env, monkeypatch):
+    """The connectivity is built speculatively (all levels into guessed
+    buffers, one count read at the end).  The per-level-read build
+    (FMMCU_CONN_SYNC) and the overflow redo (FMMCU_CONN_TIGHT: guesses too
+    small, so every build is redone) give bitwise the same lists."""
+    for name, s, e, L, theta in list(_cases())[:4]:
+        e = _evals(s, e)
+        ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=L, theta=theta, p=17)
+        want = ctx.fmm_tree(L, s.size(), e.size())
+        monkeypatch.setenv(env, "1")
+        ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=L, theta=theta, p=17)
+        got = ctx.fmm_tree(L, s.size(), e.size())
+        monkeypatch.delenv(env)
+        for lvl in range(L):
+            for g, w in ((got[4][lvl], want[4][lvl]), (got[5][lvl], want[5][lvl])):
+                assert np.array_equal(g[0], w[0]) and np.array_equal(g[1], w[1]), (name, lvl)
