@@ -193,8 +193,14 @@ typedef struct {
 
 int fmmcu_fmm_evaluate(fmmcu_ctx *ctx, const fmmcu_fmm_job *job, fmmcu_fmm_stats *stats);
 /* The same call split in two: launch returns once the potentials' D2H is
- * enqueued (job->out is not touched); finish waits and writes them to `out`
- * ([2 n_eval] doubles) chunk by chunk as they land. */
+ * enqueued; finish waits and writes them to `out` ([2 n_eval] doubles) chunk
+ * by chunk as they land.  When job->out is page-locked (fmmcu_host_register)
+ * the D2H lands in it directly, so it is written asynchronously after launch
+ * returns and finish only waits (pass the same pointer to finish).  Page-
+ * locked inputs are DMA'd in place.  A job with ids and n_eval == n_src is
+ * built speculatively as self-evaluation; launch verifies the speculation
+ * before it returns and re-runs without it if the evals are not the sources
+ * (results are identical either way). */
 int fmmcu_fmm_launch(fmmcu_ctx *ctx, const fmmcu_fmm_job *job);
 int fmmcu_fmm_finish(fmmcu_ctx *ctx, double *out, fmmcu_fmm_stats *stats);
 /* The device-built pyramid / connectivity of the last fmmcu_fmm_evaluate
