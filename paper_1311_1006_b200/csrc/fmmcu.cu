@@ -972,8 +972,8 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // Measured alternatives: the work list on a helper thread starves behind
   // the OpenMP team; all chunks first makes the work list upload wait for
   // the whole 320 MB (13.2 vs 10.4 ms per 10M step).
-  constexpr int kPre = 2;
-  const int pre = direct_in ? std::min(K, kPre) : 0;
+  static const int kPre = std::getenv("FMMCU_KPRE") ? std::atoi(std::getenv("FMMCU_KPRE")) : 2;
+  const int pre = direct_in ? std::min(K, std::max(0, kPre)) : 0;
   auto dma = [&](int64_t c0, int64_t c1) -> int {
     if (c1 <= c0) return FMMCU_OK;
     CU_TRY(c, cudaMemcpyAsync(c->d_zin.as<double>() + 2 * c0, z + 2 * c0, size_t(c1 - c0) * 16,
