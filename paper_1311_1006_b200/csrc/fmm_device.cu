@@ -14,6 +14,7 @@
 // reference's (p2p_pairs, m2l_ops, p2m_points, l2p_points); phase times are
 // device event spans.
 #include <cub/cub.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
@@ -117,10 +118,6 @@ constexpr uint32_t kResChunks = 16;
 inline uint32_t blocks(uint64_t n) { return uint32_t((n + TB - 1) / TB); }
 inline uint64_t pow4(int l) { return uint64_t(1) << (2 * l); }
 
-__global__ void iota_kernel(uint32_t* __restrict__ v, uint32_t n) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = i;
-}
 
 // M2L lists of one level: targets = boxes with evals (l >= 1), partners =
 // weak entries whose box has sources (engine.cpp:98, :108-113).
@@ -501,27 +498,25 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     EY = SY;
   }
   P->layout_same = same;  // eval slot e is source slot e (self layout)
-  // leaf-internal order = original index order (geometry.cpp:156-161)
+  // leaf-internal order = original index order (geometry.cpp:156-161): the
+  // finest x-list segments hold each leaf's ids, so one segmented sort of the
+  // ids gives the leaf-grouped permutation directly
   const uint32_t nleaf = uint32_t(pow4(L - 1));
-  int bits = 1;
-  while ((uint64_t(1) << bits) < nleaf) ++bits;
-  uint32_t* leaf_of = P->leaf_of.as<uint32_t>();
-  uint32_t* iota = P->ids.as<uint32_t>();
-  if (N) {
-    leaf_of_kernel<<<blocks(N), TB, 0, s>>>(SX, N, soff + P->off_base[L - 1], nleaf, leaf_of);
-    iota_kernel<<<blocks(N), TB, 0, s>>>(iota, N);
-    if (int rc = sort_pairs(c, P, leaf_of, P->keys1.as<uint32_t>(), iota, P->perm.as<uint32_t>(),
-                            N, bits, s))
-      return rc;
-  }
+  auto leaf_order = [&](const uint32_t* list, uint32_t n, const uint32_t* off, uint32_t* out) -> int {
+    size_t bytes = 0;
+    CU_TRY(c, cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, list, out, int64_t(n), int64_t(nleaf),
+                                                 off, off + 1, s));
+    CU_TRY(c, P->cub_tmp.ensure(bytes));
+    CU_TRY(c, cub::DeviceSegmentedSort::SortKeys(P->cub_tmp.p, bytes, list, out, int64_t(n),
+                                                 int64_t(nleaf), off, off + 1, s));
+    return FMMCU_OK;
+  };
+  if (N)
+    if (int rc = leaf_order(SX, N, soff + P->off_base[L - 1], P->perm.as<uint32_t>())) return rc;
   if (M && same) {
     CU_TRY(c, cudaMemcpyAsync(P->eperm.p, P->perm.p, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
   } else if (M) {
-    leaf_of_kernel<<<blocks(M), TB, 0, s>>>(EX, M, eoff + P->off_base[L - 1], nleaf, leaf_of);
-    iota_kernel<<<blocks(M), TB, 0, s>>>(iota, M);
-    if (int rc = sort_pairs(c, P, leaf_of, P->keys1.as<uint32_t>(), iota, P->eperm.as<uint32_t>(),
-                            M, bits, s))
-      return rc;
+    if (int rc = leaf_order(EX, M, eoff + P->off_base[L - 1], P->eperm.as<uint32_t>())) return rc;
   }
   CU_TRY(c, cudaGetLastError());
   c->launches += uint64_t(8 + 14 * (L - 1));
