@@ -49,7 +49,7 @@ class CudaBackend final : public NearFieldBackend {
   struct DeviceEval {
     WorkCounters counters;
     double t_upload = 0, t_tree = 0, t_connect = 0, t_p2m_upward = 0, t_m2l = 0, t_p2p = 0,
-           t_device = 0;
+           t_device = 0, t_far_wait = 0;
   };
   DeviceEval fmm_evaluate(const SourceSet& sources, const EvalSet& evals, int n_levels,
                           double theta, int p, Kernel kernel, const Smoother& smoother,

@@ -189,6 +189,13 @@ typedef struct {
   double t_device;      /* first H2D .. potentials on the host */
   double t_total;       /* host wall time of the call */
   uint64_t h2d_bytes, d2h_bytes;
+  /* the device analogue of the reference's cpu_wait (engine.cpp:312): how
+   * long the far chain (P2M..M2L+L2L, far stream) sat finished before the
+   * near field (P2P, main stream) ended, i.e. max(0, near end - far end) on
+   * the device clock.  > 0 means the near field is the longer branch, which
+   * is exactly what the reference's positive wait tells AT3a
+   * (autotune.cpp:155: more levels). */
+  double t_far_wait;
 } fmmcu_fmm_stats;
 
 int fmmcu_fmm_evaluate(fmmcu_ctx *ctx, const fmmcu_fmm_job *job, fmmcu_fmm_stats *stats);

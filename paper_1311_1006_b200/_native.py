@@ -63,7 +63,7 @@ class FmmStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("p2p_pairs", "m2l_ops", "p2m_points", "l2p_points")] + \
                [(n, C.c_double) for n in ("t_upload", "t_tree", "t_connect", "t_p2m_upward",
                                           "t_m2l", "t_p2p", "t_device", "t_total")] + \
-               [("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+               [("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("t_far_wait", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -39,6 +39,12 @@ struct LevelConnDev {
   uint32_t s_nnz = 0, w_nnz = 0;
 };
 
+// P->flag holds one device word per job, so no stage can see another's
+// stale value whatever the stream order: the pyramid's tied-split flag, the
+// speculative connectivity's capacity overflow and the M2L singular flag.
+constexpr int kFlagTie = 0, kFlagOverflow = 1, kFlagSingular = 2;
+constexpr uint64_t kFlagBytes = 16;
+
 struct DevicePipeline {
   // inputs (original order)
   DevBuf z, m, y, sid;
@@ -419,8 +425,8 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   const bool same = alias;
   int* differ = nullptr;
   if (same) {
-    CU_TRY(c, P->flag.ensure(8));
-    differ = P->flag.as<int>();
+    CU_TRY(c, P->flag.ensure(kFlagBytes));
+    differ = P->flag.as<int>() + kFlagTie;
   }
   if (same) CU_TRY(c, cudaMemsetAsync(differ, 0, 4, s));
   for (int l = 1; l < L; ++l) {
@@ -544,7 +550,7 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
   }
   if (!P->self_eval) return FMMCU_OK;
   CU_TRY(c, P->h_flag.ensure(16));
-  CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.p, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.as<int>() + kFlagTie, 4, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaStreamSynchronize(s));
   if (*P->h_flag.as<int>() == 0) return FMMCU_OK;
   return build_pyramid_pass(c, P, s, false);  // a split was tied: separate eval lists
@@ -592,9 +598,9 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
       scap[l] = tight ? nbox : uint32_t(std::min<uint64_t>(lc.s_idx.cap / 4, 0xFFFFFFFFull));
       wcap[l] = tight ? nbox : uint32_t(std::min<uint64_t>(lc.w_idx.cap / 4, 0xFFFFFFFFull));
     }
-    CU_TRY(c, P->flag.ensure(8));
+    CU_TRY(c, P->flag.ensure(kFlagBytes));
     CU_TRY(c, P->h_count.ensure(uint64_t(2 * L + 2) * 4));
-    int* ovf = P->flag.as<int>();
+    int* ovf = P->flag.as<int>() + kFlagOverflow;
     CU_TRY(c, cudaMemsetAsync(ovf, 0, 4, s));
     uint32_t* hc = P->h_count.as<uint32_t>();
     for (int l = 1; l < L; ++l) {
@@ -665,7 +671,7 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
 }
 
 // ------------------------------------------------------------- far field --
-int far_setup(fmmcu_ctx* c, DevicePipeline* P) {
+int far_setup(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s) {
   const int P1 = P->p + 1;
   // Pascal rows as the reference's table (expansion.cpp:12-26)
   const int brow = 2 * P1 + 4;
@@ -675,7 +681,9 @@ int far_setup(fmmcu_ctx* c, DevicePipeline* P) {
     for (int j = 1; j <= i; ++j) t[size_t(i) * brow + j] = t[size_t(i - 1) * brow + j - 1] + t[size_t(i - 1) * brow + j];
   }
   CU_TRY(c, P->binom.ensure(t.size() * 8));
-  CU_TRY(c, cudaMemcpy(P->binom.p, t.data(), t.size() * 8, cudaMemcpyHostToDevice));
+  // on the launching stream: the far stream orders behind it through ev[4]
+  // (a legacy-stream cudaMemcpy would not order the non-blocking far stream)
+  CU_TRY(c, cudaMemcpyAsync(P->binom.p, t.data(), t.size() * 8, cudaMemcpyHostToDevice, s));
   return FMMCU_OK;
 }
 
@@ -770,8 +778,8 @@ int far_field(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, cudaEvent_t e_up,
   }
   CU_TRY(c, cudaEventRecord(e_up, s));
   CU_TRY(c, P->m2l_sum.ensure(uint64_t(std::max(P->n_targets, 1u)) * P1 * 16));
-  CU_TRY(c, P->flag.ensure(8));
-  CU_TRY(c, cudaMemsetAsync(P->flag.p, 0, 8, s));
+  CU_TRY(c, P->flag.ensure(kFlagBytes));
+  CU_TRY(c, cudaMemsetAsync(P->flag.as<int>() + kFlagSingular, 0, 4, s));
   if (P->n_targets) {
     if (int rc = m2l_table(c, P->p, P->kernel, s)) return rc;
     M2LArgs m{};
@@ -786,7 +794,7 @@ int far_field(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, cudaEvent_t e_up,
     m.n_targets = P->n_targets;
     m.big_w2 = std::pow(10.0, 500.0 / double(P->p + 2));
     m.out = P->m2l_sum.as<double2>();
-    m.singular = P->flag.as<int>();
+    m.singular = P->flag.as<int>() + kFlagSingular;
     CU_TRY(c, m2l_set_const_table(c->m_table.as<double>(), P->p + 1, s));
     launch_m2l(m, s);
   }
@@ -1043,7 +1051,7 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   CU_TRY(c, cudaEventRecord(ev[3], s));  // partition done
 
   // ---- far field on its own stream (overlaps the host work list + P2P) ----
-  if (int rc = far_setup(c, P)) return rc;
+  if (int rc = far_setup(c, P, s)) return rc;
   if (int rc = m2l_lists(c, P, s)) return rc;
   CU_TRY(c, cudaEventRecord(ev[4], s));
   CU_TRY(c, cudaStreamWaitEvent(P->far, ev[4], 0));
@@ -1097,7 +1105,7 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
     c->launches += 1;
   }
   CU_TRY(c, P->h_flag.ensure(16));
-  CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.p, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaMemcpyAsync(P->h_flag.p, P->flag.as<int>() + kFlagSingular, 4, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, s));
   // D2H straight into the caller's out when it is page-locked; else in chunks
   // so that fmmcu_fmm_finish copies chunk i out of the pinned staging while
@@ -1205,6 +1213,7 @@ int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {
     st->t_m2l = 1e-3 * span_ms(ev[6], ev[7]);
     st->t_p2p = 1e-3 * span_ms(ev[8], ev[9]);
     st->t_device = 1e-3 * span_ms(ev[0], ev[10]);
+    st->t_far_wait = std::max(0.0, 1e-3 * (span_ms(ev[0], ev[9]) - span_ms(ev[0], ev[7])));
     st->t_total = std::chrono::duration<double>(Clock::now() - P->t_host0).count();
     st->h2d_bytes = P->h2d;
     st->d2h_bytes = uint64_t(M) * 16;

@@ -1234,7 +1234,6 @@ __global__ void dfma_peak_kernel(double* sink, int iters, double seed) {
 // binomial table T[k][l] of the M2L kernel (Pascal recurrence in doubles,
 // as the reference's table, expansion.cpp:12-26)
 int m2l_table(fmmcu_ctx* c, int p, int kernel, cudaStream_t stream) {
-  (void)stream;
   if (c->table_p == p && c->table_kernel == kernel) return FMMCU_OK;
   const int P1 = p + 1;
   const int rows = 2 * P1 + 2;
@@ -1251,7 +1250,12 @@ int m2l_table(fmmcu_ctx* c, int p, int kernel, cudaStream_t stream) {
       else if (k >= 1) T[size_t(k) * P1 + l] = pas[size_t(l + k - 1) * rows + (k - 1)];
     }
   CU_TRY(c, c->m_table.ensure(T.size() * 8));
-  CU_TRY(c, cudaMemcpy(c->m_table.p, T.data(), T.size() * 8, cudaMemcpyHostToDevice));
+  // Stream-ordered upload on the consuming stream. A legacy-stream cudaMemcpy
+  // from pageable memory may return before the DMA lands, and the consumers
+  // (cudaMemcpyToSymbolAsync into c_m2l_table, the M2L kernels) run on
+  // non-blocking streams that do not order behind the legacy stream. The
+  // pageable source is staged before cudaMemcpyAsync returns, so T may die.
+  CU_TRY(c, cudaMemcpyAsync(c->m_table.p, T.data(), T.size() * 8, cudaMemcpyHostToDevice, stream));
   c->table_p = p;
   c->table_kernel = kernel;
   return FMMCU_OK;

@@ -168,6 +168,7 @@ CudaBackend::DeviceEval CudaBackend::fmm_evaluate(const SourceSet& sources, cons
   d.t_m2l = st.t_m2l;
   d.t_p2p = st.t_p2p;
   d.t_device = st.t_device;
+  d.t_far_wait = st.t_far_wait;
   return d;
 }
 

@@ -355,7 +355,12 @@ void FmmEngine::evaluate_into(const SourceSet& sources, const EvalSet& evals, Ev
     T.t_total = since(t_start);
     T.t_q = T.t_partition + T.t_p2m + T.t_upward +
             std::max(0.0, d.t_device - T.t_partition - std::max(T.t_p2p, T.t_p2m + T.t_m2l));
-    T.cpu_wait = 0.0;
+    // The reference's wait signal (engine.cpp:312) is the time the far field
+    // spent waiting on the near field. Here both branches run on the device,
+    // so it is the far stream's idle tail before the P2P ends (device
+    // events): positive when the near field is longer, zero otherwise, the
+    // sign AT3a steers the level count by (autotune.cpp:155).
+    T.cpu_wait = d.t_far_wait;
     if (observer_) observer_(*this, res);
     return;
   }

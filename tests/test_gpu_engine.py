@@ -135,3 +135,60 @@ def test_engine_device_pipeline_requires_cuda_backend():
     with pytest.raises(F.InvalidParameter):
         F.FmmEngine(F.FmmConfig(n_levels=3, backend="pool", device_pipeline=True)).evaluate(
             s, F.EvalSet.self_of(s))
+
+
+def test_m2l_table_reupload_across_fresh_engines(golden_trees):
+    """the M2L binomial table and the far-field Pascal rows
+    are uploaded on the consuming stream.  Fresh engines alternating theta
+    (hence p: 0.3 -> p=25, 0.5 -> 17, 0.7 -> 39 by PRule::table) and kernel,
+    in a shuffled order, must each match the pool engine on the same input."""
+    rng = np.random.default_rng(7)
+    items = list(golden_trees.items())
+    runs = []
+    for rep in range(3):
+        for name, d in items:
+            for theta in (0.3, 0.5, 0.7):
+                runs.append((name, theta, bool(rep % 2)))
+    rng.shuffle(runs)
+    refs = {}
+    for name, theta, pipe in runs[:40]:
+        d = golden_trees[name]
+        s, e = _sets(d)
+        base = dict(theta=theta, n_levels=int(d["n_levels"]), worker_threads=4)
+        key = (name, theta)
+        if key not in refs:
+            refs[key] = F.FmmEngine(F.FmmConfig(backend="pool", **base)).evaluate(s, e)
+        ref = refs[key]
+        extra = dict(device_pipeline=True) if pipe else dict(m2l_on_device=True)
+        got = F.FmmEngine(F.FmmConfig(backend="cuda", **extra, **base)).evaluate(s, e)
+        assert got.counters == ref.counters, (name, theta, pipe)
+        err = normwise(F._c2(got.potentials), F._c2(ref.potentials))
+        assert err <= 1e-12, (name, theta, pipe, err)
+
+
+def test_device_pipeline_wait_signal_sign():
+    """The device pipeline reports the reference's wait signal (engine.cpp:312)
+    from device events: the far chain's idle tail before the P2P ends.  A
+    shallow tree (thousands of points per leaf) is near-field bound -> wait
+    > 0; a very deep one (< 1 point per leaf) is far-field bound -> wait 0."""
+    s = F.make_distribution("uniform", 400_000, 9)
+    e = F.EvalSet.self_of(s)
+    shallow = F.FmmEngine(F.FmmConfig(n_levels=4, backend="cuda", device_pipeline=True))
+    deep = F.FmmEngine(F.FmmConfig(n_levels=10, backend="cuda", device_pipeline=True))
+    for _ in range(2):  # second call: warm allocations
+        ws = shallow.evaluate(s, e).timings
+        wd = deep.evaluate(s, e).timings
+    assert ws["cpu_wait"] > 0.0, ws
+    assert wd["cpu_wait"] == 0.0, wd
+    assert ws["cpu_wait"] <= ws["t_total"]
+
+
+def test_at3a_moves_levels_with_device_wait_signal():
+    """AT3a (autotune.cpp:155) steers n_levels by the wait sign.  Starting far
+    too shallow for 60k vortices (~3750 per leaf), the device pipeline's wait
+    is positive, so AT3a must deepen the tree (the r1 hard-coded zero walked
+    it the other way)."""
+    cfg = F.FmmConfig(n_levels=3, p_rule="formula", backend="cuda", device_pipeline=True)
+    tr, _ = F.vortex_run(60_000, 8.0, 25, cfg, tuner="at3a")
+    assert (tr[:12, 4] > 0).all()  # near-bound: positive wait
+    assert tr[-1, 6] > 3, tr[:, 6]

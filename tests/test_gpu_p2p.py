@@ -317,14 +317,21 @@ def test_symmetric_kernel_vs_oracle(ctx, case):
     part = ctx.copy_out(len(want))
     e0, e1 = int(args[1][a]), int(args[1][b])
     assert normwise(part[e0:e1], want[e0:e1]) <= TOL_FP64
-    # a symmetric list staged for [a, b) refuses another range; an ordinary
-    # one (clustered inputs exceed 32 entries per leaf) may run it
-    try:
-        ctx.run_staged(0, nl)
-    except N.FmmcuError:
-        pass
+    # a symmetric list staged for [a, b) must refuse another range (its
+    # contribution slots only cover pairs inside [a, b)); an ordinary list
+    # (clustered inputs exceed 32 entries per leaf) runs any range exactly
+    sym, _ = ctx.kernel_info()
+    if sym:
+        with pytest.raises(N.FmmcuError) as ei:
+            ctx.run_staged(0, nl)
+        assert ei.value.code == 6  # FMMCU_ESTATE
     else:
+        ctx.run_staged(0, nl)
+        assert ctx.pairs() == wpairs
         assert normwise(ctx.copy_out(len(want)), want) <= TOL_FP64
+    # uniform inputs (<= 32 strong entries per leaf) always take the mutual kernel
+    if kind == 0:
+        assert sym
 
 
 def test_invalid_jobs_fail_loudly(ctx):
