@@ -50,8 +50,7 @@ def parse():
     ap.add_argument("--theta", type=float, default=0.5)
     ap.add_argument("--seed", type=int, default=4)
     ap.add_argument("--dist", default="uniform")
-    ap.add_argument("--sample-frac", type=float, default=0.125,
-                    help="fraction of target leaves in one CPU-baseline step")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fmm", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -162,54 +161,79 @@ def config_block(args, world, extra=None):
 
 
 # ------------------------------------------------------------ CPU baseline --
-def cpu_baseline(wl, args, steps=1, warmup=0, threads=None):
-    """Reference nearfield_run on a contiguous sample of target leaves."""
+DIST_KIND = {"uniform": 0, "line": 1, "gauss8": 2, "random": 3, "positive": 4}
+CPU_BLOCKS = 8  # the leaf set is cut into 8 disjoint blocks; CPU steps cycle them
+
+
+def leaf_block(n_leaves, i, n_blocks=CPU_BLOCKS):
+    """i-th of n_blocks disjoint contiguous target-leaf blocks (cycled)."""
+    i %= n_blocks
+    return n_leaves * i // n_blocks, n_leaves * (i + 1) // n_blocks
+
+
+def timed_ref_steps(r, n_leaves, steps, warmup, threads):
+    """The reference nearfield_run (backend.cpp:73-89, pool path, `threads`
+    OpenMP threads) on one leaf block per step, blocks cycled so that 8 steps
+    cover every target leaf once.  Returns (pairs/s over the timed steps,
+    per-step seconds, per-step pairs, leaves covered)."""
+    times, pairs, covered = [], [], set()
+    for i in range(warmup + steps):
+        lb, le = leaf_block(n_leaves, i)
+        _, pr, secs = r.run(lb, le, parallel=True, threads=threads)
+        if i >= warmup:
+            times.append(secs)
+            pairs.append(pr)
+            covered.add(i % CPU_BLOCKS)
+    leaves = sum(b - a for a, b in (leaf_block(n_leaves, k) for k in covered))
+    return sum(pairs) / sum(times), times, pairs, leaves
+
+
+def cpu_baseline(wl, args, steps=3, warmup=0, threads=None):
+    """Reference nearfield_run on `steps` disjoint 1/8 blocks of the target
+    leaves (oracle/_ref, compiled unmodified), else the C restatement on one
+    thread over a smaller sample."""
     from oracle import oracle as O
 
     threads = threads or os.cpu_count()
     nl = wl["n_leaves"]
-    lb = 0
-    le = max(1, int(nl * args.sample_frac))
     csr = O.LeafCSR(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"])
     if O.ref_available():
         r = O.RefNearField(csr, wl["zp"], wl["mp"], wl["yp"], wl["sid"])
-        kind, cores = "reference", threads
-        times, pairs = [], 0
-        for i in range(warmup + steps):
-            _, pairs, secs = r.run(lb, le, parallel=True, threads=threads)
-            if i >= warmup:
-                times.append(secs)
+        value, times, pairs, leaves = timed_ref_steps(r, nl, steps, warmup, threads)
         r.close()
+        kind, cores = "reference", threads
+        sample = (f"{steps} steps, each one of {CPU_BLOCKS} disjoint target-leaf blocks "
+                  f"({leaves} of {nl} leaves covered, {sum(pairs)} pairs), pairs/s = "
+                  f"sum(pairs)/sum(seconds); {cpu_desc()['model']}")
     else:  # restated loop, single thread, smaller sample
         kind, cores = "port", 1
-        le = max(1, le // 16)
-        times = []
+        lb, le = 0, max(1, nl // (16 * CPU_BLOCKS))
+        times, pairs = [], []
         for i in range(warmup + steps):
             t0 = time.perf_counter()
-            _, pairs = O.nearfield(csr, wl["zp"], wl["mp"], wl["yp"], wl["sid"], leaf_begin=lb,
-                                   leaf_end=le)
+            _, pr = O.nearfield(csr, wl["zp"], wl["mp"], wl["yp"], wl["sid"], leaf_begin=lb,
+                                leaf_end=le)
             if i >= warmup:
                 times.append(time.perf_counter() - t0)
-    best = min(times)
-    return {"value": pairs / best, "unit": "pairs/s", "cores": cores, "kind": kind,
-            "sample": f"target leaves [{lb},{le}) of {nl} ({pairs} pairs/step), "
-                      f"best of {len(times)}; {cpu_desc()['model']}",
-            "pairs_per_step": pairs, "seconds_per_step": statistics.median(times),
-            "step_seconds": times}
+                pairs.append(pr)
+        value = sum(pairs) / sum(times)
+        sample = f"target leaves [{lb},{le}) of {nl}, {steps} steps, restated loop, 1 thread"
+    return {"value": value, "unit": "pairs/s", "cores": cores, "kind": kind, "sample": sample,
+            "seconds_per_step": statistics.median(times), "step_seconds": times}
 
 
-def cpu_fmm_baseline(s, e, args):
+def cpu_fmm_baseline(z, m, args):
     """Reference FmmEngine{pool, all host threads}.evaluate once on the same
-    N = args.n problem (oracle/_ref, compiled unmodified) -> evals/s."""
+    N = args.n problem (oracle/_ref, compiled unmodified) -> evals/s.
+    z, m: [n, 2] float64."""
     from oracle import oracle as O
 
     if not O.ref_available():
         return None
     threads = os.cpu_count()
-    z = np.stack([s.z.real, s.z.imag], 1)
-    m = np.stack([s.m.real, s.m.imag], 1)
+    sid = np.arange(len(z), dtype=np.int64)
     t0 = time.perf_counter()
-    _, tim, cnt, p = O.ref_evaluate(z, m, z, e.source_id, theta=args.theta, n_levels=args.levels,
+    _, tim, cnt, p = O.ref_evaluate(z, m, z, sid, theta=args.theta, n_levels=args.levels,
                                     backend=1, threads=threads)
     wall = time.perf_counter() - t0
     return {"value": 1.0 / tim[6], "unit": "evals/s", "cores": threads, "kind": "reference",
@@ -218,25 +242,56 @@ def cpu_fmm_baseline(s, e, args):
 
 
 def run_reference(args):
+    """The reference arm: nothing from paper_1311_1006_b200 is imported or
+    loaded.  Inputs come from the reference-side generator
+    (fmmref_make_distribution = tools/atfmm.cpp:70-86), the tree from the
+    reference's own build_pyramid / build_connectivity (geometry.cpp:106-216),
+    the timed loop is the reference's nearfield_run (backend.cpp:73-89) --
+    all in oracle/_ref/libfmmref.so, compiled unmodified."""
     rank, world, local = dist_env()
     if world > 1 and rank != 0:
         return 0  # rank 0 alone runs the CPU reference
-    wl = build_workload(args, os.cpu_count())
-    cb = cpu_baseline(wl, args, steps=args.steps, warmup=args.warmup)
-    ms = 1e3 * statistics.median(cb["step_seconds"])
-    line = {"impl": "reference", "metric": "p2p_pairs_per_sec", "value": cb["value"],
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libfmmref.so not built (needs /root/reference at build)"}))
+        return 0
+    threads = os.cpu_count()
+    t0 = time.perf_counter()
+    z, m = O.make_distribution(DIST_KIND[args.dist], args.n, args.seed)
+    sid = np.arange(args.n, dtype=np.int64)
+    t1 = time.perf_counter()
+    tree = O.ref_tree(z, m, z, sid, args.levels, args.theta, threads=threads)
+    t2 = time.perf_counter()
+    csr = tree.leaf_csr()
+    nl = len(csr.pt_off) - 1
+    r = O.RefNearField(csr, z[tree.perm], m[tree.perm], z[tree.eval_perm], sid[tree.eval_perm])
+    del tree
+    value, times, pairs, leaves = timed_ref_steps(r, nl, args.steps, args.warmup, threads)
+    r.close()
+    sample = (f"{args.steps} timed steps (+{args.warmup} warm-up), step i = target-leaf block "
+              f"i mod {CPU_BLOCKS} of {CPU_BLOCKS} disjoint blocks: {leaves} of {nl} leaves "
+              f"timed ({sum(pairs)} pairs); pairs/s = sum(pairs)/sum(seconds); "
+              f"{cpu_desc()['model']}")
+    ms = 1e3 * statistics.median(times)
+    line = {"impl": "reference", "metric": "p2p_pairs_per_sec", "value": value,
             "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args, 1, {"sample": cb["sample"]}),
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": cb["value"], "unit": "pairs/s", "h2d_bytes_per_step": 0,
+            "config": config_block(args, 1, {"sample": sample}),
+            "same_config": leaves == nl,
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "host": cpu_desc()}
+            "host": cpu_desc(),
+            "setup_s": {"generate": round(t1 - t0, 3), "reference_tree": round(t2 - t1, 3)},
+            "path": "oracle/_ref/libfmmref.so only: fmmref_make_distribution, reference "
+                    "build_pyramid/build_connectivity, reference nearfield_run(parallel) "
+                    "over each block"}
     if not args.no_fmm:
-        from paper_1311_1006_b200 import fmm as F
-        s = F.make_distribution(args.dist, args.n, args.seed)
-        line["fmm_evals_per_sec"] = cpu_fmm_baseline(s, F.EvalSet.self_of(s), args)
+        line["fmm_evals_per_sec"] = cpu_fmm_baseline(z, m, args)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -370,6 +425,41 @@ def run_ours(args):
                 print(f"gathered potentials differ from the 1-rank result: {err:g}", file=sys.stderr)
         barrier()
 
+    # ---- parity of the measured result (outside the timed region) ----------------
+    # The potentials the timed steps produced (gathered over ranks for N > 1)
+    # against the CPU restatement of near_box (oracle/, the checker) on a
+    # stratified sample of target leaves: 64 blocks of 64 leaves spread over
+    # the range, the first and last leaves, and every 2/4/8-way shard cut.
+    # The total pair count is checked exactly against the reference identity
+    # over every leaf.
+    parity = None
+    if not args.no_parity and rank == 0:
+        from oracle import parity as P
+        from paper_1311_1006_b200.sharding import shard_cuts as _cuts
+
+        tp = time.perf_counter()
+        torch.cuda.synchronize()
+        got = full.cpu().numpy().reshape(-1, 2)
+        per_leaf = P.pair_identity(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"], wl["sid"])
+        prefix = np.concatenate([[0], np.cumsum(per_leaf)])
+        pc = sorted({int(c) for w in (2, 4, 8) for c in _cuts(prefix, w)})
+        blocks = P.leaf_blocks(wl["n_leaves"], cuts=pc, n_blocks=64, block=64)
+        pr = P.sampled_check(got, wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"], wl["zp"],
+                             wl["mp"], wl["yp"], wl["sid"], blocks=blocks)
+        parity = {"max_rel_err": pr["normwise"], "max_rel_err_point": pr["max_rel_err_point"],
+                  "tolerance": 1e-12, "ok": bool(pr["normwise"] <= 1e-12 and
+                                                 pr["pair_identity_ok"] and
+                                                 int(total_pairs) == pr["total_pairs_identity"]),
+                  "pairs_exact": int(total_pairs) == pr["total_pairs_identity"],
+                  "sample": f"{pr['leaves']} of {wl['n_leaves']} target leaves in "
+                            f"{pr['blocks']} blocks ({pr['evals']} evals, {pr['pairs']} pairs) "
+                            "vs the restated near_box (oracle/fmm_oracle.c); error normwise "
+                            "max|d|/max|ref| over the sample",
+                  "seconds": round(time.perf_counter() - tp, 2)}
+        del got
+        if not parity["ok"]:
+            print(f"PARITY FAILURE: {parity}", file=sys.stderr)
+
     # ---- e2e: reference-facing C ABI with host buffers (pack+H2D+kernel+D2H) ----
     e2e = None
     if not args.no_e2e:
@@ -444,7 +534,7 @@ def run_ours(args):
                                   "tree + L2L/L2P, device P2P + M2L)"}}
         assert rd.counters == rh.counters
         if not args.no_cpu and world == 1:
-            fmm["cpu_baseline"] = cpu_fmm_baseline(s, e, args)
+            fmm["cpu_baseline"] = cpu_fmm_baseline(F._c2(s.z), F._c2(s.m), args)
         del s, e
         # configs 2 and 3 (1M points): the level count autotuned
         # by sweeping L as acceptance does; device pipeline, median of 3
@@ -491,7 +581,7 @@ def run_ours(args):
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
-        cb = cpu_baseline(wl, args, steps=1)
+        cb = cpu_baseline(wl, args, steps=3)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     traffic = None
@@ -539,6 +629,8 @@ def run_ours(args):
             "host": cpu_desc(),
             "setup_s": {"generate": round(wl["gen_s"], 3), "tree": round(wl["tree_s"], 3)},
         }
+        if parity is not None:
+            line["parity"] = parity
         if gather_check is not None:
             line["gather_check"] = gather_check
         if shared:
