@@ -26,7 +26,7 @@
 
 #include "far_kernels.cuh"
 #include "fmmcu_internal.cuh"
-#include "m2l_kernels.cuh"
+#include "m2l_args.cuh"
 #include "tree_kernels.cuh"
 
 using namespace fmmcu;
@@ -781,7 +781,6 @@ int far_field(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, cudaEvent_t e_up,
   CU_TRY(c, P->flag.ensure(kFlagBytes));
   CU_TRY(c, cudaMemsetAsync(P->flag.as<int>() + kFlagSingular, 0, 4, s));
   if (P->n_targets) {
-    if (int rc = m2l_table(c, P->p, P->kernel, s)) return rc;
     M2LArgs m{};
     m.p = P->p;
     m.kernel = P->kernel;
@@ -790,13 +789,10 @@ int far_field(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, cudaEvent_t e_up,
     m.target_box = P->tbox.as<uint32_t>();
     m.weak_off = P->woff.as<uint32_t>();
     m.weak_idx = P->widx.as<uint32_t>();
-    m.table = c->m_table.as<double>();
     m.n_targets = P->n_targets;
-    m.big_w2 = std::pow(10.0, 500.0 / double(P->p + 2));
     m.out = P->m2l_sum.as<double2>();
     m.singular = P->flag.as<int>() + kFlagSingular;
-    CU_TRY(c, m2l_set_const_table(c->m_table.as<double>(), P->p + 1, s));
-    launch_m2l(m, s);
+    if (int rc = m2l_run(c, m, P->m2l_nnz, s)) return rc;
   }
   for (int l = 1; l < L; ++l) {
     FarArgs a = far_args(P, l);

@@ -1261,6 +1261,66 @@ int m2l_table(fmmcu_ctx* c, int p, int kernel, cudaStream_t stream) {
   return FMMCU_OK;
 }
 
+// All M2L sums of a job on `s` (C-ABI M2L and device pipeline): the binomial
+// table, then the register kernel over work items (weak lists longer than
+// kM2LChunk split into chunks, reduced in chunk order) for the orders it is
+// instantiated for, else the r1 per-target kernels.  a.p, a.kernel, centres,
+// coefficients, targets, lists, out and singular must be set; nnz is the
+// weak-list length (a bound for the item and partial buffers).
+int m2l_run(fmmcu_ctx* c, M2LArgs a, uint64_t nnz, cudaStream_t s) {
+  if (a.n_targets == 0) return FMMCU_OK;
+  if (int rc = m2l_table(c, a.p, a.kernel, s)) return rc;
+  const int P1 = a.p + 1;
+  a.table = c->m_table.as<double>();
+  // (p+2) log10|w| >= 250  <=>  |w|^2 >= 10^(500/(p+2))
+  a.big_w2 = std::pow(10.0, 500.0 / double(a.p + 2));
+  int tb = 64;
+  M2LKernelFn reg = m2l_old_kernel() ? nullptr
+                    : a.kernel == 0  ? m2l_reg_for<true>(P1, &tb)
+                                     : m2l_reg_for<false>(P1, &tb);
+  if (!reg) {
+    CU_TRY(c, m2l_set_const_table(c->m_table.as<double>(), P1, s));
+    launch_m2l_targets(a, s);
+    CU_TRY(c, cudaGetLastError());
+    c->launches += 1;
+    return FMMCU_OK;
+  }
+  const uint32_t nt = a.n_targets;
+  const uint64_t max_items = uint64_t(nt) + nnz / kM2LChunk + 1;
+  const uint64_t max_slots = 2 * (nnz / kM2LChunk) + 2;
+  if (max_items > 0xFFFFFFF0ull || max_slots > 0xFFFFFFF0ull)
+    return set_err(c, FMMCU_EINVAL, "m2l: too many work items");
+  CU_TRY(c, c->m_items.ensure(max_items * 16));
+  CU_TRY(c, c->m_iscan.ensure((uint64_t(nt) + 1) * 8 * 2));
+  CU_TRY(c, c->m_nitems.ensure(8));
+  CU_TRY(c, c->m_partial.ensure(max_slots * uint64_t(P1) * 16));
+  auto* cnt = c->m_iscan.as<unsigned long long>();
+  auto* off = cnt + (nt + 1);
+  m2l_item_count_kernel<<<(nt + 256) / 256, 256, 0, s>>>(a.weak_off, nt, cnt);
+  size_t tmp = 0;
+  CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, int64_t(nt) + 1, s));
+  CU_TRY(c, c->m_cubtmp.ensure(tmp));
+  CU_TRY(c, cub::DeviceScan::ExclusiveSum(c->m_cubtmp.p, tmp, cnt, off, int64_t(nt) + 1, s));
+  m2l_item_fill_kernel<<<(nt + 255) / 256, 256, 0, s>>>(a.weak_off, nt, off,
+                                                        c->m_items.as<uint4>(),
+                                                        c->m_nitems.as<uint32_t>());
+  a.items = c->m_items.as<uint4>();
+  a.n_items = c->m_nitems.as<uint32_t>();
+  a.partial = c->m_partial.as<double2>();
+  int dev_sms = 148, per_sm = 0;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+  CU_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reg, tb, 0));
+  const uint64_t want = (max_items + tb - 1) / tb;
+  const uint32_t grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(
+      want, uint64_t(dev_sms) * uint64_t(std::max(per_sm, 1)))));
+  reg<<<grid, tb, 0, s>>>(a);
+  const uint64_t nred = uint64_t(nt) * P1;
+  m2l_reduce_kernel<<<uint32_t((nred + 255) / 256), 256, 0, s>>>(off, nt, P1, a.partial, a.out);
+  CU_TRY(c, cudaGetLastError());
+  c->launches += 4;
+  return FMMCU_OK;
+}
+
 }  // namespace fmmcu::detail
 
 using namespace fmmcu::detail;
@@ -1350,7 +1410,8 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     for (DevBuf* b : {&c->d_zin, &c->d_min, &c->d_src, &c->d_evy, &c->d_eself, &c->d_pt, &c->d_ev, &c->d_soff,
                       &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter, &c->d_evr,
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
-                      &c->m_table, &c->m_out, &c->m_flag})
+                      &c->m_table, &c->m_out, &c->m_flag, &c->m_items, &c->m_iscan, &c->m_nitems,
+                      &c->m_partial, &c->m_cubtmp})
       b->release();
     for (HostBuf* b : {&c->h_src, &c->h_evy, &c->h_eself, &c->h_out, &c->h_hits, &c->h_csr,
                        &c->mh_out, &c->mh_flag})
@@ -1655,7 +1716,6 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
       return set_err(c, FMMCU_EINVAL, "bad m2l target list");
   for (uint32_t q = 0; q < nnz; ++q)
     if (j->weak_idx[q] >= nb) return set_err(c, FMMCU_EINVAL, "bad m2l weak index");
-  if (int rc = m2l_table(c, j->p, j->kernel, c->m2l_stream)) return rc;
   CU_TRY(c, c->m_centers.ensure(size_t(nb) * 16));
   CU_TRY(c, c->m_coeffs.ensure(size_t(nb) * P1 * 16));
   CU_TRY(c, c->m_tbox.ensure(size_t(nt) * 4));
@@ -1684,16 +1744,10 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
     a.target_box = c->m_tbox.as<uint32_t>();
     a.weak_off = c->m_woff.as<uint32_t>();
     a.weak_idx = c->m_widx.as<uint32_t>();
-    a.table = c->m_table.as<double>();
     a.n_targets = nt;
-    // (p+2) log10|w| >= 250  <=>  |w|^2 >= 10^(500/(p+2))
-    a.big_w2 = std::pow(10.0, 500.0 / double(j->p + 2));
     a.out = c->m_out.as<double2>();
     a.singular = c->m_flag.as<int>();
-    CU_TRY(c, m2l_set_const_table(c->m_table.as<double>(), P1, s));
-    launch_m2l(a, s);
-    CU_TRY(c, cudaGetLastError());
-    c->launches += 1;
+    if (int rc = m2l_run(c, a, nnz, s)) return rc;
     CU_TRY(c, cudaMemcpyAsync(c->mh_out.p, c->m_out.p, size_t(nt) * P1 * 16, cudaMemcpyDeviceToHost, s));
   }
   CU_TRY(c, cudaMemcpyAsync(c->mh_flag.p, c->m_flag.p, 4, cudaMemcpyDeviceToHost, s));

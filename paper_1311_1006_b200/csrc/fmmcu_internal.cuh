@@ -17,6 +17,7 @@
 #include "fmm_cuda.h"
 #include "p2p_kernels.cuh"
 #include "p2p_warp.cuh"
+#include "m2l_args.cuh"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -217,6 +218,7 @@ struct fmmcu_ctx {
 
   // m2l
   DevBuf m_centers, m_coeffs, m_tbox, m_woff, m_widx, m_table, m_out, m_flag;
+  DevBuf m_items, m_iscan, m_nitems, m_partial, m_cubtmp;  // m2l_run work items
   HostBuf mh_out, mh_flag;
   int table_p = -1, table_kernel = -1;
   bool m2l_inflight = false;
@@ -251,5 +253,6 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
                 bool reset_hits = true);
 // Batched M2L on `stream` from device-resident arrays (see m2l_kernels.cuh).
 int m2l_table(fmmcu_ctx* c, int p, int kernel, cudaStream_t stream);
+int m2l_run(fmmcu_ctx* c, fmmcu::M2LArgs a, uint64_t nnz, cudaStream_t s);
 
 }  // namespace fmmcu::detail

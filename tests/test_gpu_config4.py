@@ -117,7 +117,7 @@ def test_config4_eight_way_shards(ctx, c4):
         ctx.run_staged(a, b)
         total += ctx.pairs()
         e0, e1 = int(ev[a]), int(ev[b])
-        full[e0:e1] = ctx.copy_out(c4["n_eval"], e0, e1)
+        full[e0:e1] = ctx.copy_out(c4["n_eval"], e0, e1)[e0:e1]
     assert total == c4["total"]
     r = _check(c4, full)
     assert r["normwise"] <= TOL_FP64, r
