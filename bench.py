@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=4)
     ap.add_argument("--dist", default="uniform")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--gather", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: how the slices reach rank 0 (see include/fmm_cuda.h)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fmm", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -153,7 +155,9 @@ def config_block(args, world, extra=None):
                      f"harmonic, no smoother, P2P over every target leaf",
          "n_points": args.n, "n_levels": args.levels, "theta": args.theta, "seed": args.seed,
          "kernel": "harmonic", "precision": "fp64",
-         "parallelism": f"target-leaf shards x{world}, sources replicated, NCCL all-gather",
+         "parallelism": f"target-leaf shards x{world}, halo-only staged sources, "
+                        f"potentials gathered to rank 0 ({getattr(args, 'gather', 'peer')}: "
+                        "NVLink peer stores fused into the kernels | NCCL send/recv)",
          "l2": "inputs (320 MB packed sources + 160 MB evals) larger than the 126 MB L2"}
     if extra:
         c.update(extra)
@@ -318,43 +322,62 @@ def run_ours(args):
         torch.cuda.set_device(local)
     from paper_1311_1006_b200 import _native as N
     from paper_1311_1006_b200 import fmm as F
-    from paper_1311_1006_b200.sharding import PotentialGather, eval_slices, shard_cuts
+    from paper_1311_1006_b200.sharding import eval_slices, leaf_work_prefix, shard_cuts
 
     threads = max(1, (os.cpu_count() or 1) // world)
     wl = build_workload(args, threads)
     n_eval = len(wl["yp"])
     ctx = N.CudaContext(local)
-    # One explicit stream shared by our kernels, the torch events that time
-    # them and the NCCL gather (the legacy default stream has handle 0, which
-    # the C ABI reads as "use the context's own stream").
+    # One explicit stream shared by our kernels and the torch events that time
+    # them (the legacy default stream has handle 0, which the C ABI reads as
+    # "use the context's own stream").
     stream = torch.cuda.Stream(device=local)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    job, keep = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
-                                       wl["zp"], wl["mp"], wl["yp"], wl["sid"], None)
-    ctx.stage(job, keep)
-    prefix = ctx.work_prefix(wl["n_leaves"])
-    cuts = shard_cuts(prefix, world)
+    # Work-balanced contiguous leaf shards (pair work n_evals * |strong|).
+    cuts = shard_cuts(leaf_work_prefix(wl["pt"], wl["ev"], wl["so"], wl["si"]), world)
     lb, le = int(cuts[rank]), int(cuts[rank + 1])
-    if world > 1:
-        # the (mutual) work list is built for the rank's own leaf range
-        job, keep = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
-                                           wl["zp"], wl["mp"], wl["yp"], wl["sid"], None,
-                                           leaf_begin=lb, leaf_end=le)
-        ctx.stage(job, keep)
     slices = eval_slices(wl["ev"], cuts)
-    full = torch.zeros(2 * n_eval, dtype=torch.float64, device=f"cuda:{local}")
+    eval_cuts = np.array([a for a, _ in slices] + [slices[-1][1]], dtype=np.uint32)
+    # The rank stages its shard halo-only: only the sources its strong lists
+    # read are uploaded, and the (mutual) work list covers its range.
+    job, keep = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
+                                       wl["zp"], wl["mp"], wl["yp"], wl["sid"], None,
+                                       leaf_begin=lb, leaf_end=le)
+    ctx.stage(job, keep)
+    staged_h2d, _ = ctx.transfer_bytes()
+    # Gather of the slices into rank 0's output, inside the timed step:
+    #   peer -- rank 0 exports its output buffer over CUDA IPC, the other ranks
+    #           write their potentials into it from the kernels (NVLink stores
+    #           fused with the compute; no collective on the data path);
+    #   nccl -- one grouped ncclSend/ncclRecv of the slices after the kernels,
+    #           issued by the library on its own communicator.
+    gather_mode = args.gather if world > 1 else "none"
+    if gather_mode == "peer":
+        handle = [ctx.out_ipc_handle() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(handle, src=0)
+        if rank != 0:
+            ctx.bind_peer_out(handle[0])
+    elif gather_mode == "nccl":
+        if shared:
+            raise SystemExit("--gather nccl needs one GPU per rank (NCCL rejects shared devices)")
+        uid = [N.CudaContext.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        ctx.nccl_init(uid[0], rank, world)
     torch.cuda.synchronize()
-    ctx.bind_device_out(full.data_ptr())
-    gather = PotentialGather(slices, rank, full, via_host=shared) if world > 1 else None
     fp64_peak = ctx.fp64_peak()
     symmetric, evals_per_lane = ctx.kernel_info()
+
+    def step():
+        ctx.run_staged(lb, le)
+        if gather_mode == "nccl":
+            ctx.nccl_gather_out(0, eval_cuts)
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
-    red_dev = "cpu" if shared else full.device
+    red_dev = "cpu" if shared else torch.device("cuda", local)
 
     def allmax(x):
         if world == 1:
@@ -371,9 +394,7 @@ def run_ours(args):
         return t.item()
 
     for _ in range(args.warmup):
-        ctx.run_staged(lb, le)
-        if gather:
-            gather()
+        step()
     torch.cuda.synchronize()
     barrier()
 
@@ -389,10 +410,8 @@ def run_ours(args):
     t0.record()
     for i in range(K):
         k0[i].record()
-        ctx.run_staged(lb, le)
+        step()
         k1[i].record()
-        if gather:
-            gather()
     t1.record()
     torch.cuda.synchronize()
     barrier()
@@ -406,23 +425,26 @@ def run_ours(args):
     value = total_pairs / (ms * 1e-3)
     achieved = FLOPS_PER_PAIR * my_pairs / (kernel_ms * 1e-3) / 1e12
 
+    # rank 0's output now holds every slice (peer stores / NCCL landed before
+    # each rank's synchronize + barrier above)
+    full_host = ctx.copy_out(n_eval) if rank == 0 else None
     gather_check = None
+    if world > 1 and rank == 0:
+        # the gathered potentials must match one context evaluating every
+        # leaf (the mutual kernel sums shard-boundary pairs in another order,
+        # so 1e-12 relative, not bitwise)
+        ref_ctx = N.CudaContext(local)
+        jf, kf = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
+                                        wl["zp"], wl["mp"], wl["yp"], wl["sid"], None)
+        ref_ctx.stage(jf, kf)
+        ref_ctx.run_staged(0, wl["n_leaves"])
+        ref = ref_ctx.copy_out(n_eval)
+        ref_ctx.close()
+        err = float(np.abs(full_host - ref).max() / max(np.abs(ref).max(), 1e-300))
+        gather_check = {"max_rel_err": err, "ok": bool(err < 1e-12), "mode": gather_mode}
+        if not gather_check["ok"]:
+            print(f"gathered potentials differ from the 1-rank result: {err:g}", file=sys.stderr)
     if world > 1:
-        # The gathered potentials must match one rank evaluating every leaf
-        # (the mutual kernel sums shard-boundary pairs in a different order,
-        # so compare to 1e-12 relative, not bitwise).
-        if rank == 0:
-            ref = torch.zeros_like(full)
-            jf, kf = N.CudaContext.make_job(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"],
-                                            wl["zp"], wl["mp"], wl["yp"], wl["sid"], None)
-            ctx.stage(jf, kf)
-            ctx.bind_device_out(ref.data_ptr())
-            ctx.run_staged(0, wl["n_leaves"])
-            torch.cuda.synchronize()
-            err = ((full - ref).abs().max() / ref.abs().max().clamp_min(1e-300)).item()
-            gather_check = {"max_rel_err": err, "ok": bool(err < 1e-12)}
-            if not gather_check["ok"]:
-                print(f"gathered potentials differ from the 1-rank result: {err:g}", file=sys.stderr)
         barrier()
 
     # ---- parity of the measured result (outside the timed region) ----------------
@@ -438,8 +460,7 @@ def run_ours(args):
         from paper_1311_1006_b200.sharding import shard_cuts as _cuts
 
         tp = time.perf_counter()
-        torch.cuda.synchronize()
-        got = full.cpu().numpy().reshape(-1, 2)
+        got = full_host
         per_leaf = P.pair_identity(wl["pt"], wl["ev"], wl["so"], wl["si"], wl["perm"], wl["sid"])
         prefix = np.concatenate([[0], np.cumsum(per_leaf)])
         pc = sorted({int(c) for w in (2, 4, 8) for c in _cuts(prefix, w)})
@@ -463,7 +484,8 @@ def run_ours(args):
     # ---- e2e: reference-facing C ABI with host buffers (pack+H2D+kernel+D2H) ----
     e2e = None
     if not args.no_e2e:
-        ctx.bind_device_out(None)
+        if gather_mode == "peer" and rank != 0:
+            ctx.bind_peer_out(None)
         host_out = np.zeros((n_eval, 2))
         # The job's host arrays are page-locked once (cudaHostRegister), as the
         # e2e contract's "pinned host memory": every step still moves the
@@ -498,7 +520,7 @@ def run_ours(args):
                        "to host memory by the kernels' TMA bulk stores"}
 
     # the P2P context's pinned staging (~1 GB) is released before the engine runs
-    del full
+    del full_host
     ctx.close()
     # ---- FMM evals/s through FmmEngine(cuda) (rank 0, single device) -------------
     # (a) device_pipeline: the whole evaluate() on the GPU (tree + lists bit-exact,
@@ -599,9 +621,12 @@ def run_ours(args):
             "metric": "p2p_pairs_per_sec", "value": value, "unit": "pairs/s", "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args, world, {"pairs_per_step": int(total_pairs)}
+            "config": config_block(args, world, {"pairs_per_step": int(total_pairs),
+                                                 "gather": gather_mode,
+                                                 "staged_h2d_bytes_rank0": int(staged_h2d)}
                                    | ({"parallelism": f"target-leaf shards x{world} sharing "
-                                       "cuda:0, gloo all-gather via host"} if shared else {})),
+                                       f"cuda:0 (test mode), gather {gather_mode}"}
+                                      if shared else {})),
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
                          "peak_source": "measured DFMA micro-benchmark on this GPU in this run "

@@ -36,6 +36,10 @@ extern "C" {
 #define FMMCU_ESINGULAR 4 /* M2L with coincident centres (SingularConfiguration) */
 #define FMMCU_ENOMEM 5    /* device or pinned allocation failed */
 #define FMMCU_ESTATE 6    /* call out of order (finish without launch, ...) */
+#define FMMCU_ENCCL 7     /* NCCL unavailable or a collective failed */
+
+#define FMMCU_IPC_HANDLE_BYTES 64  /* cudaIpcMemHandle_t */
+#define FMMCU_NCCL_ID_BYTES 128    /* ncclUniqueId */
 
 #define FMMCU_KERNEL_HARMONIC 0 /* -m / (y - x)     (expansion.cpp:90-92) */
 #define FMMCU_KERNEL_LOG 1      /*  m * log(y - x) */
@@ -234,6 +238,35 @@ int fmmcu_last_transfer_bytes(const fmmcu_ctx *ctx, uint64_t *h2d, uint64_t *d2h
 int fmmcu_p2p_kernel_info(const fmmcu_ctx *ctx, int *symmetric, int *evals_per_lane);
 /* Measured FP64 FMA throughput of this device (TFLOP/s, DFMA = 2 flops). */
 int fmmcu_fp64_peak(fmmcu_ctx *ctx, double *tflops);
+
+/* ---- multi-GPU: target-leaf shards, one process (rank) per GPU ----------
+ * (replaces the per-leaf loop of backend.cpp:73-89 split over
+ * ranks; the only exchange is the potentials' gather, backend.cpp:41-69 has
+ * no cross-leaf reduction.)  Each rank stages its shard with
+ * fmmcu_p2p_stage(job with leaf_begin/leaf_end) -- halo-only: just the
+ * sources its strong lists read cross PCIe -- and runs
+ * fmmcu_p2p_run_staged over its range.  The slices reach the root either
+ *  (a) fused into the kernels' stores: the root exports its staged output
+ *      buffer, every other rank maps it and binds it as its output, so the
+ *      shard's potentials are written into the root's HBM over NVLink while
+ *      the kernels run (no collective, no extra pass); or
+ *  (b) with NCCL: one grouped ncclSend / ncclRecv of each rank's eval slice
+ *      [eval_cuts[r], eval_cuts[r+1]) into the root's output at the same
+ *      offset, enqueued on the context stream behind the kernels.
+ * The root's potentials are complete once every rank's stream has passed
+ * its kernels (a) or the gather (b). */
+/* (a) root: IPC handle (FMMCU_IPC_HANDLE_BYTES) of its staged output buffer */
+int fmmcu_p2p_out_ipc_handle(fmmcu_ctx *ctx, void *handle);
+/* (a) other ranks: write subsequent runs' potentials into the root's buffer
+ * (NULL unmaps and restores the context's own output). */
+int fmmcu_p2p_bind_peer_out(fmmcu_ctx *ctx, const void *handle);
+/* (b) NCCL (libnccl.so.2 loaded at run time): a unique id on one rank
+ * (FMMCU_NCCL_ID_BYTES, shared out of band), then every rank joins. */
+int fmmcu_nccl_unique_id(void *id);
+int fmmcu_nccl_init(fmmcu_ctx *ctx, const void *id, int rank, int world);
+/* (b) gather the ranks' eval slices of the staged output into the root's,
+ * in place (eval_cuts: [world + 1] permuted-eval offsets). */
+int fmmcu_nccl_gather_out(fmmcu_ctx *ctx, int root, const uint32_t *eval_cuts);
 
 #ifdef __cplusplus
 }

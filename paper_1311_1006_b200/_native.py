@@ -143,7 +143,12 @@ CUDA_SYMBOLS = [
     "fmmcu_fp64_peak", "fmmcu_last_transfer_bytes", "fmmcu_host_register", "fmmcu_host_unregister",
     "fmmcu_fmm_evaluate", "fmmcu_fmm_launch", "fmmcu_fmm_finish", "fmmcu_fmm_tree_level", "fmmcu_fmm_tree_perm", "fmmcu_fmm_tree_lists",
     "fmmcu_hypot_batch", "fmmcu_p2p_kernel_info",
+    "fmmcu_p2p_out_ipc_handle", "fmmcu_p2p_bind_peer_out", "fmmcu_nccl_unique_id",
+    "fmmcu_nccl_init", "fmmcu_nccl_gather_out",
 ]
+IPC_HANDLE_BYTES = 64
+NCCL_ID_BYTES = 128
+FMMCU_ENCCL = 7
 
 
 def cuda_lib():
@@ -187,6 +192,11 @@ def cuda_lib():
         lib.fmmcu_kernel_launches.restype = C.c_uint64
         lib.fmmcu_fp64_peak.argtypes = [vp, C.POINTER(C.c_double)]
         lib.fmmcu_last_transfer_bytes.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        lib.fmmcu_p2p_out_ipc_handle.argtypes = [vp, vp]
+        lib.fmmcu_p2p_bind_peer_out.argtypes = [vp, vp]
+        lib.fmmcu_nccl_unique_id.argtypes = [vp]
+        lib.fmmcu_nccl_init.argtypes = [vp, vp, C.c_int, C.c_int]
+        lib.fmmcu_nccl_gather_out.argtypes = [vp, C.c_int, vp]
         _cuda = lib
     return _cuda
 
@@ -406,6 +416,37 @@ class CudaContext:
         sym, e = C.c_int(), C.c_int()
         self._check(self.lib.fmmcu_p2p_kernel_info(self.h, C.byref(sym), C.byref(e)))
         return bool(sym.value), int(e.value)
+
+    # -- multi-GPU (include/fmm_cuda.h, fmm_multi.cu) ------------------------
+    def out_ipc_handle(self) -> bytes:
+        """Root rank: IPC handle of the staged output buffer."""
+        buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+        self._check(self.lib.fmmcu_p2p_out_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def bind_peer_out(self, handle: bytes | None):
+        """Other ranks: write the shard's potentials into the root's buffer."""
+        if handle is None:
+            self._check(self.lib.fmmcu_p2p_bind_peer_out(self.h, None))
+            return
+        buf = C.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+        self._check(self.lib.fmmcu_p2p_bind_peer_out(self.h, buf))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(NCCL_ID_BYTES)
+        rc = cuda_lib().fmmcu_nccl_unique_id(buf)
+        if rc != FMMCU_OK:
+            raise FmmcuError(rc, "ncclGetUniqueId failed (libnccl.so.2)")
+        return buf.raw
+
+    def nccl_init(self, uid: bytes, rank: int, world: int):
+        buf = C.create_string_buffer(bytes(uid), NCCL_ID_BYTES)
+        self._check(self.lib.fmmcu_nccl_init(self.h, buf, rank, world))
+
+    def nccl_gather_out(self, root: int, eval_cuts):
+        cuts = np.ascontiguousarray(eval_cuts, dtype=np.uint32)
+        self._check(self.lib.fmmcu_nccl_gather_out(self.h, root, _ptr(cuts)))
 
     def fp64_peak(self) -> float:
         v = C.c_double()

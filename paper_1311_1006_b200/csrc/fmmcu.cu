@@ -668,24 +668,55 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // device instead of uploaded (saves 20 B/eval of PCIe traffic).
   const bool maybe_self = j->eval_sid && ne == ns && ns > 0;
   bool self_layout = maybe_self;
-  constexpr int64_t kChunk = 1 << 20;  // sources per pipelined chunk (32 MB)
-  for (int64_t c0 = 0; c0 < int64_t(ns); c0 += kChunk) {
-    const int64_t c1 = std::min<int64_t>(ns, c0 + kChunk);
-    bool same = true;
-#pragma omp parallel for schedule(static) reduction(&& : same)
-    for (int64_t i = c0; i < c1; ++i) {
-      hs[4 * i + 0] = z[2 * i];
-      hs[4 * i + 1] = z[2 * i + 1];
-      hs[4 * i + 2] = m[2 * i];
-      hs[4 * i + 3] = m[2 * i + 1];
-      if (maybe_self)
-        same = same && j->eval_sid[i] == int64_t(j->perm[i]) &&
-               j->eval_y[2 * i] == z[2 * i] && j->eval_y[2 * i + 1] == z[2 * i + 1];
+  // Halo-only staging for a leaf shard [leaf_begin, leaf_end) (multi-GPU
+  // ranks): the shard's kernels read exactly the sources of its strong lists
+  // (backend.cpp:55-57) -- its own leaves plus a halo -- so only those source
+  // runs are packed and uploaded; the other slots of the device array are
+  // never read.  A full range uploads everything in one run.
+  const uint32_t lb = j->leaf_begin, le = j->leaf_end;
+  const bool partial = lb > 0 || le < nl;
+  std::vector<std::pair<int64_t, int64_t>> runs;  // source slot runs [a, b)
+  if (partial) {
+    std::vector<uint8_t> need(nl, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t t = lb; t < int64_t(le); ++t)
+      for (uint32_t q = j->strong_off[t]; q < j->strong_off[t + 1]; ++q) need[j->strong_idx[q]] = 1;
+    for (uint32_t t = 0; t < nl;) {
+      if (!need[t]) {
+        ++t;
+        continue;
+      }
+      uint32_t t1 = t + 1;
+      while (t1 < nl && need[t1]) ++t1;
+      if (j->pt_off[t1] > j->pt_off[t]) runs.emplace_back(j->pt_off[t], j->pt_off[t1]);
+      t = t1;
     }
-    self_layout = self_layout && same;
-    CU_TRY(c, cudaMemcpyAsync(c->d_src.as<double>() + 4 * c0, hs + 4 * c0, size_t(c1 - c0) * 32,
-                              cudaMemcpyHostToDevice, s));
+  } else if (ns) {
+    runs.emplace_back(0, int64_t(ns));
   }
+  uint64_t uploaded = 0;
+  constexpr int64_t kChunk = 1 << 20;  // sources per pipelined chunk (32 MB)
+  for (const auto& run : runs)
+    for (int64_t c0 = run.first; c0 < run.second; c0 += kChunk) {
+      const int64_t c1 = std::min<int64_t>(run.second, c0 + kChunk);
+      bool same = true;
+#pragma omp parallel for schedule(static) reduction(&& : same)
+      for (int64_t i = c0; i < c1; ++i) {
+        hs[4 * i + 0] = z[2 * i];
+        hs[4 * i + 1] = z[2 * i + 1];
+        hs[4 * i + 2] = m[2 * i];
+        hs[4 * i + 3] = m[2 * i + 1];
+        if (maybe_self)
+          same = same && j->eval_sid[i] == int64_t(j->perm[i]) &&
+                 j->eval_y[2 * i] == z[2 * i] && j->eval_y[2 * i + 1] == z[2 * i + 1];
+      }
+      self_layout = self_layout && same;
+      CU_TRY(c, cudaMemcpyAsync(c->d_src.as<double>() + 4 * c0, hs + 4 * c0, size_t(c1 - c0) * 32,
+                                cudaMemcpyHostToDevice, s));
+      uploaded += uint64_t(c1 - c0);
+    }
+  // a shard's own evals are its own leaves' slots: under the self layout
+  // they are checked above; other slots are never read
   tr.mark("pack+h2d sources");
   c->self_layout = self_layout;
   uint32_t* eself = c->h_eself.as<uint32_t>();
@@ -729,6 +760,8 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   }
   tr.mark("worklist");
   if (int rc = stage_csr(c, j, true)) return rc;
+  c->h2d_bytes -= (uint64_t(ns) - uploaded) * 32;
+  c->staged_src = uploaded;
   tr.mark("csr+worklist h2d");
   return FMMCU_OK;
 }
@@ -1274,10 +1307,20 @@ int m2l_run(fmmcu_ctx* c, M2LArgs a, uint64_t nnz, cudaStream_t s) {
   a.table = c->m_table.as<double>();
   // (p+2) log10|w| >= 250  <=>  |w|^2 >= 10^(500/(p+2))
   a.big_w2 = std::pow(10.0, 500.0 / double(a.p + 2));
+  // FMMCU_M2L=old | thread | warp (default): r1 per-target kernels, the
+  // thread-per-item register kernel, the warp-per-item kernel
+  static const int which = [] {
+    const char* e = std::getenv("FMMCU_M2L");
+    if (m2l_old_kernel() || (e && std::strcmp(e, "old") == 0)) return 0;
+    if (e && std::strcmp(e, "thread") == 0) return 1;
+    return 2;
+  }();
   int tb = 64;
-  M2LKernelFn reg = m2l_old_kernel() ? nullptr
-                    : a.kernel == 0  ? m2l_reg_for<true>(P1, &tb)
-                                     : m2l_reg_for<false>(P1, &tb);
+  M2LKernelFn reg = nullptr;
+  if (which == 1) reg = a.kernel == 0 ? m2l_reg_for<true>(P1, &tb) : m2l_reg_for<false>(P1, &tb);
+  if (which == 2) reg = a.kernel == 0 ? m2l_warp_for<true>(P1, &tb) : m2l_warp_for<false>(P1, &tb);
+  const uint32_t chunk = which == 2 ? kM2LWarpChunk : kM2LChunk;
+  const uint32_t per_item = which == 2 ? 32u : 1u;  // threads per item
   if (!reg) {
     CU_TRY(c, m2l_set_const_table(c->m_table.as<double>(), P1, s));
     launch_m2l_targets(a, s);
@@ -1286,8 +1329,8 @@ int m2l_run(fmmcu_ctx* c, M2LArgs a, uint64_t nnz, cudaStream_t s) {
     return FMMCU_OK;
   }
   const uint32_t nt = a.n_targets;
-  const uint64_t max_items = uint64_t(nt) + nnz / kM2LChunk + 1;
-  const uint64_t max_slots = 2 * (nnz / kM2LChunk) + 2;
+  const uint64_t max_items = uint64_t(nt) + nnz / chunk + 1;
+  const uint64_t max_slots = 2 * (nnz / chunk) + 2;
   if (max_items > 0xFFFFFFF0ull || max_slots > 0xFFFFFFF0ull)
     return set_err(c, FMMCU_EINVAL, "m2l: too many work items");
   CU_TRY(c, c->m_items.ensure(max_items * 16));
@@ -1296,7 +1339,7 @@ int m2l_run(fmmcu_ctx* c, M2LArgs a, uint64_t nnz, cudaStream_t s) {
   CU_TRY(c, c->m_partial.ensure(max_slots * uint64_t(P1) * 16));
   auto* cnt = c->m_iscan.as<unsigned long long>();
   auto* off = cnt + (nt + 1);
-  m2l_item_count_kernel<<<(nt + 256) / 256, 256, 0, s>>>(a.weak_off, nt, cnt);
+  m2l_item_count_kernel<<<(nt + 256) / 256, 256, 0, s>>>(a.weak_off, nt, chunk, cnt);
   size_t tmp = 0;
   CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, int64_t(nt) + 1, s));
   CU_TRY(c, c->m_cubtmp.ensure(tmp));
@@ -1310,7 +1353,7 @@ int m2l_run(fmmcu_ctx* c, M2LArgs a, uint64_t nnz, cudaStream_t s) {
   int dev_sms = 148, per_sm = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   CU_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reg, tb, 0));
-  const uint64_t want = (max_items + tb - 1) / tb;
+  const uint64_t want = (max_items * per_item + tb - 1) / tb;
   const uint32_t grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(
       want, uint64_t(dev_sms) * uint64_t(std::max(per_sm, 1)))));
   reg<<<grid, tb, 0, s>>>(a);
@@ -1403,6 +1446,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamSynchronize(c->h2d_stream);
     fmmcu::destroy_pipeline(c->pipe);
     c->pipe = nullptr;
+    multi_release(c);
     for (DevBuf* b : {&c->d_symseg, &c->d_syminfo, &c->d_tgt, &c->d_contrib, &c->d_cloff,
                       &c->d_clcnt, &c->d_clbase, &c->d_cubtmp})
       b->release();

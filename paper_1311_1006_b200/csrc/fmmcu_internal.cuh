@@ -199,6 +199,7 @@ struct fmmcu_ctx {
   DevBuf d_symseg, d_syminfo, d_tgt, d_contrib, d_cloff, d_clcnt, d_clbase, d_cubtmp;
   HostBuf h_sym;
   bool staged = false;
+  uint64_t staged_src = 0;     // source slots uploaded by the last stage (halo-only for a shard)
   bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
   bool warp_items = false;     // work list built for p2p_warp_kernel
   int warp_e = 4;              // evals per lane of the warp kernel (choose_warp_e)
@@ -225,6 +226,11 @@ struct fmmcu_ctx {
   fmmcu_m2l_job m2l_job{};
   uint64_t m2l_ops = 0;
   double m2l_prep = 0.0;
+
+  // multi-GPU (fmm_multi.cu): the root's output mapped over IPC, NCCL comm
+  void* peer_out = nullptr;
+  void* nccl_comm = nullptr;
+  int nccl_rank = 0, nccl_world = 1;
 
   // device FMM pipeline state (fmm_device.cu), created on first use
   fmmcu::DevicePipeline* pipe = nullptr;
@@ -254,5 +260,7 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
 // Batched M2L on `stream` from device-resident arrays (see m2l_kernels.cuh).
 int m2l_table(fmmcu_ctx* c, int p, int kernel, cudaStream_t stream);
 int m2l_run(fmmcu_ctx* c, fmmcu::M2LArgs a, uint64_t nnz, cudaStream_t s);
+// close the peer output mapping and the NCCL communicator (fmm_multi.cu)
+void multi_release(fmmcu_ctx* c);
 
 }  // namespace fmmcu::detail

@@ -3,12 +3,14 @@
 The near field shards naturally: a target leaf's potentials
 depend only on its own evals and the sources of its strong list, so each
 rank evaluates a contiguous range of finest-level leaves (Z-ordered median
-cells, spatially compact) with the sources replicated, and the only data
-exchange is gathering the potential slices.  Ranges are balanced by pair
-work n_evals * |strong sources| (clustered strong lists vary 3000x), not by
-leaf count.  The gather is one NCCL all-gather of equal-size padded slices
-over NVLink (torch.distributed), so every rank ends with the full potential
-array in permuted eval order.
+cells, spatially compact) staging only the sources its strong lists read
+(halo-only), and the only data
+exchange is gathering the potential slices to the root.  Ranges are balanced
+by pair work n_evals * |strong sources| (clustered strong lists vary 3000x),
+not by leaf count.  The gather itself lives in the library
+(include/fmm_cuda.h, csrc/fmm_multi.cu): fused into the kernels' stores over
+NVLink (IPC-mapped root buffer), or one grouped NCCL send/recv of the
+slices; gather_slices_to_root restates the latter for CPU tests.
 """
 from __future__ import annotations
 
@@ -36,43 +38,42 @@ def eval_slices(ev_off: np.ndarray, cuts: np.ndarray):
     return [(int(ev_off[cuts[r]]), int(ev_off[cuts[r + 1]])) for r in range(len(cuts) - 1)]
 
 
-class PotentialGather:
-    """All-gather of per-rank potential slices into the full array.
+def leaf_work_prefix(pt_off, ev_off, s_off, s_idx) -> np.ndarray:
+    """Inclusive prefix [n_leaves + 1] of the per-leaf pair work
+    n_evals * |strong sources| (before self-skips): the balance key of
+    shard_cuts, from the leaf CSR alone (no staging needed)."""
+    pt_off = np.asarray(pt_off, dtype=np.int64)
+    s_off = np.asarray(s_off, dtype=np.int64)
+    s_idx = np.asarray(s_idx, dtype=np.int64)
+    npts = np.diff(pt_off)
+    S = np.zeros(len(npts), dtype=np.int64)
+    if len(s_idx):
+        cs = np.concatenate([[0], np.cumsum(npts[s_idx])])
+        S = cs[s_off[1:]] - cs[s_off[:-1]]
+    work = np.diff(np.asarray(ev_off, dtype=np.int64)) * S
+    return np.concatenate([[0], np.cumsum(work)]).astype(np.uint64)
 
-    ``full`` is a flat float64 tensor [2 * n_eval] (the rank writes its own
-    slice in place, e.g. the kernel output bound with bind_device_out).  The
-    pad buffers are allocated once so the gather is allocation-free inside a
-    timed loop."""
 
-    def __init__(self, slices, rank: int, full, group=None, via_host: bool = False):
-        import torch
+def gather_slices_to_root(full, slices, rank: int, root: int = 0, group=None):
+    """The gather the library does with one grouped ncclSend / ncclRecv
+    (fmmcu_nccl_gather_out), restated over torch.distributed point-to-point
+    so the protocol runs on gloo/CPU in tests: every rank sends its eval
+    slice of ``full`` (flat float64, [2 n_eval]) to the root, which receives
+    each slice in place at its own offset -- no padding, no staging copy."""
+    import torch.distributed as dist
 
-        self.slices = slices
-        self.rank = rank
-        self.world = len(slices)
-        self.full = full
-        self.group = group
-        self.maxlen = max(1, max(e1 - e0 for e0, e1 in slices)) * 2
-        # via_host: gloo test mode (several ranks sharing one GPU)
-        dev = "cpu" if via_host else full.device
-        self.send = torch.zeros(self.maxlen, dtype=full.dtype, device=dev)
-        self.recv = torch.zeros(self.maxlen * self.world, dtype=full.dtype, device=dev)
-
-    def bytes_moved(self) -> int:
-        return int(self.recv.numel() * self.recv.element_size())
-
-    def __call__(self):
-        import torch.distributed as dist
-
-        e0, e1 = self.slices[self.rank]
-        n = (e1 - e0) * 2
-        if n:
-            self.send[:n].copy_(self.full[2 * e0: 2 * e1])
-        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
-        for r, (a, b) in enumerate(self.slices):
-            if r == self.rank or b == a:
+    world = len(slices)
+    if rank == root:
+        reqs = []
+        for r in range(world):
+            a, b = slices[r]
+            if r == root or b == a:
                 continue
-            m = (b - a) * 2
-            self.full[2 * a: 2 * b].copy_(self.recv[r * self.maxlen: r * self.maxlen + m],
-                                          non_blocking=False)
-        return self.full
+            reqs.append(dist.irecv(full[2 * a: 2 * b], src=r, group=group))
+        for q in reqs:
+            q.wait()
+    else:
+        a, b = slices[rank]
+        if b > a:
+            dist.send(full[2 * a: 2 * b].contiguous(), dst=root, group=group)
+    return full

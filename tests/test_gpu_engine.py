@@ -192,3 +192,20 @@ def test_at3a_moves_levels_with_device_wait_signal():
     tr, _ = F.vortex_run(60_000, 8.0, 25, cfg, tuner="at3a")
     assert (tr[:12, 4] > 0).all()  # near-bound: positive wait
     assert tr[-1, 6] > 3, tr[:, 6]
+
+
+@pytest.mark.parametrize("dist,n,L", [("uniform", 300_000, 8), ("gauss8", 200_000, 8)])
+def test_engine_cuda_multi_context_shards_vs_pool(dist, n, L):
+    """CudaSettings.devices with several entries: the target leaves are split
+    into pair-work-balanced ranges, one context each, every context uploading
+    only its halo and writing its slice of the potentials; with three
+    contexts on the one test GPU (devices=(0, 0, 0)) the result must match
+    the CPU pool engine: identical counters, <= 1e-12 normwise."""
+    s = F.make_distribution(dist, n, 21)
+    e = F.EvalSet.self_of(s)
+    base = dict(n_levels=L, worker_threads=8)
+    ref = F.FmmEngine(F.FmmConfig(backend="pool", **base)).evaluate(s, e)
+    for devs in ((0, 0), (0, 0, 0)):
+        got = F.FmmEngine(F.FmmConfig(backend="cuda", devices=devs, **base)).evaluate(s, e)
+        assert got.counters == ref.counters, devs
+        assert normwise(F._c2(got.potentials), F._c2(ref.potentials)) <= 1e-12, devs

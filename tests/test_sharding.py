@@ -2,8 +2,10 @@
 
 Each rank evaluates its work-balanced leaf range with the CPU oracle (the
 GPU kernel is covered by test_gpu_p2p.py::test_leaf_shards_compose...), the
-slices are all-gathered with the same PotentialGather the bench uses, and the
-assembled array must equal the unsharded oracle result bit for bit."""
+slices go to the root with gather_slices_to_root -- the send/recv pattern the
+library's fmmcu_nccl_gather_out issues as one NCCL group -- and the assembled
+array must equal the unsharded oracle result bit for bit.  World sizes 2 and
+3 (an odd split leaves one rank with a short or empty slice)."""
 import os
 import socket
 
@@ -14,7 +16,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from conftest import ROOT
-from paper_1311_1006_b200.sharding import eval_slices, shard_cuts
+from paper_1311_1006_b200.sharding import (eval_slices, gather_slices_to_root, leaf_work_prefix,
+                                           shard_cuts)
 
 
 def _free_port():
@@ -49,15 +52,15 @@ def _worker(rank, world, port, result_path):
             S = sum(int(csr.pt_off[b + 1] - csr.pt_off[b])
                     for b in csr.s_idx[csr.s_off[tl]:csr.s_off[tl + 1]])
             work[tl + 1] = work[tl] + int(csr.ev_off[tl + 1] - csr.ev_off[tl]) * S
+        assert np.array_equal(work, leaf_work_prefix(csr.pt_off, csr.ev_off, csr.s_off, csr.s_idx))
         cuts = shard_cuts(work, world)
         slices = eval_slices(csr.ev_off, cuts)
         out, pairs = O.nearfield(csr, zp, mp_, yp, sid, leaf_begin=int(cuts[rank]),
                                  leaf_end=int(cuts[rank + 1]))
-        from paper_1311_1006_b200.sharding import PotentialGather
         full = torch.zeros(out.size, dtype=torch.float64)
         e0, e1 = slices[rank]
         full[2 * e0: 2 * e1] = torch.from_numpy(out.reshape(-1)[2 * e0: 2 * e1])
-        PotentialGather(slices, rank, full)()
+        gather_slices_to_root(full, slices, rank, root=0)
         tot = torch.tensor([pairs], dtype=torch.float64)
         dist.all_reduce(tot)
         if rank == 0:
@@ -66,9 +69,10 @@ def _worker(rank, world, port, result_path):
         dist.destroy_process_group()
 
 
-def test_two_rank_gather_equals_unsharded(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_gather_equals_unsharded(tmp_path, world):
     path = str(tmp_path / "res.npz")
-    mp.spawn(_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), path), nprocs=world, join=True)
     res = np.load(path)
     O, csr, zp, mp_, yp, sid = _case()
     want, wpairs = O.nearfield(csr, zp, mp_, yp, sid)
@@ -76,8 +80,8 @@ def test_two_rank_gather_equals_unsharded(tmp_path):
     assert np.array_equal(res["full"].view(np.uint64), want.reshape(-1).view(np.uint64))
     # the split is balanced by pair work, not by leaf count
     cuts, work = res["cuts"], res["work"].astype(np.float64)
-    halves = [work[cuts[1]] - work[cuts[0]], work[cuts[2]] - work[cuts[1]]]
-    assert abs(halves[0] - halves[1]) / work[-1] < 0.05
+    parts = [work[cuts[r + 1]] - work[cuts[r]] for r in range(world)]
+    assert (max(parts) - min(parts)) / work[-1] < 0.05
 
 
 def test_shard_cuts_properties():
