@@ -1307,20 +1307,18 @@ int m2l_run(fmmcu_ctx* c, M2LArgs a, uint64_t nnz, cudaStream_t s) {
   a.table = c->m_table.as<double>();
   // (p+2) log10|w| >= 250  <=>  |w|^2 >= 10^(500/(p+2))
   a.big_w2 = std::pow(10.0, 500.0 / double(a.p + 2));
-  // FMMCU_M2L=old | thread | warp (default): r1 per-target kernels, the
-  // thread-per-item register kernel, the warp-per-item kernel
-  static const int which = [] {
+  // FMMCU_M2L=old (or FMMCU_M2L_OLD=1): the r1 per-target kernels, for A/B
+  // runs.  (A warp-per-item variant -- lane = partner, rows staged with
+  // cp.async, shuffle-tree reduction -- measured 2.9 ms against 1.27 ms at
+  // 10M / L10 and was dropped.)
+  static const bool old = [] {
     const char* e = std::getenv("FMMCU_M2L");
-    if (m2l_old_kernel() || (e && std::strcmp(e, "old") == 0)) return 0;
-    if (e && std::strcmp(e, "thread") == 0) return 1;
-    return 2;
+    return m2l_old_kernel() || (e && std::strcmp(e, "old") == 0);
   }();
   int tb = 64;
   M2LKernelFn reg = nullptr;
-  if (which == 1) reg = a.kernel == 0 ? m2l_reg_for<true>(P1, &tb) : m2l_reg_for<false>(P1, &tb);
-  if (which == 2) reg = a.kernel == 0 ? m2l_warp_for<true>(P1, &tb) : m2l_warp_for<false>(P1, &tb);
-  const uint32_t chunk = which == 2 ? kM2LWarpChunk : kM2LChunk;
-  const uint32_t per_item = which == 2 ? 32u : 1u;  // threads per item
+  if (!old) reg = a.kernel == 0 ? m2l_reg_for<true>(P1, &tb) : m2l_reg_for<false>(P1, &tb);
+  const uint32_t chunk = kM2LChunk;
   if (!reg) {
     CU_TRY(c, m2l_set_const_table(c->m_table.as<double>(), P1, s));
     launch_m2l_targets(a, s);
@@ -1350,12 +1348,10 @@ int m2l_run(fmmcu_ctx* c, M2LArgs a, uint64_t nnz, cudaStream_t s) {
   a.items = c->m_items.as<uint4>();
   a.n_items = c->m_nitems.as<uint32_t>();
   a.partial = c->m_partial.as<double2>();
-  int dev_sms = 148, per_sm = 0;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
-  CU_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reg, tb, 0));
-  const uint64_t want = (max_items * per_item + tb - 1) / tb;
-  const uint32_t grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(
-      want, uint64_t(dev_sms) * uint64_t(std::max(per_sm, 1)))));
+  // one item per thread over a grid covering the item bound: the block
+  // scheduler balances the tail (a persistent grid measured 1.45 against
+  // 1.27 ms at 10M)
+  const uint32_t grid = uint32_t(std::max<uint64_t>(1, (max_items + tb - 1) / tb));
   reg<<<grid, tb, 0, s>>>(a);
   const uint64_t nred = uint64_t(nt) * P1;
   m2l_reduce_kernel<<<uint32_t((nred + 255) / 256), 256, 0, s>>>(off, nt, P1, a.partial, a.out);

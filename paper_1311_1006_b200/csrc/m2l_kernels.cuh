@@ -287,7 +287,8 @@ static __global__ void __launch_bounds__(TBK, 384 / TBK) m2l_thread_kernel(const
 // for 3.1M ops at 1M gauss8 against 0.4 ms for 3.5M uniform ops).  A chunk of
 // a split list writes its partial local to `partial`, and m2l_reduce_kernel
 // sums a target's chunks in chunk order (deterministic); an unsplit target
-// writes `out` directly.  Threads stride over the items (persistent grid).
+// writes `out` directly.  One thread per item (m2l_run sizes the grid to the
+// item bound; threads past the device count exit).
 //
 // Per item, one thread; per partner:
 //   pass 1: v_k = (-1)^(k+1) b_k w^(k+1) (harmonic) | (-1)^k b_k w^k (log)
@@ -399,7 +400,7 @@ m2l_reg_kernel(const M2LArgs a) {
   __shared__ double2 s_v[P1][TB];
   const int tid = threadIdx.x;
   const uint32_t n_items = *a.n_items;
-  for (uint32_t it = blockIdx.x * TB + tid; it < n_items; it += gridDim.x * TB) {
+  for (uint32_t it = blockIdx.x * TB + tid; it < n_items; it += gridDim.x * TB) {  // one pass when the grid covers the items
     const uint4 item = a.items[it];
 #pragma unroll
     for (int l = 0; l < P1; ++l) s_c[l][tid] = make_double2(0.0, 0.0);
@@ -471,178 +472,6 @@ m2l_reg_kernel(const M2LArgs a) {
                                          : a.partial + (size_t)item.w * P1;
 #pragma unroll
     for (int l = 0; l < P1; ++l) o[l] = s_c[l][tid];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-per-item M2L (the default): an item is <= 32 weak partners of one
-// target box (kM2LWarpChunk; longer lists are split as above), lane j owns
-// partner j.
-//
-//  * the warp stages its partners' coefficient rows in shared memory with
-//    coalesced loads (lane k of row j reads b_j[k]: one 16(p+1)-byte run per
-//    row) -- the thread-per-target kernel gathered them lane by lane, 32
-//    cache lines per load instruction, and ncu showed L1/TEX at 82% while
-//    the FP64 pipe idled;
-//  * each lane runs its partner's translation entirely in registers: v_k
-//    formed on the fly from its row (k-outer), acc_l += T[k][l] v_k into
-//    2(p+1) independent FMA chains, then acc_l *= w^l;
-//  * the target's local is the sum over the warp's lanes, reduced with a
-//    fixed shuffle tree (deterministic), and lane l stores coefficient l --
-//    one coalesced store per item, no per-partner shared-memory traffic.
-constexpr uint32_t kM2LWarpChunk = 32;
-
-template <int P1>
-struct M2LWarpShape {
-  static constexpr int ROW = P1 + 1;  // padded row stride (double2): conflict-light LDS.128
-  static constexpr int WARPS = P1 <= 22 ? 4 : 2;  // 32 rows per warp in static shared memory
-  // 2(p+1) independent FMA chains per lane carry the latency, so residency
-  // is traded for registers: no spills of the accumulators
-  static constexpr int MINB = P1 <= 22 ? 2 : 4;
-};
-
-// acc[L] += T[K][L] v over all L of one row K
-template <bool HARM, int K, int... Ls>
-__device__ __forceinline__ void m2l_wrow(const double2 v, double* ar, double* ai,
-                                         std::integer_sequence<int, Ls...>) {
-  (constexpr_fma_pair(M2LT<HARM, K, Ls>::value, v, ar[Ls], ai[Ls]), ...);
-}
-
-// k-outer: v_k = sgn_k b_k wp, wp *= w, then the row update
-template <bool HARM, int P1, int... Ks>
-__device__ __forceinline__ void m2l_wrows(const double2* row, const double2 w, double* ar,
-                                          double* ai, std::integer_sequence<int, Ks...>) {
-  double2 wp = HARM ? w : make_double2(1.0, 0.0);  // w^(k+1) | w^k
-  (
-      [&] {
-        constexpr int k = Ks;
-        if constexpr (HARM || k > 0) {
-          const double2 bk = row[k];
-          constexpr double sgn = HARM ? ((k & 1) ? 1.0 : -1.0) : ((k & 1) ? -1.0 : 1.0);
-          const double2 v = cmul(make_double2(sgn * bk.x, sgn * bk.y), wp);
-          m2l_wrow<HARM, k>(v, ar, ai, std::make_integer_sequence<int, P1>{});
-        }
-        if (k + 1 < P1) wp = cmul(wp, w);
-      }(),
-      ...);
-}
-
-template <int P1, bool HARM>
-static __global__ void __launch_bounds__(M2LWarpShape<P1>::WARPS * 32, M2LWarpShape<P1>::MINB)
-m2l_warp_kernel(const M2LArgs a) {
-  constexpr int ROW = M2LWarpShape<P1>::ROW;
-  constexpr int kM2LWarpWarps = M2LWarpShape<P1>::WARPS;
-  __shared__ double2 s_row[kM2LWarpWarps][32 * ROW];
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  double2* rows = s_row[wid];
-  const uint32_t n_items = *a.n_items;
-  const uint32_t gw = blockIdx.x * kM2LWarpWarps + wid, nw = gridDim.x * kM2LWarpWarps;
-  for (uint32_t it = gw; it < n_items; it += nw) {
-    const uint4 item = a.items[it];
-    const uint32_t n = item.z - item.y;  // <= 32 partners
-    const uint32_t sb = lane < n ? __ldg(a.weak_idx + item.y + lane) : 0u;
-    // coalesced staging: row j = coefficients of partner j
-    __syncwarp();
-    for (uint32_t j = 0; j < n; ++j) {
-      const uint32_t sj = __shfl_sync(0xffffffffu, sb, j);
-      if (lane < P1) rows[j * ROW + lane] = __ldg(a.coeffs + (size_t)sj * P1 + lane);
-    }
-    __syncwarp();
-    double ar[P1], ai[P1];
-#pragma unroll
-    for (int l = 0; l < P1; ++l) ar[l] = ai[l] = 0.0;
-    if (lane < n) {
-      const double2 ct = a.centers[a.target_box[item.x]];
-      const double2 cs = __ldg(a.centers + sb);
-      const double2 z0 = make_double2(cs.x - ct.x, cs.y - ct.y);
-      const double2* row = rows + lane * ROW;
-      if (z0.x == 0.0 && z0.y == 0.0) {
-        atomicOr(a.singular, 1);
-      } else {
-        const double zz = fma(z0.x, z0.x, z0.y * z0.y);
-        const double2 w = make_double2(z0.x / zz, -z0.y / zz);
-        const double w2 = fma(w.x, w.x, w.y * w.y);
-        if (w2 >= a.big_w2) {
-          // rare (nearly coincident centres): progressive chains, as the
-          // reference's long double branch avoids overflow
-#pragma unroll 1
-          for (int l = 0; l < P1; ++l) {
-            double2 acc = make_double2(0.0, 0.0);
-            for (int k = HARM ? 0 : 1; k < P1; ++k) {
-              const double2 bk = row[k];
-              const double sgn = HARM ? ((k & 1) ? 1.0 : -1.0) : ((k & 1) ? -1.0 : 1.0);
-              double2 val = make_double2(sgn * bk.x, sgn * bk.y);
-              for (int r = 0; r < (HARM ? k + 1 : k); ++r) val = cmul(val, w);
-              const double tk = m2l_t<HARM>(k, l);
-              acc.x = fma(tk, val.x, acc.x);
-              acc.y = fma(tk, val.y, acc.y);
-            }
-            if (!HARM) {
-              const double2 a0 = row[0];
-              if (l == 0) {
-                const double lr = 0.5 * log(zz);
-                const double th = atan2(-z0.y, -z0.x);
-                acc.x += a0.x * lr - a0.y * th;
-                acc.y += a0.x * th + a0.y * lr;
-              } else {
-                acc.x -= a0.x / (double)l;
-                acc.y -= a0.y / (double)l;
-              }
-            }
-            if (HARM || l > 0)
-              for (int r = 0; r < l; ++r) acc = cmul(acc, w);
-#pragma unroll
-            for (int q = 0; q < P1; ++q)
-              if (q == l) {
-                ar[q] = acc.x;
-                ai[q] = acc.y;
-              }
-          }
-        } else {
-          m2l_wrows<HARM, P1>(row, w, ar, ai, std::make_integer_sequence<int, P1>{});
-          const double2 a0 = HARM ? make_double2(0.0, 0.0) : row[0];
-          double2 wl = w;
-#pragma unroll
-          for (int l = 0; l < P1; ++l) {
-            double2 acc = make_double2(ar[l], ai[l]);
-            if (!HARM && l == 0) {
-              const double lr = 0.5 * log(zz);
-              const double th = atan2(-z0.y, -z0.x);
-              acc = make_double2(acc.x + (a0.x * lr - a0.y * th), acc.y + (a0.x * th + a0.y * lr));
-            } else {
-              if (!HARM) {
-                acc.x -= a0.x / (double)l;
-                acc.y -= a0.y / (double)l;
-              }
-              if (l > 0) {
-                acc = cmul(wl, acc);
-                if (l + 1 < P1) wl = cmul(wl, w);
-              }
-            }
-            ar[l] = acc.x;
-            ai[l] = acc.y;
-          }
-        }
-      }
-    }
-    // sum over the warp's partners (fixed tree: deterministic); lane l keeps l
-    double2 mine = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int l = 0; l < P1; ++l) {
-      double x = ar[l], y = ai[l];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        x += __shfl_down_sync(0xffffffffu, x, o);
-        y += __shfl_down_sync(0xffffffffu, y, o);
-      }
-      x = __shfl_sync(0xffffffffu, x, 0);
-      y = __shfl_sync(0xffffffffu, y, 0);
-      if (lane == (l & 31)) mine = make_double2(x, y);
-    }
-    double2* o = (item.w == 0xFFFFFFFFu) ? a.out + (size_t)item.x * P1
-                                         : a.partial + (size_t)item.w * P1;
-    if (lane < P1) o[lane] = mine;
   }
 }
 
@@ -724,27 +553,6 @@ static inline M2LKernelFn m2l_reg_pick(int* tb) {
   *tb = M2LRegShape<P1>::TB;
   return m2l_reg_kernel<P1, HARM>;
 }
-template <int P1, bool HARM>
-static inline M2LKernelFn m2l_warp_pick(int* tb) {
-  *tb = M2LWarpShape<P1>::WARPS * 32;
-  return m2l_warp_kernel<P1, HARM>;
-}
-// the warp kernel for an order (P1 <= 32: lane l stores coefficient l)
-template <bool HARM>
-static inline M2LKernelFn m2l_warp_for(int P1, int* tb) {
-  switch (P1) {
-    case 12: return m2l_warp_pick<12, HARM>(tb);
-    case 14: return m2l_warp_pick<14, HARM>(tb);
-    case 16: return m2l_warp_pick<16, HARM>(tb);
-    case 18: return m2l_warp_pick<18, HARM>(tb);
-    case 20: return m2l_warp_pick<20, HARM>(tb);
-    case 22: return m2l_warp_pick<22, HARM>(tb);
-    case 25: return m2l_warp_pick<25, HARM>(tb);
-    case 29: return m2l_warp_pick<29, HARM>(tb);
-    default: return nullptr;
-  }
-}
-
 template <bool HARM>
 static inline M2LKernelFn m2l_reg_for(int P1, int* tb) {
   switch (P1) {

@@ -1,0 +1,237 @@
+// fmm-b200 — the P2P work list built on the device.
+//
+// The near-field kernels consume work items (an eval block of one target
+// leaf x a run of its strong list, see P2PItem) and, for leaves whose pair
+// work exceeds a budget, partial-sum slots reduced by p2p_finalize_kernel.
+// r1 built that list on the host from a host copy of the finest CSR
+// (build_worklist, fmmcu.cu): ~1.5 ms of host time at 10M leaves' worth of
+// strong lists, on the critical path of the reference-facing launch and,
+// after a CSR download, of the device pipeline.  Here the same list -- the
+// same items in the same order -- comes from kernels over the device CSR
+// (the loop being replaced is the leaf loop of nearfield_run,
+// proj/src/backend.cpp:73-89, cut into items):
+//
+//   wl_leaf_kernel     per leaf: S (sources of its strong list), the last
+//                      source slot it reads (-> upload group), pair work, and
+//                      the integer lane-cost model of E = 4 / 5 evals per lane
+//   (CUB sum)          total pair work -> split budget
+//   wl_setup_kernel    E, max_ev and the budget into the device header
+//   (CUB radix sort)   leaves stably ordered by group (5-bit key)
+//   wl_count_kernel    items / finals / partial evals per leaf, sorted order
+//   (CUB scans)        their offsets
+//   wl_bounds_kernel   per-group item and final ranges into the header
+//   -- one small D2H of the header; the host sizes the buffers --
+//   wl_fill_kernel     the items and finals at their offsets
+//
+// Every count is an integer, so the list is identical run to run (the E
+// choice included) and identical to the host builder's.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "p2p_kernels.cuh"
+#include "p2p_warp.cuh"
+
+namespace fmmcu {
+
+constexpr int kWlMaxGroups = 32;
+
+// device-written, host-read summary of a device work list
+struct WlHead {
+  unsigned long long cost4, cost5;  // lane-cost model sums (choose E)
+  unsigned long long total_work;    // sum of n_evals * S over the range
+  unsigned long long budget;        // pair work per item before a block splits
+  uint32_t E, max_ev;
+  uint32_t n_items, n_fins, n_pevals, pad;
+  uint32_t grp_item[kWlMaxGroups + 1];
+  uint32_t grp_fin[kWlMaxGroups + 1];
+};
+
+struct WlGroups {
+  uint32_t K;                          // upload groups (1: everything resident)
+  uint32_t slot_end[kWlMaxGroups];     // group k holds source slots below slot_end[k]
+};
+
+__device__ __forceinline__ unsigned long long wl_lane_cost(uint32_t ntl, unsigned long long S,
+                                                           uint32_t E) {
+  if (!ntl || !S) return 0ull;
+  const uint32_t max_ev = kWarpSlots * E;
+  const uint32_t nblk = (ntl + max_ev - 1) / max_ev;
+  const uint32_t nt = (ntl + nblk - 1) / nblk;
+  const uint32_t G = (nt + E - 1) / E;
+  const uint32_t K = 32 / G;
+  return (unsigned long long)nblk * E * ((S + K - 1) / K);
+}
+
+static __global__ void wl_leaf_kernel(const uint32_t* __restrict__ pt_off,
+                                      const uint32_t* __restrict__ ev_off,
+                                      const uint32_t* __restrict__ s_off,
+                                      const uint32_t* __restrict__ s_idx, uint32_t lb, uint32_t np,
+                                      const WlGroups g, uint32_t* __restrict__ key,
+                                      uint32_t* __restrict__ val,
+                                      unsigned long long* __restrict__ S_out,
+                                      unsigned long long* __restrict__ work,
+                                      WlHead* __restrict__ head) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long c4 = 0, c5 = 0;
+  if (i < np) {
+    const uint32_t t = lb + i;
+    unsigned long long S = 0;
+    uint32_t need = pt_off[t + 1];
+    for (uint32_t q = s_off[t]; q < s_off[t + 1]; ++q) {
+      const uint32_t sb = s_idx[q];
+      const uint32_t e1 = pt_off[sb + 1];
+      S += e1 - pt_off[sb];
+      need = max(need, e1);
+    }
+    uint32_t k = 0;
+    while (k + 1 < g.K && g.slot_end[k] < need) ++k;
+    const uint32_t ntl = ev_off[t + 1] - ev_off[t];
+    key[i] = k;
+    val[i] = i;
+    S_out[i] = S;
+    work[i] = (unsigned long long)ntl * S;
+    c4 = wl_lane_cost(ntl, S, 4);
+    c5 = wl_lane_cost(ntl, S, 5);
+  }
+  // integer sums: the E choice does not depend on the summation order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c4 += __shfl_down_sync(0xffffffffu, c4, o);
+    c5 += __shfl_down_sync(0xffffffffu, c5, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (c4 | c5)) {
+    atomicAdd(&head->cost4, c4);
+    atomicAdd(&head->cost5, c5);
+  }
+}
+
+// force_e: 0 = model, else 4 / 5 (FMMCU_P2P_E)
+static __global__ void wl_setup_kernel(WlHead* head, int force_e) {
+  const uint32_t E = force_e == 4 || force_e == 5 ? uint32_t(force_e)
+                                                 : (head->cost5 < head->cost4 ? 5u : 4u);
+  head->E = E;
+  head->max_ev = kWarpSlots * E;
+  const unsigned long long b = head->total_work / (148ull * 16ull);
+  head->budget = b > (1ull << 16) ? b : (1ull << 16);
+}
+
+// Items of leaf t (the host builder's leaf_items, fmmcu.cu): eval blocks of
+// <= max_ev evals, balanced; a block whose pair work exceeds the budget (and
+// has > 1 strong entry), or whose list exceeds 32 entries, is cut into
+// strong-list chunks with partial slots summed by p2p_finalize_kernel.
+// Counts only when it/fin are null.
+__device__ __forceinline__ void wl_leaf_items(uint32_t t, const uint32_t* __restrict__ pt_off,
+                                              const uint32_t* __restrict__ ev_off,
+                                              const uint32_t* __restrict__ s_off,
+                                              const uint32_t* __restrict__ s_idx,
+                                              unsigned long long S, uint32_t max_ev,
+                                              unsigned long long budget, P2PItem* it,
+                                              P2PFinal* fin, uint32_t pbase, uint32_t& n_items,
+                                              uint32_t& n_fins, uint32_t& n_pev) {
+  n_items = n_fins = n_pev = 0;
+  const uint32_t ntl = ev_off[t + 1] - ev_off[t];
+  const uint32_t sb0 = s_off[t], sb1 = s_off[t + 1];
+  const uint32_t nblk = (ntl + max_ev - 1) / max_ev;
+  for (uint32_t b = 0, e0 = 0; b < nblk; ++b) {
+    const uint32_t nt = (ntl - e0) / (nblk - b) + ((ntl - e0) % (nblk - b) ? 1u : 0u);
+    const uint32_t evb = ev_off[t] + e0;
+    e0 += nt;
+    const unsigned long long pairs = (unsigned long long)nt * S;
+    if ((pairs <= budget || sb1 - sb0 <= 1) && sb1 - sb0 <= uint32_t(kWarpMaxEntries) &&
+        S <= 0xFFFFFFFFull) {
+      if (it) it[n_items] = P2PItem{t, evb, nt, sb0, sb1, uint32_t(S), kNoSelf, 0};
+      ++n_items;
+      continue;
+    }
+    const unsigned long long spc = budget / nt > 0 ? budget / nt : 1ull;
+    const uint32_t base = pbase + n_pev;
+    uint32_t n_chunks = 0;
+    uint32_t q = sb0;
+    while (q < sb1) {
+      uint32_t q1 = q;
+      unsigned long long acc = 0;
+      while (q1 < sb1 && q1 - q < uint32_t(kWarpMaxEntries)) {
+        const uint32_t n = pt_off[s_idx[q1] + 1] - pt_off[s_idx[q1]];
+        if (acc != 0 && acc + n > spc) break;
+        acc += n;
+        ++q1;
+      }
+      if (it) it[n_items] = P2PItem{t, evb, nt, q, q1, uint32_t(acc), pbase + n_pev, 0};
+      ++n_items;
+      n_pev += nt;
+      ++n_chunks;
+      q = q1;
+    }
+    if (fin) fin[n_fins] = P2PFinal{evb, nt, base, n_chunks};
+    ++n_fins;
+  }
+}
+
+// counts in sorted (group) order: cnt[pos] = {items, fins, pevals}
+static __global__ void wl_count_kernel(const uint32_t* __restrict__ pt_off,
+                                       const uint32_t* __restrict__ ev_off,
+                                       const uint32_t* __restrict__ s_off,
+                                       const uint32_t* __restrict__ s_idx, uint32_t lb, uint32_t np,
+                                       const uint32_t* __restrict__ val_sorted,
+                                       const unsigned long long* __restrict__ S,
+                                       const WlHead* __restrict__ head,
+                                       uint32_t* __restrict__ ci, uint32_t* __restrict__ cf,
+                                       uint32_t* __restrict__ cp) {
+  const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos > np) return;
+  if (pos == np) {  // the exclusive scans run over np + 1 entries
+    ci[np] = cf[np] = cp[np] = 0;
+    return;
+  }
+  const uint32_t i = val_sorted[pos];
+  uint32_t a, b, c;
+  wl_leaf_items(lb + i, pt_off, ev_off, s_off, s_idx, S[i], head->max_ev, head->budget, nullptr,
+                nullptr, 0, a, b, c);
+  ci[pos] = a;
+  cf[pos] = b;
+  cp[pos] = c;
+}
+
+// group k = sorted positions [grp_pos[k], grp_pos[k+1]); header ranges
+static __global__ void wl_bounds_kernel(const uint32_t* __restrict__ key_sorted, uint32_t np,
+                                        uint32_t K, const uint32_t* __restrict__ io,
+                                        const uint32_t* __restrict__ fo,
+                                        const uint32_t* __restrict__ po, WlHead* __restrict__ head) {
+  const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos > np) return;
+  // groups starting at pos: (key[pos-1], key[pos]]  (pos == np closes the rest)
+  const int k0 = pos == 0 ? -1 : int(key_sorted[pos - 1]);
+  const int k1 = pos == np ? int(K) : int(key_sorted[pos]);
+  for (int k = k0 + 1; k <= k1; ++k) {
+    head->grp_item[k] = io[pos];
+    head->grp_fin[k] = fo[pos];
+  }
+  if (pos == np) {
+    head->n_items = io[np];
+    head->n_fins = fo[np];
+    head->n_pevals = po[np];
+  }
+}
+
+static __global__ void wl_fill_kernel(const uint32_t* __restrict__ pt_off,
+                                      const uint32_t* __restrict__ ev_off,
+                                      const uint32_t* __restrict__ s_off,
+                                      const uint32_t* __restrict__ s_idx, uint32_t lb, uint32_t np,
+                                      const uint32_t* __restrict__ val_sorted,
+                                      const unsigned long long* __restrict__ S,
+                                      const WlHead* __restrict__ head,
+                                      const uint32_t* __restrict__ io,
+                                      const uint32_t* __restrict__ fo,
+                                      const uint32_t* __restrict__ po, P2PItem* __restrict__ items,
+                                      P2PFinal* __restrict__ fins) {
+  const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= np) return;
+  const uint32_t i = val_sorted[pos];
+  uint32_t a, b, c;
+  wl_leaf_items(lb + i, pt_off, ev_off, s_off, s_idx, S[i], head->max_ev, head->budget,
+                items + io[pos], fins + fo[pos], po[pos], a, b, c);
+}
+
+}  // namespace fmmcu
