@@ -1006,13 +1006,18 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   P->tree_valid = true;
   const int L = P->L;
   const uint32_t nleaf = uint32_t(pow4(L - 1));
-  // the finest CSR goes to the host right away (d2h stream, pinned vectors):
-  // the host builds the P2P work list while the device permutes the inputs
-  // and starts the far field
+  // The P2P work list: by default built on the device from the finest CSR
+  // (p2p_worklist.cuh) on the d2h stream while this stream permutes the
+  // inputs and the far field starts, so the P2P kernels follow connectivity
+  // without a host round trip.  The mutual kernel (FMMCU_PIPE_SYM) and
+  // FMMCU_HOST_WL keep the host builder: the finest CSR goes to pinned host
+  // vectors right away and the host builds the list meanwhile.
   const LevelConnDev& fc = P->conn[L - 1];
-  {
+  const bool pipe_sym = self && P->layout_same && j->kernel == 0 && std::getenv("FMMCU_PIPE_SYM");
+  const bool host_wl = pipe_sym || std::getenv("FMMCU_HOST_WL") != nullptr;
+  CU_TRY(c, cudaEventRecord(ev[12], s));
+  if (host_wl) {
     cudaStream_t ds = c->d2h_stream;
-    CU_TRY(c, cudaEventRecord(ev[12], s));
     CU_TRY(c, cudaStreamWaitEvent(ds, ev[12], 0));
     P->h_pt.resize(nleaf + 1);
     P->h_evo.resize(nleaf + 1);
@@ -1054,22 +1059,8 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   CU_TRY(c, cudaEventRecord(ev[5], P->far));
   if (int rc = far_field(c, P, P->far, ev[6], ev[7])) return rc;
 
-  // ---- near field: host work list from the finest CSR, then the P2P kernels
-  CU_TRY(c, cudaEventSynchronize(ev[13]));
-  fmmcu_p2p_job pj{};
-  pj.n_leaves = nleaf;
-  pj.n_src = N;
-  pj.n_eval = M;
-  pj.pt_off = P->h_pt.data();
-  pj.ev_off = P->h_evo.data();
-  pj.strong_off = P->h_so.data();
-  pj.strong_idx = P->h_si.data();
-  pj.kernel = j->kernel;
-  pj.smoother = j->smoother;
-  pj.delta = j->delta;
-  pj.mode = FMMCU_MODE_FAST;
-  pj.leaf_begin = 0;
-  pj.leaf_end = nleaf;
+  // ---- near field: the work list (device, or host from the finest CSR), then
+  // the P2P kernels
   c->n_leaves = nleaf;
   c->n_src = N;
   c->n_eval = M;
@@ -1080,11 +1071,39 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   c->self_layout = false;
   c->ext_out = nullptr;
   c->group_k = 0;
-  // the mutual kernel saves ~0.6 ms of P2P here but its longer host work list
-  // sits on the critical path of a single evaluate; opt in with FMMCU_PIPE_SYM
-  c->sym_request = self && P->layout_same && j->kernel == 0 && std::getenv("FMMCU_PIPE_SYM");
-  if (int rc = build_worklist(c, &pj)) return rc;
-  if (int rc = stage_csr(c, &pj, true)) return rc;
+  if (!host_wl) {
+    cudaStream_t ws = c->d2h_stream;
+    CU_TRY(c, cudaStreamWaitEvent(ws, ev[12], 0));
+    if (int rc = stage_csr_dev(c, P->soff.as<uint32_t>() + P->off_base[L - 1],
+                               P->eoff.as<uint32_t>() + P->off_base[L - 1], fc.s_off.as<uint32_t>(),
+                               fc.s_idx.as<uint32_t>(), nleaf, fc.s_nnz, M, ws, ev[13]))
+      return rc;
+    CU_TRY(c, cudaStreamWaitEvent(s, ev[13], 0));
+    if (M) {  // eval records {x, y, self slot, strong entry of the self slot}
+      p2p_evrec_kernel<<<(nleaf + 7) / 8, 256, 0, s>>>(make_args(c), 0, nleaf,
+                                                       c->d_evr.as<double4>());
+      c->launches += 1;
+    }
+  } else {
+    CU_TRY(c, cudaEventSynchronize(ev[13]));
+    fmmcu_p2p_job pj{};
+    pj.n_leaves = nleaf;
+    pj.n_src = N;
+    pj.n_eval = M;
+    pj.pt_off = P->h_pt.data();
+    pj.ev_off = P->h_evo.data();
+    pj.strong_off = P->h_so.data();
+    pj.strong_idx = P->h_si.data();
+    pj.kernel = j->kernel;
+    pj.smoother = j->smoother;
+    pj.delta = j->delta;
+    pj.mode = FMMCU_MODE_FAST;
+    pj.leaf_begin = 0;
+    pj.leaf_end = nleaf;
+    c->sym_request = pipe_sym;
+    if (int rc = build_worklist(c, &pj)) return rc;
+    if (int rc = stage_csr(c, &pj, true)) return rc;
+  }
   CU_TRY(c, cudaEventRecord(ev[8], s));
   int nk = 0;
   if (int rc = run_kernels(c, 0, nleaf, FMMCU_MODE_FAST, &nk)) return rc;
@@ -1198,7 +1217,7 @@ int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {
   if (st) {
     const uint32_t nleaf = uint32_t(pow4(P->L - 1));
     const uint64_t hits = *c->h_hits.as<unsigned long long>();
-    st->p2p_pairs = c->leaf_work[nleaf] - hits;
+    st->p2p_pairs = (c->dev_wl ? c->dev_wl_total : c->leaf_work[nleaf]) - hits;
     st->m2l_ops = P->m2l_nnz;
     st->p2m_points = P->N;
     st->l2p_points = P->L >= 2 ? M : 0;

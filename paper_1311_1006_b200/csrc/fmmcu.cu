@@ -436,6 +436,7 @@ void par_prefix(T* v, int64_t n) {
 
 int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   Trace tr(c);
+  c->dev_wl = false;
   const uint32_t nl = j->n_leaves;
   c->ev_off.resize(nl + 1);
   c->leaf_work.resize(nl + 1);
@@ -766,6 +767,58 @@ int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   return FMMCU_OK;
 }
 
+// The job's finest CSR (pt_off, ev_off, strong_off, strong_idx) H2D on
+// `stream` into d_pt / d_ev / d_soff / d_sidx: DMA'd in place from page-locked
+// caller arrays, else through one pinned block.  Returns the bytes moved, or
+// ~0 on a CUDA error (c->err set).
+uint64_t upload_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, cudaStream_t stream) {
+  const uint32_t nl = j->n_leaves;
+  const uint32_t nnz = j->strong_off[nl];
+  auto fail = [&](cudaError_t e, const char* what) {
+    c->err = std::string(what) + ": " + cudaGetErrorString(e);
+    return ~0ull;
+  };
+  cudaError_t e;
+  if ((e = c->d_pt.ensure(size_t(nl + 1) * 4)) != cudaSuccess ||
+      (e = c->d_ev.ensure(size_t(nl + 1) * 4)) != cudaSuccess ||
+      (e = c->d_soff.ensure(size_t(nl + 1) * 4)) != cudaSuccess ||
+      (e = c->d_sidx.ensure(size_t(std::max(nnz, 1u)) * 4)) != cudaSuccess)
+    return fail(e, "csr buffers");
+  auto locked = [](const void* p) {
+    cudaPointerAttributes at{};
+    const bool ok = p && cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+                    at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  const size_t csr_bytes = size_t(nl + 1) * 12 + size_t(nnz) * 4;
+  if ((e = c->h_csr.ensure(csr_bytes)) != cudaSuccess) return fail(e, "csr staging");
+  unsigned char* hc = c->h_csr.as<unsigned char>();
+  size_t o = 0;
+  auto put = [&](const void* src, size_t bytes) -> const void* {
+    if (!bytes) return src;
+    if (locked(src)) return src;
+    par_memcpy(hc + o, src, bytes);
+    const void* at = hc + o;
+    o += bytes;
+    return at;
+  };
+  const void* s_pt = put(j->pt_off, size_t(nl + 1) * 4);
+  const void* s_ev = put(j->ev_off, size_t(nl + 1) * 4);
+  const void* s_so = put(j->strong_off, size_t(nl + 1) * 4);
+  const void* s_si = put(j->strong_idx, size_t(nnz) * 4);
+  if ((e = cudaMemcpyAsync(c->d_pt.p, s_pt, size_t(nl + 1) * 4, cudaMemcpyHostToDevice,
+                           stream)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(c->d_ev.p, s_ev, size_t(nl + 1) * 4, cudaMemcpyHostToDevice,
+                           stream)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(c->d_soff.p, s_so, size_t(nl + 1) * 4, cudaMemcpyHostToDevice,
+                           stream)) != cudaSuccess ||
+      (nnz && (e = cudaMemcpyAsync(c->d_sidx.p, s_si, size_t(nnz) * 4, cudaMemcpyHostToDevice,
+                                   stream)) != cudaSuccess))
+    return fail(e, "csr h2d");
+  return csr_bytes;
+}
+
 int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals) {
   const uint32_t nl = j->n_leaves, ne = j->n_eval;
   const uint32_t nnz = j->strong_off[nl];
@@ -787,37 +840,11 @@ int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals) {
   CU_TRY(c, c->h_hits.ensure(8));
   // CSR through one pinned block, unless the caller's arrays are page-locked
   // (then DMA'd in place); the work list is already in pinned vectors
-  auto locked = [](const void* p) {
-    cudaPointerAttributes at{};
-    const bool ok = p && cudaPointerGetAttributes(&at, p) == cudaSuccess &&
-                    at.type == cudaMemoryTypeHost;
-    cudaGetLastError();
-    return ok;
-  };
   const size_t ib = c->items.size() * sizeof(P2PItem), fb = c->fins.size() * sizeof(P2PFinal);
-  const size_t csr_bytes = size_t(nl + 1) * 12 + size_t(nnz) * 4;
-  CU_TRY(c, c->h_csr.ensure(csr_bytes));
-  unsigned char* hc = c->h_csr.as<unsigned char>();
-  size_t o = 0;
-  auto put = [&](const void* src, size_t bytes) -> const void* {
-    if (!bytes) return src;
-    if (locked(src)) return src;
-    par_memcpy(hc + o, src, bytes);
-    const void* at = hc + o;
-    o += bytes;
-    return at;
-  };
-  const void* s_pt = put(j->pt_off, size_t(nl + 1) * 4);
-  const void* s_ev = put(j->ev_off, size_t(nl + 1) * 4);
-  const void* s_so = put(j->strong_off, size_t(nl + 1) * 4);
-  const void* s_si = put(j->strong_idx, size_t(nnz) * 4);
+  const uint64_t csr_bytes = upload_csr(c, j, s);
+  if (csr_bytes == ~0ull) return FMMCU_ECUDA;
   c->h2d_bytes = uint64_t(c->n_src) * 32 + (self_layout ? 0 : uint64_t(ne) * 20) + csr_bytes +
                  ib + fb;
-
-  CU_TRY(c, cudaMemcpyAsync(c->d_pt.p, s_pt, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
-  CU_TRY(c, cudaMemcpyAsync(c->d_ev.p, s_ev, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
-  CU_TRY(c, cudaMemcpyAsync(c->d_soff.p, s_so, size_t(nl + 1) * 4, cudaMemcpyHostToDevice, s));
-  if (nnz) CU_TRY(c, cudaMemcpyAsync(c->d_sidx.p, s_si, size_t(nnz) * 4, cudaMemcpyHostToDevice, s));
   if (ib) CU_TRY(c, cudaMemcpyAsync(c->d_items.p, c->items.data(), ib, cudaMemcpyHostToDevice, s));
   if (fb) CU_TRY(c, cudaMemcpyAsync(c->d_fin.p, c->fins.data(), fb, cudaMemcpyHostToDevice, s));
   if (nnz) {
@@ -1006,7 +1033,6 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // the OpenMP team; all chunks first makes the work list upload wait for
   // the whole 320 MB (13.2 vs 10.4 ms per 10M step).
   static const int kPre = std::getenv("FMMCU_KPRE") ? std::atoi(std::getenv("FMMCU_KPRE")) : 2;
-  const int pre = direct_in ? std::min(K, std::max(0, kPre)) : 0;
   auto dma = [&](int64_t c0, int64_t c1) -> int {
     if (c1 <= c0) return FMMCU_OK;
     CU_TRY(c, cudaMemcpyAsync(c->d_zin.as<double>() + 2 * c0, z + 2 * c0, size_t(c1 - c0) * 16,
@@ -1016,18 +1042,50 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     if (partial) h2d += uint64_t(c1 - c0) * 32;
     return FMMCU_OK;
   };
-  for (int k = 0; k < pre; ++k) {
-    if (int rc = for_runs(k, dma)) return rc;
-    CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+  // Work list.  Default: built on the device (p2p_worklist.cuh) from the CSR,
+  // which leads the copy queue (~15 MB at 10M); page-locked source chunks
+  // queue right behind it, so the copy engine streams from t = 0 and the
+  // host only waits for one small header.  FMMCU_HOST_WL=1: the host builder
+  // (~1.5 ms at 10M) with the first kPre chunks moving meanwhile, the CSR and
+  // work list queued behind those only.
+  const bool dev_list = !std::getenv("FMMCU_HOST_WL");
+  int pre = 0;
+  if (dev_list) {
+    const uint64_t csr_bytes = upload_csr(c, j, h);
+    if (csr_bytes == ~0ull) return FMMCU_ECUDA;
+    h2d += csr_bytes;
+    CU_TRY(c, cudaEventRecord(c->ev_staged, h));
+    if (direct_in) {
+      pre = K;
+      for (int k = 0; k < K; ++k) {
+        if (int rc = for_runs(k, dma)) return rc;
+        CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+      }
+    }
+    CU_TRY(c, cudaStreamWaitEvent(s, c->ev_staged, 0));
+    WlGroups g{};
+    g.K = uint32_t(K);
+    for (int k = 0; k < K; ++k) g.slot_end[k] = j->pt_off[c->chunk_leaf[k + 1]];
+    c->n_strong = j->strong_off[nl];
+    if (int rc = build_worklist_dev(c, lb, le, g, s)) return rc;  // + the run table
+    tr.mark("csr + device worklist");
+  } else {
+    pre = direct_in ? std::min(K, std::max(0, kPre)) : 0;
+    for (int k = 0; k < pre; ++k) {
+      if (int rc = for_runs(k, dma)) return rc;
+      CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+    }
+    if (int rc = build_worklist(c, j)) return rc;
+    tr.mark("worklist");
+    if (int rc = stage_csr(c, j, false)) return rc;
+    // the remaining chunks queue behind the CSR and work list: on their own
+    // stream the copy engine would serve them first and starve the kernels
+    CU_TRY(c, cudaEventRecord(c->ev_staged, s));
+    CU_TRY(c, cudaStreamWaitEvent(h, c->ev_staged, 0));
+    h2d += c->h2d_bytes - uint64_t(ns) * 32 - (c->self_layout ? 0 : uint64_t(ne) * 20);
   }
-  if (int rc = build_worklist(c, j)) return rc;
-  tr.mark("worklist");
-  if (int rc = stage_csr(c, j, false)) return rc;
-  // the remaining chunks queue behind the CSR and work list: on their own
-  // stream the copy engine would serve them first and starve the kernels
-  CU_TRY(c, cudaEventRecord(c->ev_staged, s));
-  CU_TRY(c, cudaStreamWaitEvent(h, c->ev_staged, 0));
-  h2d += c->h2d_bytes - uint64_t(ns) * 32 - (c->self_layout ? 0 : uint64_t(ne) * 20);
+  c->run_eb = eb;
+  c->run_ee = ee;
   const P2PItem* items_dev = c->d_items.as<P2PItem>();
   const P2PFinal* fins_dev = c->d_fin.as<P2PFinal>();
   tr.mark("csr");
@@ -1109,8 +1167,19 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       p2p_evrec_kernel<<<(l1 - l0 + 7) / 8, 256, 0, s>>>(a, l0, l1, c->d_evr.as<double4>());
       ++nk;
     }
-    const uint32_t p0 = c->grp_pos[k], p1 = c->grp_pos[k + 1];
-    const uint32_t i0 = c->item_first[p0], i1 = c->item_first[p1];
+    uint32_t i0, i1, f0, f1;
+    if (c->dev_wl) {
+      i0 = c->dev_grp_item[k];
+      i1 = c->dev_grp_item[k + 1];
+      f0 = c->dev_grp_fin[k];
+      f1 = c->dev_grp_fin[k + 1];
+    } else {
+      const uint32_t p0 = c->grp_pos[k], p1 = c->grp_pos[k + 1];
+      i0 = c->item_first[p0];
+      i1 = c->item_first[p1];
+      f0 = c->fin_first[p0];
+      f1 = c->fin_first[p1];
+    }
     if (i1 > i0) {
       CU_TRY(c, cudaMemsetAsync(c->d_counter.p, 0, 8, s));
       P2PArgs aa = a;
@@ -1119,7 +1188,6 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s, c->warp_e);
       ++nk;
     }
-    const uint32_t f0 = c->fin_first[p0], f1 = c->fin_first[p1];
     if (f1 > f0) {
       p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(fins_dev + f0, f1 - f0,
                                                    c->d_partial.as<double2>(), c->out_dev);
@@ -1225,7 +1293,20 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
           c->d_tgt.as<double2>(), c->d_contrib.as<double2>(), c->out_ptr());
       ++n;
     } else {
-      const uint32_t i0 = c->item_first[lb], i1 = c->item_first[le];
+      uint32_t i0, i1, f0, f1;
+      if (c->dev_wl) {  // device-built list: its whole (ungrouped) range only
+        if (lb != c->dev_wl_lb || le != c->dev_wl_le || c->grouped)
+          return set_err(c, FMMCU_ESTATE, "device work list staged for another leaf range");
+        i0 = c->dev_grp_item.front();
+        i1 = c->dev_grp_item.back();
+        f0 = c->dev_grp_fin.front();
+        f1 = c->dev_grp_fin.back();
+      } else {
+        i0 = c->item_first[lb];
+        i1 = c->item_first[le];
+        f0 = c->fin_first[lb];
+        f1 = c->fin_first[le];
+      }
       if (i1 > i0) {
         P2PArgs aa = a;
         aa.items = c->d_items.as<P2PItem>() + i0;
@@ -1233,7 +1314,6 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
         dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s, c->warp_e);
         ++n;
       }
-      const uint32_t f0 = c->fin_first[lb], f1 = c->fin_first[le];
       if (f1 > f0) {
         p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(c->d_fin.as<P2PFinal>() + f0, f1 - f0,
                                                      c->d_partial.as<double2>(),
@@ -1451,10 +1531,11 @@ void fmmcu_destroy(fmmcu_ctx* c) {
                       &c->d_sidx, &c->d_items, &c->d_fin, &c->d_out, &c->d_partial, &c->d_hits, &c->d_seg, &c->d_counter, &c->d_evr,
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
                       &c->m_table, &c->m_out, &c->m_flag, &c->m_items, &c->m_iscan, &c->m_nitems,
-                      &c->m_partial, &c->m_cubtmp})
+                      &c->m_partial, &c->m_cubtmp, &c->d_wl_head, &c->d_wl_key, &c->d_wl_val,
+                      &c->d_wl_S, &c->d_wl_work, &c->d_wl_cnt, &c->d_wl_off})
       b->release();
     for (HostBuf* b : {&c->h_src, &c->h_evy, &c->h_eself, &c->h_out, &c->h_hits, &c->h_csr,
-                       &c->mh_out, &c->mh_flag})
+                       &c->mh_out, &c->mh_flag, &c->h_wl_head})
       b->release();
     for (cudaEvent_t ev : {c->ev_start, c->ev_end, c->ev_m2l0, c->ev_m2l1})
       if (ev) cudaEventDestroy(ev);
@@ -1511,7 +1592,8 @@ int fmmcu_p2p_launch(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     c->job = *j;
     c->run_lb = j->leaf_begin;
     c->run_le = j->leaf_end;
-    c->run_total_pairs = c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
+    c->run_total_pairs = c->dev_wl ? c->dev_wl_total
+                                   : c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
     c->prep_seconds = std::chrono::duration<double>(c->t_evstart - t0).count();
     c->inflight = true;
     return FMMCU_OK;
@@ -1600,11 +1682,13 @@ int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
       cudaEventElapsedTime(&b, c->ev_start, c->ev_group[k]);
       std::fprintf(stderr,
                    "[fmmcu] group %2d: chunk landed %8.3f ms, kernels done %8.3f ms, items %u\n",
-                   k, a, b, c->item_first[c->grp_pos[k + 1]] - c->item_first[c->grp_pos[k]]);
+                   k, a, b,
+                   c->dev_wl ? c->dev_grp_item[k + 1] - c->dev_grp_item[k]
+                             : c->item_first[c->grp_pos[k + 1]] - c->item_first[c->grp_pos[k]]);
     }
   }
   if (c->overlapped && !c->direct_out) {
-    const uint32_t eb = c->ev_off[c->run_lb], ee = c->ev_off[c->run_le];
+    const uint32_t eb = c->run_eb, ee = c->run_ee;
     if (ee > eb)
       par_memcpy(c->job.out + 2 * size_t(eb), c->h_out.as<double2>() + eb, size_t(ee - eb) * 16);
   }

@@ -18,6 +18,7 @@
 #include "p2p_kernels.cuh"
 #include "p2p_warp.cuh"
 #include "m2l_args.cuh"
+#include "p2p_worklist_types.cuh"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -175,6 +176,7 @@ struct fmmcu_ctx {
   std::vector<uint32_t> invperm;
   // host mirror of the staged job
   uint32_t n_leaves = 0, n_src = 0, n_eval = 0;
+  uint32_t n_strong = 0;  // strong entries of the finest CSR (device work list)
   int kernel = 0, smoother = 0, mode = 0;
   double delta = 0.0;
   std::vector<uint32_t> ev_off;        // host copy
@@ -198,6 +200,14 @@ struct fmmcu_ctx {
   uint64_t sym_slots = 0;               // contrib slots
   DevBuf d_symseg, d_syminfo, d_tgt, d_contrib, d_cloff, d_clcnt, d_clbase, d_cubtmp;
   HostBuf h_sym;
+  // device-built work list (worklist_dev.cu): items / fins for [dev_wl_lb,
+  // dev_wl_le) only, group ranges in dev_grp_item / dev_grp_fin
+  bool dev_wl = false;
+  uint32_t dev_wl_lb = 0, dev_wl_le = 0;
+  uint64_t dev_wl_total = 0;  // sum of n_evals * |strong sources| over the range
+  std::vector<uint32_t> dev_grp_item, dev_grp_fin;
+  DevBuf d_wl_head, d_wl_key, d_wl_val, d_wl_S, d_wl_work, d_wl_cnt, d_wl_off;
+  HostBuf h_wl_head;
   bool staged = false;
   uint64_t staged_src = 0;     // source slots uploaded by the last stage (halo-only for a shard)
   bool self_layout = false;    // eval e is source slot e (EvalSet::self_of, perm == eval_perm)
@@ -212,6 +222,7 @@ struct fmmcu_ctx {
   bool inflight = false;
   fmmcu_p2p_job job{};
   uint32_t run_lb = 0, run_le = 0;
+  uint32_t run_eb = 0, run_ee = 0;  // eval slots of the in-flight overlapped launch
   double prep_seconds = 0.0;
   Clock::time_point t_evstart{};
   uint64_t run_total_pairs = 0;
@@ -251,6 +262,19 @@ int set_err(fmmcu_ctx* c, int code, const std::string& msg);
 P2PArgs make_args(fmmcu_ctx* c);
 // Work list of a job from its host CSR (pt_off, ev_off, strong_off, strong_idx).
 int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j);
+// Work list built on the device from the CSR already in d_pt / d_ev / d_soff /
+// d_sidx (c->n_leaves leaves, c->n_strong entries), over leaves [lb, le),
+// grouped by upload chunk when g.K > 1 (worklist_dev.cu); also fills the run
+// table d_seg.  Same items as build_worklist; synchronizes `s` once.
+// The job's CSR H2D on `stream` (in place when page-locked); returns the
+// bytes moved, ~0 on error.
+uint64_t upload_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, cudaStream_t stream);
+int build_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g, cudaStream_t s);
+// Device-resident CSR -> context staging, run table and device work list on
+// stream `w` (records `done` there); eval records are left to the caller.
+int stage_csr_dev(fmmcu_ctx* c, const uint32_t* pt, const uint32_t* ev, const uint32_t* so,
+                  const uint32_t* si, uint32_t nl, uint32_t nnz, uint32_t ne, cudaStream_t w,
+                  cudaEvent_t done);
 // Device buffers for the CSR + work list, their H2D, the run table and the
 // eval records (needs d_src, d_evy, d_eself filled unless c->self_layout).
 int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals);

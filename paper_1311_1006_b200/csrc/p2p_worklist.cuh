@@ -11,6 +11,7 @@
 // (the loop being replaced is the leaf loop of nearfield_run,
 // proj/src/backend.cpp:73-89, cut into items):
 //
+//   (p2p_segments_kernel, run table seg[q] = (first slot, n) per strong entry)
 //   wl_leaf_kernel     per leaf: S (sources of its strong list), the last
 //                      source slot it reads (-> upload group), pair work, and
 //                      the integer lane-cost model of E = 4 / 5 evals per lane
@@ -25,6 +26,12 @@
 //
 // Every count is an integer, so the list is identical run to run (the E
 // choice included) and identical to the host builder's.
+//
+// One warp per leaf, reading the run table coalesced: a clustered tree has
+// strong lists of thousands of entries, and one thread walking such a list
+// through dependent pt_off[s_idx[q]] gathers took milliseconds (1M gauss8,
+// L = 8: 3 ms over the host builder).  The greedy strong-list chunking of a
+// split block becomes a warp scan + ballot per chunk of <= 32 entries.
 #pragma once
 
 #include <cstdint>
@@ -32,26 +39,9 @@
 
 #include "p2p_kernels.cuh"
 #include "p2p_warp.cuh"
+#include "p2p_worklist_types.cuh"
 
 namespace fmmcu {
-
-constexpr int kWlMaxGroups = 32;
-
-// device-written, host-read summary of a device work list
-struct WlHead {
-  unsigned long long cost4, cost5;  // lane-cost model sums (choose E)
-  unsigned long long total_work;    // sum of n_evals * S over the range
-  unsigned long long budget;        // pair work per item before a block splits
-  uint32_t E, max_ev;
-  uint32_t n_items, n_fins, n_pevals, pad;
-  uint32_t grp_item[kWlMaxGroups + 1];
-  uint32_t grp_fin[kWlMaxGroups + 1];
-};
-
-struct WlGroups {
-  uint32_t K;                          // upload groups (1: everything resident)
-  uint32_t slot_end[kWlMaxGroups];     // group k holds source slots below slot_end[k]
-};
 
 __device__ __forceinline__ unsigned long long wl_lane_cost(uint32_t ntl, unsigned long long S,
                                                            uint32_t E) {
@@ -64,46 +54,71 @@ __device__ __forceinline__ unsigned long long wl_lane_cost(uint32_t ntl, unsigne
   return (unsigned long long)nblk * E * ((S + K - 1) / K);
 }
 
+constexpr unsigned kFull = 0xffffffffu;
+
+// Over every leaf of the job (the E choice and the split budget are
+// whole-job quantities, as in the host builder, so a shard's items equal the
+// full job's items of its leaves); key / val / S only for leaves in [lb, le).
+// One warp per leaf.
 static __global__ void wl_leaf_kernel(const uint32_t* __restrict__ pt_off,
                                       const uint32_t* __restrict__ ev_off,
                                       const uint32_t* __restrict__ s_off,
-                                      const uint32_t* __restrict__ s_idx, uint32_t lb, uint32_t np,
-                                      const WlGroups g, uint32_t* __restrict__ key,
+                                      const uint2* __restrict__ seg, uint32_t nl, uint32_t lb,
+                                      uint32_t le, const WlGroups g, uint32_t* __restrict__ key,
                                       uint32_t* __restrict__ val,
                                       unsigned long long* __restrict__ S_out,
                                       unsigned long long* __restrict__ work,
                                       WlHead* __restrict__ head) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   unsigned long long c4 = 0, c5 = 0;
-  if (i < np) {
-    const uint32_t t = lb + i;
+  if (t < nl) {
     unsigned long long S = 0;
-    uint32_t need = pt_off[t + 1];
-    for (uint32_t q = s_off[t]; q < s_off[t + 1]; ++q) {
-      const uint32_t sb = s_idx[q];
-      const uint32_t e1 = pt_off[sb + 1];
-      S += e1 - pt_off[sb];
-      need = max(need, e1);
+    uint32_t need = lane == 0 ? pt_off[t + 1] : 0u;
+    for (uint32_t q = s_off[t] + lane; q < s_off[t + 1]; q += 32) {
+      const uint2 r = seg[q];
+      S += r.y;
+      need = max(need, r.x + r.y);
     }
-    uint32_t k = 0;
-    while (k + 1 < g.K && g.slot_end[k] < need) ++k;
-    const uint32_t ntl = ev_off[t + 1] - ev_off[t];
-    key[i] = k;
-    val[i] = i;
-    S_out[i] = S;
-    work[i] = (unsigned long long)ntl * S;
-    c4 = wl_lane_cost(ntl, S, 4);
-    c5 = wl_lane_cost(ntl, S, 5);
-  }
-  // integer sums: the E choice does not depend on the summation order
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    c4 += __shfl_down_sync(0xffffffffu, c4, o);
-    c5 += __shfl_down_sync(0xffffffffu, c5, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      S += __shfl_xor_sync(kFull, S, o);
+      need = max(need, __shfl_xor_sync(kFull, need, o));
+    }
+    if (lane == 0) {
+      const uint32_t ntl = ev_off[t + 1] - ev_off[t];
+      work[t] = (unsigned long long)ntl * S;
+      c4 = wl_lane_cost(ntl, S, 4);
+      c5 = wl_lane_cost(ntl, S, 5);
+      if (t >= lb && t < le) {
+        uint32_t k = 0;
+        while (k + 1 < g.K && g.slot_end[k] < need) ++k;
+        const uint32_t i = t - lb;
+        key[i] = k;
+        val[i] = i;
+        S_out[i] = S;
+      }
+    }
   }
-  if ((threadIdx.x & 31) == 0 && (c4 | c5)) {
-    atomicAdd(&head->cost4, c4);
-    atomicAdd(&head->cost5, c5);
+  // integer sums over the block's leaves: the E choice does not depend on
+  // the summation order
+  __shared__ unsigned long long s4[8], s5[8];
+  const uint32_t w = threadIdx.x >> 5;
+  if (lane == 0) {
+    s4[w] = c4;
+    s5[w] = c5;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long a4 = 0, a5 = 0;
+    for (uint32_t i = 0; i < (blockDim.x >> 5); ++i) {
+      a4 += s4[i];
+      a5 += s5[i];
+    }
+    if (a4 | a5) {
+      atomicAdd(&head->cost4, a4);
+      atomicAdd(&head->cost5, a5);
+    }
   }
 }
 
@@ -117,19 +132,22 @@ static __global__ void wl_setup_kernel(WlHead* head, int force_e) {
   head->budget = b > (1ull << 16) ? b : (1ull << 16);
 }
 
-// Items of leaf t (the host builder's leaf_items, fmmcu.cu): eval blocks of
-// <= max_ev evals, balanced; a block whose pair work exceeds the budget (and
-// has > 1 strong entry), or whose list exceeds 32 entries, is cut into
-// strong-list chunks with partial slots summed by p2p_finalize_kernel.
-// Counts only when it/fin are null.
-__device__ __forceinline__ void wl_leaf_items(uint32_t t, const uint32_t* __restrict__ pt_off,
-                                              const uint32_t* __restrict__ ev_off,
+// Items of leaf t, by the whole warp (the host builder's leaf_items,
+// fmmcu.cu): eval blocks of <= max_ev evals, balanced; a block whose pair
+// work exceeds the budget (and has > 1 strong entry), or whose list exceeds
+// 32 entries, is cut greedily into strong-list chunks -- entries are added
+// while the chunk is still empty of sources or stays within budget / nt
+// sources, at most 32 per chunk -- with partial slots summed by
+// p2p_finalize_kernel.  Lane 0 writes; counts only when it/fin are null.
+// Returns the counts in every lane.
+__device__ __forceinline__ void wl_leaf_items(uint32_t t, const uint32_t* __restrict__ ev_off,
                                               const uint32_t* __restrict__ s_off,
-                                              const uint32_t* __restrict__ s_idx,
+                                              const uint2* __restrict__ seg,
                                               unsigned long long S, uint32_t max_ev,
                                               unsigned long long budget, P2PItem* it,
                                               P2PFinal* fin, uint32_t pbase, uint32_t& n_items,
                                               uint32_t& n_fins, uint32_t& n_pev) {
+  const uint32_t lane = threadIdx.x & 31;
   n_items = n_fins = n_pev = 0;
   const uint32_t ntl = ev_off[t + 1] - ev_off[t];
   const uint32_t sb0 = s_off[t], sb1 = s_off[t + 1];
@@ -141,57 +159,65 @@ __device__ __forceinline__ void wl_leaf_items(uint32_t t, const uint32_t* __rest
     const unsigned long long pairs = (unsigned long long)nt * S;
     if ((pairs <= budget || sb1 - sb0 <= 1) && sb1 - sb0 <= uint32_t(kWarpMaxEntries) &&
         S <= 0xFFFFFFFFull) {
-      if (it) it[n_items] = P2PItem{t, evb, nt, sb0, sb1, uint32_t(S), kNoSelf, 0};
+      if (it && lane == 0) it[n_items] = P2PItem{t, evb, nt, sb0, sb1, uint32_t(S), kNoSelf, 0};
       ++n_items;
       continue;
     }
     const unsigned long long spc = budget / nt > 0 ? budget / nt : 1ull;
     const uint32_t base = pbase + n_pev;
     uint32_t n_chunks = 0;
-    uint32_t q = sb0;
-    while (q < sb1) {
-      uint32_t q1 = q;
-      unsigned long long acc = 0;
-      while (q1 < sb1 && q1 - q < uint32_t(kWarpMaxEntries)) {
-        const uint32_t n = pt_off[s_idx[q1] + 1] - pt_off[s_idx[q1]];
-        if (acc != 0 && acc + n > spc) break;
-        acc += n;
-        ++q1;
+    for (uint32_t q = sb0; q < sb1;) {
+      const uint32_t qq = q + lane;
+      const unsigned long long n = qq < sb1 ? seg[qq].y : 0ull;
+      unsigned long long incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= uint32_t(o)) incl += v;
       }
-      if (it) it[n_items] = P2PItem{t, evb, nt, q, q1, uint32_t(acc), pbase + n_pev, 0};
+      // the lanes taken form a prefix: the chunk is empty of sources before
+      // the entry, or the entry keeps it within spc sources
+      const bool take = qq < sb1 && (incl - n == 0 || incl <= spc);
+      const uint32_t len = __popc(__ballot_sync(kFull, take));  // >= 1: lane 0 always takes
+      const unsigned long long acc = __shfl_sync(kFull, incl, len - 1);
+      if (it && lane == 0)
+        it[n_items] = P2PItem{t, evb, nt, q, q + len, uint32_t(acc), pbase + n_pev, 0};
       ++n_items;
       n_pev += nt;
       ++n_chunks;
-      q = q1;
+      q += len;
     }
-    if (fin) fin[n_fins] = P2PFinal{evb, nt, base, n_chunks};
+    if (fin && lane == 0) fin[n_fins] = P2PFinal{evb, nt, base, n_chunks};
     ++n_fins;
   }
 }
 
-// counts in sorted (group) order: cnt[pos] = {items, fins, pevals}
-static __global__ void wl_count_kernel(const uint32_t* __restrict__ pt_off,
-                                       const uint32_t* __restrict__ ev_off,
+// counts in sorted (group) order: cnt[pos] = {items, fins, pevals}; one warp
+// per position
+static __global__ void wl_count_kernel(const uint32_t* __restrict__ ev_off,
                                        const uint32_t* __restrict__ s_off,
-                                       const uint32_t* __restrict__ s_idx, uint32_t lb, uint32_t np,
+                                       const uint2* __restrict__ seg, uint32_t lb, uint32_t np,
                                        const uint32_t* __restrict__ val_sorted,
                                        const unsigned long long* __restrict__ S,
                                        const WlHead* __restrict__ head,
                                        uint32_t* __restrict__ ci, uint32_t* __restrict__ cf,
                                        uint32_t* __restrict__ cp) {
-  const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t pos = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
   if (pos > np) return;
   if (pos == np) {  // the exclusive scans run over np + 1 entries
-    ci[np] = cf[np] = cp[np] = 0;
+    if (lane == 0) ci[np] = cf[np] = cp[np] = 0;
     return;
   }
   const uint32_t i = val_sorted[pos];
   uint32_t a, b, c;
-  wl_leaf_items(lb + i, pt_off, ev_off, s_off, s_idx, S[i], head->max_ev, head->budget, nullptr,
-                nullptr, 0, a, b, c);
-  ci[pos] = a;
-  cf[pos] = b;
-  cp[pos] = c;
+  wl_leaf_items(lb + i, ev_off, s_off, seg, S[i], head->max_ev, head->budget, nullptr, nullptr, 0,
+                a, b, c);
+  if (lane == 0) {
+    ci[pos] = a;
+    cf[pos] = b;
+    cp[pos] = c;
+  }
 }
 
 // group k = sorted positions [grp_pos[k], grp_pos[k+1]); header ranges
@@ -215,10 +241,10 @@ static __global__ void wl_bounds_kernel(const uint32_t* __restrict__ key_sorted,
   }
 }
 
-static __global__ void wl_fill_kernel(const uint32_t* __restrict__ pt_off,
-                                      const uint32_t* __restrict__ ev_off,
+// one warp per position
+static __global__ void wl_fill_kernel(const uint32_t* __restrict__ ev_off,
                                       const uint32_t* __restrict__ s_off,
-                                      const uint32_t* __restrict__ s_idx, uint32_t lb, uint32_t np,
+                                      const uint2* __restrict__ seg, uint32_t lb, uint32_t np,
                                       const uint32_t* __restrict__ val_sorted,
                                       const unsigned long long* __restrict__ S,
                                       const WlHead* __restrict__ head,
@@ -226,12 +252,12 @@ static __global__ void wl_fill_kernel(const uint32_t* __restrict__ pt_off,
                                       const uint32_t* __restrict__ fo,
                                       const uint32_t* __restrict__ po, P2PItem* __restrict__ items,
                                       P2PFinal* __restrict__ fins) {
-  const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t pos = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (pos >= np) return;
   const uint32_t i = val_sorted[pos];
   uint32_t a, b, c;
-  wl_leaf_items(lb + i, pt_off, ev_off, s_off, s_idx, S[i], head->max_ev, head->budget,
-                items + io[pos], fins + fo[pos], po[pos], a, b, c);
+  wl_leaf_items(lb + i, ev_off, s_off, seg, S[i], head->max_ev, head->budget, items + io[pos],
+                fins + fo[pos], po[pos], a, b, c);
 }
 
 }  // namespace fmmcu

@@ -183,3 +183,26 @@ def test_connectivity_paths_agree(ctx, env, monkeypatch):
         for lvl in range(L):
             for g, w in ((got[4][lvl], want[4][lvl]), (got[5][lvl], want[5][lvl])):
                 assert np.array_equal(g[0], w[0]) and np.array_equal(g[1], w[1]), (name, lvl)
+
+
+@pytest.mark.parametrize("force_e", [None, "4", "5"])
+def test_device_work_list_equals_host_work_list(ctx, force_e, monkeypatch):
+    """The pipeline's P2P work list is built on the device from the finest
+    CSR (p2p_worklist.cuh); FMMCU_HOST_WL=1 selects the host builder
+    (build_worklist) over a downloaded CSR.  Same items in the same order, so
+    the potentials are bitwise equal and the pair counts identical -- also
+    where heavy leaves are split into strong-list chunks (few levels,
+    clustered) and with the evals-per-lane choice forced either way."""
+    if force_e:
+        monkeypatch.setenv("FMMCU_P2P_E", force_e)
+    cases = list(_cases())[:5] + [
+        ("heavy_gauss_L3", F.make_distribution("gauss8", 40_000, 31), None, 3, 0.5),
+        ("heavy_uniform_L2", F.make_distribution("uniform", 12_000, 32), None, 2, 0.5)]
+    for name, s, e, L, theta in cases:
+        e = _evals(s, e)
+        dev, sd = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=L, theta=theta, p=17)
+        monkeypatch.setenv("FMMCU_HOST_WL", "1")
+        host, sh = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=L, theta=theta, p=17)
+        monkeypatch.delenv("FMMCU_HOST_WL")
+        assert np.array_equal(dev.view(np.uint64), host.view(np.uint64)), name
+        assert sd["p2p_pairs"] == sh["p2p_pairs"], name

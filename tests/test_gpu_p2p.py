@@ -347,3 +347,36 @@ def test_invalid_jobs_fail_loudly(ctx):
         _run(ctx, *bad)
     with pytest.raises(N.FmmcuError):
         ctx.finish()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_device_work_list_equals_host_work_list(ctx, pinned, monkeypatch):
+    """fmmcu_p2p_launch builds its work list on the device (p2p_worklist.cuh)
+    from the uploaded CSR, grouped by upload chunk; FMMCU_HOST_WL=1 selects
+    the host builder.  Same items in the same order: bitwise equal potentials
+    and equal pair counts for whole jobs, leaf shards (halo-only uploads) and
+    split heavy leaves, with pageable and page-locked inputs."""
+    cases = [_tree_case(0, 1_500_000, 8, 41)[1], _tree_case(2, 300_000, 8, 3)[1],
+             _tree_case(3, 80_000, 6, 42, self_eval=False, n_eval=50_000)[1]]
+    for args in cases:
+        args = list(args)
+        nl = len(args[0]) - 1
+        reg = []
+        if pinned:
+            args[5] = np.ascontiguousarray(args[5]).copy()
+            args[6] = np.ascontiguousarray(args[6]).copy()
+            reg = [args[5], args[6]]
+            for a in reg:
+                ctx.host_register(a)
+        try:
+            for lb, le in ((0, nl), (nl // 5, nl // 2)):
+                dev, pd, _ = _run(ctx, *args, leaf_begin=lb, leaf_end=le)
+                monkeypatch.setenv("FMMCU_HOST_WL", "1")
+                host, ph, _ = _run(ctx, *args, leaf_begin=lb, leaf_end=le)
+                monkeypatch.delenv("FMMCU_HOST_WL")
+                e0, e1 = int(args[1][lb]), int(args[1][le])
+                assert pd == ph
+                assert bitwise(dev[e0:e1], host[e0:e1])
+        finally:
+            for a in reg:
+                ctx.host_unregister(a)
