@@ -43,6 +43,20 @@ class CudaBackend final : public NearFieldBackend {
                   const std::vector<std::uint32_t>& weak_off,
                   const std::vector<std::uint32_t>& weak_idx, std::vector<cplx>& out);
   std::uint64_t m2l_finish(double* seconds = nullptr);
+  // The same on flat arrays in the context's page-locked buffers
+  // (fmmcu_m2l_host_buffers): the caller flattens straight into them, the
+  // launch DMAs them in place and the sums land in `out` ([n_targets][p+1]).
+  struct M2LBuffers {
+    cplx* centers = nullptr;  // [n_boxes]
+    cplx* coeffs = nullptr;   // [n_boxes][p+1]
+    cplx* out = nullptr;      // [n_targets][p+1]
+    std::uint32_t* target_box = nullptr;
+    std::uint32_t* weak_off = nullptr;
+    std::uint32_t* weak_idx = nullptr;
+  };
+  M2LBuffers m2l_buffers(std::uint32_t n_boxes, int p, std::uint32_t n_targets, std::uint64_t nnz);
+  void m2l_launch(int p, Kernel kernel, std::uint32_t n_boxes, std::uint32_t n_targets,
+                  const M2LBuffers& b);
 
   // The whole FmmEngine::evaluate on the first device (fmmcu_fmm_evaluate):
   // potentials in the original eval order, counters, device phase times.

@@ -148,8 +148,21 @@ int fmmcu_set_stream(fmmcu_ctx *ctx, void *stream);
 int fmmcu_synchronize(fmmcu_ctx *ctx);
 
 /* ---- M2L on the device --------------------------------------------------- */
+/* Asynchronous.  Inputs in page-locked memory (fmmcu_m2l_host_buffers,
+ * fmmcu_host_register) are DMA'd in place, and a page-locked job->out
+ * receives the sums straight from the device; other memory is staged. */
 int fmmcu_m2l_launch(fmmcu_ctx *ctx, const fmmcu_m2l_job *job);
 int fmmcu_m2l_finish(fmmcu_ctx *ctx, uint64_t *m2l_ops, double *seconds);
+/* Page-locked host arrays sized for one M2L job, owned by the context and
+ * valid until the next call or fmmcu_destroy (grown, never shrunk).  A caller
+ * that flattens its expansions and interaction lists straight into them (the
+ * hybrid engine path) saves the staging copies of fmmcu_m2l_launch. */
+typedef struct {
+  double *centers, *coeffs, *out;
+  uint32_t *target_box, *weak_off, *weak_idx;
+} fmmcu_m2l_buffers;
+int fmmcu_m2l_host_buffers(fmmcu_ctx *ctx, uint32_t n_boxes, int p, uint32_t n_targets,
+                           uint64_t nnz, fmmcu_m2l_buffers *bufs);
 
 /* ---- the whole FMM evaluation on one device ------------------------------
  * FmmEngine::evaluate (reference engine.cpp:208-347) with every phase on the

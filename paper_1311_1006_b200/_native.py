@@ -118,6 +118,13 @@ class P2PJob(C.Structure):
     ]
 
 
+class M2LBuffers(C.Structure):
+    """Mirror of ``fmmcu_m2l_buffers`` (include/fmm_cuda.h)."""
+    _fields_ = [("centers", C.POINTER(C.c_double)), ("coeffs", C.POINTER(C.c_double)),
+                ("out", C.POINTER(C.c_double)), ("target_box", C.POINTER(C.c_uint32)),
+                ("weak_off", C.POINTER(C.c_uint32)), ("weak_idx", C.POINTER(C.c_uint32))]
+
+
 class M2LJob(C.Structure):
     """Mirror of ``fmmcu_m2l_job`` (include/fmm_cuda.h)."""
 
@@ -144,7 +151,7 @@ CUDA_SYMBOLS = [
     "fmmcu_fmm_evaluate", "fmmcu_fmm_launch", "fmmcu_fmm_finish", "fmmcu_fmm_tree_level", "fmmcu_fmm_tree_perm", "fmmcu_fmm_tree_lists",
     "fmmcu_hypot_batch", "fmmcu_p2p_kernel_info",
     "fmmcu_p2p_out_ipc_handle", "fmmcu_p2p_bind_peer_out", "fmmcu_nccl_unique_id",
-    "fmmcu_nccl_init", "fmmcu_nccl_gather_out",
+    "fmmcu_nccl_init", "fmmcu_nccl_gather_out", "fmmcu_m2l_host_buffers",
 ]
 IPC_HANDLE_BYTES = 64
 NCCL_ID_BYTES = 128
@@ -188,6 +195,8 @@ def cuda_lib():
         lib.fmmcu_synchronize.argtypes = [vp]
         lib.fmmcu_m2l_launch.argtypes = [vp, C.POINTER(M2LJob)]
         lib.fmmcu_m2l_finish.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        lib.fmmcu_m2l_host_buffers.argtypes = [vp, C.c_uint32, C.c_int, C.c_uint32, C.c_uint64,
+                                               C.POINTER(M2LBuffers)]
         lib.fmmcu_kernel_launches.argtypes = [vp]
         lib.fmmcu_kernel_launches.restype = C.c_uint64
         lib.fmmcu_fp64_peak.argtypes = [vp, C.POINTER(C.c_double)]
@@ -477,6 +486,44 @@ class CudaContext:
         ops = C.c_uint64()
         secs = C.c_double()
         self._check(self.lib.fmmcu_m2l_finish(self.h, C.byref(ops), C.byref(secs)))
+        return out, int(ops.value), float(secs.value)
+
+    def m2l_pinned(self, p, kernel, centers, coeffs, target_box, weak_off, weak_idx):
+        """m2l() through the context's page-locked buffers
+        (fmmcu_m2l_host_buffers): inputs copied into them, DMA'd in place,
+        sums D2H'd straight into the pinned out."""
+        centers = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64).reshape(-1)
+        nb, nt = centers.size // 2, len(target_box)
+        nnz = int(np.asarray(weak_off)[nt]) if nt else 0
+        b = M2LBuffers()
+        self._check(self.lib.fmmcu_m2l_host_buffers(self.h, nb, p, nt, nnz, C.byref(b)))
+        view = lambda ptr, n: np.ctypeslib.as_array(ptr, shape=(n,))  # noqa: E731
+        view(b.centers, 2 * nb)[:] = centers
+        view(b.coeffs, coeffs.size)[:] = coeffs
+        if nt:
+            view(b.target_box, nt)[:] = target_box
+            view(b.weak_off, nt + 1)[:] = weak_off
+        if nnz:
+            view(b.weak_idx, nnz)[:] = weak_idx
+        j = M2LJob()
+        j.p = p
+        j.kernel = kernel
+        j.n_boxes = nb
+        vp = lambda ptr: C.cast(ptr, C.c_void_p)  # noqa: E731
+        j.centers = vp(b.centers)
+        j.coeffs = vp(b.coeffs)
+        j.n_targets = nt
+        j.target_box = vp(b.target_box) if nt else None
+        j.weak_off = vp(b.weak_off)
+        j.weak_idx = vp(b.weak_idx) if nnz else None
+        j.out = vp(b.out) if nt else None
+        self._check(self.lib.fmmcu_m2l_launch(self.h, C.byref(j)))
+        ops = C.c_uint64()
+        secs = C.c_double()
+        self._check(self.lib.fmmcu_m2l_finish(self.h, C.byref(ops), C.byref(secs)))
+        out = view(b.out, nt * (p + 1) * 2).reshape(nt, p + 1, 2).copy() if nt else \
+            np.zeros((0, p + 1, 2))
         return out, int(ops.value), float(secs.value)
 
 

@@ -202,8 +202,9 @@ void launch_sym_v(const P2PArgs& a, const P2PSymArgs& sa, uint32_t n_items, cuda
   kfn<<<grid, W * 32, smem, s>>>(a, sa);
 }
 
-// mutual-kernel shapes (FMMCU_SYM_VARIANT, harmonic / no smoother, E = 5):
-//   0 = 4w c128 u1 m3   1 = 4w c256 u1 m3   2 = 2w c128 u1 m6   3 = 4w c128 u2 m3
+// mutual-kernel shapes (FMMCU_SYM_VARIANT, harmonic / no smoother):
+//   E = 5: 0 = 4w c128 u1 m3   1 = 4w c256 u1 m3   2 = 2w c128 u1 m6   3 = 4w c128 u2 m3
+// (r2, 10M / L10: 0 and 2 4.27 ms; a 4-CTA cap at 128 registers 4.60 ms; E = 4 5.89 ms)
 int sym_variant() {
   static int v = [] {
     const char* e = std::getenv("FMMCU_SYM_VARIANT");
@@ -935,16 +936,38 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->mode = j->mode;
   c->delta = j->delta;
   Trace tr(c);
-  // leaf-aligned upload chunks of ~1M sources
-  constexpr uint32_t kChunkSrc = 1u << 20;
-  const int K = int(std::min<uint32_t>(fmmcu_ctx::kMaxChunks,
-                                       std::max<uint32_t>(1u, (ns + kChunkSrc - 1) / kChunkSrc)));
+  // Leaf-aligned upload chunks of ~kChunkSrc sources.  Group k's kernels
+  // start when chunk k lands, so the step ends one group's compute after the
+  // last chunk: with a tail (FMMCU_TAIL=n) the last n chunks halve in
+  // size, 1/2, 1/4, ... of kChunkSrc, to shorten that final group.
+  static const uint32_t kChunkSrc =
+      std::getenv("FMMCU_CHUNK") ? uint32_t(std::atol(std::getenv("FMMCU_CHUNK"))) : (1u << 20);
+  static const int kTail = std::getenv("FMMCU_TAIL") ? std::atoi(std::getenv("FMMCU_TAIL")) : 0;
+  std::vector<uint64_t> cut_src{0};
+  {
+    uint64_t rest = ns;
+    const uint64_t cs = std::max<uint32_t>(kChunkSrc, 1u << 14);
+    // full chunks while more than the tail (cs * (1 - 2^-kTail)) plus one chunk remain
+    const uint64_t tail_total = kTail > 0 ? cs - (cs >> kTail) : 0;
+    while (rest > cs + tail_total && cut_src.size() < size_t(fmmcu_ctx::kMaxChunks - kTail)) {
+      cut_src.push_back(cut_src.back() + cs);
+      rest -= cs;
+    }
+    // the remainder: halving pieces, the last two equal
+    for (int t = 0; t < kTail && rest > (cs >> (kTail + 1)); ++t) {
+      const uint64_t piece = rest / 2;
+      cut_src.push_back(cut_src.back() + (rest - piece));
+      rest = piece;
+    }
+    if (rest > 0 || cut_src.size() == 1) cut_src.push_back(ns);
+    cut_src.back() = ns;
+  }
+  const int K = int(cut_src.size()) - 1;
   c->chunk_leaf.assign(K + 1, nl);
   c->chunk_leaf[0] = 0;
   for (int k = 1; k < K; ++k) {
-    const uint64_t target = uint64_t(ns) * uint64_t(k) / uint64_t(K);
-    const uint32_t t = uint32_t(std::lower_bound(j->pt_off, j->pt_off + nl + 1, uint32_t(target)) -
-                                j->pt_off);
+    const uint32_t t = uint32_t(std::lower_bound(j->pt_off, j->pt_off + nl + 1,
+                                                 uint32_t(cut_src[k])) - j->pt_off);
     c->chunk_leaf[k] = std::max(c->chunk_leaf[k - 1], std::min(t, nl));
   }
   c->group_k = K;
@@ -1535,7 +1558,8 @@ void fmmcu_destroy(fmmcu_ctx* c) {
                       &c->d_wl_S, &c->d_wl_work, &c->d_wl_cnt, &c->d_wl_off})
       b->release();
     for (HostBuf* b : {&c->h_src, &c->h_evy, &c->h_eself, &c->h_out, &c->h_hits, &c->h_csr,
-                       &c->mh_out, &c->mh_flag, &c->h_wl_head})
+                       &c->mh_out, &c->mh_flag, &c->h_wl_head, &c->mb_centers, &c->mb_coeffs,
+                       &c->mb_out, &c->mb_tbox, &c->mb_woff, &c->mb_widx})
       b->release();
     for (cudaEvent_t ev : {c->ev_start, c->ev_end, c->ev_m2l0, c->ev_m2l1})
       if (ev) cudaEventDestroy(ev);
@@ -1835,11 +1859,14 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
   const int P1 = j->p + 1;
   const uint32_t nb = j->n_boxes, nt = j->n_targets;
   const uint32_t nnz = nt ? j->weak_off[nt] : 0;
-  for (uint32_t t = 0; t < nt; ++t)
-    if (j->target_box[t] >= nb || j->weak_off[t] > j->weak_off[t + 1])
-      return set_err(c, FMMCU_EINVAL, "bad m2l target list");
-  for (uint32_t q = 0; q < nnz; ++q)
-    if (j->weak_idx[q] >= nb) return set_err(c, FMMCU_EINVAL, "bad m2l weak index");
+  bool ok_t = true, ok_w = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok_t)
+  for (int64_t t = 0; t < int64_t(nt); ++t)
+    ok_t = ok_t && j->target_box[t] < nb && j->weak_off[t] <= j->weak_off[t + 1];
+  if (!ok_t) return set_err(c, FMMCU_EINVAL, "bad m2l target list");
+#pragma omp parallel for schedule(static) reduction(&& : ok_w)
+  for (int64_t q = 0; q < int64_t(nnz); ++q) ok_w = ok_w && j->weak_idx[q] < nb;
+  if (!ok_w) return set_err(c, FMMCU_EINVAL, "bad m2l weak index");
   CU_TRY(c, c->m_centers.ensure(size_t(nb) * 16));
   CU_TRY(c, c->m_coeffs.ensure(size_t(nb) * P1 * 16));
   CU_TRY(c, c->m_tbox.ensure(size_t(nt) * 4));
@@ -1847,8 +1874,9 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
   CU_TRY(c, c->m_widx.ensure(size_t(nnz) * 4));
   CU_TRY(c, c->m_out.ensure(size_t(nt) * P1 * 16));
   CU_TRY(c, c->m_flag.ensure(8));
-  CU_TRY(c, c->mh_out.ensure(size_t(nt) * P1 * 16));
   CU_TRY(c, c->mh_flag.ensure(8));
+  c->m2l_direct_out = nt && host_locked(j->out, size_t(nt) * P1 * 16);
+  if (!c->m2l_direct_out) CU_TRY(c, c->mh_out.ensure(size_t(nt) * P1 * 16));
   cudaStream_t s = c->m2l_stream;
   CU_TRY(c, cudaEventRecord(c->ev_m2l0, s));
   CU_TRY(c, cudaMemcpyAsync(c->m_centers.p, j->centers, size_t(nb) * 16, cudaMemcpyHostToDevice, s));
@@ -1872,7 +1900,8 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
     a.out = c->m_out.as<double2>();
     a.singular = c->m_flag.as<int>();
     if (int rc = m2l_run(c, a, nnz, s)) return rc;
-    CU_TRY(c, cudaMemcpyAsync(c->mh_out.p, c->m_out.p, size_t(nt) * P1 * 16, cudaMemcpyDeviceToHost, s));
+    CU_TRY(c, cudaMemcpyAsync(c->m2l_direct_out ? static_cast<void*>(j->out) : c->mh_out.p,
+                              c->m_out.p, size_t(nt) * P1 * 16, cudaMemcpyDeviceToHost, s));
   }
   CU_TRY(c, cudaMemcpyAsync(c->mh_flag.p, c->m_flag.p, 4, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaEventRecord(c->ev_m2l1, s));
@@ -1880,6 +1909,28 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
   c->m2l_ops = nnz;
   c->m2l_prep = std::chrono::duration<double>(Clock::now() - t0).count();
   c->m2l_inflight = true;
+  return FMMCU_OK;
+}
+
+int fmmcu_m2l_host_buffers(fmmcu_ctx* c, uint32_t n_boxes, int p, uint32_t n_targets,
+                           uint64_t nnz, fmmcu_m2l_buffers* b) {
+  if (!c || !b) return FMMCU_EINVAL;
+  if (p < 1 || p > kM2LMaxP) return set_err(c, FMMCU_EINVAL, "m2l order out of range");
+  if (c->m2l_inflight) return set_err(c, FMMCU_ESTATE, "m2l buffers while a launch is in flight");
+  CU_TRY(c, cudaSetDevice(c->device));
+  const size_t P1 = size_t(p) + 1;
+  CU_TRY(c, c->mb_centers.ensure(size_t(n_boxes) * 16));
+  CU_TRY(c, c->mb_coeffs.ensure(size_t(n_boxes) * P1 * 16));
+  CU_TRY(c, c->mb_out.ensure(size_t(n_targets) * P1 * 16));
+  CU_TRY(c, c->mb_tbox.ensure(size_t(n_targets) * 4));
+  CU_TRY(c, c->mb_woff.ensure((size_t(n_targets) + 1) * 4));
+  CU_TRY(c, c->mb_widx.ensure(size_t(nnz) * 4));
+  b->centers = c->mb_centers.as<double>();
+  b->coeffs = c->mb_coeffs.as<double>();
+  b->out = c->mb_out.as<double>();
+  b->target_box = c->mb_tbox.as<uint32_t>();
+  b->weak_off = c->mb_woff.as<uint32_t>();
+  b->weak_idx = c->mb_widx.as<uint32_t>();
   return FMMCU_OK;
 }
 
@@ -1893,8 +1944,8 @@ int fmmcu_m2l_finish(fmmcu_ctx* c, uint64_t* ops, double* seconds) {
   float ms = 0.f;
   CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_m2l0, c->ev_m2l1));
   const int P1 = c->m2l_job.p + 1;
-  if (c->m2l_job.n_targets)
-    std::memcpy(c->m2l_job.out, c->mh_out.p, size_t(c->m2l_job.n_targets) * P1 * 16);
+  if (c->m2l_job.n_targets && !c->m2l_direct_out)
+    par_memcpy(c->m2l_job.out, c->mh_out.p, size_t(c->m2l_job.n_targets) * P1 * 16);
   if (ops) *ops = c->m2l_ops;
   if (seconds) *seconds = c->m2l_prep + 1e-3 * double(ms);
   if (*c->mh_flag.as<int>())

@@ -232,6 +232,8 @@ struct fmmcu_ctx {
   DevBuf m_centers, m_coeffs, m_tbox, m_woff, m_widx, m_table, m_out, m_flag;
   DevBuf m_items, m_iscan, m_nitems, m_partial, m_cubtmp;  // m2l_run work items
   HostBuf mh_out, mh_flag;
+  HostBuf mb_centers, mb_coeffs, mb_out, mb_tbox, mb_woff, mb_widx;  // fmmcu_m2l_host_buffers
+  bool m2l_direct_out = false;  // the launched job's out is page-locked: D2H in place
   int table_p = -1, table_kernel = -1;
   bool m2l_inflight = false;
   fmmcu_m2l_job m2l_job{};

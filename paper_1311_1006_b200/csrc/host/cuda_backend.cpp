@@ -307,6 +307,38 @@ void CudaBackend::m2l_launch(int p, Kernel kernel, const std::vector<cplx>& cent
   if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l launch");
 }
 
+CudaBackend::M2LBuffers CudaBackend::m2l_buffers(std::uint32_t n_boxes, int p,
+                                                 std::uint32_t n_targets, std::uint64_t nnz) {
+  fmmcu_m2l_buffers hb{};
+  const int rc = fmmcu_m2l_host_buffers(ctx_[0], n_boxes, p, n_targets, nnz, &hb);
+  if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l buffers");
+  M2LBuffers b;
+  b.centers = reinterpret_cast<cplx*>(hb.centers);
+  b.coeffs = reinterpret_cast<cplx*>(hb.coeffs);
+  b.out = reinterpret_cast<cplx*>(hb.out);
+  b.target_box = hb.target_box;
+  b.weak_off = hb.weak_off;
+  b.weak_idx = hb.weak_idx;
+  return b;
+}
+
+void CudaBackend::m2l_launch(int p, Kernel kernel, std::uint32_t n_boxes, std::uint32_t n_targets,
+                             const M2LBuffers& b) {
+  fmmcu_m2l_job j{};
+  j.p = p;
+  j.kernel = kernel == Kernel::harmonic ? FMMCU_KERNEL_HARMONIC : FMMCU_KERNEL_LOG;
+  j.n_boxes = n_boxes;
+  j.centers = reinterpret_cast<const double*>(b.centers);
+  j.coeffs = reinterpret_cast<const double*>(b.coeffs);
+  j.n_targets = n_targets;
+  j.target_box = b.target_box;
+  j.weak_off = b.weak_off;
+  j.weak_idx = b.weak_idx;
+  j.out = reinterpret_cast<double*>(b.out);
+  const int rc = fmmcu_m2l_launch(ctx_[0], &j);
+  if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l launch");
+}
+
 std::uint64_t CudaBackend::m2l_finish(double* seconds) {
   std::uint64_t ops = 0;
   double s = 0;

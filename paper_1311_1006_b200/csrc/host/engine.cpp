@@ -14,6 +14,8 @@
 //    L2L chain and adds the device M2L sums per box (local = L2L(parent) +
 //    sum_w M2L(w)).  m2l_ops is identical to the CPU path.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 
@@ -114,48 +116,73 @@ ExpansionPyramid empty_like(const Pyramid& pyr) {
   return e;
 }
 
-// Device M2L: flatten all levels, launch on the cuda backend.
+// Device M2L (hybrid path): every level's expansions and weak lists are
+// flattened in parallel straight into the backend's page-locked buffers
+// (DMA'd in place), the batched M2L runs on the device (m2l_reg_kernel) while
+// the CPU waits on nothing else, and the host L2L chain adds the sums.
 struct DeviceM2L {
-  std::vector<cplx> centers, coeffs, sums;
-  std::vector<std::uint32_t> tbox, woff, widx;
+  CudaBackend::M2LBuffers b;
+  std::uint32_t n_boxes = 0, n_targets = 0;
   std::vector<std::uint32_t> level_base;  // global id of box 0 of level l
   std::vector<std::int64_t> slot;         // global box id -> target row (-1 if none)
 };
 
 void device_m2l_launch(CudaBackend& be, const Pyramid& pyr, const Connectivity& conn,
-                       const ExpansionPyramid& out, Kernel kernel, int p, DeviceM2L& dm) {
+                       const ExpansionPyramid& out, Kernel kernel, int p, int threads,
+                       DeviceM2L& dm) {
   const int L = pyr.n_levels;
   dm.level_base.assign(L + 1, 0);
   for (int l = 0; l < L; ++l)
     dm.level_base[l + 1] = dm.level_base[l] + std::uint32_t(pyr.levels[l].size());
   const std::uint32_t nb = dm.level_base[L];
   const std::size_t P1 = std::size_t(p) + 1;
-  dm.centers.resize(nb);
-  dm.coeffs.assign(std::size_t(nb) * P1, cplx(0, 0));
-  dm.slot.assign(nb, -1);
-  dm.tbox.clear();
-  dm.woff.assign(1, 0);
-  dm.widx.clear();
-  for (int l = 0; l < L; ++l) {
-    for (std::size_t i = 0; i < pyr.levels[l].size(); ++i) {
-      const std::uint32_t g = dm.level_base[l] + std::uint32_t(i);
-      dm.centers[g] = pyr.levels[l][i].center;
-      const Expansion& e = out.levels[l][i];
-      if (!e.coeffs.empty()) std::copy(e.coeffs.begin(), e.coeffs.end(), dm.coeffs.begin() + g * P1);
-    }
-  }
+  // per box: target flag and its nonempty weak partners (pass 1), prefix
+  // sums (serial over boxes, cheap), then the parallel fill (pass 2)
+  std::vector<std::uint32_t> tcnt(std::size_t(nb) + 1, 0), wcnt(std::size_t(nb) + 1, 0);
   for (int l = 1; l < L; ++l) {
-    for (std::size_t i = 0; i < pyr.levels[l].size(); ++i) {
+    const std::int64_t n = std::int64_t(pyr.levels[l].size());
+    const std::uint32_t base = dm.level_base[l];
+#pragma omp parallel for schedule(static) num_threads(threads)
+    for (std::int64_t i = 0; i < n; ++i) {
       if (pyr.levels[l][i].n_evals() == 0) continue;
-      const std::uint32_t g = dm.level_base[l] + std::uint32_t(i);
-      dm.slot[g] = std::int64_t(dm.tbox.size());
-      dm.tbox.push_back(g);
-      for (std::uint32_t w : conn.levels[l].weak[i])
-        if (!out.levels[l][w].coeffs.empty()) dm.widx.push_back(dm.level_base[l] + w);
-      dm.woff.push_back(std::uint32_t(dm.widx.size()));
+      std::uint32_t k = 0;
+      for (std::uint32_t w : conn.levels[l].weak[i]) k += out.levels[l][w].coeffs.empty() ? 0u : 1u;
+      tcnt[base + i + 1] = 1;
+      wcnt[base + i + 1] = k;
     }
   }
-  be.m2l_launch(p, kernel, dm.centers, dm.coeffs, dm.tbox, dm.woff, dm.widx, dm.sums);
+  for (std::uint32_t g = 0; g < nb; ++g) {
+    tcnt[g + 1] += tcnt[g];
+    wcnt[g + 1] += wcnt[g];
+  }
+  dm.n_boxes = nb;
+  dm.n_targets = tcnt[nb];
+  dm.b = be.m2l_buffers(nb, p, dm.n_targets, wcnt[nb]);
+  dm.slot.assign(nb, -1);
+  const CudaBackend::M2LBuffers& b = dm.b;
+  b.weak_off[0] = 0;
+  for (int l = 0; l < L; ++l) {
+    const std::int64_t n = std::int64_t(pyr.levels[l].size());
+    const std::uint32_t base = dm.level_base[l];
+#pragma omp parallel for schedule(static) num_threads(threads)
+    for (std::int64_t i = 0; i < n; ++i) {
+      const std::uint32_t g = base + std::uint32_t(i);
+      b.centers[g] = pyr.levels[l][i].center;
+      const Expansion& e = out.levels[l][i];
+      cplx* dst = b.coeffs + std::size_t(g) * P1;
+      if (!e.coeffs.empty()) std::copy(e.coeffs.begin(), e.coeffs.end(), dst);
+      else std::fill(dst, dst + P1, cplx(0, 0));
+      if (tcnt[g + 1] == tcnt[g]) continue;  // not a target
+      const std::uint32_t t = tcnt[g];
+      dm.slot[g] = std::int64_t(t);
+      b.target_box[t] = g;
+      std::uint32_t o = wcnt[g];
+      for (std::uint32_t w : conn.levels[l].weak[i])
+        if (!out.levels[l][w].coeffs.empty()) b.weak_idx[o++] = base + w;
+      b.weak_off[t + 1] = o;
+    }
+  }
+  be.m2l_launch(p, kernel, nb, dm.n_targets, b);
 }
 
 // Host half of the device downward pass: L2L chain + device M2L sums.
@@ -176,7 +203,7 @@ ExpansionPyramid device_m2l_assemble(const Pyramid& pyr, const DeviceM2L& dm, Ke
         if (!up.coeffs.empty()) l2l_add(up, me);
       }
       const std::int64_t row = dm.slot[dm.level_base[l] + std::uint32_t(i)];
-      const cplx* s = dm.sums.data() + std::size_t(row) * P1;
+      const cplx* s = dm.b.out + std::size_t(row) * P1;
       for (std::size_t k = 0; k < P1; ++k) me.coeffs[k] += s[k];
     }
   }
@@ -397,9 +424,15 @@ void FmmEngine::evaluate_into(const SourceSet& sources, const EvalSet& evals, Ev
   if (cfg_.m2l_on_device) {
     auto* cb = dynamic_cast<CudaBackend*>(backend_.get());
     DeviceM2L dm;
+    static const bool trace = std::getenv("FMM_TRACE") != nullptr;
     try {
-      device_m2l_launch(*cb, pyr, conn, outgoing, cfg_.kernel, p, dm);
-      res.counters.m2l_ops += cb->m2l_finish();
+      device_m2l_launch(*cb, pyr, conn, outgoing, cfg_.kernel, p, threads, dm);
+      const double t_fl = since(t_m2l);
+      double dev_s = 0.0;
+      res.counters.m2l_ops += cb->m2l_finish(&dev_s);
+      if (trace)
+        std::fprintf(stderr, "[fmm] hybrid m2l: flatten+launch %.2f ms, finish at %.2f ms "
+                     "(device span %.2f ms)\n", 1e3 * t_fl, 1e3 * since(t_m2l), 1e3 * dev_s);
     } catch (const SingularConfiguration&) {
       try {
         backend_->finish();
@@ -414,6 +447,7 @@ void FmmEngine::evaluate_into(const SourceSet& sources, const EvalSet& evals, Ev
       throw BackendError("m2l", e.what());
     }
     locals = device_m2l_assemble(pyr, dm, cfg_.kernel, p, threads);
+    if (trace) std::fprintf(stderr, "[fmm] hybrid m2l: assembled at %.2f ms\n", 1e3 * since(t_m2l));
   } else {
     locals = downward_pass(pyr, conn, outgoing, p, cfg_.task_split_level, threads, &res.counters);
   }

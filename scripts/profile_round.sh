@@ -12,7 +12,7 @@ ncu --set full --clock-control none --import-source on -k regex:${P2P_KPAT:-p2p_
   -o gpurun_out/${TAG}_p2p python bench.py --no-e2e --no-fmm --no-cpu --steps 1 --warmup 3 \
   > gpurun_out/${TAG}_p2p.log 2>&1
 echo "p2p full $?"
-ncu --set full --clock-control none --import-source on -k regex:m2l_thread_kernel -s 1 -c 1 -f \
+ncu --set full --clock-control none --import-source on -k regex:${M2L_KPAT:-m2l_reg_kernel} -s 1 -c 1 -f \
   -o gpurun_out/${TAG}_m2l python scripts/fmm_pipeline_probe.py --reps 2 > gpurun_out/${TAG}_m2l.log 2>&1
 echo "m2l full $?"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_pipe_launches.csv \

@@ -84,6 +84,28 @@ def test_device_m2l_matches_reference_operator():
     ctx.close()
 
 
+def test_device_m2l_pinned_buffers_equal_pageable():
+    """fmmcu_m2l_host_buffers: the same job flattened into the context's
+    page-locked buffers (DMA'd in place, sums D2H'd into the pinned out) gives
+    bitwise the pageable-input result; the buffers are reused across sizes."""
+    rng = np.random.default_rng(5)
+    ctx = N.CudaContext(0)
+    for nb, nt, p in ((3000, 2000, 17), (500, 400, 9), (5000, 4500, 17)):
+        centers = rng.random((nb, 2))
+        coeffs = rng.standard_normal((nb, p + 1, 2)) * 1e-3
+        target_box = rng.choice(nb, nt, replace=False).astype(np.uint32)
+        deg = rng.integers(0, 30, nt)
+        weak_off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint32)
+        weak_idx = rng.integers(0, nb, int(weak_off[-1])).astype(np.uint32)
+        # no coincident centres: partners distinct from their target
+        weak_idx = np.where(weak_idx == np.repeat(target_box, deg), (weak_idx + 1) % nb, weak_idx)
+        a, oa, _ = ctx.m2l(p, 0, centers, coeffs, target_box, weak_off, weak_idx)
+        b, ob, _ = ctx.m2l_pinned(p, 0, centers, coeffs, target_box, weak_off, weak_idx)
+        assert oa == ob == int(weak_off[-1])
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    ctx.close()
+
+
 def test_device_m2l_singular_raises():
     ctx = N.CudaContext(0)
     centers = np.array([[0.5, 0.5], [0.5, 0.5]])
