@@ -1159,6 +1159,8 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   std::vector<char> chunk_self(K, 0);
   int launched = 0;
   int nk = 0;
+  static const bool two_streams = !(std::getenv("FMMCU_GRP_STREAMS") &&
+                                    std::atoi(std::getenv("FMMCU_GRP_STREAMS")) == 1);
   auto run_group = [&](int k) -> int {
     CU_TRY(c, cudaStreamWaitEvent(s, c->ev_chunk[k], 0));
     if (evals_event) CU_TRY(c, cudaStreamWaitEvent(s, c->ev_evals, 0));
@@ -1203,20 +1205,34 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       f0 = c->fin_first[p0];
       f1 = c->fin_first[p1];
     }
+    // The group's P2P kernels alternate between two streams behind the chunk
+    // preparation on s, so group k+1 fills the SMs while group k's last items
+    // drain; each stream has its own scheduler counter.  Group k reads only
+    // sources and eval records of chunks <= k, all prepared on s before
+    // ev_prep[k]; partial slots are per item.  FMMCU_GRP_STREAMS=1: one stream.
+    cudaStream_t gs = s;
+    unsigned int* counter = c->d_counter.as<unsigned int>();
+    if (two_streams) {
+      CU_TRY(c, cudaEventRecord(c->ev_prep[k], s));
+      gs = c->grp_stream[k & 1];
+      CU_TRY(c, cudaStreamWaitEvent(gs, c->ev_prep[k], 0));
+      counter += (k & 1);
+    }
     if (i1 > i0) {
-      CU_TRY(c, cudaMemsetAsync(c->d_counter.p, 0, 8, s));
+      CU_TRY(c, cudaMemsetAsync(counter, 0, 4, gs));
       P2PArgs aa = a;
       aa.items = items_dev + i0;
       aa.n_items = i1 - i0;
-      dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, s, c->warp_e);
+      aa.next_item = counter;
+      dispatch_tile(c->kernel, c->smoother, aa, i1 - i0, gs, c->warp_e);
       ++nk;
     }
     if (f1 > f0) {
-      p2p_finalize_kernel<<<f1 - f0, 128, 0, s>>>(fins_dev + f0, f1 - f0,
-                                                   c->d_partial.as<double2>(), c->out_dev);
+      p2p_finalize_kernel<<<f1 - f0, 128, 0, gs>>>(fins_dev + f0, f1 - f0,
+                                                    c->d_partial.as<double2>(), c->out_dev);
       ++nk;
     }
-    CU_TRY(c, cudaEventRecord(c->ev_group[k], s));
+    CU_TRY(c, cudaEventRecord(c->ev_group[k], gs));
     CU_TRY(c, cudaGetLastError());
     return FMMCU_OK;
   };
@@ -1273,6 +1289,8 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   }
   tr.mark("pack+h2d (overlapped)");
   c->self_layout = all_self;
+  if (two_streams)  // the last group of each group stream
+    for (int g = std::max(0, K - 2); g < K; ++g) CU_TRY(c, cudaStreamWaitEvent(s, c->ev_group[g], 0));
   CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaEventRecord(c->ev_end, s));
   tr.mark("enqueue done");
@@ -1512,6 +1530,10 @@ int fmmcu_create(fmmcu_ctx** out, int device) {
     return fail(e);
   if ((e = cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming)) != cudaSuccess)
     return fail(e);
+  for (cudaStream_t& gs : c->grp_stream)
+    if ((e = cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+  for (cudaEvent_t& ep : c->ev_prep)
+    if ((e = cudaEventCreateWithFlags(&ep, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
   for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
     if ((e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDefault)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_group[i], cudaEventDefault)) != cudaSuccess)
@@ -1573,6 +1595,10 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamDestroy(c->h2d_stream);
     if (c->ev_evals) cudaEventDestroy(c->ev_evals);
     if (c->ev_staged) cudaEventDestroy(c->ev_staged);
+    for (cudaStream_t gs : c->grp_stream)
+      if (gs) cudaStreamSynchronize(gs), cudaStreamDestroy(gs);
+    for (cudaEvent_t ep : c->ev_prep)
+      if (ep) cudaEventDestroy(ep);
     for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
       if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
     for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)

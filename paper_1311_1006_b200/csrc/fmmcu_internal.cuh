@@ -154,6 +154,8 @@ struct fmmcu_ctx {
   cudaStream_t h2d_stream = nullptr;
   static constexpr int kMaxChunks = 32;
   cudaEvent_t ev_chunk[kMaxChunks] = {}, ev_group[kMaxChunks] = {};
+  cudaEvent_t ev_prep[kMaxChunks] = {};  // chunk k prepared on the stream (two-stream groups)
+  cudaStream_t grp_stream[2] = {};       // group kernels alternate between these
   int n_groups = 0;
   cudaEvent_t ev_evals = nullptr;  // evals uploaded (overlapped launch, non-self layouts)
   cudaEvent_t ev_staged = nullptr;  // CSR + work list uploaded (overlapped launch)

@@ -27,6 +27,16 @@ out = np.zeros((len(zp), 2))
 for arr in (out, zp, mp, pt, ev, so, si):
     ctx.host_register(arr)
 ts = []
+for r in range(3 if a.reps > 2 else 0):  # split: make_job / launch / finish
+    t0 = time.perf_counter()
+    job, keep = N.CudaContext.make_job(pt, ev, so, si, t.perm, zp, mp, zp, sid, out)
+    t1 = time.perf_counter()
+    ctx.launch(job, keep)
+    t2 = time.perf_counter()
+    pairs, secs = ctx.finish()
+    t3 = time.perf_counter()
+    print(f"split: make_job {1e3 * (t1 - t0):.3f} ms, launch {1e3 * (t2 - t1):.3f} ms, "
+          f"finish {1e3 * (t3 - t2):.3f} ms, busy {1e3 * secs:.3f} ms", flush=True)
 for r in range(a.reps):
     t0 = time.perf_counter()
     _, pairs, secs = N.p2p(ctx, pt, ev, so, si, t.perm, zp, mp, zp, sid, out=out)
