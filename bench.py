@@ -600,6 +600,28 @@ def run_ours(args):
             "workload": "init_shear_layer(2e6, aspect 8), gaussian smoother, p formula (19), "
                         "AT3b cap 0.1 from theta 0.5 / L 9, FmmEngine device_pipeline; wall "
                         "includes the host Euler steps"}
+        # the same with AT3a (level count steered by the wait sign, autotune.cpp:155):
+        # (a) device pipeline, wait = far stream's idle tail before the P2P end;
+        # (b) the paper's split -- CPU far field (host tree, P2M/M2M/M2L/L2L on all
+        #     host cores) against the GPU near field, wait = CPU time blocked in
+        #     finish() -- 20 steps (each evaluate runs the host tree)
+        for key, steps, extra in (("config5_vortex_at3a", 100, dict(device_pipeline=True)),
+                                  ("config5_vortex_hybrid_at3a", 20, {})):
+            acfg = F.FmmConfig(theta=0.5, n_levels=9, p_rule="formula", backend="cuda",
+                               devices=(local,), worker_threads=os.cpu_count(), **extra)
+            t0 = time.perf_counter()
+            tra, _ = F.vortex_run(2_000_000, 8.0, steps, acfg, tuner="at3a", cap=0.1, seed=1)
+            wall = time.perf_counter() - t0
+            fmm[key] = {
+                "value": steps / wall, "unit": "steps/s", "steps": steps, "wall_s": round(wall, 3),
+                "t_total_ms_median": round(1e3 * float(np.median(tra[:, 0])), 3),
+                "n_levels_trajectory": [int(x) for x in tra[:, 6]],
+                "wait_ms_first_last": [round(1e3 * float(tra[0, 4]), 3),
+                                       round(1e3 * float(tra[-1, 4]), 3)],
+                "workload": "init_shear_layer(2e6, aspect 8), gaussian smoother, p formula, AT3a "
+                            "from theta 0.5 / L 9, " +
+                            ("FmmEngine device_pipeline" if extra else
+                             "FmmEngine hybrid: CPU far field || GPU near field")}
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:

@@ -213,7 +213,10 @@ class Tree:
 
     def __del__(self):
         if getattr(self, "h", None):
-            host_lib().fmmh_tree_free(self.h)
+            try:
+                host_lib().fmmh_tree_free(self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def leaf_csr(self):
