@@ -611,12 +611,12 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
       const double* rad = P->radius.as<double>() + P->box_base[l];
       CU_TRY(c, cudaMemsetAsync(cs + nbox, 0, 4, s));
       CU_TRY(c, cudaMemsetAsync(cw + nbox, 0, 4, s));
-      classify_kernel<false><<<blocks(nbox), TB, 0, s>>>(
+      classify_kernel<false><<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
           pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, cs, cw, nullptr,
           nullptr, nullptr, nullptr, 0xFFFFFFFFu, 0xFFFFFFFFu, ovf);
       if (int rc = scan_excl(c, P, cs, lc.s_off.as<uint32_t>(), nbox + 1, s)) return rc;
       if (int rc = scan_excl(c, P, cw, lc.w_off.as<uint32_t>(), nbox + 1, s)) return rc;
-      classify_kernel<true><<<blocks(nbox), TB, 0, s>>>(
+      classify_kernel<true><<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
           pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, nullptr, nullptr,
           lc.s_off.as<uint32_t>(), lc.w_off.as<uint32_t>(), lc.s_idx.as<uint32_t>(),
           lc.w_idx.as<uint32_t>(), scap[l], wcap[l], ovf);
@@ -647,7 +647,7 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
     CU_TRY(c, lc.w_off.ensure((nbox + 1) * 4));
     CU_TRY(c, cudaMemsetAsync(cs + nbox, 0, 4, s));
     CU_TRY(c, cudaMemsetAsync(cw + nbox, 0, 4, s));
-    classify_kernel<false><<<blocks(nbox), TB, 0, s>>>(
+    classify_kernel<false><<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
         pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, cs, cw, nullptr,
         nullptr, nullptr, nullptr);
     if (int rc = scan_excl(c, P, cs, lc.s_off.as<uint32_t>(), nbox + 1, s)) return rc;
@@ -660,7 +660,7 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
     lc.w_nnz = hc[1];
     CU_TRY(c, lc.s_idx.ensure(uint64_t(std::max(lc.s_nnz, 1u)) * 4));
     CU_TRY(c, lc.w_idx.ensure(uint64_t(std::max(lc.w_nnz, 1u)) * 4));
-    classify_kernel<true><<<blocks(nbox), TB, 0, s>>>(
+    classify_kernel<true><<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
         pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, nullptr, nullptr,
         lc.s_off.as<uint32_t>(), lc.w_off.as<uint32_t>(), lc.s_idx.as<uint32_t>(),
         lc.w_idx.as<uint32_t>());

@@ -304,6 +304,23 @@ __global__ void leaf_of_kernel(const uint32_t* __restrict__ list, uint32_t n,
 }
 
 // ------------------------------------------------------- connectivity -----
+// The reference's theta criterion (geometry.cpp:13-19):
+//   max(ra, rb) + theta * min(ra, rb) <= theta * |ca - cb|,  |.| = glibc hypot
+__device__ __forceinline__ bool theta_weak_exact(double big, double small, double dx, double dy,
+                                                 double theta) {
+  const double d = fmm_hypot(dx, dy);
+  return __dadd_rn(big, __dmul_rn(theta, small)) <= __dmul_rn(theta, d);
+}
+
+// Same decision, bit for bit, at a fraction of the cost: a single-precision
+// square root of dx^2 + dy^2 (relative error < 3e-7) settles every candidate
+// whose two sides differ by more than 1e-6 relative; only the band around
+// equality (and out-of-range magnitudes) runs the restated glibc hypot.
+// Soundness: with l = big + theta*small as rounded above, D = |(dx, dy)|
+// exactly and a = the fast root, theta*hypot(dx, dy) as rounded lies in
+// theta*D*(1 +- 4e-16) while a lies in D*(1 +- 3e-7); so l < theta*a*(1-1e-6)
+// implies l <= theta (x) hypot, and l > theta*a*(1+1e-6) implies the
+// opposite.
 __device__ __forceinline__ bool theta_weak(const double2* __restrict__ c,
                                            const double* __restrict__ r, uint32_t a, uint32_t b,
                                            double theta) {
@@ -311,11 +328,24 @@ __device__ __forceinline__ bool theta_weak(const double2* __restrict__ c,
   const double big = ra < rb ? rb : ra;    // std::max
   const double small = rb < ra ? rb : ra;  // std::min
   const double2 ca = c[a], cb = c[b];
-  const double d = fmm_hypot(__dsub_rn(ca.x, cb.x), __dsub_rn(ca.y, cb.y));
-  return __dadd_rn(big, __dmul_rn(theta, small)) <= __dmul_rn(theta, d);
+  const double dx = __dsub_rn(ca.x, cb.x), dy = __dsub_rn(ca.y, cb.y);
+  const double l = __dadd_rn(big, __dmul_rn(theta, small));
+  const double d2 = dx * dx + dy * dy;
+  if (d2 > 1e-30 && d2 < 1e30) {
+    const double ta = theta * double(sqrtf(float(d2)));
+    if (l < ta * (1.0 - 1e-6)) return true;
+    if (l > ta * (1.0 + 1e-6)) return false;
+  }
+  return theta_weak_exact(big, small, dx, dy, theta);
 }
 
-// Pass 1 (fill == false): counts; pass 2: rows at the scanned offsets.
+// One warp per box a: its candidates are the children 4pq..4pq+3 of its
+// parent's strong partners pq, in ascending order (so every row comes out
+// sorted, as the reference's); 32 candidates per step, classified by the
+// lanes, compacted in order by ballots.  Pass 1 (fill == false) counts;
+// pass 2 writes the rows at the scanned offsets.  (A thread per box walked a
+// clustered box's thousands of candidates serially: 9 ms of the 1M gauss8
+// pipeline.)
 template <bool FILL>
 __global__ void classify_kernel(const uint32_t* __restrict__ ps_off,
                                 const uint32_t* __restrict__ ps_idx, const double2* __restrict__ c,
@@ -325,32 +355,37 @@ __global__ void classify_kernel(const uint32_t* __restrict__ ps_off,
                                 uint32_t* __restrict__ s_idx, uint32_t* __restrict__ w_idx,
                                 uint32_t s_cap = 0xFFFFFFFFu, uint32_t w_cap = 0xFFFFFFFFu,
                                 int* __restrict__ overflow = nullptr) {
-  const uint32_t a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= nbox) return;
+  const uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (a >= nbox) return;  // warp-uniform
   if (overflow && *overflow) return;  // a coarser level did not fit: lists are invalid
   const uint32_t p = a >> 2;
-  uint32_t ns = 0, nw = 0;
   uint32_t so = FILL ? s_off[a] : 0, wo = FILL ? w_off[a] : 0;
   // capacity guard: the lists may be filled into buffers sized by a guess
   // before the host has read the counts (a miss is flagged and redone)
   if (FILL && overflow && (uint64_t(s_off[a + 1]) > s_cap || uint64_t(w_off[a + 1]) > w_cap)) {
-    *overflow = 1;
+    if (lane == 0) *overflow = 1;
     return;
   }
-  for (uint32_t q = ps_off[p]; q < ps_off[p + 1]; ++q) {
-    const uint32_t pq = ps_idx[q];
-    for (uint32_t b = 4 * pq; b < 4 * pq + 4; ++b) {
-      const bool weak = (a != b) && theta_weak(c, r, a, b, theta);
-      if (weak) {
-        if (FILL) w_idx[wo + nw] = b;
-        ++nw;
-      } else {
-        if (FILL) s_idx[so + ns] = b;
-        ++ns;
-      }
+  const uint32_t q0 = ps_off[p];
+  const uint32_t ncand = 4 * (ps_off[p + 1] - q0);
+  const unsigned below = (1u << lane) - 1u;
+  uint32_t ns = 0, nw = 0;
+  for (uint32_t k0 = 0; k0 < ncand; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    const bool valid = k < ncand;
+    const uint32_t b = valid ? 4 * ps_idx[q0 + (k >> 2)] + (k & 3u) : 0u;
+    const bool weak = valid && a != b && theta_weak(c, r, a, b, theta);
+    const unsigned mw = __ballot_sync(0xffffffffu, valid && weak);
+    const unsigned ms = __ballot_sync(0xffffffffu, valid && !weak);
+    if (FILL && valid) {
+      if (weak) w_idx[wo + nw + __popc(mw & below)] = b;
+      else s_idx[so + ns + __popc(ms & below)] = b;
     }
+    nw += __popc(mw);
+    ns += __popc(ms);
   }
-  if (!FILL) {
+  if (!FILL && lane == 0) {
     s_cnt[a] = ns;
     w_cnt[a] = nw;
   }

@@ -206,3 +206,28 @@ def test_device_work_list_equals_host_work_list(ctx, force_e, monkeypatch):
         monkeypatch.delenv("FMMCU_HOST_WL")
         assert np.array_equal(dev.view(np.uint64), host.view(np.uint64)), name
         assert sd["p2p_pairs"] == sh["p2p_pairs"], name
+
+
+def test_device_tree_bitwise_equal_to_reference_golden(ctx, golden_trees):
+    """The device pyramid and connectivity against the trees the REFERENCE
+    built (tests/golden/tree_*.npz, make_golden.py over build_pyramid /
+    build_connectivity, geometry.cpp:106-216) -- directly, not through the
+    host library: box ranges, geometry, perm, eval_perm and the strong and
+    weak lists of every level, bitwise."""
+    for name, d in golden_trees.items():
+        L, theta = int(d["n_levels"]), float(d["theta"])
+        z = d["z"][:, 0] + 1j * d["z"][:, 1]
+        m = d["m"][:, 0] + 1j * d["m"][:, 1]
+        y = d["y"][:, 0] + 1j * d["y"][:, 1]
+        sid = d["sid"] if "sid" in d else None
+        ctx.fmm_evaluate(z, m, y, sid, n_levels=L, theta=theta, p=17)
+        bf, bu, perm, eperm, strong, weak = ctx.fmm_tree(L, len(z), len(y))
+        for lvl in range(L):
+            assert np.array_equal(bu[lvl], d[f"boxes_u_{lvl}"]), (name, lvl, "ranges")
+            assert np.array_equal(bf[lvl].view(np.uint64),
+                                  d[f"boxes_f_{lvl}"].view(np.uint64)), (name, lvl, "geometry")
+            for kind, got in (("strong", strong[lvl]), ("weak", weak[lvl])):
+                assert np.array_equal(got[0], d[f"{kind}_off_{lvl}"]), (name, lvl, kind)
+                assert np.array_equal(got[1], d[f"{kind}_idx_{lvl}"]), (name, lvl, kind)
+        assert np.array_equal(perm, d["perm"]), name
+        assert np.array_equal(eperm, d["eval_perm"]), name
