@@ -121,6 +121,12 @@ int fmmcu_p2p_finish(fmmcu_ctx *ctx, uint64_t *pair_evals, double *seconds);
  * slice by slice instead of through pinned staging + a host copy in finish. */
 int fmmcu_host_register(fmmcu_ctx *ctx, void *ptr, uint64_t bytes);
 int fmmcu_host_unregister(fmmcu_ctx *ctx, void *ptr);
+/* The same without a context (portable registration, every context sees it):
+ * used by owners of long-lived host buffers, e.g. the engine handle of
+ * include/fmm_host.h that keeps its SourceSet / EvalSet / EvalResult between
+ * evaluations, so the device pipeline DMAs them in place. */
+int fmmcu_pin_host(void *ptr, uint64_t bytes);
+int fmmcu_unpin_host(void *ptr);
 
 /* ---- device-resident near field (benchmarks, multi-GPU sharding) -------- */
 /* Uploads and packs the job's inputs once (synchronous); they stay resident. */

@@ -1764,6 +1764,27 @@ int fmmcu_host_register(fmmcu_ctx* c, void* ptr, uint64_t bytes) {
   return FMMCU_OK;
 }
 
+int fmmcu_pin_host(void* ptr, uint64_t bytes) {
+  if (!ptr || !bytes) return FMMCU_EINVAL;
+  const cudaError_t e =
+      cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? FMMCU_ENOMEM : FMMCU_ECUDA;
+  }
+  return FMMCU_OK;
+}
+
+int fmmcu_unpin_host(void* ptr) {
+  if (!ptr) return FMMCU_EINVAL;
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return FMMCU_ECUDA;
+  }
+  return FMMCU_OK;
+}
+
 int fmmcu_host_unregister(fmmcu_ctx* c, void* ptr) {
   if (!c || !ptr) return FMMCU_EINVAL;
   CU_TRY(c, cudaSetDevice(c->device));

@@ -9,6 +9,7 @@
 #include "fmm/autotune.hpp"
 #include "fmm/cuda_backend.hpp"
 #include "fmm/engine.hpp"
+#include "fmm_cuda.h"
 #include "fmm/sims.hpp"
 #include "fmm_host.h"
 
@@ -131,12 +132,45 @@ namespace {
 // An engine handle keeps the last call's SourceSet / EvalSet / EvalResult, so
 // repeated evaluations of one problem size (time stepping, benchmarks) refill
 // warm storage instead of allocating and first-touching ~56 B per point.
+// The handle keeps its SourceSet / EvalSet / EvalResult between calls (one
+// problem size evaluated repeatedly: benchmarks, time stepping).  With the
+// cuda backend their storage is page-locked once (fmmcu_pin_host) so the
+// device paths DMA inputs and potentials in place instead of through pinned
+// staging and a host copy; the handle owns the vectors, so it unpins before
+// any of them can reallocate and when it is destroyed.
+struct PinnedRange {
+  void* p = nullptr;
+  std::size_t bytes = 0;
+};
+
 struct EngineHandle {
   FmmEngine eng;
   SourceSet s;
   EvalSet e;
   EvalResult r;
+  PinnedRange pin[4];  // z, m, y, potentials
   explicit EngineHandle(FmmConfig cfg) : eng(std::move(cfg)) {}
+  ~EngineHandle() { unpin_all(); }
+  void unpin_all() {
+    for (PinnedRange& q : pin) {
+      if (q.p) fmmcu_unpin_host(q.p);
+      q = PinnedRange{};
+    }
+  }
+  // pin the current storage of the four vectors (sizes already final)
+  void pin_all() {
+    void* ptr[4] = {s.z.data(), s.m.data(), e.y.data(), r.potentials.data()};
+    const std::size_t bytes[4] = {s.z.size() * 16, s.m.size() * 16, e.y.size() * 16,
+                                  r.potentials.size() * 16};
+    for (int i = 0; i < 4; ++i) {
+      PinnedRange& q = pin[i];
+      if (q.p == ptr[i] && q.bytes == bytes[i]) continue;
+      if (q.p) fmmcu_unpin_host(q.p);
+      q = PinnedRange{};
+      if (bytes[i] >= (std::size_t(1) << 20) && fmmcu_pin_host(ptr[i], bytes[i]) == FMMCU_OK)
+        q = PinnedRange{ptr[i], bytes[i]};
+    }
+  }
 };
 
 void par_copy(void* dst, const void* src, std::size_t bytes) {
@@ -312,6 +346,13 @@ int fmmh_engine_evaluate(void* h, const double* z, const double* m, int64_t n_sr
                          double* timings, uint64_t* counters, int* p) {
   return guarded([&] {
     EngineHandle* H = static_cast<EngineHandle*>(h);
+    const std::size_t ns = std::size_t(n_src > 0 ? n_src : 0);
+    const std::size_t ne = std::size_t(n_eval > 0 ? n_eval : 0);
+    const bool cuda = H->eng.config().backend == BackendKind::cuda;
+    // a vector that will reallocate must not be freed while registered
+    if (H->s.z.capacity() < ns || H->s.m.capacity() < ns || H->e.y.capacity() < ne ||
+        H->r.potentials.capacity() < ne || !cuda)
+      H->unpin_all();
     fill_par(H->s.z, z, n_src);
     fill_par(H->s.m, m, n_src);
     fill_par(H->e.y, y, n_eval > 0 ? n_eval : 0);
@@ -319,6 +360,10 @@ int fmmh_engine_evaluate(void* h, const double* z, const double* m, int64_t n_sr
       fill_par(H->e.source_id, sid, n_eval);
     else
       H->e.source_id.clear();
+    if (cuda) {
+      H->r.potentials.resize(ne);  // evaluate_into keeps storage of the right size
+      H->pin_all();
+    }
     H->eng.evaluate_into(H->s, H->e, H->r);
     const EvalResult& r = H->r;
     if (out && !r.potentials.empty()) par_copy(out, r.potentials.data(), r.potentials.size() * 16);

@@ -231,3 +231,23 @@ def test_device_tree_bitwise_equal_to_reference_golden(ctx, golden_trees):
                 assert np.array_equal(got[1], d[f"{kind}_idx_{lvl}"]), (name, lvl, kind)
         assert np.array_equal(perm, d["perm"]), name
         assert np.array_equal(eperm, d["eval_perm"]), name
+
+
+def test_engine_handle_pinned_io_is_identical(ctx):
+    """The engine handle page-locks its kept SourceSet / EvalSet / EvalResult
+    (fmmcu_pin_host) once the cuda backend is in use, so the device pipeline
+    DMAs inputs and potentials in place.  Results must be bitwise those of a
+    plain fmm_evaluate, across repeated calls, a size change (the storage is
+    unpinned before it reallocates) and a switch to the pool backend."""
+    a = F.make_distribution("uniform", 1_200_000, 41)
+    b = F.make_distribution("uniform", 1_500_000, 42)
+    eng = F.FmmEngine(F.FmmConfig(n_levels=8, backend="cuda", device_pipeline=True))
+    for s in (a, a, b, a):
+        e = F.EvalSet.self_of(s)
+        got = eng.evaluate(s, e).potentials
+        want, _ = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=8, theta=0.5, p=17)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    eng.set_config(F.FmmConfig(n_levels=8, backend="pool", worker_threads=8))
+    e = F.EvalSet.self_of(a)
+    ref = eng.evaluate(a, e).potentials
+    assert np.abs(ref - want).max() <= 1e-12 * np.abs(ref).max()
