@@ -184,9 +184,9 @@ void dispatch_exact(int kn, int sm, const P2PArgs& a, uint32_t lb, uint32_t le, 
   }
 }
 
-template <int SM, int E, int W = 4, int C = 128, int U = 1, int MINB = 3>
+template <int SM, int E, int W = 4, int C = 128, int U = 1, int MINB = 3, int SS = 1>
 void launch_sym_v(const P2PArgs& a, const P2PSymArgs& sa, uint32_t n_items, cudaStream_t s) {
-  auto kfn = p2p_sym_kernel<SM, E, W, C, U, MINB>;
+  auto kfn = p2p_sym_kernel<SM, E, W, C, U, MINB, SS>;
   constexpr size_t smem = size_t(W) * sym_region_bytes(C, E);
   static int grid_cap = [&] {
     cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -203,13 +203,14 @@ void launch_sym_v(const P2PArgs& a, const P2PSymArgs& sa, uint32_t n_items, cuda
 }
 
 // mutual-kernel shapes (FMMCU_SYM_VARIANT, harmonic / no smoother):
-//   E = 5: 0 = 4w c128 u1 m3   1 = 4w c256 u1 m3   2 = 2w c128 u1 m6   3 = 4w c128 u2 m3
-// (r2, 10M / L10: 0 and 2 4.27 ms; a 4-CTA cap at 128 registers 4.60 ms; E = 4 5.89 ms)
+//   E = 5: 0 = 4w c128 u1 m3, one symmetric source per step   1 = c256   2 = 2w m6
+//          3 = u2   4 = m4 (128 registers)   5 = two sources per step   6 = three
+// (r2, 10M / L10: 0 4.06 ms, 4 4.25, 5 4.27-4.45, 6 4.67; E = 4 5.89 ms)
 int sym_variant() {
   static int v = [] {
     const char* e = std::getenv("FMMCU_SYM_VARIANT");
     const int i = e ? std::atoi(e) : 0;
-    return (i >= 0 && i < 4) ? i : 0;
+    return (i >= 0 && i < 7) ? i : 0;
   }();
   return v;
 }
@@ -221,6 +222,9 @@ void dispatch_sym(int sm, const P2PArgs& a, const P2PSymArgs& sa, uint32_t n, cu
       case 1: launch_sym_v<0, 5, 4, 256, 1, 3>(a, sa, n, s); return;
       case 2: launch_sym_v<0, 5, 2, 128, 1, 6>(a, sa, n, s); return;
       case 3: launch_sym_v<0, 5, 4, 128, 2, 3>(a, sa, n, s); return;
+      case 4: launch_sym_v<0, 5, 4, 128, 1, 4, 1>(a, sa, n, s); return;
+      case 5: launch_sym_v<0, 5, 4, 128, 1, 3, 2>(a, sa, n, s); return;
+      case 6: launch_sym_v<0, 5, 4, 128, 1, 3, 3>(a, sa, n, s); return;
       default: break;
     }
   }

@@ -3,6 +3,7 @@
 #include <numeric>
 
 #include "fmm/sims.hpp"
+#include "fmm_cuda.h"
 
 namespace fmm::sims {
 
@@ -20,6 +21,41 @@ void use_vortex_kernel(FmmEngine& engine, double delta) {
   cfg.smoother = Smoother::gaussian(delta);
   engine.set_config(cfg);
 }
+
+// Per-thread step buffers.  With the cuda backend their storage is
+// page-locked (fmmcu_pin_host) so the device pipeline DMAs the sources and
+// the potentials in place; unpinned before any reallocation and at thread
+// exit.
+struct StepBuffers {
+  SourceSet src;
+  EvalSet ev;
+  EvalResult r;
+  void* p[4] = {};
+  std::size_t b[4] = {};
+  ~StepBuffers() { unpin(); }
+  void unpin() {
+    for (int i = 0; i < 4; ++i) {
+      if (p[i]) fmmcu_unpin_host(p[i]);
+      p[i] = nullptr;
+      b[i] = 0;
+    }
+  }
+  void pin() {
+    void* ptr[4] = {src.z.data(), src.m.data(), ev.y.data(), r.potentials.data()};
+    const std::size_t bytes[4] = {src.z.size() * 16, src.m.size() * 16, ev.y.size() * 16,
+                                  r.potentials.size() * 16};
+    for (int i = 0; i < 4; ++i) {
+      if (p[i] == ptr[i] && b[i] == bytes[i]) continue;
+      if (p[i]) fmmcu_unpin_host(p[i]);
+      p[i] = nullptr;
+      b[i] = 0;
+      if (bytes[i] >= (std::size_t(1) << 20) && fmmcu_pin_host(ptr[i], bytes[i]) == FMMCU_OK) {
+        p[i] = ptr[i];
+        b[i] = bytes[i];
+      }
+    }
+  }
+};
 
 }  // namespace
 
@@ -72,19 +108,25 @@ std::vector<cplx> vortex_velocities(const VortexSystem& sys, FmmEngine& engine, 
   // (self) evals and the result live in per-thread buffers that are refilled
   // in parallel, and evaluate_into() reuses the result storage.  Same values
   // as building them afresh (reference sims.cpp:66-84).
-  thread_local SourceSet tl_src;
-  thread_local EvalSet tl_ev;
-  thread_local EvalResult tl_r;
+  thread_local StepBuffers tl;
   // plain references: inside the OpenMP regions a thread_local name would
   // denote each worker's own (empty) copy
-  SourceSet& src = tl_src;
-  EvalSet& ev = tl_ev;
-  EvalResult& r = tl_r;
+  StepBuffers& B = tl;
+  SourceSet& src = B.src;
+  EvalSet& ev = B.ev;
+  EvalResult& r = B.r;
   const std::int64_t n = std::int64_t(sys.size());
+  const bool cuda = engine.config().backend == BackendKind::cuda;
+  if (!cuda || src.z.capacity() < std::size_t(n) || r.potentials.capacity() < std::size_t(n))
+    B.unpin();  // never free registered storage
   src.z.resize(n);
   src.m.resize(n);
   ev.y.resize(n);
   ev.source_id.resize(n);
+  if (cuda) {
+    r.potentials.resize(n);  // evaluate_into keeps storage of the right size
+    B.pin();
+  }
 #pragma omp parallel for schedule(static)
   for (std::int64_t k = 0; k < n; ++k) {
     src.z[k] = sys.pos[k];

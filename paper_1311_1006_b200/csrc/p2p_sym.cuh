@@ -66,7 +66,7 @@ __device__ __forceinline__ void sym_pair(double yx, double yy, double mex, doubl
   ci = fma(mex, wi, fma(mey, wr, ci));
 }
 
-template <int SMOOTH, int E, int WARPS, int C, int U, int MINB>
+template <int SMOOTH, int E, int WARPS, int C, int U, int MINB, int SS = 1>
 __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs a,
                                                                    const P2PSymArgs sa) {
   static_assert(C % 32 == 0, "shape");
@@ -222,23 +222,28 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
         const uint32_t F = 32 / K;
         for (uint32_t sb = 0; sb < steps; sb += F) {
           const uint32_t nst = min(F, steps - sb);
-          for (uint32_t st = 0; st < nst; st += 2) {
-            const uint32_t j0 = ord_end + (sb + st) * K + k, j1 = j0 + K;
-            const bool v0ok = active && j0 < len;
-            const bool v1ok = active && st + 1 < nst && j1 < len;
-            const double4 s0 = v0ok ? chunk[j0] : make_double4(-1e30, -1e30, 0.0, 0.0);
-            const double4 s1 = v1ok ? chunk[j1] : make_double4(-1e30, -1e30, 0.0, 0.0);
-            double c0r = 0.0, c0i = 0.0, c1r = 0.0, c1i = 0.0;
+          // SS symmetric sources per step (x E evals in flight per lane)
+          for (uint32_t st = 0; st < nst; st += SS) {
+            double4 sv[SS];
+            double cr[SS], ci[SS];
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-              sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], s0, a.inv_delta2, a.delta2, ar[e],
-                               ai[e], c0r, c0i);
-              sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], s1, a.inv_delta2, a.delta2, ar[e],
-                               ai[e], c1r, c1i);
+            for (int u = 0; u < SS; ++u) {
+              const uint32_t j = ord_end + (sb + st + u) * K + k;
+              const bool ok = active && st + u < nst && j < len;
+              sv[u] = ok ? chunk[j] : make_double4(-1e30, -1e30, 0.0, 0.0);
+              cr[u] = 0.0;
+              ci[u] = 0.0;
             }
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+#pragma unroll
+              for (int u = 0; u < SS; ++u)
+                sym_pair<SMOOTH>(yx[e], yy[e], mx[e], my[e], sv[u], a.inv_delta2, a.delta2, ar[e],
+                                 ai[e], cr[u], ci[u]);
             if (active) {
-              part[g * 32 + st * K + k] = make_double2(c0r, c0i);
-              if (st + 1 < nst) part[g * 32 + (st + 1) * K + k] = make_double2(c1r, c1i);
+#pragma unroll
+              for (int u = 0; u < SS; ++u)
+                if (st + u < nst) part[g * 32 + (st + u) * K + k] = make_double2(cr[u], ci[u]);
             }
           }
           __syncwarp();
