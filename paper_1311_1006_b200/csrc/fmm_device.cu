@@ -1191,7 +1191,7 @@ int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {
   double t_wait = 0, t_copy = 0;
   for (int i = 0; i < P->n_chunks; ++i) {
     const auto a = Clock::now();
-    CU_TRY(c, cudaEventSynchronize(P->ev_res[i]));
+    CU_TRY(c, wait_event(P->ev_res[i]));
     const auto b = Clock::now();
     const uint32_t e0 = P->chunk_off[i], e1 = P->chunk_off[i + 1];
     if (reinterpret_cast<double2*>(out) != P->res_host)
@@ -1210,7 +1210,7 @@ int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {
     std::fprintf(stderr, "\n");
   }
   cudaEvent_t* ev = P->ev;
-  CU_TRY(c, cudaEventSynchronize(ev[10]));
+  CU_TRY(c, wait_event(ev[10]));
   CU_TRY(c, cudaGetLastError());
   if (*P->h_flag.as<int>())
     return set_err(c, FMMCU_ESINGULAR, "m2l: target center coincides with source center");

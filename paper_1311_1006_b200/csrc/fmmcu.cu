@@ -1722,12 +1722,12 @@ int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
   CU_TRY(c, cudaSetDevice(c->device));
   // staged output: copy each slice out as soon as its D2H has landed
   for (int i = 0; i < c->n_slices; ++i) {
-    CU_TRY(c, cudaEventSynchronize(c->ev_cslice[i]));
+    CU_TRY(c, wait_event(c->ev_cslice[i]));
     const uint32_t sb = c->slice_eb[i], se = c->slice_eb[i + 1];
     if (!c->direct_out && se > sb)
       par_memcpy(c->job.out + 2 * size_t(sb), c->h_out.as<double2>() + sb, size_t(se - sb) * 16);
   }
-  CU_TRY(c, cudaEventSynchronize(c->ev_end));
+  CU_TRY(c, wait_event(c->ev_end));
   CU_TRY(c, cudaGetLastError());
   if (c->overlapped && c->trace) {
     for (int k = 0; k < c->n_groups; ++k) {
@@ -1990,7 +1990,7 @@ int fmmcu_m2l_finish(fmmcu_ctx* c, uint64_t* ops, double* seconds) {
   if (!c->m2l_inflight) return set_err(c, FMMCU_ESTATE, "m2l finish without launch");
   c->m2l_inflight = false;
   CU_TRY(c, cudaSetDevice(c->device));
-  CU_TRY(c, cudaEventSynchronize(c->ev_m2l1));
+  CU_TRY(c, wait_event(c->ev_m2l1));
   CU_TRY(c, cudaGetLastError());
   float ms = 0.f;
   CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_m2l0, c->ev_m2l1));
