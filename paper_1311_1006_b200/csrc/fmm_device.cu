@@ -1013,8 +1013,12 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   // FMMCU_HOST_WL keep the host builder: the finest CSR goes to pinned host
   // vectors right away and the host builds the list meanwhile.
   const LevelConnDev& fc = P->conn[L - 1];
-  const bool pipe_sym = self && P->layout_same && j->kernel == 0 && std::getenv("FMMCU_PIPE_SYM");
-  const bool host_wl = pipe_sym || std::getenv("FMMCU_HOST_WL") != nullptr;
+  // The mutual kernel applies to self-evaluation with the harmonic kernel
+  // (antisymmetric pair term) in the self layout; FMMCU_PIPE_ORDERED=1 keeps
+  // the ordered kernel.
+  const bool pipe_sym = self && P->layout_same && j->kernel == 0 &&
+                        !std::getenv("FMMCU_PIPE_ORDERED");
+  const bool host_wl = std::getenv("FMMCU_HOST_WL") != nullptr;
   CU_TRY(c, cudaEventRecord(ev[12], s));
   if (host_wl) {
     cudaStream_t ds = c->d2h_stream;
@@ -1072,11 +1076,11 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   c->ext_out = nullptr;
   c->group_k = 0;
   if (!host_wl) {
-    cudaStream_t ws = c->d2h_stream;
+    cudaStream_t ws = c->wl_stream;
     CU_TRY(c, cudaStreamWaitEvent(ws, ev[12], 0));
     if (int rc = stage_csr_dev(c, P->soff.as<uint32_t>() + P->off_base[L - 1],
                                P->eoff.as<uint32_t>() + P->off_base[L - 1], fc.s_off.as<uint32_t>(),
-                               fc.s_idx.as<uint32_t>(), nleaf, fc.s_nnz, M, ws, ev[13]))
+                               fc.s_idx.as<uint32_t>(), nleaf, fc.s_nnz, M, ws, ev[13], pipe_sym))
       return rc;
     CU_TRY(c, cudaStreamWaitEvent(s, ev[13], 0));
     if (M) {  // eval records {x, y, self slot, strong entry of the self slot}
@@ -1217,7 +1221,7 @@ int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {
   if (st) {
     const uint32_t nleaf = uint32_t(pow4(P->L - 1));
     const uint64_t hits = *c->h_hits.as<unsigned long long>();
-    st->p2p_pairs = (c->dev_wl ? c->dev_wl_total : c->leaf_work[nleaf]) - hits;
+    st->p2p_pairs = (c->dev_list ? c->dev_list_total : c->leaf_work[nleaf]) - hits;
     st->m2l_ops = P->m2l_nnz;
     st->p2m_points = P->N;
     st->l2p_points = P->L >= 2 ? M : 0;

@@ -393,6 +393,7 @@ int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
                                 i < int64_t(np) ? uint32_t(ssym[i]) : 0u);
   tr.mark("sym: contributions");
   c->sym_slots = slots[np];
+  c->sym_n_items = uint32_t(c->items.size());
   c->sym_lb = lb;
   c->sym_le = le;
   c->sym_items = true;
@@ -442,6 +443,7 @@ void par_prefix(T* v, int64_t n) {
 int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   Trace tr(c);
   c->dev_wl = false;
+  c->dev_list = false;
   const uint32_t nl = j->n_leaves;
   c->ev_off.resize(nl + 1);
   c->leaf_work.resize(nl + 1);
@@ -1324,7 +1326,7 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
     } else if (c->sym_items) {
       if (lb != c->sym_lb || le != c->sym_le)
         return set_err(c, FMMCU_ESTATE, "symmetric work list staged for another leaf range");
-      const uint32_t ni = uint32_t(c->items.size());
+      const uint32_t ni = c->sym_n_items;
       P2PSymArgs sa{c->d_symseg.as<uint4>(), c->d_tgt.as<double2>(), c->d_contrib.as<double2>()};
       if (ni) {
         P2PArgs aa = a;
@@ -1530,6 +1532,15 @@ int fmmcu_create(fmmcu_ctx** out, int device) {
     return fail(e);
   if ((e = cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(e);
+  {
+    // the device work list is a short chain of small latency-bound kernels on
+    // the pipeline's critical path, run beside the far-field kernels: give
+    // it the highest stream priority
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if ((e = cudaStreamCreateWithPriority(&c->wl_stream, cudaStreamNonBlocking, hi)) != cudaSuccess)
+      return fail(e);
+  }
   if ((e = cudaEventCreateWithFlags(&c->ev_evals, cudaEventDisableTiming)) != cudaSuccess)
     return fail(e);
   if ((e = cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming)) != cudaSuccess)
@@ -1569,6 +1580,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamSynchronize(c->m2l_stream);
     cudaStreamSynchronize(c->d2h_stream);
     cudaStreamSynchronize(c->h2d_stream);
+    if (c->wl_stream) cudaStreamSynchronize(c->wl_stream);
     fmmcu::destroy_pipeline(c->pipe);
     c->pipe = nullptr;
     multi_release(c);
@@ -1581,7 +1593,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
                       &c->m_table, &c->m_out, &c->m_flag, &c->m_items, &c->m_iscan, &c->m_nitems,
                       &c->m_partial, &c->m_cubtmp, &c->d_wl_head, &c->d_wl_key, &c->d_wl_val,
-                      &c->d_wl_S, &c->d_wl_work, &c->d_wl_cnt, &c->d_wl_off})
+                      &c->d_wl_S, &c->d_wl_work, &c->d_wl_cnt, &c->d_wl_off, &c->d_wls})
       b->release();
     for (HostBuf* b : {&c->h_src, &c->h_evy, &c->h_eself, &c->h_out, &c->h_hits, &c->h_csr,
                        &c->mh_out, &c->mh_flag, &c->h_wl_head, &c->mb_centers, &c->mb_coeffs,
@@ -1597,6 +1609,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     cudaStreamDestroy(c->m2l_stream);
     cudaStreamDestroy(c->d2h_stream);
     cudaStreamDestroy(c->h2d_stream);
+    if (c->wl_stream) cudaStreamDestroy(c->wl_stream);
     if (c->ev_evals) cudaEventDestroy(c->ev_evals);
     if (c->ev_staged) cudaEventDestroy(c->ev_staged);
     for (cudaStream_t gs : c->grp_stream)
@@ -1646,8 +1659,8 @@ int fmmcu_p2p_launch(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     c->job = *j;
     c->run_lb = j->leaf_begin;
     c->run_le = j->leaf_end;
-    c->run_total_pairs = c->dev_wl ? c->dev_wl_total
-                                   : c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
+    c->run_total_pairs = c->dev_list ? c->dev_list_total
+                                     : c->leaf_work[j->leaf_end] - c->leaf_work[j->leaf_begin];
     c->prep_seconds = std::chrono::duration<double>(c->t_evstart - t0).count();
     c->inflight = true;
     return FMMCU_OK;

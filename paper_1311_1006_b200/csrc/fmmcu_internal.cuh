@@ -162,6 +162,7 @@ struct fmmcu_ctx {
   cudaStream_t stream = nullptr;  // current (own or external)
   cudaStream_t m2l_stream = nullptr;
   cudaStream_t d2h_stream = nullptr;  // potentials D2H, overlapping the next slice's kernels
+  cudaStream_t wl_stream = nullptr;   // highest priority: the device pipeline's work-list build
   static constexpr int kMaxSlices = 8;
   cudaEvent_t ev_kslice[kMaxSlices] = {}, ev_cslice[kMaxSlices] = {};
   int n_slices = 0;
@@ -217,13 +218,16 @@ struct fmmcu_ctx {
   std::vector<uint32_t> sw_ent, sw_nblk;
   std::vector<uint64_t> sw_ssym, sw_sord, sw_slots;
   uint64_t sym_slots = 0;               // contrib slots
+  uint32_t sym_n_items = 0;             // items of the symmetric list (host or device built)
+  DevBuf d_wls;                         // device symmetric-list scratch
   DevBuf d_symseg, d_syminfo, d_tgt, d_contrib, d_cloff, d_clcnt, d_clbase, d_cubtmp;
   HostBuf h_sym;
   // device-built work list (worklist_dev.cu): items / fins for [dev_wl_lb,
   // dev_wl_le) only, group ranges in dev_grp_item / dev_grp_fin
-  bool dev_wl = false;
+  bool dev_wl = false;          // the ordered list is device-built
   uint32_t dev_wl_lb = 0, dev_wl_le = 0;
-  uint64_t dev_wl_total = 0;  // sum of n_evals * |strong sources| over the range
+  bool dev_list = false;        // the staged list (ordered or symmetric) is device-built
+  uint64_t dev_list_total = 0;  // its range's sum of n_evals * |strong sources|
   std::vector<uint32_t> dev_grp_item, dev_grp_fin;
   DevBuf d_wl_head, d_wl_key, d_wl_val, d_wl_S, d_wl_work, d_wl_cnt, d_wl_off;
   HostBuf h_wl_head;
@@ -291,11 +295,15 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j);
 // bytes moved, ~0 on error.
 uint64_t upload_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, cudaStream_t stream);
 int build_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g, cudaStream_t s);
+// Symmetric (mutual-kernel) list + contribution lists on the device over
+// [lb, le) of the staged CSR (worklist_dev.cu); -1 = the job does not qualify.
+int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t s);
 // Device-resident CSR -> context staging, run table and device work list on
-// stream `w` (records `done` there); eval records are left to the caller.
+// stream `w` (records `done` there); want_sym: the mutual kernel's list when
+// the job qualifies.  Eval records are left to the caller.
 int stage_csr_dev(fmmcu_ctx* c, const uint32_t* pt, const uint32_t* ev, const uint32_t* so,
                   const uint32_t* si, uint32_t nl, uint32_t nnz, uint32_t ne, cudaStream_t w,
-                  cudaEvent_t done);
+                  cudaEvent_t done, bool want_sym);
 // Device buffers for the CSR + work list, their H2D, the run table and the
 // eval records (needs d_src, d_evy, d_eself filled unless c->self_layout).
 int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals);

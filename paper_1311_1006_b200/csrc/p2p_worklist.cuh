@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include "p2p_kernels.cuh"
+#include "p2p_sym.cuh"
 #include "p2p_warp.cuh"
 #include "p2p_worklist_types.cuh"
 
@@ -258,6 +259,130 @@ static __global__ void wl_fill_kernel(const uint32_t* __restrict__ ev_off,
   uint32_t a, b, c;
   wl_leaf_items(lb + i, ev_off, s_off, seg, S[i], head->max_ev, head->budget, items + io[pos],
                 fins + fo[pos], po[pos], a, b, c);
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric (mutual-kernel) work list on the device: the host builder
+// build_sym_worklist (fmmcu.cu) restated as kernels, same entries, items and
+// contribution slots.  Item = eval block of leaf t; its entries are t's
+// strong partners B outside the range or B >= t, ordered runs (B == t is
+// the self run) first, then the symmetric ones (B > t inside the range),
+// each in strong-list order.  Partners B < t inside the range are skipped:
+// B's items cover the pair.  One warp per leaf.
+
+struct WlSymHead {
+  unsigned long long ent, items, slots;  // totals (from the scans)
+  uint32_t bad;                          // a leaf does not qualify
+  uint32_t pad;
+};
+
+static __global__ void wls_count_kernel(const uint32_t* __restrict__ ev_off,
+                                        const uint32_t* __restrict__ s_off,
+                                        const uint32_t* __restrict__ s_idx,
+                                        const uint2* __restrict__ seg, uint32_t lb, uint32_t le,
+                                        const WlHead* __restrict__ head,
+                                        uint32_t* __restrict__ n_ent, uint32_t* __restrict__ n_blk,
+                                        unsigned long long* __restrict__ ssym,
+                                        unsigned long long* __restrict__ sord,
+                                        unsigned long long* __restrict__ n_slot,
+                                        WlSymHead* __restrict__ sh) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t np = le - lb;
+  if (i > np) return;
+  if (i == np) {  // the exclusive scans run over np + 1 entries
+    if (lane == 0) n_ent[np] = n_blk[np] = 0, n_slot[np] = 0ull;
+    return;
+  }
+  const uint32_t t = lb + i;
+  uint32_t n = 0;
+  unsigned long long so = 0, ss = 0;
+  for (uint32_t q = s_off[t] + lane; q < s_off[t + 1]; q += 32) {
+    const uint32_t B = s_idx[q];
+    const bool inr = B >= lb && B < le;
+    if (inr && B < t) continue;
+    ++n;
+    if (inr && B > t) ss += seg[q].y;
+    else so += seg[q].y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n += __shfl_xor_sync(kFull, n, o);
+    so += __shfl_xor_sync(kFull, so, o);
+    ss += __shfl_xor_sync(kFull, ss, o);
+  }
+  if (lane == 0) {
+    const uint32_t max_ev = head->max_ev;
+    const uint32_t ntl = ev_off[t + 1] - ev_off[t];
+    const uint32_t nb = ntl ? (ntl + max_ev - 1) / max_ev : 0u;
+    if (n > uint32_t(kWarpMaxEntries) || so + ss >= (1ull << 31)) atomicOr(&sh->bad, 1u);
+    n_ent[i] = n;
+    n_blk[i] = nb;
+    ssym[i] = ss;
+    sord[i] = so;
+    n_slot[i] = (unsigned long long)nb * ss;
+  }
+}
+
+static __global__ void wls_fill_kernel(const uint32_t* __restrict__ pt_off,
+                                       const uint32_t* __restrict__ ev_off,
+                                       const uint32_t* __restrict__ s_off,
+                                       const uint32_t* __restrict__ s_idx,
+                                       const uint2* __restrict__ seg, uint32_t lb, uint32_t le,
+                                       const WlHead* __restrict__ head,
+                                       const uint32_t* __restrict__ ent,
+                                       const uint32_t* __restrict__ blk,
+                                       const unsigned long long* __restrict__ ssym,
+                                       const unsigned long long* __restrict__ sord,
+                                       const unsigned long long* __restrict__ slots,
+                                       uint4* __restrict__ sym_seg, P2PItem* __restrict__ items,
+                                       uint4* __restrict__ sym_info) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t np = le - lb;
+  if (i > np) return;
+  if (i == np) {
+    if (lane == 0) sym_info[np] = make_uint4(ent[np], blk[np], uint32_t(slots[np]), 0u);
+    return;
+  }
+  const uint32_t t = lb + i;
+  const unsigned below = (1u << lane) - 1u;
+  // entries: ordered runs first, then symmetric, each in strong-list order
+  uint32_t o = ent[i];
+  for (int pass = 0; pass < 2; ++pass) {
+    for (uint32_t q0 = s_off[t]; q0 < s_off[t + 1]; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      bool take = false;
+      uint32_t kind = kRunOrdered, B = 0;
+      if (q < s_off[t + 1]) {
+        B = s_idx[q];
+        const bool inr = B >= lb && B < le;
+        const bool sym = inr && B > t;
+        take = !(inr && B < t) && (sym == (pass == 1));
+        kind = sym ? kRunSym : (B == t ? kRunSelf : kRunOrdered);
+      }
+      const unsigned m = __ballot_sync(kFull, take);
+      if (take) {
+        const uint2 r = seg[q];
+        sym_seg[o + __popc(m & below)] = make_uint4(r.x, r.y, kind, 0u);
+      }
+      o += __popc(m);
+    }
+  }
+  if (lane == 0) {
+    const uint32_t ntl = ev_off[t + 1] - ev_off[t];
+    const uint32_t nb = blk[i + 1] - blk[i];
+    const unsigned long long ss = ssym[i], so = sord[i];
+    for (uint32_t b = 0, e0 = 0; b < nb; ++b) {
+      const uint32_t nt = (ntl - e0) / (nb - b) + ((ntl - e0) % (nb - b) ? 1u : 0u);
+      items[blk[i] + b] = P2PItem{t, ev_off[t] + e0, nt, ent[i], ent[i + 1], uint32_t(so + ss),
+                                  uint32_t(slots[i] + (unsigned long long)b * ss), uint32_t(so)};
+      e0 += nt;
+    }
+    sym_info[i] = make_uint4(ent[i], blk[i], uint32_t(slots[i]), uint32_t(ss));
+  }
+  (void)pt_off;
+  (void)head;
 }
 
 }  // namespace fmmcu
