@@ -79,6 +79,7 @@ struct DevicePipeline {
   bool direct_res = false;      // D2H straight into the caller's page-locked out
   double2* res_host = nullptr;  // where the D2H lands (out, or the hres staging)
   Clock::time_point t_host0{};
+  double t_launch_ms = 0.0;     // host time of the launch call (FMMCU_TRACE_SLOW)
   uint64_t h2d = 0;
   std::thread m_stager;         // stages the masses / checks self-evaluation
   bool self_ok = true;          // the helper's self-evaluation verdict
@@ -627,7 +628,15 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
       c->launches += 2;
     }
     CU_TRY(c, cudaMemcpyAsync(hc, ovf, 4, cudaMemcpyDeviceToHost, s));
+    const auto tq0 = Clock::now();
     CU_TRY(c, cudaStreamSynchronize(s));
+    if (c->trace) {
+      std::fprintf(stderr, "[fmmcu] connectivity (speculative): %s, waited %.3f ms, nnz strong/weak:",
+                   hc[0] ? "overflow -> redo" : "fits",
+                   std::chrono::duration<double, std::milli>(Clock::now() - tq0).count());
+      for (int l = 1; l < L; ++l) std::fprintf(stderr, " %u/%u", hc[2 * l], hc[2 * l + 1]);
+      std::fprintf(stderr, "\n");
+    }
     if (hc[0] == 0) {
       for (int l = 1; l < L; ++l) {
         P->conn[l].s_nnz = hc[2 * l];
@@ -658,8 +667,12 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
     CU_TRY(c, cudaStreamSynchronize(s));
     lc.s_nnz = hc[0];
     lc.w_nnz = hc[1];
-    CU_TRY(c, lc.s_idx.ensure(uint64_t(std::max(lc.s_nnz, 1u)) * 4));
-    CU_TRY(c, lc.w_idx.ensure(uint64_t(std::max(lc.w_nnz, 1u)) * 4));
+    // 25% headroom: the next (speculative) build of a similar tree -- time
+    // stepping moves the points a little per step -- then fits without a
+    // redo; exact sizes made every vortex step redo and reallocate
+    // (cudaFree + cudaMalloc of ~0.2 GB, up to ~1 s per step)
+    CU_TRY(c, lc.s_idx.ensure((uint64_t(std::max(lc.s_nnz, 1u)) * 5 / 4 + 1024) * 4));
+    CU_TRY(c, lc.w_idx.ensure((uint64_t(std::max(lc.w_nnz, 1u)) * 5 / 4 + 1024) * 4));
     classify_kernel<true><<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
         pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, nullptr, nullptr,
         lc.s_off.as<uint32_t>(), lc.w_off.as<uint32_t>(), lc.s_idx.as<uint32_t>(),
@@ -1151,6 +1164,7 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   CU_TRY(c, cudaEventRecord(ev[10], s));
   P->pending = true;
   P->t_host0 = t_host0;
+  P->t_launch_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_host0).count();
   P->h2d = h2d;
   if (P->m_stager.joinable()) P->m_stager.join();
   if (maybe_self) {  // verify the speculation
@@ -1216,6 +1230,20 @@ int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {
   cudaEvent_t* ev = P->ev;
   CU_TRY(c, wait_event(ev[10]));
   CU_TRY(c, cudaGetLastError());
+  // FMMCU_TRACE_SLOW=<ms>: the device timeline of evaluations slower than that
+  // (no extra synchronization, unlike FMMCU_TRACE)
+  static const double slow_ms = std::getenv("FMMCU_TRACE_SLOW") ? std::atof(std::getenv("FMMCU_TRACE_SLOW")) : 0.0;
+  if (slow_ms > 0.0) {
+    const double host_ms = std::chrono::duration<double, std::milli>(Clock::now() - P->t_host0).count();
+    if (host_ms > slow_ms) {
+      std::fprintf(stderr, "[fmmcu] slow evaluate: host %.2f ms (launch returned at %.2f), device:", host_ms,
+                   P->t_launch_ms);
+      static const char* names[] = {"start", "positions", "pyramid", "connect+perm", "m2l lists",
+                                    "far start", "upward", "m2l", "p2p start", "p2p end", "end"};
+      for (int e = 1; e <= 10; ++e) std::fprintf(stderr, " %s %.2f", names[e], span_ms(ev[0], ev[e]));
+      std::fprintf(stderr, "\n");
+    }
+  }
   if (*P->h_flag.as<int>())
     return set_err(c, FMMCU_ESINGULAR, "m2l: target center coincides with source center");
   if (st) {
