@@ -646,6 +646,7 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
       return FMMCU_OK;
     }
   }
+  const auto t_redo = Clock::now();
   for (int l = 1; l < L; ++l) {
     const uint32_t nbox = uint32_t(pow4(l));
     LevelConnDev& pc = P->conn[l - 1];
@@ -680,6 +681,9 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
     c->launches += 2;
   }
   CU_TRY(c, cudaGetLastError());
+  if (c->trace || std::getenv("FMMCU_TRACE_SLOW"))
+    std::fprintf(stderr, "[fmmcu] connectivity redo (per-level counts): %.3f ms host\n",
+                 std::chrono::duration<double, std::milli>(Clock::now() - t_redo).count());
   return FMMCU_OK;
 }
 

@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <string>
@@ -26,17 +27,38 @@
 
 namespace fmmcu {
 
+// FMMCU_TRACE_SLOW: report buffer (re)allocations slower than 5 ms
+inline void slow_alloc_note(const char* what, size_t bytes,
+                            std::chrono::steady_clock::time_point t0,
+                            std::chrono::steady_clock::time_point t1 =
+                                std::chrono::steady_clock::time_point::max()) {
+  static const bool on = std::getenv("FMMCU_TRACE_SLOW") != nullptr;
+  if (!on) return;
+  if (t1 == std::chrono::steady_clock::time_point::max()) t1 = std::chrono::steady_clock::now();
+  const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  if (ms > 5.0) std::fprintf(stderr, "[fmmcu] slow %s allocation: %.1f MB in %.1f ms\n", what,
+                             double(bytes) / 1e6, ms);
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  // Grows only.  A buffer that has to grow again grows by at least half its
+  // size: autotuned time stepping changes the level count and theta every few
+  // steps, and each regrowth is a cudaFree (device-wide sync) + cudaMalloc.
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap) return cudaSuccess;
+    const size_t grown = cap ? cap + cap / 2 : 0;
+    const auto t0 = std::chrono::steady_clock::now();
     if (p) cudaFree(p);
+    const auto t1 = std::chrono::steady_clock::now();
     p = nullptr;
     cap = 0;
-    size_t want = std::max<size_t>(bytes, 256);
+    size_t want = std::max<size_t>(std::max(bytes, grown), 256);
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) cap = want;
+    slow_alloc_note("device free", want, t0, t1);
+    slow_alloc_note("device malloc", want, t1);
     if (e == cudaSuccess && std::getenv("FMMCU_DEBUG_POISON")) e = cudaMemset(p, 0xFF, want);
     return e;
   }
@@ -54,14 +76,17 @@ struct DevBuf {
 struct HostBuf {
   void* p = nullptr;
   size_t cap = 0;
-  cudaError_t ensure(size_t bytes) {
+  cudaError_t ensure(size_t bytes) {  // grows only, by at least half (see DevBuf)
     if (bytes <= cap) return cudaSuccess;
+    const size_t grown = cap ? cap + cap / 2 : 0;
+    const auto t0 = std::chrono::steady_clock::now();
     if (p) cudaFreeHost(p);
     p = nullptr;
     cap = 0;
-    size_t want = std::max<size_t>(bytes, 256);
+    size_t want = std::max<size_t>(std::max(bytes, grown), 256);
     cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocPortable | cudaHostAllocMapped);
     if (e == cudaSuccess) cap = want;
+    slow_alloc_note("pinned host", want, t0);
     return e;
   }
   void release() {
