@@ -544,6 +544,7 @@ def run_ours(args):
                     worker_threads=os.cpu_count())
         rd = run_engine(F.FmmConfig(device_pipeline=True, **base), 5)
         rh = run_engine(F.FmmConfig(m2l_on_device=True, **base), 1)
+        rt = run_engine(F.FmmConfig(m2l_on_device=True, device_tree=True, **base), 3)
         fmm = {"value": 1.0 / rd.timings["t_total"], "unit": "evals/s",
                "median_of": 5,
                "timings_s": {k: round(v, 5) for k, v in rd.timings.items()},
@@ -553,8 +554,14 @@ def run_ours(args):
                "hybrid": {"value": 1.0 / rh.timings["t_total"], "unit": "evals/s",
                           "timings_s": {k: round(v, 4) for k, v in rh.timings.items()},
                           "path": "FmmEngine::evaluate, backend=cuda, m2l_on_device (host "
-                                  "tree + L2L/L2P, device P2P + M2L)"}}
-        assert rd.counters == rh.counters
+                                  "tree + L2L/L2P, device P2P + M2L)"},
+               "hybrid_device_tree": {
+                   "value": 1.0 / rt.timings["t_total"], "unit": "evals/s", "median_of": 3,
+                   "timings_s": {k: round(v, 4) for k, v in rt.timings.items()},
+                   "path": "FmmEngine::evaluate, backend=cuda, m2l_on_device, device_tree "
+                           "(bit-exact tree + lists built on the GPU and read back; host "
+                           "P2M/M2M/L2L/L2P, device P2P + M2L)"}}
+        assert rd.counters == rh.counters == rt.counters
         if not args.no_cpu and world == 1:
             fmm["cpu_baseline"] = cpu_fmm_baseline(F._c2(s.z), F._c2(s.m), args)
         del s, e
@@ -602,11 +609,11 @@ def run_ours(args):
                         "includes the host Euler steps"}
         # the same with AT3a (level count steered by the wait sign, autotune.cpp:155):
         # (a) device pipeline, wait = far stream's idle tail before the P2P end;
-        # (b) the paper's split -- CPU far field (host tree, P2M/M2M/M2L/L2L on all
-        #     host cores) against the GPU near field, wait = CPU time blocked in
-        #     finish() -- 20 steps (each evaluate runs the host tree)
+        # (b) the paper's split -- CPU far field (P2M/M2M/M2L/L2L/L2P on all host
+        #     cores) against the GPU near field, wait = CPU time blocked in
+        #     finish(); the bit-exact tree is built on the GPU (device_tree)
         for key, steps, extra in (("config5_vortex_at3a", 100, dict(device_pipeline=True)),
-                                  ("config5_vortex_hybrid_at3a", 20, {})):
+                                  ("config5_vortex_hybrid_at3a", 100, dict(device_tree=True))):
             acfg = F.FmmConfig(theta=0.5, n_levels=9, p_rule="formula", backend="cuda",
                                devices=(local,), worker_threads=os.cpu_count(), **extra)
             t0 = time.perf_counter()
@@ -620,8 +627,10 @@ def run_ours(args):
                                        round(1e3 * float(tra[-1, 4]), 3)],
                 "workload": "init_shear_layer(2e6, aspect 8), gaussian smoother, p formula, AT3a "
                             "from theta 0.5 / L 9, " +
-                            ("FmmEngine device_pipeline" if extra else
-                             "FmmEngine hybrid: CPU far field || GPU near field")}
+                            ("FmmEngine device_pipeline" if "device_pipeline" in extra else
+                             "FmmEngine hybrid: CPU far field (P2M/M2M/M2L/L2L/L2P on all host "
+                             "cores) || GPU near field, tree + lists built on the GPU "
+                             "(device_tree)")}
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:

@@ -16,6 +16,7 @@
 
 #include "fmm/backend.hpp"
 #include "fmm/engine.hpp"
+#include "fmm/geometry.hpp"
 
 struct fmmcu_ctx;
 
@@ -68,6 +69,12 @@ class CudaBackend final : public NearFieldBackend {
   DeviceEval fmm_evaluate(const SourceSet& sources, const EvalSet& evals, int n_levels,
                           double theta, int p, Kernel kernel, const Smoother& smoother,
                           std::vector<cplx>& out);
+
+  // The pyramid and the theta-connectivity built on the first device
+  // (fmmcu_tree_build; bit-exact with build_pyramid / build_connectivity)
+  // and read back into the host structures the CPU far field uses.
+  void device_tree(const SourceSet& sources, const EvalSet& evals, int n_levels, double theta,
+                   Pyramid& pyr, Connectivity& conn);
 
   std::uint64_t kernel_launches() const;
 

@@ -233,6 +233,11 @@ int fmmcu_fmm_evaluate(fmmcu_ctx *ctx, const fmmcu_fmm_job *job, fmmcu_fmm_stats
  * (results are identical either way). */
 int fmmcu_fmm_launch(fmmcu_ctx *ctx, const fmmcu_fmm_job *job);
 int fmmcu_fmm_finish(fmmcu_ctx *ctx, double *out, fmmcu_fmm_stats *stats);
+/* Only the pyramid and the theta-connectivity of the job (bit-exact with
+ * build_pyramid / build_connectivity, geometry.cpp:106-216) on the device,
+ * synchronously; src_m may be NULL.  Read the tree back with
+ * fmmcu_fmm_tree_level / _perm / _lists (the hybrid engine's device_tree). */
+int fmmcu_tree_build(fmmcu_ctx *ctx, const fmmcu_fmm_job *job);
 /* The device-built pyramid / connectivity of the last fmmcu_fmm_evaluate
  * (parity checks).  Box layout as fmmh_tree_boxes: f64[5 n] = centre x, y,
  * half width, half height, radius; u32[4 n] = point and eval ranges. */

@@ -834,12 +834,13 @@ float span_ms(cudaEvent_t a, cudaEvent_t b) {
 extern "C" {
 
 namespace {
-int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
+int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate, bool tree_only = false) {
   if (!c) return FMMCU_EINVAL;
   if (!j) return set_err(c, FMMCU_EINVAL, "null fmm job");
   if (c->pipe && c->pipe->pending) return set_err(c, FMMCU_ESTATE, "fmm launch while in flight");
   if (c->inflight || c->m2l_inflight) return set_err(c, FMMCU_ESTATE, "context busy");
-  if (j->n_src == 0 || !j->src_z || !j->src_m) return set_err(c, FMMCU_EINVAL, "empty source set");
+  if (j->n_src == 0 || !j->src_z || (!j->src_m && !tree_only))
+    return set_err(c, FMMCU_EINVAL, "empty source set");
   if (j->n_levels < 1 || j->n_levels > 14) return set_err(c, FMMCU_EINVAL, "n_levels out of range");
   if (!(j->theta > 0.0 && j->theta < 1.0)) return set_err(c, FMMCU_EINVAL, "theta outside (0,1)");
   if (j->p < 1 || j->p > kM2LMaxP || j->p + 1 > kFarMaxP1)
@@ -885,7 +886,8 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   CU_TRY(c, P->z.ensure(uint64_t(N) * 16));
   CU_TRY(c, P->m.ensure(uint64_t(N) * 16));
   const bool z_locked = host_locked(j->src_z, uint64_t(N) * 16);
-  const bool m_locked = host_locked(j->src_m, uint64_t(N) * 16);
+  // tree only: no masses (treated as resident so nothing is staged)
+  const bool m_locked = tree_only || host_locked(j->src_m, uint64_t(N) * 16);
   if (!z_locked) CU_TRY(c, P->hz.ensure(uint64_t(N) * 16));
   if (!m_locked) CU_TRY(c, P->hm.ensure(uint64_t(N) * 16));
   const bool maybe_self = speculate && j->eval_sid && M == N && j->eval_y;
@@ -963,7 +965,7 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   // masses: behind the positions on the PCIe link, in parallel with the pyramid
   cudaStream_t hs = c->h2d_stream;
   CU_TRY(c, cudaStreamWaitEvent(hs, ev[1], 0));
-  if (m_locked) {
+  if (m_locked && !tree_only) {
     CU_TRY(c, cudaMemcpyAsync(P->m.p, j->src_m, uint64_t(N) * 16, cudaMemcpyHostToDevice, hs));
     CU_TRY(c, cudaEventRecord(ev[11], hs));
   }
@@ -1021,6 +1023,11 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate) {
   if (int rc = join_masses()) return rc;
   const bool self = P->self_eval;
   P->tree_valid = true;
+  if (tree_only) {  // fmmcu_tree_build: the tree is all the caller wants
+    CU_TRY(c, cudaStreamSynchronize(s));
+    CU_TRY(c, cudaGetLastError());
+    return FMMCU_OK;
+  }
   const int L = P->L;
   const uint32_t nleaf = uint32_t(pow4(L - 1));
   // The P2P work list: by default built on the device from the finest CSR
@@ -1200,6 +1207,27 @@ int fmmcu_fmm_launch(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
   const int rc2 = fmm_launch_impl(c, &j2, false);
   P->t_host0 = t0;
   return rc2;
+}
+
+int fmmcu_tree_build(fmmcu_ctx* c, const fmmcu_fmm_job* j) {
+  if (!c || !j) return FMMCU_EINVAL;
+  // self-evaluation (evals = the sources, ids = their indices) lets the
+  // build alias the eval lists to the source lists; checked here up front,
+  // there is no later verification in this mode
+  bool self = j->eval_sid && j->n_eval == j->n_src && j->eval_y && j->src_z;
+  if (self) {
+    const int64_t n = j->n_src;
+    const bool same_ptr = j->eval_y == j->src_z;
+#pragma omp parallel for schedule(static) reduction(&& : self)
+    for (int64_t i = 0; i < n; ++i)
+      self = self && j->eval_sid[i] == i &&
+             (same_ptr || (j->eval_y[2 * i] == j->src_z[2 * i] &&
+                           j->eval_y[2 * i + 1] == j->src_z[2 * i + 1]));
+  }
+  fmmcu_fmm_job jj = *j;
+  jj.inputs_consumed = nullptr;
+  if (jj.p < 1) jj.p = 1;  // the order is irrelevant to the tree
+  return fmm_launch_impl(c, &jj, self, true);
 }
 
 int fmmcu_fmm_finish(fmmcu_ctx* c, double* out, fmmcu_fmm_stats* st) {

@@ -18,39 +18,13 @@
 
 #include "fmm/cuda_backend.hpp"
 #include "fmm_cuda.h"
+#include "host_util.hpp"
 
 namespace fmm {
 
-namespace {
+using detail::resize_huge;
 
-// Size `v` to n value-initialised elements with transparent huge pages on
-// its storage (madvise before the first touch): the zero fill of a 160 MB
-// result then takes 80 page faults instead of 40k (61 ms -> 21 ms measured
-// on the B200 hosts).  Same vector, same contents; only the page size differs.
-void resize_huge(std::vector<cplx>& v, std::size_t n) {
-  v.clear();
-  v.reserve(n);
-  const std::size_t bytes = n * sizeof(cplx);
-  constexpr std::uintptr_t kHuge = std::uintptr_t(2) << 20;
-  if (bytes >= 2 * kHuge) {
-    const auto b = reinterpret_cast<std::uintptr_t>(v.data());
-    const std::uintptr_t a0 = (b + kHuge - 1) & ~(kHuge - 1);
-    const std::uintptr_t a1 = (b + bytes) & ~(kHuge - 1);
-    if (a1 > a0) {
-      madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
-#ifdef MADV_POPULATE_WRITE
-      // fault the pages in from all cores (the value-initialising memset
-      // below then runs over populated memory)
-      const std::int64_t pages = std::int64_t((a1 - a0) / kHuge);
-#pragma omp parallel for schedule(static)
-      for (std::int64_t p = 0; p < pages; ++p)
-        madvise(reinterpret_cast<void*>(a0 + std::uintptr_t(p) * kHuge), kHuge,
-                MADV_POPULATE_WRITE);
-#endif
-    }
-  }
-  v.resize(n);
-}
+namespace {
 
 [[noreturn]] void raise(fmmcu_ctx* c, int rc, const char* what) {
   const std::string msg = std::string(what) + ": " + (c ? fmmcu_last_error(c) : "no context");
@@ -305,6 +279,85 @@ void CudaBackend::m2l_launch(int p, Kernel kernel, const std::vector<cplx>& cent
   j.out = reinterpret_cast<double*>(out.data());
   const int rc = fmmcu_m2l_launch(ctx_[0], &j);
   if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l launch");
+}
+
+void CudaBackend::device_tree(const SourceSet& sources, const EvalSet& evals, int n_levels,
+                              double theta, Pyramid& pyr, Connectivity& conn) {
+  if (inflight_) throw InvalidState("cuda backend: tree build while a near field is in flight");
+  if (sources.size() == 0) throw InvalidInput("build_pyramid: empty source set");
+  if (sources.size() > 0xFFFFFFFFull || evals.size() > 0xFFFFFFFFull)
+    throw InvalidInput("device tree: more than 2^32 points");
+  fmmcu_ctx* c = ctx_[0];
+  fmmcu_fmm_job j{};
+  j.n_src = std::uint32_t(sources.size());
+  j.n_eval = std::uint32_t(evals.size());
+  j.src_z = reinterpret_cast<const double*>(sources.z.data());
+  j.src_m = nullptr;
+  j.eval_y = evals.size() ? reinterpret_cast<const double*>(evals.y.data()) : nullptr;
+  j.eval_sid = evals.source_id.empty() ? nullptr : evals.source_id.data();
+  j.n_levels = n_levels;
+  j.theta = theta;
+  j.p = 1;
+  using TClock = std::chrono::steady_clock;
+  const auto t0 = TClock::now();
+  int rc = fmmcu_tree_build(c, &j);
+  if (rc != FMMCU_OK) raise(c, rc, "cuda tree build");
+  const auto t1 = TClock::now();
+  const int L = n_levels;
+  pyr = Pyramid{};
+  pyr.n_levels = L;
+  pyr.levels.resize(L);
+  conn = Connectivity{};
+  conn.levels.resize(L);
+  std::vector<double> f64;
+  std::vector<std::uint32_t> u32, off, idx;
+  for (int l = 0; l < L; ++l) {
+    std::uint32_t nb = 0;
+    if ((rc = fmmcu_fmm_tree_level(c, l, &nb, nullptr, nullptr)) != FMMCU_OK) raise(c, rc, "tree");
+    f64.resize(std::size_t(nb) * 5);
+    u32.resize(std::size_t(nb) * 4);
+    if ((rc = fmmcu_fmm_tree_level(c, l, &nb, f64.data(), u32.data())) != FMMCU_OK)
+      raise(c, rc, "tree");
+    std::vector<MBox>& boxes = pyr.levels[l];
+    boxes.resize(nb);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < std::int64_t(nb); ++i) {
+      MBox& b = boxes[i];
+      b.center = cplx(f64[5 * i], f64[5 * i + 1]);
+      b.half_width = f64[5 * i + 2];
+      b.half_height = f64[5 * i + 3];
+      b.radius = f64[5 * i + 4];
+      b.level = l;
+      b.index_in_level = std::uint32_t(i);
+      b.point_begin = u32[4 * i];
+      b.point_end = u32[4 * i + 1];
+      b.eval_begin = u32[4 * i + 2];
+      b.eval_end = u32[4 * i + 3];
+    }
+    for (int weak = 0; weak < 2; ++weak) {
+      std::uint64_t nnz = 0;
+      if ((rc = fmmcu_fmm_tree_lists(c, l, weak, &nnz, nullptr, nullptr)) != FMMCU_OK)
+        raise(c, rc, "tree");
+      off.resize(std::size_t(nb) + 1);
+      idx.resize(std::max<std::uint64_t>(nnz, 1));
+      if ((rc = fmmcu_fmm_tree_lists(c, l, weak, &nnz, off.data(), idx.data())) != FMMCU_OK)
+        raise(c, rc, "tree");
+      auto& rows = weak ? conn.levels[l].weak : conn.levels[l].strong;
+      rows.resize(nb);
+#pragma omp parallel for schedule(static)
+      for (std::int64_t i = 0; i < std::int64_t(nb); ++i)
+        rows[i].assign(idx.begin() + off[i], idx.begin() + off[i + 1]);
+    }
+  }
+  pyr.perm.resize(sources.size());
+  pyr.eval_perm.resize(evals.size());
+  if ((rc = fmmcu_fmm_tree_perm(c, pyr.perm.data(), evals.size() ? pyr.eval_perm.data() : nullptr)) !=
+      FMMCU_OK)
+    raise(c, rc, "tree");
+  if (std::getenv("FMM_TRACE"))
+    std::fprintf(stderr, "[fmm] device tree: build %.2f ms, read back + host lists %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(TClock::now() - t1).count());
 }
 
 CudaBackend::M2LBuffers CudaBackend::m2l_buffers(std::uint32_t n_boxes, int p,

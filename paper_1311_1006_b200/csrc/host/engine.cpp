@@ -21,6 +21,7 @@
 
 #include "fmm/cuda_backend.hpp"
 #include "fmm/engine.hpp"
+#include "host_util.hpp"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -280,16 +281,18 @@ namespace {
 void permute_inputs(const Pyramid& pyr, const SourceSet& s, const EvalSet& e, int threads,
                     std::vector<cplx>& zp, std::vector<cplx>& mp, std::vector<cplx>& yp,
                     std::vector<std::int64_t>& sidp) {
-  zp.resize(s.size());
-  mp.resize(s.size());
+  // huge pages, populated from all cores: the value-initialising resize of
+  // four 80-160 MB vectors was ~200 ms of page faults at 10M
+  detail::resize_huge(zp, s.size());
+  detail::resize_huge(mp, s.size());
 #pragma omp parallel for schedule(static) num_threads(threads)
   for (std::int64_t i = 0; i < std::int64_t(s.size()); ++i) {
     zp[i] = s.z[pyr.perm[i]];
     mp[i] = s.m[pyr.perm[i]];
   }
-  yp.resize(e.size());
+  detail::resize_huge(yp, e.size());
   sidp.clear();
-  if (!e.source_id.empty()) sidp.resize(e.size());
+  if (!e.source_id.empty()) detail::resize_huge(sidp, e.size());
 #pragma omp parallel for schedule(static) num_threads(threads)
   for (std::int64_t i = 0; i < std::int64_t(e.size()); ++i) {
     yp[i] = e.y[pyr.eval_perm[i]];
@@ -393,12 +396,31 @@ void FmmEngine::evaluate_into(const SourceSet& sources, const EvalSet& evals, Ev
   }
 
   // ---- partition ------------------------------------------------------------
-  const Pyramid pyr = build_pyramid(sources, evals, cfg_.n_levels, threads);
-  const Connectivity conn = build_connectivity(pyr, cfg_.theta);
+  // (device_tree: the same pyramid and lists built on the GPU and read back)
+  Pyramid pyr;
+  Connectivity conn;
+  if (cfg_.device_tree && cfg_.backend == BackendKind::cuda) {
+    auto* cb = dynamic_cast<CudaBackend*>(backend_.get());
+    try {
+      cb->device_tree(sources, evals, cfg_.n_levels, cfg_.theta, pyr, conn);
+    } catch (const InvalidInput&) {
+      throw;
+    } catch (const std::exception& e) {
+      throw BackendError("device tree", e.what());
+    }
+  } else {
+    pyr = build_pyramid(sources, evals, cfg_.n_levels, threads);
+    conn = build_connectivity(pyr, cfg_.theta);
+  }
   std::vector<cplx> zp, mp, yp;
   std::vector<std::int64_t> sidp;
+  const double t_tree = since(t_start);
   permute_inputs(pyr, sources, evals, threads, zp, mp, yp, sidp);
   T.t_partition = since(t_start);
+  static const bool trace_part = std::getenv("FMM_TRACE") != nullptr;
+  if (trace_part)
+    std::fprintf(stderr, "[fmm] partition: tree + lists %.2f ms, permute %.2f ms\n", 1e3 * t_tree,
+                 1e3 * (T.t_partition - t_tree));
 
   // ---- upward -------------------------------------------------------------
   const auto t_p2m = Clock::now();

@@ -99,6 +99,7 @@ FmmConfig config_of(const double* f, const int* i, const int* devices, int n_dev
   c.cuda.exact = i[8] != 0;
   c.m2l_on_device = i[9] != 0;
   c.device_pipeline = i[10] != 0;
+  c.device_tree = i[11] != 0;
   for (int d = 0; d < n_devices; ++d) c.cuda.devices.push_back(devices[d]);
   return c;
 }

@@ -273,6 +273,7 @@ class FmmConfig:
     exact: bool = False
     m2l_on_device: bool = False
     device_pipeline: bool = False
+    device_tree: bool = False
 
     def pack(self):
         f = np.array([self.theta, self.tol, self.p_calibration, self.delta,
@@ -280,7 +281,7 @@ class FmmConfig:
         i = np.array([self.n_levels, KERNEL[self.kernel], PRULE[self.p_rule], self.p_override,
                       BACKEND[self.backend], self.worker_threads, self.task_split_level,
                       SMOOTHER[self.smoother], int(self.exact), int(self.m2l_on_device),
-                      int(self.device_pipeline)],
+                      int(self.device_pipeline), int(self.device_tree)],
                      dtype=np.int32)
         d = np.asarray(self.devices, dtype=np.int32)
         return f, i, d

@@ -12,11 +12,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=10_000_000)
 ap.add_argument("--levels", type=int, default=10)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--device-tree", action="store_true")
+ap.add_argument("--host-m2l", action="store_true")
 a = ap.parse_args()
 s = F.make_distribution("uniform", a.n, 4)
 e = F.EvalSet.self_of(s)
-eng = F.FmmEngine(F.FmmConfig(n_levels=a.levels, backend="cuda", m2l_on_device=True,
-                              worker_threads=os.cpu_count()))
+eng = F.FmmEngine(F.FmmConfig(n_levels=a.levels, backend="cuda", m2l_on_device=not a.host_m2l,
+                              device_tree=a.device_tree, worker_threads=os.cpu_count()))
 for r in range(a.reps):
     t0 = time.perf_counter()
     res = eng.evaluate(s, e)

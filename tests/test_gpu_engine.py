@@ -231,3 +231,26 @@ def test_engine_cuda_multi_context_shards_vs_pool(dist, n, L):
         got = F.FmmEngine(F.FmmConfig(backend="cuda", devices=devs, **base)).evaluate(s, e)
         assert got.counters == ref.counters, devs
         assert normwise(F._c2(got.potentials), F._c2(ref.potentials)) <= 1e-12, devs
+
+
+@pytest.mark.parametrize("m2l_dev", [False, True])
+def test_hybrid_device_tree_equals_host_tree(golden_trees, m2l_dev):
+    """FmmConfig.device_tree: the hybrid engine builds the pyramid and lists
+    on the GPU (fmmcu_tree_build) and reads them back for the CPU far field.
+    The device tree is bit-exact, and everything downstream is the same
+    code, so the potentials are bitwise those of the host-tree hybrid, with
+    equal counters -- golden trees (ties, separate evals, theta 0.65), a
+    lattice with tied splits and a clustered set."""
+    cases = [(_sets(d), int(d["n_levels"]), float(d["theta"])) for d in golden_trees.values()]
+    g = np.arange(120) / 120.0
+    lat = F.SourceSet((g[:, None] + 1j * g[None, :] * 0.25).ravel(), np.full(14400, 0.5j))
+    cases.append(((lat, F.EvalSet.self_of(lat)), 6, 0.5))
+    s = F.make_distribution("gauss8", 60_000, 7)
+    cases.append(((s, F.EvalSet.self_of(s)), 6, 0.5))
+    for (s, e), L, theta in cases:
+        base = dict(n_levels=L, theta=theta, backend="cuda", m2l_on_device=m2l_dev,
+                    worker_threads=8)
+        a = F.FmmEngine(F.FmmConfig(**base)).evaluate(s, e)
+        b = F.FmmEngine(F.FmmConfig(device_tree=True, **base)).evaluate(s, e)
+        assert a.counters == b.counters
+        assert np.array_equal(a.potentials.view(np.uint64), b.potentials.view(np.uint64))
