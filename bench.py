@@ -613,7 +613,7 @@ def run_ours(args):
         #     cores) against the GPU near field, wait = CPU time blocked in
         #     finish(); the bit-exact tree is built on the GPU (device_tree)
         for key, steps, extra in (("config5_vortex_at3a", 100, dict(device_pipeline=True)),
-                                  ("config5_vortex_hybrid_at3a", 100, dict(device_tree=True))):
+                                  ("config5_vortex_hybrid_at3a", 30, dict(device_tree=True))):
             acfg = F.FmmConfig(theta=0.5, n_levels=9, p_rule="formula", backend="cuda",
                                devices=(local,), worker_threads=os.cpu_count(), **extra)
             t0 = time.perf_counter()
