@@ -127,24 +127,30 @@ inline uint64_t pow4(int l) { return uint64_t(1) << (2 * l); }
 
 
 // M2L lists of one level: targets = boxes with evals (l >= 1), partners =
-// weak entries whose box has sources (engine.cpp:98, :108-113).
+// weak entries whose box has sources (engine.cpp:98, :108-113).  One warp
+// per box: clustered weak lists run to thousands of entries, which a thread
+// per box walked serially (1.3 ms of the 1M gauss8 pipeline).
 __global__ void m2l_count_kernel(const uint32_t* __restrict__ w_off,
                                  const uint32_t* __restrict__ w_idx,
                                  const uint32_t* __restrict__ soff, const uint32_t* __restrict__ eoff,
                                  uint32_t nbox, uint32_t base, uint32_t* __restrict__ tcnt,
                                  uint32_t* __restrict__ wcnt) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nbox) return;
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (i >= nbox) return;  // warp-uniform
   uint32_t t = 0, w = 0;
   if (eoff[i + 1] > eoff[i]) {
     t = 1;
-    for (uint32_t q = w_off[i]; q < w_off[i + 1]; ++q) {
+    for (uint32_t q = w_off[i] + lane; q < w_off[i + 1]; q += 32) {
       const uint32_t b = w_idx[q];
       w += soff[b + 1] > soff[b] ? 1u : 0u;
     }
+    w = __reduce_add_sync(0xffffffffu, w);
   }
-  tcnt[base + i] = t;
-  wcnt[base + i] = w;
+  if (lane == 0) {
+    tcnt[base + i] = t;
+    wcnt[base + i] = w;
+  }
 }
 
 __global__ void m2l_fill_kernel(const uint32_t* __restrict__ w_off, const uint32_t* __restrict__ w_idx,
@@ -153,21 +159,33 @@ __global__ void m2l_fill_kernel(const uint32_t* __restrict__ w_off, const uint32
                                 const uint32_t* __restrict__ wstart, uint32_t* __restrict__ tbox,
                                 uint32_t* __restrict__ woff_out, uint32_t* __restrict__ widx,
                                 int32_t* __restrict__ m2l_row) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nbox) return;
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (i >= nbox) return;  // warp-uniform
   const uint32_t g = base + i;
   if (eoff[i + 1] == eoff[i]) {
-    m2l_row[g] = -1;
+    if (lane == 0) m2l_row[g] = -1;
     return;
   }
   const uint32_t row = trow[g];
-  m2l_row[g] = int32_t(row);
-  tbox[row] = g;
   uint32_t o = wstart[g];
-  woff_out[row] = o;
-  for (uint32_t q = w_off[i]; q < w_off[i + 1]; ++q) {
-    const uint32_t b = w_idx[q];
-    if (soff[b + 1] > soff[b]) widx[o++] = base + b;
+  if (lane == 0) {
+    m2l_row[g] = int32_t(row);
+    tbox[row] = g;
+    woff_out[row] = o;
+  }
+  const unsigned below = (1u << lane) - 1u;
+  for (uint32_t q0 = w_off[i]; q0 < w_off[i + 1]; q0 += 32) {
+    const uint32_t q = q0 + lane;
+    bool take = false;
+    uint32_t b = 0;
+    if (q < w_off[i + 1]) {
+      b = w_idx[q];
+      take = soff[b + 1] > soff[b];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (take) widx[o + __popc(m & below)] = base + b;
+    o += __popc(m);
   }
 }
 
@@ -739,7 +757,7 @@ int m2l_lists(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s) {
   CU_TRY(c, cudaMemsetAsync(P->m2l_row.p, 0xFF, nb * 4, s));
   for (int l = 1; l < L; ++l) {
     const uint32_t nbox = uint32_t(pow4(l));
-    m2l_count_kernel<<<blocks(nbox), TB, 0, s>>>(
+    m2l_count_kernel<<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
         P->conn[l].w_off.as<uint32_t>(), P->conn[l].w_idx.as<uint32_t>(),
         P->soff.as<uint32_t>() + P->off_base[l], P->eoff.as<uint32_t>() + P->off_base[l], nbox,
         uint32_t(P->box_base[l]), tc, wc);
@@ -757,7 +775,7 @@ int m2l_lists(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s) {
   CU_TRY(c, P->widx.ensure(uint64_t(std::max(P->m2l_nnz, 1u)) * 4));
   for (int l = 1; l < L; ++l) {
     const uint32_t nbox = uint32_t(pow4(l));
-    m2l_fill_kernel<<<blocks(nbox), TB, 0, s>>>(
+    m2l_fill_kernel<<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
         P->conn[l].w_off.as<uint32_t>(), P->conn[l].w_idx.as<uint32_t>(),
         P->soff.as<uint32_t>() + P->off_base[l], P->eoff.as<uint32_t>() + P->off_base[l], nbox,
         uint32_t(P->box_base[l]), P->trow.as<uint32_t>(), P->wstart.as<uint32_t>(),
@@ -1060,6 +1078,13 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate, bool t
                               cudaMemcpyDeviceToHost, ds));
     CU_TRY(c, cudaEventRecord(ev[13], ds));
   }
+  // The M2L lists first: their two count reads then wait only for their own
+  // small kernels (connectivity already ended with a host read), not for the
+  // permutation behind them, and the work-list build after the permutation is
+  // enqueued overlaps it.
+  if (int rc = far_setup(c, P, s)) return rc;
+  if (int rc = m2l_lists(c, P, s)) return rc;
+  CU_TRY(c, cudaEventRecord(ev[4], s));
   CU_TRY(c, cudaStreamWaitEvent(s, ev[11], 0));  // pack_sources reads the masses
 
   // ---- permuted inputs into the P2P staging of the context ----------------
@@ -1079,11 +1104,9 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate, bool t
   c->launches += 3;
   CU_TRY(c, cudaEventRecord(ev[3], s));  // partition done
 
-  // ---- far field on its own stream (overlaps the host work list + P2P) ----
-  if (int rc = far_setup(c, P, s)) return rc;
-  if (int rc = m2l_lists(c, P, s)) return rc;
-  CU_TRY(c, cudaEventRecord(ev[4], s));
-  CU_TRY(c, cudaStreamWaitEvent(P->far, ev[4], 0));
+  // ---- far field on its own stream (overlaps the work list + P2P); P2M
+  // reads the packed sources ----
+  CU_TRY(c, cudaStreamWaitEvent(P->far, ev[3], 0));
   CU_TRY(c, cudaEventRecord(ev[5], P->far));
   if (int rc = far_field(c, P, P->far, ev[6], ev[7])) return rc;
 
@@ -1104,7 +1127,10 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate, bool t
     CU_TRY(c, cudaStreamWaitEvent(ws, ev[12], 0));
     if (int rc = stage_csr_dev(c, P->soff.as<uint32_t>() + P->off_base[L - 1],
                                P->eoff.as<uint32_t>() + P->off_base[L - 1], fc.s_off.as<uint32_t>(),
-                               fc.s_idx.as<uint32_t>(), nleaf, fc.s_nnz, M, ws, ev[13], pipe_sym))
+                               fc.s_idx.as<uint32_t>(), nleaf, fc.s_nnz, M, ws, ev[13],
+                               // more than 32 entries per leaf on average: some leaf exceeds
+                               // the mutual kernel's 32, skip the attempt
+                               pipe_sym && uint64_t(fc.s_nnz) <= 32ull * nleaf))
       return rc;
     CU_TRY(c, cudaStreamWaitEvent(s, ev[13], 0));
     if (M) {  // eval records {x, y, self slot, strong entry of the self slot}

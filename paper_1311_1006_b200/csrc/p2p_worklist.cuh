@@ -167,9 +167,22 @@ __device__ __forceinline__ void wl_leaf_items(uint32_t t, const uint32_t* __rest
     const unsigned long long spc = budget / nt > 0 ? budget / nt : 1ull;
     const uint32_t base = pbase + n_pev;
     uint32_t n_chunks = 0;
+    // The entries' source counts sit in a 96-entry window in registers
+    // (lane-distributed thirds [wq, wq+32), [wq+32, wq+64), [wq+64, wq+96)),
+    // refilled a third ahead, so a step of this sequential greedy waits on
+    // shuffles, not on a global load (clustered leaves run ~750 steps)
+    uint32_t wq = sb0;
+    auto ld = [&](uint32_t from) -> uint32_t {
+      const uint32_t qq = from + lane;
+      return qq < sb1 ? seg[qq].y : 0u;
+    };
+    uint32_t w0 = ld(wq), w1 = ld(wq + 32), w2 = ld(wq + 64);
     for (uint32_t q = sb0; q < sb1;) {
       const uint32_t qq = q + lane;
-      const unsigned long long n = qq < sb1 ? seg[qq].y : 0ull;
+      const uint32_t d = q - wq;  // < 32
+      const uint32_t from = (d + lane) & 31u;
+      const uint32_t a0 = __shfl_sync(kFull, w0, from), a1 = __shfl_sync(kFull, w1, from);
+      const unsigned long long n = qq < sb1 ? (d + lane < 32 ? a0 : a1) : 0ull;
       unsigned long long incl = n;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -187,6 +200,12 @@ __device__ __forceinline__ void wl_leaf_items(uint32_t t, const uint32_t* __rest
       n_pev += nt;
       ++n_chunks;
       q += len;
+      if (q - wq >= 32) {  // slide the window by a third
+        w0 = w1;
+        w1 = w2;
+        wq += 32;
+        w2 = ld(wq + 64);
+      }
     }
     if (fin && lane == 0) fin[n_fins] = P2PFinal{evb, nt, base, n_chunks};
     ++n_fins;
