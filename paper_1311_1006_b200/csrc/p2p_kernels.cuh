@@ -214,15 +214,23 @@ static __global__ void p2p_segments_kernel(const uint32_t* __restrict__ s_idx,
 // Eval record as staged on the device: {x, y, self slot (bits), q_self (bits)}
 // where q_self is the global strong-entry index (position in strong_idx) of
 // the eval's own leaf's entry whose source run holds the self slot, or
-// kNoSelf -- this makes the per-tile self lookup O(1).
+// kNoSelf -- this makes the per-tile self lookup O(1).  The runs of a strong
+// list are disjoint and ascending in slot order (the list is sorted by leaf
+// and pt_off is monotone), so the entry holding the slot is the last one
+// starting at or before it: a binary search (clustered leaves have lists of
+// thousands of entries; the former linear scan cost 0.67 ms at 1M gauss8).
 __device__ __forceinline__ uint32_t find_self_entry(const P2PArgs& a, uint32_t leaf,
                                                     uint32_t self) {
   if (self == kNoSelf) return kNoSelf;
-  for (uint32_t q = a.s_off[leaf]; q < a.s_off[leaf + 1]; ++q) {
-    const uint2 sg = a.seg[q];
-    if (self - sg.x < sg.y) return q;
+  uint32_t lo = a.s_off[leaf], hi = a.s_off[leaf + 1];  // answer in [lo, hi)
+  if (lo == hi || a.seg[lo].x > self) return kNoSelf;
+  while (hi - lo > 1) {  // invariant: seg[lo].x <= self, entries >= hi start after self
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a.seg[mid].x <= self) lo = mid;
+    else hi = mid;
   }
-  return kNoSelf;
+  const uint2 sg = a.seg[lo];
+  return self - sg.x < sg.y ? lo : kNoSelf;
 }
 
 // One warp per leaf of [leaf_begin, leaf_end), lanes over its evals.
