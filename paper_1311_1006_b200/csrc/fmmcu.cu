@@ -1524,6 +1524,7 @@ int fmmcu_create(fmmcu_ctx** out, int device) {
     return FMMCU_ECUDA;
   };
   if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(e);
+  c->d_out.plain = true;  // exported over CUDA IPC (fmmcu_p2p_out_ipc_handle)
   if ((e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(e);
   if ((e = cudaStreamCreateWithFlags(&c->m2l_stream, cudaStreamNonBlocking)) != cudaSuccess)

@@ -40,9 +40,26 @@ inline void slow_alloc_note(const char* what, size_t bytes,
                              double(bytes) / 1e6, ms);
 }
 
+// The current device's default memory pool keeps what is freed into it
+// (called before every DevBuf allocation; cheap after the first per device).
+inline void keep_pool_memory() {
+  static thread_local int done_mask = 0;  // devices 0..30
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev > 30) return;
+  if (done_mask & (1 << dev)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~uint64_t(0);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done_mask |= 1 << dev;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  bool plain = false;  // cudaMalloc (a buffer exported over CUDA IPC), not the pool
   // Grows only.  A buffer that has to grow again grows by at least half its
   // size: autotuned time stepping changes the level count and theta every few
   // steps, and each regrowth is a cudaFree (device-wide sync) + cudaMalloc.
@@ -50,12 +67,31 @@ struct DevBuf {
     if (bytes <= cap) return cudaSuccess;
     const size_t grown = cap ? cap + cap / 2 : 0;
     const auto t0 = std::chrono::steady_clock::now();
-    if (p) cudaFree(p);
+    // Stream-ordered allocations from the device's default pool, which keeps
+    // freed memory (release threshold raised once per device): regrowing a
+    // buffer reuses pooled memory instead of mapping new pages, which took
+    // up to hundreds of ms per cudaMalloc in autotuned time stepping.  The
+    // old buffer may still be read by queued work on any stream, so the
+    // device is synchronized before it goes back to the pool (as cudaFree
+    // would); the new one is complete once the legacy stream is.
+    if (p && plain) {
+      cudaFree(p);
+    } else if (p) {
+      cudaDeviceSynchronize();
+      cudaFreeAsync(p, 0);
+    }
     const auto t1 = std::chrono::steady_clock::now();
     p = nullptr;
     cap = 0;
     size_t want = std::max<size_t>(std::max(bytes, grown), 256);
-    cudaError_t e = cudaMalloc(&p, want);
+    cudaError_t e;
+    if (plain) {
+      e = cudaMalloc(&p, want);
+    } else {
+      keep_pool_memory();
+      e = cudaMallocAsync(&p, want, 0);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    }
     if (e == cudaSuccess) cap = want;
     slow_alloc_note("device free", want, t0, t1);
     slow_alloc_note("device malloc", want, t1);
@@ -63,7 +99,13 @@ struct DevBuf {
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && plain) {
+      cudaFree(p);
+    } else if (p) {
+      cudaDeviceSynchronize();
+      cudaFreeAsync(p, 0);
+      cudaStreamSynchronize(0);
+    }
     p = nullptr;
     cap = 0;
   }
