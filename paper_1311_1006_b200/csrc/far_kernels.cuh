@@ -231,29 +231,32 @@ __global__ void __launch_bounds__(kFarWarps * 32) local_kernel(const FarArgs a, 
 
 // Assembly (engine.cpp:316-339): potential of permuted eval e in finest box
 // t = near[e] + eval_local(local_t, y_e) (Horner, expansion.cpp:298-303),
-// written to its original slot eval_perm[e].
+// written to its original slot eval_perm[e].  One warp per finest box, lanes
+// over its evals (the box's coefficients are read by the whole warp at once;
+// a thread per eval binary-searched its box over all leaves, 18 dependent
+// loads at 10M / L10).
 __global__ void assemble_kernel(const FarArgs a, const double2* __restrict__ near,
                                 const double2* __restrict__ evy, const uint32_t* __restrict__ eperm,
                                 uint32_t n_eval, int has_local, double2* __restrict__ out) {
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n_eval) return;
-  double2 v = near[e];
-  if (has_local) {
-    uint32_t lo = 0, hi = a.nbox;  // finest box containing eval slot e
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (a.eoff_l[mid] <= e) lo = mid;
-      else hi = mid;
+  (void)n_eval;
+  const uint32_t box = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (box >= a.nbox) return;
+  const uint32_t e0 = a.eoff_l[box], e1 = a.eoff_l[box + 1];
+  const uint32_t g = a.base + box;
+  const int P1 = a.p + 1;
+  const double2 c = a.center[g];
+  const double2* cf = a.loc + size_t(g) * P1;
+  for (uint32_t e = e0 + lane; e < e1; e += 32) {
+    double2 v = near[e];
+    if (has_local) {
+      const double2 w = cx_sub(evy[e], c);
+      double2 acc = make_double2(0.0, 0.0);
+      for (int k = P1 - 1; k >= 0; --k) acc = cx_add(cx_mul(acc, w), cf[k]);
+      v = cx_add(v, acc);
     }
-    const uint32_t g = a.base + lo;
-    const int P1 = a.p + 1;
-    const double2 w = cx_sub(evy[e], a.center[g]);
-    const double2* cf = a.loc + size_t(g) * P1;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int k = P1 - 1; k >= 0; --k) acc = cx_add(cx_mul(acc, w), cf[k]);
-    v = cx_add(v, acc);
+    out[eperm[e]] = v;
   }
-  out[eperm[e]] = v;
 }
 
 // ---- permutation / packing ------------------------------------------------

@@ -1168,7 +1168,7 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate, bool t
   CU_TRY(c, P->res.ensure(uint64_t(std::max(M, 1u)) * 16));
   if (M) {
     FarArgs a = far_args(P, L - 1);
-    assemble_kernel<<<blocks(M), TB, 0, s>>>(a, c->out_ptr(), c->d_evy.as<double2>(),
+    assemble_kernel<<<blocks(uint64_t(a.nbox) * 32), TB, 0, s>>>(a, c->out_ptr(), c->d_evy.as<double2>(),
                                              P->eperm.as<uint32_t>(), M, L >= 2 ? 1 : 0,
                                              P->res.as<double2>());
     c->launches += 1;
