@@ -15,8 +15,14 @@
 // records so selection and partitioning stream through memory instead of
 // gathering coordinates through the permutation, the two y-splits of a
 // parent run in parallel, and connectivity is built per child box in
-// parallel (each list emerges sorted; no post-sort).
+// parallel (each list emerges sorted; no post-sort).  The few huge boxes
+// near the root are split one at a time with every step parallel: a
+// sample-bracketed parallel selection, a parallel stable eval split and
+// parallel extents (10M points: the two top levels 1.2 s -> see DESIGN).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 
@@ -108,6 +114,181 @@ void fill_box(MBox& box, const std::vector<Rec>& src, const std::vector<Rec>& ev
   box.radius = std::hypot(box.half_width, box.half_height);
 }
 
+// ---- parallel versions for the few huge boxes near the root --------------
+// (a box of n >= kParMin points; below that, one thread per box).  They give
+// the same SETS, split values, eval order and extents as the serial helpers,
+// so the pyramid is unchanged (the low half is a set; evals split stably).
+constexpr std::uint32_t kParMin = 1u << 18;
+
+std::uint32_t par_min_size() {
+  static const std::uint32_t v = [] {
+    const char* s = std::getenv("FMM_PAR_SELECT_MIN");  // tests force the parallel path
+    return s ? std::uint32_t(std::strtoul(s, nullptr, 10)) : kParMin;
+  }();
+  return v;
+}
+
+// Low half of recs[b,e) by a sample-bracketed parallel partition: two
+// pivots from a sorted sample bracket the median rank; one parallel pass
+// scatters [< lo | between | > hi] through tmp, and nth_element finishes
+// inside the (small) middle bucket.  Falls back to the serial selection if
+// the sample missed the rank.
+Cut select_low_half_par(std::vector<Rec>& recs, std::vector<Rec>& tmp, std::uint32_t b,
+                        std::uint32_t e, bool x_axis, double fallback, int threads) {
+  const std::uint32_t n = e - b;
+  if (n < par_min_size() || threads < 2 || n < 4096) return select_low_half(recs, b, e, x_axis, fallback);
+  auto less = [x_axis](const Rec& p, const Rec& q) {
+    const double cp = along(p, x_axis), cq = along(q, x_axis);
+    if (cp != cq) return cp < cq;
+    return p.id < q.id;
+  };
+  const std::uint32_t k = (n + 1) / 2, r = k - 1;
+  constexpr int S = 4096, D = 96;
+  std::vector<Rec> smp(S);
+  for (int i = 0; i < S; ++i) smp[i] = recs[b + std::uint32_t(std::uint64_t(i) * n / S)];
+  std::sort(smp.begin(), smp.end(), less);
+  const int at = int(std::uint64_t(r) * S / n);
+  const Rec plo = smp[std::max(0, at - D)], phi = smp[std::min(S - 1, at + D)];
+  const int T = threads;
+  const std::uint64_t per = (std::uint64_t(n) + T - 1) / T;
+  std::vector<std::uint64_t> c(3 * std::size_t(T) + 3, 0);  // [t] lt, mid, gt
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
+    const std::uint64_t i0 = b + std::min<std::uint64_t>(n, t * per);
+    const std::uint64_t i1 = b + std::min<std::uint64_t>(n, (t + 1) * per);
+    std::uint64_t lt = 0, gt = 0;
+    for (std::uint64_t i = i0; i < i1; ++i) {
+      if (less(recs[i], plo)) ++lt;
+      else if (less(phi, recs[i])) ++gt;
+    }
+    c[3 * t] = lt;
+    c[3 * t + 1] = (i1 - i0) - lt - gt;
+    c[3 * t + 2] = gt;
+  }
+  std::uint64_t L = 0, M = 0;
+  for (int t = 0; t < T; ++t) L += c[3 * t], M += c[3 * t + 1];
+  if (!(L <= r && r < L + M)) return select_low_half(recs, b, e, x_axis, fallback);
+  std::vector<std::uint64_t> o(3 * std::size_t(T), 0);  // per-thread output starts
+  {
+    std::uint64_t ol = b, om = b + L, og = b + L + M;
+    for (int t = 0; t < T; ++t) {
+      o[3 * t] = ol, ol += c[3 * t];
+      o[3 * t + 1] = om, om += c[3 * t + 1];
+      o[3 * t + 2] = og, og += c[3 * t + 2];
+    }
+  }
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
+    const std::uint64_t i0 = b + std::min<std::uint64_t>(n, t * per);
+    const std::uint64_t i1 = b + std::min<std::uint64_t>(n, (t + 1) * per);
+    std::uint64_t pl = o[3 * t], pm = o[3 * t + 1], pg = o[3 * t + 2];
+    for (std::uint64_t i = i0; i < i1; ++i) {
+      const Rec v = recs[i];
+      if (less(v, plo)) tmp[pl++] = v;
+      else if (less(phi, v)) tmp[pg++] = v;
+      else tmp[pm++] = v;
+    }
+  }
+#pragma omp parallel for schedule(static) num_threads(T)
+  for (std::int64_t i = b; i < std::int64_t(e); ++i) recs[i] = tmp[i];
+  Rec* base = recs.data();
+  std::nth_element(base + b + L, base + b + r, base + b + L + M, less);
+  return {b + k, along(recs[b + k - 1], x_axis)};
+}
+
+// split_evals over a huge range: per-thread counts, then every record goes
+// through tmp to its stable place (lows first), and back.
+std::uint32_t split_evals_par(std::vector<Rec>& evs, std::vector<Rec>& tmp, std::uint32_t b,
+                              std::uint32_t e, bool x_axis, double value, int threads) {
+  const std::uint32_t n = e - b;
+  if (n < par_min_size() || threads < 2) return split_evals(evs, tmp, b, e, x_axis, value);
+  const int T = threads;
+  const std::uint64_t per = (std::uint64_t(n) + T - 1) / T;
+  std::vector<std::uint64_t> lo(std::size_t(T) + 1, 0);
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
+    const std::uint64_t i0 = b + std::min<std::uint64_t>(n, t * per);
+    const std::uint64_t i1 = b + std::min<std::uint64_t>(n, (t + 1) * per);
+    std::uint64_t cnt = 0;
+    for (std::uint64_t i = i0; i < i1; ++i) cnt += along(evs[i], x_axis) <= value ? 1 : 0;
+    lo[t + 1] = cnt;
+  }
+  for (int t = 0; t < T; ++t) lo[t + 1] += lo[t];
+  const std::uint64_t nlo = lo[T];
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
+    const std::uint64_t i0 = b + std::min<std::uint64_t>(n, t * per);
+    const std::uint64_t i1 = b + std::min<std::uint64_t>(n, (t + 1) * per);
+    std::uint64_t pl = b + lo[t], ph = b + nlo + ((i0 - b) - lo[t]);
+    for (std::uint64_t i = i0; i < i1; ++i) {
+      const Rec v = evs[i];
+      if (along(v, x_axis) <= value) tmp[pl++] = v;
+      else tmp[ph++] = v;
+    }
+  }
+#pragma omp parallel for schedule(static) num_threads(T)
+  for (std::int64_t i = b; i < std::int64_t(e); ++i) evs[i] = tmp[i];
+  return std::uint32_t(b + nlo);
+}
+
+// fill_box with the extents reduced over all threads (huge boxes)
+void fill_box_par(MBox& box, const std::vector<Rec>& src, const std::vector<Rec>& evs,
+                  cplx fallback, int threads) {
+  const std::uint32_t n = (box.point_end - box.point_begin) + (box.eval_end - box.eval_begin);
+  if (n < par_min_size() || threads < 2) return fill_box(box, src, evs, fallback);
+  if (box.point_begin == box.point_end && box.eval_begin == box.eval_end) {
+    box.center = fallback;
+    box.half_width = box.half_height = box.radius = 0.0;
+    return;
+  }
+  // per-thread partial extents combined in thread order with the serial
+  // helper's std::min / std::max: ties (+0.0 / -0.0) resolve as in index order
+  const int T = threads;
+  std::vector<double> part(4 * std::size_t(T));
+  const std::uint64_t np = box.point_end - box.point_begin, ne = box.eval_end - box.eval_begin;
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
+    double a0 = std::numeric_limits<double>::infinity(), a1 = -a0, b0 = a0, b1 = -a0;
+    const std::uint64_t s0 = box.point_begin + np * t / T, s1 = box.point_begin + np * (t + 1) / T;
+    for (std::uint64_t i = s0; i < s1; ++i) {
+      a0 = std::min(a0, src[i].x);
+      a1 = std::max(a1, src[i].x);
+      b0 = std::min(b0, src[i].y);
+      b1 = std::max(b1, src[i].y);
+    }
+    part[4 * t] = a0, part[4 * t + 1] = a1, part[4 * t + 2] = b0, part[4 * t + 3] = b1;
+  }
+  double x0 = std::numeric_limits<double>::infinity(), x1 = -x0, y0 = x0, y1 = -x0;
+  for (int t = 0; t < T; ++t) {
+    x0 = std::min(x0, part[4 * t]);
+    x1 = std::max(x1, part[4 * t + 1]);
+    y0 = std::min(y0, part[4 * t + 2]);
+    y1 = std::max(y1, part[4 * t + 3]);
+  }
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
+    double a0 = std::numeric_limits<double>::infinity(), a1 = -a0, b0 = a0, b1 = -a0;
+    const std::uint64_t s0 = box.eval_begin + ne * t / T, s1 = box.eval_begin + ne * (t + 1) / T;
+    for (std::uint64_t i = s0; i < s1; ++i) {
+      a0 = std::min(a0, evs[i].x);
+      a1 = std::max(a1, evs[i].x);
+      b0 = std::min(b0, evs[i].y);
+      b1 = std::max(b1, evs[i].y);
+    }
+    part[4 * t] = a0, part[4 * t + 1] = a1, part[4 * t + 2] = b0, part[4 * t + 3] = b1;
+  }
+  for (int t = 0; t < T; ++t) {
+    x0 = std::min(x0, part[4 * t]);
+    x1 = std::max(x1, part[4 * t + 1]);
+    y0 = std::min(y0, part[4 * t + 2]);
+    y1 = std::max(y1, part[4 * t + 3]);
+  }
+  box.center = cplx(0.5 * (x0 + x1), 0.5 * (y0 + y1));
+  box.half_width = 0.5 * (x1 - x0);
+  box.half_height = 0.5 * (y1 - y0);
+  box.radius = std::hypot(box.half_width, box.half_height);
+}
+
 }  // namespace
 
 Pyramid build_pyramid(const SourceSet& sources, const EvalSet& evals, int n_levels, int threads) {
@@ -137,41 +318,27 @@ Pyramid build_pyramid(const SourceSet& sources, const EvalSet& evals, int n_leve
   MBox root;
   root.point_end = ns;
   root.eval_end = ne;
-  fill_box(root, src, evs, cplx(0, 0));
+  fill_box_par(root, src, evs, cplx(0, 0), threads);
   pyr.levels[0].push_back(root);
 
-  std::vector<Rec> scratch(ne);
+  std::vector<Rec> scratch(ne), src_tmp;
+  if (threads > 1 && ns >= par_min_size()) src_tmp.resize(ns);
+  static const bool trace = std::getenv("FMM_TRACE") != nullptr;
+  auto tl = std::chrono::steady_clock::now();
   for (int l = 1; l < n_levels; ++l) {
+    if (trace && l > 1) {
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[fmm] host pyramid level %d: %.1f ms\n", l - 1,
+                   std::chrono::duration<double, std::milli>(now - tl).count());
+      tl = now;
+    }
     const std::vector<MBox>& up = pyr.levels[l - 1];
     std::vector<MBox>& kids = pyr.levels[l];
     kids.resize(up.size() * 4);
     const std::int64_t np = std::int64_t(up.size());
-    // Few huge parents near the root: parallelise inside the parent (the
-    // two y-splits); many parents deeper down: parallelise across parents.
     const bool inner = np < threads;
-#pragma omp parallel for schedule(dynamic) num_threads(threads) if (!inner)
-    for (std::int64_t pi = 0; pi < np; ++pi) {
-      const MBox& par = up[pi];
-      const Cut cx = select_low_half(src, par.point_begin, par.point_end, true, par.center.real());
-      const std::uint32_t emx =
-          split_evals(evs, scratch, par.eval_begin, par.eval_end, true, cx.value);
-      Cut cyl{}, cyh{};
-      std::uint32_t emyl = 0, emyh = 0;
-#pragma omp parallel sections num_threads(2) if (inner)
-      {
-#pragma omp section
-        {
-          cyl = select_low_half(src, par.point_begin, cx.mid, false, par.center.imag());
-          emyl = split_evals(evs, scratch, par.eval_begin, emx, false, cyl.value);
-        }
-#pragma omp section
-        {
-          cyh = select_low_half(src, cx.mid, par.point_end, false, par.center.imag());
-          emyh = split_evals(evs, scratch, emx, par.eval_end, false, cyh.value);
-        }
-      }
-      const std::uint32_t pb[5] = {par.point_begin, cyl.mid, cx.mid, cyh.mid, par.point_end};
-      const std::uint32_t eb[5] = {par.eval_begin, emyl, emx, emyh, par.eval_end};
+    auto place = [&](std::int64_t pi, const MBox& par, const std::uint32_t* pb,
+                     const std::uint32_t* eb, bool par_fill) {
       for (int c = 0; c < 4; ++c) {
         MBox& kid = kids[4 * pi + c];
         kid.level = l;
@@ -180,8 +347,47 @@ Pyramid build_pyramid(const SourceSet& sources, const EvalSet& evals, int n_leve
         kid.point_end = pb[c + 1];
         kid.eval_begin = eb[c];
         kid.eval_end = eb[c + 1];
-        fill_box(kid, src, evs, par.center);
+        if (par_fill) fill_box_par(kid, src, evs, par.center, threads);
+        else fill_box(kid, src, evs, par.center);
       }
+    };
+    if (inner) {
+      // Few huge parents near the root: one parent at a time, each step
+      // (selection, eval split, extents) parallel over all threads.
+      for (std::int64_t pi = 0; pi < np; ++pi) {
+        const MBox& par = up[pi];
+        const Cut cx = select_low_half_par(src, src_tmp, par.point_begin, par.point_end, true,
+                                           par.center.real(), threads);
+        const std::uint32_t emx =
+            split_evals_par(evs, scratch, par.eval_begin, par.eval_end, true, cx.value, threads);
+        const Cut cyl = select_low_half_par(src, src_tmp, par.point_begin, cx.mid, false,
+                                            par.center.imag(), threads);
+        const std::uint32_t emyl =
+            split_evals_par(evs, scratch, par.eval_begin, emx, false, cyl.value, threads);
+        const Cut cyh = select_low_half_par(src, src_tmp, cx.mid, par.point_end, false,
+                                            par.center.imag(), threads);
+        const std::uint32_t emyh =
+            split_evals_par(evs, scratch, emx, par.eval_end, false, cyh.value, threads);
+        const std::uint32_t pb[5] = {par.point_begin, cyl.mid, cx.mid, cyh.mid, par.point_end};
+        const std::uint32_t eb[5] = {par.eval_begin, emyl, emx, emyh, par.eval_end};
+        place(pi, par, pb, eb, true);
+      }
+      continue;
+    }
+    // many parents deeper down: parallelise across parents
+#pragma omp parallel for schedule(dynamic) num_threads(threads)
+    for (std::int64_t pi = 0; pi < np; ++pi) {
+      const MBox& par = up[pi];
+      const Cut cx = select_low_half(src, par.point_begin, par.point_end, true, par.center.real());
+      const std::uint32_t emx =
+          split_evals(evs, scratch, par.eval_begin, par.eval_end, true, cx.value);
+      const Cut cyl = select_low_half(src, par.point_begin, cx.mid, false, par.center.imag());
+      const std::uint32_t emyl = split_evals(evs, scratch, par.eval_begin, emx, false, cyl.value);
+      const Cut cyh = select_low_half(src, cx.mid, par.point_end, false, par.center.imag());
+      const std::uint32_t emyh = split_evals(evs, scratch, emx, par.eval_end, false, cyh.value);
+      const std::uint32_t pb[5] = {par.point_begin, cyl.mid, cx.mid, cyh.mid, par.point_end};
+      const std::uint32_t eb[5] = {par.eval_begin, emyl, emx, emyh, par.eval_end};
+      place(pi, par, pb, eb, false);
     }
   }
 

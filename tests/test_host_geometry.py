@@ -179,3 +179,49 @@ def test_errors():
     with pytest.raises(F.InvalidInput):
         F.Tree(F.SourceSet(np.array([np.nan + 0j]), np.ones(1)), F.EvalSet(np.zeros(0, complex)), 2,
                0.5)
+
+
+_PAR_SCRIPT = r"""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+from conftest import bitwise
+from oracle import oracle as O
+from paper_1311_1006_b200 import fmm as F
+g = np.arange(40) * 0.025
+lat = (g[:, None] + 1j * g[None, :]).ravel()
+cases = [(F.make_distribution(0, 60_000, 11), None, 7), (F.make_distribution(2, 40_000, 12), None, 6),
+         (F.make_distribution(0, 30_000, 13), 20_000, 6),
+         (F.SourceSet(np.concatenate([lat, lat[:300]]), np.ones(1900)), None, 5)]
+for s, ne, L in cases:
+    e = F.EvalSet.self_of(s) if ne is None else F.EvalSet(F.make_distribution(3, ne, 5).z * 1.2 - 0.1)
+    t = F.Tree(s, e, L, 0.5, threads=8)
+    r = O.ref_tree(F._c2(s.z), F._c2(s.m), F._c2(e.y), e.source_id, L, 0.5, threads=8)
+    assert np.array_equal(t.perm, r.perm) and np.array_equal(t.eval_perm, r.eval_perm)
+    for lvl in range(L):
+        assert bitwise(t.boxes_f[lvl], r.boxes_f[lvl]), lvl
+        assert np.array_equal(t.boxes_u[lvl], r.boxes_u[lvl]), lvl
+        for a, b in ((t.strong[lvl], r.strong[lvl]), (t.weak[lvl], r.weak[lvl])):
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+print("ok")
+"""
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
+def test_parallel_top_level_splits_bitwise_vs_live_reference():
+    """The huge boxes near the root are split with a parallel selection, a
+    parallel stable eval split and parallel extents (geometry.cpp).  Forced
+    onto every box above 64 points (FMM_PAR_SELECT_MIN, read once per
+    process, hence the subprocess), trees and lists stay bitwise the
+    reference's -- uniform, clustered, separate evals and a lattice with
+    duplicated points (ties)."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    env = dict(os.environ, FMM_PAR_SELECT_MIN="64", ROOT=ROOT, OMP_NUM_THREADS="8")
+    out = subprocess.run([sys.executable, "-c", _PAR_SCRIPT], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
