@@ -25,6 +25,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <limits>
+#include <memory>
+#include <sys/mman.h>
 
 #include "fmm/geometry.hpp"
 
@@ -52,6 +54,36 @@ struct Rec {
 
 inline double along(const Rec& r, bool x_axis) { return x_axis ? r.x : r.y; }
 
+// Uninitialised record storage (no serial zero fill of ~240 MB per array at
+// 10M; the pages are first touched by the parallel fills), on transparent
+// huge pages.
+class RecBuf {
+ public:
+  RecBuf() = default;
+  explicit RecBuf(std::size_t n) { resize(n); }
+  void resize(std::size_t n) {
+    p_.reset(n ? new Rec[n] : nullptr);  // default-initialised: no zeroing
+    n_ = n;
+    const std::size_t bytes = n * sizeof(Rec);
+    constexpr std::uintptr_t kHuge = std::uintptr_t(2) << 20;
+    if (bytes >= 2 * kHuge) {
+      const auto b = reinterpret_cast<std::uintptr_t>(p_.get());
+      const std::uintptr_t a0 = (b + kHuge - 1) & ~(kHuge - 1), a1 = (b + bytes) & ~(kHuge - 1);
+      if (a1 > a0) madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
+    }
+  }
+  std::size_t size() const { return n_; }
+  Rec* data() { return p_.get(); }
+  const Rec* data() const { return p_.get(); }
+  Rec* begin() { return p_.get(); }
+  Rec& operator[](std::size_t i) { return p_[i]; }
+  const Rec& operator[](std::size_t i) const { return p_[i]; }
+
+ private:
+  std::unique_ptr<Rec[]> p_;
+  std::size_t n_ = 0;
+};
+
 // Selects the low half of recs[b,e) in place; returns the split position
 // and the split coordinate (fallback when the range is empty).
 struct Cut {
@@ -59,7 +91,7 @@ struct Cut {
   double value;
 };
 
-Cut select_low_half(std::vector<Rec>& recs, std::uint32_t b, std::uint32_t e, bool x_axis,
+Cut select_low_half(RecBuf& recs, std::uint32_t b, std::uint32_t e, bool x_axis,
                     double fallback) {
   if (e == b) return {b, fallback};
   const std::uint32_t k = (e - b + 1) / 2;
@@ -75,7 +107,7 @@ Cut select_low_half(std::vector<Rec>& recs, std::uint32_t b, std::uint32_t e, bo
 
 // Stable two-way partition of evs[b,e) by coord <= value; returns the
 // boundary.  tmp[b,e) is this range's private scratch.
-std::uint32_t split_evals(std::vector<Rec>& evs, std::vector<Rec>& tmp, std::uint32_t b,
+std::uint32_t split_evals(RecBuf& evs, RecBuf& tmp, std::uint32_t b,
                           std::uint32_t e, bool x_axis, double value) {
   std::uint32_t lo = b, hi = 0;
   for (std::uint32_t i = b; i < e; ++i) {
@@ -89,7 +121,7 @@ std::uint32_t split_evals(std::vector<Rec>& evs, std::vector<Rec>& tmp, std::uin
   return lo;
 }
 
-void fill_box(MBox& box, const std::vector<Rec>& src, const std::vector<Rec>& evs, cplx fallback) {
+void fill_box(MBox& box, const RecBuf& src, const RecBuf& evs, cplx fallback) {
   if (box.point_begin == box.point_end && box.eval_begin == box.eval_end) {
     box.center = fallback;
     box.half_width = box.half_height = box.radius = 0.0;
@@ -133,7 +165,7 @@ std::uint32_t par_min_size() {
 // scatters [< lo | between | > hi] through tmp, and nth_element finishes
 // inside the (small) middle bucket.  Falls back to the serial selection if
 // the sample missed the rank.
-Cut select_low_half_par(std::vector<Rec>& recs, std::vector<Rec>& tmp, std::uint32_t b,
+Cut select_low_half_par(RecBuf& recs, RecBuf& tmp, std::uint32_t b,
                         std::uint32_t e, bool x_axis, double fallback, int threads) {
   const std::uint32_t n = e - b;
   if (n < par_min_size() || threads < 2 || n < 4096) return select_low_half(recs, b, e, x_axis, fallback);
@@ -198,7 +230,7 @@ Cut select_low_half_par(std::vector<Rec>& recs, std::vector<Rec>& tmp, std::uint
 
 // split_evals over a huge range: per-thread counts, then every record goes
 // through tmp to its stable place (lows first), and back.
-std::uint32_t split_evals_par(std::vector<Rec>& evs, std::vector<Rec>& tmp, std::uint32_t b,
+std::uint32_t split_evals_par(RecBuf& evs, RecBuf& tmp, std::uint32_t b,
                               std::uint32_t e, bool x_axis, double value, int threads) {
   const std::uint32_t n = e - b;
   if (n < par_min_size() || threads < 2) return split_evals(evs, tmp, b, e, x_axis, value);
@@ -232,7 +264,7 @@ std::uint32_t split_evals_par(std::vector<Rec>& evs, std::vector<Rec>& tmp, std:
 }
 
 // fill_box with the extents reduced over all threads (huge boxes)
-void fill_box_par(MBox& box, const std::vector<Rec>& src, const std::vector<Rec>& evs,
+void fill_box_par(MBox& box, const RecBuf& src, const RecBuf& evs,
                   cplx fallback, int threads) {
   const std::uint32_t n = (box.point_end - box.point_begin) + (box.eval_end - box.eval_begin);
   if (n < par_min_size() || threads < 2) return fill_box(box, src, evs, fallback);
@@ -292,19 +324,23 @@ void fill_box_par(MBox& box, const std::vector<Rec>& src, const std::vector<Rec>
 }  // namespace
 
 Pyramid build_pyramid(const SourceSet& sources, const EvalSet& evals, int n_levels, int threads) {
+  const auto t_setup = std::chrono::steady_clock::now();
   if (n_levels < 1) throw InvalidParameter("build_pyramid: n_levels must be >= 1");
   if (sources.size() == 0) throw InvalidInput("build_pyramid: empty source set");
-  for (const cplx& z : sources.z)
-    if (!std::isfinite(z.real()) || !std::isfinite(z.imag()))
-      throw InvalidInput("build_pyramid: non-finite source position");
-  for (const cplx& y : evals.y)
-    if (!std::isfinite(y.real()) || !std::isfinite(y.imag()))
-      throw InvalidInput("build_pyramid: non-finite eval position");
   if (threads < 1) threads = 1;
+  bool fin_s = true, fin_e = true;
+#pragma omp parallel for schedule(static) num_threads(threads) reduction(&& : fin_s)
+  for (std::int64_t i = 0; i < std::int64_t(sources.size()); ++i)
+    fin_s = fin_s && std::isfinite(sources.z[i].real()) && std::isfinite(sources.z[i].imag());
+  if (!fin_s) throw InvalidInput("build_pyramid: non-finite source position");
+#pragma omp parallel for schedule(static) num_threads(threads) reduction(&& : fin_e)
+  for (std::int64_t i = 0; i < std::int64_t(evals.size()); ++i)
+    fin_e = fin_e && std::isfinite(evals.y[i].real()) && std::isfinite(evals.y[i].imag());
+  if (!fin_e) throw InvalidInput("build_pyramid: non-finite eval position");
 
   const std::uint32_t ns = static_cast<std::uint32_t>(sources.size());
   const std::uint32_t ne = static_cast<std::uint32_t>(evals.size());
-  std::vector<Rec> src(ns), evs(ne);
+  RecBuf src(ns), evs(ne);
 #pragma omp parallel for schedule(static) num_threads(threads)
   for (std::int64_t i = 0; i < std::int64_t(ns); ++i)
     src[i] = Rec{sources.z[i].real(), sources.z[i].imag(), std::uint32_t(i)};
@@ -321,10 +357,13 @@ Pyramid build_pyramid(const SourceSet& sources, const EvalSet& evals, int n_leve
   fill_box_par(root, src, evs, cplx(0, 0), threads);
   pyr.levels[0].push_back(root);
 
-  std::vector<Rec> scratch(ne), src_tmp;
+  RecBuf scratch(ne), src_tmp;
   if (threads > 1 && ns >= par_min_size()) src_tmp.resize(ns);
   static const bool trace = std::getenv("FMM_TRACE") != nullptr;
   auto tl = std::chrono::steady_clock::now();
+  if (trace)
+    std::fprintf(stderr, "[fmm] host pyramid setup: %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(tl - t_setup).count());
   for (int l = 1; l < n_levels; ++l) {
     if (trace && l > 1) {
       const auto now = std::chrono::steady_clock::now();
@@ -391,6 +430,10 @@ Pyramid build_pyramid(const SourceSet& sources, const EvalSet& evals, int n_leve
     }
   }
 
+  if (trace)
+    std::fprintf(stderr, "[fmm] host pyramid levels done: %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_setup)
+                     .count());
   // Canonical (ascending original index) order of sources inside each leaf.
   const std::vector<MBox>& fine = pyr.levels.back();
   pyr.perm.resize(ns);
@@ -452,11 +495,17 @@ LevelConn classify_level(const LevelConn& parent, const Pyramid& pyramid, int le
 }
 
 Connectivity build_connectivity(const Pyramid& pyramid, double theta) {
+  static const bool trace = std::getenv("FMM_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   Connectivity c;
   c.levels.resize(pyramid.n_levels);
   c.levels[0] = classify_level(LevelConn{}, pyramid, 0, theta);
   for (int l = 1; l < pyramid.n_levels; ++l)
     c.levels[l] = classify_level(c.levels[l - 1], pyramid, l, theta);
+  if (trace)
+    std::fprintf(stderr, "[fmm] host connectivity: %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                     .count());
   return c;
 }
 
