@@ -50,7 +50,9 @@ struct DevicePipeline {
   DevBuf z, m, y, sid;
   HostBuf hz, hm, hy, hsid, hres;
   // pyramid
-  DevBuf px_s, py_s, px_e, py_e, lowbase, tstate;  // list positions (fused partition)
+  DevBuf px_s, py_s, px_e, py_e, lowbase, tstate, tstate_e;  // list positions (fused partition)
+  size_t tstate_bytes[2] = {0, 0};  // one of the two alternating tile-state buffers [src, evals]
+  uint32_t part_parity[2] = {0, 0};
   DevBuf keys0, keys1, ids, sx, sy, ex, ey, sxn, syn, exn, eyn, flag_s, flag_e, ind, scan,
       cub_tmp, xmid_s, xmid_e, ymid_s, ymid_e, half_s, half_e, leaf_of, perm, eperm, inv;
   DevBuf soff, eoff;                       // all levels: level l at off_base[l]
@@ -97,7 +99,7 @@ void destroy_pipeline(DevicePipeline* p) {
     if (e) cudaEventDestroy(e);
   DevBuf* bufs[] = {&p->z, &p->m, &p->y, &p->sid, &p->keys0, &p->keys1, &p->ids, &p->sx, &p->sy,
                     &p->ex, &p->ey, &p->sxn, &p->syn, &p->exn, &p->eyn, &p->flag_s, &p->flag_e,
-                    &p->px_s, &p->py_s, &p->px_e, &p->py_e, &p->lowbase, &p->tstate,
+                    &p->px_s, &p->py_s, &p->px_e, &p->py_e, &p->lowbase, &p->tstate, &p->tstate_e,
                     &p->ind, &p->scan, &p->cub_tmp, &p->xmid_s, &p->xmid_e, &p->ymid_s,
                     &p->ymid_e, &p->half_s, &p->half_e, &p->leaf_of, &p->perm, &p->eperm,
                     &p->inv, &p->soff, &p->eoff, &p->center, &p->hw, &p->hh, &p->radius,
@@ -243,7 +245,11 @@ __global__ void __launch_bounds__(kPartTB)
                            const uint32_t* __restrict__ off, const uint32_t* __restrict__ mid,
                            uint32_t nseg, const uint32_t* __restrict__ lowbase,
                            const uint32_t* __restrict__ pos_other, uint32_t* __restrict__ out,
-                           uint32_t* __restrict__ pos_self, PartTileState ts) {
+                           uint32_t* __restrict__ pos_self, PartTileState ts,
+                           PartTileState ts_next, int init_next) {
+  // the next partition's tile states (same tile count: every partition runs
+  // over all n ids), initialised here instead of by a kernel of its own
+  if (init_next) ts_next.InitializeStatus(int(gridDim.x));
   using BlockScan = cub::BlockScan<uint32_t, kPartTB>;
   using Prefix = cub::TilePrefixCallbackOp<uint32_t, cuda::std::plus<uint32_t>, PartTileState>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
@@ -305,25 +311,77 @@ __global__ void list_positions_kernel(const uint32_t* __restrict__ list, uint32_
   if (i < n) pos[list[i]] = i;
 }
 
-int fused_partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint32_t n,
-                    const uint32_t* off, const uint32_t* mid, uint32_t nseg,
-                    const uint32_t* pos_other, uint32_t* out, uint32_t* pos_self, cudaStream_t s) {
-  if (!n) return FMMCU_OK;
-  uint32_t* lowbase = P->lowbase.as<uint32_t>();
-  auto cnt = thrust::make_transform_iterator(thrust::counting_iterator<uint32_t>(0), LowCount{off, mid});
-  size_t bytes = 0;
-  CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, lowbase, int64_t(nseg), s));
-  CU_TRY(c, P->cub_tmp.ensure(bytes));
-  CU_TRY(c, cub::DeviceScan::ExclusiveSum(P->cub_tmp.p, bytes, cnt, lowbase, int64_t(nseg), s));
-  const int tiles = int((uint64_t(n) + kPartTB * kPartIPT - 1) / (kPartTB * kPartIPT));
+// lowbase[s] = lows in the segments before s, for nseg <= kLowScanMax in one
+// block (a CUB scan is two launches; the deep levels of a 1M pyramid are
+// launch-latency bound)
+constexpr uint32_t kLowScanMax = 1u << 16;
+constexpr int kLowScanTB = 1024;
+
+__global__ void __launch_bounds__(kLowScanTB)
+    lowbase_scan_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ mid,
+                        uint32_t nseg, uint32_t* __restrict__ lowbase) {
+  using BlockScan = cub::BlockScan<uint32_t, kLowScanTB>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t s0 = 0; s0 < nseg; s0 += kLowScanTB) {
+    const uint32_t s = s0 + threadIdx.x;
+    const uint32_t v = s < nseg ? mid[s] - off[s] : 0u;
+    uint32_t ex, agg;
+    BlockScan(tmp).ExclusiveSum(v, ex, agg);
+    if (s < nseg) lowbase[s] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+}
+
+// Tile states of the fused partitions: two buffers used alternately; each
+// partition initialises the other for the next one (the first is
+// initialised by tiles_reset).
+// (one pair for the source-list partitions, one for the eval lists: their
+// lengths, hence tile counts, differ)
+int tiles_reset(fmmcu_ctx* c, DevicePipeline* P, uint32_t n, bool evals, cudaStream_t s) {
+  const int tiles = int((uint64_t(std::max(n, 1u)) + kPartTB * kPartIPT - 1) / (kPartTB * kPartIPT));
   size_t tbytes = 0;
   CU_TRY(c, PartTileState::AllocationSize(tiles, tbytes));
-  CU_TRY(c, P->tstate.ensure(tbytes));
+  tbytes = (tbytes + 255) & ~size_t(255);
+  DevBuf& buf = evals ? P->tstate_e : P->tstate;
+  CU_TRY(c, buf.ensure(2 * tbytes));
+  P->tstate_bytes[evals] = tbytes;
+  P->part_parity[evals] = 0;
   PartTileState ts;
-  CU_TRY(c, ts.Init(tiles, P->tstate.p, tbytes));
+  CU_TRY(c, ts.Init(tiles, buf.p, tbytes));
   part_tiles_init_kernel<<<(tiles + 32 + 255) / 256, 256, 0, s>>>(ts, tiles);
+  return FMMCU_OK;
+}
+
+int fused_partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint32_t n,
+                    const uint32_t* off, const uint32_t* mid, uint32_t nseg,
+                    const uint32_t* pos_other, uint32_t* out, uint32_t* pos_self, cudaStream_t s,
+                    bool evals = false) {
+  if (!n) return FMMCU_OK;
+  uint32_t* lowbase = P->lowbase.as<uint32_t>();
+  if (nseg <= kLowScanMax) {
+    lowbase_scan_kernel<<<1, kLowScanTB, 0, s>>>(off, mid, nseg, lowbase);
+  } else {
+    auto cnt = thrust::make_transform_iterator(thrust::counting_iterator<uint32_t>(0), LowCount{off, mid});
+    size_t bytes = 0;
+    CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, lowbase, int64_t(nseg), s));
+    CU_TRY(c, P->cub_tmp.ensure(bytes));
+    CU_TRY(c, cub::DeviceScan::ExclusiveSum(P->cub_tmp.p, bytes, cnt, lowbase, int64_t(nseg), s));
+  }
+  const int tiles = int((uint64_t(n) + kPartTB * kPartIPT - 1) / (kPartTB * kPartIPT));
+  const size_t tb = P->tstate_bytes[evals];
+  char* base = (evals ? P->tstate_e : P->tstate).as<char>();
+  uint32_t& par = P->part_parity[evals];
+  PartTileState ts, tn;
+  CU_TRY(c, ts.Init(tiles, base + (par & 1) * tb, tb));
+  CU_TRY(c, tn.Init(tiles, base + ((par + 1) & 1) * tb, tb));
+  ++par;
   fused_partition_kernel<<<tiles, kPartTB, 0, s>>>(list, n, off, mid, nseg, lowbase, pos_other,
-                                                   out, pos_self, ts);
+                                                   out, pos_self, ts, tn, 1);
   return FMMCU_OK;
 }
 
@@ -448,6 +506,11 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     differ = P->flag.as<int>() + kFlagTie;
   }
   if (same) CU_TRY(c, cudaMemsetAsync(differ, 0, 4, s));
+  if (L > 1) {
+    if (int rc = tiles_reset(c, P, N, false, s)) return rc;
+    if (!same && M)
+      if (int rc = tiles_reset(c, P, M, true, s)) return rc;
+  }
   for (int l = 1; l < L; ++l) {
     const uint32_t np = uint32_t(pow4(l - 1));
     const uint32_t* ps = soff + P->off_base[l - 1];
@@ -468,15 +531,14 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     a.smid = xmid_s;
     a.emid = xmid_e;
     a.differ = same ? differ : nullptr;
+    a.s_out = half_s;  // the halves' offsets, fused (no child_offsets launch)
+    a.e_out = same ? nullptr : half_e;
     split_kernel<<<blocks(np), TB, 0, s>>>(a);
     if (int rc = fused_partition(c, P, SY, N, ps, xmid_s, np, pxs, SYn, pys, s)) return rc;
     if (!same)
-      if (int rc = fused_partition(c, P, EY, M, pe, xmid_e, np, pxe, EYn, pye, s)) return rc;
+      if (int rc = fused_partition(c, P, EY, M, pe, xmid_e, np, pxe, EYn, pye, s, true)) return rc;
     std::swap(SY, SYn);
     if (!same) std::swap(EY, EYn);
-    child_offsets_kernel<<<blocks(np), TB, 0, s>>>(ps, xmid_s, nullptr, np, half_s, nullptr);
-    if (!same)
-      child_offsets_kernel<<<blocks(np), TB, 0, s>>>(pe, xmid_e, nullptr, np, half_e, nullptr);
     // y split of both halves (geometry.cpp:143-146)
     a.slist = SY;
     a.elist = same ? SY : EY;
@@ -488,22 +550,17 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     a.smid = ymid_s;
     a.emid = ymid_e;
     a.differ = same ? differ : nullptr;
+    // the children's offsets, fused; aliased: the eval offsets are the same
+    // (a tie discards this pass anyway)
+    a.s_out = soff + P->off_base[l];
+    a.e_out = eoff + P->off_base[l];
     split_kernel<<<blocks(2 * np), TB, 0, s>>>(a);
     if (int rc = fused_partition(c, P, SX, N, half_s, ymid_s, 2 * np, pys, SXn, pxs, s)) return rc;
     if (!same)
-      if (int rc = fused_partition(c, P, EX, M, half_e, ymid_e, 2 * np, pye, EXn, pxe, s))
+      if (int rc = fused_partition(c, P, EX, M, half_e, ymid_e, 2 * np, pye, EXn, pxe, s, true))
         return rc;
     std::swap(SX, SXn);
     if (!same) std::swap(EX, EXn);
-    child_offsets_kernel<<<blocks(np), TB, 0, s>>>(ps, xmid_s, ymid_s, np, nullptr,
-                                                   soff + P->off_base[l]);
-    if (!same) {
-      child_offsets_kernel<<<blocks(np), TB, 0, s>>>(pe, xmid_e, ymid_e, np, nullptr,
-                                                     eoff + P->off_base[l]);
-    } else {
-      CU_TRY(c, cudaMemcpyAsync(eoff + P->off_base[l], soff + P->off_base[l],
-                                (pow4(l) + 1) * 4, cudaMemcpyDeviceToDevice, s));
-    }
     if (same) {
       // geometry reads the eval lists: they are the source lists
       uint32_t* ex_save = EX;

@@ -144,6 +144,12 @@ struct SplitArgs {
   uint32_t* __restrict__ smid;  // [nseg] first high position
   uint32_t* __restrict__ emid;  // [nseg]
   int* __restrict__ differ;     // non-null: set when emid != smid (eval lists alias sources)
+  // fused offsets (null: not written).  x split: the halves' offsets
+  // [2 nseg + 1] = (off[s], mid[s]) per parent s; y split: the children's
+  // offsets [2 nseg + 1] = (off[s], mid[s]) per half s (children of parent p
+  // are halves 2p, 2p+1 split in two) -- child_offsets_kernel's output.
+  uint32_t* __restrict__ s_out;
+  uint32_t* __restrict__ e_out;
 };
 
 __global__ void split_kernel(const SplitArgs a) {
@@ -167,6 +173,16 @@ __global__ void split_kernel(const SplitArgs a) {
   }
   a.emid[s] = lo;
   if (a.differ && lo != mid) atomicOr(a.differ, 1);
+  if (a.s_out) {
+    a.s_out[2 * s] = b;
+    a.s_out[2 * s + 1] = mid;
+    if (s == a.nseg - 1) a.s_out[2 * a.nseg] = e;
+  }
+  if (a.e_out) {
+    a.e_out[2 * s] = a.eoff[s];
+    a.e_out[2 * s + 1] = lo;
+    if (s == a.nseg - 1) a.e_out[2 * a.nseg] = a.eoff[a.nseg];
+  }
 }
 
 // flag[id] = 1 for the entries of list that fall before mid of their segment
