@@ -53,6 +53,7 @@ struct DevicePipeline {
   DevBuf px_s, py_s, px_e, py_e, lowbase, tstate, tstate_e;  // list positions (fused partition)
   size_t tstate_bytes[2] = {0, 0};  // one of the two alternating tile-state buffers [src, evals]
   uint32_t part_parity[2] = {0, 0};
+  DevBuf keys2, keys3, ids2, cub_tmp2;  // the concurrent y sorts' scratch
   DevBuf keys0, keys1, ids, sx, sy, ex, ey, sxn, syn, exn, eyn, flag_s, flag_e, ind, scan,
       cub_tmp, xmid_s, xmid_e, ymid_s, ymid_e, half_s, half_e, leaf_of, perm, eperm, inv;
   DevBuf soff, eoff;                       // all levels: level l at off_base[l]
@@ -71,6 +72,7 @@ struct DevicePipeline {
   bool tree_valid = false;
   cudaStream_t far = nullptr;
   cudaEvent_t ev[14] = {};
+  cudaEvent_t ev_sort[2] = {};  // x / y sorts on two streams
   cudaEvent_t ev_lvl[18] = {};  // FMMCU_TRACE: pyramid phases
   fmmcu::pinned_vector<uint32_t> h_pt, h_evo, h_so, h_si;  // finest CSR for the work list
   static constexpr int kChunksMax = 64;
@@ -93,11 +95,14 @@ void destroy_pipeline(DevicePipeline* p) {
   if (p->far) cudaStreamDestroy(p->far);
   for (cudaEvent_t e : p->ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_sort)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_lvl)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_res)
     if (e) cudaEventDestroy(e);
-  DevBuf* bufs[] = {&p->z, &p->m, &p->y, &p->sid, &p->keys0, &p->keys1, &p->ids, &p->sx, &p->sy,
+  DevBuf* bufs[] = {&p->z, &p->m, &p->y, &p->sid, &p->keys0, &p->keys1, &p->ids, &p->keys2,
+                    &p->keys3, &p->ids2, &p->cub_tmp2, &p->sx, &p->sy,
                     &p->ex, &p->ey, &p->sxn, &p->syn, &p->exn, &p->eyn, &p->flag_s, &p->flag_e,
                     &p->px_s, &p->py_s, &p->px_e, &p->py_e, &p->lowbase, &p->tstate, &p->tstate_e,
                     &p->ind, &p->scan, &p->cub_tmp, &p->xmid_s, &p->xmid_e, &p->ymid_s,
@@ -213,13 +218,21 @@ int sort_pairs(fmmcu_ctx* c, DevicePipeline* P, const K* kin, K* kout, const uin
 }
 
 // list sorted along axis of points p[0..n) (ties by index)
+// second=true: the second set of key / id / CUB scratch, so the x and y
+// sorts can run at the same time on two streams
 int sorted_list(fmmcu_ctx* c, DevicePipeline* P, const double2* pts, uint32_t n, int axis,
-                uint32_t* list, cudaStream_t s) {
+                uint32_t* list, cudaStream_t s, bool second = false) {
   if (!n) return FMMCU_OK;
-  auto* k0 = P->keys0.as<unsigned long long>();
-  auto* k1 = P->keys1.as<unsigned long long>();
-  coord_keys_kernel<<<blocks(n), TB, 0, s>>>(pts, n, axis, k0, P->ids.as<uint32_t>());
-  return sort_pairs(c, P, k0, k1, P->ids.as<uint32_t>(), list, n, 64, s);
+  auto* k0 = (second ? P->keys2 : P->keys0).as<unsigned long long>();
+  auto* k1 = (second ? P->keys3 : P->keys1).as<unsigned long long>();
+  uint32_t* ids = (second ? P->ids2 : P->ids).as<uint32_t>();
+  coord_keys_kernel<<<blocks(n), TB, 0, s>>>(pts, n, axis, k0, ids);
+  size_t bytes = 0;
+  CU_TRY(c, cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0, k1, ids, list, int64_t(n), 0, 64, s));
+  DevBuf& tmp = second ? P->cub_tmp2 : P->cub_tmp;
+  CU_TRY(c, tmp.ensure(bytes));
+  CU_TRY(c, cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k0, k1, ids, list, int64_t(n), 0, 64, s));
+  return FMMCU_OK;
 }
 
 // One-pass stable segmented partition (decoupled look-back).  Each id's low
@@ -406,6 +419,9 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   CU_TRY(c, P->keys0.ensure(nmax * 8));
   CU_TRY(c, P->keys1.ensure(nmax * 8));
   CU_TRY(c, P->ids.ensure(nmax * 4));
+  CU_TRY(c, P->keys2.ensure(nmax * 8));
+  CU_TRY(c, P->keys3.ensure(nmax * 8));
+  CU_TRY(c, P->ids2.ensure(nmax * 4));
   for (DevBuf* b : {&P->sx, &P->sy, &P->sxn, &P->syn, &P->perm, &P->inv})
     CU_TRY(c, b->ensure(uint64_t(std::max(N, 1u)) * 4));
   for (DevBuf* b : {&P->ex, &P->ey, &P->exn, &P->eyn, &P->eperm})
@@ -436,16 +452,22 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   uint32_t* SYn = P->syn.as<uint32_t>();
   uint32_t* EXn = P->exn.as<uint32_t>();
   uint32_t* EYn = P->eyn.as<uint32_t>();
+  // the y sorts on the (idle) far stream, concurrently with the x sorts
+  cudaStream_t ys = P->far;
+  CU_TRY(c, cudaEventRecord(P->ev_sort[0], s));
+  CU_TRY(c, cudaStreamWaitEvent(ys, P->ev_sort[0], 0));
+  if (int rc = sorted_list(c, P, zp, N, 1, SY, ys, true)) return rc;
   if (int rc = sorted_list(c, P, zp, N, 0, SX, s)) return rc;
   if (c->trace) cudaEventRecord(P->ev_lvl[0], s);
-  if (int rc = sorted_list(c, P, zp, N, 1, SY, s)) return rc;
   if (P->self_eval) {  // evals are the sources: same sorted lists
     CU_TRY(c, cudaMemcpyAsync(EX, SX, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
-    CU_TRY(c, cudaMemcpyAsync(EY, SY, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, s));
+    CU_TRY(c, cudaMemcpyAsync(EY, SY, uint64_t(N) * 4, cudaMemcpyDeviceToDevice, ys));
   } else {
+    if (int rc = sorted_list(c, P, yp, M, 1, EY, ys, true)) return rc;
     if (int rc = sorted_list(c, P, yp, M, 0, EX, s)) return rc;
-    if (int rc = sorted_list(c, P, yp, M, 1, EY, s)) return rc;
   }
+  CU_TRY(c, cudaEventRecord(P->ev_sort[1], ys));
+  CU_TRY(c, cudaStreamWaitEvent(s, P->ev_sort[1], 0));
 
   uint32_t* soff = P->soff.as<uint32_t>();
   uint32_t* eoff = P->eoff.as<uint32_t>();
@@ -931,6 +953,8 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate, bool t
     c->pipe = new DevicePipeline();
     CU_TRY(c, cudaStreamCreateWithFlags(&c->pipe->far, cudaStreamNonBlocking));
     for (cudaEvent_t& e : c->pipe->ev) CU_TRY(c, cudaEventCreate(&e));
+    for (cudaEvent_t& e : c->pipe->ev_sort)
+      CU_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (cudaEvent_t& e : c->pipe->ev_lvl) CU_TRY(c, cudaEventCreate(&e));
     for (cudaEvent_t& e : c->pipe->ev_res)
       CU_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
