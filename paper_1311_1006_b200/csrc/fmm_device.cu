@@ -61,7 +61,7 @@ struct DevicePipeline {
   std::vector<uint64_t> off_base, box_base;
   // connectivity
   std::vector<LevelConnDev> conn;
-  DevBuf cnt_s, cnt_w;
+  DevBuf cnt_s, cnt_w, dcount;
   // far field
   DevBuf binom, out, loc, tcnt, wcnt, trow, wstart, m2l_row, tbox, woff, widx, m2l_sum, flag, res;
   HostBuf h_flag, h_count;
@@ -108,7 +108,7 @@ void destroy_pipeline(DevicePipeline* p) {
                     &p->ind, &p->scan, &p->cub_tmp, &p->xmid_s, &p->xmid_e, &p->ymid_s,
                     &p->ymid_e, &p->half_s, &p->half_e, &p->leaf_of, &p->perm, &p->eperm,
                     &p->inv, &p->soff, &p->eoff, &p->center, &p->hw, &p->hh, &p->radius,
-                    &p->cnt_s, &p->cnt_w, &p->binom, &p->out, &p->loc, &p->tcnt, &p->wcnt,
+                    &p->cnt_s, &p->cnt_w, &p->dcount, &p->binom, &p->out, &p->loc, &p->tcnt, &p->wcnt,
                     &p->trow, &p->wstart, &p->m2l_row, &p->tbox, &p->woff, &p->widx,
                     &p->m2l_sum, &p->flag, &p->res};
   for (DevBuf* b : bufs) b->release();
@@ -655,6 +655,52 @@ int build_pyramid_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_
 }
 
 // ----------------------------------------------------------- connectivity --
+// Both per-box count arrays (strong, weak) exclusive-scanned in one block
+// (levels up to kLowScanMax boxes; launch latency dominates them).
+__global__ void __launch_bounds__(kLowScanTB)
+    scan2_kernel(const uint32_t* __restrict__ a_in, const uint32_t* __restrict__ b_in, uint32_t n,
+                 uint32_t* __restrict__ a_out, uint32_t* __restrict__ b_out) {
+  using BlockScan = cub::BlockScan<uint32_t, kLowScanTB>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  __shared__ uint32_t ca, cb;
+  if (threadIdx.x == 0) ca = cb = 0;
+  __syncthreads();
+  for (uint32_t s0 = 0; s0 < n; s0 += kLowScanTB) {
+    const uint32_t i = s0 + threadIdx.x;
+    uint32_t ea, eb, ga, gb;
+    BlockScan(tmp).ExclusiveSum(i < n ? a_in[i] : 0u, ea, ga);
+    __syncthreads();
+    BlockScan(tmp).ExclusiveSum(i < n ? b_in[i] : 0u, eb, gb);
+    if (i < n) {
+      a_out[i] = ca + ea;
+      b_out[i] = cb + eb;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ca += ga;
+      cb += gb;
+    }
+    __syncthreads();
+  }
+}
+
+// every level's list totals (the last scanned offsets) and the overflow
+// flag in one array: a single D2H for the whole speculative build
+struct ConnTotals {
+  const uint32_t* s_end[16];
+  const uint32_t* w_end[16];
+  int L;
+};
+__global__ void conn_totals_kernel(ConnTotals t, const int* __restrict__ ovf,
+                                   uint32_t* __restrict__ out) {
+  const int l = threadIdx.x;
+  if (l == 0) out[0] = uint32_t(*ovf);
+  if (l >= 1 && l < t.L) {
+    out[2 * l] = *t.s_end[l];
+    out[2 * l + 1] = *t.w_end[l];
+  }
+}
+
 int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaStream_t s) {
   const int L = P->L;
   P->conn.resize(L);
@@ -701,30 +747,37 @@ int build_connectivity_dev(fmmcu_ctx* c, DevicePipeline* P, double theta, cudaSt
     int* ovf = P->flag.as<int>() + kFlagOverflow;
     CU_TRY(c, cudaMemsetAsync(ovf, 0, 4, s));
     uint32_t* hc = P->h_count.as<uint32_t>();
+    // per level: count (the count kernel also zeroes the scans' end entries),
+    // one scan launch for both lists, fill; the totals are read once at the end
+    ConnTotals tot{};
+    tot.L = L;
     for (int l = 1; l < L; ++l) {
       const uint32_t nbox = uint32_t(pow4(l));
       LevelConnDev& pc = P->conn[l - 1];
       LevelConnDev& lc = P->conn[l];
       const double2* cen = P->center.as<double2>() + P->box_base[l];
       const double* rad = P->radius.as<double>() + P->box_base[l];
-      CU_TRY(c, cudaMemsetAsync(cs + nbox, 0, 4, s));
-      CU_TRY(c, cudaMemsetAsync(cw + nbox, 0, 4, s));
       classify_kernel<false><<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
           pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, cs, cw, nullptr,
           nullptr, nullptr, nullptr, 0xFFFFFFFFu, 0xFFFFFFFFu, ovf);
-      if (int rc = scan_excl(c, P, cs, lc.s_off.as<uint32_t>(), nbox + 1, s)) return rc;
-      if (int rc = scan_excl(c, P, cw, lc.w_off.as<uint32_t>(), nbox + 1, s)) return rc;
+      if (nbox + 1 <= kLowScanMax) {
+        scan2_kernel<<<1, kLowScanTB, 0, s>>>(cs, cw, nbox + 1, lc.s_off.as<uint32_t>(),
+                                              lc.w_off.as<uint32_t>());
+      } else {
+        if (int rc = scan_excl(c, P, cs, lc.s_off.as<uint32_t>(), nbox + 1, s)) return rc;
+        if (int rc = scan_excl(c, P, cw, lc.w_off.as<uint32_t>(), nbox + 1, s)) return rc;
+      }
       classify_kernel<true><<<blocks(uint64_t(nbox) * 32), TB, 0, s>>>(
           pc.s_off.as<uint32_t>(), pc.s_idx.as<uint32_t>(), cen, rad, nbox, theta, nullptr, nullptr,
           lc.s_off.as<uint32_t>(), lc.w_off.as<uint32_t>(), lc.s_idx.as<uint32_t>(),
           lc.w_idx.as<uint32_t>(), scap[l], wcap[l], ovf);
-      CU_TRY(c, cudaMemcpyAsync(hc + 2 * l, lc.s_off.as<uint32_t>() + nbox, 4,
-                                cudaMemcpyDeviceToHost, s));
-      CU_TRY(c, cudaMemcpyAsync(hc + 2 * l + 1, lc.w_off.as<uint32_t>() + nbox, 4,
-                                cudaMemcpyDeviceToHost, s));
-      c->launches += 2;
+      tot.s_end[l] = lc.s_off.as<uint32_t>() + nbox;
+      tot.w_end[l] = lc.w_off.as<uint32_t>() + nbox;
+      c->launches += 3;
     }
-    CU_TRY(c, cudaMemcpyAsync(hc, ovf, 4, cudaMemcpyDeviceToHost, s));
+    CU_TRY(c, P->dcount.ensure(uint64_t(2 * L + 2) * 4));
+    conn_totals_kernel<<<1, 32, 0, s>>>(tot, ovf, P->dcount.as<uint32_t>());
+    CU_TRY(c, cudaMemcpyAsync(hc, P->dcount.p, uint64_t(2 * L) * 4, cudaMemcpyDeviceToHost, s));
     const auto tq0 = Clock::now();
     CU_TRY(c, cudaStreamSynchronize(s));
     if (c->trace) {

@@ -374,6 +374,10 @@ __global__ void classify_kernel(const uint32_t* __restrict__ ps_off,
   const uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (a >= nbox) return;  // warp-uniform
+  if (!FILL && a == 0 && lane == 0) {  // the exclusive scans' end entries
+    s_cnt[nbox] = 0;
+    w_cnt[nbox] = 0;
+  }
   if (overflow && *overflow) return;  // a coarser level did not fit: lists are invalid
   const uint32_t p = a >> 2;
   uint32_t so = FILL ? s_off[a] : 0, wo = FILL ? w_off[a] : 0;
