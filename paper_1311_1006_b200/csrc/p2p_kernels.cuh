@@ -132,6 +132,15 @@ __device__ __forceinline__ void fence_mbar_init() {
 // Per-pair contribution accumulated with the sign folded out:
 //   harmonic: acc += m * conj(d) / |d|^2     (term = -acc)
 //   log     : acc += m * log(d)              (term = +acc)
+// Gaussian smoother factor 1 - exp(-x), x = r^2 / delta^2 (expansion.cpp:83).
+// For x >= 38, exp(-x) < 2^-54, so the difference rounds to exactly 1.0:
+// when every active lane of the warp is that far (source runs of distant
+// strong partners), the whole warp skips the exp -- same bits.
+__device__ __forceinline__ double gauss_g(double x) {
+  if (__all_sync(__activemask(), x >= 38.0)) return 1.0;
+  return 1.0 - exp(-x);
+}
+
 // The smoother multiplies the term; g == 0 contributes nothing (backend.cpp:61-63).
 template <int KERNEL, int SMOOTH>
 __device__ __forceinline__ void pair_accum(double yx, double yy, const double4 s, double inv_d2,
@@ -142,7 +151,7 @@ __device__ __forceinline__ void pair_accum(double yx, double yy, const double4 s
   if (KERNEL == 0) {
     double inv = rcp_fast(r2);
     if (SMOOTH == 1) {
-      const double g = 1.0 - exp(-r2 * inv_d2);
+      const double g = gauss_g(r2 * inv_d2);
       inv = (g == 0.0) ? 0.0 : inv * g;
     } else if (SMOOTH == 2) {
       const double g = sqrt(r2 / (d2 + r2));
@@ -158,7 +167,7 @@ __device__ __forceinline__ void pair_accum(double yx, double yy, const double4 s
     double L = 0.5 * log(r2);
     double T = atan2(dy, dx);
     double g = 1.0;
-    if (SMOOTH == 1) g = 1.0 - exp(-r2 * inv_d2);
+    if (SMOOTH == 1) g = gauss_g(r2 * inv_d2);
     if (SMOOTH == 2) g = sqrt(r2 / (d2 + r2));
     const bool use = live && (g != 0.0);
     L = use ? L * g : 0.0;

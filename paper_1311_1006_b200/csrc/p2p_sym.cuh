@@ -52,7 +52,7 @@ __device__ __forceinline__ void sym_pair(double yx, double yy, double mex, doubl
   const double r2 = fma(dx, dx, dy * dy);
   double inv = rcp_fast(r2);
   if (SMOOTH == 1) {
-    const double g = 1.0 - exp(-r2 * inv_d2);
+    const double g = gauss_g(r2 * inv_d2);
     inv = (g == 0.0) ? 0.0 : inv * g;
   } else if (SMOOTH == 2) {
     const double g = sqrt(r2 / (d2 + r2));
