@@ -1262,9 +1262,9 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate, bool t
     if (int rc = stage_csr_dev(c, P->soff.as<uint32_t>() + P->off_base[L - 1],
                                P->eoff.as<uint32_t>() + P->off_base[L - 1], fc.s_off.as<uint32_t>(),
                                fc.s_idx.as<uint32_t>(), nleaf, fc.s_nnz, M, ws, ev[13],
-                               // more than 32 entries per leaf on average: some leaf exceeds
-                               // the mutual kernel's 32, skip the attempt
-                               pipe_sym && uint64_t(fc.s_nnz) <= 32ull * nleaf))
+                               // more strong entries per leaf on average than a mutual item
+                               // holds: some leaf exceeds it, skip the attempt
+                               pipe_sym && uint64_t(fc.s_nnz) <= uint64_t(kSymMaxEntries) * nleaf))
       return rc;
     CU_TRY(c, cudaStreamWaitEvent(s, ev[13], 0));
     if (M) {  // eval records {x, y, self slot, strong entry of the self slot}

@@ -184,9 +184,10 @@ void dispatch_exact(int kn, int sm, const P2PArgs& a, uint32_t lb, uint32_t le, 
   }
 }
 
-template <int SM, int E, int W = 4, int C = 128, int U = 1, int MINB = 3, int SS = 1>
+template <int SM, int E, int W = 4, int C = 128, int U = 1, int MINB = 3, int SS = 1,
+          bool ROUNDS = false>
 void launch_sym_v(const P2PArgs& a, const P2PSymArgs& sa, uint32_t n_items, cudaStream_t s) {
-  auto kfn = p2p_sym_kernel<SM, E, W, C, U, MINB, SS>;
+  auto kfn = p2p_sym_kernel<SM, E, W, C, U, MINB, SS, ROUNDS>;
   constexpr size_t smem = size_t(W) * sym_region_bytes(C, E);
   static int grid_cap = [&] {
     cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -216,7 +217,19 @@ int sym_variant() {
 }
 
 void dispatch_sym(int sm, const P2PArgs& a, const P2PSymArgs& sa, uint32_t n, cudaStream_t s,
-                  int E) {
+                  int E, bool rounds) {
+  if (rounds) {  // items with more than 32 entries: the entry-round instantiation
+    if (E == 5) {
+      if (sm == 0) launch_sym_v<0, 5, 4, 128, 1, 3, 1, true>(a, sa, n, s);
+      else if (sm == 1) launch_sym_v<1, 5, 4, 128, 1, 3, 1, true>(a, sa, n, s);
+      else launch_sym_v<2, 5, 4, 128, 1, 3, 1, true>(a, sa, n, s);
+    } else {
+      if (sm == 0) launch_sym_v<0, 4, 4, 128, 1, 3, 1, true>(a, sa, n, s);
+      else if (sm == 1) launch_sym_v<1, 4, 4, 128, 1, 3, 1, true>(a, sa, n, s);
+      else launch_sym_v<2, 4, 4, 128, 1, 3, 1, true>(a, sa, n, s);
+    }
+    return;
+  }
   if (E == 5 && sm == 0) {
     switch (sym_variant()) {
       case 1: launch_sym_v<0, 5, 4, 256, 1, 3>(a, sa, n, s); return;
@@ -324,7 +337,8 @@ int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
   nblk[0] = 0;
   slots[0] = 0;
   bool ok = true;
-#pragma omp parallel for schedule(static) reduction(&& : ok)
+  uint32_t max_n = 0;
+#pragma omp parallel for schedule(static) reduction(&& : ok) reduction(max : max_n)
   for (int64_t i = 0; i < int64_t(np); ++i) {
     const uint32_t t = lb + uint32_t(i);
     uint32_t n = 0;
@@ -338,7 +352,8 @@ int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
     }
     const uint32_t ntl = j->ev_off[t + 1] - j->ev_off[t];
     const uint32_t nb = ntl ? (ntl + max_ev - 1) / max_ev : 0;
-    ok = ok && n <= uint32_t(kWarpMaxEntries) && so + ss < (1ull << 31);
+    ok = ok && n <= uint32_t(kSymMaxEntries) && so + ss < (1ull << 31);
+    max_n = std::max(max_n, n);
     ent[i + 1] = n;
     nblk[i + 1] = nb;
     ssym[i] = ss;
@@ -394,6 +409,7 @@ int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
   tr.mark("sym: contributions");
   c->sym_slots = slots[np];
   c->sym_n_items = uint32_t(c->items.size());
+  c->sym_rounds = max_n > uint32_t(kWarpMaxEntries);
   c->sym_lb = lb;
   c->sym_le = le;
   c->sym_items = true;
@@ -1331,7 +1347,7 @@ int run_kernels(fmmcu_ctx* c, uint32_t lb, uint32_t le, int mode, int* nlaunch,
       if (ni) {
         P2PArgs aa = a;
         aa.n_items = ni;
-        dispatch_sym(c->smoother, aa, sa, ni, s, c->warp_e);
+        dispatch_sym(c->smoother, aa, sa, ni, s, c->warp_e, c->sym_rounds);
         ++n;
       }
       const uint32_t nlr = le - lb;

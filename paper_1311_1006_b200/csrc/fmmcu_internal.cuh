@@ -285,6 +285,7 @@ struct fmmcu_ctx {
   std::vector<uint32_t> sw_ent, sw_nblk;
   std::vector<uint64_t> sw_ssym, sw_sord, sw_slots;
   uint64_t sym_slots = 0;               // contrib slots
+  bool sym_rounds = false;              // some symmetric item has more than 32 entries
   uint32_t sym_n_items = 0;             // items of the symmetric list (host or device built)
   DevBuf d_wls;                         // device symmetric-list scratch
   DevBuf d_symseg, d_syminfo, d_tgt, d_contrib, d_cloff, d_clcnt, d_clbase, d_cubtmp;

@@ -66,7 +66,7 @@ __device__ __forceinline__ void sym_pair(double yx, double yy, double mex, doubl
   ci = fma(mex, wi, fma(mey, wr, ci));
 }
 
-template <int SMOOTH, int E, int WARPS, int C, int U, int MINB, int SS = 1>
+template <int SMOOTH, int E, int WARPS, int C, int U, int MINB, int SS = 1, bool ROUNDS = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs a,
                                                                    const P2PSymArgs sa) {
   static_assert(C % 32 == 0, "shape");
@@ -98,34 +98,42 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
     if (lane == 0) claim = atomicAdd(a.next_item, 1u);
     const P2PItem it = a.items[id];
     const uint32_t nt = it.nt, ev0 = it.ev_begin;
-    const uint32_t nent = it.s_end - it.s_begin;  // <= 32 (host)
-    const uint32_t nsrc = it.n_src;
+    // entries in rounds of 32 (one per lane); a leaf with more strong
+    // entries than that runs several rounds over the same evals
+    const uint32_t nent_all = it.s_end - it.s_begin;
     const uint32_t V0 = it.pad;             // virtual positions of the ordered runs
     const uint32_t sym_base = it.partial_off;
 
-    uint32_t rb = 0, rn = 0, kind = kRunOrdered;
-    if (uint32_t(lane) < nent) {
-      const uint4 sg = sa.sym_seg[it.s_begin + lane];
-      rb = sg.x;
-      rn = sg.y;
-      kind = sg.z;
-    }
-    uint32_t incl = rn;
+    uint32_t rb = 0, rn = 0, kind = kRunOrdered, roff = 0, round_src = 0;
+    unsigned self_mask = 0;
+    uint32_t self_rb = 0, self_roff = 0;
+    auto load_round = [&](uint32_t r, uint32_t vbase) {
+      const uint32_t q = r * 32u + uint32_t(lane);
+      rb = rn = 0;
+      kind = kRunOrdered;
+      if (q < nent_all) {
+        const uint4 sg = sa.sym_seg[it.s_begin + q];
+        rb = sg.x;
+        rn = sg.y;
+        kind = sg.z;
+      }
+      uint32_t incl = rn;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const uint32_t roff = incl - rn;
-    // the self run (one per item): its first slot and virtual offset
-    const unsigned self_mask = __ballot_sync(FULL, uint32_t(lane) < nent && kind == kRunSelf);
-    const int self_lane = self_mask ? __ffs(self_mask) - 1 : 0;
-    const uint32_t self_rb = __shfl_sync(FULL, rb, self_lane);
-    const uint32_t self_roff = __shfl_sync(FULL, roff, self_lane);
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      roff = vbase + incl - rn;  // the run's position in the item's virtual stream
+      round_src = __shfl_sync(FULL, incl, 31);
+      // the self run (one per item): its first slot and virtual offset
+      self_mask = __ballot_sync(FULL, q < nent_all && kind == kRunSelf);
+      const int self_lane = self_mask ? __ffs(self_mask) - 1 : 0;
+      self_rb = __shfl_sync(FULL, rb, self_lane);
+      self_roff = __shfl_sync(FULL, roff, self_lane);
+    };
+    load_round(0, 0);
 
-    auto issue_chunk = [&](uint32_t c, int b) {
-      const uint32_t v0 = c * C;
-      const uint32_t v1 = min(nsrc, v0 + C);
+    auto issue_chunk = [&](uint32_t v0, uint32_t v1, int b) {
       if (lane == 0) {
         fence_proxy_async();
         mbar_expect_tx(&bar[b], (v1 - v0) * 32u);
@@ -134,8 +142,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
       const uint32_t lo = max(roff, v0), hi = min(roff + rn, v1);
       if (hi > lo) bulk_g2s(buf + b * C + (lo - v0), a.src + rb + (lo - roff), (hi - lo) * 32u, &bar[b]);
     };
-    const uint32_t nchunk = (nsrc + C - 1) / C;
-    if (nchunk > 0) issue_chunk(0, 0);
+    if (round_src > 0) issue_chunk(0, min(round_src, uint32_t(C)), 0);
 
     const uint32_t G = (nt + E - 1) / E;
     const float rG = 1.0f / float(G);
@@ -146,6 +153,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
 
     double yx[E], yy[E], ar[E], ai[E], mx[E], my[E];
     uint32_t vself[E];
+    auto set_self = [&]() {  // self layout: eval slot ev0 + le is its own source slot
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t le = g * E + e;
+        const bool ok = active && le < nt;
+        if (ok && self_mask) {
+          vself[e] = self_roff + (ev0 + le - self_rb);
+          if (k == 0) ++hits;
+        }
+      }
+    };
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t le = g * E + e;
@@ -159,16 +177,26 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
       my[e] = me.w;
       ar[e] = 0.0;
       ai[e] = 0.0;
-      // self layout: eval slot ev0 + le is its own source slot
-      vself[e] = (ok && self_mask) ? self_roff + (ev0 + le - self_rb) : kNoSelf;
-      if (vself[e] != kNoSelf && k == 0) ++hits;
+      vself[e] = kNoSelf;
     }
+    set_self();
 
-    for (uint32_t c = 0; c < nchunk; ++c) {
-      const int b = int(c & 1u);
-      if (c + 1 < nchunk) issue_chunk(c + 1, b ^ 1);
-      const uint32_t v0 = c * C;
-      const uint32_t len = min(nsrc - v0, uint32_t(C));
+    const uint32_t nrounds = ROUNDS ? (nent_all + 31u) / 32u : 1u;
+    uint32_t cg = 0;        // chunks consumed so far (double-buffer parity)
+    uint32_t rv0 = 0;       // virtual start of the current round
+    for (uint32_t rd = 0; rd < nrounds; ++rd) {
+    if (rd > 0) {
+      load_round(rd, rv0);
+      set_self();
+      if (round_src > 0) issue_chunk(rv0, rv0 + min(round_src, uint32_t(C)), int(cg & 1u));
+    }
+    const uint32_t rv1 = rv0 + round_src;
+    const uint32_t nchunk = (round_src + C - 1) / C;
+    for (uint32_t c = 0; c < nchunk; ++c, ++cg) {
+      const int b = int(cg & 1u);
+      const uint32_t v0 = rv0 + c * C;
+      if (c + 1 < nchunk) issue_chunk(v0 + C, min(rv1, v0 + 2 * uint32_t(C)), b ^ 1);
+      const uint32_t len = min(rv1 - v0, uint32_t(C));
       const uint32_t ord_end = V0 > v0 ? min(V0 - v0, len) : 0u;  // chunk-relative
       uint32_t ps[E];
       uint32_t plo = kNoSelf, phi = 0u;
@@ -262,6 +290,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) p2p_sym_kernel(const P2PArgs
       }
       __syncwarp();
     }
+    rv0 = rv1;
+    }  // rounds
 
     if (lane == 0) bulk_wait_read();
     __syncwarp();
@@ -317,11 +347,18 @@ __global__ void p2p_sym_lists_kernel(uint32_t leaf0, uint32_t n_leaves,
       n += nblk;
       continue;
     }
-    const uint4 sg = uint32_t(lane) < nx.x - it.x ? seg[it.x + lane] : make_uint4(0, 0, 0, 0);
-    const bool sym = sg.z == kRunSym;
-    const unsigned hit = __ballot_sync(0xffffffffu, sym && sg.x == b);
-    const int at = __ffs(hit) - 1;
-    const uint32_t voff = __reduce_add_sync(0xffffffffu, (sym && lane < at) ? sg.y : 0u);
+    // B's run offset inside t's symmetric part: the sources of t's symmetric
+    // entries before it (t's entries in rounds of 32, one per lane)
+    const uint32_t ne = nx.x - it.x;
+    uint32_t voff = 0;
+    for (uint32_t r0 = 0; r0 < ne; r0 += 32) {
+      const uint4 sg = r0 + uint32_t(lane) < ne ? seg[it.x + r0 + lane] : make_uint4(0, 0, 0, 0);
+      const bool sym = sg.z == kRunSym;
+      const unsigned hit = __ballot_sync(0xffffffffu, sym && sg.x == b);
+      const int at = hit ? __ffs(hit) - 1 : 32;
+      voff += __reduce_add_sync(0xffffffffu, (sym && lane < at) ? sg.y : 0u);
+      if (hit) break;
+    }
     for (uint32_t blk = uint32_t(lane); blk < nblk; blk += 32) cl_base[o + blk] = it.z + blk * it.w + voff;
     o += nblk;
   }

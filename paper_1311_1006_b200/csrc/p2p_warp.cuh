@@ -25,6 +25,8 @@ namespace fmmcu {
 
 constexpr int kWarpSlots = 8;        // eval slots per warp item: <= 8E evals, K >= 4 source lanes
 constexpr int kWarpMaxEntries = 32;  // strong entries per warp item (one per lane)
+// strong entries per mutual-kernel item: rounds of 32 (p2p_sym.cuh ROUNDS)
+constexpr int kSymMaxEntries = 256;
 
 constexpr size_t warp_region_bytes(int C, int E) {
   return 128 + size_t(2 * C) * 32 + size_t(kWarpSlots * E) * 16;

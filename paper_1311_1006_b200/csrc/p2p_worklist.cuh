@@ -334,7 +334,8 @@ static __global__ void wls_count_kernel(const uint32_t* __restrict__ ev_off,
     const uint32_t max_ev = head->max_ev;
     const uint32_t ntl = ev_off[t + 1] - ev_off[t];
     const uint32_t nb = ntl ? (ntl + max_ev - 1) / max_ev : 0u;
-    if (n > uint32_t(kWarpMaxEntries) || so + ss >= (1ull << 31)) atomicOr(&sh->bad, 1u);
+    if (n > uint32_t(kSymMaxEntries) || so + ss >= (1ull << 31)) atomicOr(&sh->bad, 1u);
+    else if (n > uint32_t(kWarpMaxEntries)) atomicOr(&sh->bad, 2u);  // needs entry rounds
     n_ent[i] = n;
     n_blk[i] = nb;
     ssym[i] = ss;

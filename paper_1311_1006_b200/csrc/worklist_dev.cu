@@ -234,7 +234,7 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   const WlHead h = *reinterpret_cast<const WlHead*>(hh);
   const uint64_t n_entries = tot[0], n_items = tot[1], n_slots = tot[2];
   c->launches += uint64_t(nk);
-  if (tot[3] || n_slots > 0xFFFFFFF0ull || n_items > 0xFFFFFFF0ull) return -1;
+  if ((tot[3] & 1u) || n_slots > 0xFFFFFFF0ull || n_items > 0xFFFFFFF0ull) return -1;
   CU_TRY(c, c->d_symseg.ensure(std::max<uint64_t>(n_entries, 1) * 16));
   CU_TRY(c, c->d_items.ensure(std::max<uint64_t>(n_items, 1) * sizeof(P2PItem)));
   CU_TRY(c, c->d_syminfo.ensure(n1 * 16));
@@ -277,6 +277,7 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   c->sym_le = le;
   c->sym_slots = n_slots;
   c->sym_n_items = uint32_t(n_items);
+  c->sym_rounds = (tot[3] & 2u) != 0;
   c->grouped = false;
   c->partial_evals = 0;
   c->dev_wl = false;

@@ -197,7 +197,10 @@ def test_device_work_list_equals_host_work_list(ctx, force_e, monkeypatch):
         monkeypatch.setenv("FMMCU_P2P_E", force_e)
     cases = list(_cases())[:5] + [
         ("heavy_gauss_L3", F.make_distribution("gauss8", 40_000, 31), None, 3, 0.5),
-        ("heavy_uniform_L2", F.make_distribution("uniform", 12_000, 32), None, 2, 0.5)]
+        ("heavy_uniform_L2", F.make_distribution("uniform", 12_000, 32), None, 2, 0.5),
+        # more than 32 strong entries per leaf: the mutual kernel's entry rounds
+        ("rounds_uniform_t015", F.make_distribution("uniform", 50_000, 33), None, 6, 0.15),
+        ("rounds_gauss_t02", F.make_distribution("gauss8", 50_000, 34), None, 6, 0.2)]
     for name, s, e, L, theta in cases:
         e = _evals(s, e)
         dev, sd = ctx.fmm_evaluate(s.z, s.m, e.y, e.source_id, n_levels=L, theta=theta, p=17)

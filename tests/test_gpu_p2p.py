@@ -334,6 +334,39 @@ def test_symmetric_kernel_vs_oracle(ctx, case):
         assert sym
 
 
+@pytest.mark.parametrize("case", [(0, 50_000, 6, 0.15, 0, 35), (1, 50_000, 6, 0.2, 1, 36),
+                                  (0, 50_000, 6, 0.15, 2, 37)])
+def test_symmetric_kernel_entry_rounds(ctx, case):
+    """Leaves with more than 32 strong entries (small theta, or the
+    non-uniform distribution) run the mutual kernel's entry-round
+    instantiation (p2p_sym.cuh ROUNDS: 32 entries per round over the same
+    evals, chunks continuing across rounds).  Pair counts exact, <= 1e-12
+    normwise of the oracle, deterministic; the launch path (ordered device
+    work list) agrees to the same bar."""
+    kind, n, L, theta, sm, seed = case
+    t, args = _tree_case(kind, n, L, seed, theta=theta)
+    so, si = args[2], args[3]
+    upper = [int((si[so[i]:so[i + 1]] >= i).sum()) for i in range(len(so) - 1)]
+    assert 32 < max(upper) <= 256  # the case exercises entry rounds
+    delta = 0.01 if sm else 0.0
+    csr = O.LeafCSR(*args[:5])
+    want, wpairs = O.nearfield(csr, *args[5:9], smoother=sm, delta=delta)
+    nl = len(args[0]) - 1
+    outs = []
+    for rep in range(2):
+        job, keep = N.CudaContext.make_job(*args, None, smoother=sm, delta=delta)
+        ctx.stage(job, keep)
+        ctx.run_staged(0, nl)
+        assert ctx.kernel_info()[0]
+        assert ctx.pairs() == wpairs
+        outs.append(ctx.copy_out(len(want)))
+    assert normwise(outs[0], want) <= TOL_FP64
+    assert bitwise(outs[0], outs[1])
+    dev, pd, _ = _run(ctx, *args, smoother=sm, delta=delta)
+    assert pd == wpairs
+    assert normwise(dev, want) <= TOL_FP64
+
+
 def test_invalid_jobs_fail_loudly(ctx):
     t, args = _tree_case(0, 1000, 3, 1)
     with pytest.raises(N.FmmcuError):
