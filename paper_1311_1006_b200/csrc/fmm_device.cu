@@ -253,13 +253,21 @@ struct LowCount {
   __host__ __device__ uint32_t operator()(uint32_t s) const { return mid[s] - off[s]; }
 };
 
+// FLAGS (source lists, whose splits are rank-based: mid = off + ceil(n/2),
+// split_kernel): instead of positions, one byte per id says whether the id is
+// low in the NEXT split.  The partition knows each id's segment after this
+// split, hence that split's rank-based mid: flag_out[id] = dst < next mid.
+// The byte arrays (N bytes each) stay in L2, where the 4-byte position
+// gathers / scatters went to DRAM.  flag_out null: the last split.
+template <bool FLAGS>
 __global__ void __launch_bounds__(kPartTB)
     fused_partition_kernel(const uint32_t* __restrict__ in, uint32_t n,
                            const uint32_t* __restrict__ off, const uint32_t* __restrict__ mid,
                            uint32_t nseg, const uint32_t* __restrict__ lowbase,
                            const uint32_t* __restrict__ pos_other, uint32_t* __restrict__ out,
                            uint32_t* __restrict__ pos_self, PartTileState ts,
-                           PartTileState ts_next, int init_next) {
+                           PartTileState ts_next, int init_next,
+                           const uint8_t* __restrict__ flag_in, uint8_t* __restrict__ flag_out) {
   // the next partition's tile states (same tile count: every partition runs
   // over all n ids), initialised here instead of by a kernel of its own
   if (init_next) ts_next.InitializeStatus(int(gridDim.x));
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(kPartTB)
       if (i < n) {
         while (off[g + 1] <= i) ++g;
         sg[k] = g;
-        const uint32_t lo = pos_other[id[k]] < mid[g] ? 1u : 0u;
+        const uint32_t lo = FLAGS ? uint32_t(flag_in[id[k]]) : (pos_other[id[k]] < mid[g] ? 1u : 0u);
         lowmask |= lo << k;
         cnt += lo;
       }
@@ -310,11 +318,26 @@ __global__ void __launch_bounds__(kPartTB)
     const uint32_t g = sg[k], b = off[g];
     const uint32_t rl = excl - lowbase[g];  // lows of this segment before i
     const bool lo = (lowmask >> k) & 1u;
-    const uint32_t dst = lo ? b + rl : mid[g] + (i - b - rl);
+    const uint32_t m = mid[g];
+    const uint32_t dst = lo ? b + rl : m + (i - b - rl);
     out[dst] = id[k];
-    pos_self[id[k]] = dst;
+    if (FLAGS) {
+      if (flag_out) {
+        const uint32_t cb = lo ? b : m, cn = lo ? m - b : off[g + 1] - m;
+        flag_out[id[k]] = dst < cb + (cn + 1) / 2 ? 1 : 0;
+      }
+    } else {
+      pos_self[id[k]] = dst;
+    }
     excl += lo ? 1u : 0u;
   }
+}
+
+// the first split's flags of a source list: flag[list[i]] = i < ceil(n/2)
+__global__ void root_flags_kernel(const uint32_t* __restrict__ list, uint32_t n,
+                                  uint8_t* __restrict__ flag) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[list[i]] = i < (n + 1) / 2 ? 1 : 0;
 }
 
 // list -> positions: pos[list[i]] = i
@@ -373,7 +396,8 @@ int tiles_reset(fmmcu_ctx* c, DevicePipeline* P, uint32_t n, bool evals, cudaStr
 int fused_partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint32_t n,
                     const uint32_t* off, const uint32_t* mid, uint32_t nseg,
                     const uint32_t* pos_other, uint32_t* out, uint32_t* pos_self, cudaStream_t s,
-                    bool evals = false) {
+                    bool evals = false, const uint8_t* flag_in = nullptr,
+                    uint8_t* flag_out = nullptr) {
   if (!n) return FMMCU_OK;
   uint32_t* lowbase = P->lowbase.as<uint32_t>();
   if (nseg <= kLowScanMax) {
@@ -393,8 +417,14 @@ int fused_partition(fmmcu_ctx* c, DevicePipeline* P, const uint32_t* list, uint3
   CU_TRY(c, ts.Init(tiles, base + (par & 1) * tb, tb));
   CU_TRY(c, tn.Init(tiles, base + ((par + 1) & 1) * tb, tb));
   ++par;
-  fused_partition_kernel<<<tiles, kPartTB, 0, s>>>(list, n, off, mid, nseg, lowbase, pos_other,
-                                                   out, pos_self, ts, tn, 1);
+  if (flag_in)
+    fused_partition_kernel<true><<<tiles, kPartTB, 0, s>>>(list, n, off, mid, nseg, lowbase, nullptr,
+                                                           out, nullptr, ts, tn, 1, flag_in,
+                                                           flag_out);
+  else
+    fused_partition_kernel<false><<<tiles, kPartTB, 0, s>>>(list, n, off, mid, nseg, lowbase,
+                                                            pos_other, out, pos_self, ts, tn, 1,
+                                                            nullptr, nullptr);
   return FMMCU_OK;
 }
 
@@ -427,7 +457,8 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   for (DevBuf* b : {&P->ex, &P->ey, &P->exn, &P->eyn, &P->eperm})
     CU_TRY(c, b->ensure(uint64_t(std::max(M, 1u)) * 4));
   CU_TRY(c, P->leaf_of.ensure(nmax * 4));
-  for (DevBuf* b : {&P->px_s, &P->py_s}) CU_TRY(c, b->ensure(uint64_t(std::max(N, 1u)) * 4));
+  // source lists: low flags of the next split (px_s / py_s hold N bytes each)
+  for (DevBuf* b : {&P->px_s, &P->py_s}) CU_TRY(c, b->ensure(uint64_t(std::max(N, 1u))));
   for (DevBuf* b : {&P->px_e, &P->py_e}) CU_TRY(c, b->ensure(uint64_t(std::max(M, 1u)) * 4));
   CU_TRY(c, P->ind.ensure((nmax + 1) * 4));
   CU_TRY(c, P->scan.ensure((nmax + 1) * 4));
@@ -503,14 +534,11 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
   uint32_t* ymid_e = P->ymid_e.as<uint32_t>();
   uint32_t* half_s = P->half_s.as<uint32_t>();
   uint32_t* half_e = P->half_e.as<uint32_t>();
-  uint32_t* pxs = P->px_s.as<uint32_t>();
-  uint32_t* pys = P->py_s.as<uint32_t>();
+  uint8_t* fxs = P->px_s.as<uint8_t>();  // low in the next x split
+  uint8_t* fys = P->py_s.as<uint8_t>();  // low in the next y split
   uint32_t* pxe = P->px_e.as<uint32_t>();
   uint32_t* pye = P->py_e.as<uint32_t>();
-  if (N) {
-    list_positions_kernel<<<blocks(N), TB, 0, s>>>(SX, N, pxs);
-    list_positions_kernel<<<blocks(N), TB, 0, s>>>(SY, N, pys);
-  }
+  if (N && L > 1) root_flags_kernel<<<blocks(N), TB, 0, s>>>(SX, N, fxs);
   if (M && !alias) {
     list_positions_kernel<<<blocks(M), TB, 0, s>>>(EX, M, pxe);
     list_positions_kernel<<<blocks(M), TB, 0, s>>>(EY, M, pye);
@@ -556,7 +584,9 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     a.s_out = half_s;  // the halves' offsets, fused (no child_offsets launch)
     a.e_out = same ? nullptr : half_e;
     split_kernel<<<blocks(np), TB, 0, s>>>(a);
-    if (int rc = fused_partition(c, P, SY, N, ps, xmid_s, np, pxs, SYn, pys, s)) return rc;
+    if (int rc = fused_partition(c, P, SY, N, ps, xmid_s, np, nullptr, SYn, nullptr, s, false,
+                                 fxs, fys))
+      return rc;
     if (!same)
       if (int rc = fused_partition(c, P, EY, M, pe, xmid_e, np, pxe, EYn, pye, s, true)) return rc;
     std::swap(SY, SYn);
@@ -577,7 +607,9 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     a.s_out = soff + P->off_base[l];
     a.e_out = eoff + P->off_base[l];
     split_kernel<<<blocks(2 * np), TB, 0, s>>>(a);
-    if (int rc = fused_partition(c, P, SX, N, half_s, ymid_s, 2 * np, pys, SXn, pxs, s)) return rc;
+    if (int rc = fused_partition(c, P, SX, N, half_s, ymid_s, 2 * np, nullptr, SXn, nullptr, s,
+                                 false, fys, l + 1 < L ? fxs : nullptr))
+      return rc;
     if (!same)
       if (int rc = fused_partition(c, P, EX, M, half_e, ymid_e, 2 * np, pye, EXn, pxe, s, true))
         return rc;
@@ -623,7 +655,7 @@ int build_pyramid_pass(fmmcu_ctx* c, DevicePipeline* P, cudaStream_t s, bool ali
     if (int rc = leaf_order(EX, M, eoff + P->off_base[L - 1], P->eperm.as<uint32_t>())) return rc;
   }
   CU_TRY(c, cudaGetLastError());
-  c->launches += uint64_t(8 + 14 * (L - 1));
+  c->launches += uint64_t(7 + 14 * (L - 1));
   return FMMCU_OK;
 }
 

@@ -125,7 +125,10 @@ void launch_warp_v(const P2PArgs& a, uint32_t n_items, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, W * 32, smem);
-    return std::max(1, sms * std::max(1, per_sm));
+    // FMMCU_GRID_PCT (experiments): persistent grid as a percentage of full residency
+    const char* pct = std::getenv("FMMCU_GRID_PCT");
+    const int g = sms * std::max(1, per_sm);
+    return std::max(1, pct ? g * std::atoi(pct) / 100 : g);
   }();
   const uint32_t need = (n_items + W - 1) / W;
   const uint32_t grid = std::max(1u, std::min<uint32_t>(need, uint32_t(grid_cap)));
@@ -269,6 +272,16 @@ int validate(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     return set_err(c, FMMCU_EINVAL, "pt_off does not span the sources");
   if (j->ev_off[0] != 0 || j->ev_off[nl] != j->n_eval)
     return set_err(c, FMMCU_EINVAL, "ev_off does not span the evals");
+  if (j->leaf_begin > j->leaf_end || j->leaf_end > nl)
+    return set_err(c, FMMCU_EINVAL, "bad leaf shard");
+  if (j->strong_off[nl] > 0 && !j->strong_idx) return set_err(c, FMMCU_EINVAL, "null strong list");
+  return FMMCU_OK;
+}
+
+// The O(leaves + strong entries) part of validate: offsets monotone, strong
+// indices in range.  launch_overlapped runs it while the first copies move.
+int validate_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  const uint32_t nl = j->n_leaves;
   bool mono = true;
 #pragma omp parallel for schedule(static) reduction(&& : mono)
   for (int64_t i = 0; i < int64_t(nl); ++i)
@@ -276,13 +289,10 @@ int validate(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
            j->strong_off[i] <= j->strong_off[i + 1];
   if (!mono) return set_err(c, FMMCU_EINVAL, "leaf offsets not monotone");
   const uint32_t nnz = j->strong_off[nl];
-  if (nnz > 0 && !j->strong_idx) return set_err(c, FMMCU_EINVAL, "null strong list");
   bool in_range = true;
 #pragma omp parallel for schedule(static) reduction(&& : in_range)
   for (int64_t q = 0; q < int64_t(nnz); ++q) in_range = in_range && j->strong_idx[q] < nl;
   if (!in_range) return set_err(c, FMMCU_EINVAL, "strong index out of range");
-  if (j->leaf_begin > j->leaf_end || j->leaf_end > nl)
-    return set_err(c, FMMCU_EINVAL, "bad leaf shard");
   return FMMCU_OK;
 }
 
@@ -410,6 +420,7 @@ int build_sym_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j, uint32_t max_ev) {
   c->sym_slots = slots[np];
   c->sym_n_items = uint32_t(c->items.size());
   c->sym_rounds = max_n > uint32_t(kWarpMaxEntries);
+  c->sym_grouped = false;
   c->sym_lb = lb;
   c->sym_le = le;
   c->sym_items = true;
@@ -651,6 +662,7 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
 // Host packing + work list + H2D.  `sync` = wait for the uploads.
 int stage_job(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   if (int rc = validate(c, j)) return rc;
+  if (int rc = validate_csr(c, j)) return rc;
   CU_TRY(c, cudaSetDevice(c->device));
   c->group_k = 0;
   const uint32_t nl = j->n_leaves, ns = j->n_src, ne = j->n_eval;
@@ -946,7 +958,18 @@ int stage_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, bool evals) {
 //  * potentials are written by the kernels' TMA bulk stores straight into
 //    the page-locked output (the caller's, or pinned staging): no D2H pass.
 int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
+  Trace tr(c);
   if (int rc = validate(c, j)) return rc;
+  // Whole-job launches with the device work list check the CSR while the
+  // CSR and the source chunks are already moving (0.27 ms of host time at
+  // 10M off the critical path); the copies only read [pt_off[cut k],
+  // pt_off[cut k+1]) ranges, checked below.  Leaf ranges walk the strong
+  // lists on the host first, so they check up front.
+  const bool defer_csr = !std::getenv("FMMCU_HOST_WL") && !std::getenv("FMMCU_NO_DEFER") &&
+                         j->leaf_begin == 0 && j->leaf_end == j->n_leaves;
+  if (!defer_csr)
+    if (int rc = validate_csr(c, j)) return rc;
+  tr.mark("validate");
   CU_TRY(c, cudaSetDevice(c->device));
   const uint32_t nl = j->n_leaves, ns = j->n_src, ne = j->n_eval;
   const uint32_t lb = j->leaf_begin, le = j->leaf_end;
@@ -957,7 +980,6 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->smoother = j->smoother;
   c->mode = j->mode;
   c->delta = j->delta;
-  Trace tr(c);
   // Leaf-aligned upload chunks of ~kChunkSrc sources.  Group k's kernels
   // start when chunk k lands, so the step ends one group's compute after the
   // last chunk: with a tail (FMMCU_TAIL=n) the last n chunks halve in
@@ -992,6 +1014,9 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
                                                  uint32_t(cut_src[k])) - j->pt_off);
     c->chunk_leaf[k] = std::max(c->chunk_leaf[k - 1], std::min(t, nl));
   }
+  for (int k = 0; k < K; ++k)  // the copies' source ranges (pt_off[nl] == ns checked)
+    if (j->pt_off[c->chunk_leaf[k]] > j->pt_off[c->chunk_leaf[k + 1]])
+      return set_err(c, FMMCU_EINVAL, "leaf offsets not monotone");
   c->group_k = K;
   c->sym_request = false;
 
@@ -1019,6 +1044,10 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     CU_TRY(c, cudaHostGetDevicePointer(&dev_out, c->h_out.p, 0));
   }
   c->out_dev = static_cast<double2*>(dev_out);
+  // host address of the same output (copy-engine D2H of the grouped mutual list)
+  double2* host_out = c->direct_out ? reinterpret_cast<double2*>(j->out) : c->h_out.as<double2>();
+  CU_TRY(c, c->d_out.ensure(size_t(std::max(ne, 1u)) * 16));
+  tr.mark("chunks + buffers");
   CU_TRY(c, cudaEventRecord(c->ev_start, s));
   c->t_evstart = Clock::now();
   CU_TRY(c, cudaStreamWaitEvent(h, c->ev_start, 0));
@@ -1094,6 +1123,26 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // (~1.5 ms at 10M) with the first kPre chunks moving meanwhile, the CSR and
   // work list queued behind those only.
   const bool dev_list = !std::getenv("FMMCU_HOST_WL");
+  // FMMCU_E2E_SYM=1: the grouped mutual list for self-evaluation.  Off by
+  // default: the launch is PCIe bound (H2D + D2H share the link, ~75 GB/s
+  // together), the ordered kernels store each result over PCIe while they
+  // compute, and the mutual list needs a finalize + copy-engine D2H per group
+  // after its kernel -- 10M / L10: 8.0-8.3 ms against 7.6-7.9 ms ordered
+  // (e2e).
+  const bool e2e_sym = std::getenv("FMMCU_E2E_SYM") != nullptr;
+  bool sym_candidate = false;
+  if (dev_list && e2e_sym && j->kernel == 0 && !c->no_sym_once && !std::getenv("FMMCU_NO_SYM") &&
+      j->eval_sid && ne == ns && ns > 0 &&
+      std::memcmp(j->ev_off, j->pt_off, size_t(nl + 1) * 4) == 0) {
+    sym_candidate = true;
+    const uint32_t nchk = std::min<uint32_t>(ns, 4096);
+    for (uint32_t i = 0; i < nchk && sym_candidate; ++i)
+      sym_candidate = j->eval_sid[i] == int64_t(j->perm[i]) &&
+                      (j->eval_y == j->src_z ||
+                       (j->eval_y[2 * i] == j->src_z[2 * i] &&
+                        j->eval_y[2 * i + 1] == j->src_z[2 * i + 1]));
+  }
+  c->no_sym_once = false;
   int pre = 0;
   if (dev_list) {
     const uint64_t csr_bytes = upload_csr(c, j, h);
@@ -1107,12 +1156,30 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
         CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
       }
     }
+    if (defer_csr) {
+      const int rc = validate_csr(c, j);
+      tr.mark("validate (overlapped)");
+      if (rc) {  // the queued copies read the caller's arrays: drain them first
+        cudaStreamSynchronize(h);
+        return rc;
+      }
+    }
     CU_TRY(c, cudaStreamWaitEvent(s, c->ev_staged, 0));
     WlGroups g{};
     g.K = uint32_t(K);
     for (int k = 0; k < K; ++k) g.slot_end[k] = j->pt_off[c->chunk_leaf[k + 1]];
     c->n_strong = j->strong_off[nl];
-    if (int rc = build_worklist_dev(c, lb, le, g, s)) return rc;  // + the run table
+    // Self-evaluation with the harmonic kernel: the mutual kernel, its list
+    // grouped by upload chunk (pairs inside a group once, across groups
+    // ordered).  The per-chunk self-layout check below confirms it chunk by
+    // chunk; a sample of the first ids decides here.
+    int rc_sym = -1;
+    if (sym_candidate) {
+      rc_sym = build_sym_worklist_dev(c, lb, le, s, &g);
+      if (rc_sym != FMMCU_OK && rc_sym != -1) return rc_sym;
+    }
+    if (rc_sym != FMMCU_OK)
+      if (int rc = build_worklist_dev(c, lb, le, g, s)) return rc;  // + the run table
     tr.mark("csr + device worklist");
   } else {
     pre = direct_in ? std::min(K, std::max(0, kPre)) : 0;
@@ -1215,7 +1282,7 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       ++nk;
     }
     uint32_t i0, i1, f0, f1;
-    if (c->dev_wl) {
+    if (c->dev_wl || c->sym_items) {  // device-built lists (ordered or mutual)
       i0 = c->dev_grp_item[k];
       i1 = c->dev_grp_item[k + 1];
       f0 = c->dev_grp_fin[k];
@@ -1239,6 +1306,53 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       gs = c->grp_stream[k & 1];
       CU_TRY(c, cudaStreamWaitEvent(gs, c->ev_prep[k], 0));
       counter += (k & 1);
+    }
+    if (c->sym_items) {  // grouped mutual list: f0 / f1 are leaf positions
+      if (i1 > i0) {
+        CU_TRY(c, cudaMemsetAsync(counter, 0, 4, gs));
+        P2PArgs aa = a;
+        aa.items = items_dev + i0;
+        aa.n_items = i1 - i0;
+        aa.next_item = counter;
+        P2PSymArgs sa{c->d_symseg.as<uint4>(), c->d_tgt.as<double2>(),
+                      c->d_contrib.as<double2>()};
+        dispatch_sym(c->smoother, aa, sa, i1 - i0, gs, c->warp_e, c->sym_rounds);
+        ++nk;
+      }
+      // Results.  Leaves of chunk k go to device memory and chunk k's eval
+      // range goes down by one copy-engine D2H (d2h stream, in chunk order)
+      // after this finalize; the few leaves of earlier chunks that land in
+      // group k (a partner in chunk k) are written straight into the host
+      // output by TMA bulk stores -- after the D2H of chunk k - 1, hence of
+      // their own chunk, whose stale copy of them they replace.  (All 160 MB
+      // as SM stores to mapped memory held each group's finalize for the
+      // whole transfer and slowed the H2D chunks by 14%.)
+      const uint32_t c0 = std::max(lb, l0), c1 = std::min(le, l1);
+      auto fin = [&](int host_part) {
+        p2p_sym_finalize_bulk_kernel<<<(f1 - f0 + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0,
+                                       gs>>>(
+            lb, f1 - f0, c->d_pt.as<uint32_t>(), c->d_cloff.as<uint32_t>(),
+            c->d_clbase.as<uint32_t>(), c->d_tgt.as<double2>(), c->d_contrib.as<double2>(),
+            c->out_dev, c->sym_order, f0, c0, c1, c->d_out.as<double2>(), host_part);
+        ++nk;
+      };
+      if (f1 > f0) fin(0);
+      CU_TRY(c, cudaEventRecord(c->ev_fin[k], gs));
+      CU_TRY(c, cudaStreamWaitEvent(c->d2h_stream, c->ev_fin[k], 0));
+      if (c1 > c0) {
+        const uint32_t e0 = j->ev_off[c0], e1 = j->ev_off[c1];
+        if (e1 > e0)
+          CU_TRY(c, cudaMemcpyAsync(host_out + e0, c->d_out.as<double2>() + e0,
+                                    size_t(e1 - e0) * 16, cudaMemcpyDeviceToHost, c->d2h_stream));
+      }
+      CU_TRY(c, cudaEventRecord(c->ev_copy[k], c->d2h_stream));
+      if (k > 0 && f1 > f0) {  // leaves of earlier chunks: after those chunks' copies
+        CU_TRY(c, cudaStreamWaitEvent(gs, c->ev_copy[k - 1], 0));
+        fin(1);
+      }
+      CU_TRY(c, cudaEventRecord(c->ev_group[k], gs));
+      CU_TRY(c, cudaGetLastError());
+      return FMMCU_OK;
     }
     if (i1 > i0) {
       CU_TRY(c, cudaMemsetAsync(counter, 0, 4, gs));
@@ -1302,6 +1416,15 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     chunk_self[k] = maybe_self ? 1 : 0;
     if (int rc = for_runs(k, [&](int64_t c0, int64_t c1) { return upload(c0, c1, k); })) return rc;
     if (k >= pre) CU_TRY(c, cudaEventRecord(c->ev_chunk[k], h));
+    if (c->sym_items && !chunk_self[k]) {
+      // the mutual list assumed the self layout and chunk k breaks it: drain
+      // what was queued and redo the job with the ordered list (correct
+      // either way; only jobs whose first ids match their sources get here)
+      for (cudaStream_t q : {s, h, c->grp_stream[0], c->grp_stream[1]})
+        if (q) CU_TRY(c, cudaStreamSynchronize(q));
+      c->no_sym_once = true;
+      return launch_overlapped(c, j);
+    }
     const bool same = chunk_self[k] != 0;
     all_self = all_self && same;
     if (c->trace)
@@ -1313,6 +1436,8 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   c->self_layout = all_self;
   if (two_streams)  // the last group of each group stream
     for (int g = std::max(0, K - 2); g < K; ++g) CU_TRY(c, cudaStreamWaitEvent(s, c->ev_group[g], 0));
+  if (c->sym_items && K > 0)  // the last chunk's D2H (grouped mutual list)
+    CU_TRY(c, cudaStreamWaitEvent(s, c->ev_copy[K - 1], 0));
   CU_TRY(c, cudaMemcpyAsync(c->h_hits.p, c->d_hits.p, 8, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaEventRecord(c->ev_end, s));
   tr.mark("enqueue done");
@@ -1567,6 +1692,10 @@ int fmmcu_create(fmmcu_ctx** out, int device) {
   for (cudaEvent_t& ep : c->ev_prep)
     if ((e = cudaEventCreateWithFlags(&ep, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
   for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
+    if ((e = cudaEventCreateWithFlags(&c->ev_fin[i], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming)) != cudaSuccess)
+      return fail(e);
+  for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
     if ((e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDefault)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_group[i], cudaEventDefault)) != cudaSuccess)
       return fail(e);
@@ -1601,7 +1730,7 @@ void fmmcu_destroy(fmmcu_ctx* c) {
     fmmcu::destroy_pipeline(c->pipe);
     c->pipe = nullptr;
     multi_release(c);
-    for (DevBuf* b : {&c->d_symseg, &c->d_syminfo, &c->d_tgt, &c->d_contrib, &c->d_cloff,
+    for (DevBuf* b : {&c->d_symseg, &c->d_syminfo, &c->d_symcnt, &c->d_tgt, &c->d_contrib, &c->d_cloff,
                       &c->d_clcnt, &c->d_clbase, &c->d_cubtmp})
       b->release();
     c->h_sym.release();
@@ -1633,6 +1762,10 @@ void fmmcu_destroy(fmmcu_ctx* c) {
       if (gs) cudaStreamSynchronize(gs), cudaStreamDestroy(gs);
     for (cudaEvent_t ep : c->ev_prep)
       if (ep) cudaEventDestroy(ep);
+    for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i) {
+      if (c->ev_fin[i]) cudaEventDestroy(c->ev_fin[i]);
+      if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
+    }
     for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
       if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
     for (int i = 0; i < fmmcu_ctx::kMaxChunks; ++i)
@@ -1767,7 +1900,7 @@ int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
       std::fprintf(stderr,
                    "[fmmcu] group %2d: chunk landed %8.3f ms, kernels done %8.3f ms, items %u\n",
                    k, a, b,
-                   c->dev_wl ? c->dev_grp_item[k + 1] - c->dev_grp_item[k]
+                   (c->dev_wl || c->sym_items) ? c->dev_grp_item[k + 1] - c->dev_grp_item[k]
                              : c->item_first[c->grp_pos[k + 1]] - c->item_first[c->grp_pos[k]]);
     }
   }
@@ -1778,6 +1911,10 @@ int fmmcu_p2p_finish(fmmcu_ctx* c, uint64_t* pair_evals, double* seconds) {
   }
   float ms = 0.f;
   CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_start, c->ev_end));
+  if (c->trace && c->overlapped)
+    std::fprintf(stderr, "[fmmcu] device span %8.3f ms, host prep %8.3f ms, finish returns at %8.3f ms\n",
+                 ms, 1e3 * c->prep_seconds,
+                 std::chrono::duration<double, std::milli>(Clock::now() - c->t_evstart).count());
   if (c->trace && !c->overlapped) {
     float kms = 0.f;
     cudaEventElapsedTime(&kms, c->ev_start, c->ev_kslice[c->n_slices - 1]);

@@ -240,6 +240,7 @@ struct fmmcu_ctx {
   static constexpr int kMaxChunks = 32;
   cudaEvent_t ev_chunk[kMaxChunks] = {}, ev_group[kMaxChunks] = {};
   cudaEvent_t ev_prep[kMaxChunks] = {};  // chunk k prepared on the stream (two-stream groups)
+  cudaEvent_t ev_fin[kMaxChunks] = {}, ev_copy[kMaxChunks] = {};  // grouped mutual: finalize k, D2H k
   cudaStream_t grp_stream[2] = {};       // group kernels alternate between these
   int n_groups = 0;
   cudaEvent_t ev_evals = nullptr;  // evals uploaded (overlapped launch, non-self layouts)
@@ -285,10 +286,13 @@ struct fmmcu_ctx {
   std::vector<uint32_t> sw_ent, sw_nblk;
   std::vector<uint64_t> sw_ssym, sw_sord, sw_slots;
   uint64_t sym_slots = 0;               // contrib slots
+  bool no_sym_once = false;             // next overlapped launch: ordered list (self check failed)
+  bool sym_grouped = false;             // symmetric list grouped by upload chunk
+  const uint32_t* sym_order = nullptr;  // grouped: leaf position -> leaf (device)
   bool sym_rounds = false;              // some symmetric item has more than 32 entries
   uint32_t sym_n_items = 0;             // items of the symmetric list (host or device built)
   DevBuf d_wls;                         // device symmetric-list scratch
-  DevBuf d_symseg, d_syminfo, d_tgt, d_contrib, d_cloff, d_clcnt, d_clbase, d_cubtmp;
+  DevBuf d_symseg, d_syminfo, d_symcnt, d_tgt, d_contrib, d_cloff, d_clcnt, d_clbase, d_cubtmp;
   HostBuf h_sym;
   // device-built work list (worklist_dev.cu): items / fins for [dev_wl_lb,
   // dev_wl_le) only, group ranges in dev_grp_item / dev_grp_fin
@@ -365,7 +369,8 @@ uint64_t upload_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, cudaStream_t stream);
 int build_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g, cudaStream_t s);
 // Symmetric (mutual-kernel) list + contribution lists on the device over
 // [lb, le) of the staged CSR (worklist_dev.cu); -1 = the job does not qualify.
-int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t s);
+int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t s,
+                           const WlGroups* g = nullptr);
 // Device-resident CSR -> context staging, run table and device work list on
 // stream `w` (records `done` there); want_sym: the mutual kernel's list when
 // the job qualifies.  Eval records are left to the caller.

@@ -331,7 +331,9 @@ __global__ void p2p_sym_lists_kernel(uint32_t leaf0, uint32_t n_leaves,
                                      const uint4* __restrict__ info,
                                      const uint4* __restrict__ seg, uint32_t* __restrict__ cnt,
                                      const uint32_t* __restrict__ cl_off,
-                                     uint32_t* __restrict__ cl_base) {
+                                     uint32_t* __restrict__ cl_base,
+                                     const uint32_t* __restrict__ grp = nullptr,
+                                     const uint2* __restrict__ leaf_cnt = nullptr) {
   const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= n_leaves) return;
   const int lane = threadIdx.x & 31;
@@ -341,15 +343,19 @@ __global__ void p2p_sym_lists_kernel(uint32_t leaf0, uint32_t n_leaves,
   for (uint32_t q = s_off[B]; q < s_off[B + 1]; ++q) {
     const uint32_t t = s_idx[q];
     if (t < leaf0 || t >= B) continue;
-    const uint4 it = info[t - leaf0], nx = info[t - leaf0 + 1];
-    const uint32_t nblk = nx.y - it.y;
+    // grouped list (per-leaf counts given): symmetric only inside the group
+    if (grp && grp[t - leaf0] != grp[w]) continue;
+    const uint4 it = info[t - leaf0];
+    const uint2 ct = leaf_cnt ? leaf_cnt[t - leaf0]
+                              : make_uint2(info[t - leaf0 + 1].x - it.x, info[t - leaf0 + 1].y - it.y);
+    const uint32_t nblk = ct.y;
     if (!FILL) {
       n += nblk;
       continue;
     }
     // B's run offset inside t's symmetric part: the sources of t's symmetric
     // entries before it (t's entries in rounds of 32, one per lane)
-    const uint32_t ne = nx.x - it.x;
+    const uint32_t ne = ct.x;
     uint32_t voff = 0;
     for (uint32_t r0 = 0; r0 < ne; r0 += 32) {
       const uint4 sg = r0 + uint32_t(lane) < ne ? seg[it.x + r0 + lane] : make_uint4(0, 0, 0, 0);
@@ -367,15 +373,20 @@ __global__ void p2p_sym_lists_kernel(uint32_t leaf0, uint32_t n_leaves,
 
 // out[i] = tgt[i] + the contributions listed for i's leaf, in list order
 // (fixed: deterministic).  One warp per leaf.
+// order (grouped lists): leaves order[pos0 + w] - in group order - instead
+// of leaf0 + w.
 static __global__ void p2p_sym_finalize_kernel(uint32_t leaf0, uint32_t n_leaves,
                                                const uint32_t* __restrict__ pt_off,
                                                const uint32_t* __restrict__ cl_off,
                                                const uint32_t* __restrict__ cl_base,
                                                const double2* __restrict__ tgt,
                                                const double2* __restrict__ contrib,
-                                               double2* __restrict__ out) {
-  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= n_leaves) return;
+                                               double2* __restrict__ out,
+                                               const uint32_t* __restrict__ order = nullptr,
+                                               uint32_t pos0 = 0) {
+  const uint32_t w0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w0 >= n_leaves) return;
+  const uint32_t w = order ? order[pos0 + w0] : w0;
   const uint32_t L = leaf0 + w;
   const uint32_t b = pt_off[L], e = pt_off[L + 1];
   const uint32_t q0 = cl_off[w], q1 = cl_off[w + 1];
@@ -388,6 +399,72 @@ static __global__ void p2p_sym_finalize_kernel(uint32_t leaf0, uint32_t n_leaves
     }
     out[i] = v;
   }
+}
+
+// As p2p_sym_finalize_kernel for the overlapped launch (one upload group),
+// in two launches: host_part = 0 stores the leaves in [dev_l0, dev_l1) (the
+// group's own chunk) to dev_out, which the caller copies down with the copy
+// engine; host_part = 1 writes the others straight into the page-locked host
+// output: each warp stages its leaf's potentials in shared memory and writes
+// them with TMA bulk stores.
+constexpr int kFinWarps = 8, kFinStage = 256;  // evals staged per warp and round
+
+static __global__ void __launch_bounds__(kFinWarps * 32)
+    p2p_sym_finalize_bulk_kernel(uint32_t leaf0, uint32_t n_leaves,
+                                 const uint32_t* __restrict__ pt_off,
+                                 const uint32_t* __restrict__ cl_off,
+                                 const uint32_t* __restrict__ cl_base,
+                                 const double2* __restrict__ tgt,
+                                 const double2* __restrict__ contrib, double2* __restrict__ out,
+                                 const uint32_t* __restrict__ order, uint32_t pos0,
+                                 uint32_t dev_l0, uint32_t dev_l1, double2* __restrict__ dev_out,
+                                 int host_part) {
+  __shared__ __align__(128) double2 stage_all[kFinWarps][kFinStage];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t w0 = blockIdx.x * kFinWarps + wid;
+  double2* stage = stage_all[wid];
+  if (w0 < n_leaves) {
+    const uint32_t w = order ? order[pos0 + w0] : w0;
+    const uint32_t L = leaf0 + w;
+    const uint32_t b = pt_off[L], e = pt_off[L + 1];
+    const uint32_t q0 = cl_off[w], q1 = cl_off[w + 1];
+    const bool dev_leaf = L >= dev_l0 && L < dev_l1;
+    if (dev_leaf == bool(host_part)) return;  // the other launch's leaf (warp-uniform)
+    if (dev_leaf) {  // device memory, plain coalesced stores
+      for (uint32_t i = b + lane; i < e; i += 32) {
+        double2 v = tgt[i];
+        for (uint32_t q = q0; q < q1; ++q) {
+          const double2 c = contrib[cl_base[q] + (i - b)];
+          v.x += c.x;
+          v.y += c.y;
+        }
+        dev_out[i] = v;
+      }
+      return;  // (warp-uniform: no bulk store of this warp is pending)
+    }
+    for (uint32_t r0 = b; r0 < e; r0 += kFinStage) {
+      const uint32_t r1 = min(e, r0 + uint32_t(kFinStage));
+      if (r0 > b) {  // the previous round's store has read the staging area
+        if (lane == 0) bulk_wait_read();
+        __syncwarp();
+      }
+      for (uint32_t i = r0 + lane; i < r1; i += 32) {
+        double2 v = tgt[i];
+        for (uint32_t q = q0; q < q1; ++q) {
+          const double2 c = contrib[cl_base[q] + (i - b)];
+          v.x += c.x;
+          v.y += c.y;
+        }
+        stage[i - r0] = v;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) bulk_s2g(out + r0, stage, (r1 - r0) * 16u);
+    }
+  }
+  // exit once the stores have read the staging: the PCIe writes drain after
+  // the CTA is gone (its SM slot goes to the next group's kernels)
+  if (lane == 0) bulk_wait_read();
 }
 
 }  // namespace fmmcu

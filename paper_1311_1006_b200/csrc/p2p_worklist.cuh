@@ -280,6 +280,21 @@ static __global__ void wl_fill_kernel(const uint32_t* __restrict__ ev_off,
                 fins + fo[pos], po[pos], a, b, c);
 }
 
+// Grouped symmetric list: per upload group k, its first item and first leaf
+// position (positions in group order), from the sorted group keys.
+static __global__ void wls_bounds_kernel(const uint32_t* __restrict__ key_sorted, uint32_t np,
+                                         uint32_t K, const uint32_t* __restrict__ blk,
+                                         WlHead* __restrict__ head) {
+  const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos > np) return;
+  const int k0 = pos == 0 ? -1 : int(key_sorted[pos - 1]);
+  const int k1 = pos == np ? int(K) : int(key_sorted[pos]);
+  for (int k = k0 + 1; k <= k1; ++k) {
+    head->grp_item[k] = blk[pos];
+    head->grp_fin[k] = pos;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Symmetric (mutual-kernel) work list on the device: the host builder
 // build_sym_worklist (fmmcu.cu) restated as kernels, same entries, items and
@@ -293,6 +308,7 @@ struct WlSymHead {
   unsigned long long ent, items, slots;  // totals (from the scans)
   uint32_t bad;                          // a leaf does not qualify
   uint32_t pad;
+  unsigned long long ncl;  // contribution-list entries: sum of eval blocks x symmetric entries
 };
 
 static __global__ void wls_count_kernel(const uint32_t* __restrict__ ev_off,
@@ -304,29 +320,38 @@ static __global__ void wls_count_kernel(const uint32_t* __restrict__ ev_off,
                                         unsigned long long* __restrict__ ssym,
                                         unsigned long long* __restrict__ sord,
                                         unsigned long long* __restrict__ n_slot,
-                                        WlSymHead* __restrict__ sh) {
+                                        WlSymHead* __restrict__ sh,
+                                        const uint32_t* __restrict__ grp,
+                                        const uint32_t* __restrict__ order) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // output position
   const uint32_t np = le - lb;
-  if (i > np) return;
-  if (i == np) {  // the exclusive scans run over np + 1 entries
+  if (p > np) return;
+  if (p == np) {  // the exclusive scans run over np + 1 entries
     if (lane == 0) n_ent[np] = n_blk[np] = 0, n_slot[np] = 0ull;
     return;
   }
+  const uint32_t i = order ? order[p] : p;  // grouped: positions in group order
   const uint32_t t = lb + i;
-  uint32_t n = 0;
+  uint32_t n = 0, nsym = 0;
   unsigned long long so = 0, ss = 0;
   for (uint32_t q = s_off[t] + lane; q < s_off[t + 1]; q += 32) {
     const uint32_t B = s_idx[q];
-    const bool inr = B >= lb && B < le;
+    // grouped: symmetric only inside the upload group
+    const bool inr = B >= lb && B < le && (!grp || grp[B - lb] == grp[i]);
     if (inr && B < t) continue;
     ++n;
-    if (inr && B > t) ss += seg[q].y;
-    else so += seg[q].y;
+    if (inr && B > t) {
+      ss += seg[q].y;
+      ++nsym;
+    } else {
+      so += seg[q].y;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     n += __shfl_xor_sync(kFull, n, o);
+    nsym += __shfl_xor_sync(kFull, nsym, o);
     so += __shfl_xor_sync(kFull, so, o);
     ss += __shfl_xor_sync(kFull, ss, o);
   }
@@ -336,11 +361,13 @@ static __global__ void wls_count_kernel(const uint32_t* __restrict__ ev_off,
     const uint32_t nb = ntl ? (ntl + max_ev - 1) / max_ev : 0u;
     if (n > uint32_t(kSymMaxEntries) || so + ss >= (1ull << 31)) atomicOr(&sh->bad, 1u);
     else if (n > uint32_t(kWarpMaxEntries)) atomicOr(&sh->bad, 2u);  // needs entry rounds
-    n_ent[i] = n;
-    n_blk[i] = nb;
-    ssym[i] = ss;
-    sord[i] = so;
-    n_slot[i] = (unsigned long long)nb * ss;
+    n_ent[p] = n;
+    n_blk[p] = nb;
+    ssym[p] = ss;
+    sord[p] = so;
+    n_slot[p] = (unsigned long long)nb * ss;
+    // each symmetric entry B of t puts t's nb eval blocks on B's list
+    if (nsym && nb) atomicAdd(&sh->ncl, (unsigned long long)nb * nsym);
   }
 }
 
@@ -356,19 +383,23 @@ static __global__ void wls_fill_kernel(const uint32_t* __restrict__ pt_off,
                                        const unsigned long long* __restrict__ sord,
                                        const unsigned long long* __restrict__ slots,
                                        uint4* __restrict__ sym_seg, P2PItem* __restrict__ items,
-                                       uint4* __restrict__ sym_info) {
+                                       uint4* __restrict__ sym_info,
+                                       const uint32_t* __restrict__ grp,
+                                       const uint32_t* __restrict__ order,
+                                       uint2* __restrict__ sym_cnt) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // position
   const uint32_t np = le - lb;
-  if (i > np) return;
-  if (i == np) {
-    if (lane == 0) sym_info[np] = make_uint4(ent[np], blk[np], uint32_t(slots[np]), 0u);
+  if (p > np) return;
+  if (p == np) {
+    if (lane == 0 && !order) sym_info[np] = make_uint4(ent[np], blk[np], uint32_t(slots[np]), 0u);
     return;
   }
+  const uint32_t i = order ? order[p] : p;
   const uint32_t t = lb + i;
   const unsigned below = (1u << lane) - 1u;
   // entries: ordered runs first, then symmetric, each in strong-list order
-  uint32_t o = ent[i];
+  uint32_t o = ent[p];
   for (int pass = 0; pass < 2; ++pass) {
     for (uint32_t q0 = s_off[t]; q0 < s_off[t + 1]; q0 += 32) {
       const uint32_t q = q0 + lane;
@@ -376,7 +407,7 @@ static __global__ void wls_fill_kernel(const uint32_t* __restrict__ pt_off,
       uint32_t kind = kRunOrdered, B = 0;
       if (q < s_off[t + 1]) {
         B = s_idx[q];
-        const bool inr = B >= lb && B < le;
+        const bool inr = B >= lb && B < le && (!grp || grp[B - lb] == grp[i]);
         const bool sym = inr && B > t;
         take = !(inr && B < t) && (sym == (pass == 1));
         kind = sym ? kRunSym : (B == t ? kRunSelf : kRunOrdered);
@@ -391,15 +422,19 @@ static __global__ void wls_fill_kernel(const uint32_t* __restrict__ pt_off,
   }
   if (lane == 0) {
     const uint32_t ntl = ev_off[t + 1] - ev_off[t];
-    const uint32_t nb = blk[i + 1] - blk[i];
-    const unsigned long long ss = ssym[i], so = sord[i];
+    const uint32_t nb = blk[p + 1] - blk[p];
+    const unsigned long long ss = ssym[p], so = sord[p];
     for (uint32_t b = 0, e0 = 0; b < nb; ++b) {
       const uint32_t nt = (ntl - e0) / (nb - b) + ((ntl - e0) % (nb - b) ? 1u : 0u);
-      items[blk[i] + b] = P2PItem{t, ev_off[t] + e0, nt, ent[i], ent[i + 1], uint32_t(so + ss),
-                                  uint32_t(slots[i] + (unsigned long long)b * ss), uint32_t(so)};
+      items[blk[p] + b] = P2PItem{t, ev_off[t] + e0, nt, ent[p], ent[p + 1], uint32_t(so + ss),
+                                  uint32_t(slots[p] + (unsigned long long)b * ss), uint32_t(so)};
       e0 += nt;
     }
-    sym_info[i] = make_uint4(ent[i], blk[i], uint32_t(slots[i]), uint32_t(ss));
+    // per leaf (leaf order): first entry / item / slot, symmetric sources;
+    // grouped lists also need the counts (consecutive leaves are not
+    // consecutive positions)
+    sym_info[i] = make_uint4(ent[p], blk[p], uint32_t(slots[p]), uint32_t(ss));
+    if (sym_cnt) sym_cnt[i] = make_uint2(ent[p + 1] - ent[p], nb);
   }
   (void)pt_off;
   (void)head;

@@ -170,15 +170,43 @@ int build_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g
 // the job does not qualify (a leaf with more than 32 entries, or too many
 // contribution slots): the caller then builds the ordinary list.  Two small
 // header reads synchronize `s`.
-int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t s) {
+//
+// Upload groups (gp->K > 1, the overlapped launch): a pair is symmetric only
+// when both leaves are in the same group (the group of a leaf is the upload
+// chunk of the last source slot its strong list reads, wl_leaf_kernel), so
+// group k's items read chunks <= k only and its finalize needs only its own
+// items; cross-group partners run as ordered pairs from both sides.  Items
+// are laid out in group order (a stable sort of the leaves by group, as
+// build_worklist_dev); c->dev_grp_item / dev_grp_fin hold each group's
+// first item and first leaf position, and the positions -> leaves map stays
+// in d_wl_val for the finalize.
+int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t s,
+                           const WlGroups* gp) {
   const uint32_t np = le - lb;
   WlGroups g{};
   g.K = 1;
+  if (gp) g = *gp;
+  const uint32_t K = g.K ? g.K : 1u;
+  const bool grouped = K > 1;
   int nk = 0;
   size_t need = 0;
   if (int rc = wl_prepare(c, lb, le, g, s, nk, need)) return rc;
   const size_t n1 = size_t(np) + 1;
   WlHead* head = c->d_wl_head.as<WlHead>();
+  // grouped: leaves stably ordered by group; grp = group per leaf (leaf order)
+  const uint32_t* grp = nullptr;
+  const uint32_t* order = nullptr;
+  const uint32_t* key_sorted = nullptr;
+  if (grouped && np) {
+    uint32_t* key = c->d_wl_key.as<uint32_t>();
+    uint32_t* val = c->d_wl_val.as<uint32_t>();
+    size_t tb = need;
+    CU_TRY(c, cub::DeviceRadixSort::SortPairs(c->d_cubtmp.p, tb, key, key + n1, val, val + n1,
+                                              int64_t(np), 0, 5, s));
+    grp = key;
+    key_sorted = key + n1;
+    order = val + n1;
+  }
   auto rup = [](size_t b) { return (b + 255) & ~size_t(255); };
   CU_TRY(c, c->d_wls.ensure(256 + 4 * rup(n1 * 4) + 4 * rup(n1 * 8)));
   char* base = c->d_wls.as<char>();
@@ -206,7 +234,7 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   const uint2* seg = c->d_seg.as<uint2>();
   wls_count_kernel<<<nblocks(uint64_t(n1) * 32, 256), 256, 0, s>>>(ev, so, si, seg, lb, le, head,
                                                                   n_ent, n_blk, ssym, sord, n_slot,
-                                                                  sh);
+                                                                  sh, grp, order);
   ++nk;
   size_t tb = 0;
   CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, tb, n_slot, slot, int64_t(n1), s));
@@ -220,16 +248,21 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   CU_TRY(c, cub::DeviceScan::ExclusiveSum(c->d_cubtmp.p, tb, n_blk, blk, int64_t(n1), s));
   tb = need;
   CU_TRY(c, cub::DeviceScan::ExclusiveSum(c->d_cubtmp.p, tb, n_slot, slot, int64_t(n1), s));
+  if (grouped && np) {
+    wls_bounds_kernel<<<nblocks(n1, 256), 256, 0, s>>>(key_sorted, np, K, blk, head);
+    ++nk;
+  }
   // totals + the qualification flag + the header (E)
   CU_TRY(c, c->h_wl_head.ensure(sizeof(WlHead) + 64));
   auto* hh = c->h_wl_head.as<char>();
   CU_TRY(c, cudaMemcpyAsync(hh, head, sizeof(WlHead), cudaMemcpyDeviceToHost, s));
   auto* tot = reinterpret_cast<uint64_t*>(hh + sizeof(WlHead));
-  for (int q = 0; q < 5; ++q) tot[q] = 0;  // 4-byte copies land in the low halves
+  for (int q = 0; q < 6; ++q) tot[q] = 0;  // 4-byte copies land in the low halves
   CU_TRY(c, cudaMemcpyAsync(&tot[0], ent + np, 4, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaMemcpyAsync(&tot[1], blk + np, 4, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaMemcpyAsync(&tot[2], slot + np, 8, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaMemcpyAsync(&tot[3], &sh->bad, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaMemcpyAsync(&tot[5], &sh->ncl, 8, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaStreamSynchronize(s));
   const WlHead h = *reinterpret_cast<const WlHead*>(hh);
   const uint64_t n_entries = tot[0], n_items = tot[1], n_slots = tot[2];
@@ -240,9 +273,14 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   CU_TRY(c, c->d_syminfo.ensure(n1 * 16));
   CU_TRY(c, c->d_contrib.ensure(std::max<uint64_t>(n_slots, 1) * 16));
   CU_TRY(c, c->d_tgt.ensure(size_t(std::max(c->n_eval, 1u)) * 16));
+  uint2* cnt = nullptr;
+  if (grouped) {
+    CU_TRY(c, c->d_symcnt.ensure(n1 * 8));
+    cnt = c->d_symcnt.as<uint2>();
+  }
   wls_fill_kernel<<<nblocks(uint64_t(n1) * 32, 256), 256, 0, s>>>(
       pt, ev, so, si, seg, lb, le, head, ent, blk, ssym, sord, slot, c->d_symseg.as<uint4>(),
-      c->d_items.as<P2PItem>(), c->d_syminfo.as<uint4>());
+      c->d_items.as<P2PItem>(), c->d_syminfo.as<uint4>(), grp, order, cnt);
   c->launches += 1;
   // per-leaf contribution lists (count, scan, fill), as stage_csr
   CU_TRY(c, c->d_cloff.ensure(n1 * 4));
@@ -252,24 +290,34 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   if (np)
     p2p_sym_lists_kernel<false><<<gb, 256, 0, s>>>(lb, np, pt, so, si, c->d_syminfo.as<uint4>(),
                                                    c->d_symseg.as<uint4>(),
-                                                   c->d_clcnt.as<uint32_t>(), nullptr, nullptr);
+                                                   c->d_clcnt.as<uint32_t>(), nullptr, nullptr,
+                                                   grp, cnt);
   tb = 0;
   CU_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, tb, c->d_clcnt.as<uint32_t>(),
                                           c->d_cloff.as<uint32_t>(), int64_t(n1), s));
   CU_TRY(c, c->d_cubtmp.ensure(tb));
   CU_TRY(c, cub::DeviceScan::ExclusiveSum(c->d_cubtmp.p, tb, c->d_clcnt.as<uint32_t>(),
                                           c->d_cloff.as<uint32_t>(), int64_t(n1), s));
-  CU_TRY(c, cudaMemcpyAsync(&tot[4], c->d_cloff.as<uint32_t>() + np, 4, cudaMemcpyDeviceToHost, s));
-  CU_TRY(c, cudaStreamSynchronize(s));
-  const uint32_t ncl = uint32_t(tot[4]);
+  // cl_base sized from the count kernel's total (no second header read)
+  if (tot[5] > 0xFFFFFFF0ull) return set_err(c, FMMCU_EINVAL, "contribution lists overflow");
+  const uint32_t ncl = uint32_t(tot[5]);
   CU_TRY(c, c->d_clbase.ensure(size_t(std::max(ncl, 1u)) * 4));
   if (np)
     p2p_sym_lists_kernel<true><<<gb, 256, 0, s>>>(lb, np, pt, so, si, c->d_syminfo.as<uint4>(),
                                                   c->d_symseg.as<uint4>(), nullptr,
                                                   c->d_cloff.as<uint32_t>(),
-                                                  c->d_clbase.as<uint32_t>());
+                                                  c->d_clbase.as<uint32_t>(), grp, cnt);
   CU_TRY(c, cudaGetLastError());
   c->launches += 3;
+  c->sym_grouped = grouped;
+  if (grouped) {
+    c->dev_grp_item.assign(h.grp_item, h.grp_item + K + 1);
+    c->dev_grp_fin.assign(h.grp_fin, h.grp_fin + K + 1);  // first leaf positions
+  } else {
+    c->dev_grp_item.assign({0u, uint32_t(n_items)});
+    c->dev_grp_fin.assign({0u, np});
+  }
+  c->sym_order = order;
   c->warp_e = int(h.E);
   c->warp_items = true;
   c->sym_items = true;
@@ -278,7 +326,7 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   c->sym_slots = n_slots;
   c->sym_n_items = uint32_t(n_items);
   c->sym_rounds = (tot[3] & 2u) != 0;
-  c->grouped = false;
+  c->grouped = grouped;
   c->partial_evals = 0;
   c->dev_wl = false;
   c->dev_list = true;

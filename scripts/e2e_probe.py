@@ -16,6 +16,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=10_000_000)
 ap.add_argument("--levels", type=int, default=10)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--pageable-out", action="store_true",
+                help="leave the output pageable (device buffer + copy in finish)")
 a = ap.parse_args()
 s = F.make_distribution("uniform", a.n, 4)
 e = F.EvalSet.self_of(s)
@@ -24,7 +26,7 @@ zp, mp, yp, sid = t.permuted()
 pt, ev, so, si = t.leaf_csr()
 ctx = N.CudaContext(0)
 out = np.zeros((len(zp), 2))
-for arr in (out, zp, mp, pt, ev, so, si):
+for arr in ((zp, mp, pt, ev, so, si) if a.pageable_out else (out, zp, mp, pt, ev, so, si)):
     ctx.host_register(arr)
 ts = []
 for r in range(3 if a.reps > 2 else 0):  # split: make_job / launch / finish

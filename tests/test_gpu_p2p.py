@@ -143,7 +143,15 @@ def test_heavy_leaves_are_split_and_reduced(ctx):
     assert bitwise(out, out2)  # deterministic
 
 
-def test_leaf_shards_compose_to_the_full_result(ctx):
+@pytest.mark.parametrize("ordered", [True, False])
+def test_leaf_shards_compose_to_the_full_result(ctx, ordered, monkeypatch):
+    """Leaf-range launches compose to the whole job: bitwise with the ordered
+    list; with the mutual kernel (FMMCU_E2E_SYM=1) pairs across a shard cut
+    run ordered, so the bar is 1e-12 normwise -- and exact pair counts."""
+    if ordered:
+        monkeypatch.setenv("FMMCU_NO_SYM", "1")
+    else:
+        monkeypatch.setenv("FMMCU_E2E_SYM", "1")
     t, args = _tree_case(0, 120_000, 7, 12)
     full, pairs_full, _ = _run(ctx, *args)
     nl = len(args[0]) - 1
@@ -156,7 +164,10 @@ def test_leaf_shards_compose_to_the_full_result(ctx):
         acc[e0:e1] = out[e0:e1]
         tot += pairs
     assert tot == pairs_full
-    assert bitwise(acc, full)
+    if ordered:
+        assert bitwise(acc, full)
+    else:
+        assert normwise(acc, full) <= TOL_FP64
 
 
 def test_staged_device_path_matches_launch(ctx):
@@ -205,7 +216,8 @@ def test_linearity_at_scale(ctx):
 def test_sliced_launch_direct_into_registered_output(ctx):
     """n_eval > 2^20: the launch runs 8 pair-balanced leaf slices whose D2H
     overlaps the next slice.  Staged and page-locked (direct DMA) outputs,
-    a shard spanning slices and the device-resident path all agree bitwise."""
+    and the device-resident path agree bitwise, a shard spanning slices to
+    1e-12 (its cross-cut pairs run ordered)."""
     t, args = _tree_case(0, 1_500_000, 8, 6)
     staged, p_staged, _ = _run(ctx, *args)
     host = np.full_like(staged, np.nan)
@@ -220,7 +232,8 @@ def test_sliced_launch_direct_into_registered_output(ctx):
     a, b = nl // 5, nl - nl // 7
     part, _, _ = _run(ctx, *args, leaf_begin=a, leaf_end=b)
     e0, e1 = int(args[1][a]), int(args[1][b])
-    assert bitwise(part[e0:e1], staged[e0:e1])
+    # (mutual kernel: pairs across the shard cut run ordered -> 1e-12, not bitwise)
+    assert normwise(part[e0:e1], staged[e0:e1]) <= TOL_FP64
     job, keep = N.CudaContext.make_job(*args, None)
     ctx.stage(job, keep)
     ctx.run_staged(0, nl)
@@ -319,8 +332,13 @@ def test_symmetric_kernel_vs_oracle(ctx, case):
     assert normwise(part[e0:e1], want[e0:e1]) <= TOL_FP64
     # a symmetric list staged for [a, b) must refuse another range (its
     # contribution slots only cover pairs inside [a, b)); an ordinary list
-    # (clustered inputs exceed 32 entries per leaf) runs any range exactly
+    # (a leaf of the range with more than 256 entries once its in-range lower
+    # partners are dropped: the clustered case) runs any range exactly
+    so, si = args[2], args[3]
+    most = max(int(((r < a) | (r >= i)).sum()) for i in range(a, b)
+               for r in [si[so[i]:so[i + 1]]])
     sym, _ = ctx.kernel_info()
+    assert sym == (most <= 256)
     if sym:
         with pytest.raises(N.FmmcuError) as ei:
             ctx.run_staged(0, nl)
@@ -329,7 +347,7 @@ def test_symmetric_kernel_vs_oracle(ctx, case):
         ctx.run_staged(0, nl)
         assert ctx.pairs() == wpairs
         assert normwise(ctx.copy_out(len(want)), want) <= TOL_FP64
-    # uniform inputs (<= 32 strong entries per leaf) always take the mutual kernel
+    # uniform inputs always take the mutual kernel
     if kind == 0:
         assert sym
 
@@ -389,6 +407,9 @@ def test_device_work_list_equals_host_work_list(ctx, pinned, monkeypatch):
     the host builder.  Same items in the same order: bitwise equal potentials
     and equal pair counts for whole jobs, leaf shards (halo-only uploads) and
     split heavy leaves, with pageable and page-locked inputs."""
+    # the ordered list on both sides (self-evaluation jobs would otherwise
+    # take the grouped mutual list: test_launch_mutual_kernel_grouped)
+    monkeypatch.setenv("FMMCU_NO_SYM", "1")
     cases = [_tree_case(0, 1_500_000, 8, 41)[1], _tree_case(2, 300_000, 8, 3)[1],
              _tree_case(3, 80_000, 6, 42, self_eval=False, n_eval=50_000)[1]]
     for args in cases:
@@ -413,3 +434,57 @@ def test_device_work_list_equals_host_work_list(ctx, pinned, monkeypatch):
         finally:
             for a in reg:
                 ctx.host_unregister(a)
+
+
+def test_launch_mutual_kernel_grouped(ctx, monkeypatch):
+    """FMMCU_E2E_SYM=1: self-evaluation through fmmcu_p2p_launch (the e2e
+    path) runs the mutual kernel on a list grouped by upload chunk
+    (worklist_dev.cu, build_sym_worklist_dev with groups): pairs inside a
+    group once, across groups ordered; each group's finalize stores its own
+    chunk to device memory for a copy-engine D2H and the other leaves
+    straight into the host output.  Against the ordered launch: equal pair
+    counts, <= 1e-12 normwise; deterministic; page-locked and pageable
+    inputs; more than 32 entries per leaf (entry rounds); and a job whose
+    first ids match their sources but a later chunk does not falls back to
+    the ordered list (bitwise equal to it)."""
+    monkeypatch.setenv("FMMCU_E2E_SYM", "1")
+    for kind, n, L, seed, theta in ((0, 2_500_000, 9, 51, 0.5), (0, 1_200_000, 8, 52, 0.2),
+                                    (2, 1_500_000, 8, 53, 0.5)):
+        t, args = _tree_case(kind, n, L, seed, theta=theta)
+        args = list(args)
+        for pinned in (False, True):
+            reg = []
+            if pinned:
+                args[5] = np.ascontiguousarray(args[5]).copy()
+                args[6] = np.ascontiguousarray(args[6]).copy()
+                reg = [args[5], args[6]]
+                for a in reg:
+                    ctx.host_register(a)
+            try:
+                a1, p1, _ = _run(ctx, *args)
+                sym, _ = ctx.kernel_info()
+                a2, p2, _ = _run(ctx, *args)
+                monkeypatch.setenv("FMMCU_NO_SYM", "1")
+                want, pw, _ = _run(ctx, *args)
+                monkeypatch.delenv("FMMCU_NO_SYM")
+            finally:
+                for a in reg:
+                    ctx.host_unregister(a)
+            if kind == 0:
+                assert sym
+            assert p1 == pw and p2 == pw
+            assert bitwise(a1, a2)
+            assert normwise(a1, want) <= TOL_FP64
+    # fallback: the positions of one point in the second upload chunk moved
+    t, args = _tree_case(0, 2_500_000, 9, 54)
+    args = list(args)
+    yp = np.array(args[7], copy=True)
+    yp.reshape(-1)[2 * 1_600_000] += 1e-9
+    args[7] = yp
+    got, pg, _ = _run(ctx, *args)
+    assert not ctx.kernel_info()[0]
+    monkeypatch.setenv("FMMCU_NO_SYM", "1")
+    want, pw, _ = _run(ctx, *args)
+    monkeypatch.delenv("FMMCU_NO_SYM")
+    assert pg == pw
+    assert bitwise(got, want)
