@@ -282,17 +282,25 @@ int validate(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
 // indices in range.  launch_overlapped runs it while the first copies move.
 int validate_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   const uint32_t nl = j->n_leaves;
-  bool mono = true;
-#pragma omp parallel for schedule(static) reduction(&& : mono)
-  for (int64_t i = 0; i < int64_t(nl); ++i)
-    mono = mono && j->pt_off[i] <= j->pt_off[i + 1] && j->ev_off[i] <= j->ev_off[i + 1] &&
-           j->strong_off[i] <= j->strong_off[i + 1];
-  if (!mono) return set_err(c, FMMCU_EINVAL, "leaf offsets not monotone");
   const uint32_t nnz = j->strong_off[nl];
-  bool in_range = true;
-#pragma omp parallel for schedule(static) reduction(&& : in_range)
-  for (int64_t q = 0; q < int64_t(nnz); ++q) in_range = in_range && j->strong_idx[q] < nl;
-  if (!in_range) return set_err(c, FMMCU_EINVAL, "strong index out of range");
+  const uint32_t* pt = j->pt_off;
+  const uint32_t* ev = j->ev_off;
+  const uint32_t* so = j->strong_off;
+  const uint32_t* si = j->strong_idx;
+  // one parallel region, branch-free (vectorised) reductions: a descent in
+  // any offset array, and the largest strong index
+  uint32_t desc = 0, top = 0;
+#pragma omp parallel reduction(| : desc) reduction(max : top)
+  {
+#pragma omp for schedule(static) nowait
+    for (int64_t i = 0; i < int64_t(nl); ++i)
+      desc |= uint32_t(pt[i] > pt[i + 1]) | uint32_t(ev[i] > ev[i + 1]) |
+              uint32_t(so[i] > so[i + 1]);
+#pragma omp for schedule(static) nowait
+    for (int64_t q = 0; q < int64_t(nnz); ++q) top = std::max(top, si[q]);
+  }
+  if (desc) return set_err(c, FMMCU_EINVAL, "leaf offsets not monotone");
+  if (nnz && top >= nl) return set_err(c, FMMCU_EINVAL, "strong index out of range");
   return FMMCU_OK;
 }
 
@@ -1379,15 +1387,21 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     if (direct_in) {
       if (k >= pre)
         if (int rc = dma(c0, c1)) return rc;
+      // branch-free (vectorised) reductions: a short-circuit && does not vectorise
+      const int64_t* sid = j->eval_sid;
+      const uint32_t* pm = j->perm;
+      const double* ey = j->eval_y;
+      uint32_t diff = 0;
       if (maybe_self && y_is_z) {  // the positions are the same array: ids only
-#pragma omp parallel for schedule(static) reduction(&& : same)
-        for (int64_t i = c0; i < c1; ++i) same = same && j->eval_sid[i] == int64_t(j->perm[i]);
+#pragma omp parallel for schedule(static) reduction(| : diff)
+        for (int64_t i = c0; i < c1; ++i) diff |= uint32_t(sid[i] != int64_t(pm[i]));
       } else if (maybe_self) {
-#pragma omp parallel for schedule(static) reduction(&& : same)
+#pragma omp parallel for schedule(static) reduction(| : diff)
         for (int64_t i = c0; i < c1; ++i)
-          same = same && j->eval_sid[i] == int64_t(j->perm[i]) &&
-                 j->eval_y[2 * i] == z[2 * i] && j->eval_y[2 * i + 1] == z[2 * i + 1];
+          diff |= uint32_t(sid[i] != int64_t(pm[i])) | uint32_t(ey[2 * i] != z[2 * i]) |
+                  uint32_t(ey[2 * i + 1] != z[2 * i + 1]);
       }
+      same = same && diff == 0;
     } else {
 #pragma omp parallel for schedule(static) reduction(&& : same)
       for (int64_t i = c0; i < c1; ++i) {
