@@ -36,4 +36,8 @@ std::vector<cplx> vortex_velocities(const VortexSystem& sys, FmmEngine& engine,
 
 void euler_step(VortexSystem& sys, const std::vector<cplx>& velocities);
 
+// euler_step(sys, vortex_velocities(sys, engine)) fused: same positions,
+// without materialising the velocity vector (time-stepping drivers).
+void vortex_step(VortexSystem& sys, FmmEngine& engine);
+
 }  // namespace fmm::sims

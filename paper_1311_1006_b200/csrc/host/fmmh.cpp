@@ -444,7 +444,7 @@ int fmmh_vortex_run(int n, double aspect, int steps, int tuner, double cap, uint
         e.set_config(nc);
       }
     });
-    for (int s = 0; s < steps; ++s) sims::euler_step(sys, sims::vortex_velocities(sys, engine));
+    for (int s = 0; s < steps; ++s) sims::vortex_step(sys, engine);
     if (final_pos) std::memcpy(final_pos, sys.pos.data(), sys.pos.size() * 16);
   });
 }

@@ -1,5 +1,8 @@
 // fmm-b200 — vortex-sheet driver (reference proj/src/sims.cpp:13-89).
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 
 #include "fmm/sims.hpp"
@@ -32,6 +35,7 @@ struct StepBuffers {
   EvalResult r;
   void* p[4] = {};
   std::size_t b[4] = {};
+  std::int64_t ids_n = -1;  // ev.source_id holds 0..ids_n-1
   ~StepBuffers() { unpin(); }
   void unpin() {
     for (int i = 0; i < 4; ++i) {
@@ -97,12 +101,10 @@ VortexSystem init_shear_layer(int n, double aspect, double gamma) {
   return sys;
 }
 
-std::vector<cplx> vortex_velocities(const VortexSystem& sys, FmmEngine& engine, EvalResult* info) {
-  if (sys.size() == 0) return {};
-  if (sys.size() == 1) {
-    if (info) *info = EvalResult{};
-    return {cplx(0, 0)};
-  }
+namespace {
+// Sources / self evals of the system in the thread's step buffers, then one
+// evaluation into B.r (shared by vortex_velocities and vortex_step).
+StepBuffers& evaluate_system(const VortexSystem& sys, FmmEngine& engine) {
   use_vortex_kernel(engine, sys.delta);
   // Time stepping evaluates one problem size over and over: the sources, the
   // (self) evals and the result live in per-thread buffers that are refilled
@@ -122,24 +124,61 @@ std::vector<cplx> vortex_velocities(const VortexSystem& sys, FmmEngine& engine, 
   src.z.resize(n);
   src.m.resize(n);
   ev.y.resize(n);
+  // the ids are 0..n-1 every step: rewritten only when the size changes
+  const bool ids = B.ids_n != n || ev.source_id.size() != std::size_t(n);
   ev.source_id.resize(n);
   if (cuda) {
     r.potentials.resize(n);  // evaluate_into keeps storage of the right size
     B.pin();
   }
+  int64_t* sid = ev.source_id.data();
 #pragma omp parallel for schedule(static)
   for (std::int64_t k = 0; k < n; ++k) {
     src.z[k] = sys.pos[k];
     src.m[k] = sys.gamma[k] * kOneOverTwoPiI;
     ev.y[k] = sys.pos[k];
-    ev.source_id[k] = k;
+    if (ids) sid[k] = k;
   }
+  B.ids_n = n;
   engine.evaluate_into(src, ev, r);
+  return B;
+}
+}  // namespace
+
+std::vector<cplx> vortex_velocities(const VortexSystem& sys, FmmEngine& engine, EvalResult* info) {
+  if (sys.size() == 0) return {};
+  if (sys.size() == 1) {
+    if (info) *info = EvalResult{};
+    return {cplx(0, 0)};
+  }
+  const EvalResult& r = evaluate_system(sys, engine).r;
+  const std::int64_t n = std::int64_t(sys.size());
   std::vector<cplx> v(n);
 #pragma omp parallel for schedule(static)
   for (std::int64_t k = 0; k < n; ++k) v[k] = std::conj(r.potentials[k]);
   if (info) *info = r;
   return v;
+}
+
+// euler_step(sys, vortex_velocities(sys, engine)) without the velocity
+// vector (a fresh 16 B/vortex allocation, zero-filled by one thread, every
+// step): pos += dt * conj(potential), the same arithmetic.
+void vortex_step(VortexSystem& sys, FmmEngine& engine) {
+  if (sys.size() < 2) return;  // one vortex: zero velocity
+  static const bool trace = std::getenv("FMM_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  const EvalResult& r = evaluate_system(sys, engine).r;
+  const auto t1 = std::chrono::steady_clock::now();
+  const std::int64_t n = std::int64_t(sys.size());
+  const cplx* pot = r.potentials.data();
+#pragma omp parallel for schedule(static)
+  for (std::int64_t k = 0; k < n; ++k) sys.pos[k] += sys.dt * std::conj(pot[k]);
+  if (trace) {
+    const auto t2 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[fmm] vortex step: fill+evaluate %.2f ms (t_total %.2f), update %.2f ms\n",
+                 ms(t0, t1), 1e3 * r.timings.t_total, ms(t1, t2));
+  }
 }
 
 void euler_step(VortexSystem& sys, const std::vector<cplx>& velocities) {
