@@ -311,25 +311,43 @@ __global__ void __launch_bounds__(kPartTB)
     Prefix op(ts, prefix_tmp, cuda::std::plus<uint32_t>{}, tile);
     BlockScan(scan_tmp).ExclusiveSum(cnt, excl, op);
   }
+  // Destinations in the blocked layout, then an exchange through shared
+  // memory so that each store instruction covers 32 consecutive elements of
+  // the tile (runs of consecutive destinations) instead of 32 elements 8
+  // apart: the L1 wavefronts of the scattered stores bound this kernel.
+  // (slot i + i/8: conflict-free 8-byte accesses both ways)
+  __shared__ uint2 xch[kPartTB * kPartIPT + kPartTB * kPartIPT / 8];
+  __shared__ uint8_t xfl[kPartTB * kPartIPT];
 #pragma unroll
   for (int k = 0; k < kPartIPT; ++k) {
     const uint32_t i = i0 + k;
+    const uint32_t li = threadIdx.x * kPartIPT + k;
     if (i >= n) break;
     const uint32_t g = sg[k], b = off[g];
     const uint32_t rl = excl - lowbase[g];  // lows of this segment before i
     const bool lo = (lowmask >> k) & 1u;
     const uint32_t m = mid[g];
     const uint32_t dst = lo ? b + rl : m + (i - b - rl);
-    out[dst] = id[k];
-    if (FLAGS) {
-      if (flag_out) {
-        const uint32_t cb = lo ? b : m, cn = lo ? m - b : off[g + 1] - m;
-        flag_out[id[k]] = dst < cb + (cn + 1) / 2 ? 1 : 0;
-      }
-    } else {
-      pos_self[id[k]] = dst;
+    xch[li + (li >> 3)] = make_uint2(dst, id[k]);
+    if (FLAGS && flag_out) {
+      const uint32_t cb = lo ? b : m, cn = lo ? m - b : off[g + 1] - m;
+      xfl[li] = dst < cb + (cn + 1) / 2 ? 1 : 0;
     }
     excl += lo ? 1u : 0u;
+  }
+  __syncthreads();
+  const uint32_t tile0 = uint32_t(tile) * (kPartTB * kPartIPT);
+#pragma unroll
+  for (int k = 0; k < kPartIPT; ++k) {
+    const uint32_t li = uint32_t(k) * kPartTB + threadIdx.x;
+    if (tile0 + li >= n) break;
+    const uint2 e = xch[li + (li >> 3)];
+    out[e.x] = e.y;
+    if (FLAGS) {
+      if (flag_out) flag_out[e.y] = xfl[li];
+    } else {
+      pos_self[e.y] = e.x;
+    }
   }
 }
 
