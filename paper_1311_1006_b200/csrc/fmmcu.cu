@@ -1131,6 +1131,35 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // (~1.5 ms at 10M) with the first kPre chunks moving meanwhile, the CSR and
   // work list queued behind those only.
   const bool dev_list = !std::getenv("FMMCU_HOST_WL");
+  // self layout per chunk requires eval slot e == source slot e
+  const bool maybe_self = j->eval_sid && ne == ns && ns > 0 &&
+                          std::memcmp(j->ev_off, j->pt_off, size_t(nl + 1) * 4) == 0;
+  // the per-chunk self check reads 44 B per point, which paces the chunks at
+  // host memory speed; a caller passing one array for both positions saves
+  // the 32 B position comparison
+  const bool y_is_z = j->eval_y == j->src_z;
+  // slots [c0, c1) are self layout (ids and positions), branch-free
+  // (vectorised) reductions: a short-circuit && does not vectorise
+  auto self_check = [&](int64_t c0, int64_t c1) -> bool {
+    const int64_t* sid = j->eval_sid;
+    const uint32_t* pm = j->perm;
+    const double* ey = j->eval_y;
+    const double* zz = j->src_z;
+    uint32_t diff = 0;
+    if (y_is_z) {  // the positions are the same array: ids only
+#pragma omp parallel for schedule(static) reduction(| : diff)
+      for (int64_t i = c0; i < c1; ++i) diff |= uint32_t(sid[i] != int64_t(pm[i]));
+    } else {
+#pragma omp parallel for schedule(static) reduction(| : diff)
+      for (int64_t i = c0; i < c1; ++i)
+        diff |= uint32_t(sid[i] != int64_t(pm[i])) | uint32_t(ey[2 * i] != zz[2 * i]) |
+                uint32_t(ey[2 * i + 1] != zz[2 * i + 1]);
+    }
+    return diff == 0;
+  };
+  // chunk 0's check runs while the work-list header is in flight (whole
+  // jobs with page-locked inputs: one run per chunk)
+  int self0 = -1;  // -1: not checked yet
   // FMMCU_E2E_SYM=1: the grouped mutual list for self-evaluation.  Off by
   // default: the launch is PCIe bound (H2D + D2H share the link, ~75 GB/s
   // together), the ordered kernels store each result over PCIe while they
@@ -1186,8 +1215,16 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
       rc_sym = build_sym_worklist_dev(c, lb, le, s, &g);
       if (rc_sym != FMMCU_OK && rc_sym != -1) return rc_sym;
     }
-    if (rc_sym != FMMCU_OK)
-      if (int rc = build_worklist_dev(c, lb, le, g, s)) return rc;  // + the run table
+    if (rc_sym != FMMCU_OK) {
+      const bool pre0 = maybe_self && direct_in && lb == 0 && le == nl && K > 0;
+      auto check0 = [&] {
+        self0 = self_check(int64_t(j->pt_off[c->chunk_leaf[0]]),
+                           int64_t(j->pt_off[c->chunk_leaf[1]])) ? 1 : 0;
+      };
+      if (int rc = build_worklist_dev(c, lb, le, g, s,
+                                      pre0 ? std::function<void()>(check0) : std::function<void()>()))
+        return rc;  // + the run table
+    }
     tr.mark("csr + device worklist");
   } else {
     pre = direct_in ? std::min(K, std::max(0, kPre)) : 0;
@@ -1211,13 +1248,6 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   tr.mark("csr");
   double2* hy = c->h_evy.as<double2>();
   uint32_t* hself = c->h_eself.as<uint32_t>();
-  // self layout per chunk requires eval slot e == source slot e
-  const bool maybe_self = j->eval_sid && ne == ns && ns > 0 &&
-                          std::memcmp(j->ev_off, j->pt_off, size_t(nl + 1) * 4) == 0;
-  // the per-chunk self check reads 44 B per point, which paces the chunks at
-  // host memory speed; a caller passing one array for both positions saves
-  // the 32 B position comparison
-  const bool y_is_z = j->eval_y == j->src_z;
   bool all_self = maybe_self;
   // eval arrays of slots [e0, e1) on the host (non-self chunks / layouts)
   bool inv_ready = false;
@@ -1387,21 +1417,7 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
     if (direct_in) {
       if (k >= pre)
         if (int rc = dma(c0, c1)) return rc;
-      // branch-free (vectorised) reductions: a short-circuit && does not vectorise
-      const int64_t* sid = j->eval_sid;
-      const uint32_t* pm = j->perm;
-      const double* ey = j->eval_y;
-      uint32_t diff = 0;
-      if (maybe_self && y_is_z) {  // the positions are the same array: ids only
-#pragma omp parallel for schedule(static) reduction(| : diff)
-        for (int64_t i = c0; i < c1; ++i) diff |= uint32_t(sid[i] != int64_t(pm[i]));
-      } else if (maybe_self) {
-#pragma omp parallel for schedule(static) reduction(| : diff)
-        for (int64_t i = c0; i < c1; ++i)
-          diff |= uint32_t(sid[i] != int64_t(pm[i])) | uint32_t(ey[2 * i] != z[2 * i]) |
-                  uint32_t(ey[2 * i + 1] != z[2 * i + 1]);
-      }
-      same = same && diff == 0;
+      if (maybe_self) same = (k == 0 && self0 >= 0) ? self0 == 1 : self_check(c0, c1);
     } else {
 #pragma omp parallel for schedule(static) reduction(&& : same)
       for (int64_t i = c0; i < c1; ++i) {

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "fmm_cuda.h"
@@ -366,7 +367,8 @@ int build_worklist(fmmcu_ctx* c, const fmmcu_p2p_job* j);
 // The job's CSR H2D on `stream` (in place when page-locked); returns the
 // bytes moved, ~0 on error.
 uint64_t upload_csr(fmmcu_ctx* c, const fmmcu_p2p_job* j, cudaStream_t stream);
-int build_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g, cudaStream_t s);
+int build_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g, cudaStream_t s,
+                       const std::function<void()>& while_waiting = {});
 // Symmetric (mutual-kernel) list + contribution lists on the device over
 // [lb, le) of the staged CSR (worklist_dev.cu); -1 = the job does not qualify.
 int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t s,

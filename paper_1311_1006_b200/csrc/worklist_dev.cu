@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <functional>
 
 #include "fmmcu_internal.cuh"
 #include "p2p_worklist.cuh"
@@ -91,7 +92,7 @@ int wl_prepare(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g, cudaSt
 }
 
 int build_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g,
-                       cudaStream_t s) {
+                       cudaStream_t s, const std::function<void()>& while_waiting) {
   const uint32_t np = le - lb;
   const uint32_t K = g.K ? g.K : 1u;
   int nk = 0;
@@ -135,6 +136,7 @@ int build_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, const WlGroups& g
   wl_bounds_kernel<<<nblocks(n1, 256), 256, 0, s>>>(ks, np, K, io, fo, po, head);
   ++nk;
   CU_TRY(c, cudaMemcpyAsync(c->h_wl_head.p, head, sizeof(WlHead), cudaMemcpyDeviceToHost, s));
+  if (while_waiting) while_waiting();  // host work overlapping the list build
   CU_TRY(c, cudaStreamSynchronize(s));
   const WlHead h = *c->h_wl_head.as<WlHead>();
   // the ordering key and val arrays stay valid for the fill
