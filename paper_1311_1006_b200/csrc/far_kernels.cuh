@@ -271,6 +271,22 @@ __global__ void pack_sources_kernel(const double2* __restrict__ z, const double2
   src[i] = make_double4(zz.x, zz.y, mm.x, mm.y);
 }
 
+// Self layout (evals are the sources, eval order == source order): the
+// packed sources and the eval arrays in one pass over the permutation (no
+// inverse permutation, no second gather): evy[i] = z[perm[i]], eself[i] = i.
+__global__ void pack_self_kernel(const double2* __restrict__ z, const double2* __restrict__ m,
+                                 const uint32_t* __restrict__ perm, uint32_t n,
+                                 double4* __restrict__ src, double2* __restrict__ evy,
+                                 uint32_t* __restrict__ eself) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t o = perm[i];
+  const double2 zz = z[o], mm = m[o];
+  src[i] = make_double4(zz.x, zz.y, mm.x, mm.y);
+  evy[i] = zz;
+  eself[i] = i;
+}
+
 __global__ void inverse_perm_kernel(const uint32_t* __restrict__ perm, uint32_t n,
                                     uint32_t* __restrict__ inv) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;

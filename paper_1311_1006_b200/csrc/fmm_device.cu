@@ -1275,9 +1275,16 @@ int fmm_launch_impl(fmmcu_ctx* c, const fmmcu_fmm_job* j, bool speculate, bool t
   CU_TRY(c, c->d_src.ensure(uint64_t(N) * 32));
   CU_TRY(c, c->d_evy.ensure(uint64_t(std::max(M, 1u)) * 16));
   CU_TRY(c, c->d_eself.ensure(uint64_t(std::max(M, 1u)) * 4));
-  pack_sources_kernel<<<blocks(N), TB, 0, s>>>(P->z.as<double2>(), P->m.as<double2>(),
-                                               P->perm.as<uint32_t>(), N, c->d_src.as<double4>());
-  if (M) {
+  if (self && P->layout_same && M == N) {
+    pack_self_kernel<<<blocks(N), TB, 0, s>>>(P->z.as<double2>(), P->m.as<double2>(),
+                                              P->perm.as<uint32_t>(), N, c->d_src.as<double4>(),
+                                              c->d_evy.as<double2>(), c->d_eself.as<uint32_t>());
+  } else {
+    pack_sources_kernel<<<blocks(N), TB, 0, s>>>(P->z.as<double2>(), P->m.as<double2>(),
+                                                 P->perm.as<uint32_t>(), N,
+                                                 c->d_src.as<double4>());
+  }
+  if (M && !(self && P->layout_same && M == N)) {
     inverse_perm_kernel<<<blocks(N), TB, 0, s>>>(P->perm.as<uint32_t>(), N, P->inv.as<uint32_t>());
     permute_evals_kernel<<<blocks(M), TB, 0, s>>>(
         self ? P->z.as<double2>() : P->y.as<double2>(),
