@@ -1164,7 +1164,7 @@ int launch_overlapped(fmmcu_ctx* c, const fmmcu_p2p_job* j) {
   // default: the launch is PCIe bound (H2D + D2H share the link, ~75 GB/s
   // together), the ordered kernels store each result over PCIe while they
   // compute, and the mutual list needs a finalize + copy-engine D2H per group
-  // after its kernel -- 10M / L10: 8.0-8.3 ms against 7.6-7.9 ms ordered
+  // after its kernel -- 10M / L10: 8.0-8.3 ms against 7.5-7.6 ms ordered
   // (e2e).
   const bool e2e_sym = std::getenv("FMMCU_E2E_SYM") != nullptr;
   bool sym_candidate = false;

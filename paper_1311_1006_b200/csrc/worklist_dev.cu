@@ -269,7 +269,9 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   const WlHead h = *reinterpret_cast<const WlHead*>(hh);
   const uint64_t n_entries = tot[0], n_items = tot[1], n_slots = tot[2];
   c->launches += uint64_t(nk);
-  if ((tot[3] & 1u) || n_slots > 0xFFFFFFF0ull || n_items > 0xFFFFFFF0ull) return -1;
+  if ((tot[3] & 1u) || n_slots > 0xFFFFFFF0ull || n_items > 0xFFFFFFF0ull ||
+      tot[5] > 0xFFFFFFF0ull)
+    return -1;
   CU_TRY(c, c->d_symseg.ensure(std::max<uint64_t>(n_entries, 1) * 16));
   CU_TRY(c, c->d_items.ensure(std::max<uint64_t>(n_items, 1) * sizeof(P2PItem)));
   CU_TRY(c, c->d_syminfo.ensure(n1 * 16));
@@ -301,7 +303,6 @@ int build_sym_worklist_dev(fmmcu_ctx* c, uint32_t lb, uint32_t le, cudaStream_t 
   CU_TRY(c, cub::DeviceScan::ExclusiveSum(c->d_cubtmp.p, tb, c->d_clcnt.as<uint32_t>(),
                                           c->d_cloff.as<uint32_t>(), int64_t(n1), s));
   // cl_base sized from the count kernel's total (no second header read)
-  if (tot[5] > 0xFFFFFFF0ull) return set_err(c, FMMCU_EINVAL, "contribution lists overflow");
   const uint32_t ncl = uint32_t(tot[5]);
   CU_TRY(c, c->d_clbase.ensure(size_t(std::max(ncl, 1u)) * 4));
   if (np)
