@@ -58,6 +58,14 @@ class CudaBackend final : public NearFieldBackend {
   M2LBuffers m2l_buffers(std::uint32_t n_boxes, int p, std::uint32_t n_targets, std::uint64_t nnz);
   void m2l_launch(int p, Kernel kernel, std::uint32_t n_boxes, std::uint32_t n_targets,
                   const M2LBuffers& b);
+  // Downward pass on the device (fmmcu_m2l_downward): launch with
+  // keep_on_device = true, then the L2L chain runs on the device and the
+  // finest level's locals land in finest_out ([boxes of the finest level][p+1],
+  // rows of boxes with a target slot) at m2l_finish.
+  void m2l_launch_keep(int p, Kernel kernel, std::uint32_t n_boxes, std::uint32_t n_targets,
+                       const M2LBuffers& b);
+  void m2l_downward(int n_levels, const std::uint32_t* level_base, const std::int32_t* target_of,
+                    cplx* finest_out);
 
   // The whole FmmEngine::evaluate on the first device (fmmcu_fmm_evaluate):
   // potentials in the original eval order, counters, device phase times.

@@ -169,6 +169,20 @@ typedef struct {
 } fmmcu_m2l_buffers;
 int fmmcu_m2l_host_buffers(fmmcu_ctx *ctx, uint32_t n_boxes, int p, uint32_t n_targets,
                            uint64_t nnz, fmmcu_m2l_buffers *bufs);
+/* Downward pass on the device after fmmcu_m2l_launch with job->out = NULL
+ * (the sums then stay on the device): level by level, the local expansion of
+ * every box with a target slot = l2l_add(parent local) (expansion.cpp,
+ * levels >= 2) + its M2L sum, as the reference's downward pass
+ * (engine.cpp:96-114); the locals of the finest level's boxes go to
+ * finest_out (row = box index within the finest level; rows of boxes without
+ * a slot are not written).  Completes with fmmcu_m2l_finish. */
+typedef struct {
+  int n_levels;
+  const uint32_t *level_base; /* [n_levels + 1] first global box id per level */
+  const int32_t *target_of;   /* [n_boxes] target slot of each box, or -1 */
+  double *finest_out;         /* [2 (p+1) boxes of the finest level] host */
+} fmmcu_l2l_job;
+int fmmcu_m2l_downward(fmmcu_ctx *ctx, const fmmcu_l2l_job *job);
 
 /* ---- the whole FMM evaluation on one device ------------------------------
  * FmmEngine::evaluate (reference engine.cpp:208-347) with every phase on the

@@ -152,7 +152,7 @@ CUDA_SYMBOLS = [
     "fmmcu_hypot_batch", "fmmcu_p2p_kernel_info",
     "fmmcu_p2p_out_ipc_handle", "fmmcu_p2p_bind_peer_out", "fmmcu_nccl_unique_id",
     "fmmcu_nccl_init", "fmmcu_nccl_gather_out", "fmmcu_m2l_host_buffers",
-    "fmmcu_pin_host", "fmmcu_unpin_host", "fmmcu_tree_build",
+    "fmmcu_pin_host", "fmmcu_unpin_host", "fmmcu_tree_build", "fmmcu_m2l_downward",
 ]
 IPC_HANDLE_BYTES = 64
 NCCL_ID_BYTES = 128

@@ -1590,6 +1590,120 @@ int fmmcu_fmm_tree_lists(fmmcu_ctx* c, int level, int weak, uint64_t* nnz, uint3
   return FMMCU_OK;
 }
 
+// Hybrid downward pass (fmmcu_m2l_downward): one level of locals from the
+// parents' locals and the batched M2L sums, arithmetic as local_kernel (and
+// so as the host's l2l_add + sum).  Boxes without a target slot have no
+// evals; neither have their children.
+__global__ void __launch_bounds__(kFarWarps * 32)
+    hybrid_local_kernel(const double2* __restrict__ center, const double* __restrict__ binom,
+                        int brow, int p, uint32_t base, uint32_t pbase, uint32_t nbox, int level,
+                        const int32_t* __restrict__ target_of, const double2* __restrict__ m2l,
+                        double2* __restrict__ loc) {
+  __shared__ double2 s_pow[kFarWarps][kFarMaxP1];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const uint32_t box = blockIdx.x * kFarWarps + w;
+  if (box >= nbox) return;
+  const uint32_t g = base + box;
+  const int32_t row = target_of[g];
+  if (row < 0) return;
+  const int P1 = p + 1;
+  double2 acc[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) acc[r] = make_double2(0.0, 0.0);
+  if (level >= 2) {
+    const uint32_t pg = pbase + (box >> 2);
+    const double2 s = cx_sub(center[g], center[pg]);
+    if (lane == 0) {
+      double2 v = make_double2(1.0, 0.0);
+      s_pow[w][0] = v;
+      for (int k = 1; k < P1; ++k) {
+        v = cx_mul(v, s);
+        s_pow[w][k] = v;
+      }
+    }
+    __syncwarp();
+    const double2* pc = loc + size_t(pg) * P1;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int l = r * 32 + lane;
+      if (l >= P1) break;
+      double2 t = make_double2(0.0, 0.0);
+      for (int k = l; k < P1; ++k)
+        t = cx_add(t, cx_mul(cx_scale(binom[size_t(k) * brow + l], s_pow[w][k - l]), pc[k]));
+      acc[r] = cx_add(acc[r], t);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int l = r * 32 + lane;
+    if (l >= P1) break;
+    acc[r] = cx_add(acc[r], m2l[size_t(row) * P1 + l]);
+    loc[size_t(g) * P1 + l] = acc[r];
+  }
+}
+
+int fmmcu_m2l_downward(fmmcu_ctx* c, const fmmcu_l2l_job* j) {
+  if (!c) return FMMCU_EINVAL;
+  if (!c->m2l_inflight || !c->m2l_keep)
+    return set_err(c, FMMCU_ESTATE, "m2l downward needs an m2l launch with out = NULL");
+  if (!j || j->n_levels < 1 || !j->level_base || !j->target_of)
+    return set_err(c, FMMCU_EINVAL, "bad downward job");
+  const fmmcu_m2l_job& m = c->m2l_job;
+  const int L = j->n_levels;
+  if (j->level_base[0] != 0 || j->level_base[L] != m.n_boxes)
+    return set_err(c, FMMCU_EINVAL, "level_base does not span the boxes");
+  for (int l = 0; l < L; ++l)
+    if (j->level_base[l] > j->level_base[l + 1])
+      return set_err(c, FMMCU_EINVAL, "level_base not monotone");
+  const uint32_t nb = m.n_boxes, nt = m.n_targets;
+  int32_t bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+  for (int64_t g = 0; g < int64_t(nb); ++g)
+    bad |= int32_t(j->target_of[g] >= int32_t(nt)) | int32_t(j->target_of[g] < -1);
+  if (bad) return set_err(c, FMMCU_EINVAL, "target_of out of range");
+  const uint32_t nfin = j->level_base[L] - j->level_base[L - 1];
+  if (nfin && !j->finest_out) return set_err(c, FMMCU_EINVAL, "null finest_out");
+  CU_TRY(c, cudaSetDevice(c->device));
+  const int p = m.p, P1 = p + 1;
+  cudaStream_t s = c->m2l_stream;
+  // binomials C(k, l) (the reference's Pascal rows: exact integers in double)
+  if (c->m_binom_host.size() != size_t(P1) * P1) {
+    c->m_binom_host.assign(size_t(P1) * P1, 0.0);
+    for (int k = 0; k < P1; ++k) {
+      c->m_binom_host[size_t(k) * P1] = 1.0;
+      for (int l = 1; l <= k; ++l)
+        c->m_binom_host[size_t(k) * P1 + l] =
+            c->m_binom_host[size_t(k - 1) * P1 + l - 1] +
+            (l <= k - 1 ? c->m_binom_host[size_t(k - 1) * P1 + l] : 0.0);
+    }
+  }
+  CU_TRY(c, c->m_binom.ensure(size_t(P1) * P1 * 8));
+  CU_TRY(c, c->m_tof.ensure(size_t(std::max(nb, 1u)) * 4));
+  CU_TRY(c, c->m_loc.ensure(size_t(std::max(nb, 1u)) * P1 * 16));
+  // host copies kept in the context: the (pageable) sources outlive the copies
+  c->m_tof_host.assign(j->target_of, j->target_of + nb);
+  CU_TRY(c, cudaMemcpyAsync(c->m_binom.p, c->m_binom_host.data(), size_t(P1) * P1 * 8,
+                            cudaMemcpyHostToDevice, s));
+  if (nb)
+    CU_TRY(c, cudaMemcpyAsync(c->m_tof.p, c->m_tof_host.data(), size_t(nb) * 4,
+                              cudaMemcpyHostToDevice, s));
+  for (int l = 1; l < L; ++l) {
+    const uint32_t base = j->level_base[l], nbox = j->level_base[l + 1] - base;
+    if (!nbox) continue;
+    hybrid_local_kernel<<<(nbox + kFarWarps - 1) / kFarWarps, kFarWarps * 32, 0, s>>>(
+        c->m_centers.as<double2>(), c->m_binom.as<double>(), P1, p, base, j->level_base[l - 1],
+        nbox, l, c->m_tof.as<int32_t>(), c->m_out.as<double2>(), c->m_loc.as<double2>());
+    c->launches += 1;
+  }
+  if (nfin && L >= 2)
+    CU_TRY(c, cudaMemcpyAsync(j->finest_out, c->m_loc.as<double2>() + size_t(j->level_base[L - 1]) * P1,
+                              size_t(nfin) * P1 * 16, cudaMemcpyDeviceToHost, s));
+  CU_TRY(c, cudaGetLastError());
+  CU_TRY(c, cudaEventRecord(c->ev_m2l1, s));  // fmmcu_m2l_finish waits for this
+  return FMMCU_OK;
+}
+
 int fmmcu_hypot_batch(fmmcu_ctx* c, const double* xy, uint32_t n, double* out) {
   if (!c || (n && (!xy || !out))) return FMMCU_EINVAL;
   if (!n) return FMMCU_OK;

@@ -2107,14 +2107,15 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
   const int P1 = j->p + 1;
   const uint32_t nb = j->n_boxes, nt = j->n_targets;
   const uint32_t nnz = nt ? j->weak_off[nt] : 0;
-  bool ok_t = true, ok_w = true;
-#pragma omp parallel for schedule(static) reduction(&& : ok_t)
+  // branch-free (vectorised) checks
+  uint32_t bad_t = 0, top_w = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad_t)
   for (int64_t t = 0; t < int64_t(nt); ++t)
-    ok_t = ok_t && j->target_box[t] < nb && j->weak_off[t] <= j->weak_off[t + 1];
-  if (!ok_t) return set_err(c, FMMCU_EINVAL, "bad m2l target list");
-#pragma omp parallel for schedule(static) reduction(&& : ok_w)
-  for (int64_t q = 0; q < int64_t(nnz); ++q) ok_w = ok_w && j->weak_idx[q] < nb;
-  if (!ok_w) return set_err(c, FMMCU_EINVAL, "bad m2l weak index");
+    bad_t |= uint32_t(j->target_box[t] >= nb) | uint32_t(j->weak_off[t] > j->weak_off[t + 1]);
+  if (bad_t) return set_err(c, FMMCU_EINVAL, "bad m2l target list");
+#pragma omp parallel for schedule(static) reduction(max : top_w)
+  for (int64_t q = 0; q < int64_t(nnz); ++q) top_w = std::max(top_w, j->weak_idx[q]);
+  if (nnz && top_w >= nb) return set_err(c, FMMCU_EINVAL, "bad m2l weak index");
   CU_TRY(c, c->m_centers.ensure(size_t(nb) * 16));
   CU_TRY(c, c->m_coeffs.ensure(size_t(nb) * P1 * 16));
   CU_TRY(c, c->m_tbox.ensure(size_t(nt) * 4));
@@ -2123,8 +2124,10 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
   CU_TRY(c, c->m_out.ensure(size_t(nt) * P1 * 16));
   CU_TRY(c, c->m_flag.ensure(8));
   CU_TRY(c, c->mh_flag.ensure(8));
-  c->m2l_direct_out = nt && host_locked(j->out, size_t(nt) * P1 * 16);
-  if (!c->m2l_direct_out) CU_TRY(c, c->mh_out.ensure(size_t(nt) * P1 * 16));
+  // out == NULL: the sums stay on the device for fmmcu_m2l_downward
+  c->m2l_keep = j->out == nullptr;
+  c->m2l_direct_out = nt && !c->m2l_keep && host_locked(j->out, size_t(nt) * P1 * 16);
+  if (!c->m2l_direct_out && !c->m2l_keep) CU_TRY(c, c->mh_out.ensure(size_t(nt) * P1 * 16));
   cudaStream_t s = c->m2l_stream;
   CU_TRY(c, cudaEventRecord(c->ev_m2l0, s));
   CU_TRY(c, cudaMemcpyAsync(c->m_centers.p, j->centers, size_t(nb) * 16, cudaMemcpyHostToDevice, s));
@@ -2148,8 +2151,9 @@ int fmmcu_m2l_launch(fmmcu_ctx* c, const fmmcu_m2l_job* j) {
     a.out = c->m_out.as<double2>();
     a.singular = c->m_flag.as<int>();
     if (int rc = m2l_run(c, a, nnz, s)) return rc;
-    CU_TRY(c, cudaMemcpyAsync(c->m2l_direct_out ? static_cast<void*>(j->out) : c->mh_out.p,
-                              c->m_out.p, size_t(nt) * P1 * 16, cudaMemcpyDeviceToHost, s));
+    if (!c->m2l_keep)
+      CU_TRY(c, cudaMemcpyAsync(c->m2l_direct_out ? static_cast<void*>(j->out) : c->mh_out.p,
+                                c->m_out.p, size_t(nt) * P1 * 16, cudaMemcpyDeviceToHost, s));
   }
   CU_TRY(c, cudaMemcpyAsync(c->mh_flag.p, c->m_flag.p, 4, cudaMemcpyDeviceToHost, s));
   CU_TRY(c, cudaEventRecord(c->ev_m2l1, s));
@@ -2192,7 +2196,7 @@ int fmmcu_m2l_finish(fmmcu_ctx* c, uint64_t* ops, double* seconds) {
   float ms = 0.f;
   CU_TRY(c, cudaEventElapsedTime(&ms, c->ev_m2l0, c->ev_m2l1));
   const int P1 = c->m2l_job.p + 1;
-  if (c->m2l_job.n_targets && !c->m2l_direct_out)
+  if (c->m2l_job.n_targets && !c->m2l_direct_out && !c->m2l_keep)
     par_memcpy(c->m2l_job.out, c->mh_out.p, size_t(c->m2l_job.n_targets) * P1 * 16);
   if (ops) *ops = c->m2l_ops;
   if (seconds) *seconds = c->m2l_prep + 1e-3 * double(ms);

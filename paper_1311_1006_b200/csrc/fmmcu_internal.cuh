@@ -333,6 +333,10 @@ struct fmmcu_ctx {
   int table_p = -1, table_kernel = -1;
   bool m2l_inflight = false;
   fmmcu_m2l_job m2l_job{};
+  bool m2l_keep = false;            // M2L sums left on the device (fmmcu_m2l_downward)
+  DevBuf m_loc, m_tof, m_binom;     // downward pass: locals, target slots, binomials
+  std::vector<double> m_binom_host;
+  std::vector<int32_t> m_tof_host;
   uint64_t m2l_ops = 0;
   double m2l_prep = 0.0;
 

@@ -392,6 +392,34 @@ void CudaBackend::m2l_launch(int p, Kernel kernel, std::uint32_t n_boxes, std::u
   if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l launch");
 }
 
+void CudaBackend::m2l_launch_keep(int p, Kernel kernel, std::uint32_t n_boxes,
+                                  std::uint32_t n_targets, const M2LBuffers& b) {
+  fmmcu_m2l_job j{};
+  j.p = p;
+  j.kernel = kernel == Kernel::harmonic ? FMMCU_KERNEL_HARMONIC : FMMCU_KERNEL_LOG;
+  j.n_boxes = n_boxes;
+  j.centers = reinterpret_cast<const double*>(b.centers);
+  j.coeffs = reinterpret_cast<const double*>(b.coeffs);
+  j.n_targets = n_targets;
+  j.target_box = b.target_box;
+  j.weak_off = b.weak_off;
+  j.weak_idx = b.weak_idx;
+  j.out = nullptr;  // the sums stay on the device for m2l_downward
+  const int rc = fmmcu_m2l_launch(ctx_[0], &j);
+  if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l launch");
+}
+
+void CudaBackend::m2l_downward(int n_levels, const std::uint32_t* level_base,
+                               const std::int32_t* target_of, cplx* finest_out) {
+  fmmcu_l2l_job j{};
+  j.n_levels = n_levels;
+  j.level_base = level_base;
+  j.target_of = target_of;
+  j.finest_out = reinterpret_cast<double*>(finest_out);
+  const int rc = fmmcu_m2l_downward(ctx_[0], &j);
+  if (rc != FMMCU_OK) raise(ctx_[0], rc, "cuda m2l downward");
+}
+
 std::uint64_t CudaBackend::m2l_finish(double* seconds) {
   std::uint64_t ops = 0;
   double s = 0;

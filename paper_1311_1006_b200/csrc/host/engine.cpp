@@ -126,64 +126,108 @@ struct DeviceM2L {
   std::uint32_t n_boxes = 0, n_targets = 0;
   std::vector<std::uint32_t> level_base;  // global id of box 0 of level l
   std::vector<std::int64_t> slot;         // global box id -> target row (-1 if none)
+  // device downward pass (default; FMM_HOST_L2L=1: L2L on the host): the
+  // finest level's locals land in b.out, row = finest box index
+  bool device_l2l = false;
+  std::vector<std::int32_t> target_of;    // slot as int32 for fmmcu_m2l_downward
 };
 
 void device_m2l_launch(CudaBackend& be, const Pyramid& pyr, const Connectivity& conn,
                        const ExpansionPyramid& out, Kernel kernel, int p, int threads,
                        DeviceM2L& dm) {
+  static const bool trace = std::getenv("FMM_TRACE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[fmm]   m2l flatten: %-16s %.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
   const int L = pyr.n_levels;
   dm.level_base.assign(L + 1, 0);
   for (int l = 0; l < L; ++l)
     dm.level_base[l + 1] = dm.level_base[l] + std::uint32_t(pyr.levels[l].size());
   const std::uint32_t nb = dm.level_base[L];
   const std::size_t P1 = std::size_t(p) + 1;
-  // per box: target flag and its nonempty weak partners (pass 1), prefix
-  // sums (serial over boxes, cheap), then the parallel fill (pass 2)
+  // Global box g = level_base[l] + i.  One parallel region per pass over
+  // all levels' boxes: nonempty flags (a byte per box: the weak-list scans
+  // then read bytes, not Expansion objects), then per target its nonempty
+  // weak partners; prefix sums (serial, cheap); then the fill.
+  auto level_of = [&](std::uint32_t g) {
+    return int(std::upper_bound(dm.level_base.begin(), dm.level_base.end(), g) -
+               dm.level_base.begin()) - 1;
+  };
   std::vector<std::uint32_t> tcnt(std::size_t(nb) + 1, 0), wcnt(std::size_t(nb) + 1, 0);
-  for (int l = 1; l < L; ++l) {
-    const std::int64_t n = std::int64_t(pyr.levels[l].size());
-    const std::uint32_t base = dm.level_base[l];
-#pragma omp parallel for schedule(static) num_threads(threads)
-    for (std::int64_t i = 0; i < n; ++i) {
+  std::vector<std::uint8_t> nonempty(nb);
+#pragma omp parallel num_threads(threads)
+  {
+#pragma omp for schedule(static)
+    for (std::int64_t g = 0; g < std::int64_t(nb); ++g) {
+      const int l = level_of(std::uint32_t(g));
+      nonempty[g] = out.levels[l][std::uint32_t(g) - dm.level_base[l]].coeffs.empty() ? 0 : 1;
+    }
+#pragma omp for schedule(static)
+    for (std::int64_t g = dm.level_base[std::min(1, L)]; g < std::int64_t(nb); ++g) {
+      const int l = level_of(std::uint32_t(g));
+      const std::uint32_t base = dm.level_base[l], i = std::uint32_t(g) - base;
       if (pyr.levels[l][i].n_evals() == 0) continue;
       std::uint32_t k = 0;
-      for (std::uint32_t w : conn.levels[l].weak[i]) k += out.levels[l][w].coeffs.empty() ? 0u : 1u;
-      tcnt[base + i + 1] = 1;
-      wcnt[base + i + 1] = k;
+      for (std::uint32_t w : conn.levels[l].weak[i]) k += nonempty[base + w];
+      tcnt[g + 1] = 1;
+      wcnt[g + 1] = k;
     }
   }
   for (std::uint32_t g = 0; g < nb; ++g) {
     tcnt[g + 1] += tcnt[g];
     wcnt[g + 1] += wcnt[g];
   }
+  mark("count + prefix");
   dm.n_boxes = nb;
   dm.n_targets = tcnt[nb];
-  dm.b = be.m2l_buffers(nb, p, dm.n_targets, wcnt[nb]);
+  static const bool host_l2l = std::getenv("FMM_HOST_L2L") != nullptr;
+  dm.device_l2l = !host_l2l && L >= 2;
+  const std::uint32_t n_fin = dm.level_base[L] - dm.level_base[L - 1];
+  // out holds the sums ([n_targets][p+1]) or, with the device downward
+  // pass, the finest locals ([n_fin][p+1])
+  dm.b = be.m2l_buffers(nb, p, dm.device_l2l ? std::max(dm.n_targets, n_fin) : dm.n_targets,
+                        wcnt[nb]);
   dm.slot.assign(nb, -1);
+  dm.target_of.resize(nb);
   const CudaBackend::M2LBuffers& b = dm.b;
   b.weak_off[0] = 0;
-  for (int l = 0; l < L; ++l) {
-    const std::int64_t n = std::int64_t(pyr.levels[l].size());
-    const std::uint32_t base = dm.level_base[l];
 #pragma omp parallel for schedule(static) num_threads(threads)
-    for (std::int64_t i = 0; i < n; ++i) {
-      const std::uint32_t g = base + std::uint32_t(i);
-      b.centers[g] = pyr.levels[l][i].center;
-      const Expansion& e = out.levels[l][i];
-      cplx* dst = b.coeffs + std::size_t(g) * P1;
-      if (!e.coeffs.empty()) std::copy(e.coeffs.begin(), e.coeffs.end(), dst);
-      else std::fill(dst, dst + P1, cplx(0, 0));
-      if (tcnt[g + 1] == tcnt[g]) continue;  // not a target
-      const std::uint32_t t = tcnt[g];
-      dm.slot[g] = std::int64_t(t);
-      b.target_box[t] = g;
-      std::uint32_t o = wcnt[g];
-      for (std::uint32_t w : conn.levels[l].weak[i])
-        if (!out.levels[l][w].coeffs.empty()) b.weak_idx[o++] = base + w;
-      b.weak_off[t + 1] = o;
+  for (std::int64_t gg = 0; gg < std::int64_t(nb); ++gg) {
+    const std::uint32_t g = std::uint32_t(gg);
+    const int l = level_of(g);
+    const std::uint32_t base = dm.level_base[l], i = g - base;
+    b.centers[g] = pyr.levels[l][i].center;
+    const Expansion& e = out.levels[l][i];
+    cplx* dst = b.coeffs + std::size_t(g) * P1;
+    if (nonempty[g]) std::copy(e.coeffs.begin(), e.coeffs.end(), dst);
+    else std::fill(dst, dst + P1, cplx(0, 0));
+    if (tcnt[g + 1] == tcnt[g]) {  // not a target
+      dm.target_of[g] = -1;
+      continue;
     }
+    const std::uint32_t t = tcnt[g];
+    dm.slot[g] = std::int64_t(t);
+    dm.target_of[g] = std::int32_t(t);
+    b.target_box[t] = g;
+    std::uint32_t o = wcnt[g];
+    for (std::uint32_t w : conn.levels[l].weak[i])
+      if (nonempty[base + w]) b.weak_idx[o++] = base + w;
+    b.weak_off[t + 1] = o;
   }
-  be.m2l_launch(p, kernel, nb, dm.n_targets, b);
+  mark("fill");
+  if (!dm.device_l2l) {
+    be.m2l_launch(p, kernel, nb, dm.n_targets, b);
+    return;
+  }
+  be.m2l_launch_keep(p, kernel, nb, dm.n_targets, b);
+  mark("launch");
+  be.m2l_downward(L, dm.level_base.data(), dm.target_of.data(), b.out);
+  mark("downward");
 }
 
 // Host half of the device downward pass: L2L chain + device M2L sums.
@@ -443,9 +487,9 @@ void FmmEngine::evaluate_into(const SourceSet& sources, const EvalSet& evals, Ev
 
   const auto t_m2l = Clock::now();
   ExpansionPyramid locals;
+  DeviceM2L dm;  // (device downward pass: the finest locals stay in dm.b.out)
   if (cfg_.m2l_on_device) {
     auto* cb = dynamic_cast<CudaBackend*>(backend_.get());
-    DeviceM2L dm;
     static const bool trace = std::getenv("FMM_TRACE") != nullptr;
     try {
       device_m2l_launch(*cb, pyr, conn, outgoing, cfg_.kernel, p, threads, dm);
@@ -468,8 +512,11 @@ void FmmEngine::evaluate_into(const SourceSet& sources, const EvalSet& evals, Ev
       }
       throw BackendError("m2l", e.what());
     }
-    locals = device_m2l_assemble(pyr, dm, cfg_.kernel, p, threads);
-    if (trace) std::fprintf(stderr, "[fmm] hybrid m2l: assembled at %.2f ms\n", 1e3 * since(t_m2l));
+    if (!dm.device_l2l) {
+      locals = device_m2l_assemble(pyr, dm, cfg_.kernel, p, threads);
+      if (trace)
+        std::fprintf(stderr, "[fmm] hybrid m2l: assembled at %.2f ms\n", 1e3 * since(t_m2l));
+    }
   } else {
     locals = downward_pass(pyr, conn, outgoing, p, cfg_.task_split_level, threads, &res.counters);
   }
@@ -489,19 +536,44 @@ void FmmEngine::evaluate_into(const SourceSet& sources, const EvalSet& evals, Ev
   // ---- assembly (engine.cpp:316-339) -----------------------------------------
   const auto t_asm = Clock::now();
   const std::vector<MBox>& fine = pyr.finest();
-  const std::vector<Expansion>& floc = locals.levels[pyr.finest_level()];
   res.potentials.resize(evals.size());
   std::uint64_t l2p = 0;
+  if (dm.device_l2l) {
+    // the finest locals from the device downward pass, flat ([box][p+1]);
+    // Horner exactly as eval_local (expansion.cpp)
+    const cplx* fl = dm.b.out;
+    const std::int32_t* tof = dm.target_of.data() + dm.level_base[pyr.finest_level()];
+    const std::size_t P1 = std::size_t(p) + 1;
 #pragma omp parallel for schedule(dynamic) reduction(+ : l2p) num_threads(threads)
-  for (std::int64_t i = 0; i < std::int64_t(fine.size()); ++i) {
-    const MBox& b = fine[i];
-    const Expansion& loc = floc[i];
-    const bool far = !loc.coeffs.empty();
-    for (std::uint32_t e = b.eval_begin; e < b.eval_end; ++e) {
-      const cplx v = far ? near[e] + eval_local(loc, yp[e]) : near[e];
-      res.potentials[pyr.eval_perm[e]] = v;
+    for (std::int64_t i = 0; i < std::int64_t(fine.size()); ++i) {
+      const MBox& b = fine[i];
+      const bool far = tof[i] >= 0;
+      const cplx* c = fl + std::size_t(i) * P1;
+      for (std::uint32_t e = b.eval_begin; e < b.eval_end; ++e) {
+        cplx v = near[e];
+        if (far) {
+          const cplx d = yp[e] - b.center;
+          cplx s(0, 0);
+          for (int k = p; k >= 0; --k) s = s * d + c[k];
+          v = near[e] + s;
+        }
+        res.potentials[pyr.eval_perm[e]] = v;
+      }
+      if (far) l2p += b.n_evals();
     }
-    if (far) l2p += b.n_evals();
+  } else {
+    const std::vector<Expansion>& floc = locals.levels[pyr.finest_level()];
+#pragma omp parallel for schedule(dynamic) reduction(+ : l2p) num_threads(threads)
+    for (std::int64_t i = 0; i < std::int64_t(fine.size()); ++i) {
+      const MBox& b = fine[i];
+      const Expansion& loc = floc[i];
+      const bool far = !loc.coeffs.empty();
+      for (std::uint32_t e = b.eval_begin; e < b.eval_end; ++e) {
+        const cplx v = far ? near[e] + eval_local(loc, yp[e]) : near[e];
+        res.potentials[pyr.eval_perm[e]] = v;
+      }
+      if (far) l2p += b.n_evals();
+    }
   }
   res.counters.l2p_points += l2p;
   const double t_assembly = since(t_asm);
