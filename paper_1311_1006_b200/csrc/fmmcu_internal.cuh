@@ -52,6 +52,27 @@ inline void keep_pool_memory() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t keep = ~uint64_t(0);
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    // Reserve the pool up front (FMMCU_POOL_RESERVE_GB, default 16; 0: off):
+    // growing it maps new pages, 10-15 ms per GB and up to ~0.4 s for one
+    // allocation under autotuned time stepping, where a level probe can need
+    // a few GB of symmetric contributions at once.  One allocation + free
+    // maps the memory once; later buffers are carved from it.  Failure is
+    // ignored (the pool then grows on demand as before).
+    const char* env = std::getenv("FMMCU_POOL_RESERVE_GB");
+    const double gb = env ? std::atof(env) : 16.0;
+    uint64_t have = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have);
+    const uint64_t want = uint64_t(gb * double(1ull << 30));
+    if (want > have) {
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && want - have < free_b / 2) {
+        void* r = nullptr;
+        if (cudaMallocAsync(&r, size_t(want - have), 0) == cudaSuccess) {
+          cudaFreeAsync(r, 0);
+          cudaStreamSynchronize(0);
+        }
+      }
+    }
   }
   cudaGetLastError();
   done_mask |= 1 << dev;
