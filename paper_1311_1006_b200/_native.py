@@ -125,6 +125,11 @@ class M2LBuffers(C.Structure):
                 ("weak_off", C.POINTER(C.c_uint32)), ("weak_idx", C.POINTER(C.c_uint32))]
 
 
+class L2LJob(C.Structure):
+    _fields_ = [("n_levels", C.c_int), ("level_base", C.c_void_p), ("target_of", C.c_void_p),
+                ("finest_out", C.c_void_p)]
+
+
 class M2LJob(C.Structure):
     """Mirror of ``fmmcu_m2l_job`` (include/fmm_cuda.h)."""
 
@@ -195,6 +200,7 @@ def cuda_lib():
         lib.fmmcu_p2p_kernel_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         lib.fmmcu_synchronize.argtypes = [vp]
         lib.fmmcu_m2l_launch.argtypes = [vp, C.POINTER(M2LJob)]
+        lib.fmmcu_m2l_downward.argtypes = [vp, C.POINTER(L2LJob)]
         lib.fmmcu_m2l_finish.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
         lib.fmmcu_m2l_host_buffers.argtypes = [vp, C.c_uint32, C.c_int, C.c_uint32, C.c_uint64,
                                                C.POINTER(M2LBuffers)]
@@ -488,6 +494,46 @@ class CudaContext:
         secs = C.c_double()
         self._check(self.lib.fmmcu_m2l_finish(self.h, C.byref(ops), C.byref(secs)))
         return out, int(ops.value), float(secs.value)
+
+    def m2l_downward(self, p, kernel, centers, coeffs, target_box, weak_off, weak_idx,
+                     level_base, target_of):
+        """m2l() with the sums kept on the device, then fmmcu_m2l_downward:
+        the finest level's locals ([boxes of the finest level, p+1, 2]; rows
+        of boxes without a target slot are zero here)."""
+        centers = np.ascontiguousarray(centers, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        target_box = np.ascontiguousarray(target_box, dtype=np.uint32)
+        weak_off = np.ascontiguousarray(weak_off, dtype=np.uint32)
+        weak_idx = np.ascontiguousarray(weak_idx, dtype=np.uint32)
+        level_base = np.ascontiguousarray(level_base, dtype=np.uint32)
+        target_of = np.ascontiguousarray(target_of, dtype=np.int32)
+        L = len(level_base) - 1
+        nfin = int(level_base[L] - level_base[L - 1])
+        out = np.zeros((nfin, p + 1, 2))
+        j = M2LJob()
+        j.p = p
+        j.kernel = kernel
+        j.n_boxes = centers.size // 2
+        j.centers = _ptr(centers)
+        j.coeffs = _ptr(coeffs)
+        j.n_targets = len(target_box)
+        j.target_box = _ptr(target_box) if len(target_box) else None
+        j.weak_off = _ptr(weak_off)
+        j.weak_idx = _ptr(weak_idx) if weak_idx.size else None
+        j.out = None  # keep the sums on the device
+        self._check(self.lib.fmmcu_m2l_launch(self.h, C.byref(j)))
+        d = L2LJob()
+        d.n_levels = L
+        d.level_base = _ptr(level_base)
+        d.target_of = _ptr(target_of)
+        d.finest_out = _ptr(out)
+        rc = self.lib.fmmcu_m2l_downward(self.h, C.byref(d))
+        ops = C.c_uint64()
+        secs = C.c_double()
+        rc2 = self.lib.fmmcu_m2l_finish(self.h, C.byref(ops), C.byref(secs))
+        self._check(rc)
+        self._check(rc2)
+        return out, int(ops.value)
 
     def m2l_pinned(self, p, kernel, centers, coeffs, target_box, weak_off, weak_idx):
         """m2l() through the context's page-locked buffers

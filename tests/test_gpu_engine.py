@@ -7,6 +7,8 @@
 * m2l_on_device: <= 1e-12 normwise; m2l_ops identical;
 * the concurrent-backend contract: cpu_wait >= 0, t_p2p > 0.
 """
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -103,6 +105,77 @@ def test_device_m2l_pinned_buffers_equal_pageable():
         b, ob, _ = ctx.m2l_pinned(p, 0, centers, coeffs, target_box, weak_off, weak_idx)
         assert oa == ob == int(weak_off[-1])
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    ctx.close()
+
+
+def test_device_downward_pass_vs_restated_l2l():
+    """fmmcu_m2l_downward on a 4-level toy pyramid (1 + 4 + 16 + 64 boxes,
+    children of box i are 4i..4i+3 of the next level): every box of levels
+    >= 1 except a few (no evals) is a target with random partners; the
+    finest locals against local = l2l_add(parent) + own M2L sum restated in
+    numpy (sum_k C(k,l) d^(k-l) a_k, expansion.cpp l2l_add), <= 1e-12
+    normwise; a downward call without a keep-on-device launch is refused."""
+    from math import comb
+    rng = np.random.default_rng(7)
+    p, L = 12, 4
+    sizes = [4 ** l for l in range(L)]
+    level_base = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint32)
+    nb = int(level_base[-1])
+    centers = np.zeros((nb, 2))
+    for l in range(L):
+        n = sizes[l]
+        side = 2 ** l
+        idx = np.arange(n)
+        centers[level_base[l]:level_base[l + 1], 0] = (idx % side + 0.5) / side
+        centers[level_base[l]:level_base[l + 1], 1] = (idx // side + 0.5) / side
+    coeffs = rng.standard_normal((nb, p + 1, 2)) * 1e-2
+    empty = set(int(x) for x in rng.choice(np.arange(level_base[3], nb), 6, replace=False))
+    # a box without evals has children without evals
+    is_t = np.zeros(nb, dtype=bool)
+    is_t[level_base[1]:] = True
+    for g in list(empty):
+        is_t[g] = False
+    targets = np.nonzero(is_t)[0].astype(np.uint32)
+    target_of = np.full(nb, -1, dtype=np.int32)
+    target_of[targets] = np.arange(len(targets))
+    weak, off = [], [0]
+    for g in targets:
+        lvl = int(np.searchsorted(level_base, g, side="right") - 1)
+        cand = np.arange(level_base[lvl], level_base[lvl + 1])
+        cand = cand[np.abs(centers[cand] - centers[g]).max(axis=1) > 1.5 / 2 ** lvl]
+        pick = rng.choice(cand, min(len(cand), 5), replace=False) if len(cand) else []
+        weak.extend(sorted(int(x) for x in pick))
+        off.append(len(weak))
+    weak_off, weak_idx = np.array(off, dtype=np.uint32), np.array(weak, dtype=np.uint32)
+    ctx = N.CudaContext(0)
+    sums, _, _ = ctx.m2l(p, 0, centers, coeffs, targets, weak_off, weak_idx)
+    fin, ops = ctx.m2l_downward(p, 0, centers, coeffs, targets, weak_off, weak_idx, level_base,
+                                target_of)
+    assert ops == len(weak_idx)
+    s = sums[..., 0] + 1j * sums[..., 1]
+    cz = centers[:, 0] + 1j * centers[:, 1]
+    loc = {}
+    for l in range(1, L):
+        for i in range(sizes[l]):
+            g = int(level_base[l]) + i
+            if target_of[g] < 0:
+                continue
+            v = np.zeros(p + 1, dtype=complex)
+            if l >= 2:
+                pg = int(level_base[l - 1]) + i // 4
+                a, d = loc[pg], cz[g] - cz[pg]
+                for ll in range(p + 1):
+                    v[ll] += sum(comb(k, ll) * d ** (k - ll) * a[k] for k in range(ll, p + 1))
+            loc[g] = v + s[target_of[g]]
+    got = fin[..., 0] + 1j * fin[..., 1]
+    for i in range(sizes[L - 1]):
+        g = int(level_base[L - 1]) + i
+        if target_of[g] >= 0:
+            assert np.abs(got[i] - loc[g]).max() <= 1e-12 * max(1.0, np.abs(loc[g]).max())
+    with pytest.raises(N.FmmcuError) as ei:
+        d = N.L2LJob()
+        ctx._check(ctx.lib.fmmcu_m2l_downward(ctx.h, C.byref(d)))
+    assert ei.value.code == 6  # FMMCU_ESTATE: no keep-on-device launch in flight
     ctx.close()
 
 
