@@ -336,37 +336,59 @@ __global__ void p2p_sym_lists_kernel(uint32_t leaf0, uint32_t n_leaves,
                                      const uint2* __restrict__ leaf_cnt = nullptr) {
   const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= n_leaves) return;
-  const int lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31;
   const uint32_t B = leaf0 + w;
   const uint32_t b = pt_off[B];
   uint32_t n = 0, o = FILL ? cl_off[w] : 0;
-  for (uint32_t q = s_off[B]; q < s_off[B + 1]; ++q) {
-    const uint32_t t = s_idx[q];
-    if (t < leaf0 || t >= B) continue;
+  // B's strong partners 32 at a time, one per lane (list order = ascending t)
+  for (uint32_t q0 = s_off[B]; q0 < s_off[B + 1]; q0 += 32) {
+    const uint32_t q = q0 + lane;
+    bool ok = q < s_off[B + 1];
+    const uint32_t t = ok ? s_idx[q] : 0u;
+    ok = ok && t >= leaf0 && t < B;
     // grouped list (per-leaf counts given): symmetric only inside the group
-    if (grp && grp[t - leaf0] != grp[w]) continue;
-    const uint4 it = info[t - leaf0];
-    const uint2 ct = leaf_cnt ? leaf_cnt[t - leaf0]
-                              : make_uint2(info[t - leaf0 + 1].x - it.x, info[t - leaf0 + 1].y - it.y);
+    if (ok && grp) ok = grp[t - leaf0] == grp[w];
+    uint4 it = make_uint4(0, 0, 0, 0);
+    uint2 ct = make_uint2(0, 0);
+    if (ok) {
+      it = info[t - leaf0];
+      ct = leaf_cnt ? leaf_cnt[t - leaf0]
+                    : make_uint2(info[t - leaf0 + 1].x - it.x, info[t - leaf0 + 1].y - it.y);
+    }
     const uint32_t nblk = ct.y;
+    // exclusive prefix of the partners' block counts over the lanes
+    uint32_t incl = nblk;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= uint32_t(d)) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
     if (!FILL) {
-      n += nblk;
+      n += total;
       continue;
     }
-    // B's run offset inside t's symmetric part: the sources of t's symmetric
-    // entries before it (t's entries in rounds of 32, one per lane)
-    const uint32_t ne = ct.x;
-    uint32_t voff = 0;
-    for (uint32_t r0 = 0; r0 < ne; r0 += 32) {
-      const uint4 sg = r0 + uint32_t(lane) < ne ? seg[it.x + r0 + lane] : make_uint4(0, 0, 0, 0);
-      const bool sym = sg.z == kRunSym;
-      const unsigned hit = __ballot_sync(0xffffffffu, sym && sg.x == b);
-      const int at = hit ? __ffs(hit) - 1 : 32;
-      voff += __reduce_add_sync(0xffffffffu, (sym && lane < at) ? sg.y : 0u);
-      if (hit) break;
+    if (ok && nblk) {
+      // B's run offset inside t's symmetric part: the sources of t's
+      // symmetric entries before B's run (entries read four at a time)
+      uint32_t voff = 0;
+      bool found = false;
+      for (uint32_t r = 0; r < ct.x && !found; r += 4) {
+        uint4 e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          e[u] = r + u < ct.x ? seg[it.x + r + u] : make_uint4(0, 0, kRunOrdered, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (found || e[u].z != kRunSym) continue;
+          if (e[u].x == b) found = true;
+          else voff += e[u].y;
+        }
+      }
+      const uint32_t base = o + incl - nblk;
+      for (uint32_t blk = 0; blk < nblk; ++blk) cl_base[base + blk] = it.z + blk * it.w + voff;
     }
-    for (uint32_t blk = uint32_t(lane); blk < nblk; blk += 32) cl_base[o + blk] = it.z + blk * it.w + voff;
-    o += nblk;
+    o += total;
   }
   if (!FILL && lane == 0) cnt[w] = n;
 }
