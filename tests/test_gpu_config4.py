@@ -94,6 +94,18 @@ def test_config4_c_abi_launch_path(ctx, c4):
     assert r["normwise"] <= TOL_FP64, r
 
 
+def test_config4_grouped_mutual_launch(ctx, c4, monkeypatch):
+    """FMMCU_E2E_SYM=1: the C-ABI launch with the mutual kernel on the list
+    grouped by upload chunk (10 groups at 10M) and the split finalize."""
+    monkeypatch.setenv("FMMCU_E2E_SYM", "1")
+    pt, ev, so, si, perm, zp, mp, yp, sid = c4["args"]
+    out, pairs, _ = N.p2p(ctx, pt, ev, so, si, perm, zp, mp, zp, sid)
+    assert ctx.kernel_info()[0]
+    assert pairs == c4["total"]
+    r = _check(c4, out)
+    assert r["normwise"] <= TOL_FP64, r
+
+
 def test_config4_exact_mode_bitwise(ctx, c4):
     out, pairs, _ = N.p2p(ctx, *c4["args"], mode=1)
     assert pairs == c4["total"]
