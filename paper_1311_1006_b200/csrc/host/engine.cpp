@@ -160,20 +160,28 @@ void device_m2l_launch(CudaBackend& be, const Pyramid& pyr, const Connectivity& 
   };
   std::vector<std::uint32_t> tcnt(std::size_t(nb) + 1, 0), wcnt(std::size_t(nb) + 1, 0);
   std::vector<std::uint8_t> nonempty(nb);
+  std::uint32_t n_empty = 0;
 #pragma omp parallel num_threads(threads)
   {
-#pragma omp for schedule(static)
+#pragma omp for schedule(static) reduction(+ : n_empty)
     for (std::int64_t g = 0; g < std::int64_t(nb); ++g) {
       const int l = level_of(std::uint32_t(g));
       nonempty[g] = out.levels[l][std::uint32_t(g) - dm.level_base[l]].coeffs.empty() ? 0 : 1;
+      n_empty += nonempty[g] ? 0u : 1u;
     }
+    // (every box has sources -- uniform inputs -- : the weak lists are taken
+    // whole, no per-partner test)
 #pragma omp for schedule(static)
     for (std::int64_t g = dm.level_base[std::min(1, L)]; g < std::int64_t(nb); ++g) {
       const int l = level_of(std::uint32_t(g));
       const std::uint32_t base = dm.level_base[l], i = std::uint32_t(g) - base;
       if (pyr.levels[l][i].n_evals() == 0) continue;
-      std::uint32_t k = 0;
-      for (std::uint32_t w : conn.levels[l].weak[i]) k += nonempty[base + w];
+      const std::vector<std::uint32_t>& wl = conn.levels[l].weak[i];
+      std::uint32_t k = std::uint32_t(wl.size());
+      if (n_empty) {
+        k = 0;
+        for (std::uint32_t w : wl) k += nonempty[base + w];
+      }
       tcnt[g + 1] = 1;
       wcnt[g + 1] = k;
     }
@@ -215,8 +223,12 @@ void device_m2l_launch(CudaBackend& be, const Pyramid& pyr, const Connectivity& 
     dm.target_of[g] = std::int32_t(t);
     b.target_box[t] = g;
     std::uint32_t o = wcnt[g];
-    for (std::uint32_t w : conn.levels[l].weak[i])
-      if (nonempty[base + w]) b.weak_idx[o++] = base + w;
+    if (n_empty) {
+      for (std::uint32_t w : conn.levels[l].weak[i])
+        if (nonempty[base + w]) b.weak_idx[o++] = base + w;
+    } else {
+      for (std::uint32_t w : conn.levels[l].weak[i]) b.weak_idx[o++] = base + w;
+    }
     b.weak_off[t + 1] = o;
   }
   mark("fill");
