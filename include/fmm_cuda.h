@@ -12,6 +12,8 @@
  *   NearFieldStats                      :39-42    pair_evals / seconds outputs
  *   m2l_add (expansion.hpp:60, called at
  *            engine.cpp:108-113)                  fmmcu_m2l_launch / _finish
+ *   l2l_add chain of the downward pass
+ *            (engine.cpp:96-114)                  fmmcu_m2l_downward
  *   errors thrown as BackendError /
  *   SingularConfiguration (types.hpp:70-78)       int status + fmmcu_last_error
  *
