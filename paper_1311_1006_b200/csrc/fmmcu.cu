@@ -1769,7 +1769,8 @@ void fmmcu_destroy(fmmcu_ctx* c) {
                       &c->m_centers, &c->m_coeffs, &c->m_tbox, &c->m_woff, &c->m_widx,
                       &c->m_table, &c->m_out, &c->m_flag, &c->m_items, &c->m_iscan, &c->m_nitems,
                       &c->m_partial, &c->m_cubtmp, &c->d_wl_head, &c->d_wl_key, &c->d_wl_val,
-                      &c->d_wl_S, &c->d_wl_work, &c->d_wl_cnt, &c->d_wl_off, &c->d_wls})
+                      &c->d_wl_S, &c->d_wl_work, &c->d_wl_cnt, &c->d_wl_off, &c->d_wls,
+                      &c->m_loc, &c->m_tof, &c->m_binom})
       b->release();
     for (HostBuf* b : {&c->h_src, &c->h_evy, &c->h_eself, &c->h_out, &c->h_hits, &c->h_csr,
                        &c->mh_out, &c->mh_flag, &c->h_wl_head, &c->mb_centers, &c->mb_coeffs,

@@ -1,6 +1,8 @@
 // fmm-b200 — flat C ABI over the C++ host library (include/fmm_host.h).
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -414,8 +416,15 @@ int fmmh_vortex_run(int n, double aspect, int steps, int tuner, double cap, uint
                     const double* cfg_f, const int* cfg_i, const int* devices, int n_devices,
                     double* trace, double* final_pos) {
   return guarded([&] {
+    static const bool vtrace = std::getenv("FMM_TRACE") != nullptr;
+    const auto tv0 = std::chrono::steady_clock::now();
+    auto since_ms = [&] {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tv0).count();
+    };
     sims::VortexSystem sys = sims::init_shear_layer(n, aspect, 2.0 * aspect / n);
+    const double t_init = since_ms();
     FmmEngine engine(config_of(cfg_f, cfg_i, devices, n_devices));
+    if (vtrace) std::fprintf(stderr, "[fmm] vortex run: init %.1f ms, engine %.1f ms\n", t_init, since_ms());
     ControllerConfig cc;
     cc.cap = cap;
     cc.nl_max = std::max(engine.config().n_levels + 3, 8);
@@ -445,6 +454,7 @@ int fmmh_vortex_run(int n, double aspect, int steps, int tuner, double cap, uint
       }
     });
     for (int s = 0; s < steps; ++s) sims::vortex_step(sys, engine);
+    if (vtrace) std::fprintf(stderr, "[fmm] vortex run: steps done at %.1f ms\n", since_ms());
     if (final_pos) std::memcpy(final_pos, sys.pos.data(), sys.pos.size() * 16);
   });
 }
