@@ -39,5 +39,8 @@ void euler_step(VortexSystem& sys, const std::vector<cplx>& velocities);
 // euler_step(sys, vortex_velocities(sys, engine)) fused: same positions,
 // without materialising the velocity vector (time-stepping drivers).
 void vortex_step(VortexSystem& sys, FmmEngine& engine);
+// `steps` vortex_step calls, each update also writing the next step's
+// inputs (same positions, one pass less per step).
+void vortex_steps(VortexSystem& sys, FmmEngine& engine, int steps);
 
 }  // namespace fmm::sims

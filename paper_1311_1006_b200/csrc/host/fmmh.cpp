@@ -423,7 +423,8 @@ int fmmh_vortex_run(int n, double aspect, int steps, int tuner, double cap, uint
     };
     sims::VortexSystem sys = sims::init_shear_layer(n, aspect, 2.0 * aspect / n);
     const double t_init = since_ms();
-    FmmEngine engine(config_of(cfg_f, cfg_i, devices, n_devices));
+    auto engine_owner = std::make_unique<FmmEngine>(config_of(cfg_f, cfg_i, devices, n_devices));
+    FmmEngine& engine = *engine_owner;
     if (vtrace) std::fprintf(stderr, "[fmm] vortex run: init %.1f ms, engine %.1f ms\n", t_init, since_ms());
     ControllerConfig cc;
     cc.cap = cap;
@@ -453,9 +454,11 @@ int fmmh_vortex_run(int n, double aspect, int steps, int tuner, double cap, uint
         e.set_config(nc);
       }
     });
-    for (int s = 0; s < steps; ++s) sims::vortex_step(sys, engine);
+    sims::vortex_steps(sys, engine, steps);
     if (vtrace) std::fprintf(stderr, "[fmm] vortex run: steps done at %.1f ms\n", since_ms());
     if (final_pos) std::memcpy(final_pos, sys.pos.data(), sys.pos.size() * 16);
+    engine_owner.reset();
+    if (vtrace) std::fprintf(stderr, "[fmm] vortex run: engine destroyed at %.1f ms\n", since_ms());
   });
 }
 

@@ -104,7 +104,7 @@ VortexSystem init_shear_layer(int n, double aspect, double gamma) {
 namespace {
 // Sources / self evals of the system in the thread's step buffers, then one
 // evaluation into B.r (shared by vortex_velocities and vortex_step).
-StepBuffers& evaluate_system(const VortexSystem& sys, FmmEngine& engine) {
+StepBuffers& evaluate_system(const VortexSystem& sys, FmmEngine& engine, bool prefilled = false) {
   use_vortex_kernel(engine, sys.delta);
   // Time stepping evaluates one problem size over and over: the sources, the
   // (self) evals and the result live in per-thread buffers that are refilled
@@ -132,12 +132,16 @@ StepBuffers& evaluate_system(const VortexSystem& sys, FmmEngine& engine) {
     B.pin();
   }
   int64_t* sid = ev.source_id.data();
+  // prefilled (vortex_steps): the previous step's update already wrote the
+  // positions into src.z / ev.y, and the strengths have not changed
+  if (!prefilled || ids) {
 #pragma omp parallel for schedule(static)
-  for (std::int64_t k = 0; k < n; ++k) {
-    src.z[k] = sys.pos[k];
-    src.m[k] = sys.gamma[k] * kOneOverTwoPiI;
-    ev.y[k] = sys.pos[k];
-    if (ids) sid[k] = k;
+    for (std::int64_t k = 0; k < n; ++k) {
+      src.z[k] = sys.pos[k];
+      src.m[k] = sys.gamma[k] * kOneOverTwoPiI;
+      ev.y[k] = sys.pos[k];
+      if (ids) sid[k] = k;
+    }
   }
   B.ids_n = n;
   engine.evaluate_into(src, ev, r);
@@ -158,6 +162,27 @@ std::vector<cplx> vortex_velocities(const VortexSystem& sys, FmmEngine& engine, 
   for (std::int64_t k = 0; k < n; ++k) v[k] = std::conj(r.potentials[k]);
   if (info) *info = r;
   return v;
+}
+
+// steps x vortex_step with the next step's inputs written by the update
+// (pos, src.z and ev.y in one pass; the strengths are constant): the system
+// is not visible between the steps, so nothing else can change it.
+void vortex_steps(VortexSystem& sys, FmmEngine& engine, int steps) {
+  if (sys.size() < 2 || steps <= 0) return;
+  const std::int64_t n = std::int64_t(sys.size());
+  for (int s = 0; s < steps; ++s) {
+    StepBuffers& B = evaluate_system(sys, engine, s > 0);
+    const cplx* pot = B.r.potentials.data();
+    cplx* z = B.src.z.data();
+    cplx* y = B.ev.y.data();
+#pragma omp parallel for schedule(static)
+    for (std::int64_t k = 0; k < n; ++k) {
+      const cplx p = sys.pos[k] + sys.dt * std::conj(pot[k]);
+      sys.pos[k] = p;
+      z[k] = p;
+      y[k] = p;
+    }
+  }
 }
 
 // euler_step(sys, vortex_velocities(sys, engine)) without the velocity

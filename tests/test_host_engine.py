@@ -231,3 +231,31 @@ def test_m2l_singular_and_single_source_accuracy():
 def test_normwise_helper():
     a = np.array([[1.0, 0.0], [0.0, 2.0]])
     assert normwise(a, a) == 0.0
+
+
+def test_vortex_run_matches_a_python_euler_loop():
+    """fmmh_vortex_run (sims::vortex_steps: the update also writes the next
+    step's inputs) against a Python loop of engine evaluations with the same
+    smoother and time step (pos += dt * conj(phi), m = gamma / (2 pi i)):
+    bitwise equal positions after 3 steps (pool backend)."""
+    import sys
+    sys.path.insert(0, __file__.rsplit("/", 1)[0])
+    from test_gpu_config5 import shear_layer
+    n, aspect, steps = 2000, 8.0, 3
+    cfg = dict(theta=0.5, n_levels=4, p_rule="formula", backend="pool", worker_threads=4)
+    _, got = F.vortex_run(n, aspect, steps, F.FmmConfig(**cfg), want_positions=True)
+    pos, gam, delta = shear_layer(n, aspect, 2.0 * aspect / n)
+    rows = int(round(np.sqrt(n / aspect)))
+    rows = max(2, rows - rows % 2)
+    while n % rows:
+        rows -= 2
+    dt = 0.5 * 1.0 / rows
+    m = gam * (complex(0.0, -1.0) / (2.0 * np.pi))
+    eng = F.FmmEngine(F.FmmConfig(smoother="gaussian", delta=delta, **cfg))
+    for _ in range(steps):
+        s = F.SourceSet(pos, m)
+        r = eng.evaluate(s, F.EvalSet.self_of(s))
+        phi = r.potentials
+        phi = phi[:, 0] + 1j * phi[:, 1] if phi.ndim == 2 else phi
+        pos = pos + dt * np.conj(phi)
+    assert np.array_equal(np.asarray(got).view(np.uint64), pos.view(np.uint64))
