@@ -327,3 +327,30 @@ def test_hybrid_device_tree_equals_host_tree(golden_trees, m2l_dev):
         b = F.FmmEngine(F.FmmConfig(device_tree=True, **base)).evaluate(s, e)
         assert a.counters == b.counters
         assert np.array_equal(a.potentials.view(np.uint64), b.potentials.view(np.uint64))
+
+
+def test_hybrid_device_downward_bitwise_equal_to_host_l2l(tmp_path):
+    """The hybrid engine's device downward pass (fmmcu_m2l_downward, default)
+    and its host L2L chain (FMM_HOST_L2L=1, read once per process, hence the
+    subprocesses) give bitwise the same potentials: the device restates
+    l2l_add's arithmetic operation for operation."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "from paper_1311_1006_b200 import fmm as F\n"
+        "s = F.make_distribution('gauss8', 200000, 3); e = F.EvalSet.self_of(s)\n"
+        "r = F.FmmEngine(F.FmmConfig(n_levels=7, backend='cuda', m2l_on_device=True,"
+        " worker_threads=8)).evaluate(s, e)\n"
+        "np.save(sys.argv[1], np.asarray(r.potentials))\n")
+    out = {}
+    for tag, extra in (("dev", {}), ("host", {"FMM_HOST_L2L": "1"})):
+        path = str(tmp_path / f"{tag}.npy")
+        env = {k: v for k, v in os.environ.items() if k != "FMM_HOST_L2L"}
+        env.update(extra)
+        subprocess.run([sys.executable, "-c", code, path], env=env, check=True, timeout=300)
+        out[tag] = np.load(path)
+    assert np.array_equal(out["dev"].view(np.uint64), out["host"].view(np.uint64))
